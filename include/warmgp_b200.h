@@ -1,0 +1,183 @@
+/*
+ * warmgp_b200.h — C-ABI of the B200-native iterative-GP hot path.
+ *
+ * This is the drop-in boundary that replaces the dense-Eigen hot path of the
+ * reference library `warmgp` (/root/reference/proj).  Every entry point below
+ * names the reference interface it replaces (file:line); INTEGRATION.md shows
+ * the C++ adapter and the ctypes stub that bind it.
+ *
+ * Conventions:
+ *   - plain pointers and sizes only; matrices are column-major like
+ *     Eigen::MatrixXd (element (i, c) at ptr[i + c * ld]); `*_host` entry points
+ *     take host memory, `*_device` ones take device memory on the context's GPU;
+ *   - status codes mirror the reference's exception -> exit-code mapping
+ *     (proj/tools/main.cpp:336-358): 0 ok, 2 std::invalid_argument,
+ *     3 NumericalError, 4 device / IO error; wgp_last_error() returns the
+ *     thread-local message, carrying the reference's message text
+ *     ("...not positive definite", "...use a smaller learning rate", "step N: ...");
+ *   - one context per thread/stream; the library owns all device buffers,
+ *     including the warm-start state; there is NO CPU fallback: without a
+ *     B200 every compute entry point returns 4.
+ */
+#ifndef WARMGP_B200_H
+#define WARMGP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WGP_OK 0
+#define WGP_INVALID 2
+#define WGP_NUMERICAL 3
+#define WGP_DEVICE 4
+
+typedef struct wgp_ctx wgp_ctx;
+
+/* Hyperparameter transform: 0 softplus (kernel.cpp:14-31), 1 log (BASELINE). */
+#define WGP_TRANSFORM_SOFTPLUS 0
+#define WGP_TRANSFORM_LOG 1
+/* Solver kinds: solvers.hpp:13 SolverKind {Cg, Ap, Sgd}. */
+#define WGP_SOLVER_CG 0
+#define WGP_SOLVER_AP 1
+#define WGP_SOLVER_SGD 2
+/* H.V implementation: tcgen05 3xTF32 (default) or the SIMT fp32 kernel. */
+#define WGP_HV_TC 0
+#define WGP_HV_SIMT 1
+
+/** Thread-local message of the last failing call. */
+const char* wgp_last_error(void);
+/** Library version string, build flags and the compiled sm target. */
+const char* wgp_version(void);
+/** Number of visible CUDA devices (0 on a GPU-less host; never an error). */
+int wgp_device_count(void);
+
+/** Create a context on `device`.  Replaces nothing in the reference (which
+ *  has no device); owns the stream, workspaces and warm-start buffers. */
+int wgp_create(int device, wgp_ctx** out);
+int wgp_destroy(wgp_ctx* ctx);
+/** Select the H.V kernel (WGP_HV_TC / WGP_HV_SIMT). */
+int wgp_set_hv_impl(wgp_ctx* ctx, int impl);
+/** The cudaStream_t the context launches on (for event timing by callers). */
+void* wgp_stream(wgp_ctx* ctx);
+
+/** Upload the n x d training inputs (host, column-major fp32).  Replaces the
+ *  X argument of build_kernel_matrices (proj/src/kernel.cpp:120-139): the
+ *  B200 path never materialises H. */
+int wgp_set_data(wgp_ctx* ctx, const float* X_host, int64_t n, int d);
+/** Constrained hyperparameters [lengthscales(d), signal, noise]
+ *  (Hyperparameters::to_constrained_vector, proj/src/kernel.cpp:70-76). */
+int wgp_set_hyper(wgp_ctx* ctx, const double* constrained);
+/** Restrict H.V outputs to rows [r0, r1) (row-block sharding);
+ *  default is all rows.  Inputs V always span all n rows. */
+int wgp_set_rows(wgp_ctx* ctx, int64_t r0, int64_t r1);
+
+/** out = H V = (K + sigma^2 I) V, V/out n x s (host).  Replaces the dense
+ *  products H * P / H * X at proj/src/solvers.cpp:71,92,110,120,169,188,211
+ *  and proj/src/estimator.cpp:90. */
+int wgp_hv(wgp_ctx* ctx, const float* V_host, int s, float* out_host);
+/** Device-pointer variant; `stream` may be NULL (context stream). */
+int wgp_hv_device(wgp_ctx* ctx, const float* V, int64_t ldv, int s, float* out, int64_t ldo);
+
+/* SolverConfig, proj/include/warmgp/solvers.hpp:20-32 (same defaults). */
+typedef struct {
+  int kind;
+  double tol_mean;
+  double tol_samples;
+  int max_iterations;
+  int block_size;
+  int minibatch_size;
+  double momentum;
+  double learning_rate;
+  uint64_t seed;
+} wgp_solver_cfg;
+
+/* SolveState, proj/include/warmgp/solvers.hpp:38-46 (caller-owned arrays). */
+typedef struct {
+  float* solutions;                      /* n x s */
+  float* residuals;                      /* n x s, solver-tracked */
+  double* per_column_relative_residual;  /* s, exact at exit */
+  int* converged;                        /* s */
+  int iterations_used;
+} wgp_solve_state;
+
+/** solve(H, rhs, init, config) (proj/src/solvers.cpp:265-279) with H given
+ *  matrix-free by the context's X and hyperparameters.  rhs/init host n x s
+ *  (init may be NULL = zeros). */
+int wgp_solve(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const float* rhs, const float* init, int s,
+              wgp_solve_state* state);
+
+/** derivative_contractions (proj/src/kernel.cpp:216-252) for the estimator's
+ *  low-rank contractions (proj/src/estimator.cpp:63-82):
+ *     A = 1/2 vy vy^T,  B = coef_b L R^T      (vy: n, L/R: n x s; host)
+ *  out_a/out_b (d+2): raw-space <dH/dtheta_k, A>, <dH/dtheta_k, B>, with the
+ *  chain rule of `transform` at `raw`.  Uses the context's X; the context's
+ *  hyperparameters are set from `raw`. */
+int wgp_grad(wgp_ctx* ctx, int transform, const double* raw, const float* vy, const float* L,
+             const float* R, int s, double coef_b, double* out_a, double* out_b);
+
+/** sample_probes (proj/src/estimator.cpp:21-37): host mt19937_64, bitwise the
+ *  reference's values (then rounded to fp32).  dist 0 gaussian, 1 rademacher. */
+int wgp_sample_probes(int64_t n, int s, int dist, uint64_t seed, float* out_host);
+
+/** Pathwise prior-sample probes (BASELINE a12, not in the reference):
+ *  z_j(x_i) = sf sqrt(2/F) sum_f w_fj cos(omega_f . x_i/ls + b_f) + sigma eps_ij,
+ *  base randomness drawn on the host from mt19937_64(seed) exactly like the
+ *  oracle (omega_z, chi2_3, b, w, eps order), evaluated on the GPU at the
+ *  context's hyperparameters.  out host n x s. */
+int wgp_rff_probes(wgp_ctx* ctx, int F, int s, uint64_t seed, float* out_host);
+
+/* TrainConfig, proj/include/warmgp/optimizer.hpp:23-38, plus BASELINE fields. */
+typedef struct {
+  int steps;
+  double learning_rate;
+  double adam_beta1;
+  double adam_beta2;
+  double adam_eps;
+  int num_probes;
+  int probe_distribution; /* 0 gaussian, 1 rademacher */
+  int mode;               /* 0 warm, 1 cold (resampled), 2 cold-fixed (TrainMode) */
+  wgp_solver_cfg solver;
+  double init_constrained;
+  uint64_t seed;
+  int transform;          /* WGP_TRANSFORM_* */
+  int estimator;          /* 0 hutchinson (reference), 1 pathwise RFF */
+  int rff_features;
+  double init_noise;      /* <= 0: init_constrained */
+  double init_signal;     /* <= 0: init_constrained */
+  int warm_start_distance;/* 1: compute the diagnostic (+1 H.V per warm step) */
+} wgp_train_cfg;
+
+/* StepRecord fields (proj/include/warmgp/optimizer.hpp:54-67), caller-owned,
+ * any pointer may be NULL. */
+typedef struct {
+  double* raw_params;          /* steps x p (row per step) */
+  double* constrained_params;  /* steps x p */
+  double* gradient;            /* steps x p */
+  int* solver_iterations;      /* steps */
+  double* per_column_relative_residual; /* steps x (num_probes + 1) */
+  double* warm_start_distance; /* steps */
+  uint64_t* probe_seed;        /* steps */
+  double* solver_ms;           /* steps: device time of the solve */
+  double* step_ms;             /* steps: device time of the whole outer step */
+  float* final_solutions;      /* n x (num_probes + 1) */
+} wgp_trace;
+
+/** train(X, y, config) (proj/src/optimizer.cpp:175-177, run_loop :81-171):
+ *  the full outer loop on the device — solves warm-started from the
+ *  device-resident previous solutions, gradients, Adam on the host.
+ *  Uses the context's data (wgp_set_data); y host n. */
+int wgp_train(wgp_ctx* ctx, const float* y_host, const wgp_train_cfg* cfg, wgp_trace* trace);
+
+/** adam_step (proj/src/optimizer.cpp:48-65). */
+int wgp_adam_step(double* raw, const double* grad, double* m, double* v, int p, int t,
+                  double lr, double beta1, double beta2, double eps);
+
+/** Utilities of the reference's common.hpp:25-36. */
+uint64_t wgp_derive_seed(uint64_t base, uint64_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -83,6 +83,10 @@ typedef struct {
   double momentum;
   double learning_rate;
   uint64_t seed;
+  /* 1: CG stores x, r, p and H p rounded to fp32 after every update (dots and
+   * alpha/beta stay fp64) -- the arithmetic of the fp32 GPU path, used as the
+   * reference for iteration-count parity.  0: the reference's fp64. */
+  int f32_vectors;
 } or_solver_cfg;
 
 /* SolveState, solvers.hpp:38-46 (arrays supplied by the caller). */

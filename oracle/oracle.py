@@ -41,7 +41,8 @@ class _SolverCfg(C.Structure):
     _fields_ = [("kind", C.c_int), ("tol_mean", C.c_double), ("tol_samples", C.c_double),
                 ("max_iterations", C.c_int), ("block_size", C.c_int),
                 ("minibatch_size", C.c_int), ("momentum", C.c_double),
-                ("learning_rate", C.c_double), ("seed", C.c_uint64)]
+                ("learning_rate", C.c_double), ("seed", C.c_uint64),
+                ("f32_vectors", C.c_int)]
 
 
 class _SolveState(C.Structure):
@@ -211,11 +212,12 @@ class SolverConfig:
     momentum: float = 0.9
     learning_rate: float = 10.0
     seed: int = 0
+    f32_vectors: bool = False  # CG in the fp32 arithmetic of the GPU path
 
     def _c(self):
         return _SolverCfg(SOLVER_KINDS[self.kind], self.tol_mean, self.tol_samples,
                           self.max_iterations, self.block_size, self.minibatch_size,
-                          self.momentum, self.learning_rate, self.seed)
+                          self.momentum, self.learning_rate, self.seed, int(self.f32_vectors))
 
 
 @dataclass

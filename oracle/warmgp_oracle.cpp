@@ -307,8 +307,10 @@ void check_shapes(const double* rhs, const double* init, int64_t n, int s) {  //
     throw std::invalid_argument("solve: non-finite right-hand side or init");
 }
 
+inline double rnd(double v, bool f32) { return f32 ? static_cast<double>(static_cast<float>(v)) : v; }
+
 void cg_solve(const Op& op, const double* rhs, const double* init, int s, double tm, double ts,
-              int max_it, or_solve_state* st) {  // solvers.cpp:81-139
+              int max_it, or_solve_state* st, bool f32 = false) {  // solvers.cpp:81-139
   const int64_t n = op.n;
   check_shapes(rhs, init, n, s);
   const Tol tol = column_tolerances(rhs, n, s, tm, ts);
@@ -319,7 +321,7 @@ void cg_solve(const Op& op, const double* rhs, const double* init, int s, double
   std::memcpy(Xs, init, ns * sizeof(double));
   std::vector<double> hx(ns);
   op.hv(Xs, s, hx.data());
-  for (size_t k = 0; k < ns; ++k) R[k] = rhs[k] - hx[k];
+  for (size_t k = 0; k < ns; ++k) R[k] = rnd(rhs[k] - rnd(hx[k], f32), f32);
   std::vector<int> conv(s, 0);
   std::vector<double> P(ns, 0.0), rs(s), HP(ns);
   for (int c = 0; c < s; ++c) {
@@ -334,6 +336,8 @@ void cg_solve(const Op& op, const double* rhs, const double* init, int s, double
   while (!all_conv() && it < max_it) {
     ++it;
     op.hv(P.data(), s, HP.data());
+    if (f32)
+      for (double& v : HP) v = rnd(v, true);
     const bool refresh = (it % 50 == 0);
     for (int c = 0; c < s; ++c) {
       if (conv[c]) continue;
@@ -346,13 +350,14 @@ void cg_solve(const Op& op, const double* rhs, const double* init, int s, double
       const double alpha = rs[c] / pHp;
       double* x = Xs + c * n;
       double* r = R + c * n;
-      for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+      const double a_v = rnd(alpha, f32);
+      for (int64_t i = 0; i < n; ++i) x[i] = rnd(x[i] + a_v * p[i], f32);
       if (refresh) {
         std::vector<double> hxc(n);
         op.hv(x, 1, hxc.data());
-        for (int64_t i = 0; i < n; ++i) r[i] = rhs[c * n + i] - hxc[i];
+        for (int64_t i = 0; i < n; ++i) r[i] = rnd(rhs[c * n + i] - rnd(hxc[i], f32), f32);
       } else {
-        for (int64_t i = 0; i < n; ++i) r[i] -= alpha * hp[i];
+        for (int64_t i = 0; i < n; ++i) r[i] = rnd(r[i] - a_v * hp[i], f32);
       }
       const double rs_new = col_norm2(r, n);
       if (!std::isfinite(rs_new))
@@ -361,8 +366,8 @@ void cg_solve(const Op& op, const double* rhs, const double* init, int s, double
         conv[c] = 1;
         std::fill(p, p + n, 0.0);
       } else {
-        const double beta = rs_new / rs[c];
-        for (int64_t i = 0; i < n; ++i) p[i] = r[i] + beta * p[i];
+        const double beta = rnd(rs_new / rs[c], f32);
+        for (int64_t i = 0; i < n; ++i) p[i] = rnd(r[i] + beta * p[i], f32);
       }
       rs[c] = rs_new;
     }
@@ -502,7 +507,9 @@ void solve_op(const Op& op, const or_solver_cfg& c, const double* rhs, const dou
               or_solve_state* st) {  // solvers.cpp:265-279
   validate_solver(c);
   switch (c.kind) {
-    case 0: cg_solve(op, rhs, init, s, c.tol_mean, c.tol_samples, c.max_iterations, st); return;
+    case 0:
+      cg_solve(op, rhs, init, s, c.tol_mean, c.tol_samples, c.max_iterations, st, c.f32_vectors != 0);
+      return;
     case 1:
       ap_solve(op, rhs, init, s, c.tol_mean, c.tol_samples, c.block_size, c.max_iterations, st);
       return;

@@ -1,0 +1,785 @@
+// hv_tc.cu — fused Matern-3/2 H.V on the 5th-generation tensor cores (v1).
+//
+// Replaces the dense products H * V of the reference solvers
+// (proj/src/solvers.cpp:71,92,110,120,169,186,188,211,242) without forming H.
+// One CTA owns a 128-row tile I and streams 64-point tiles J (FlashAttention
+// shape, no online-softmax state):
+//
+//   MMA-1  S[I,J]  = A_I . B_J^T           (tcgen05.mma kind::tf32, 3xTF32,
+//                    a_i = [x_i, |x_i|^2, 1], b_j = [-2 x_j, 1, |x_j|^2]
+//                    so S = u^2, the squared scaled distance, lands in TMEM)
+//   epilogue       k = sf^2 (1 + u ln2) 2^-u from S (tcgen05.ld -> registers,
+//                    sqrt + ex2 on the MUFU), the diagonal entry zeroed
+//                    (H_ii V_i = (sf^2 + sigma^2) V_i is added exactly at the end),
+//                    split k = k_hi + k_lo, tcgen05.st back to TMEM
+//   MMA-2  O[I,:] += K[I,J] . V[J,:]       (A operand from TMEM, 3xTF32)
+//
+// Warp roles: warp 0 TMA producer, warp 1 MMA issuer (one thread), warp 2
+// TMEM allocator, warps 4..15 epilogue (three warpgroups; group w owns TMEM
+// buffer w and tiles t = w, w+3, ...).  Three 128-column TMEM buffers hold S
+// and then, in place, K = k_hi | k_lo, so MMA-1 runs three tiles ahead of
+// MMA-2 and the epilogue latency of one tile hides behind the MMAs of the
+// next two.  Shared memory holds separate rings for the Gram operand B_J
+// (4 stages, consumed by MMA-1) and for V_J (2-3 stages, consumed by MMA-2).
+// J tiles of a row tile may be split across CTAs (fixed split count per
+// launch shape, partials summed in fixed order -> deterministic).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+#include <cstdio>
+
+#include "common.cuh"
+#include "hv_tc.cuh"
+
+namespace wgp {
+namespace {
+
+constexpr int kTI = 128;   // rows per tile (MMA M)
+constexpr int kTJ = 64;    // points per tile (MMA-1 N, MMA-2 K)
+constexpr int kKA = 32;    // augmented Gram dimension (d + 2 <= 32)
+constexpr int kThreads = 512;  // 4 control warps + 3 epilogue warpgroups
+constexpr uint32_t kTfMask = 0xFFFFE000u;  // keep sign, exponent, 10 mantissa bits
+constexpr int kSmemLimit = 232448 - 2048;  // 227 KB opt-in minus static smem (barriers)
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t addr = smem_u32(b);
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) break;
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// MMA issue helpers are called by a whole converged warp with warp-uniform
+// operands (so descriptors live in uniform registers); one lane, chosen by
+// elect.sync, issues.
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// TMA issue by one elected lane of a converged warp.
+__device__ __forceinline__ void tma_load_2d_warp(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];\n}\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_warp(uint64_t* b, uint32_t bytes) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(b)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* b) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(smem_u32(b))
+      : "memory");
+}
+
+#define R8(i) "=r"(r[i + 0]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3]), "=r"(r[i + 4]), \
+              "=r"(r[i + 5]), "=r"(r[i + 6]), "=r"(r[i + 7])
+#define W8(i) "r"(r[i + 0]), "r"(r[i + 1]), "r"(r[i + 2]), "r"(r[i + 3]), "r"(r[i + 4]), \
+              "r"(r[i + 5]), "r"(r[i + 6]), "r"(r[i + 7])
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : R8(0), R8(8), R8(16), R8(24)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : R8(0)
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      W8(0), W8(8), W8(16), W8(24)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms of
+// 1024 bytes (SBO), version 1 (sm_100), LBO unused for swizzled K-major.
+__device__ __forceinline__ uint64_t umma_desc(const void* p) {
+  const uint32_t a = smem_u32(p);
+  return static_cast<uint64_t>((a >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// 32 squared scaled distances -> tf32 hi / lo planes of k; the diagonal
+// entry (dg in [0, 32)) is zeroed: H_ii V_i is applied exactly at the end.
+__device__ __forceinline__ void to_k(const uint32_t (&r)[32], uint32_t (&khi)[32], uint32_t (&klo)[32],
+                                     float sf2, float ac, bool diag_tile, int64_t dg) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float r2 = fmaxf(__uint_as_float(r[i]), 0.f);
+    const float k = matern_from_u(sqrt_approx(r2), sf2, ac);
+    khi[i] = __float_as_uint(k) & kTfMask;
+    klo[i] = __float_as_uint(k - __uint_as_float(khi[i]));
+  }
+  if (diag_tile) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (dg == i) {
+        khi[i] = 0u;
+        klo[i] = 0u;
+      }
+    }
+  }
+}
+
+struct TcArgs {
+  int64_t m;         // output rows
+  int a_row0;        // first A-map row of this launch
+  int64_t j0, j1;    // contracted points
+  int num_jt;        // 64-point tiles in [j0, j1)
+  int splits;
+  int s, s_pad;
+  int nb, nv;              // B-ring and V-ring stages
+  uint32_t vstage_bytes;   // 4 V boxes (hi/lo x two 32-point halves)
+  const int* row_idx;
+  int64_t r0;
+  const float* V;
+  int64_t ldv;
+  float* out;
+  int64_t ldo;
+  const float* B;
+  int64_t ldb;
+  int mode;
+  float sf2, a, diag;
+  float* part;
+  int64_t m_pad;
+  const int* done;
+  long long* trace;  // WGP_TC_TRACE: per-tile clock64 stamps of CTA 0 ([T][4])
+  int dbg;  // ablation bits (WGP_TC_DEBUG): 1 no epilogue math, 2 no MMA-2, 4 no MMA-1, 8 no V loads,
+            // 16 no epilogue TMEM traffic, 32 no B loads
+};
+
+// TMEM: O accumulator in columns [0, 128); three tile buffers of 128 columns
+// at 128 + 128 b.  Buffer layout: [0, 64) holds S (MMA-1 output) and is
+// overwritten in place by k_hi once the epilogue has read it; [64, 128)
+// holds k_lo.
+constexpr int kBuf = 3;
+constexpr uint32_t buf_col(int b) { return 128u + 128u * static_cast<uint32_t>(b); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    hv_tc_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                 const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                 const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
+                 const TcArgs p) {
+  if (p.done && *p.done) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bar_bfull[4], bar_bempty[4], bar_vfull[4], bar_vempty[4];
+  __shared__ __align__(8) uint64_t bar_a, bar_sfull[kBuf], bar_kfull[kBuf], bar_o;
+  __shared__ uint32_t tmem_slot;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sAhi = smem;
+  uint8_t* sAlo = smem + 16384;
+  uint8_t* sB = smem + 32768;                   // nb x [B_hi 8K | B_lo 8K]
+  uint8_t* sV = sB + static_cast<size_t>(p.nb) * 16384;  // nv x vstage
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rt = blockIdx.x / p.splits, sp = blockIdx.x % p.splits;
+  const int jt_begin = static_cast<int>(static_cast<int64_t>(p.num_jt) * sp / p.splits);
+  const int jt_end = static_cast<int>(static_cast<int64_t>(p.num_jt) * (sp + 1) / p.splits);
+  const int T = jt_end - jt_begin;
+  const int NB = p.nb, NV = p.nv;
+  const int spad = p.s_pad;
+  const uint32_t vbox = static_cast<uint32_t>(spad) * 128u;  // one 32-point V box
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&bar_bfull[i], 1);
+      mbar_init(&bar_bempty[i], 1);
+    }
+    for (int i = 0; i < NV; ++i) {
+      mbar_init(&bar_vfull[i], 1);
+      mbar_init(&bar_vempty[i], 1);
+    }
+    mbar_init(&bar_a, 1);
+    for (int i = 0; i < kBuf; ++i) {
+      mbar_init(&bar_sfull[i], 1);
+      mbar_init(&bar_kfull[i], 4);
+    }
+    mbar_init(&bar_o, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (T > 0) {  // whole warp, one elected lane issues
+      const int arow = p.a_row0 + rt * kTI;
+      mbar_expect_tx_warp(&bar_a, 2 * 16384);
+      tma_load_2d_warp(sAhi, &mAhi, &bar_a, 0, arow);
+      tma_load_2d_warp(sAlo, &mAlo, &bar_a, 0, arow);
+      // consumption order of the MMA issuer: B(0..2), then V(t), B(t+3)
+      auto load_b = [&](int t) {
+        const int st = t % NB;
+        if (t >= NB) mbar_wait(&bar_bempty[st], ((t / NB) - 1) & 1);
+        uint8_t* base = sB + static_cast<size_t>(st) * 16384;
+        if (p.dbg & 32) {
+          mbar_arrive_warp(&bar_bfull[st]);
+          return;
+        }
+        mbar_expect_tx_warp(&bar_bfull[st], 16384u);
+        const int pt = static_cast<int>(p.j0) + (jt_begin + t) * kTJ;
+        tma_load_2d_warp(base, &mBhi, &bar_bfull[st], 0, pt);
+        tma_load_2d_warp(base + 8192, &mBlo, &bar_bfull[st], 0, pt);
+      };
+      auto load_v = [&](int t) {
+        const int st = t % NV;
+        if (t >= NV) mbar_wait(&bar_vempty[st], ((t / NV) - 1) & 1);
+        uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
+        const int vp = (jt_begin + t) * kTJ;
+        if (p.dbg & 8) {
+          mbar_arrive_warp(&bar_vfull[st]);
+          return;
+        }
+        mbar_expect_tx_warp(&bar_vfull[st], p.vstage_bytes);
+        tma_load_2d_warp(base, &mVhi, &bar_vfull[st], vp, 0);
+        tma_load_2d_warp(base + vbox, &mVhi, &bar_vfull[st], vp + 32, 0);
+        tma_load_2d_warp(base + 2 * vbox, &mVlo, &bar_vfull[st], vp, 0);
+        tma_load_2d_warp(base + 3 * vbox, &mVlo, &bar_vfull[st], vp + 32, 0);
+      };
+      for (int t = 0; t < T && t < kBuf; ++t) load_b(t);
+      for (int t = 0; t < T; ++t) {
+        load_v(t);
+        if (t + kBuf < T) load_b(t + kBuf);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // Issue order: MMA-1 for tiles 0..2, then for every t: [K(t) ready]
+    // MMA-2(t), MMA-1(t+3).  MMA-1(t+3) writes buffer t % 3 right after
+    // MMA-2(t) read it; tcgen05.mma from one thread executes in issue order,
+    // so the epilogue of tile t+3 (woken by the commit after MMA-1(t+3))
+    // starts while tiles t+1, t+2 are still in flight.  The whole warp runs
+    // this loop (uniform operands); elect.sync picks the issuing lane.
+    if (T > 0) {
+      constexpr uint32_t id1 = idesc_tf32(kTI, kTJ);
+      const uint32_t id2 = idesc_tf32(kTI, spad);
+      mbar_wait(&bar_a, 0);
+      tc_after();
+      const uint64_t dAhi = umma_desc(sAhi), dAlo = umma_desc(sAlo);
+      auto mma1 = [&](int t) {
+        const int st = t % NB, b = t % kBuf;
+        mbar_wait(&bar_bfull[st], (t / NB) & 1);
+        tc_after();
+        uint8_t* base = sB + static_cast<size_t>(st) * 16384;
+        const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + 8192);
+        const uint32_t d = tmem + buf_col(b);
+        if (!(p.dbg & 4)) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_ss(d, dAhi + 2 * k, dBhi + 2 * k, id1, k > 0);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_ss(d, dAhi + 2 * k, dBlo + 2 * k, id1, 1);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_ss(d, dAlo + 2 * k, dBhi + 2 * k, id1, 1);
+        }
+        mma_commit(&bar_sfull[b]);
+        mma_commit(&bar_bempty[st]);
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 0] = clock64();
+      };
+      for (int t = 0; t < T && t < kBuf; ++t) mma1(t);
+      for (int t = 0; t < T; ++t) {
+        const int b = t % kBuf, st = t % NV;
+        mbar_wait(&bar_vfull[st], (t / NV) & 1);
+        mbar_wait(&bar_kfull[b], (t / kBuf) & 1);
+        tc_after();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 3] = clock64();
+        uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
+        const uint32_t khi = tmem + buf_col(b), klo = khi + 64;
+        if (!(p.dbg & 2)) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t off = static_cast<uint32_t>(k & 3) * 2;  // 32 bytes >> 4
+            const uint64_t vhi = umma_desc(base + (k >> 2) * vbox) + off;
+            const uint64_t vlo = umma_desc(base + (2 + (k >> 2)) * vbox) + off;
+            mma_ts(tmem, khi + 8 * k, vhi, id2, (t > 0 || k > 0) ? 1u : 0u);
+            mma_ts(tmem, khi + 8 * k, vlo, id2, 1);
+            mma_ts(tmem, klo + 8 * k, vhi, id2, 1);
+          }
+        }
+        mma_commit(&bar_vempty[st]);
+        if (t + kBuf < T) mma1(t + kBuf);
+      }
+      mma_commit(&bar_o);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    // Warpgroup w owns buffer w and tiles t = w, w+3, ...; warp w%4 of the
+    // group reads TMEM lanes 32 (w%4) .. +31 (= its 32 output rows).
+    const int ew = warp - 4, q = ew & 3, w = ew >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+    const int64_t lr = static_cast<int64_t>(rt) * kTI + row;
+    const bool valid = lr < p.m;
+    int64_t g = -1;
+    if (valid) g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
+    const float sf2 = p.sf2, ac = p.a;
+    const uint32_t bcol = buf_col(w);
+    const bool nomath = p.dbg & 1;
+    for (int t = w; t < T; t += kBuf) {
+      const int64_t tstart = p.j0 + static_cast<int64_t>(jt_begin + t) * kTJ;
+      const int64_t dg = valid ? g - tstart : -1;
+      const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < kTJ);
+      mbar_wait(&bar_sfull[w], (t / kBuf) & 1);
+      tc_after();
+      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 4 + 1] = clock64();
+#pragma unroll 1
+      for (int half = 0; half < ((p.dbg & 16) ? 0 : 2); ++half) {
+        uint32_t r[32], khi[32], klo[32];
+        __syncwarp();
+        tmem_ld32(tmem + lanes + bcol + 32 * half, r);
+        tmem_wait_ld();
+        if (nomath) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) khi[i] = r[i], klo[i] = 0u;
+        } else {
+          to_k(r, khi, klo, sf2, ac, diag_tile, dg - 32 * half);
+        }
+        __syncwarp();
+        // k_hi overwrites the S columns just read; k_lo goes to [64, 128)
+        tmem_st32(tmem + lanes + bcol + 32 * half, khi);
+        tmem_st32(tmem + lanes + bcol + 64 + 32 * half, klo);
+      }
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_kfull[w]);
+      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 4 + 2] = clock64();
+    }
+    if (T > 0) {
+      mbar_wait(&bar_o, 0);
+      tc_after();
+      const bool diag = g >= p.j0 && g < p.j1;
+      for (int c8 = 8 * w; c8 < spad; c8 += 8 * kBuf) {
+        uint32_t o[8];
+        __syncwarp();
+        tmem_ld8(tmem + lanes + c8, o);
+        tmem_wait_ld();
+        if (!valid) continue;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = c8 + i;
+          if (c >= p.s) continue;
+          float v = __uint_as_float(o[i]);
+          if (p.splits > 1) {
+            p.part[(static_cast<int64_t>(sp) * spad + c) * p.m_pad + lr] = v;
+            continue;
+          }
+          if (diag) v = fmaf(p.diag, p.V[g + c * p.ldv], v);
+          float* dst = p.out + lr + c * p.ldo;
+          if (p.mode == kHvStore)
+            *dst = v;
+          else if (p.mode == kHvResidual)
+            *dst = p.B[g + c * p.ldb] - v;
+          else
+            *dst -= v;
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// Sum of split partials in fixed order + the same epilogue as the kernel.
+__global__ void tc_reduce_kernel(const TcArgs p) {
+  if (p.done && *p.done) return;
+  const int64_t lr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (lr >= p.m) return;
+  float v = 0.f;
+  for (int sp = 0; sp < p.splits; ++sp) v += p.part[(static_cast<int64_t>(sp) * p.s_pad + c) * p.m_pad + lr];
+  const int64_t g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
+  if (g >= p.j0 && g < p.j1) v = fmaf(p.diag, p.V[g + c * p.ldv], v);
+  float* dst = p.out + lr + c * p.ldo;
+  if (p.mode == kHvStore)
+    *dst = v;
+  else if (p.mode == kHvResidual)
+    *dst = p.B[g + c * p.ldb] - v;
+  else
+    *dst -= v;
+}
+
+// V[j0:j1, :s] -> tf32 hi / lo planes [s][ldw] (point index j - j0).
+__global__ void split_v_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, float* hi, float* lo,
+                               int64_t ldw) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (j >= nv) return;
+  const float v = V[j0 + j + c * ldv];
+  const float vh = __uint_as_float(__float_as_uint(v) & kTfMask);
+  hi[c * ldw + j] = vh;
+  lo[c * ldw + j] = v - vh;
+}
+
+// Augmented operand rows from the prepared points (see TcOperands).
+__global__ void build_ops_kernel(const float* xs, int64_t n, int64_t n_pad, int dp, int d, float* ahi,
+                                 float* alo, float* bhi, float* blo) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  float a[kKA], b[kKA];
+#pragma unroll
+  for (int k = 0; k < kKA; ++k) a[k] = b[k] = 0.f;
+  if (i < n) {
+    double sq = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const float x = xs[i * dp + k];
+      sq += static_cast<double>(x) * x;
+    }
+    for (int k = 0; k < kKA; ++k) {
+      if (k < d) {
+        a[k] = xs[i * dp + k];
+        b[k] = -2.f * xs[i * dp + k];
+      }
+    }
+    a[d] = static_cast<float>(sq);
+    a[d + 1] = 1.f;
+    b[d] = 1.f;
+    b[d + 1] = static_cast<float>(sq);
+  }
+#pragma unroll
+  for (int k = 0; k < kKA; ++k) {
+    const float ah = __uint_as_float(__float_as_uint(a[k]) & kTfMask);
+    const float bh = __uint_as_float(__float_as_uint(b[k]) & kTfMask);
+    ahi[i * kKA + k] = ah;
+    alo[i * kKA + k] = a[k] - ah;
+    bhi[i * kKA + k] = bh;
+    blo[i * kKA + k] = b[k] - bh;
+  }
+}
+
+__global__ void gather_rows_kernel(const float* ahi, const float* alo, const int* idx, int64_t m,
+                                   float* ghi, float* glo, int64_t m_pad) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m_pad * kKA) return;
+  const int64_t r = e / kKA, k = e % kKA;
+  float h = 0.f, l = 0.f;
+  if (r < m) {
+    const int64_t g = idx[r];
+    h = ahi[g * kKA + k];
+    l = alo[g * kKA + k];
+  }
+  ghi[e] = h;
+  glo[e] = l;
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  if (!fn) throw DeviceError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
+                     uint32_t box_out) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_in, box_out};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
+int choose_splits(int64_t row_tiles, int jt, int sms) {
+  int best = 1;
+  double best_cost = 1e300;
+  for (int sp = 1; sp <= 16; ++sp) {
+    if (sp > 1 && jt / sp < 4) break;
+    const double waves = std::ceil(static_cast<double>(row_tiles * sp) / sms);
+    const double cost = waves * std::ceil(static_cast<double>(jt) / sp) + (sp > 1 ? 1.0 + 0.25 * sp : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+}  // namespace
+
+struct Workspace {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* ensure(size_t b) {
+    if (b > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      WGP_CUDA(cudaMalloc(&p, b));
+      bytes = b;
+    }
+    return p;
+  }
+  ~Workspace() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct TcWorkspaces {
+  Workspace v, rows, part;
+};
+
+namespace {
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+}  // namespace
+
+TcOperands::~TcOperands() {
+  if (a_hi) cudaFree(a_hi);
+  delete ws;
+}
+
+void TcOperands::build(const float* xs, int64_t n_, int dp, int d_, cudaStream_t st) {
+  n = n_;
+  d = d_;
+  n_pad = round_up(n, 128);
+  const size_t plane = sizeof(float) * n_pad * kKA;
+  if (4 * plane > bytes) {
+    if (a_hi) cudaFree(a_hi);
+    a_hi = nullptr;
+    WGP_CUDA(cudaMalloc(&a_hi, 4 * plane));
+    bytes = 4 * plane;
+  }
+  a_lo = static_cast<char*>(a_hi) + plane;
+  b_hi = static_cast<char*>(a_hi) + 2 * plane;
+  b_lo = static_cast<char*>(a_hi) + 3 * plane;
+  build_ops_kernel<<<static_cast<unsigned>(ceil_div(n_pad, 128)), 128, 0, st>>>(
+      xs, n, n_pad, dp, d, static_cast<float*>(a_hi), static_cast<float*>(a_lo), static_cast<float*>(b_hi),
+      static_cast<float*>(b_lo));
+  WGP_LAUNCH_CHECK();
+  valid = true;
+}
+
+bool hv_tc_supported(int d, int s) { return d + 2 <= kKA && s >= 1 && s <= 128; }
+
+void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st) {
+  if (hp.s > 96) {  // the V ring holds at most 96 columns: balanced column chunks
+    const int chunks = static_cast<int>(ceil_div(hp.s, 96));
+    for (int c = 0; c < chunks; ++c) {
+      const int c0 = hp.s * c / chunks, c1 = hp.s * (c + 1) / chunks;
+      HvParams q = hp;
+      q.s = c1 - c0;
+      q.V = hp.V + c0 * hp.ldv;
+      q.out = hp.out + c0 * hp.ldo;
+      if (hp.B) q.B = hp.B + c0 * hp.ldb;
+      hv_tc(ops, q, st);
+    }
+    return;
+  }
+  if (!ops.ws) ops.ws = new TcWorkspaces();
+  Workspace& ws_v = ops.ws->v;
+  Workspace& ws_rows = ops.ws->rows;
+  Workspace& ws_part = ops.ws->part;
+  if (hp.m <= 0 || hp.j1 <= hp.j0) return;
+  const int s = hp.s;
+  const int spad = static_cast<int>(round_up(s, 16));
+  const int64_t nv = hp.j1 - hp.j0;
+  const int64_t ldw = round_up(nv, 4);
+  // tf32 planes of V[j0:j1]
+  float* vhi = static_cast<float*>(ws_v.ensure(sizeof(float) * ldw * s * 2));
+  float* vlo = vhi + ldw * s;
+  split_v_kernel<<<dim3(static_cast<unsigned>(ceil_div(nv, 256)), s), 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, vhi,
+                                                                                    vlo, ldw);
+  WGP_LAUNCH_CHECK();
+  // A rows: the operand planes directly (row range) or a gathered copy
+  const float* ahi = static_cast<const float*>(ops.a_hi);
+  const float* alo = static_cast<const float*>(ops.a_lo);
+  int64_t a_rows = ops.n_pad;
+  int a_row0 = static_cast<int>(hp.r0);
+  const int64_t m_pad = round_up(hp.m, 128);
+  if (hp.row_idx) {
+    float* g = static_cast<float*>(ws_rows.ensure(sizeof(float) * m_pad * kKA * 2));
+    gather_rows_kernel<<<static_cast<unsigned>(ceil_div(m_pad * kKA, 256)), 256, 0, st>>>(
+        ahi, alo, hp.row_idx, hp.m, g, g + m_pad * kKA, m_pad);
+    WGP_LAUNCH_CHECK();
+    ahi = g;
+    alo = g + m_pad * kKA;
+    a_rows = m_pad;
+    a_row0 = 0;
+  }
+  const CUtensorMap mAhi = make_map(ahi, kKA, a_rows, kKA * 4, kKA, kTI);
+  const CUtensorMap mAlo = make_map(alo, kKA, a_rows, kKA * 4, kKA, kTI);
+  const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, kTJ);
+  const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, kTJ);
+  const CUtensorMap mVhi = make_map(vhi, nv, s, ldw * 4, 32, spad);
+  const CUtensorMap mVlo = make_map(vlo, nv, s, ldw * 4, 32, spad);
+
+  TcArgs a{};
+  a.m = hp.m;
+  a.a_row0 = a_row0;
+  a.j0 = hp.j0;
+  a.j1 = hp.j1;
+  a.num_jt = static_cast<int>(ceil_div(nv, kTJ));
+  a.s = s;
+  a.s_pad = spad;
+  a.nb = 4;
+  a.vstage_bytes = 4u * static_cast<uint32_t>(spad) * 128u;
+  a.nv = std::min<int>(3, (kSmemLimit - 32768 - 1024 - a.nb * 16384) / static_cast<int>(a.vstage_bytes));
+  if (a.nv < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
+  a.row_idx = hp.row_idx;
+  a.r0 = hp.r0;
+  a.V = hp.V;
+  a.ldv = hp.ldv;
+  a.out = hp.out;
+  a.ldo = hp.ldo;
+  a.B = hp.B;
+  a.ldb = hp.ldb;
+  a.mode = hp.mode;
+  a.sf2 = hp.sf2;
+  a.a = hp.a;
+  a.diag = hp.diag;
+  a.m_pad = m_pad;
+  a.done = hp.done;
+  static const int dbg = [] {
+    const char* e = getenv("WGP_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  a.dbg = dbg;
+  static const bool tracing = getenv("WGP_TC_TRACE") != nullptr;
+  static Workspace ws_trace;
+  a.trace = nullptr;
+  if (tracing) {
+    a.trace = static_cast<long long*>(ws_trace.ensure(sizeof(long long) * 4 * (a.num_jt + 4)));
+    WGP_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(long long) * 4 * (a.num_jt + 4), st));
+  }
+  const int64_t row_tiles = ceil_div(hp.m, kTI);
+  a.splits = choose_splits(row_tiles, a.num_jt, sm_count());
+  static const int force_splits = [] {
+    const char* e = getenv("WGP_TC_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  if (force_splits > 0) a.splits = std::min(force_splits, a.num_jt);
+  if (a.splits > 1) a.part = static_cast<float*>(ws_part.ensure(sizeof(float) * a.splits * spad * m_pad));
+  const int smem = 32768 + 1024 + a.nb * 16384 + a.nv * static_cast<int>(a.vstage_bytes);
+  static bool configured = false;
+  if (!configured) {
+    WGP_CUDA(cudaFuncSetAttribute(hv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+    configured = true;
+  }
+  hv_tc_kernel<<<static_cast<unsigned>(row_tiles * a.splits), kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo,
+                                                                                   mVhi, mVlo, a);
+  WGP_LAUNCH_CHECK();
+  if (tracing) {
+    const int T0 = static_cast<int>(static_cast<int64_t>(a.num_jt) / a.splits);
+    std::vector<long long> h(4 * (a.num_jt + 4));
+    WGP_CUDA(cudaMemcpyAsync(h.data(), a.trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    double s_wake = 0, s_epi = 0, s_back = 0, s_per = 0;
+    int cnt = 0;
+    for (int t = 3; t + 1 < T0; ++t) {
+      const long long* r = &h[4 * t];
+      s_wake += r[1] - r[0];
+      s_epi += r[2] - r[1];
+      s_back += r[3] - r[2];
+      s_per += h[4 * (t + 1) + 3] - r[3];
+      ++cnt;
+    }
+    if (cnt)
+      fprintf(stderr, "[hv_tc trace] tiles=%d  mma1-commit->epi-wake %.0f  epi %.0f  kfull->mma-wake %.0f  period %.0f clk\n",
+              cnt, s_wake / cnt, s_epi / cnt, s_back / cnt, s_per / cnt);
+  }
+  if (a.splits > 1) {
+    tc_reduce_kernel<<<dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), 256, 0, st>>>(a);
+    WGP_LAUNCH_CHECK();
+  }
+}
+
+}  // namespace wgp

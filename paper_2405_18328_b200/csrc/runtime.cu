@@ -1,0 +1,972 @@
+// runtime.cu — context, solver drivers, training loop and the C-ABI.
+//
+// Host C++ side of the drop-in boundary (include/warmgp_b200.h).  The solver
+// drivers restate proj/src/solvers.cpp over a matrix-free device operator;
+// the outer loop restates proj/src/optimizer.cpp:81-171 with the solver state
+// (warm-start solutions, residuals, directions) resident in HBM across steps.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/warmgp_b200.h"
+#include "common.cuh"
+#include "host_rng.hpp"
+#include "hv_tc.cuh"
+#include "kernels.cuh"
+#include "solver_kernels.cuh"
+
+namespace wgp {
+namespace {
+
+thread_local std::string g_last_error;
+constexpr uint64_t kSolverStream = 0x736f6c7665ULL;  // proj/src/optimizer.cpp:15
+constexpr double kUScale = kSqrt3 * kLog2e;            // u = sqrt(3) log2(e) r
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  Buf() = default;
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) WGP_CUDA(cudaFree(p));
+    p = nullptr;
+    bytes = 0;
+    WGP_CUDA(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PinnedCtrl {
+  SolveCtrl* h = nullptr;
+  PinnedCtrl() { WGP_CUDA(cudaMallocHost(&h, sizeof(SolveCtrl))); }
+  ~PinnedCtrl() {
+    if (h) cudaFreeHost(h);
+  }
+};
+
+const char* solver_name(int kind) { return kind == 0 ? "cg_solve" : kind == 1 ? "ap_solve" : "sgd_solve"; }
+
+}  // namespace
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t cusolver = nullptr;
+  int hv_impl = WGP_HV_TC;
+
+  int64_t n = 0, n_pad = 0, ld = 0;
+  int d = 0, dp = 0;
+  Buf X;    // raw inputs, column-major n x d
+  Buf xs;   // prepared points [n_pad][dp]
+  std::vector<double> mu, ls;
+  double sf = 1.0, sigma = 1.0;
+  bool have_hyper = false;
+  int64_t r0 = 0, r1 = -1;
+  TcOperands tc;
+
+  // workspaces
+  Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum;
+  Buf P, HP, Rtmp, vel, batch, idx, hbuf, Rb, D64, D32, lapack_work, info;
+  Buf gpart, gout;
+  Buf io_in, io_out;  // staging for the host-pointer entry points
+  PinnedCtrl hctrl;
+
+  ~Ctx() {
+    if (cublas) cublasDestroy(cublas);
+    if (cusolver) cusolverDnDestroy(cusolver);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  float sf2() const { return static_cast<float>(sf * sf); }
+  float a_coef() const { return static_cast<float>(sf * sf * kLn2); }
+  float noise2() const { return static_cast<float>(sigma * sigma); }
+
+  void require_data() const {
+    if (n < 1) throw std::invalid_argument("no training inputs: call wgp_set_data first");
+    if (!have_hyper) throw std::invalid_argument("no hyperparameters: call wgp_set_hyper first");
+  }
+
+  // ---------------------------------------------------------------- data
+  void set_data(const float* Xh, int64_t n_, int d_) {
+    if (n_ < 1) throw std::invalid_argument("build_kernel_matrices: need at least one row");
+    if (d_ < 1 || d_ > 64) throw std::invalid_argument("input dimension must lie in [1, 64]");
+    for (int64_t e = 0; e < n_ * d_; ++e)
+      if (!std::isfinite(Xh[e])) throw std::invalid_argument("build_kernel_matrices: non-finite input");
+    n = n_;
+    d = d_;
+    dp = static_cast<int>(round_up(d, 4));
+    n_pad = round_up(n, 128);
+    ld = n_pad;
+    X.ensure(sizeof(float) * n * d);
+    WGP_CUDA(cudaMemcpyAsync(X.p, Xh, sizeof(float) * n * d, cudaMemcpyHostToDevice, st));
+    mu.assign(d, 0.0);
+    for (int k = 0; k < d; ++k) {
+      double acc = 0.0;
+      for (int64_t i = 0; i < n; ++i) acc += Xh[i + k * n];
+      mu[k] = acc / static_cast<double>(n);
+    }
+    xs.ensure(sizeof(float) * n_pad * dp);
+    have_hyper = false;
+    r0 = 0;
+    r1 = n;
+    tc.invalidate();
+    WGP_CUDA(cudaStreamSynchronize(st));
+  }
+
+  void set_hyper(const double* c) {
+    if (n < 1) throw std::invalid_argument("no training inputs: call wgp_set_data first");
+    for (int k = 0; k < d + 2; ++k)
+      if (!(c[k] > 0.0) || !std::isfinite(c[k]))
+        throw std::invalid_argument("hyperparameters must be positive and finite");
+    ls.assign(c, c + d);
+    sf = c[d];
+    sigma = c[d + 1];
+    std::vector<double> scale(d);
+    for (int k = 0; k < d; ++k) scale[k] = kUScale / ls[k];
+    Buf tmp;
+    tmp.ensure(sizeof(double) * 2 * d);
+    std::vector<double> h(2 * d);
+    std::copy(mu.begin(), mu.end(), h.begin());
+    std::copy(scale.begin(), scale.end(), h.begin() + d);
+    WGP_CUDA(cudaMemcpyAsync(tmp.p, h.data(), sizeof(double) * 2 * d, cudaMemcpyHostToDevice, st));
+    prepare_points(X.as<float>(), n, d, tmp.as<double>(), tmp.as<double>() + d, xs.as<float>(), n_pad,
+                   dp, st);
+    tc.invalidate();
+    WGP_CUDA(cudaStreamSynchronize(st));
+    have_hyper = true;
+  }
+
+  // ---------------------------------------------------------------- H.V
+  void hv(const float* V, int64_t ldv, int s, float* out, int64_t ldo, int mode, const float* B,
+          int64_t ldb, int64_t j0, int64_t j1, const int* row_idx, int64_t rr0, int64_t m,
+          const int* done = nullptr) {
+    HvParams p{};
+    p.xs = xs.as<float>();
+    p.n = n;
+    p.dp = dp;
+    p.row_idx = row_idx;
+    p.r0 = rr0;
+    p.m = m;
+    p.j0 = j0;
+    p.j1 = j1;
+    p.V = V;
+    p.ldv = ldv;
+    p.s = s;
+    p.out = out;
+    p.ldo = ldo;
+    p.B = B;
+    p.ldb = ldb;
+    p.mode = mode;
+    p.sf2 = sf2();
+    p.a = a_coef();
+    p.noise2 = noise2();
+    p.diag = static_cast<float>(sf * sf + sigma * sigma);
+    p.done = done;
+    if (hv_impl == WGP_HV_TC && hv_tc_supported(d, s)) {
+      if (!tc.valid) tc.build(xs.as<float>(), n, dp, d, st);
+      hv_tc(tc, p, st);
+    } else {
+      hv_simt(p, st);
+    }
+  }
+  // full-operator convenience: out (rows all) = H V
+  void hv_all(const float* V, int s, float* out, int mode = kHvStore, const float* B = nullptr,
+              const int* done = nullptr) {
+    hv(V, ld, s, out, ld, mode, B, ld, 0, n, nullptr, 0, n, done);
+  }
+
+  // ---------------------------------------------------------------- workspace
+  SolveCtrl* dctrl() { return ctrl.as<SolveCtrl>(); }
+  void ensure_solver_ws(int s) {
+    if (!ctrl.p) {
+      ctrl.ensure(sizeof(SolveCtrl));
+      WGP_CUDA(cudaMemsetAsync(ctrl.p, 0, sizeof(SolveCtrl), st));
+    }
+    conv.ensure(sizeof(int) * (s + 1));
+    rs.ensure(sizeof(double) * (s + 1));
+    alpha.ensure(sizeof(double) * (s + 1));
+    beta.ensure(sizeof(double) * (s + 1));
+    bnorm.ensure(sizeof(double) * (s + 1));
+    tol.ensure(sizeof(double) * (s + 1));
+    colsum.ensure(sizeof(double) * (s + 1));
+    part.ensure(sizeof(double) * static_cast<size_t>(reduce_blocks(n)) * (s + 2));
+    P.ensure(sizeof(float) * ld * s);
+    HP.ensure(sizeof(float) * ld * s);
+    Rtmp.ensure(sizeof(float) * ld * s);
+  }
+  ColState colstate() {
+    return ColState{conv.as<int>(), rs.as<double>(), alpha.as<double>(), beta.as<double>(),
+                    bnorm.as<double>(), tol.as<double>()};
+  }
+  std::vector<double> dots(const float* A, const float* B_, int s) {
+    ensure_solver_ws(s);
+    col_dots(A, B_, ld, n, s, part.as<double>(), &dctrl()->ticket, colsum.as<double>(), st);
+    std::vector<double> h(s);
+    WGP_CUDA(cudaMemcpyAsync(h.data(), colsum.p, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    return h;
+  }
+  void reset_ctrl(int max_it) {
+    SolveCtrl h{};
+    h.max_it = max_it;
+    WGP_CUDA(cudaMemcpyAsync(ctrl.p, &h, sizeof(SolveCtrl), cudaMemcpyHostToDevice, st));
+  }
+  const SolveCtrl& poll() {
+    WGP_CUDA(cudaMemcpyAsync(hctrl.h, ctrl.p, sizeof(SolveCtrl), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    return *hctrl.h;
+  }
+  void lazy_handles() {
+    if (!cublas) {
+      if (cublasCreate(&cublas) != CUBLAS_STATUS_SUCCESS) throw DeviceError("cublasCreate failed");
+      cublasSetStream(cublas, st);
+    }
+    if (!cusolver) {
+      if (cusolverDnCreate(&cusolver) != CUSOLVER_STATUS_SUCCESS) throw DeviceError("cusolverDnCreate failed");
+      cusolverDnSetStream(cusolver, st);
+    }
+  }
+
+  // ---------------------------------------------------------------- solvers
+  struct SolveOut {
+    int iterations = 0;
+    std::vector<double> rel;
+    std::vector<int> conv;
+  };
+
+  static void validate(const wgp_solver_cfg& c) {  // proj/src/solvers.cpp:31-37
+    if (!(c.tol_mean > 0.0 && c.tol_mean < 1.0) || !(c.tol_samples > 0.0 && c.tol_samples < 1.0))
+      throw std::invalid_argument("SolverConfig: tolerances must lie in (0, 1)");
+    if (c.block_size < 1) throw std::invalid_argument("SolverConfig: block_size must be >= 1");
+    if (c.minibatch_size < 1) throw std::invalid_argument("SolverConfig: minibatch_size must be >= 1");
+    if (c.max_iterations < 0) throw std::invalid_argument("SolverConfig: max_iterations must be >= 0");
+    if (c.kind < 0 || c.kind > 2) throw std::invalid_argument("solve: unknown solver kind");
+  }
+
+  [[noreturn]] void fail(const SolveCtrl& h, int kind) {
+    const std::string who = solver_name(kind);
+    if (h.status == kStatusNotPd)
+      throw NumericalError(kind == 0
+                               ? "cg_solve: non-positive curvature encountered, H is not positive definite"
+                               : who + ": H is not positive definite");
+    if (h.status == kStatusNaN)
+      throw NumericalError(who + (kind == 1 ? ": NaN in iterate at epoch " : ": NaN in iterate at iteration ") +
+                           std::to_string(h.fail_it));
+    throw NumericalError("sgd_solve: iterate diverged at step " + std::to_string(h.fail_it) +
+                         "; use a smaller learning rate");
+  }
+
+  // solve(H, rhs, init, config), proj/src/solvers.cpp:265-279.  Device
+  // pointers with leading dimension ld; init == nullptr means zeros.
+  SolveOut solve(const wgp_solver_cfg& cfg, const float* B, const float* init, float* Xo, float* Ro,
+                 int s) {
+    require_data();
+    validate(cfg);
+    if (s < 1) throw std::invalid_argument("solve: rhs needs at least one column");
+    ensure_solver_ws(s);
+    std::vector<double> bn = dots(B, B, s);
+    for (double& v : bn) {
+      if (!std::isfinite(v)) throw std::invalid_argument("solve: non-finite right-hand side or init");
+      v = std::sqrt(v);
+    }
+    if (init) {
+      for (double v : dots(init, init, s))
+        if (!std::isfinite(v)) throw std::invalid_argument("solve: non-finite right-hand side or init");
+    }
+    std::vector<double> tl(s);
+    for (int c = 0; c < s; ++c) tl[c] = c == 0 ? cfg.tol_mean : cfg.tol_samples;  // :49-56
+    WGP_CUDA(cudaMemcpyAsync(bnorm.p, bn.data(), sizeof(double) * s, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpyAsync(tol.p, tl.data(), sizeof(double) * s, cudaMemcpyHostToDevice, st));
+    // X = init; R = rhs - H X (exactly rhs for a zero init)
+    if (init) {
+      copy_cols(init, ld, Xo, ld, n, s, st);
+      hv_all(Xo, s, Ro, kHvResidual, B);
+    } else {
+      fill_zero(Xo, ld, n, s, st);
+      copy_cols(B, ld, Ro, ld, n, s, st);
+    }
+    SolveOut out;
+    if (cfg.kind == WGP_SOLVER_CG) cg(cfg, B, Xo, Ro, s, out);
+    else if (cfg.kind == WGP_SOLVER_AP) ap(cfg, B, Xo, Ro, s, out);
+    else sgd(cfg, B, Xo, Ro, s, out);
+    // finalize_exact_residuals, :69-77
+    float* E = Rtmp.as<float>();
+    hv_all(Xo, s, E, kHvResidual, B);
+    std::vector<double> en = dots(E, E, s);
+    out.rel.resize(s);
+    for (int c = 0; c < s; ++c) out.rel[c] = bn[c] > 0.0 ? std::sqrt(en[c]) / bn[c] : 0.0;
+    out.conv.resize(s);
+    WGP_CUDA(cudaMemcpyAsync(out.conv.data(), conv.p, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    for (int& c : out.conv) c = c != 0;
+    return out;
+  }
+
+  void cg(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {
+    const int max_it = cfg.max_iterations > 0 ? cfg.max_iterations : static_cast<int>(10 * n);
+    reset_ctrl(max_it);
+    float* Pp = P.as<float>();
+    float* HPp = HP.as<float>();
+    float* Rt = Rtmp.as<float>();
+    const ColState cs = colstate();
+    SolveCtrl* c = dctrl();
+    double* pt = part.as<double>();
+    cg_init(Pp, R, ld, n, s, cs, pt, c, st);
+    const int* done = &c->done;
+    int launched = 0;
+    int chunk = 2;
+    while (true) {
+      const SolveCtrl& h = poll();
+      if (h.done) {
+        if (h.status != kStatusOk) fail(h, 0);
+        out.iterations = h.it;
+        return;
+      }
+      for (int k = 0; k < chunk; ++k) {
+        const int it = ++launched;
+        const bool refresh = it % 50 == 0;  // :111
+        hv_all(Pp, s, HPp, kHvStore, nullptr, done);
+        cg_alpha(Pp, HPp, ld, n, s, cs, pt, c, st);
+        if (!refresh) {
+          cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, false, st);
+        } else {
+          cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, true, st);
+          hv_all(Xo, s, Rt, kHvResidual, B, done);
+          cg_refresh_norm(R, Rt, ld, n, s, cs, pt, c, st);
+        }
+        cg_direction(Pp, R, ld, n, s, cs, pt, c, st);
+      }
+      chunk = std::min(chunk * 2, 8);
+    }
+  }
+
+  void ap(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {
+    lazy_handles();
+    const int max_ep = cfg.max_iterations > 0 ? cfg.max_iterations : 1000;
+    const int64_t bs = std::min<int64_t>(std::max(cfg.block_size, 1), n);
+    const int64_t nb = ceil_div(n, bs);
+    // Factor every diagonal block once per solve (:151-165): H[b,b] in fp64,
+    // Cholesky, explicit inverse, so each Gauss-Seidel step is one symmetric
+    // GEMM on the tensor-free fp64 path.
+    hbuf.ensure(sizeof(double) * static_cast<size_t>(nb) * bs * bs);
+    info.ensure(sizeof(int) * nb);
+    WGP_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int) * nb, st));
+    int lw1 = 0, lw2 = 0;
+    cusolverDnDpotrf_bufferSize(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(bs), hbuf.as<double>(),
+                                static_cast<int>(bs), &lw1);
+    cusolverDnDpotri_bufferSize(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(bs), hbuf.as<double>(),
+                                static_cast<int>(bs), &lw2);
+    const int lw = std::max(lw1, lw2);
+    lapack_work.ensure(sizeof(double) * std::max(lw, 1));
+    const double sf2d = sf * sf, ad = sf * sf * kLn2, n2d = sigma * sigma;
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t start = b * bs, size = std::min(bs, n - start);
+      double* Hb = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
+      build_block(xs.as<float>(), dp, start, size, sf2d, ad, n2d, Hb, st);
+      cusolverDnDpotrf(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(size), Hb, static_cast<int>(size),
+                       lapack_work.as<double>(), lw, info.as<int>() + b);
+    }
+    std::vector<int> hinfo(nb);
+    WGP_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    for (int v : hinfo)
+      if (v != 0)
+        throw NumericalError("ap_solve: diagonal block factorization failed, H is not positive definite");
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t start = b * bs, size = std::min(bs, n - start);
+      double* Hb = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
+      cusolverDnDpotri(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(size), Hb, static_cast<int>(size),
+                       lapack_work.as<double>(), lw, info.as<int>() + b);
+      (void)start;
+    }
+    Rb.ensure(sizeof(double) * bs * s);
+    D64.ensure(sizeof(double) * bs * s);
+    D32.ensure(sizeof(float) * bs * s);
+    reset_ctrl(max_ep);
+    const ColState cs = colstate();
+    SolveCtrl* c = dctrl();
+    double* pt = part.as<double>();
+    norms_convergence(R, ld, n, s, cs, pt, c, false, true, st);  // :172-178
+    const double one = 1.0, zero = 0.0;
+    while (true) {
+      const SolveCtrl& h = poll();
+      if (h.done) {
+        if (h.status != kStatusOk) fail(h, 1);
+        out.iterations = h.it;
+        return;
+      }
+      for (int64_t b = 0; b < nb; ++b) {  // :183-187
+        const int64_t start = b * bs, size = std::min(bs, n - start);
+        const double* Hinv = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
+        ap_gather(R, ld, start, size, s, Rb.as<double>(), c, st);
+        cublasDsymm(cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, static_cast<int>(size), s, &one,
+                    Hinv, static_cast<int>(size), Rb.as<double>(), static_cast<int>(size), &zero,
+                    D64.as<double>(), static_cast<int>(size));
+        ap_apply(Xo, ld, start, size, s, D64.as<double>(), D32.as<float>(), c, st);
+        // R -= H[:, blk] delta : contracted points [start, start + size)
+        hv(D32.as<float>() - start, size, s, R, ld, kHvSubtract, nullptr, 0, start, start + size,
+           nullptr, 0, n, &c->done);
+      }
+      hv_all(Xo, s, R, kHvResidual, B);                            // :188
+      norms_convergence(R, ld, n, s, cs, pt, c, true, true, st);  // :189-191
+    }
+  }
+
+  void sgd(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {
+    const int64_t m = std::min<int64_t>(std::max(cfg.minibatch_size, 1), n);
+    const int max_steps = cfg.max_iterations > 0 ? cfg.max_iterations : static_cast<int>((100 * n) / m);
+    vel.ensure(sizeof(float) * ld * s);
+    fill_zero(vel.as<float>(), ld, n, s, st);
+    batch.ensure(sizeof(float) * m * s);
+    constexpr int K = 8;  // steps per host round trip
+    idx.ensure(sizeof(int) * m * K);
+    std::vector<int> hidx(static_cast<size_t>(m) * K);
+    reset_ctrl(max_steps);
+    const ColState cs = colstate();
+    SolveCtrl* c = dctrl();
+    double* pt = part.as<double>();
+    norms_convergence(R, ld, n, s, cs, pt, c, false, true, st);
+    std::vector<int64_t> pool(n);
+    std::iota(pool.begin(), pool.end(), 0);
+    std::mt19937_64 rng(cfg.seed);
+    const float gs = static_cast<float>(static_cast<double>(n) / static_cast<double>(m));
+    const float ss = static_cast<float>(cfg.learning_rate / static_cast<double>(n));
+    while (true) {
+      const SolveCtrl& h = poll();
+      if (h.done) {
+        if (h.status != kStatusOk) fail(h, 2);
+        out.iterations = h.it;
+        return;
+      }
+      // minibatch index stream, partial Fisher-Yates on the persistent pool (:237-240)
+      for (int k = 0; k < K; ++k)
+        for (int64_t i = 0; i < m; ++i) {
+          const int64_t j = i + static_cast<int64_t>(uniform_below(rng, static_cast<uint64_t>(n - i)));
+          std::swap(pool[i], pool[j]);
+          hidx[static_cast<size_t>(k) * m + i] = static_cast<int>(pool[i]);
+        }
+      WGP_CUDA(cudaMemcpyAsync(idx.p, hidx.data(), sizeof(int) * m * K, cudaMemcpyHostToDevice, st));
+      for (int k = 0; k < K; ++k) {
+        const int* ik = idx.as<int>() + static_cast<size_t>(k) * m;
+        // batch = B[I] - H[I, :] X  (:241-243)
+        hv(Xo, ld, s, batch.as<float>(), m, kHvResidual, B, ld, 0, n, ik, 0, m, &c->done);
+        sgd_scatter(Xo, R, vel.as<float>(), ld, ik, m, s, batch.as<float>(),
+                    static_cast<float>(cfg.momentum), gs, ss, c, st);
+        sgd_check(Xo, R, ld, n, s, cs, pt, c, st);
+      }
+    }
+  }
+
+  // warm_start_distance, proj/src/estimator.cpp:84-95
+  double warm_distance(const float* init, const float* sol, int s) {
+    ensure_solver_ws(s);
+    float* D = P.as<float>();
+    float* HD = HP.as<float>();
+    sub_into(init, sol, D, ld, n, s, st);
+    hv_all(D, s, HD);
+    const std::vector<double> q = dots(D, HD, s);
+    double acc = 0.0;
+    for (double v : q) acc += v;
+    return std::sqrt(std::max(acc / s / static_cast<double>(n), 0.0));
+  }
+
+  // ---------------------------------------------------------------- gradient
+  // derivative_contractions for A = vy vy^T / 2, B = coef L R^T (device
+  // inputs, ld); raw-space outputs on the host.
+  void grad(int transform, const double* raw, const float* vy, const float* L, const float* R,
+            int s, double coef_b, double* out_a, double* out_b) {
+    std::vector<double> cons(d + 2);
+    for (int k = 0; k < d + 2; ++k) cons[k] = transform == 1 ? std::exp(raw[k]) : softplus(raw[k]);
+    set_hyper(cons.data());
+    const int nblk = grad_blocks(n);
+    const int W = 2 * (d + 1);
+    gpart.ensure(sizeof(double) * nblk * W);
+    gout.ensure(sizeof(double) * W);
+    GradParams gp{};
+    gp.xs = xs.as<float>();
+    gp.n = n;
+    gp.dp = dp;
+    gp.d = d;
+    gp.vy = vy;
+    gp.L = L;
+    gp.R = R;
+    gp.ld = ld;
+    gp.s = s;
+    gp.coef_b = static_cast<float>(coef_b);
+    gp.sf2 = sf2();
+    gp.a = a_coef();
+    gp.part = gpart.as<double>();
+    grad_simt(gp, st);
+    grad_finalize(gpart.as<double>(), nblk, W, gout.as<double>(), st);
+    std::vector<double> acc(W);
+    WGP_CUDA(cudaMemcpyAsync(acc.data(), gout.p, sizeof(double) * W, cudaMemcpyDeviceToHost, st));
+    const std::vector<double> yy = dots(vy, vy, 1);
+    const std::vector<double> lr = dots(L, R, s);
+    double tb = 0.0;
+    for (double v : lr) tb += v;
+    auto chain = [&](double r) { return transform == 1 ? std::exp(r) : softplus_derivative(r); };
+    const double c2 = kUScale * kUScale;
+    for (int k = 0; k < d; ++k) {
+      const double scale = 3.0 * sf * sf * chain(raw[k]) / (ls[k] * c2);
+      out_a[k] = scale * acc[k];
+      out_b[k] = scale * acc[d + 1 + k];
+    }
+    const double csf = 2.0 * chain(raw[d]) / sf;
+    out_a[d] = csf * acc[d];
+    out_b[d] = csf * acc[d + 1 + d];
+    const double dn = 2.0 * sigma * chain(raw[d + 1]);
+    out_a[d + 1] = dn * 0.5 * yy[0];
+    out_b[d + 1] = dn * coef_b * tb;
+  }
+
+  static double softplus(double x) { return x > 0.0 ? x + std::log1p(std::exp(-x)) : std::log1p(std::exp(x)); }
+  static double softplus_inverse(double v) {
+    if (!(v > 0.0)) throw std::invalid_argument("softplus_inverse: argument must be positive");
+    return v > 0.6931471805599453 ? v + std::log1p(-std::exp(-v)) : std::log(std::expm1(v));
+  }
+  static double softplus_derivative(double x) {
+    if (x > 0.0) return 1.0 / (1.0 + std::exp(-x));
+    const double e = std::exp(x);
+    return e / (1.0 + e);
+  }
+
+  // ---------------------------------------------------------------- RFF probes
+  struct DevRff {
+    int F = 0, s = 0;
+    Buf b, w, eps, om;
+    RffBase host;
+  };
+  void rff_upload(DevRff& r, int F, int s, uint64_t seed) {
+    r.host = rff_base_host(n, d, F, s, seed, ld);
+    r.F = F;
+    r.s = s;
+    std::vector<float> wf(r.host.w.begin(), r.host.w.end());
+    r.b.ensure(sizeof(double) * F);
+    r.w.ensure(sizeof(float) * F * s);
+    r.eps.ensure(sizeof(float) * ld * s);
+    r.om.ensure(sizeof(double) * F * d);
+    WGP_CUDA(cudaMemcpyAsync(r.b.p, r.host.b.data(), sizeof(double) * F, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpyAsync(r.w.p, wf.data(), sizeof(float) * F * s, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpyAsync(r.eps.p, r.host.eps.data(), sizeof(float) * ld * s, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+  }
+  void rff_eval(DevRff& r, float* out) {
+    std::vector<double> om(static_cast<size_t>(r.F) * d);
+    for (int f = 0; f < r.F; ++f) {
+      const double scale = 1.0 / std::sqrt(r.host.chi2[f] / 3.0);
+      for (int k = 0; k < d; ++k)
+        om[static_cast<size_t>(f) * d + k] = r.host.omega_z[static_cast<size_t>(f) * d + k] * scale / ls[k];
+    }
+    WGP_CUDA(cudaMemcpyAsync(r.om.p, om.data(), sizeof(double) * om.size(), cudaMemcpyHostToDevice, st));
+    for (int c0 = 0; c0 < r.s; c0 += 128) {
+      RffParams p{};
+      p.x = X.as<float>();
+      p.n = n;
+      p.d = d;
+      p.om = r.om.as<double>();
+      p.b = r.b.as<double>();
+      p.w = r.w.as<float>() + static_cast<size_t>(c0) * r.F;
+      p.eps = r.eps.as<float>() + static_cast<size_t>(c0) * ld;
+      p.F = r.F;
+      p.s = std::min(128, r.s - c0);
+      p.ld = ld;
+      p.amp = static_cast<float>(sf * std::sqrt(2.0 / r.F));
+      p.sigma = static_cast<float>(sigma);
+      p.out = out + static_cast<size_t>(c0) * ld;
+      rff_probes(p, st);
+    }
+    WGP_CUDA(cudaStreamSynchronize(st));  // om host buffer lifetime
+  }
+
+  // ---------------------------------------------------------------- training
+  double to_c(int tr, double raw) const { return tr == 1 ? std::exp(raw) : softplus(raw); }
+  double to_r(int tr, double v) const {
+    if (tr == 1) {
+      if (!(v > 0.0)) throw std::invalid_argument("log transform: argument must be positive");
+      return std::log(v);
+    }
+    return softplus_inverse(v);
+  }
+
+  void train(const float* yh, const wgp_train_cfg& cfg, wgp_trace* tr) {  // optimizer.cpp:81-171
+    if (cfg.steps < 1) throw std::invalid_argument("TrainConfig: steps must be >= 1");
+    if (cfg.num_probes < 1) throw std::invalid_argument("TrainConfig: num_probes must be >= 1");
+    if (!(cfg.learning_rate > 0.0)) throw std::invalid_argument("TrainConfig: learning rate must be positive");
+    if (!(cfg.init_constrained > 0.0))
+      throw std::invalid_argument("TrainConfig: initial constrained value must be positive");
+    validate(cfg.solver);
+    if (n < 1) throw std::invalid_argument("train: dataset is empty");
+    const int p = d + 2, s = cfg.num_probes, sp = s + 1;
+    const int T = cfg.transform;
+    std::vector<double> raw(p), m(p, 0.0), v(p, 0.0);
+    for (int k = 0; k < d; ++k) raw[k] = to_r(T, cfg.init_constrained);
+    raw[d] = to_r(T, cfg.init_signal > 0.0 ? cfg.init_signal : cfg.init_constrained);
+    raw[d + 1] = to_r(T, cfg.init_noise > 0.0 ? cfg.init_noise : cfg.init_constrained);
+    const bool fixed = cfg.mode != 1, warm = cfg.mode == 0, pathwise = cfg.estimator == 1;
+    const int F = cfg.rff_features > 0 ? cfg.rff_features : 1000;
+
+    Buf rhs, sol0, sol1, Rres;
+    rhs.ensure(sizeof(float) * ld * sp);
+    sol0.ensure(sizeof(float) * ld * sp);
+    sol1.ensure(sizeof(float) * ld * sp);
+    Rres.ensure(sizeof(float) * ld * sp);
+    WGP_CUDA(cudaMemsetAsync(rhs.p, 0, sizeof(float) * ld * sp, st));
+    WGP_CUDA(cudaMemcpyAsync(rhs.p, yh, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+    float* Z = rhs.as<float>() + ld;
+    std::vector<float> hz;
+    DevRff rff;
+    uint64_t probe_seed = 0;
+    auto draw = [&](uint64_t seed) {
+      probe_seed = seed;
+      if (pathwise) {
+        rff_upload(rff, F, s, seed);
+      } else {
+        hz.assign(static_cast<size_t>(ld) * s, 0.f);
+        sample_probes_host(n, s, cfg.probe_distribution, seed, hz.data(), ld);
+        WGP_CUDA(cudaMemcpyAsync(Z, hz.data(), sizeof(float) * ld * s, cudaMemcpyHostToDevice, st));
+        WGP_CUDA(cudaStreamSynchronize(st));
+      }
+    };
+    if (fixed) draw(derive_seed(cfg.seed, 1));
+    float* cur = sol0.as<float>();
+    float* prev = sol1.as<float>();
+    bool have_prev = false;
+    cudaEvent_t e0, e1, e2;
+    WGP_CUDA(cudaEventCreate(&e0));
+    WGP_CUDA(cudaEventCreate(&e1));
+    WGP_CUDA(cudaEventCreate(&e2));
+    try {
+      for (int t = 1; t <= cfg.steps; ++t) {
+        try {
+          std::vector<double> cons(p);
+          for (int k = 0; k < p; ++k) cons[k] = to_c(T, raw[k]);
+          WGP_CUDA(cudaEventRecord(e0, st));
+          set_hyper(cons.data());
+          if (!fixed) draw(derive_seed(cfg.seed, static_cast<uint64_t>(t)));
+          if (pathwise) rff_eval(rff, Z);
+          wgp_solver_cfg sc = cfg.solver;
+          sc.seed = derive_seed(derive_seed(cfg.seed, kSolverStream), static_cast<uint64_t>(t));
+          const bool have_warm = warm && have_prev;
+          SolveOut so = solve(sc, rhs.as<float>(), have_warm ? prev : nullptr, cur, Rres.as<float>(), sp);
+          WGP_CUDA(cudaEventRecord(e1, st));
+          double wsd = 0.0;
+          if (have_warm && cfg.warm_start_distance) wsd = warm_distance(prev, cur, sp);
+          std::vector<double> qa(p), qb(p), g(p);
+          grad(T, raw.data(), cur, cur + ld, pathwise ? cur + ld : Z, s, 0.5 / s, qa.data(), qb.data());
+          for (int k = 0; k < p; ++k) g[k] = qa[k] - qb[k];
+          adam(raw.data(), g.data(), m.data(), v.data(), p, t, cfg.learning_rate, cfg.adam_beta1,
+               cfg.adam_beta2, cfg.adam_eps);
+          WGP_CUDA(cudaEventRecord(e2, st));
+          WGP_CUDA(cudaEventSynchronize(e2));
+          if (tr) {
+            const size_t off = static_cast<size_t>(t - 1) * p;
+            if (tr->raw_params) std::memcpy(tr->raw_params + off, raw.data(), sizeof(double) * p);
+            if (tr->constrained_params)
+              for (int k = 0; k < p; ++k) tr->constrained_params[off + k] = to_c(T, raw[k]);
+            if (tr->gradient) std::memcpy(tr->gradient + off, g.data(), sizeof(double) * p);
+            if (tr->solver_iterations) tr->solver_iterations[t - 1] = so.iterations;
+            if (tr->per_column_relative_residual)
+              std::memcpy(tr->per_column_relative_residual + static_cast<size_t>(t - 1) * sp, so.rel.data(),
+                          sizeof(double) * sp);
+            if (tr->warm_start_distance) tr->warm_start_distance[t - 1] = wsd;
+            if (tr->probe_seed) tr->probe_seed[t - 1] = probe_seed;
+            float ms_solve = 0.f, ms_step = 0.f;
+            WGP_CUDA(cudaEventElapsedTime(&ms_solve, e0, e1));
+            WGP_CUDA(cudaEventElapsedTime(&ms_step, e0, e2));
+            if (tr->solver_ms) tr->solver_ms[t - 1] = ms_solve;
+            if (tr->step_ms) tr->step_ms[t - 1] = ms_step;
+          }
+          std::swap(cur, prev);
+          have_prev = true;
+        } catch (const NumericalError& e) {
+          throw NumericalError("step " + std::to_string(t) + ": " + e.what());
+        }
+      }
+      if (tr && tr->final_solutions) {
+        // prev holds the last step's solutions after the swap
+        WGP_CUDA(cudaMemcpy2DAsync(tr->final_solutions, sizeof(float) * n, prev, sizeof(float) * ld,
+                                   sizeof(float) * n, sp, cudaMemcpyDeviceToHost, st));
+        WGP_CUDA(cudaStreamSynchronize(st));
+      }
+    } catch (...) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      cudaEventDestroy(e2);
+      throw;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+  }
+
+  static void adam(double* raw, const double* g, double* m, double* v, int p, int t, double lr,
+                   double b1, double b2, double eps) {  // optimizer.cpp:48-65
+    if (t < 1) throw std::invalid_argument("adam_step: t must be >= 1");
+    for (int k = 0; k < p; ++k)
+      if (!std::isfinite(g[k])) throw NumericalError("adam_step: non-finite gradient at step " + std::to_string(t));
+    const double c1 = 1.0 - std::pow(b1, t), c2 = 1.0 - std::pow(b2, t);
+    for (int k = 0; k < p; ++k) {
+      m[k] = b1 * m[k] + (1.0 - b1) * g[k];
+      v[k] = b2 * v[k] + (1.0 - b2) * (g[k] * g[k]);
+      raw[k] += lr * (m[k] / c1) / (std::sqrt(v[k] / c2) + eps);
+    }
+  }
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return WGP_OK;
+  } catch (const NumericalError& e) {
+    g_last_error = e.what();
+    return WGP_NUMERICAL;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return WGP_INVALID;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return WGP_DEVICE;
+  }
+}
+
+}  // namespace wgp
+
+struct wgp_ctx {
+  wgp::Ctx c;
+};
+
+using wgp::guarded;
+
+extern "C" {
+
+const char* wgp_last_error(void) { return wgp::g_last_error.c_str(); }
+
+const char* wgp_version(void) {
+  return "warmgp_b200 0.1 (sm_100a; tcgen05 3xTF32 H.V + SIMT fp32 kernels; NCCL row sharding)";
+}
+
+int wgp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int wgp_create(int device, wgp_ctx** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("wgp_create: null output pointer");
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+      cudaGetLastError();
+      throw wgp::DeviceError("no CUDA device available (warmgp_b200 has no CPU fallback)");
+    }
+    if (device < 0 || device >= count) throw std::invalid_argument("wgp_create: device out of range");
+    WGP_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    WGP_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw wgp::DeviceError("warmgp_b200 is built for sm_100a (B200); found sm_" +
+                             std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* ctx = new wgp_ctx();
+    ctx->c.device = device;
+    if (cudaStreamCreateWithFlags(&ctx->c.st, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      throw wgp::DeviceError("cudaStreamCreate failed");
+    }
+    *out = ctx;
+  });
+}
+
+int wgp_destroy(wgp_ctx* ctx) {
+  return guarded([&] {
+    if (ctx) {
+      cudaSetDevice(ctx->c.device);
+      delete ctx;
+    }
+  });
+}
+
+int wgp_set_hv_impl(wgp_ctx* ctx, int impl) {
+  return guarded([&] {
+    if (impl != WGP_HV_TC && impl != WGP_HV_SIMT) throw std::invalid_argument("unknown H.V implementation");
+    ctx->c.hv_impl = impl;
+  });
+}
+
+void* wgp_stream(wgp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.st) : nullptr; }
+
+int wgp_set_data(wgp_ctx* ctx, const float* X, int64_t n, int d) {
+  return guarded([&] {
+    WGP_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.set_data(X, n, d);
+  });
+}
+
+int wgp_set_hyper(wgp_ctx* ctx, const double* c) {
+  return guarded([&] {
+    WGP_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.set_hyper(c);
+  });
+}
+
+int wgp_set_rows(wgp_ctx* ctx, int64_t r0, int64_t r1) {
+  return guarded([&] {
+    if (r0 < 0 || r1 > ctx->c.n || r1 <= r0) throw std::invalid_argument("wgp_set_rows: bad row range");
+    ctx->c.r0 = r0;
+    ctx->c.r1 = r1;
+  });
+}
+
+int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    WGP_CUDA(cudaSetDevice(c.device));
+    c.require_data();
+    if (s < 1) throw std::invalid_argument("wgp_hv: s must be >= 1");
+    const int64_t m = c.r1 - c.r0;
+    wgp::Buf& dv = c.io_in;
+    wgp::Buf& dout = c.io_out;
+    dv.ensure(sizeof(float) * c.ld * s);
+    dout.ensure(sizeof(float) * m * s);
+    WGP_CUDA(cudaMemcpy2DAsync(dv.p, sizeof(float) * c.ld, V, sizeof(float) * c.n, sizeof(float) * c.n, s,
+                               cudaMemcpyHostToDevice, c.st));
+    c.hv(dv.as<float>(), c.ld, s, dout.as<float>(), m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, m);
+    WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(float) * m * s, cudaMemcpyDeviceToHost, c.st));
+    WGP_CUDA(cudaStreamSynchronize(c.st));
+  });
+}
+
+int wgp_hv_device(wgp_ctx* ctx, const float* V, int64_t ldv, int s, float* out, int64_t ldo) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    c.require_data();
+    if (s < 1) throw std::invalid_argument("wgp_hv: s must be >= 1");
+    if (ldv < c.n || ldo < c.r1 - c.r0) throw std::invalid_argument("wgp_hv: leading dimension too small");
+    c.hv(V, ldv, s, out, ldo, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, c.r1 - c.r0);
+  });
+}
+
+int wgp_solve(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const float* rhs, const float* init, int s,
+              wgp_solve_state* state) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    WGP_CUDA(cudaSetDevice(c.device));
+    c.require_data();
+    if (s < 1) throw std::invalid_argument("solve: rhs needs at least one column");
+    for (int64_t e = 0; e < c.n * s; ++e)
+      if (!std::isfinite(rhs[e]) || (init && !std::isfinite(init[e])))
+        throw std::invalid_argument("solve: non-finite right-hand side or init");
+    wgp::Buf B, X0, Xs, Rs;
+    const size_t bytes = sizeof(float) * c.ld * s;
+    B.ensure(bytes);
+    Xs.ensure(bytes);
+    Rs.ensure(bytes);
+    WGP_CUDA(cudaMemsetAsync(B.p, 0, bytes, c.st));
+    WGP_CUDA(cudaMemcpy2DAsync(B.p, sizeof(float) * c.ld, rhs, sizeof(float) * c.n, sizeof(float) * c.n, s,
+                               cudaMemcpyHostToDevice, c.st));
+    if (init) {
+      X0.ensure(bytes);
+      WGP_CUDA(cudaMemsetAsync(X0.p, 0, bytes, c.st));
+      WGP_CUDA(cudaMemcpy2DAsync(X0.p, sizeof(float) * c.ld, init, sizeof(float) * c.n, sizeof(float) * c.n,
+                                 s, cudaMemcpyHostToDevice, c.st));
+    }
+    const wgp::Ctx::SolveOut so =
+        c.solve(*cfg, B.as<float>(), init ? X0.as<float>() : nullptr, Xs.as<float>(), Rs.as<float>(), s);
+    if (state) {
+      if (state->solutions)
+        WGP_CUDA(cudaMemcpy2DAsync(state->solutions, sizeof(float) * c.n, Xs.p, sizeof(float) * c.ld,
+                                   sizeof(float) * c.n, s, cudaMemcpyDeviceToHost, c.st));
+      if (state->residuals)
+        WGP_CUDA(cudaMemcpy2DAsync(state->residuals, sizeof(float) * c.n, Rs.p, sizeof(float) * c.ld,
+                                   sizeof(float) * c.n, s, cudaMemcpyDeviceToHost, c.st));
+      WGP_CUDA(cudaStreamSynchronize(c.st));
+      if (state->per_column_relative_residual)
+        std::copy(so.rel.begin(), so.rel.end(), state->per_column_relative_residual);
+      if (state->converged) std::copy(so.conv.begin(), so.conv.end(), state->converged);
+      state->iterations_used = so.iterations;
+    }
+  });
+}
+
+int wgp_grad(wgp_ctx* ctx, int transform, const double* raw, const float* vy, const float* L,
+             const float* R, int s, double coef_b, double* out_a, double* out_b) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    WGP_CUDA(cudaSetDevice(c.device));
+    if (c.n < 1) throw std::invalid_argument("no training inputs: call wgp_set_data first");
+    if (s < 1) throw std::invalid_argument("wgp_grad: s must be >= 1");
+    wgp::Buf dvy, dL, dR;
+    const size_t bytes = sizeof(float) * c.ld * s;
+    dvy.ensure(sizeof(float) * c.ld);
+    dL.ensure(bytes);
+    dR.ensure(bytes);
+    WGP_CUDA(cudaMemsetAsync(dvy.p, 0, sizeof(float) * c.ld, c.st));
+    WGP_CUDA(cudaMemsetAsync(dL.p, 0, bytes, c.st));
+    WGP_CUDA(cudaMemsetAsync(dR.p, 0, bytes, c.st));
+    WGP_CUDA(cudaMemcpyAsync(dvy.p, vy, sizeof(float) * c.n, cudaMemcpyHostToDevice, c.st));
+    WGP_CUDA(cudaMemcpy2DAsync(dL.p, sizeof(float) * c.ld, L, sizeof(float) * c.n, sizeof(float) * c.n, s,
+                               cudaMemcpyHostToDevice, c.st));
+    WGP_CUDA(cudaMemcpy2DAsync(dR.p, sizeof(float) * c.ld, R, sizeof(float) * c.n, sizeof(float) * c.n, s,
+                               cudaMemcpyHostToDevice, c.st));
+    c.grad(transform, raw, dvy.as<float>(), dL.as<float>(), dR.as<float>(), s, coef_b, out_a, out_b);
+  });
+}
+
+int wgp_sample_probes(int64_t n, int s, int dist, uint64_t seed, float* out) {
+  return guarded([&] { wgp::sample_probes_host(n, s, dist, seed, out, n); });
+}
+
+int wgp_rff_probes(wgp_ctx* ctx, int F, int s, uint64_t seed, float* out) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    WGP_CUDA(cudaSetDevice(c.device));
+    c.require_data();
+    if (F < 1 || s < 1) throw std::invalid_argument("rff_probes: F and s must be >= 1");
+    wgp::Ctx::DevRff r;
+    c.rff_upload(r, F, s, seed);
+    wgp::Buf dz;
+    dz.ensure(sizeof(float) * c.ld * s);
+    c.rff_eval(r, dz.as<float>());
+    WGP_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * c.n, dz.p, sizeof(float) * c.ld, sizeof(float) * c.n, s,
+                               cudaMemcpyDeviceToHost, c.st));
+    WGP_CUDA(cudaStreamSynchronize(c.st));
+  });
+}
+
+int wgp_train(wgp_ctx* ctx, const float* y, const wgp_train_cfg* cfg, wgp_trace* trace) {
+  return guarded([&] {
+    WGP_CUDA(cudaSetDevice(ctx->c.device));
+    if (ctx->c.n < 1) throw std::invalid_argument("train: dataset is empty");
+    ctx->c.train(y, *cfg, trace);
+  });
+}
+
+int wgp_adam_step(double* raw, const double* grad, double* m, double* v, int p, int t, double lr,
+                  double beta1, double beta2, double eps) {
+  return guarded([&] { wgp::Ctx::adam(raw, grad, m, v, p, t, lr, beta1, beta2, eps); });
+}
+
+uint64_t wgp_derive_seed(uint64_t base, uint64_t stream) { return wgp::derive_seed(base, stream); }
+
+}  // extern "C"

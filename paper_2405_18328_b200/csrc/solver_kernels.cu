@@ -1,0 +1,487 @@
+// solver_kernels.cu — CG / AP / SGD vector kernels with fused column
+// reductions.  Semantics follow proj/src/solvers.cpp:
+// CG :81-139, AP :141-196, SGD :198-263; see solver_kernels.cuh.
+#include <math.h>
+
+#include "common.cuh"
+#include "solver_kernels.cuh"
+
+namespace wgp {
+namespace {
+
+constexpr int NT = 256;
+constexpr int SMAX = 256;
+
+struct Red {
+  double v[NT / 32][SMAX];
+};
+
+// Per-column partial of the CTA's row range; lane 0 of each warp deposits.
+__device__ __forceinline__ void deposit(Red& red, int c, double v) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red.v[threadIdx.x >> 5][c] = v;
+}
+
+// Writes this CTA's partials and returns true in the last CTA to finish.
+__device__ bool publish(Red& red, int s, double* part, SolveCtrl* ctrl) {
+  __syncthreads();
+  for (int c = threadIdx.x; c < s; c += blockDim.x) {
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t += red.v[w][c];
+    part[static_cast<int64_t>(blockIdx.x) * s + c] = t;
+  }
+  __threadfence();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  return true;
+}
+
+__device__ __forceinline__ double total_of(const double* part, int c, int s) {
+  double t = 0.0;
+  for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(part + static_cast<int64_t>(b) * s + c);
+  return t;
+}
+
+// After the per-column work of the last CTA: count converged columns, promote
+// "converged this iteration" to frozen, and decide whether to run another
+// iteration (the while-condition of solvers.cpp:107 / :181 / :234).
+__device__ void loop_check(int s, ColState cs, SolveCtrl* ctrl, bool begin_next) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctrl->ticket = 0;
+    int nconv = 0;
+    for (int c = 0; c < s; ++c) nconv += cs.conv[c] != 0;
+    ctrl->nconv = nconv;
+    if (ctrl->status != kStatusOk) {
+      ctrl->done = 1;
+    } else if (begin_next) {
+      if (nconv == s || ctrl->it >= ctrl->max_it)
+        ctrl->done = 1;
+      else
+        ctrl->it += 1;
+    }
+  }
+}
+
+#define ROWS_OF_BLOCK                                                   \
+  const int64_t rb = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock;  \
+  const int64_t re = rb + kRowsPerBlock < n ? rb + kRowsPerBlock : n;
+
+__global__ void col_dots_kernel(const float* A, const float* B, int64_t ld, int64_t n, int s,
+                                double* part, unsigned* ticket, double* out) {
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  for (int c = 0; c < s; ++c) {
+    double v = 0.0;
+    for (int64_t i = rb + threadIdx.x; i < re; i += NT)
+      v += static_cast<double>(A[i + c * ld]) * static_cast<double>(B[i + c * ld]);
+    deposit(red, c, v);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < s; c += NT) {
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t += red.v[w][c];
+    part[static_cast<int64_t>(blockIdx.x) * s + c] = t;
+  }
+  __threadfence();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < s; c += NT) out[c] = total_of(part, c, s);
+  if (threadIdx.x == 0) *ticket = 0;
+}
+
+__global__ void cg_init_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
+                               ColState cs, double* part, SolveCtrl* ctrl) {
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  for (int c = 0; c < s; ++c) {
+    double v = 0.0;
+    for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
+      const double r = R[i + c * ld];
+      v += r * r;
+    }
+    deposit(red, c, v);
+  }
+  if (!publish(red, s, part, ctrl)) return;
+  for (int c = threadIdx.x; c < s; c += NT) {
+    const double rs = total_of(part, c, s);
+    cs.rs[c] = rs;
+    const bool conv = cs.bnorm[c] == 0.0 || sqrt(rs) <= cs.tol[c] * cs.bnorm[c];
+    cs.conv[c] = conv ? 1 : 0;
+  }
+  loop_check(s, cs, ctrl, true);
+}
+
+// P = R for active columns, 0 otherwise (separate pass: needs conv flags).
+__global__ void cg_seed_direction_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
+                                         const int* conv) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= n) return;
+  P[i + c * ld] = conv[c] ? 0.f : R[i + c * ld];
+}
+
+__global__ void cg_alpha_kernel(const float* P, const float* HP, int64_t ld, int64_t n, int s,
+                                ColState cs, double* part, SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  for (int c = 0; c < s; ++c) {
+    double v = 0.0;
+    if (!cs.conv[c])
+      for (int64_t i = rb + threadIdx.x; i < re; i += NT)
+        v += static_cast<double>(P[i + c * ld]) * static_cast<double>(HP[i + c * ld]);
+    deposit(red, c, v);
+  }
+  if (!publish(red, s, part, ctrl)) return;
+  for (int c = threadIdx.x; c < s; c += NT) {
+    if (cs.conv[c]) continue;
+    const double pHp = total_of(part, c, s);
+    if (!(pHp > 0.0)) {
+      atomicCAS(&ctrl->status, kStatusOk, kStatusNotPd);
+      ctrl->fail_it = ctrl->it;
+    }
+    cs.alpha[c] = cs.rs[c] / pHp;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctrl->ticket = 0;
+    if (ctrl->status != kStatusOk) ctrl->done = 1;
+  }
+}
+
+__device__ void beta_epilogue(int s, ColState cs, const double* part, SolveCtrl* ctrl) {
+  for (int c = threadIdx.x; c < s; c += NT) {
+    if (cs.conv[c]) continue;
+    const double rs_new = total_of(part, c, s);
+    if (!isfinite(rs_new)) {
+      atomicCAS(&ctrl->status, kStatusOk, kStatusNaN);
+      ctrl->fail_it = ctrl->it;
+    }
+    if (sqrt(rs_new) <= cs.tol[c] * cs.bnorm[c]) {
+      cs.conv[c] = 2;
+      cs.beta[c] = 0.0;
+    } else {
+      cs.beta[c] = rs_new / cs.rs[c];
+    }
+    cs.rs[c] = rs_new;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctrl->ticket = 0;
+    if (ctrl->status != kStatusOk) ctrl->done = 1;
+  }
+}
+
+__global__ void cg_update_kernel(float* X, float* R, const float* P, const float* HP, int64_t ld,
+                                 int64_t n, int s, ColState cs, double* part, SolveCtrl* ctrl,
+                                 int refresh) {
+  if (ctrl->done) return;
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  for (int c = 0; c < s; ++c) {
+    double v = 0.0;
+    if (!cs.conv[c]) {
+      const float a = static_cast<float>(cs.alpha[c]);
+      for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
+        const int64_t e = i + c * ld;
+        X[e] = fmaf(a, P[e], X[e]);
+        if (!refresh) {
+          const float r = fmaf(-a, HP[e], R[e]);
+          R[e] = r;
+          v += static_cast<double>(r) * r;
+        }
+      }
+    }
+    if (!refresh) deposit(red, c, v);
+  }
+  if (refresh) return;
+  if (!publish(red, s, part, ctrl)) return;
+  beta_epilogue(s, cs, part, ctrl);
+}
+
+__global__ void cg_refresh_norm_kernel(float* R, const float* Rtmp, int64_t ld, int64_t n, int s,
+                                       ColState cs, double* part, SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  for (int c = 0; c < s; ++c) {
+    double v = 0.0;
+    if (!cs.conv[c])
+      for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
+        const int64_t e = i + c * ld;
+        const float r = Rtmp[e];
+        R[e] = r;
+        v += static_cast<double>(r) * r;
+      }
+    deposit(red, c, v);
+  }
+  if (!publish(red, s, part, ctrl)) return;
+  beta_epilogue(s, cs, part, ctrl);
+}
+
+__global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
+                                    ColState cs, double* part, SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  ROWS_OF_BLOCK
+  for (int c = 0; c < s; ++c) {
+    const int st = cs.conv[c];
+    if (st == 1) continue;
+    const float b = static_cast<float>(cs.beta[c]);
+    for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
+      const int64_t e = i + c * ld;
+      P[e] = st == 2 ? 0.f : fmaf(b, P[e], R[e]);
+    }
+  }
+  __syncthreads();
+  __threadfence();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int c = threadIdx.x; c < s; c += NT)
+    if (cs.conv[c] == 2) cs.conv[c] = 1;
+  loop_check(s, cs, ctrl, true);
+}
+
+__global__ void norms_convergence_kernel(const float* R, int64_t ld, int64_t n, int s, ColState cs,
+                                         double* part, SolveCtrl* ctrl, int check_nan,
+                                         int begin_next) {
+  if (begin_next && ctrl->done) return;
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  for (int c = 0; c < s; ++c) {
+    double v = 0.0;
+    for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
+      const double r = R[i + c * ld];
+      v += r * r;
+    }
+    deposit(red, c, v);
+  }
+  if (!publish(red, s, part, ctrl)) return;
+  for (int c = threadIdx.x; c < s; c += NT) {
+    const double t = total_of(part, c, s);
+    if (check_nan && !isfinite(t)) {
+      atomicCAS(&ctrl->status, kStatusOk, kStatusNaN);
+      ctrl->fail_it = ctrl->it;
+    }
+    cs.rs[c] = t;
+    cs.conv[c] = (cs.bnorm[c] == 0.0 || sqrt(t) <= cs.tol[c] * cs.bnorm[c]) ? 1 : 0;
+  }
+  loop_check(s, cs, ctrl, begin_next != 0);
+}
+
+__global__ void ap_gather_kernel(const float* R, int64_t ld, int64_t start, int64_t b, int s,
+                                 double* Rb, const SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i < b) Rb[i + c * b] = R[start + i + c * ld];
+}
+
+__global__ void ap_apply_kernel(float* X, int64_t ld, int64_t start, int64_t b, int s,
+                                const double* delta, float* d32, const SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= b) return;
+  const double dv = delta[i + c * b];
+  X[start + i + c * ld] = static_cast<float>(static_cast<double>(X[start + i + c * ld]) + dv);
+  d32[i + c * b] = static_cast<float>(dv);
+}
+
+__global__ void build_block_kernel(const float* xs, int dp, int64_t start, int64_t b, double sf2,
+                                   double a, double noise2, double* out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= b * b) return;
+  const int64_t i = e % b, j = e / b;
+  const float* xa = xs + (start + i) * dp;
+  const float* xb = xs + (start + j) * dp;
+  double r2 = 0.0;
+  for (int k = 0; k < dp; ++k) {
+    const double df = static_cast<double>(xa[k]) - static_cast<double>(xb[k]);
+    r2 += df * df;
+  }
+  const double u = sqrt(r2);
+  double v = (a * u + sf2) * exp2(-u);
+  if (i == j) v += noise2;
+  out[e] = v;
+}
+
+__global__ void sgd_scatter_kernel(float* X, float* R, float* vel, int64_t ld, const int* idx,
+                                   int64_t m, int s, const float* batch, float mu, float gs,
+                                   float ss, const SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= m) return;
+  const int64_t row = idx[i];
+  const int64_t e = row + c * ld;
+  const float br = batch[i + c * m];
+  const float v = mu * vel[e] - gs * br;
+  vel[e] = v;
+  X[e] -= ss * v;
+  R[e] = br;
+}
+
+__global__ void sgd_check_kernel(const float* X, const float* R, int64_t ld, int64_t n, int s,
+                                 ColState cs, double* part, SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  // columns 0..s-1: ||R_c||^2 ; column s: ||X||_F^2 (part has s+1 columns)
+  double xs = 0.0;
+  for (int c = 0; c < s; ++c) {
+    double v = 0.0;
+    for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
+      const double r = R[i + c * ld];
+      v += r * r;
+      const double x = X[i + c * ld];
+      xs += x * x;
+    }
+    deposit(red, c, v);
+  }
+  deposit(red, s, xs);
+  if (!publish(red, s + 1, part, ctrl)) return;
+  for (int c = threadIdx.x; c < s; c += NT) {
+    const double t = total_of(part, c, s + 1);
+    cs.conv[c] = (cs.bnorm[c] == 0.0 || sqrt(t) <= cs.tol[c] * cs.bnorm[c]) ? 1 : 0;
+  }
+  if (threadIdx.x == 0) {
+    const double xn = sqrt(total_of(part, s, s + 1));
+    if (!isfinite(xn) || xn > 1e12) {
+      ctrl->status = kStatusDiverged;
+      ctrl->fail_it = ctrl->it;
+    }
+  }
+  loop_check(s, cs, ctrl, true);
+}
+
+__global__ void fill_zero_kernel(float* A, int64_t ld, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) A[i + blockIdx.y * ld] = 0.f;
+}
+__global__ void sub_kernel(const float* A, const float* B, float* out, int64_t ld, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t e = i + blockIdx.y * ld;
+  if (i < n) out[e] = A[e] - B[e];
+}
+__global__ void copy_kernel(const float* A, int64_t lda, float* B, int64_t ldb, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) B[i + blockIdx.y * ldb] = A[i + blockIdx.y * lda];
+}
+
+inline dim3 grid2(int64_t n, int s) { return dim3(static_cast<unsigned>(ceil_div(n, NT)), s); }
+
+void check_s(int s) {
+  if (s < 1 || s >= SMAX) throw std::invalid_argument("solver kernels support 1 <= s < 256 columns");
+}
+
+}  // namespace
+
+void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, double* part,
+              unsigned* ticket, double* out, cudaStream_t st) {
+  check_s(s);
+  col_dots_kernel<<<reduce_blocks(n), NT, 0, st>>>(A, B, ld, n, s, part, ticket, out);
+  WGP_LAUNCH_CHECK();
+}
+
+void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
+             SolveCtrl* ctrl, cudaStream_t st) {
+  check_s(s);
+  cg_init_kernel<<<reduce_blocks(n), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
+  WGP_LAUNCH_CHECK();
+  cg_seed_direction_kernel<<<grid2(n, s), NT, 0, st>>>(P, R, ld, n, s, cs.conv);
+  WGP_LAUNCH_CHECK();
+}
+
+void cg_alpha(const float* P, const float* HP, int64_t ld, int64_t n, int s, ColState cs,
+              double* part, SolveCtrl* ctrl, cudaStream_t st) {
+  cg_alpha_kernel<<<reduce_blocks(n), NT, 0, st>>>(P, HP, ld, n, s, cs, part, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void cg_update(float* X, float* R, const float* P, const float* HP, int64_t ld, int64_t n, int s,
+               ColState cs, double* part, SolveCtrl* ctrl, bool refresh, cudaStream_t st) {
+  cg_update_kernel<<<reduce_blocks(n), NT, 0, st>>>(X, R, P, HP, ld, n, s, cs, part, ctrl,
+                                                    refresh ? 1 : 0);
+  WGP_LAUNCH_CHECK();
+}
+
+void cg_refresh_norm(float* R, const float* Rtmp, int64_t ld, int64_t n, int s, ColState cs,
+                     double* part, SolveCtrl* ctrl, cudaStream_t st) {
+  cg_refresh_norm_kernel<<<reduce_blocks(n), NT, 0, st>>>(R, Rtmp, ld, n, s, cs, part, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void cg_direction(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs,
+                  double* part, SolveCtrl* ctrl, cudaStream_t st) {
+  cg_direction_kernel<<<reduce_blocks(n), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void norms_convergence(const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
+                       SolveCtrl* ctrl, bool check_nan, bool begin_next, cudaStream_t st) {
+  check_s(s);
+  norms_convergence_kernel<<<reduce_blocks(n), NT, 0, st>>>(R, ld, n, s, cs, part, ctrl,
+                                                            check_nan ? 1 : 0, begin_next ? 1 : 0);
+  WGP_LAUNCH_CHECK();
+}
+
+void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, double* Rb,
+               const SolveCtrl* ctrl, cudaStream_t st) {
+  ap_gather_kernel<<<grid2(b, s), NT, 0, st>>>(R, ld, start, b, s, Rb, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
+              float* delta32, const SolveCtrl* ctrl, cudaStream_t st) {
+  ap_apply_kernel<<<grid2(b, s), NT, 0, st>>>(X, ld, start, b, s, delta, delta32, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void build_block(const float* xs, int dp, int64_t start, int64_t b, double sf2, double a,
+                 double noise2, double* out, cudaStream_t st) {
+  build_block_kernel<<<static_cast<unsigned>(ceil_div(b * b, NT)), NT, 0, st>>>(
+      xs, dp, start, b, sf2, a, noise2, out);
+  WGP_LAUNCH_CHECK();
+}
+
+void sgd_scatter(float* X, float* R, float* vel, int64_t ld, const int* idx, int64_t m, int s,
+                 const float* batch, float momentum, float grad_scale, float step_scale,
+                 const SolveCtrl* ctrl, cudaStream_t st) {
+  sgd_scatter_kernel<<<grid2(m, s), NT, 0, st>>>(X, R, vel, ld, idx, m, s, batch, momentum,
+                                                 grad_scale, step_scale, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void sgd_check(const float* X, const float* R, int64_t ld, int64_t n, int s, ColState cs,
+               double* part, SolveCtrl* ctrl, cudaStream_t st) {
+  check_s(s + 1);
+  sgd_check_kernel<<<reduce_blocks(n), NT, 0, st>>>(X, R, ld, n, s, cs, part, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void fill_zero(float* A, int64_t ld, int64_t n, int s, cudaStream_t st) {
+  fill_zero_kernel<<<grid2(n, s), NT, 0, st>>>(A, ld, n);
+  WGP_LAUNCH_CHECK();
+}
+void sub_into(const float* A, const float* B, float* out, int64_t ld, int64_t n, int s,
+              cudaStream_t st) {
+  sub_kernel<<<grid2(n, s), NT, 0, st>>>(A, B, out, ld, n);
+  WGP_LAUNCH_CHECK();
+}
+void copy_cols(const float* A, int64_t lda, float* B, int64_t ldb, int64_t n, int s,
+               cudaStream_t st) {
+  copy_kernel<<<grid2(n, s), NT, 0, st>>>(A, lda, B, ldb, n);
+  WGP_LAUNCH_CHECK();
+}
+
+}  // namespace wgp

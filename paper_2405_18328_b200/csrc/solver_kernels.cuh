@@ -1,0 +1,92 @@
+// solver_kernels.cuh — fused solver-vector kernels.
+//
+// Control state lives on the device so an iteration is a fixed launch
+// sequence with no host round trip; the host polls `SolveCtrl` every few
+// iterations.  All column reductions are two-phase (per-CTA fp64 partials,
+// then a fixed-order sum by the last CTA to finish) so results are bitwise
+// reproducible.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wgp {
+
+struct SolveCtrl {
+  int done;       // 1: the iteration loop has finished (or failed)
+  int it;         // iterations / epochs / steps performed
+  int status;     // kStatus*
+  int fail_it;    // iteration at which a failure was detected
+  int nconv;      // converged columns
+  int max_it;
+  unsigned ticket;
+  int pad;
+};
+
+enum : int { kStatusOk = 0, kStatusNotPd = 1, kStatusNaN = 2, kStatusDiverged = 3 };
+
+// Column state: 0 active, 1 converged (frozen), 2 converged in this iteration.
+struct ColState {
+  int* conv;
+  double* rs;      // CG: ||r||^2
+  double* alpha;   // CG
+  double* beta;    // CG
+  const double* bnorm;
+  const double* tol;
+};
+
+constexpr int kRowsPerBlock = 2048;
+inline int reduce_blocks(int64_t n) { return static_cast<int>((n + kRowsPerBlock - 1) / kRowsPerBlock); }
+
+// out[c] = sum_i A[i,c] * B[i,c]  (fp64, fixed order), all columns.
+void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, double* part,
+              unsigned* ticket, double* out, cudaStream_t st);
+
+// CG: before the loop.  R = rhs - H X0 must already be in R; computes
+// rs = ||r||^2, convergence, P = R (active) / 0, and the loop-entry check.
+void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
+             SolveCtrl* ctrl, cudaStream_t st);
+// alpha_c = rs_c / (p_c . hp_c); non-positive curvature -> kStatusNotPd.
+void cg_alpha(const float* P, const float* HP, int64_t ld, int64_t n, int s, ColState cs,
+              double* part, SolveCtrl* ctrl, cudaStream_t st);
+// x += alpha p; r -= alpha hp (refresh=false) or x += alpha p only (refresh=true).
+void cg_update(float* X, float* R, const float* P, const float* HP, int64_t ld, int64_t n, int s,
+               ColState cs, double* part, SolveCtrl* ctrl, bool refresh, cudaStream_t st);
+// refresh: r = rtmp for active columns; then ||r||^2, convergence, beta.
+void cg_refresh_norm(float* R, const float* Rtmp, int64_t ld, int64_t n, int s, ColState cs,
+                     double* part, SolveCtrl* ctrl, cudaStream_t st);
+// p = r + beta p (active) / 0 (just converged); then the next-iteration check.
+void cg_direction(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs,
+                  double* part, SolveCtrl* ctrl, cudaStream_t st);
+
+// Convergence from exact residual norms (AP epochs, SGD init): conv_c =
+// bnorm_c == 0 || ||R_c|| <= tol_c bnorm_c; NaN -> kStatusNaN (when check_nan);
+// then the loop check (all converged or it >= max_it -> done, else ++it).
+void norms_convergence(const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
+                       SolveCtrl* ctrl, bool check_nan, bool begin_next, cudaStream_t st);
+
+// AP block step helpers.
+void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, double* Rb,
+               const SolveCtrl* ctrl, cudaStream_t st);
+void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
+              float* delta32, const SolveCtrl* ctrl, cudaStream_t st);
+// H[b, b] in fp64 from the prepared points.
+void build_block(const float* xs, int dp, int64_t start, int64_t b, double sf2, double a,
+                 double noise2, double* out, cudaStream_t st);
+
+// SGD: vel/X/R row scatter (proj/src/solvers.cpp:247-252) then divergence and
+// convergence on the stored residual estimate (:254-258).
+void sgd_scatter(float* X, float* R, float* vel, int64_t ld, const int* idx, int64_t m, int s,
+                 const float* batch, float momentum, float grad_scale, float step_scale,
+                 const SolveCtrl* ctrl, cudaStream_t st);
+void sgd_check(const float* X, const float* R, int64_t ld, int64_t n, int s, ColState cs,
+               double* part, SolveCtrl* ctrl, cudaStream_t st);
+
+// Small helpers.
+void fill_zero(float* A, int64_t ld, int64_t n, int s, cudaStream_t st);
+void sub_into(const float* A, const float* B, float* out, int64_t ld, int64_t n, int s,
+              cudaStream_t st);  // out = A - B
+void copy_cols(const float* A, int64_t lda, float* B, int64_t ldb, int64_t n, int s,
+               cudaStream_t st);
+
+}  // namespace wgp
