@@ -98,6 +98,28 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, 
       " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
+// The three 3xTF32 partial products of one K step from a single asm block
+// (one elect): D (+)= A_hi B_hi + A_hi B_lo + A_lo B_hi.
+__device__ __forceinline__ void mma3_ss(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                        uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, t, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %6, 0;\n"
+      " setp.eq.u32 t, 0, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, t;\n}\n" ::"r"(d),
+      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma3_ts(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+                                        uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, t, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %6, 0;\n"
+      " setp.eq.u32 t, 0, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, t;\n}\n" ::"r"(d),
+      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
@@ -234,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.done && *p.done) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar_bfull[4], bar_bempty[4], bar_vfull[4], bar_vempty[4];
-  __shared__ __align__(8) uint64_t bar_a, bar_sfull[kBuf], bar_kfull[kBuf], bar_o;
+  __shared__ __align__(8) uint64_t bar_a, bar_sfull[kBuf], bar_kfull[kBuf], bar_kempty[kBuf], bar_o;
   __shared__ uint32_t tmem_slot;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -265,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kBuf; ++i) {
       mbar_init(&bar_sfull[i], 1);
       mbar_init(&bar_kfull[i], 4);
+      mbar_init(&bar_kempty[i], 1);
     }
     mbar_init(&bar_o, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -288,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // consumption order of the MMA issuer: B(0..2), then V(t), B(t+3)
       auto load_b = [&](int t) {
         const int st = t % NB;
-        if (t >= NB) mbar_wait(&bar_bempty[st], ((t / NB) - 1) & 1);
+        if (t >= NB && !(p.dbg & 64)) mbar_wait(&bar_bempty[st], ((t / NB) - 1) & 1);
         uint8_t* base = sB + static_cast<size_t>(st) * 16384;
         if (p.dbg & 32) {
           mbar_arrive_warp(&bar_bfull[st]);
@@ -301,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto load_v = [&](int t) {
         const int st = t % NV;
-        if (t >= NV) mbar_wait(&bar_vempty[st], ((t / NV) - 1) & 1);
+        if (t >= NV && !(p.dbg & 64)) mbar_wait(&bar_vempty[st], ((t / NV) - 1) & 1);
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const int vp = (jt_begin + t) * kTJ;
         if (p.dbg & 8) {
@@ -321,21 +344,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    // Issue order: MMA-1 for tiles 0..2, then for every t: [K(t) ready]
-    // MMA-2(t), MMA-1(t+3).  MMA-1(t+3) writes buffer t % 3 right after
-    // MMA-2(t) read it; tcgen05.mma from one thread executes in issue order,
-    // so the epilogue of tile t+3 (woken by the commit after MMA-1(t+3))
-    // starts while tiles t+1, t+2 are still in flight.  The whole warp runs
-    // this loop (uniform operands); elect.sync picks the issuing lane.
+    // ------------------------------------------------------------ MMA-1 issuer
+    // Two issuing warps: tcgen05.mma issue blocks while the tensor pipe is
+    // busy (queue depth ~1, measured), so one warp's barrier waits and
+    // commits would idle the pipe.  Warp 1 issues MMA-1 (Gram) and warp 3
+    // MMA-2 (K.V); each one's waits overlap the other's MMAs.  MMA-1(t)
+    // reuses buffer t % 3 only after MMA-2(t-3) has committed kempty.  The
+    // whole warp runs the loop (uniform operands); elect.sync picks the lane.
     if (T > 0) {
       constexpr uint32_t id1 = idesc_tf32(kTI, kTJ);
-      const uint32_t id2 = idesc_tf32(kTI, spad);
       mbar_wait(&bar_a, 0);
       tc_after();
       const uint64_t dAhi = umma_desc(sAhi), dAlo = umma_desc(sAlo);
-      auto mma1 = [&](int t) {
+      for (int t = 0; t < T; ++t) {
         const int st = t % NB, b = t % kBuf;
+        if (t >= kBuf) mbar_wait(&bar_kempty[b], ((t / kBuf) - 1) & 1);
         mbar_wait(&bar_bfull[st], (t / NB) & 1);
         tc_after();
         uint8_t* base = sB + static_cast<size_t>(st) * 16384;
@@ -343,17 +366,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t d = tmem + buf_col(b);
         if (!(p.dbg & 4)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) mma_ss(d, dAhi + 2 * k, dBhi + 2 * k, id1, k > 0);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) mma_ss(d, dAhi + 2 * k, dBlo + 2 * k, id1, 1);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) mma_ss(d, dAlo + 2 * k, dBhi + 2 * k, id1, 1);
+          for (int k = 0; k < 4; ++k)
+            mma3_ss(d, dAhi + 2 * k, dAlo + 2 * k, dBhi + 2 * k, dBlo + 2 * k, id1, k > 0);
         }
         mma_commit(&bar_sfull[b]);
         mma_commit(&bar_bempty[st]);
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 0] = clock64();
-      };
-      for (int t = 0; t < T && t < kBuf; ++t) mma1(t);
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ MMA-2 issuer
+    if (T > 0) {
+      const uint32_t id2 = idesc_tf32(kTI, spad);
+      const uint64_t box = vbox >> 4;
       for (int t = 0; t < T; ++t) {
         const int b = t % kBuf, st = t % NV;
         mbar_wait(&bar_vfull[st], (t / NV) & 1);
@@ -362,19 +387,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 3] = clock64();
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const uint32_t khi = tmem + buf_col(b), klo = khi + 64;
+        const uint64_t dv = umma_desc(base);
         if (!(p.dbg & 2)) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            const uint32_t off = static_cast<uint32_t>(k & 3) * 2;  // 32 bytes >> 4
-            const uint64_t vhi = umma_desc(base + (k >> 2) * vbox) + off;
-            const uint64_t vlo = umma_desc(base + (2 + (k >> 2)) * vbox) + off;
-            mma_ts(tmem, khi + 8 * k, vhi, id2, (t > 0 || k > 0) ? 1u : 0u);
-            mma_ts(tmem, khi + 8 * k, vlo, id2, 1);
-            mma_ts(tmem, klo + 8 * k, vhi, id2, 1);
+            const uint64_t off = static_cast<uint64_t>(k >> 2) * box + static_cast<uint64_t>(k & 3) * 2;
+            mma3_ts(tmem, khi + 8 * k, klo + 8 * k, dv + off, dv + 2 * box + off, id2,
+                    (t > 0 || k > 0) ? 1u : 0u);
           }
         }
         mma_commit(&bar_vempty[st]);
-        if (t + kBuf < T) mma1(t + kBuf);
+        mma_commit(&bar_kempty[b]);
       }
       mma_commit(&bar_o);
     }
