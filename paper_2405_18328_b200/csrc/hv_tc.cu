@@ -764,7 +764,8 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st) {
     WGP_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(long long) * 4 * (a.num_jt + 4), st));
   }
   const int64_t row_tiles = ceil_div(hp.m, kTI);
-  a.splits = choose_splits(row_tiles, a.num_jt, sm_count());
+  const int64_t key_tiles = hp.split_rows > 0 ? ceil_div(hp.split_rows, kTI) : row_tiles;
+  a.splits = choose_splits(key_tiles, a.num_jt, sm_count());
   static const int force_splits = [] {
     const char* e = getenv("WGP_TC_SPLITS");
     return e ? atoi(e) : 0;

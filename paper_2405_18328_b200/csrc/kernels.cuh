@@ -42,6 +42,9 @@ struct HvParams {
                          // (the streamed sum skips j == row so fp32 accumulation
                          // never carries the dominant diagonal term)
   const int* done;       // optional device flag: skip the launch body when *done != 0
+  int64_t split_rows;    // rows that key the J-split decomposition (0: m).  Row shards
+                         // pass the global row count so every shard sums in the same
+                         // order as the single-GPU launch (bitwise identical rows).
 };
 
 // SIMT fp32 fused H.V (direct differences; any d, s <= 128).

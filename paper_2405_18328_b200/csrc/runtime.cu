@@ -179,6 +179,7 @@ struct Ctx {
     p.noise2 = noise2();
     p.diag = static_cast<float>(sf * sf + sigma * sigma);
     p.done = done;
+    p.split_rows = row_idx ? 0 : n;  // shards of the full operator decompose like the whole
     if (hv_impl == WGP_HV_TC && hv_tc_supported(d, s)) {
       if (!tc.valid) tc.build(xs.as<float>(), n, dp, d, st);
       hv_tc(tc, p, st);

@@ -1,0 +1,141 @@
+"""Row-block sharded CG across ranks.
+
+Each rank owns a contiguous, 128-aligned block of rows I_g of the solutions,
+residuals and directions; X (and hence H) is available to every rank.  One CG
+iteration (proj/src/solvers.cpp:107-135) becomes:
+
+    all-gather P            (n x s; NCCL over NVLink on B200s)
+    HP[I_g] = H[I_g, :] P   (the rank's row block of the fused H.V:
+                             ``Context.set_rows`` + ``hv_device``)
+    per-column partial dots -> all-gather -> summed in rank order (fp64),
+    so every rank computes bitwise identical alpha / beta / convergence flags.
+
+The local product is injected (``local_hv``), so the same host logic runs
+with the CUDA kernels under NCCL and, in tests, with a host matrix under
+gloo.  Semantics (tolerances, refresh every 50 iterations, per-column freeze,
+error messages) follow ``cg_solve``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List
+
+import torch
+import torch.distributed as dist
+
+
+def row_range(n: int, rank: int, world: int, align: int = 128):
+    """Contiguous rows of `rank`: whole 128-row tiles, balanced across ranks."""
+    tiles = -(-n // align)
+    t0, t1 = tiles * rank // world, tiles * (rank + 1) // world
+    return min(n, t0 * align), min(n, t1 * align)
+
+
+@dataclass
+class ShardedSolveState:
+    solutions: torch.Tensor        # local rows x s
+    residuals: torch.Tensor        # local rows x s
+    per_column_relative_residual: List[float]
+    converged: List[bool]
+    iterations_used: int
+
+
+class NumericalError(RuntimeError):
+    pass
+
+
+def _gather_rows(local: torch.Tensor, n: int, world: int, group=None) -> torch.Tensor:
+    """All-gather row blocks (padded to the largest block) into an n x s tensor."""
+    if world == 1:
+        return local
+    m = torch.tensor([local.shape[0]], device=local.device)
+    sizes = [torch.zeros_like(m) for _ in range(world)]
+    dist.all_gather(sizes, m, group=group)
+    mx = int(max(s.item() for s in sizes))
+    pad = torch.zeros((mx, local.shape[1]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([b[: int(s.item())] for b, s in zip(bufs, sizes)], dim=0)[:n]
+
+
+def _sum_ranks(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """Deterministic all-reduce: gather fp64 partials, sum in rank order."""
+    x = x.to(torch.float64)
+    if world == 1:
+        return x
+    bufs = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(bufs, x, group=group)
+    out = torch.zeros_like(x)
+    for b in bufs:
+        out += b
+    return out
+
+
+def sharded_cg(local_hv: Callable[[torch.Tensor], torch.Tensor], B_local: torch.Tensor, n: int,
+               tol_mean: float = 0.01, tol_samples: float = 0.1, max_iterations: int = 0,
+               init_local: torch.Tensor | None = None, group=None) -> ShardedSolveState:
+    """cg_solve (proj/src/solvers.cpp:81-139) over row shards.
+
+    local_hv(V_full) must return H[I_g, :] @ V_full for this rank's rows.
+    """
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    s = B_local.shape[1]
+    dt = B_local.dtype
+    X = torch.zeros_like(B_local) if init_local is None else init_local.clone()
+    bn = torch.sqrt(_sum_ranks((B_local.double() ** 2).sum(0), world, group))
+    tols = torch.tensor([tol_mean] + [tol_samples] * (s - 1), dtype=torch.float64, device=bn.device)
+    if max_iterations <= 0:
+        max_iterations = 10 * n
+    R = B_local - local_hv(_gather_rows(X, n, world, group)) if init_local is not None else B_local.clone()
+    rs = _sum_ranks((R.double() ** 2).sum(0), world, group)
+    conv = (bn == 0) | (torch.sqrt(rs) <= tols * bn)
+    P = torch.where(conv[None, :], torch.zeros_like(R), R)
+    it = 0
+    while not bool(conv.all()) and it < max_iterations:
+        it += 1
+        HP = local_hv(_gather_rows(P, n, world, group))
+        pHp = _sum_ranks((P.double() * HP.double()).sum(0), world, group)
+        active = ~conv
+        if bool((pHp[active] <= 0).any()):
+            raise NumericalError("cg_solve: non-positive curvature encountered, H is not positive definite")
+        alpha = torch.where(active, rs / torch.where(active, pHp, torch.ones_like(pHp)), torch.zeros_like(rs))
+        X = X + alpha.to(dt)[None, :] * P
+        if it % 50 == 0:
+            R_new = B_local - local_hv(_gather_rows(X, n, world, group))
+            R = torch.where(active[None, :], R_new, R)
+        else:
+            R = R - alpha.to(dt)[None, :] * HP
+        rs_new = _sum_ranks((R.double() ** 2).sum(0), world, group)
+        if not bool(torch.isfinite(rs_new[active]).all()):
+            raise NumericalError(f"cg_solve: NaN in iterate at iteration {it}")
+        newly = active & (torch.sqrt(rs_new) <= tols * bn)
+        beta = torch.where(active, rs_new / torch.where(active, rs, torch.ones_like(rs)), torch.zeros_like(rs))
+        P = torch.where(newly[None, :] | conv[None, :], torch.zeros_like(P), R + beta.to(dt)[None, :] * P)
+        rs = torch.where(active, rs_new, rs)
+        conv = conv | newly
+    E = B_local - local_hv(_gather_rows(X, n, world, group))
+    en = torch.sqrt(_sum_ranks((E.double() ** 2).sum(0), world, group))
+    rel = torch.where(bn > 0, en / torch.where(bn > 0, bn, torch.ones_like(bn)), torch.zeros_like(bn))
+    return ShardedSolveState(X, R, rel.tolist(), conv.tolist(), it)
+
+
+def device_local_hv(ctx, r0: int, r1: int):
+    """local_hv backed by the fused CUDA H.V on this rank's rows (device tensors).
+
+    V_full: n x s (row-major torch view of a column-major buffer is taken by
+    transposing into a contiguous [s][n] tensor)."""
+    ctx.set_rows(r0, r1)
+    n = ctx.n
+
+    def f(V_full: torch.Tensor) -> torch.Tensor:
+        Vt = V_full.t().contiguous()                      # [s][n] = column-major n x s
+        out = torch.empty((Vt.shape[0], r1 - r0), device=Vt.device, dtype=Vt.dtype)
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        cur = torch.cuda.current_stream()
+        stream.wait_stream(cur)
+        ctx.hv_device(Vt.data_ptr(), n, Vt.shape[0], out.data_ptr(), r1 - r0)
+        cur.wait_stream(stream)
+        return out.t()
+
+    return f

@@ -265,3 +265,38 @@ def test_train_solver_failure_names_step(ctx):
                          solver=wg.SolverConfig(kind="sgd", learning_rate=1e9, max_iterations=1000))
     with pytest.raises(wg.NumericalError, match="step 1"):
         ctx.train(p.y, cfg)
+
+
+def test_row_shards_reassemble_bitwise(ctx):
+    """Row-block sharding: the per-rank row blocks of the fused
+    H.V concatenate to exactly the single-GPU result, for 2, 3 and 8 ranks."""
+    import torch
+    from paper_2405_18328_b200 import sharded
+
+    X, V, ls = make(5000, 9, 65, seed=31)
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, 1.0, 0.3])
+    full = ctx.hv(V)
+    Vd = torch.from_numpy(V).cuda()
+    for world in (2, 3, 8):
+        parts = []
+        for rank in range(world):
+            r0, r1 = sharded.row_range(5000, rank, world)
+            parts.append(sharded.device_local_hv(ctx, r0, r1)(Vd).cpu().numpy())
+        assert np.array_equal(np.concatenate(parts, axis=0), full)
+    ctx.set_rows(0, 5000)
+
+
+def test_sharded_cg_single_rank_on_device(ctx):
+    import torch
+    from paper_2405_18328_b200 import sharded
+
+    X, ls, sf, sig, rhs = kernel_problem(3000, 8, 5, seed=32)
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, sf, sig])
+    st = sharded.sharded_cg(sharded.device_local_hv(ctx, 0, 3000), torch.from_numpy(rhs).cuda(), 3000,
+                            tol_mean=0.01, tol_samples=0.05)
+    ref = ctx.solve(rhs, wg.SolverConfig(kind="cg", tol_mean=0.01, tol_samples=0.05))
+    assert all(st.converged)
+    assert abs(st.iterations_used - ref.iterations_used) <= max(1, 0.1 * ref.iterations_used)
+    assert np.all(np.array(st.per_column_relative_residual) <= np.array([0.01] + [0.05] * 4) * 1.05)
