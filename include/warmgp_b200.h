@@ -42,9 +42,11 @@ typedef struct wgp_ctx wgp_ctx;
 #define WGP_SOLVER_CG 0
 #define WGP_SOLVER_AP 1
 #define WGP_SOLVER_SGD 2
-/* H.V implementation: tcgen05 3xTF32 (default) or the SIMT fp32 kernel. */
+/* H.V implementation: tcgen05 with 3xTF32 K.V (default), the SIMT fp32
+ * kernel, or tcgen05 with bf16x3 K.V (faster, ~5e-6 instead of ~1e-6 relative). */
 #define WGP_HV_TC 0
 #define WGP_HV_SIMT 1
+#define WGP_HV_TC_BF16 2
 
 /** Thread-local message of the last failing call. */
 const char* wgp_last_error(void);

@@ -29,7 +29,8 @@ _LIB_NAME = "libwarmgp_b200.so"
 _lib = None
 
 WGP_OK, WGP_INVALID, WGP_NUMERICAL, WGP_DEVICE = 0, 2, 3, 4
-HV_TC, HV_SIMT = 0, 1
+HV_TC, HV_SIMT, HV_TC_BF16 = 0, 1, 2
+_HV_IMPLS = {"tc": HV_TC, "simt": HV_SIMT, "tc_bf16": HV_TC_BF16}
 _KINDS = {"cg": 0, "ap": 1, "sgd": 2}
 _MODES = {"warm": 0, "cold": 1, "cold-fixed": 2}
 _TRANSFORMS = {"softplus": 0, "log": 1}
@@ -368,7 +369,9 @@ class Context:
         return int(self._lib.wgp_stream(self._h) or 0)
 
     def set_hv_impl(self, impl: str):
-        _check(self._lib.wgp_set_hv_impl(self._h, HV_TC if impl == "tc" else HV_SIMT))
+        if impl not in _HV_IMPLS:
+            raise ValueError(f"unknown H.V implementation {impl!r}; one of {sorted(_HV_IMPLS)}")
+        _check(self._lib.wgp_set_hv_impl(self._h, _HV_IMPLS[impl]))
 
     def set_data(self, X):
         X = _f32(X)

@@ -42,6 +42,25 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return r;
 }
 
+// 2^x for x <= 0 on the FMA/ALU pipes (no MUFU): round-to-nearest split
+// x = n + f via the 1.5*2^23 magic constant (no F2I), degree-5 minimax
+// polynomial for 2^f on [-1/2, 1/2] (max rel. error 2.4e-7 in fp32 Horner,
+// the same order as ex2.approx), exponent add for 2^n.  Used for half the
+// entries of the tensor-core epilogue so the MUFU pipe stops binding (FA4).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const int n = __float_as_int(t) - 0x4B400000;
+  float p = 1.3276466634e-3f;
+  p = fmaf(p, f, 9.6755409613e-3f);
+  p = fmaf(p, f, 5.5507134646e-2f);
+  p = fmaf(p, f, 2.4022120237e-1f);
+  p = fmaf(p, f, 6.9314694405e-1f);
+  p = fmaf(p, f, 1.0000001192f);
+  return __int_as_float(__float_as_int(p) + (n << 23));
+}
+
 // Matern-3/2 value from u = sqrt(3) * log2(e) * r (the scaled distance the
 // kernels carry): k = sf^2 (1 + sqrt3 r) exp(-sqrt3 r) = (a u + sf^2) 2^-u,
 // a = sf^2 ln 2.  (proj/src/kernel.cpp:79-93, 130-134)

@@ -25,6 +25,7 @@
 // launch shape, partials summed in fixed order -> deterministic).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <mutex>
@@ -43,6 +44,7 @@ constexpr int kKA = 32;    // augmented Gram dimension (d + 2 <= 32)
 constexpr int kThreads = 512;  // 4 control warps + 3 epilogue warpgroups
 constexpr uint32_t kTfMask = 0xFFFFE000u;  // keep sign, exponent, 10 mantissa bits
 constexpr int kSmemLimit = 232448 - 2048;  // 227 KB opt-in minus static smem (barriers)
+constexpr int kMaxStages = 8;              // smem ring depth cap (barrier arrays)
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -194,23 +196,66 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
 
 // 32 squared scaled distances -> tf32 hi / lo planes of k; the diagonal
 // entry (dg in [0, 32)) is zeroed: H_ii V_i is applied exactly at the end.
+template <bool DIAG>
 __device__ __forceinline__ void to_k(const uint32_t (&r)[32], uint32_t (&khi)[32], uint32_t (&klo)[32],
-                                     float sf2, float ac, bool diag_tile, int64_t dg) {
+                                     float sf2, float ac, int dg) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    const float r2 = fmaxf(__uint_as_float(r[i]), 0.f);
-    const float k = matern_from_u(sqrt_approx(r2), sf2, ac);
+    const float k = matern_from_u(sqrt_approx(fabsf(__uint_as_float(r[i]))), sf2, ac);
     khi[i] = __float_as_uint(k) & kTfMask;
     klo[i] = __float_as_uint(k - __uint_as_float(khi[i]));
-  }
-  if (diag_tile) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (dg == i) {
-        khi[i] = 0u;
-        klo[i] = 0u;
-      }
+    if (DIAG && dg == i) {
+      khi[i] = 0u;
+      klo[i] = 0u;
     }
+  }
+}
+
+// bf16 x 3 MMA-2 (kind::f16, K = 16 per instruction): D (+)= k1 v1 + k1 v2 + k2 v1.
+__device__ __forceinline__ void mma3_ts_bf16(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+                                             uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, t, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %6, 0;\n"
+      " setp.eq.u32 t, 0, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n}\n" ::"r"(d),
+      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
+}
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// 32 squared distances -> 16 packed bf16x2 words of k1 = bf16(k) and of
+// k2 = bf16(k - k1) (lower K index in the low half), written at w[OFF..OFF+16).
+// 32 squared distances (one half of a tile) -> 32 packed bf16x2 words:
+// w[c] = k1 pair c = bf16(k), w[16 + c] = k2 pair c = bf16(k - k1) (lower K
+// index in the low half).  POLY evaluates 2^-u of the odd entries on the FMA
+// pipe (ex2_poly) instead of the MUFU.
+// The squared distance from the tensor core can be a tiny negative number
+// for (near-)duplicate points; sqrt(|u^2|) keeps it finite and folds the abs
+// into the MUFU operand (no separate clamp instruction).  DIAG is a separate
+// instantiation for the rare tiles that contain the diagonal, so the common
+// path carries no per-entry index compares.
+template <bool POLY, bool DIAG>
+__device__ __forceinline__ void to_k_bf16(const uint32_t (&r)[32], uint32_t (&w)[32], float sf2, float ac,
+                                          int dg) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    float ka = matern_from_u(sqrt_approx(fabsf(__uint_as_float(r[2 * c]))), sf2, ac);
+    const float ub = sqrt_approx(fabsf(__uint_as_float(r[2 * c + 1])));
+    float kb = POLY ? fmaf(ac, ub, sf2) * ex2_poly(-ub) : matern_from_u(ub, sf2, ac);
+    if (DIAG) {
+      if (dg == 2 * c) ka = 0.f;
+      if (dg == 2 * c + 1) kb = 0.f;
+    }
+    const __nv_bfloat162 h = __floats2bfloat162_rn(ka, kb);
+    const float2 hf = __bfloat1622float2(h);
+    const __nv_bfloat162 l = __floats2bfloat162_rn(ka - hf.x, kb - hf.y);
+    w[c] = *reinterpret_cast<const uint32_t*>(&h);
+    w[16 + c] = *reinterpret_cast<const uint32_t*>(&l);
   }
 }
 
@@ -222,7 +267,7 @@ struct TcArgs {
   int splits;
   int s, s_pad;
   int nb, nv;              // B-ring and V-ring stages
-  uint32_t vstage_bytes;   // 4 V boxes (hi/lo x two 32-point halves)
+  uint32_t vstage_bytes;   // V boxes of one tile (tf32: 4 x 32 points, bf16: 2 x 64 points)
   const int* row_idx;
   int64_t r0;
   const float* V;
@@ -238,31 +283,52 @@ struct TcArgs {
   const int* done;
   long long* trace;  // WGP_TC_TRACE: per-tile clock64 stamps of CTA 0 ([T][4])
   int dbg;  // ablation bits (WGP_TC_DEBUG): 1 no epilogue math, 2 no MMA-2, 4 no MMA-1, 8 no V loads,
-            // 16 no epilogue TMEM traffic, 32 no B loads
+            // 16 no epilogue TMEM traffic, 32 no B loads, 128 bf16: FMA-pipe ex2 for odd entries
 };
 
-// TMEM: O accumulator in columns [0, 128); three tile buffers of 128 columns
-// at 128 + 128 b.  Buffer layout: [0, 64) holds S (MMA-1 output) and is
-// overwritten in place by k_hi once the epilogue has read it; [64, 128)
-// holds k_lo.
-constexpr int kBuf = 3;
-constexpr uint32_t buf_col(int b) { return 128u + 128u * static_cast<uint32_t>(b); }
+// TMEM: O accumulator in columns [0, 128); tile buffers from column 128.
+//   tf32 x 3 (BF = false): 3 buffers x 128 columns; S in [0, 64) is overwritten
+//     in place by k_hi once read, k_lo in [64, 128).
+//   bf16 x 3 (BF = true): 6 buffers x 64 columns; S in [0, 64) is overwritten by
+//     the packed k1 (32 columns) and k2 (32 columns).
+template <bool BF>
+struct Layout {
+  // bf16: O [0, 96), A_I hi/lo [96, 160) (MMA-1 reads A from TMEM: with A in
+  // shared memory MMA-1 is smem-bandwidth bound at 48 clk/MMA, measured), five
+  // 64-column buffers from 160.  tf32: O [0, 128), three 128-column buffers.
+  static constexpr int kBufs = BF ? 5 : 3;
+  static constexpr uint32_t kWidth = BF ? 64u : 128u;
+  static constexpr uint32_t kFirst = BF ? 160u : 128u;
+  static constexpr uint32_t kAhi = 96u, kAlo = 128u;
+  static __device__ __forceinline__ uint32_t col(int b) { return kFirst + kWidth * static_cast<uint32_t>(b); }
+};
+constexpr int kEpiGroups = 3;
+// Warp roles.  The warp scheduler prefers the highest warp id among eligible
+// warps, so the latency-critical control warps get the top ids and the 12
+// always-eligible epilogue warps (0..11; warp w reads TMEM lanes 32 (w % 4))
+// cannot starve them.
+constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kWarpBProd = 12, kWarpM1 = 13, kWarpVProd = 14, kWarpM2 = 15;
 
+template <bool BF>
 __global__ void __launch_bounds__(kThreads, 1)
     hv_tc_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                  const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                  const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
                  const TcArgs p) {
+  using L = Layout<BF>;
+  constexpr int NBUF = L::kBufs;
   if (p.done && *p.done) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bar_bfull[4], bar_bempty[4], bar_vfull[4], bar_vempty[4];
-  __shared__ __align__(8) uint64_t bar_a, bar_sfull[kBuf], bar_kfull[kBuf], bar_kempty[kBuf], bar_o;
+  __shared__ __align__(8) uint64_t bar_bfull[kMaxStages], bar_bempty[kMaxStages], bar_vfull[kMaxStages],
+      bar_vempty[kMaxStages];
+  __shared__ __align__(8) uint64_t bar_a, bar_atm, bar_sfull[NBUF], bar_kfull[NBUF], bar_kempty[NBUF], bar_o;
   __shared__ uint32_t tmem_slot;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAhi = smem;
   uint8_t* sAlo = smem + 16384;
-  uint8_t* sB = smem + 32768;                   // nb x [B_hi 8K | B_lo 8K]
+  uint8_t* sB = smem + 32768;                            // nb x [B_hi 8K | B_lo 8K]
   uint8_t* sV = sB + static_cast<size_t>(p.nb) * 16384;  // nv x vstage
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -272,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int T = jt_end - jt_begin;
   const int NB = p.nb, NV = p.nv;
   const int spad = p.s_pad;
-  const uint32_t vbox = static_cast<uint32_t>(spad) * 128u;  // one 32-point V box
+  const uint32_t vbox = static_cast<uint32_t>(spad) * 128u;  // one V box (128-byte rows)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) {
@@ -284,7 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_vempty[i], 1);
     }
     mbar_init(&bar_a, 1);
-    for (int i = 0; i < kBuf; ++i) {
+    mbar_init(&bar_atm, 4);
+    for (int i = 0; i < NBUF; ++i) {
       mbar_init(&bar_sfull[i], 1);
       mbar_init(&bar_kfull[i], 4);
       mbar_init(&bar_kempty[i], 1);
@@ -292,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bar_o, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == kWarpVProd) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -301,99 +368,123 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_after();
   const uint32_t tmem = tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp == kWarpBProd) {
+    // ------------------------------------------------------------ TMA producer: A, B ring
     if (T > 0) {  // whole warp, one elected lane issues
       const int arow = p.a_row0 + rt * kTI;
       mbar_expect_tx_warp(&bar_a, 2 * 16384);
       tma_load_2d_warp(sAhi, &mAhi, &bar_a, 0, arow);
       tma_load_2d_warp(sAlo, &mAlo, &bar_a, 0, arow);
-      // consumption order of the MMA issuer: B(0..2), then V(t), B(t+3)
-      auto load_b = [&](int t) {
+      for (int t = 0; t < T; ++t) {
         const int st = t % NB;
-        if (t >= NB && !(p.dbg & 64)) mbar_wait(&bar_bempty[st], ((t / NB) - 1) & 1);
+        if (t >= NB) mbar_wait(&bar_bempty[st], ((t / NB) - 1) & 1);
         uint8_t* base = sB + static_cast<size_t>(st) * 16384;
         if (p.dbg & 32) {
           mbar_arrive_warp(&bar_bfull[st]);
-          return;
+          continue;
         }
         mbar_expect_tx_warp(&bar_bfull[st], 16384u);
         const int pt = static_cast<int>(p.j0) + (jt_begin + t) * kTJ;
         tma_load_2d_warp(base, &mBhi, &bar_bfull[st], 0, pt);
         tma_load_2d_warp(base + 8192, &mBlo, &bar_bfull[st], 0, pt);
-      };
-      auto load_v = [&](int t) {
+      }
+    }
+  } else if (warp == kWarpVProd) {
+    // ------------------------------------------------------------ TMA producer: V ring
+    // (separate warp so the two rings never block each other)
+    if (T > 0) {
+      for (int t = 0; t < T; ++t) {
         const int st = t % NV;
-        if (t >= NV && !(p.dbg & 64)) mbar_wait(&bar_vempty[st], ((t / NV) - 1) & 1);
+        if (t >= NV) mbar_wait(&bar_vempty[st], ((t / NV) - 1) & 1);
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const int vp = (jt_begin + t) * kTJ;
         if (p.dbg & 8) {
           mbar_arrive_warp(&bar_vfull[st]);
-          return;
+          continue;
         }
         mbar_expect_tx_warp(&bar_vfull[st], p.vstage_bytes);
-        tma_load_2d_warp(base, &mVhi, &bar_vfull[st], vp, 0);
-        tma_load_2d_warp(base + vbox, &mVhi, &bar_vfull[st], vp + 32, 0);
-        tma_load_2d_warp(base + 2 * vbox, &mVlo, &bar_vfull[st], vp, 0);
-        tma_load_2d_warp(base + 3 * vbox, &mVlo, &bar_vfull[st], vp + 32, 0);
-      };
-      for (int t = 0; t < T && t < kBuf; ++t) load_b(t);
-      for (int t = 0; t < T; ++t) {
-        load_v(t);
-        if (t + kBuf < T) load_b(t + kBuf);
+        if constexpr (BF) {  // one 64-point box per plane
+          tma_load_2d_warp(base, &mVhi, &bar_vfull[st], vp, 0);
+          tma_load_2d_warp(base + vbox, &mVlo, &bar_vfull[st], vp, 0);
+        } else {  // two 32-point boxes per plane
+          tma_load_2d_warp(base, &mVhi, &bar_vfull[st], vp, 0);
+          tma_load_2d_warp(base + vbox, &mVhi, &bar_vfull[st], vp + 32, 0);
+          tma_load_2d_warp(base + 2 * vbox, &mVlo, &bar_vfull[st], vp, 0);
+          tma_load_2d_warp(base + 3 * vbox, &mVlo, &bar_vfull[st], vp + 32, 0);
+        }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kWarpM1) {
     // ------------------------------------------------------------ MMA-1 issuer
     // Two issuing warps: tcgen05.mma issue blocks while the tensor pipe is
     // busy (queue depth ~1, measured), so one warp's barrier waits and
     // commits would idle the pipe.  Warp 1 issues MMA-1 (Gram) and warp 3
     // MMA-2 (K.V); each one's waits overlap the other's MMAs.  MMA-1(t)
-    // reuses buffer t % 3 only after MMA-2(t-3) has committed kempty.  The
-    // whole warp runs the loop (uniform operands); elect.sync picks the lane.
+    // reuses buffer t % NBUF only after MMA-2(t - NBUF) has committed kempty.
+    // The whole warp runs the loop (uniform operands); elect.sync picks the lane.
     if (T > 0) {
       constexpr uint32_t id1 = idesc_tf32(kTI, kTJ);
-      mbar_wait(&bar_a, 0);
+      if constexpr (BF) {
+        mbar_wait(&bar_atm, 0);  // A_I copied into TMEM by epilogue group 0
+      } else {
+        mbar_wait(&bar_a, 0);
+      }
       tc_after();
       const uint64_t dAhi = umma_desc(sAhi), dAlo = umma_desc(sAlo);
       for (int t = 0; t < T; ++t) {
-        const int st = t % NB, b = t % kBuf;
-        if (t >= kBuf) mbar_wait(&bar_kempty[b], ((t / kBuf) - 1) & 1);
+        const int st = t % NB, b = t % NBUF;
+        if (t >= NBUF) mbar_wait(&bar_kempty[b], ((t / NBUF) - 1) & 1);
         mbar_wait(&bar_bfull[st], (t / NB) & 1);
         tc_after();
         uint8_t* base = sB + static_cast<size_t>(st) * 16384;
         const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + 8192);
-        const uint32_t d = tmem + buf_col(b);
+        const uint32_t d = tmem + L::col(b);
         if (!(p.dbg & 4)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma3_ss(d, dAhi + 2 * k, dAlo + 2 * k, dBhi + 2 * k, dBlo + 2 * k, id1, k > 0);
+          for (int k = 0; k < 4; ++k) {
+            if constexpr (BF)
+              mma3_ts(d, tmem + L::kAhi + 8 * k, tmem + L::kAlo + 8 * k, dBhi + 2 * k, dBlo + 2 * k, id1,
+                      k > 0);
+            else
+              mma3_ss(d, dAhi + 2 * k, dAlo + 2 * k, dBhi + 2 * k, dBlo + 2 * k, id1, k > 0);
+          }
         }
         mma_commit(&bar_sfull[b]);
         mma_commit(&bar_bempty[st]);
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 0] = clock64();
       }
     }
-  } else if (warp == 3) {
+  } else if (warp == kWarpM2) {
     // ------------------------------------------------------------ MMA-2 issuer
     if (T > 0) {
-      const uint32_t id2 = idesc_tf32(kTI, spad);
+      const uint32_t id2 = BF ? idesc_bf16(kTI, spad) : idesc_tf32(kTI, spad);
       const uint64_t box = vbox >> 4;
       for (int t = 0; t < T; ++t) {
-        const int b = t % kBuf, st = t % NV;
+        const int b = t % NBUF, st = t % NV;
         mbar_wait(&bar_vfull[st], (t / NV) & 1);
-        mbar_wait(&bar_kfull[b], (t / kBuf) & 1);
+        mbar_wait(&bar_kfull[b], (t / NBUF) & 1);
         tc_after();
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 3] = clock64();
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
-        const uint32_t khi = tmem + buf_col(b), klo = khi + 64;
+        const uint32_t kb = tmem + L::col(b);
         const uint64_t dv = umma_desc(base);
         if (!(p.dbg & 2)) {
+          if constexpr (BF) {
+            // per 32-point half h: k1 in columns [32h, 32h+16), k2 in
+            // [32h+16, 32h+32); a 16-point K step is 8 columns
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint64_t off = static_cast<uint64_t>(k >> 2) * box + static_cast<uint64_t>(k & 3) * 2;
-            mma3_ts(tmem, khi + 8 * k, klo + 8 * k, dv + off, dv + 2 * box + off, id2,
-                    (t > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t c1 = 32u * (k >> 1) + 8u * (k & 1);
+              mma3_ts_bf16(tmem, kb + c1, kb + c1 + 16, dv + 2 * k, dv + box + 2 * k, id2,
+                           (t > 0 || k > 0) ? 1u : 0u);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const uint64_t off = static_cast<uint64_t>(k >> 2) * box + static_cast<uint64_t>(k & 3) * 2;
+              mma3_ts(tmem, kb + 8 * k, kb + 64 + 8 * k, dv + off, dv + 2 * box + off, id2,
+                      (t > 0 || k > 0) ? 1u : 0u);
+            }
           }
         }
         mma_commit(&bar_vempty[st]);
@@ -401,11 +492,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_commit(&bar_o);
     }
-  } else if (warp >= 4) {
+  } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    // Warpgroup w owns buffer w and tiles t = w, w+3, ...; warp w%4 of the
-    // group reads TMEM lanes 32 (w%4) .. +31 (= its 32 output rows).
-    const int ew = warp - 4, q = ew & 3, w = ew >> 2;
+    // Warpgroup w handles tiles t = w, w+3, ... (buffer t % NBUF); warp w%4
+    // of the group reads TMEM lanes 32 (w%4) .. +31 (= its 32 output rows).
+    const int ew = warp, q = ew & 3, w = ew >> 2;
     const int row = q * 32 + lane;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
     const int64_t lr = static_cast<int64_t>(rt) * kTI + row;
@@ -413,43 +504,99 @@ __global__ void __launch_bounds__(kThreads, 1)
     int64_t g = -1;
     if (valid) g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
     const float sf2 = p.sf2, ac = p.a;
-    const uint32_t bcol = buf_col(w);
     const bool nomath = p.dbg & 1;
-    for (int t = w; t < T; t += kBuf) {
+    if (BF && w == 0 && T > 0) {
+      // Copy this row of A_I (hi, lo: 32 fp32 each) from the 128B-swizzled
+      // TMA tile into TMEM columns [96, 160): MMA-1 then reads A from TMEM.
+      mbar_wait(&bar_a, 0);
+      uint32_t ah[32], al[32];
+      const uint8_t* rh = sAhi + (row >> 3) * 1024 + (row & 7) * 128;
+      const uint8_t* rl = sAlo + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int pc = (c ^ (row & 7)) * 16;
+        const uint4 vh = *reinterpret_cast<const uint4*>(rh + pc);
+        const uint4 vl = *reinterpret_cast<const uint4*>(rl + pc);
+        ah[4 * c] = vh.x, ah[4 * c + 1] = vh.y, ah[4 * c + 2] = vh.z, ah[4 * c + 3] = vh.w;
+        al[4 * c] = vl.x, al[4 * c + 1] = vl.y, al[4 * c + 2] = vl.z, al[4 * c + 3] = vl.w;
+      }
+      __syncwarp();
+      tmem_st32(tmem + lanes + Layout<BF>::kAhi, ah);
+      tmem_st32(tmem + lanes + Layout<BF>::kAlo, al);
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_atm);
+    }
+    for (int t = w; t < T; t += kEpiGroups) {
+      const int b = t % NBUF;
+      const uint32_t bcol = L::col(b);
       const int64_t tstart = p.j0 + static_cast<int64_t>(jt_begin + t) * kTJ;
       const int64_t dg = valid ? g - tstart : -1;
       const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < kTJ);
-      mbar_wait(&bar_sfull[w], (t / kBuf) & 1);
+      mbar_wait(&bar_sfull[b], (t / NBUF) & 1);
       tc_after();
       if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 4 + 1] = clock64();
-#pragma unroll 1
-      for (int half = 0; half < ((p.dbg & 16) ? 0 : 2); ++half) {
-        uint32_t r[32], khi[32], klo[32];
-        __syncwarp();
-        tmem_ld32(tmem + lanes + bcol + 32 * half, r);
-        tmem_wait_ld();
-        if (nomath) {
+      const int dgi = static_cast<int>(dg < 0 || dg >= kTJ ? -1 : dg);
+      if constexpr (BF) {
+        if (!(p.dbg & 16)) {
+          // both 32-column halves of S are read first; each half is then
+          // overwritten in place by [k1 pairs (16 cols) | k2 pairs (16 cols)]
+          uint32_t r0[32], r1[32], wds[32];
+          __syncwarp();
+          tmem_ld32(tmem + lanes + bcol, r0);
+          tmem_ld32(tmem + lanes + bcol + 32, r1);
+          tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) khi[i] = r[i], klo[i] = 0u;
-        } else {
-          to_k(r, khi, klo, sf2, ac, diag_tile, dg - 32 * half);
+          for (int half = 0; half < 2; ++half) {
+            const uint32_t(&r)[32] = half ? r1 : r0;
+            const int dh = dgi - 32 * half;
+            if (nomath) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) wds[i] = r[i];
+            } else if (diag_tile) {
+              to_k_bf16<false, true>(r, wds, sf2, ac, dh);
+            } else if (p.dbg & 128) {
+              to_k_bf16<true, false>(r, wds, sf2, ac, dh);
+            } else {
+              to_k_bf16<false, false>(r, wds, sf2, ac, dh);
+            }
+            __syncwarp();
+            tmem_st32(tmem + lanes + bcol + 32 * half, wds);
+          }
         }
-        __syncwarp();
-        // k_hi overwrites the S columns just read; k_lo goes to [64, 128)
-        tmem_st32(tmem + lanes + bcol + 32 * half, khi);
-        tmem_st32(tmem + lanes + bcol + 64 + 32 * half, klo);
+      } else {
+#pragma unroll 1
+        for (int half = 0; half < ((p.dbg & 16) ? 0 : 2); ++half) {
+          uint32_t r[32], khi[32], klo[32];
+          __syncwarp();
+          tmem_ld32(tmem + lanes + bcol + 32 * half, r);
+          tmem_wait_ld();
+          if (nomath) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) khi[i] = r[i], klo[i] = 0u;
+          } else if (diag_tile) {
+            to_k<true>(r, khi, klo, sf2, ac, dgi - 32 * half);
+          } else {
+            to_k<false>(r, khi, klo, sf2, ac, dgi - 32 * half);
+          }
+          __syncwarp();
+          // k_hi overwrites the S columns just read; k_lo goes to [64, 128)
+          tmem_st32(tmem + lanes + bcol + 32 * half, khi);
+          tmem_st32(tmem + lanes + bcol + 64 + 32 * half, klo);
+        }
       }
       tmem_wait_st();
       tc_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_kfull[w]);
+      if (lane == 0) mbar_arrive(&bar_kfull[b]);
       if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 4 + 2] = clock64();
     }
     if (T > 0) {
       mbar_wait(&bar_o, 0);
       tc_after();
       const bool diag = g >= p.j0 && g < p.j1;
-      for (int c8 = 8 * w; c8 < spad; c8 += 8 * kBuf) {
+      for (int c8 = 8 * w; c8 < spad; c8 += 8 * kEpiGroups) {
         uint32_t o[8];
         __syncwarp();
         tmem_ld8(tmem + lanes + c8, o);
@@ -479,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_before();
   __syncthreads();
   tc_after();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == kWarpVProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // Sum of split partials in fixed order + the same epilogue as the kernel.
@@ -511,6 +658,18 @@ __global__ void split_v_kernel(const float* V, int64_t ldv, int64_t j0, int64_t 
   const float vh = __uint_as_float(__float_as_uint(v) & kTfMask);
   hi[c * ldw + j] = vh;
   lo[c * ldw + j] = v - vh;
+}
+
+// V[j0:j1, :s] -> bf16 planes v1 = bf16(v), v2 = bf16(v - v1) [s][ldw].
+__global__ void split_v_bf16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, __nv_bfloat16* v1,
+                                    __nv_bfloat16* v2, int64_t ldw) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (j >= nv) return;
+  const float v = V[j0 + j + c * ldv];
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  v1[c * ldw + j] = h;
+  v2[c * ldw + j] = __float2bfloat16_rn(v - __bfloat162float(h));
 }
 
 // Augmented operand rows from the prepared points (see TcOperands).
@@ -580,13 +739,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
-                     uint32_t box_out) {
+                     uint32_t box_out, CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_bytes};
   cuuint32_t box[2] = {box_in, box_out};
   cuuint32_t es[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+  const CUresult r = encode_fn()(&m, dtype, 2, const_cast<void*>(base), dims, strides,
                                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
@@ -673,7 +832,20 @@ void TcOperands::build(const float* xs, int64_t n_, int dp, int d_, cudaStream_t
 
 bool hv_tc_supported(int d, int s) { return d + 2 <= kKA && s >= 1 && s <= 128; }
 
-void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st) {
+template <bool BF>
+void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorMap& mBhi, const CUtensorMap& mBlo,
+               const CUtensorMap& mVhi, const CUtensorMap& mVlo, const TcArgs& a, unsigned grid, int smem,
+               cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    WGP_CUDA(cudaFuncSetAttribute(hv_tc_kernel<BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+    configured = true;
+  }
+  hv_tc_kernel<BF><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a);
+  WGP_LAUNCH_CHECK();
+}
+
+void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   if (hp.s > 96) {  // the V ring holds at most 96 columns: balanced column chunks
     const int chunks = static_cast<int>(ceil_div(hp.s, 96));
     for (int c = 0; c < chunks; ++c) {
@@ -683,7 +855,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st) {
       q.V = hp.V + c0 * hp.ldv;
       q.out = hp.out + c0 * hp.ldo;
       if (hp.B) q.B = hp.B + c0 * hp.ldb;
-      hv_tc(ops, q, st);
+      hv_tc(ops, q, st, bf16);
     }
     return;
   }
@@ -695,12 +867,18 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st) {
   const int s = hp.s;
   const int spad = static_cast<int>(round_up(s, 16));
   const int64_t nv = hp.j1 - hp.j0;
-  const int64_t ldw = round_up(nv, 4);
-  // tf32 planes of V[j0:j1]
-  float* vhi = static_cast<float*>(ws_v.ensure(sizeof(float) * ldw * s * 2));
-  float* vlo = vhi + ldw * s;
-  split_v_kernel<<<dim3(static_cast<unsigned>(ceil_div(nv, 256)), s), 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, vhi,
-                                                                                    vlo, ldw);
+  const int64_t ldw = round_up(nv, 8);
+  // hi / lo planes of V[j0:j1]: tf32 (fp32 storage) or bf16
+  const size_t esz = bf16 ? 2 : 4;
+  char* vhi = static_cast<char*>(ws_v.ensure(esz * ldw * s * 2));
+  char* vlo = vhi + esz * ldw * s;
+  const dim3 vgrid(static_cast<unsigned>(ceil_div(nv, 256)), s);
+  if (bf16)
+    split_v_bf16_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<__nv_bfloat16*>(vhi),
+                                               reinterpret_cast<__nv_bfloat16*>(vlo), ldw);
+  else
+    split_v_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<float*>(vhi),
+                                          reinterpret_cast<float*>(vlo), ldw);
   WGP_LAUNCH_CHECK();
   // A rows: the operand planes directly (row range) or a gathered copy
   const float* ahi = static_cast<const float*>(ops.a_hi);
@@ -722,8 +900,10 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st) {
   const CUtensorMap mAlo = make_map(alo, kKA, a_rows, kKA * 4, kKA, kTI);
   const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, kTJ);
   const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, kTJ);
-  const CUtensorMap mVhi = make_map(vhi, nv, s, ldw * 4, 32, spad);
-  const CUtensorMap mVlo = make_map(vlo, nv, s, ldw * 4, 32, spad);
+  const CUtensorMapDataType vt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const uint32_t vbox_pts = bf16 ? 64 : 32;  // 128-byte box rows
+  const CUtensorMap mVhi = make_map(vhi, nv, s, ldw * esz, vbox_pts, spad, vt);
+  const CUtensorMap mVlo = make_map(vlo, nv, s, ldw * esz, vbox_pts, spad, vt);
 
   TcArgs a{};
   a.m = hp.m;
@@ -733,10 +913,22 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st) {
   a.num_jt = static_cast<int>(ceil_div(nv, kTJ));
   a.s = s;
   a.s_pad = spad;
-  a.nb = 4;
-  a.vstage_bytes = 4u * static_cast<uint32_t>(spad) * 128u;
-  a.nv = std::min<int>(3, (kSmemLimit - 32768 - 1024 - a.nb * 16384) / static_cast<int>(a.vstage_bytes));
-  if (a.nv < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
+  // Ring depths: V tiles are consumed by MMA-2 and must be prefetched far
+  // enough ahead to cover the L2->SMEM latency (measured: 3 stages starve
+  // MMA-2); the B ring only feeds MMA-1, which runs ahead anyway.
+  static const int env_nb = [] {
+    const char* e = getenv("WGP_TC_NB");
+    return e ? atoi(e) : 0;
+  }();
+  static const int env_nv = [] {
+    const char* e = getenv("WGP_TC_NV");
+    return e ? atoi(e) : 0;
+  }();
+  a.vstage_bytes = (bf16 ? 2u : 4u) * static_cast<uint32_t>(spad) * 128u;
+  a.nb = env_nb > 0 ? std::min(env_nb, kMaxStages) : (bf16 ? 4 : 2);
+  a.nv = std::min<int>(kMaxStages, (kSmemLimit - 32768 - 1024 - a.nb * 16384) / static_cast<int>(a.vstage_bytes));
+  if (env_nv > 0) a.nv = std::min(a.nv, env_nv);
+  if (a.nv < 2 || a.nb < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
   a.row_idx = hp.row_idx;
   a.r0 = hp.r0;
   a.V = hp.V;
@@ -773,32 +965,35 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st) {
   if (force_splits > 0) a.splits = std::min(force_splits, a.num_jt);
   if (a.splits > 1) a.part = static_cast<float*>(ws_part.ensure(sizeof(float) * a.splits * spad * m_pad));
   const int smem = 32768 + 1024 + a.nb * 16384 + a.nv * static_cast<int>(a.vstage_bytes);
-  static bool configured = false;
-  if (!configured) {
-    WGP_CUDA(cudaFuncSetAttribute(hv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-    configured = true;
-  }
-  hv_tc_kernel<<<static_cast<unsigned>(row_tiles * a.splits), kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo,
-                                                                                   mVhi, mVlo, a);
-  WGP_LAUNCH_CHECK();
+  const unsigned grid = static_cast<unsigned>(row_tiles * a.splits);
+  if (bf16)
+    launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a, grid, smem, st);
+  else
+    launch_tc<false>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a, grid, smem, st);
   if (tracing) {
     const int T0 = static_cast<int>(static_cast<int64_t>(a.num_jt) / a.splits);
     std::vector<long long> h(4 * (a.num_jt + 4));
     WGP_CUDA(cudaMemcpyAsync(h.data(), a.trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
-    double s_wake = 0, s_epi = 0, s_back = 0, s_per = 0;
+    // r[0] MMA-1 committed, r[1] epilogue woke (S ready), r[2] epilogue arrived
+    // kfull, r[3] MMA-2 warp passed its waits.  Means over steady-state tiles.
+    double s_wake = 0, s_epi = 0, s_back = 0, s_per2 = 0, s_per1 = 0;
     int cnt = 0;
-    for (int t = 3; t + 1 < T0; ++t) {
+    for (int t = 6; t + 1 < T0; ++t) {
       const long long* r = &h[4 * t];
       s_wake += r[1] - r[0];
       s_epi += r[2] - r[1];
       s_back += r[3] - r[2];
-      s_per += h[4 * (t + 1) + 3] - r[3];
+      s_per2 += h[4 * (t + 1) + 3] - r[3];
+      s_per1 += h[4 * (t + 1) + 0] - r[0];
       ++cnt;
     }
     if (cnt)
-      fprintf(stderr, "[hv_tc trace] tiles=%d  mma1-commit->epi-wake %.0f  epi %.0f  kfull->mma-wake %.0f  period %.0f clk\n",
-              cnt, s_wake / cnt, s_epi / cnt, s_back / cnt, s_per / cnt);
+      fprintf(stderr,
+              "[hv_tc trace] tiles=%d  S-ready->epi-wake %.0f  epi %.0f  kfull->mma2 %.0f  mma2 period %.0f  "
+              "mma1 period %.0f  mma1-lead %.0f clk\n",
+              cnt, s_wake / cnt, s_epi / cnt, s_back / cnt, s_per2 / cnt, s_per1 / cnt,
+              static_cast<double>(h[4 * (T0 - 2) + 3] - h[4 * (T0 - 2) + 0]));
   }
   if (a.splits > 1) {
     tc_reduce_kernel<<<dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), 256, 0, st>>>(a);

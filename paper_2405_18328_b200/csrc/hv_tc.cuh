@@ -29,6 +29,8 @@ struct TcOperands {
 };
 
 bool hv_tc_supported(int d, int s);
-void hv_tc(TcOperands& ops, const HvParams& p, cudaStream_t st);
+// bf16 = false: 3xTF32 K.V (~2^-21 per product); true: bf16x3 K.V (kind::f16,
+// half the tensor work, ~2^-17 per product).  The Gram (MMA-1) is 3xTF32 in both.
+void hv_tc(TcOperands& ops, const HvParams& p, cudaStream_t st, bool bf16);
 
 }  // namespace wgp

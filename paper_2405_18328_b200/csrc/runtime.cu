@@ -180,9 +180,9 @@ struct Ctx {
     p.diag = static_cast<float>(sf * sf + sigma * sigma);
     p.done = done;
     p.split_rows = row_idx ? 0 : n;  // shards of the full operator decompose like the whole
-    if (hv_impl == WGP_HV_TC && hv_tc_supported(d, s)) {
+    if ((hv_impl == WGP_HV_TC || hv_impl == WGP_HV_TC_BF16) && hv_tc_supported(d, s)) {
       if (!tc.valid) tc.build(xs.as<float>(), n, dp, d, st);
-      hv_tc(tc, p, st);
+      hv_tc(tc, p, st, hv_impl == WGP_HV_TC_BF16);
     } else {
       hv_simt(p, st);
     }
@@ -810,7 +810,8 @@ int wgp_destroy(wgp_ctx* ctx) {
 
 int wgp_set_hv_impl(wgp_ctx* ctx, int impl) {
   return guarded([&] {
-    if (impl != WGP_HV_TC && impl != WGP_HV_SIMT) throw std::invalid_argument("unknown H.V implementation");
+    if (impl != WGP_HV_TC && impl != WGP_HV_SIMT && impl != WGP_HV_TC_BF16)
+      throw std::invalid_argument("unknown H.V implementation");
     ctx->c.hv_impl = impl;
   });
 }

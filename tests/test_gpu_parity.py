@@ -36,7 +36,7 @@ def make(n, d, s, seed, scale=1.0):
     return X, V, ls
 
 
-@pytest.mark.parametrize("impl", ["tc", "simt"])
+@pytest.mark.parametrize("impl", ["tc", "tc_bf16", "simt"])
 @pytest.mark.parametrize("n,d,s", [(1, 2, 1), (2, 1, 3), (129, 3, 16), (300, 3, 5), (1000, 9, 17),
                                    (2048, 8, 17), (777, 26, 65), (513, 11, 128)])
 def test_hv_matches_oracle(ctx, impl, n, d, s):
@@ -49,7 +49,7 @@ def test_hv_matches_oracle(ctx, impl, n, d, s):
     assert rel(out, ref) <= HV_TOL
 
 
-@pytest.mark.parametrize("impl", ["tc", "simt"])
+@pytest.mark.parametrize("impl", ["tc", "tc_bf16", "simt"])
 def test_hv_config1_full_size_row_samples(ctx, impl):
     """BASELINE config 1 at full size (n=13,500, d=26, s=65), checked on row
     samples against the oracle, plus a size-independent linearity check."""
