@@ -223,6 +223,9 @@ def main():
             dist.barrier()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
+        launches0 = wg.launch_count()
+        if args.hv_impl == "tc":
+            ctx.profile(True)
         with ClockSampler(local) as clk:
             for a, b in evs:
                 flush.zero_()
@@ -230,8 +233,14 @@ def main():
                 one_step()
                 b.record(stream)
             stream.synchronize()
+    launches = wg.launch_count() - launches0
+    kernel_ms, kernel_launches = ctx.profile_read() if args.hv_impl == "tc" else (0.0, 0)
+    ctx.profile(False)
     times = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.mean(times))
+    # dominant kernel's mean launch duration (events on the context stream);
+    # the SIMT path is a single kernel per step
+    kernel_ms = kernel_ms / kernel_launches if kernel_launches else ms
     if ws > 1:
         import torch.distributed as dist
         t = torch.tensor([ms], device=dev)
@@ -274,17 +283,22 @@ def main():
     f_entry = 2 * d + 2 * s + 8                       # SURVEY §8d F_hv
     flops = f_entry * n * n
     if args.hv_impl == "tc":
-        p_tf32 = pk["bf16"] / 2 * 1e12                 # TF32 = half the bf16 rate
+        # issued tensor work per entry: 3xTF32 Gram over the 32-wide augmented
+        # rows + bf16x3 K.V over s_pad columns; the epilogue needs one sqrt and
+        # one ex2 per entry on the MUFU (16/clk/SM).  The binding one is the peak.
+        spad = 16 * -(-s // 16)
+        p_bf16 = pk["bf16"] * 1e12
+        p_tf32 = p_bf16 / 2                            # TF32 = half the bf16 rate
         p_mufu = 16 * 148 * pk["mhz"] * 1e6            # ex2/sqrt per s (nominal)
-        t_entry = max((2 * d + 2 * s) * 3 / p_tf32, 2 / p_mufu)
+        t_tensor = 3 * 2 * 32 / p_tf32 + 3 * 2 * spad / p_bf16
+        t_entry = max(t_tensor, 2 / p_mufu)
         bound = "tensor"
     else:
         p_ffma = 2 * 128 * 148 * pk["mhz"] * 1e6
         t_entry = max(f_entry / p_ffma, 2 / (16 * 148 * pk["mhz"] * 1e6))
         bound = "tensor"  # compute (FFMA) bound; contract field admits hbm|tensor only
     peak = f_entry / t_entry / 1e12
-    kernel_ms = ms  # single launch per step at N=1
-    achieved = flops / (kernel_ms / 1e3) / 1e12
+    achieved = flops / ws / (kernel_ms / 1e3) / 1e12  # this rank's rows per launch
     traffic = None
     prof = os.path.join(ROOT, "profiles", "hv_tc_traffic.json")
     if os.path.exists(prof):
@@ -306,9 +320,11 @@ def main():
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_basis": (f"{pk['src']} peaks: F_hv={f_entry} flop/entry; "
-                                    + ("3xTF32 at bf16/2 and MUFU 16/clk/SM"
-                                       if args.hv_impl == "tc" else "FFMA 256 flop/clk/SM"))},
-        "gpu_launches": args.steps * (1 if ws == 1 else 1),
+                                    + ("max(3xTF32 Gram at bf16/2 + bf16x3 K.V at bf16, "
+                                       "2 MUFU ops at 16/clk/SM) per entry; MUFU binds"
+                                       if args.hv_impl == "tc" else "FFMA 256 flop/clk/SM")),
+                     "kernel_ms": kernel_ms},
+        "gpu_launches": int(launches),
         "clocks": clocks,
     }
     if ws == 1 and not args.no_cpu_baseline:

@@ -42,8 +42,12 @@ typedef struct wgp_ctx wgp_ctx;
 #define WGP_SOLVER_CG 0
 #define WGP_SOLVER_AP 1
 #define WGP_SOLVER_SGD 2
-/* H.V implementation: tcgen05 with 3xTF32 K.V (default), the SIMT fp32
- * kernel, or tcgen05 with bf16x3 K.V (faster, ~5e-6 instead of ~1e-6 relative). */
+/* H.V implementation (all: fp32 accumulation in chunks of 1024 points summed
+ * at higher precision, so the error does not grow with n):
+ *   WGP_HV_TC       tcgen05, Gram and K.V in 3xTF32 (default, ~1e-6 relative)
+ *   WGP_HV_SIMT     CUDA-core fp32 kernel (direct differences, ~1e-7)
+ *   WGP_HV_TC_BF16  tcgen05, K.V in bf16x3 (faster; ~5e-6 relative, too
+ *                   coarse for tight solver tolerances) */
 #define WGP_HV_TC 0
 #define WGP_HV_SIMT 1
 #define WGP_HV_TC_BF16 2
@@ -54,6 +58,8 @@ const char* wgp_last_error(void);
 const char* wgp_version(void);
 /** Number of visible CUDA devices (0 on a GPU-less host; never an error). */
 int wgp_device_count(void);
+/** Kernels launched by this library in this process so far (all contexts). */
+uint64_t wgp_launch_count(void);
 
 /** Create a context on `device`.  Replaces nothing in the reference (which
  *  has no device); owns the stream, workspaces and warm-start buffers. */
@@ -63,6 +69,11 @@ int wgp_destroy(wgp_ctx* ctx);
 int wgp_set_hv_impl(wgp_ctx* ctx, int impl);
 /** The cudaStream_t the context launches on (for event timing by callers). */
 void* wgp_stream(wgp_ctx* ctx);
+/** Kernel timing: while enabled, CUDA events bracket every tensor-core H.V
+ *  kernel launch on the context stream; wgp_profile_read syncs, returns the
+ *  summed kernel time (ms) and launch count since the last read, and resets. */
+int wgp_profile(wgp_ctx* ctx, int enable);
+int wgp_profile_read(wgp_ctx* ctx, double* kernel_ms, int* launches);
 
 /** Upload the n x d training inputs (host, column-major fp32).  Replaces the
  *  X argument of build_kernel_matrices (proj/src/kernel.cpp:120-139): the

@@ -30,6 +30,8 @@ _lib = None
 
 WGP_OK, WGP_INVALID, WGP_NUMERICAL, WGP_DEVICE = 0, 2, 3, 4
 HV_TC, HV_SIMT, HV_TC_BF16 = 0, 1, 2
+# tc: tcgen05 3xTF32 (default); simt: CUDA-core fp32; tc_bf16: tcgen05 with
+# bf16x3 K.V (faster, ~5e-6 relative: not for tight solver tolerances)
 _HV_IMPLS = {"tc": HV_TC, "simt": HV_SIMT, "tc_bf16": HV_TC_BF16}
 _KINDS = {"cg": 0, "ap": 1, "sgd": 2}
 _MODES = {"warm": 0, "cold": 1, "cold-fixed": 2}
@@ -83,7 +85,7 @@ EXPORTS = [
     "wgp_last_error", "wgp_version", "wgp_device_count", "wgp_create", "wgp_destroy",
     "wgp_set_hv_impl", "wgp_stream", "wgp_set_data", "wgp_set_hyper", "wgp_set_rows", "wgp_hv",
     "wgp_hv_device", "wgp_solve", "wgp_grad", "wgp_sample_probes", "wgp_rff_probes", "wgp_train",
-    "wgp_adam_step", "wgp_derive_seed",
+    "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
 ]
 
 
@@ -105,6 +107,9 @@ def load():
     lib.wgp_version.restype = C.c_char_p
     lib.wgp_stream.restype = C.c_void_p
     lib.wgp_stream.argtypes = [C.c_void_p]
+    lib.wgp_launch_count.restype = C.c_uint64
+    lib.wgp_profile.argtypes = [C.c_void_p, C.c_int]
+    lib.wgp_profile_read.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.wgp_derive_seed.restype = C.c_uint64
     lib.wgp_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
     lib.wgp_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
@@ -136,6 +141,11 @@ def _check(rc: int):
     if rc == WGP_INVALID:
         raise ValueError(msg)
     raise DeviceError(msg)
+
+
+def launch_count() -> int:
+    """Kernels this library has launched in this process (all contexts)."""
+    return int(load().wgp_launch_count())
 
 
 def device_count() -> int:
@@ -367,6 +377,16 @@ class Context:
     @property
     def stream(self) -> int:
         return int(self._lib.wgp_stream(self._h) or 0)
+
+    def profile(self, enable: bool = True):
+        """Bracket every tensor-core H.V kernel launch with CUDA events."""
+        _check(self._lib.wgp_profile(self._h, int(enable)))
+
+    def profile_read(self):
+        """(summed kernel ms, launches) since the last read; resets."""
+        ms, k = C.c_double(0.0), C.c_int(0)
+        _check(self._lib.wgp_profile_read(self._h, C.byref(ms), C.byref(k)))
+        return float(ms.value), int(k.value)
 
     def set_hv_impl(self, impl: str):
         if impl not in _HV_IMPLS:

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -25,7 +26,14 @@ struct DeviceError : std::runtime_error {
                                " at " + __FILE__ + ":" + std::to_string(__LINE__));      \
   } while (0)
 
-#define WGP_LAUNCH_CHECK() WGP_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by WGP_LAUNCH_CHECK, which
+// also counts it (wgp_launch_count: bench.py's gpu_launches).
+std::atomic<uint64_t>& launch_counter();
+#define WGP_LAUNCH_CHECK()                                                   \
+  do {                                                                       \
+    ::wgp::launch_counter().fetch_add(1, std::memory_order_relaxed);         \
+    WGP_CUDA(cudaGetLastError());                                            \
+  } while (0)
 
 constexpr double kSqrt3 = 1.7320508075688772;
 constexpr double kLog2e = 1.4426950408889634;

@@ -49,11 +49,15 @@ __global__ void __launch_bounds__(NT) hv_simt_kernel(HvParams p) {
   const int ty = tid / 16, tx = tid % 16;
   const int ii = ty * 4;   // rows of this thread (K phase and GEMM phase)
   const int jj = tx * 4;   // points of this thread (K phase)
-  float acc[4][CPT];
+  // Each 64-point tile is accumulated in fp32 (tacc) and added to an fp64
+  // running sum, so the rounding error does not grow with n (one fp32 sum
+  // over all n points drifts like sqrt(n) 2^-24 |out|: 2.7e-6 relative at
+  // n = 20000 on dense data, measured).
+  double acc[4][CPT];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
 #pragma unroll
-    for (int q = 0; q < CPT; ++q) acc[r][q] = 0.f;
+    for (int q = 0; q < CPT; ++q) acc[r][q] = 0.0;
 
   for (int64_t jt = p.j0; jt < p.j1; jt += TJ) {
     __syncthreads();
@@ -100,6 +104,11 @@ __global__ void __launch_bounds__(NT) hv_simt_kernel(HvParams p) {
     }
     __syncthreads();
     // acc[4 rows][CPT cols] += K[rows, j] * V[j, cols]
+    float tacc[4][CPT];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) tacc[r][q] = 0.f;
 #pragma unroll 4
     for (int j = 0; j < TJ; ++j) {
       const float4 kk = *reinterpret_cast<const float4*>(&ks[j * (TM + 4) + ii]);
@@ -108,12 +117,16 @@ __global__ void __launch_bounds__(NT) hv_simt_kernel(HvParams p) {
       for (int q = 0; q < CPT; ++q) vb[q] = vs[j * SP + tx + 16 * q];
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
-        acc[0][q] = fmaf(kk.x, vb[q], acc[0][q]);
-        acc[1][q] = fmaf(kk.y, vb[q], acc[1][q]);
-        acc[2][q] = fmaf(kk.z, vb[q], acc[2][q]);
-        acc[3][q] = fmaf(kk.w, vb[q], acc[3][q]);
+        tacc[0][q] = fmaf(kk.x, vb[q], tacc[0][q]);
+        tacc[1][q] = fmaf(kk.y, vb[q], tacc[1][q]);
+        tacc[2][q] = fmaf(kk.z, vb[q], tacc[2][q]);
+        tacc[3][q] = fmaf(kk.w, vb[q], tacc[3][q]);
       }
     }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) acc[r][q] += static_cast<double>(tacc[r][q]);
   }
   // Epilogue: + sigma^2 V on the diagonal, then store / residual / subtract.
 #pragma unroll
@@ -126,7 +139,7 @@ __global__ void __launch_bounds__(NT) hv_simt_kernel(HvParams p) {
     for (int q = 0; q < CPT; ++q) {
       const int c = tx + 16 * q;
       if (c >= p.s) continue;
-      float v = acc[a][q];
+      float v = static_cast<float>(acc[a][q]);
       if (diag) v = fmaf(p.diag, p.V[g + c * p.ldv], v);
       float* o = p.out + lr + c * p.ldo;
       if (p.mode == kHvStore)

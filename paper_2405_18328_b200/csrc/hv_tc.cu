@@ -1,4 +1,4 @@
-// hv_tc.cu — fused Matern-3/2 H.V on the 5th-generation tensor cores (v1).
+// hv_tc.cu — fused Matern-3/2 H.V on the 5th-generation tensor cores.
 //
 // Replaces the dense products H * V of the reference solvers
 // (proj/src/solvers.cpp:71,92,110,120,169,186,188,211,242) without forming H.
@@ -11,18 +11,19 @@
 //   epilogue       k = sf^2 (1 + u ln2) 2^-u from S (tcgen05.ld -> registers,
 //                    sqrt + ex2 on the MUFU), the diagonal entry zeroed
 //                    (H_ii V_i = (sf^2 + sigma^2) V_i is added exactly at the end),
-//                    split k = k_hi + k_lo, tcgen05.st back to TMEM
-//   MMA-2  O[I,:] += K[I,J] . V[J,:]       (A operand from TMEM, 3xTF32)
+//                    split k = k1 + k2 into two bf16, tcgen05.st back to TMEM
+//   MMA-2  O[I,:] += K[I,J] . V[J,:]       (kind::f16, A = K from TMEM, bf16x3:
+//                    k1 v1 + k1 v2 + k2 v1 with V = v1 + v2 split likewise)
 //
-// Warp roles: warp 0 TMA producer, warp 1 MMA issuer (one thread), warp 2
-// TMEM allocator, warps 4..15 epilogue (three warpgroups; group w owns TMEM
-// buffer w and tiles t = w, w+3, ...).  Three 128-column TMEM buffers hold S
-// and then, in place, K = k_hi | k_lo, so MMA-1 runs three tiles ahead of
-// MMA-2 and the epilogue latency of one tile hides behind the MMAs of the
-// next two.  Shared memory holds separate rings for the Gram operand B_J
-// (4 stages, consumed by MMA-1) and for V_J (2-3 stages, consumed by MMA-2).
-// J tiles of a row tile may be split across CTAs (fixed split count per
-// launch shape, partials summed in fixed order -> deterministic).
+// Warp roles (512 threads): warps 0..11 epilogue (three warpgroups; group w
+// takes tiles t = w, w+3, ...), warp 12 TMA producer of A_I and the B_J ring,
+// 13 MMA-1 issuer, 14 TMA producer of the V_J ring (+ TMEM allocation), 15
+// MMA-2 issuer.  Five 64-column TMEM buffers hold S and then, in place, the
+// packed K, so MMA-1 runs ahead of MMA-2 and the epilogue latency of one tile
+// hides behind the MMAs of the next.  MMA-2 accumulates in fp32 chunks of 16
+// tiles that the epilogue drains into fp64 (accumulation error independent of
+// n).  J tiles of a row tile may be split across CTAs (split count fixed per
+// launch shape, fp64 partials summed in fixed order -> deterministic).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -39,9 +40,8 @@ namespace wgp {
 namespace {
 
 constexpr int kTI = 128;   // rows per tile (MMA M)
-constexpr int kTJ = 64;    // points per tile (MMA-1 N, MMA-2 K)
 constexpr int kKA = 32;    // augmented Gram dimension (d + 2 <= 32)
-constexpr int kThreads = 512;  // 4 control warps + 3 epilogue warpgroups
+constexpr int kThreads = 512;  // 3 epilogue warpgroups + 4 control warps
 constexpr uint32_t kTfMask = 0xFFFFE000u;  // keep sign, exponent, 10 mantissa bits
 constexpr int kSmemLimit = 232448 - 2048;  // 227 KB opt-in minus static smem (barriers)
 constexpr int kMaxStages = 8;              // smem ring depth cap (barrier arrays)
@@ -52,10 +52,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-               : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
@@ -73,33 +69,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     if (ok) break;
   }
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                            int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
-      "[%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // MMA issue helpers are called by a whole converged warp with warp-uniform
 // operands (so descriptors live in uniform registers); one lane, chosen by
 // elect.sync, issues.
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
-      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
-                                       uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
-      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
-}
 // The three 3xTF32 partial products of one K step from a single asm block
 // (one elect): D (+)= A_hi B_hi + A_hi B_lo + A_lo B_hi.
 __device__ __forceinline__ void mma3_ss(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
@@ -194,23 +169,6 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-// 32 squared scaled distances -> tf32 hi / lo planes of k; the diagonal
-// entry (dg in [0, 32)) is zeroed: H_ii V_i is applied exactly at the end.
-template <bool DIAG>
-__device__ __forceinline__ void to_k(const uint32_t (&r)[32], uint32_t (&khi)[32], uint32_t (&klo)[32],
-                                     float sf2, float ac, int dg) {
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const float k = matern_from_u(sqrt_approx(fabsf(__uint_as_float(r[i]))), sf2, ac);
-    khi[i] = __float_as_uint(k) & kTfMask;
-    klo[i] = __float_as_uint(k - __uint_as_float(khi[i]));
-    if (DIAG && dg == i) {
-      khi[i] = 0u;
-      klo[i] = 0u;
-    }
-  }
-}
-
 // bf16 x 3 MMA-2 (kind::f16, K = 16 per instruction): D (+)= k1 v1 + k1 v2 + k2 v1.
 __device__ __forceinline__ void mma3_ts_bf16(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
                                              uint32_t idesc, uint32_t acc) {
@@ -228,17 +186,32 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-// 32 squared distances -> 16 packed bf16x2 words of k1 = bf16(k) and of
-// k2 = bf16(k - k1) (lower K index in the low half), written at w[OFF..OFF+16).
-// 32 squared distances (one half of a tile) -> 32 packed bf16x2 words:
-// w[c] = k1 pair c = bf16(k), w[16 + c] = k2 pair c = bf16(k - k1) (lower K
-// index in the low half).  POLY evaluates 2^-u of the odd entries on the FMA
-// pipe (ex2_poly) instead of the MUFU.
-// The squared distance from the tensor core can be a tiny negative number
-// for (near-)duplicate points; sqrt(|u^2|) keeps it finite and folds the abs
-// into the MUFU operand (no separate clamp instruction).  DIAG is a separate
-// instantiation for the rare tiles that contain the diagonal, so the common
-// path carries no per-entry index compares.
+// 32 squared scaled distances -> tf32 hi / lo planes of k (k_hi keeps sign,
+// exponent and 10 mantissa bits; k_lo = k - k_hi is exact); the diagonal
+// entry (dg in [0, 32)) is zeroed: H_ii V_i is applied exactly at the end.
+template <bool DIAG>
+__device__ __forceinline__ void to_k(const uint32_t (&r)[32], uint32_t (&khi)[32], uint32_t (&klo)[32],
+                                     float sf2, float ac, int dg) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float k = matern_from_u(sqrt_approx(fabsf(__uint_as_float(r[i]))), sf2, ac);
+    khi[i] = __float_as_uint(k) & kTfMask;
+    klo[i] = __float_as_uint(k - __uint_as_float(khi[i]));
+    if (DIAG && dg == i) {
+      khi[i] = 0u;
+      klo[i] = 0u;
+    }
+  }
+}
+
+// 32 squared distances (one half of a 64-point tile) -> 32 packed bf16x2
+// words: w[c] = k1 pair c = bf16(k), w[16 + c] = k2 pair c = bf16(k - k1)
+// (lower K index in the low half).  POLY evaluates 2^-u of the odd entries on
+// the FMA pipe (ex2_poly) instead of the MUFU.  The squared distance from the
+// tensor core can be a tiny negative number for (near-)duplicate points;
+// sqrt(|u^2|) keeps it finite and folds the abs into the MUFU operand.  DIAG
+// is a separate instantiation for the rare tiles that contain the diagonal,
+// so the common path carries no per-entry index compares.
 template <bool POLY, bool DIAG>
 __device__ __forceinline__ void to_k_bf16(const uint32_t (&r)[32], uint32_t (&w)[32], float sf2, float ac,
                                           int dg) {
@@ -263,11 +236,13 @@ struct TcArgs {
   int64_t m;         // output rows
   int a_row0;        // first A-map row of this launch
   int64_t j0, j1;    // contracted points
-  int num_jt;        // 64-point tiles in [j0, j1)
+  int num_jt;        // J tiles in [j0, j1)
   int splits;
+  int chunk;         // tiles per fp32 accumulation chunk
   int s, s_pad;
   int nb, nv;              // B-ring and V-ring stages
-  uint32_t vstage_bytes;   // V boxes of one tile (tf32: 4 x 32 points, bf16: 2 x 64 points)
+  uint32_t vstage_bytes;   // V planes of one tile (2 x s_pad rows of 128 bytes)
+  uint32_t a_region;       // shared bytes of A_I (+ the running sum R)
   const int* row_idx;
   int64_t r0;
   const float* V;
@@ -278,30 +253,39 @@ struct TcArgs {
   int64_t ldb;
   int mode;
   float sf2, a, diag;
-  float* part;
+  float* part;       // [splits][s_pad][m_pad] fp32 split partials (splits > 1)
+  double* flush;     // [splits][s_pad][m_pad] fp64 running sums (T > flush_every * chunk)
+  int flush_every;   // chunks per fp32 running sum before it is flushed to fp64
   int64_t m_pad;
   const int* done;
   long long* trace;  // WGP_TC_TRACE: per-tile clock64 stamps of CTA 0 ([T][4])
   int dbg;  // ablation bits (WGP_TC_DEBUG): 1 no epilogue math, 2 no MMA-2, 4 no MMA-1, 8 no V loads,
-            // 16 no epilogue TMEM traffic, 32 no B loads, 128 bf16: FMA-pipe ex2 for odd entries
+            // 16 no epilogue TMEM traffic, 32 no B loads, 128 (bf16) FMA-pipe ex2 for odd entries
 };
 
-// TMEM: O accumulator in columns [0, 128); tile buffers from column 128.
-//   tf32 x 3 (BF = false): 3 buffers x 128 columns; S in [0, 64) is overwritten
-//     in place by k_hi once read, k_lo in [64, 128).
-//   bf16 x 3 (BF = true): 6 buffers x 64 columns; S in [0, 64) is overwritten by
-//     the packed k1 (32 columns) and k2 (32 columns).
+// Two K.V precisions share the pipeline:
+//   BF = false (default, WGP_HV_TC): K.V in 3xTF32 (k_hi v_hi + k_hi v_lo +
+//     k_lo v_hi, ~2^-21 per product), 32-point J tiles.  TMEM: O0 [0, 96),
+//     O1 [96, 192), A_I hi/lo [192, 256) (MMA-1 reads A from TMEM), four
+//     64-column buffers from 256, each holding S (32 fp32 columns) and then,
+//     in place, k_hi | k_lo (32 + 32 columns).
+//   BF = true (WGP_HV_TC_BF16): K.V in bf16x3 (k1 v1 + k1 v2 + k2 v1, ~2^-17
+//     per product: half the tensor work, too coarse for tight solver
+//     tolerances), 64-point J tiles.  TMEM: O0, O1, five 64-column buffers
+//     from 192 (S: 64 fp32 columns, overwritten by the packed k1 | k2 pairs);
+//     A_I stays in shared memory (SS MMA-1).
+// The Gram (MMA-1) is 3xTF32 in both.
 template <bool BF>
-struct Layout {
-  // bf16: O [0, 96), A_I hi/lo [96, 160) (MMA-1 reads A from TMEM: with A in
-  // shared memory MMA-1 is smem-bandwidth bound at 48 clk/MMA, measured), five
-  // 64-column buffers from 160.  tf32: O [0, 128), three 128-column buffers.
-  static constexpr int kBufs = BF ? 5 : 3;
-  static constexpr uint32_t kWidth = BF ? 64u : 128u;
-  static constexpr uint32_t kFirst = BF ? 160u : 128u;
-  static constexpr uint32_t kAhi = 96u, kAlo = 128u;
-  static __device__ __forceinline__ uint32_t col(int b) { return kFirst + kWidth * static_cast<uint32_t>(b); }
+struct Cfg {
+  static constexpr int kTJ = BF ? 64 : 32;        // points per J tile
+  static constexpr int kBufs = BF ? 5 : 4;
+  static constexpr uint32_t kOStride = 96;
+  static constexpr uint32_t kAhi = 192, kAlo = 224;  // BF = false only
+  static constexpr uint32_t kBufFirst = BF ? 192u : 256u;
+  static constexpr uint32_t kBStage = 2u * kTJ * 128u;  // B_hi | B_lo planes
+  static __device__ __forceinline__ uint32_t buf_col(int b) { return kBufFirst + 64u * static_cast<uint32_t>(b); }
 };
+
 constexpr int kEpiGroups = 3;
 // Warp roles.  The warp scheduler prefers the highest warp id among eligible
 // warps, so the latency-critical control warps get the top ids and the 12
@@ -310,35 +294,54 @@ constexpr int kEpiGroups = 3;
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kWarpBProd = 12, kWarpM1 = 13, kWarpVProd = 14, kWarpM2 = 15;
 
+// Accumulation precision.  MMA-2 accumulates into fp32 TMEM, and every
+// K-step instruction rounds the running sum: with ~3 n / 8 roundings per
+// output the error of one long accumulation grows like sqrt(n) 2^-24 |O|
+// (measured 1e-5 relative at n = 20000 on dense data, beyond the 1e-5 bar at
+// the reference's larger sizes).  The J tiles of a CTA are therefore
+// accumulated in chunks of `chunk` tiles (1024 points), alternating between
+// O0 and O1; the epilogue warps add each finished chunk into an fp32 running
+// sum R in shared memory (row-private, no synchronisation) while MMA-2 fills
+// the other accumulator, and every `flush_every` chunks R is moved to a
+// CTA-private fp64 sum in global memory.  Error per output: ~sqrt(roundings
+// per chunk) + sqrt(flush_every) roundings, independent of n; the
+// shared-memory drain costs no L2 traffic (an fp64 global drain per chunk
+// measured +20% time).
 template <bool BF>
 __global__ void __launch_bounds__(kThreads, 1)
     hv_tc_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                  const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                  const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
                  const TcArgs p) {
-  using L = Layout<BF>;
-  constexpr int NBUF = L::kBufs;
+  using K = Cfg<BF>;
+  constexpr int NBUF = K::kBufs;
+  constexpr int TJ = K::kTJ;
   if (p.done && *p.done) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bar_bfull[kMaxStages], bar_bempty[kMaxStages], bar_vfull[kMaxStages],
       bar_vempty[kMaxStages];
-  __shared__ __align__(8) uint64_t bar_a, bar_atm, bar_sfull[NBUF], bar_kfull[NBUF], bar_kempty[NBUF], bar_o;
+  __shared__ __align__(8) uint64_t bar_a, bar_atm, bar_sfull[NBUF], bar_kfull[NBUF], bar_kempty[NBUF],
+      bar_ofull[2], bar_odrained[2];
   __shared__ uint32_t tmem_slot;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAhi = smem;
   uint8_t* sAlo = smem + 16384;
-  uint8_t* sB = smem + 32768;                            // nb x [B_hi 8K | B_lo 8K]
-  uint8_t* sV = sB + static_cast<size_t>(p.nb) * 16384;  // nv x vstage
+  // R: [s_pad][128] fp32 running sum; with A_I in TMEM (BF = false) it reuses
+  // A's staging area, which is dead once A has been copied to TMEM.
+  float* sR = reinterpret_cast<float*>(BF ? smem + 32768 : smem);
+  uint8_t* sB = smem + p.a_region;                            // nb x [B_hi | B_lo]
+  uint8_t* sV = sB + static_cast<size_t>(p.nb) * K::kBStage;  // nv x vstage
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rt = blockIdx.x / p.splits, sp = blockIdx.x % p.splits;
   const int jt_begin = static_cast<int>(static_cast<int64_t>(p.num_jt) * sp / p.splits);
   const int jt_end = static_cast<int>(static_cast<int64_t>(p.num_jt) * (sp + 1) / p.splits);
   const int T = jt_end - jt_begin;
+  const int C = p.chunk;
   const int NB = p.nb, NV = p.nv;
   const int spad = p.s_pad;
-  const uint32_t vbox = static_cast<uint32_t>(spad) * 128u;  // one V box (128-byte rows)
+  const uint32_t vbox = static_cast<uint32_t>(spad) * 128u;  // one V plane (128-byte rows)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NB; ++i) {
@@ -356,7 +359,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_kfull[i], 4);
       mbar_init(&bar_kempty[i], 1);
     }
-    mbar_init(&bar_o, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_ofull[i], 1);
+      mbar_init(&bar_odrained[i], kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kWarpVProd) {
@@ -378,56 +384,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < T; ++t) {
         const int st = t % NB;
         if (t >= NB) mbar_wait(&bar_bempty[st], ((t / NB) - 1) & 1);
-        uint8_t* base = sB + static_cast<size_t>(st) * 16384;
+        uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
         if (p.dbg & 32) {
           mbar_arrive_warp(&bar_bfull[st]);
           continue;
         }
-        mbar_expect_tx_warp(&bar_bfull[st], 16384u);
-        const int pt = static_cast<int>(p.j0) + (jt_begin + t) * kTJ;
+        mbar_expect_tx_warp(&bar_bfull[st], K::kBStage);
+        const int pt = static_cast<int>(p.j0) + (jt_begin + t) * TJ;
         tma_load_2d_warp(base, &mBhi, &bar_bfull[st], 0, pt);
-        tma_load_2d_warp(base + 8192, &mBlo, &bar_bfull[st], 0, pt);
+        tma_load_2d_warp(base + K::kBStage / 2, &mBlo, &bar_bfull[st], 0, pt);
       }
     }
   } else if (warp == kWarpVProd) {
     // ------------------------------------------------------------ TMA producer: V ring
-    // (separate warp so the two rings never block each other)
+    // (separate warp so the two rings never block each other); one box of
+    // 128-byte rows (32 tf32 / 64 bf16 points) per plane and tile
     if (T > 0) {
       for (int t = 0; t < T; ++t) {
         const int st = t % NV;
         if (t >= NV) mbar_wait(&bar_vempty[st], ((t / NV) - 1) & 1);
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
-        const int vp = (jt_begin + t) * kTJ;
+        const int vp = (jt_begin + t) * TJ;
         if (p.dbg & 8) {
           mbar_arrive_warp(&bar_vfull[st]);
           continue;
         }
         mbar_expect_tx_warp(&bar_vfull[st], p.vstage_bytes);
-        if constexpr (BF) {  // one 64-point box per plane
-          tma_load_2d_warp(base, &mVhi, &bar_vfull[st], vp, 0);
-          tma_load_2d_warp(base + vbox, &mVlo, &bar_vfull[st], vp, 0);
-        } else {  // two 32-point boxes per plane
-          tma_load_2d_warp(base, &mVhi, &bar_vfull[st], vp, 0);
-          tma_load_2d_warp(base + vbox, &mVhi, &bar_vfull[st], vp + 32, 0);
-          tma_load_2d_warp(base + 2 * vbox, &mVlo, &bar_vfull[st], vp, 0);
-          tma_load_2d_warp(base + 3 * vbox, &mVlo, &bar_vfull[st], vp + 32, 0);
-        }
+        tma_load_2d_warp(base, &mVhi, &bar_vfull[st], vp, 0);
+        tma_load_2d_warp(base + vbox, &mVlo, &bar_vfull[st], vp, 0);
       }
     }
   } else if (warp == kWarpM1) {
     // ------------------------------------------------------------ MMA-1 issuer
     // Two issuing warps: tcgen05.mma issue blocks while the tensor pipe is
     // busy (queue depth ~1, measured), so one warp's barrier waits and
-    // commits would idle the pipe.  Warp 1 issues MMA-1 (Gram) and warp 3
-    // MMA-2 (K.V); each one's waits overlap the other's MMAs.  MMA-1(t)
-    // reuses buffer t % NBUF only after MMA-2(t - NBUF) has committed kempty.
-    // The whole warp runs the loop (uniform operands); elect.sync picks the lane.
+    // commits would idle the pipe.  This warp issues MMA-1 (Gram, 3xTF32) and
+    // kWarpM2 MMA-2 (K.V); each one's waits overlap the other's MMAs.
+    // MMA-1(t) reuses buffer t % NBUF only after MMA-2(t - NBUF) committed
+    // kempty.  The whole warp runs the loop (uniform operands); elect.sync
+    // picks the issuing lane.
     if (T > 0) {
-      constexpr uint32_t id1 = idesc_tf32(kTI, kTJ);
+      constexpr uint32_t id1 = idesc_tf32(kTI, TJ);
       if constexpr (BF) {
-        mbar_wait(&bar_atm, 0);  // A_I copied into TMEM by epilogue group 0
-      } else {
         mbar_wait(&bar_a, 0);
+      } else {
+        mbar_wait(&bar_atm, 0);  // A_I copied into TMEM by epilogue group 0
       }
       tc_after();
       const uint64_t dAhi = umma_desc(sAhi), dAlo = umma_desc(sAlo);
@@ -436,17 +437,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t >= NBUF) mbar_wait(&bar_kempty[b], ((t / NBUF) - 1) & 1);
         mbar_wait(&bar_bfull[st], (t / NB) & 1);
         tc_after();
-        uint8_t* base = sB + static_cast<size_t>(st) * 16384;
-        const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + 8192);
-        const uint32_t d = tmem + L::col(b);
+        uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
+        const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + K::kBStage / 2);
+        const uint32_t d = tmem + K::buf_col(b);
         if (!(p.dbg & 4)) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             if constexpr (BF)
-              mma3_ts(d, tmem + L::kAhi + 8 * k, tmem + L::kAlo + 8 * k, dBhi + 2 * k, dBlo + 2 * k, id1,
-                      k > 0);
-            else
               mma3_ss(d, dAhi + 2 * k, dAlo + 2 * k, dBhi + 2 * k, dBlo + 2 * k, id1, k > 0);
+            else
+              mma3_ts(d, tmem + K::kAhi + 8 * k, tmem + K::kAlo + 8 * k, dBhi + 2 * k, dBlo + 2 * k, id1,
+                      k > 0);
           }
         }
         mma_commit(&bar_sfull[b]);
@@ -461,36 +462,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t box = vbox >> 4;
       for (int t = 0; t < T; ++t) {
         const int b = t % NBUF, st = t % NV;
+        const int c = t / C, tc = t - c * C;
+        const uint32_t o = tmem + static_cast<uint32_t>(c & 1) * K::kOStride;
+        // chunk c reuses O[c & 1] once the epilogue drained chunk c - 2
+        if (tc == 0 && c >= 2) mbar_wait(&bar_odrained[c & 1], ((c >> 1) - 1) & 1);
         mbar_wait(&bar_vfull[st], (t / NV) & 1);
         mbar_wait(&bar_kfull[b], (t / NBUF) & 1);
         tc_after();
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 3] = clock64();
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
-        const uint32_t kb = tmem + L::col(b);
+        const uint32_t kb = tmem + K::buf_col(b);
         const uint64_t dv = umma_desc(base);
         if (!(p.dbg & 2)) {
-          if constexpr (BF) {
-            // per 32-point half h: k1 in columns [32h, 32h+16), k2 in
-            // [32h+16, 32h+32); a 16-point K step is 8 columns
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < 4; ++k) {
+            if constexpr (BF) {
+              // per 32-point half h: k1 in columns [32h, 32h+16), k2 in
+              // [32h+16, 32h+32); a 16-point K step is 8 columns
               const uint32_t c1 = 32u * (k >> 1) + 8u * (k & 1);
-              mma3_ts_bf16(tmem, kb + c1, kb + c1 + 16, dv + 2 * k, dv + box + 2 * k, id2,
-                           (t > 0 || k > 0) ? 1u : 0u);
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const uint64_t off = static_cast<uint64_t>(k >> 2) * box + static_cast<uint64_t>(k & 3) * 2;
-              mma3_ts(tmem, kb + 8 * k, kb + 64 + 8 * k, dv + off, dv + 2 * box + off, id2,
-                      (t > 0 || k > 0) ? 1u : 0u);
+              mma3_ts_bf16(o, kb + c1, kb + c1 + 16, dv + 2 * k, dv + box + 2 * k, id2,
+                           (tc > 0 || k > 0) ? 1u : 0u);
+            } else {
+              // k_hi in columns [0, 32), k_lo in [32, 64); an 8-point K step is 8 columns
+              mma3_ts(o, kb + 8 * k, kb + 32 + 8 * k, dv + 2 * k, dv + box + 2 * k, id2,
+                      (tc > 0 || k > 0) ? 1u : 0u);
             }
           }
         }
         mma_commit(&bar_vempty[st]);
         mma_commit(&bar_kempty[b]);
+        if (tc == C - 1 || t == T - 1) mma_commit(&bar_ofull[c & 1]);
       }
-      mma_commit(&bar_o);
     }
   } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
@@ -505,9 +507,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (valid) g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
     const float sf2 = p.sf2, ac = p.a;
     const bool nomath = p.dbg & 1;
-    if (BF && w == 0 && T > 0) {
+    const int nch = (T + C - 1) / C;
+    const bool diag = g >= p.j0 && g < p.j1;
+    if (!BF && w == 0 && T > 0) {
       // Copy this row of A_I (hi, lo: 32 fp32 each) from the 128B-swizzled
-      // TMA tile into TMEM columns [96, 160): MMA-1 then reads A from TMEM.
+      // TMA tile into TMEM: MMA-1 then reads A from TMEM (with A in shared
+      // memory MMA-1 is smem-bandwidth bound, 48 clk per MMA, measured).
       mbar_wait(&bar_a, 0);
       uint32_t ah[32], al[32];
       const uint8_t* rh = sAhi + (row >> 3) * 1024 + (row & 7) * 128;
@@ -521,25 +526,98 @@ __global__ void __launch_bounds__(kThreads, 1)
         al[4 * c] = vl.x, al[4 * c + 1] = vl.y, al[4 * c + 2] = vl.z, al[4 * c + 3] = vl.w;
       }
       __syncwarp();
-      tmem_st32(tmem + lanes + Layout<BF>::kAhi, ah);
-      tmem_st32(tmem + lanes + Layout<BF>::kAlo, al);
+      tmem_st32(tmem + lanes + K::kAhi, ah);
+      tmem_st32(tmem + lanes + K::kAlo, al);
       tmem_wait_st();
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_atm);
     }
+    // Drain chunk c: R (+)= O[c & 1] over this group's columns; every
+    // flush_every chunks R moves into the fp64
+    // global sum F.  The accumulator is released to MMA-2 as soon as it has
+    // been read.  The last chunk finishes the row: the exact diagonal term and
+    // the output mode, or the fp32 partial when the J tiles are split across
+    // CTAs.
+    double* F = p.flush + static_cast<int64_t>(sp) * spad * p.m_pad + lr;  // column c at F[c * m_pad]
+    float* R = sR + row;                                                   // column c at R[c * 128]
+    const int FE = p.flush_every;
+    // Group w owns the contiguous column block [cb, ce) (<= 32 columns,
+    // multiples of 8): one TMEM round trip per drain.
+    const int cpg = ((spad + 3 * 8 - 1) / (3 * 8)) * 8;
+    const int cb = min(spad, w * cpg), ce = min(spad, (w + 1) * cpg);
+    auto drain = [&](int c) {
+      mbar_wait(&bar_ofull[c & 1], (c >> 1) & 1);
+      tc_after();
+      const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
+      const bool last = c == nch - 1;
+      const bool fresh = c % FE == 0;  // R starts over with this chunk
+      const bool flush = !last && (c + 1) % FE == 0;
+      uint32_t o[4][8];
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (cb + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + cb + 8 * k, o[k]);
+      tmem_wait_ld();
+      if (!last) {  // O[c & 1] is free for chunk c + 2 once read
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_odrained[c & 1]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (cb + 8 * k >= ce) break;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int col = cb + 8 * k + i;
+          const float r = (fresh ? 0.f : R[col * 128]) + __uint_as_float(o[k][i]);
+          if (!last) {
+            if (flush) {
+              if (valid && col < p.s) {
+                double* f = F + static_cast<int64_t>(col) * p.m_pad;
+                *f = (c + 1 == FE ? 0.0 : *f) + static_cast<double>(r);
+              }
+            } else {
+              R[col * 128] = r;
+            }
+            continue;
+          }
+          if (!valid || col >= p.s) continue;
+          float v = r;
+          if (c >= FE) v = static_cast<float>(F[static_cast<int64_t>(col) * p.m_pad] + static_cast<double>(r));
+          if (p.splits > 1) {
+            p.part[(static_cast<int64_t>(sp) * spad + col) * p.m_pad + lr] = v;
+            continue;
+          }
+          if (diag) v = fmaf(p.diag, p.V[g + col * p.ldv], v);
+          float* dst = p.out + lr + col * p.ldo;
+          if (p.mode == kHvStore)
+            *dst = v;
+          else if (p.mode == kHvResidual)
+            *dst = p.B[g + col * p.ldb] - v;
+          else
+            *dst -= v;
+        }
+      }
+    };
+    // Chunk dc is drained `lag` tiles after it ended, so its last MMA-2 has
+    // retired by then; every group still drains it before MMA-2 reaches
+    // chunk dc + 2 (lag + 2 <= C), so MMA-2 never waits for a drain.
+    const int lag = max(2, C / 2);
+    int dc = 0;  // next chunk to drain
     for (int t = w; t < T; t += kEpiGroups) {
+      while (dc < nch - 1 && t >= (dc + 1) * C + lag) drain(dc++);
       const int b = t % NBUF;
-      const uint32_t bcol = L::col(b);
-      const int64_t tstart = p.j0 + static_cast<int64_t>(jt_begin + t) * kTJ;
+      const uint32_t bcol = K::buf_col(b);
+      const int64_t tstart = p.j0 + static_cast<int64_t>(jt_begin + t) * TJ;
       const int64_t dg = valid ? g - tstart : -1;
-      const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < kTJ);
+      const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < TJ);
       mbar_wait(&bar_sfull[b], (t / NBUF) & 1);
       tc_after();
       if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 4 + 1] = clock64();
-      const int dgi = static_cast<int>(dg < 0 || dg >= kTJ ? -1 : dg);
-      if constexpr (BF) {
-        if (!(p.dbg & 16)) {
+      const int dgi = static_cast<int>(dg < 0 || dg >= TJ ? -1 : dg);
+      if (!(p.dbg & 16)) {
+        if constexpr (BF) {
           // both 32-column halves of S are read first; each half is then
           // overwritten in place by [k1 pairs (16 cols) | k2 pairs (16 cols)]
           uint32_t r0[32], r1[32], wds[32];
@@ -564,26 +642,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             tmem_st32(tmem + lanes + bcol + 32 * half, wds);
           }
-        }
-      } else {
-#pragma unroll 1
-        for (int half = 0; half < ((p.dbg & 16) ? 0 : 2); ++half) {
+        } else {
+          // S (32 columns) -> k_hi in place, k_lo in the next 32 columns
           uint32_t r[32], khi[32], klo[32];
           __syncwarp();
-          tmem_ld32(tmem + lanes + bcol + 32 * half, r);
+          tmem_ld32(tmem + lanes + bcol, r);
           tmem_wait_ld();
           if (nomath) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) khi[i] = r[i], klo[i] = 0u;
           } else if (diag_tile) {
-            to_k<true>(r, khi, klo, sf2, ac, dgi - 32 * half);
+            to_k<true>(r, khi, klo, sf2, ac, dgi);
           } else {
-            to_k<false>(r, khi, klo, sf2, ac, dgi - 32 * half);
+            to_k<false>(r, khi, klo, sf2, ac, dgi);
           }
           __syncwarp();
-          // k_hi overwrites the S columns just read; k_lo goes to [64, 128)
-          tmem_st32(tmem + lanes + bcol + 32 * half, khi);
-          tmem_st32(tmem + lanes + bcol + 64 + 32 * half, klo);
+          tmem_st32(tmem + lanes + bcol, khi);
+          tmem_st32(tmem + lanes + bcol + 32, klo);
         }
       }
       tmem_wait_st();
@@ -592,36 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&bar_kfull[b]);
       if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 4 + 2] = clock64();
     }
-    if (T > 0) {
-      mbar_wait(&bar_o, 0);
-      tc_after();
-      const bool diag = g >= p.j0 && g < p.j1;
-      for (int c8 = 8 * w; c8 < spad; c8 += 8 * kEpiGroups) {
-        uint32_t o[8];
-        __syncwarp();
-        tmem_ld8(tmem + lanes + c8, o);
-        tmem_wait_ld();
-        if (!valid) continue;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c = c8 + i;
-          if (c >= p.s) continue;
-          float v = __uint_as_float(o[i]);
-          if (p.splits > 1) {
-            p.part[(static_cast<int64_t>(sp) * spad + c) * p.m_pad + lr] = v;
-            continue;
-          }
-          if (diag) v = fmaf(p.diag, p.V[g + c * p.ldv], v);
-          float* dst = p.out + lr + c * p.ldo;
-          if (p.mode == kHvStore)
-            *dst = v;
-          else if (p.mode == kHvResidual)
-            *dst = p.B[g + c * p.ldb] - v;
-          else
-            *dst -= v;
-        }
-      }
-    }
+    while (dc < nch) drain(dc++);
   }
   tc_before();
   __syncthreads();
@@ -629,14 +675,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarpVProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-// Sum of split partials in fixed order + the same epilogue as the kernel.
+// Sum of the split partials (in fp64, fixed order) + the kernel's row epilogue.
 __global__ void tc_reduce_kernel(const TcArgs p) {
   if (p.done && *p.done) return;
   const int64_t lr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (lr >= p.m) return;
-  float v = 0.f;
-  for (int sp = 0; sp < p.splits; ++sp) v += p.part[(static_cast<int64_t>(sp) * p.s_pad + c) * p.m_pad + lr];
+  double acc = 0.0;
+  for (int sp = 0; sp < p.splits; ++sp)
+    acc += static_cast<double>(p.part[(static_cast<int64_t>(sp) * p.s_pad + c) * p.m_pad + lr]);
+  float v = static_cast<float>(acc);
   const int64_t g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
   if (g >= p.j0 && g < p.j1) v = fmaf(p.diag, p.V[g + c * p.ldv], v);
   float* dst = p.out + lr + c * p.ldo;
@@ -805,8 +853,24 @@ int sm_count() {
 }  // namespace
 
 TcOperands::~TcOperands() {
+  int k = 0;
+  profile_ms(&k);
   if (a_hi) cudaFree(a_hi);
   delete ws;
+}
+
+double TcOperands::profile_ms(int* launches) {
+  double ms = 0.0;
+  for (auto& e : events) {
+    float t = 0.f;
+    if (cudaEventSynchronize(e.second) == cudaSuccess && cudaEventElapsedTime(&t, e.first, e.second) == cudaSuccess)
+      ms += t;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (launches) *launches = static_cast<int>(events.size());
+  events.clear();
+  return ms;
 }
 
 void TcOperands::build(const float* xs, int64_t n_, int dp, int d_, cudaStream_t st) {
@@ -830,8 +894,6 @@ void TcOperands::build(const float* xs, int64_t n_, int dp, int d_, cudaStream_t
   valid = true;
 }
 
-bool hv_tc_supported(int d, int s) { return d + 2 <= kKA && s >= 1 && s <= 128; }
-
 template <bool BF>
 void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorMap& mBhi, const CUtensorMap& mBlo,
                const CUtensorMap& mVhi, const CUtensorMap& mVlo, const TcArgs& a, unsigned grid, int smem,
@@ -844,6 +906,8 @@ void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorM
   hv_tc_kernel<BF><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a);
   WGP_LAUNCH_CHECK();
 }
+
+bool hv_tc_supported(int d, int s) { return d + 2 <= kKA && s >= 1 && s <= 128; }
 
 void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   if (hp.s > 96) {  // the V ring holds at most 96 columns: balanced column chunks
@@ -868,7 +932,8 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   const int spad = static_cast<int>(round_up(s, 16));
   const int64_t nv = hp.j1 - hp.j0;
   const int64_t ldw = round_up(nv, 8);
-  // hi / lo planes of V[j0:j1]: tf32 (fp32 storage) or bf16
+  const int TJ = bf16 ? Cfg<true>::kTJ : Cfg<false>::kTJ;
+  // hi / lo planes of V[j0:j1]: tf32 (fp32 storage) or bf16 v1 = bf16(v), v2 = bf16(v - v1)
   const size_t esz = bf16 ? 2 : 4;
   char* vhi = static_cast<char*>(ws_v.ensure(esz * ldw * s * 2));
   char* vlo = vhi + esz * ldw * s;
@@ -898,19 +963,19 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   }
   const CUtensorMap mAhi = make_map(ahi, kKA, a_rows, kKA * 4, kKA, kTI);
   const CUtensorMap mAlo = make_map(alo, kKA, a_rows, kKA * 4, kKA, kTI);
-  const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, kTJ);
-  const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, kTJ);
+  const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, TJ);
+  const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, TJ);
+  // one TJ-point x s_pad box per plane (128-byte rows: 32 tf32 / 64 bf16 points)
   const CUtensorMapDataType vt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  const uint32_t vbox_pts = bf16 ? 64 : 32;  // 128-byte box rows
-  const CUtensorMap mVhi = make_map(vhi, nv, s, ldw * esz, vbox_pts, spad, vt);
-  const CUtensorMap mVlo = make_map(vlo, nv, s, ldw * esz, vbox_pts, spad, vt);
+  const CUtensorMap mVhi = make_map(vhi, nv, s, ldw * esz, TJ, spad, vt);
+  const CUtensorMap mVlo = make_map(vlo, nv, s, ldw * esz, TJ, spad, vt);
 
   TcArgs a{};
   a.m = hp.m;
   a.a_row0 = a_row0;
   a.j0 = hp.j0;
   a.j1 = hp.j1;
-  a.num_jt = static_cast<int>(ceil_div(nv, kTJ));
+  a.num_jt = static_cast<int>(ceil_div(nv, TJ));
   a.s = s;
   a.s_pad = spad;
   // Ring depths: V tiles are consumed by MMA-2 and must be prefetched far
@@ -924,9 +989,13 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
     const char* e = getenv("WGP_TC_NV");
     return e ? atoi(e) : 0;
   }();
-  a.vstage_bytes = (bf16 ? 2u : 4u) * static_cast<uint32_t>(spad) * 128u;
-  a.nb = env_nb > 0 ? std::min(env_nb, kMaxStages) : (bf16 ? 4 : 2);
-  a.nv = std::min<int>(kMaxStages, (kSmemLimit - 32768 - 1024 - a.nb * 16384) / static_cast<int>(a.vstage_bytes));
+  a.vstage_bytes = 2u * static_cast<uint32_t>(spad) * 128u;
+  // A_I (32 KB) + the running sum R (512 s_pad bytes; aliases A when A lives in TMEM)
+  a.a_region = bf16 ? 32768u + 512u * spad : std::max(32768u, 512u * spad);
+  const int bstage = 2 * TJ * 128;
+  a.nb = env_nb > 0 ? std::min(env_nb, kMaxStages) : (bf16 ? 3 : 4);
+  a.nv = std::min<int>(kMaxStages, (kSmemLimit - static_cast<int>(a.a_region) - 1024 - a.nb * bstage) /
+                                       static_cast<int>(a.vstage_bytes));
   if (env_nv > 0) a.nv = std::min(a.nv, env_nv);
   if (a.nv < 2 || a.nb < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
   a.row_idx = hp.row_idx;
@@ -963,13 +1032,40 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
     return e ? atoi(e) : 0;
   }();
   if (force_splits > 0) a.splits = std::min(force_splits, a.num_jt);
-  if (a.splits > 1) a.part = static_cast<float*>(ws_part.ensure(sizeof(float) * a.splits * spad * m_pad));
-  const int smem = 32768 + 1024 + a.nb * 16384 + a.nv * static_cast<int>(a.vstage_bytes);
+  // fp32 accumulation chunk (tiles): bounds the accumulation error, see the kernel
+  static const int env_chunk = [] {
+    const char* e = getenv("WGP_TC_CHUNK");
+    return e ? atoi(e) : 0;
+  }();
+  a.chunk = env_chunk >= 4 ? env_chunk : 1024 / TJ;
+  static const int env_flush = [] {
+    const char* e = getenv("WGP_TC_FLUSH");
+    return e ? atoi(e) : 0;
+  }();
+  a.flush_every = env_flush >= 1 ? env_flush : 64;
+  const int max_tiles = static_cast<int>(ceil_div(a.num_jt, a.splits));
+  const bool flushes = max_tiles > a.flush_every * a.chunk;
+  const size_t part_bytes = a.splits > 1 ? sizeof(float) * a.splits * spad * m_pad : 0;
+  const size_t flush_bytes = flushes ? sizeof(double) * a.splits * spad * m_pad : 0;
+  char* pw = static_cast<char*>(ws_part.ensure(round_up(part_bytes, 256) + flush_bytes + 256));
+  a.part = reinterpret_cast<float*>(pw);
+  a.flush = reinterpret_cast<double*>(pw + round_up(part_bytes, 256));
+  const int smem = static_cast<int>(a.a_region) + 1024 + a.nb * bstage + a.nv * static_cast<int>(a.vstage_bytes);
   const unsigned grid = static_cast<unsigned>(row_tiles * a.splits);
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (ops.profiling) {
+    WGP_CUDA(cudaEventCreate(&ev0));
+    WGP_CUDA(cudaEventCreate(&ev1));
+    WGP_CUDA(cudaEventRecord(ev0, st));
+  }
   if (bf16)
     launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a, grid, smem, st);
   else
     launch_tc<false>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a, grid, smem, st);
+  if (ops.profiling) {
+    WGP_CUDA(cudaEventRecord(ev1, st));
+    ops.events.emplace_back(ev0, ev1);
+  }
   if (tracing) {
     const int T0 = static_cast<int>(static_cast<int64_t>(a.num_jt) / a.splits);
     std::vector<long long> h(4 * (a.num_jt + 4));

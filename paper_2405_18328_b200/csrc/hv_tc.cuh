@@ -1,8 +1,11 @@
-// hv_tc.cuh — tcgen05 / TMEM / TMA fused H.V (3xTF32), see hv_tc.cu.
+// hv_tc.cuh — tcgen05 / TMEM / TMA fused H.V, see hv_tc.cu.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <utility>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -23,14 +26,19 @@ struct TcOperands {
   void* sq = nullptr;    // [n_pad] fp32 |x|^2 (diagonal fix)
   size_t bytes = 0;
   TcWorkspaces* ws = nullptr;  // per-launch scratch (V planes, gathered rows, split partials)
+  // Kernel timing (wgp_profile): CUDA events around every hv_tc_kernel launch.
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  double profile_ms(int* launches);  // sums and releases the recorded events
   void invalidate() { valid = false; }
   void build(const float* xs, int64_t n, int dp, int d, cudaStream_t st);
   ~TcOperands();
 };
 
 bool hv_tc_supported(int d, int s);
-// bf16 = false: 3xTF32 K.V (~2^-21 per product); true: bf16x3 K.V (kind::f16,
-// half the tensor work, ~2^-17 per product).  The Gram (MMA-1) is 3xTF32 in both.
+// Gram (MMA-1) in 3xTF32; K.V (MMA-2) in 3xTF32 (bf16 = false, ~2^-21 per
+// product) or bf16x3 (bf16 = true, ~2^-17, half the tensor work); fp32
+// accumulation in chunks of 1024 points summed at higher precision.
 void hv_tc(TcOperands& ops, const HvParams& p, cudaStream_t st, bool bf16);
 
 }  // namespace wgp

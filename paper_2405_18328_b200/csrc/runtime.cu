@@ -748,6 +748,11 @@ int guarded(F&& f) {
   }
 }
 
+std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> c{0};
+  return c;
+}
+
 }  // namespace wgp
 
 struct wgp_ctx {
@@ -761,8 +766,10 @@ extern "C" {
 const char* wgp_last_error(void) { return wgp::g_last_error.c_str(); }
 
 const char* wgp_version(void) {
-  return "warmgp_b200 0.1 (sm_100a; tcgen05 3xTF32 H.V + SIMT fp32 kernels; NCCL row sharding)";
+  return "warmgp_b200 0.2 (sm_100a; tcgen05 H.V: 3xTF32 Gram + bf16x3 K.V, fp64 chunk sums; SIMT fp32/fp64 kernel)";
 }
+
+uint64_t wgp_launch_count(void) { return wgp::launch_counter().load(); }
 
 int wgp_device_count(void) {
   int n = 0;
@@ -813,6 +820,21 @@ int wgp_set_hv_impl(wgp_ctx* ctx, int impl) {
     if (impl != WGP_HV_TC && impl != WGP_HV_SIMT && impl != WGP_HV_TC_BF16)
       throw std::invalid_argument("unknown H.V implementation");
     ctx->c.hv_impl = impl;
+  });
+}
+
+int wgp_profile(wgp_ctx* ctx, int enable) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    ctx->c.tc.profiling = enable != 0;
+  });
+}
+
+int wgp_profile_read(wgp_ctx* ctx, double* kernel_ms, int* launches) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("null context");
+    const double ms = ctx->c.tc.profile_ms(launches);
+    if (kernel_ms) *kernel_ms = ms;
   });
 }
 

@@ -156,7 +156,14 @@ __global__ void cg_alpha_kernel(const float* P, const float* HP, int64_t ld, int
   }
 }
 
-__device__ void beta_epilogue(int s, ColState cs, const double* part, SolveCtrl* ctrl) {
+// restart: a refresh step (:119-120).  The reference keeps the direction
+// across the residual replacement (beta = |r_true|^2 / |r_old|^2), harmless
+// in fp64; in fp32, once the recursive residual has fallen below the
+// attainable floor, the true residual jumps by orders of magnitude and the
+// inflated beta derails the iteration (measured: residuals 1e17 at tol 1e-6).
+// So when the replaced residual exceeds 4x the previous one, the direction
+// restarts (beta = 0); at reachable tolerances this does not trigger.
+__device__ void beta_epilogue(int s, ColState cs, const double* part, SolveCtrl* ctrl, bool restart = false) {
   for (int c = threadIdx.x; c < s; c += NT) {
     if (cs.conv[c]) continue;
     const double rs_new = total_of(part, c, s);
@@ -168,7 +175,7 @@ __device__ void beta_epilogue(int s, ColState cs, const double* part, SolveCtrl*
       cs.conv[c] = 2;
       cs.beta[c] = 0.0;
     } else {
-      cs.beta[c] = rs_new / cs.rs[c];
+      cs.beta[c] = (restart && rs_new > 4.0 * cs.rs[c]) ? 0.0 : rs_new / cs.rs[c];
     }
     cs.rs[c] = rs_new;
   }
@@ -223,7 +230,7 @@ __global__ void cg_refresh_norm_kernel(float* R, const float* Rtmp, int64_t ld, 
     deposit(red, c, v);
   }
   if (!publish(red, s, part, ctrl)) return;
-  beta_epilogue(s, cs, part, ctrl);
+  beta_epilogue(s, cs, part, ctrl, true);
 }
 
 __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,

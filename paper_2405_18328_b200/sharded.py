@@ -111,6 +111,8 @@ def sharded_cg(local_hv: Callable[[torch.Tensor], torch.Tensor], B_local: torch.
             raise NumericalError(f"cg_solve: NaN in iterate at iteration {it}")
         newly = active & (torch.sqrt(rs_new) <= tols * bn)
         beta = torch.where(active, rs_new / torch.where(active, rs, torch.ones_like(rs)), torch.zeros_like(rs))
+        if it % 50 == 0:  # fp32 refresh safeguard, as cg_refresh_norm_kernel: restart on a 4x jump
+            beta = torch.where(rs_new > 4.0 * rs, torch.zeros_like(beta), beta)
         P = torch.where(newly[None, :] | conv[None, :], torch.zeros_like(P), R + beta.to(dt)[None, :] * P)
         rs = torch.where(active, rs_new, rs)
         conv = conv | newly

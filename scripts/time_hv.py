@@ -26,11 +26,15 @@ with torch.cuda.stream(st):
     for _ in range(3):
         ctx.hv_device(Vt.data_ptr(), n, s, out.data_ptr(), n)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if impl == "tc":
+        ctx.profile(True)
     a.record(st)
     for _ in range(reps):
         ctx.hv_device(Vt.data_ptr(), n, s, out.data_ptr(), n)
     b.record(st)
     b.synchronize()
 ms = a.elapsed_time(b) / reps
-print(f"impl={impl} n={n} d={d} s={s} dbg={os.environ.get('WGP_TC_DEBUG', '0')} ms={ms:.4f} "
+kms, kl = ctx.profile_read() if impl == "tc" else (ms * reps, reps)
+env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("WGP_TC"))
+print(f"impl={impl} n={n} d={d} s={s} [{env}] ms={ms:.4f} kernel_ms={kms / max(kl, 1):.4f} "
       f"entries/s={n * n / ms * 1e3:.3e}")
