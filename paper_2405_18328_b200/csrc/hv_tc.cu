@@ -45,6 +45,7 @@ constexpr int kThreads = 512;  // 3 epilogue warpgroups + 4 control warps
 constexpr uint32_t kTfMask = 0xFFFFE000u;  // keep sign, exponent, 10 mantissa bits
 constexpr int kSmemLimit = 232448 - 2048;  // 227 KB opt-in minus static smem (barriers)
 constexpr int kMaxStages = 8;              // smem ring depth cap (barrier arrays)
+constexpr int kDoneRing = 8;               // MMA completion rings (>= kMaxStages, NBUF)
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -318,10 +319,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int TJ = K::kTJ;
   if (p.done && *p.done) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bar_bfull[kMaxStages], bar_bempty[kMaxStages], bar_vfull[kMaxStages],
-      bar_vempty[kMaxStages];
-  __shared__ __align__(8) uint64_t bar_a, bar_atm, bar_sfull[NBUF], bar_kfull[NBUF], bar_kempty[NBUF],
-      bar_ofull[2], bar_odrained[2];
+  // m1done[t % 8]: MMA-1(t) complete (S_t ready; B slot of t free);
+  // m2done[t % 8]: MMA-2(t) complete (K buffer and V slot of t free).  One
+  // commit per tile and MMA warp: each commit costs ~175 clk of issue in the
+  // MMA warp (measured), two per tile bounded the loop.  Ring depth 8 >= every
+  // waiter's lag (NB, NV, NBUF <= 8), so no waiter aliases a phase.
+  __shared__ __align__(8) uint64_t bar_bfull[kMaxStages], bar_vfull[kMaxStages], bar_m1done[kDoneRing],
+      bar_m2done[kDoneRing];
+  __shared__ __align__(8) uint64_t bar_a, bar_atm, bar_kfull[NBUF], bar_ofull[2], bar_odrained[2];
   __shared__ uint32_t tmem_slot;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -344,21 +349,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t vbox = static_cast<uint32_t>(spad) * 128u;  // one V plane (128-byte rows)
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NB; ++i) {
-      mbar_init(&bar_bfull[i], 1);
-      mbar_init(&bar_bempty[i], 1);
-    }
-    for (int i = 0; i < NV; ++i) {
-      mbar_init(&bar_vfull[i], 1);
-      mbar_init(&bar_vempty[i], 1);
+    for (int i = 0; i < NB; ++i) mbar_init(&bar_bfull[i], 1);
+    for (int i = 0; i < NV; ++i) mbar_init(&bar_vfull[i], 1);
+    for (int i = 0; i < kDoneRing; ++i) {
+      mbar_init(&bar_m1done[i], 1);
+      mbar_init(&bar_m2done[i], 1);
     }
     mbar_init(&bar_a, 1);
     mbar_init(&bar_atm, 4);
-    for (int i = 0; i < NBUF; ++i) {
-      mbar_init(&bar_sfull[i], 1);
-      mbar_init(&bar_kfull[i], 4);
-      mbar_init(&bar_kempty[i], 1);
-    }
+    for (int i = 0; i < NBUF; ++i) mbar_init(&bar_kfull[i], 4);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar_ofull[i], 1);
       mbar_init(&bar_odrained[i], kEpiWarps);
@@ -381,9 +380,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_expect_tx_warp(&bar_a, 2 * 16384);
       tma_load_2d_warp(sAhi, &mAhi, &bar_a, 0, arow);
       tma_load_2d_warp(sAlo, &mAlo, &bar_a, 0, arow);
-      for (int t = 0; t < T; ++t) {
-        const int st = t % NB;
-        if (t >= NB) mbar_wait(&bar_bempty[st], ((t / NB) - 1) & 1);
+      int st = 0;
+      for (int t = 0; t < T; ++t, st = (st + 1 == NB) ? 0 : st + 1) {
+        if (t >= NB) mbar_wait(&bar_m1done[(t - NB) & (kDoneRing - 1)], ((t - NB) >> 3) & 1);
         uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
         if (p.dbg & 32) {
           mbar_arrive_warp(&bar_bfull[st]);
@@ -400,9 +399,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (separate warp so the two rings never block each other); one box of
     // 128-byte rows (32 tf32 / 64 bf16 points) per plane and tile
     if (T > 0) {
-      for (int t = 0; t < T; ++t) {
-        const int st = t % NV;
-        if (t >= NV) mbar_wait(&bar_vempty[st], ((t / NV) - 1) & 1);
+      // ring slots and phases advance incrementally: runtime divisions by
+      // NV / NB / C cost tens of clk each in these single-warp loops
+      int st = 0;
+      for (int t = 0; t < T; ++t, st = (st + 1 == NV) ? 0 : st + 1) {
+        if (t >= NV) mbar_wait(&bar_m2done[(t - NV) & (kDoneRing - 1)], ((t - NV) >> 3) & 1);
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const int vp = (jt_begin + t) * TJ;
         if (p.dbg & 8) {
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // commits would idle the pipe.  This warp issues MMA-1 (Gram, 3xTF32) and
     // kWarpM2 MMA-2 (K.V); each one's waits overlap the other's MMAs.
     // MMA-1(t) reuses buffer t % NBUF only after MMA-2(t - NBUF) committed
-    // kempty.  The whole warp runs the loop (uniform operands); elect.sync
+    // m2done.  The whole warp runs the loop (uniform operands); elect.sync
     // picks the issuing lane.
     if (T > 0) {
       constexpr uint32_t id1 = idesc_tf32(kTI, TJ);
@@ -432,11 +433,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_after();
       const uint64_t dAhi = umma_desc(sAhi), dAlo = umma_desc(sAlo);
+      int st = 0, b = 0;
+      uint32_t bph = 0;
       for (int t = 0; t < T; ++t) {
-        const int st = t % NB, b = t % NBUF;
-        if (t >= NBUF) mbar_wait(&bar_kempty[b], ((t / NBUF) - 1) & 1);
-        mbar_wait(&bar_bfull[st], (t / NB) & 1);
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 6] = clock64();
+        if (t >= NBUF) mbar_wait(&bar_m2done[(t - NBUF) & (kDoneRing - 1)], ((t - NBUF) >> 3) & 1);
+        mbar_wait(&bar_bfull[st], bph);
         tc_after();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 7] = clock64();
         uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
         const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + K::kBStage / 2);
         const uint32_t d = tmem + K::buf_col(b);
@@ -450,9 +454,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                       k > 0);
           }
         }
-        mma_commit(&bar_sfull[b]);
-        mma_commit(&bar_bempty[st]);
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 0] = clock64();
+        mma_commit(&bar_m1done[t & (kDoneRing - 1)]);
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 0] = clock64();
+        if (++st == NB) st = 0, bph ^= 1u;
+        if (++b == NBUF) b = 0;
       }
     }
   } else if (warp == kWarpM2) {
@@ -460,16 +465,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (T > 0) {
       const uint32_t id2 = BF ? idesc_bf16(kTI, spad) : idesc_tf32(kTI, spad);
       const uint64_t box = vbox >> 4;
+      int b = 0, st = 0, c = 0, tc = 0;
+      uint32_t kph = 0, vph = 0;
       for (int t = 0; t < T; ++t) {
-        const int b = t % NBUF, st = t % NV;
-        const int c = t / C, tc = t - c * C;
         const uint32_t o = tmem + static_cast<uint32_t>(c & 1) * K::kOStride;
         // chunk c reuses O[c & 1] once the epilogue drained chunk c - 2
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 4] = clock64();
         if (tc == 0 && c >= 2) mbar_wait(&bar_odrained[c & 1], ((c >> 1) - 1) & 1);
-        mbar_wait(&bar_vfull[st], (t / NV) & 1);
-        mbar_wait(&bar_kfull[b], (t / NBUF) & 1);
+        mbar_wait(&bar_vfull[st], vph);
+        mbar_wait(&bar_kfull[b], kph);
         tc_after();
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 4 + 3] = clock64();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 3] = clock64();
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const uint32_t kb = tmem + K::buf_col(b);
         const uint64_t dv = umma_desc(base);
@@ -489,9 +495,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        mma_commit(&bar_vempty[st]);
-        mma_commit(&bar_kempty[b]);
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 5] = clock64();
+        mma_commit(&bar_m2done[t & (kDoneRing - 1)]);
         if (tc == C - 1 || t == T - 1) mma_commit(&bar_ofull[c & 1]);
+        if (++st == NV) st = 0, vph ^= 1u;
+        if (++b == NBUF) b = 0, kph ^= 1u;
+        if (++tc == C) tc = 0, ++c;
       }
     }
   } else if (warp < kEpiWarps) {
@@ -612,9 +621,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t tstart = p.j0 + static_cast<int64_t>(jt_begin + t) * TJ;
       const int64_t dg = valid ? g - tstart : -1;
       const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < TJ);
-      mbar_wait(&bar_sfull[b], (t / NBUF) & 1);
+      mbar_wait(&bar_m1done[t & (kDoneRing - 1)], (t >> 3) & 1);
       tc_after();
-      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 4 + 1] = clock64();
+      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 8 + 1] = clock64();
       const int dgi = static_cast<int>(dg < 0 || dg >= TJ ? -1 : dg);
       if (!(p.dbg & 16)) {
         if constexpr (BF) {
@@ -665,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_kfull[b]);
-      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 4 + 2] = clock64();
+      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 8 + 2] = clock64();
     }
     while (dc < nch) drain(dc++);
   }
@@ -1021,8 +1030,8 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   static Workspace ws_trace;
   a.trace = nullptr;
   if (tracing) {
-    a.trace = static_cast<long long*>(ws_trace.ensure(sizeof(long long) * 4 * (a.num_jt + 4)));
-    WGP_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(long long) * 4 * (a.num_jt + 4), st));
+    a.trace = static_cast<long long*>(ws_trace.ensure(sizeof(long long) * 8 * (a.num_jt + 4)));
+    WGP_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(long long) * 8 * (a.num_jt + 4), st));
   }
   const int64_t row_tiles = ceil_div(hp.m, kTI);
   const int64_t key_tiles = hp.split_rows > 0 ? ceil_div(hp.split_rows, kTI) : row_tiles;
@@ -1068,28 +1077,36 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   }
   if (tracing) {
     const int T0 = static_cast<int>(static_cast<int64_t>(a.num_jt) / a.splits);
-    std::vector<long long> h(4 * (a.num_jt + 4));
+    std::vector<long long> h(8 * (a.num_jt + 4));
     WGP_CUDA(cudaMemcpyAsync(h.data(), a.trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
-    // r[0] MMA-1 committed, r[1] epilogue woke (S ready), r[2] epilogue arrived
-    // kfull, r[3] MMA-2 warp passed its waits.  Means over steady-state tiles.
-    double s_wake = 0, s_epi = 0, s_back = 0, s_per2 = 0, s_per1 = 0;
+    // per tile: [0] MMA-1 committed, [1] epilogue woke (S ready), [2] epilogue
+    // arrived kfull, [3] MMA-2 passed its waits, [4] MMA-2 loop top, [5] MMA-2
+    // issued, [6] MMA-1 loop top, [7] MMA-1 passed its waits.  Means over the
+    // steady-state tiles of CTA 0 (clk).
+    double v[10] = {0};
     int cnt = 0;
-    for (int t = 6; t + 1 < T0; ++t) {
-      const long long* r = &h[4 * t];
-      s_wake += r[1] - r[0];
-      s_epi += r[2] - r[1];
-      s_back += r[3] - r[2];
-      s_per2 += h[4 * (t + 1) + 3] - r[3];
-      s_per1 += h[4 * (t + 1) + 0] - r[0];
+    for (int t = 8; t + 2 < T0; ++t) {
+      const long long* r = &h[8 * t];
+      const long long* n = &h[8 * (t + 1)];
+      v[0] += r[1] - r[0];   // S ready -> epilogue wake
+      v[1] += r[2] - r[1];   // epilogue
+      v[2] += r[3] - r[2];   // kfull -> MMA-2 past waits
+      v[3] += n[4] - r[4];   // MMA-2 period
+      v[4] += r[3] - r[4];   // MMA-2 waiting (odrained, vfull, kfull)
+      v[5] += r[5] - r[3];   // MMA-2 issuing
+      v[6] += n[4] - r[5];   // MMA-2 commits + loop
+      v[7] += r[7] - r[6];   // MMA-1 waiting (m2done, bfull)
+      v[8] += r[0] - r[7];   // MMA-1 issuing + commits
+      v[9] += n[6] - r[6];   // MMA-1 period
       ++cnt;
     }
     if (cnt)
       fprintf(stderr,
-              "[hv_tc trace] tiles=%d  S-ready->epi-wake %.0f  epi %.0f  kfull->mma2 %.0f  mma2 period %.0f  "
-              "mma1 period %.0f  mma1-lead %.0f clk\n",
-              cnt, s_wake / cnt, s_epi / cnt, s_back / cnt, s_per2 / cnt, s_per1 / cnt,
-              static_cast<double>(h[4 * (T0 - 2) + 3] - h[4 * (T0 - 2) + 0]));
+              "[hv_tc trace] tiles=%d S->epi %.0f epi %.0f kfull->mma2 %.0f | MMA-2 period %.0f = wait %.0f + "
+              "issue %.0f + commit %.0f | MMA-1 period %.0f: wait %.0f issue+commit %.0f clk\n",
+              cnt, v[0] / cnt, v[1] / cnt, v[2] / cnt, v[3] / cnt, v[4] / cnt, v[5] / cnt, v[6] / cnt, v[9] / cnt,
+              v[7] / cnt, v[8] / cnt);
   }
   if (a.splits > 1) {
     tc_reduce_kernel<<<dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), 256, 0, st>>>(a);
