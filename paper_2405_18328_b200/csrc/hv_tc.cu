@@ -436,11 +436,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int st = 0, b = 0;
       uint32_t bph = 0;
       for (int t = 0; t < T; ++t) {
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 6] = clock64();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 6] = clock64();
         if (t >= NBUF) mbar_wait(&bar_m2done[(t - NBUF) & (kDoneRing - 1)], ((t - NBUF) >> 3) & 1);
         mbar_wait(&bar_bfull[st], bph);
         tc_after();
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 7] = clock64();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 7] = clock64();
         uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
         const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + K::kBStage / 2);
         const uint32_t d = tmem + K::buf_col(b);
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         mma_commit(&bar_m1done[t & (kDoneRing - 1)]);
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 0] = clock64();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 0] = clock64();
         if (++st == NB) st = 0, bph ^= 1u;
         if (++b == NBUF) b = 0;
       }
@@ -470,12 +470,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < T; ++t) {
         const uint32_t o = tmem + static_cast<uint32_t>(c & 1) * K::kOStride;
         // chunk c reuses O[c & 1] once the epilogue drained chunk c - 2
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 4] = clock64();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 4] = clock64();
         if (tc == 0 && c >= 2) mbar_wait(&bar_odrained[c & 1], ((c >> 1) - 1) & 1);
         mbar_wait(&bar_vfull[st], vph);
         mbar_wait(&bar_kfull[b], kph);
         tc_after();
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 3] = clock64();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 3] = clock64();
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const uint32_t kb = tmem + K::buf_col(b);
         const uint64_t dv = umma_desc(base);
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 8 + 5] = clock64();
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 5] = clock64();
         mma_commit(&bar_m2done[t & (kDoneRing - 1)]);
         if (tc == C - 1 || t == T - 1) mma_commit(&bar_ofull[c & 1]);
         if (++st == NV) st = 0, vph ^= 1u;
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < TJ);
       mbar_wait(&bar_m1done[t & (kDoneRing - 1)], (t >> 3) & 1);
       tc_after();
-      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 8 + 1] = clock64();
+      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 16 + 1] = clock64();
       const int dgi = static_cast<int>(dg < 0 || dg >= TJ ? -1 : dg);
       if (!(p.dbg & 16)) {
         if constexpr (BF) {
@@ -674,7 +674,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_kfull[b]);
-      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 8 + 2] = clock64();
+      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 16 + 2] = clock64();
+      if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 8 + q] = clock64();
     }
     while (dc < nch) drain(dc++);
   }
@@ -1030,8 +1031,8 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   static Workspace ws_trace;
   a.trace = nullptr;
   if (tracing) {
-    a.trace = static_cast<long long*>(ws_trace.ensure(sizeof(long long) * 8 * (a.num_jt + 4)));
-    WGP_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(long long) * 8 * (a.num_jt + 4), st));
+    a.trace = static_cast<long long*>(ws_trace.ensure(sizeof(long long) * 16 * (a.num_jt + 4)));
+    WGP_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(long long) * 16 * (a.num_jt + 4), st));
   }
   const int64_t row_tiles = ceil_div(hp.m, kTI);
   const int64_t key_tiles = hp.split_rows > 0 ? ceil_div(hp.split_rows, kTI) : row_tiles;
@@ -1077,18 +1078,19 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   }
   if (tracing) {
     const int T0 = static_cast<int>(static_cast<int64_t>(a.num_jt) / a.splits);
-    std::vector<long long> h(8 * (a.num_jt + 4));
+    std::vector<long long> h(16 * (a.num_jt + 4));
     WGP_CUDA(cudaMemcpyAsync(h.data(), a.trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
     // per tile: [0] MMA-1 committed, [1] epilogue woke (S ready), [2] epilogue
     // arrived kfull, [3] MMA-2 passed its waits, [4] MMA-2 loop top, [5] MMA-2
     // issued, [6] MMA-1 loop top, [7] MMA-1 passed its waits.  Means over the
     // steady-state tiles of CTA 0 (clk).
-    double v[10] = {0};
+    double v[14] = {0};
     int cnt = 0;
     for (int t = 8; t + 2 < T0; ++t) {
-      const long long* r = &h[8 * t];
-      const long long* n = &h[8 * (t + 1)];
+      const long long* r = &h[16 * t];
+      const long long* n = &h[16 * (t + 1)];
+      for (int q = 0; q < 4; ++q) v[10 + q] += r[8 + q] - r[1];  // wake -> kfull arrive, lane quarter q
       v[0] += r[1] - r[0];   // S ready -> epilogue wake
       v[1] += r[2] - r[1];   // epilogue
       v[2] += r[3] - r[2];   // kfull -> MMA-2 past waits
@@ -1107,6 +1109,9 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
               "issue %.0f + commit %.0f | MMA-1 period %.0f: wait %.0f issue+commit %.0f clk\n",
               cnt, v[0] / cnt, v[1] / cnt, v[2] / cnt, v[3] / cnt, v[4] / cnt, v[5] / cnt, v[6] / cnt, v[9] / cnt,
               v[7] / cnt, v[8] / cnt);
+    if (cnt)  // quarter q shares SMSP q with control warp 12 + q (measured: the MMA-warp SMSPs lag)
+      fprintf(stderr, "[hv_tc trace] epilogue per lane quarter (SMSP): %.0f %.0f %.0f %.0f clk\n", v[10] / cnt,
+              v[11] / cnt, v[12] / cnt, v[13] / cnt);
   }
   if (a.splits > 1) {
     tc_reduce_kernel<<<dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), 256, 0, st>>>(a);
