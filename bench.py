@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--hv-impl", default="tc", choices=["tc", "simt"])
+    ap.add_argument("--hv-impl", default="tc", choices=["tc", "tc_bf16", "simt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--outer", action="store_true", help="also time config-2 outer steps")
@@ -130,6 +130,31 @@ def cpu_baseline(p, seconds):
     return {"value": rows * n / elapsed, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
             "sample": f"oracle matrix-free fp64 H.V, rows 0..{rows} of config 1 (x {n} points, "
                       f"s=65), {elapsed:.1f} s"}
+
+
+def outer_steps(wg, datasets, device, args):
+    """BASELINE config 2 outer loop (n=41,157, d=9, 64 pathwise probes + y,
+    1000 RFF features, log-space Adam lr 0.1, warm-started CG at tol 0.01):
+    device time per outer step (solve + gradient + probes, from the library's
+    per-step CUDA events), over `steps` steps after `warmup` steps."""
+    p = datasets.config2()
+    n_steps = args.warmup + max(args.steps, 1)
+    ctx = wg.Context(device, hv_impl=args.hv_impl)
+    ctx.set_data(p.X)
+    cfg = wg.TrainConfig(steps=n_steps, learning_rate=0.1, num_probes=64, mode="warm", seed=0,
+                         transform="log", estimator="pathwise", rff_features=1000, init_noise=0.5,
+                         init_constrained=1.0, warm_start_distance=False,
+                         solver=wg.SolverConfig(kind="cg", tol_mean=0.01, tol_samples=0.01,
+                                                max_iterations=1000))
+    tr = ctx.train(p.y, cfg)
+    timed = tr.steps[args.warmup:]
+    step_ms = [r.step_ms for r in timed]
+    its = [r.solver_iterations for r in timed]
+    ctx.close()
+    return {"workload": "config2 n=41157 d=9 s=65 CG tol 0.01 warm, pathwise RFF 1000, log-space Adam",
+            "ms_per_step": float(np.mean(step_ms)), "solver_ms_per_step": float(np.mean([r.solver_ms for r in timed])),
+            "cg_iterations_mean": float(np.mean(its)), "steps": len(timed), "warmup_steps": args.warmup,
+            "timing": "CUDA events on the context stream around each outer step (device time)"}
 
 
 def run_reference(args):
@@ -224,7 +249,7 @@ def main():
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         launches0 = wg.launch_count()
-        if args.hv_impl == "tc":
+        if args.hv_impl != "simt":
             ctx.profile(True)
         with ClockSampler(local) as clk:
             for a, b in evs:
@@ -234,7 +259,7 @@ def main():
                 b.record(stream)
             stream.synchronize()
     launches = wg.launch_count() - launches0
-    kernel_ms, kernel_launches = ctx.profile_read() if args.hv_impl == "tc" else (0.0, 0)
+    kernel_ms, kernel_launches = ctx.profile_read() if args.hv_impl != "simt" else (0.0, 0)
     ctx.profile(False)
     times = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.mean(times))
@@ -282,21 +307,27 @@ def main():
     clocks = clk.summary()
     f_entry = 2 * d + 2 * s + 8                       # SURVEY §8d F_hv
     flops = f_entry * n * n
-    if args.hv_impl == "tc":
+    if args.hv_impl in ("tc", "tc_bf16"):
         # issued tensor work per entry: 3xTF32 Gram over the 32-wide augmented
-        # rows + bf16x3 K.V over s_pad columns; the epilogue needs one sqrt and
-        # one ex2 per entry on the MUFU (16/clk/SM).  The binding one is the peak.
+        # rows + 3-pass K.V over s_pad columns (3xTF32 for "tc", bf16x3 for
+        # "tc_bf16"); the epilogue needs one sqrt and one ex2 per entry on the
+        # MUFU (16/clk/SM).  The binding resource sets the peak.
         spad = 16 * -(-s // 16)
         p_bf16 = pk["bf16"] * 1e12
         p_tf32 = p_bf16 / 2                            # TF32 = half the bf16 rate
         p_mufu = 16 * 148 * pk["mhz"] * 1e6            # ex2/sqrt per s (nominal)
-        t_tensor = 3 * 2 * 32 / p_tf32 + 3 * 2 * spad / p_bf16
+        p_kv = p_tf32 if args.hv_impl == "tc" else p_bf16
+        t_tensor = 3 * 2 * 32 / p_tf32 + 3 * 2 * spad / p_kv
         t_entry = max(t_tensor, 2 / p_mufu)
         bound = "tensor"
+        basis = (f"max(3xTF32 Gram (K=32) at bf16/2 + 3-pass K.V (N={spad}) at "
+                 f"{'bf16/2' if args.hv_impl == 'tc' else 'bf16'}, 2 MUFU ops at 16/clk/SM) per entry; "
+                 f"{'tensor' if t_tensor >= 2 / p_mufu else 'MUFU'} binds")
     else:
         p_ffma = 2 * 128 * 148 * pk["mhz"] * 1e6
         t_entry = max(f_entry / p_ffma, 2 / (16 * 148 * pk["mhz"] * 1e6))
         bound = "tensor"  # compute (FFMA) bound; contract field admits hbm|tensor only
+        basis = "FFMA 256 flop/clk/SM"
     peak = f_entry / t_entry / 1e12
     achieved = flops / ws / (kernel_ms / 1e3) / 1e12  # this rank's rows per launch
     traffic = None
@@ -319,14 +350,13 @@ def main():
                 "ms_per_step": e2e_ms},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "peak_basis": (f"{pk['src']} peaks: F_hv={f_entry} flop/entry; "
-                                    + ("max(3xTF32 Gram at bf16/2 + bf16x3 K.V at bf16, "
-                                       "2 MUFU ops at 16/clk/SM) per entry; MUFU binds"
-                                       if args.hv_impl == "tc" else "FFMA 256 flop/clk/SM")),
+                     "peak_basis": f"{pk['src']} peaks: F_hv={f_entry} flop/entry; " + basis,
                      "kernel_ms": kernel_ms},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if args.outer:
+        line["outer"] = outer_steps(wg, datasets, local, args)
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(p, args.cpu_seconds)
     print(json.dumps(line), flush=True)

@@ -259,7 +259,8 @@ struct TcArgs {
   int flush_every;   // chunks per fp32 running sum before it is flushed to fp64
   int64_t m_pad;
   const int* done;
-  long long* trace;  // WGP_TC_TRACE: per-tile clock64 stamps of CTA 0 ([T][4])
+  long long* trace;  // WGP_TC_TRACE: per-tile clock64 stamps of CTA 0 ([T][16])
+  long long* ctatime;  // WGP_TC_TRACE: per CTA {smid, globaltimer at start, after the tile loop, at exit}
   int dbg;  // ablation bits (WGP_TC_DEBUG): 1 no epilogue math, 2 no MMA-2, 4 no MMA-1, 8 no V loads,
             // 16 no epilogue TMEM traffic, 32 no B loads, 128 (bf16) FMA-pipe ex2 for odd entries
 };
@@ -267,24 +268,43 @@ struct TcArgs {
 // Two K.V precisions share the pipeline:
 //   BF = false (default, WGP_HV_TC): K.V in 3xTF32 (k_hi v_hi + k_hi v_lo +
 //     k_lo v_hi, ~2^-21 per product), 32-point J tiles.  TMEM: O0 [0, 96),
-//     O1 [96, 192), A_I hi/lo [192, 256) (MMA-1 reads A from TMEM), four
-//     64-column buffers from 256, each holding S (32 fp32 columns) and then,
-//     in place, k_hi | k_lo (32 + 32 columns).
+//     O1 [96, 192), A_I hi/lo [192, 256) (MMA-1 reads A from TMEM), two
+//     128-column groups from 256.  A group serves two tiles: MMA-1 writes
+//     S(t) | S(t+1) (64 fp32 columns, one N = 64 instruction per K step: a
+//     tf32 MMA costs >= 35 clk whatever its size, so N = 32 ran at half the
+//     tensor rate, measured), the epilogue overwrites each S in place with
+//     k_hi and writes k_lo 64 columns further.
 //   BF = true (WGP_HV_TC_BF16): K.V in bf16x3 (k1 v1 + k1 v2 + k2 v1, ~2^-17
 //     per product: half the tensor work, too coarse for tight solver
-//     tolerances), 64-point J tiles.  TMEM: O0, O1, five 64-column buffers
-//     from 192 (S: 64 fp32 columns, overwritten by the packed k1 | k2 pairs);
-//     A_I stays in shared memory (SS MMA-1).
-// The Gram (MMA-1) is 3xTF32 in both.
+//     tolerances), 64-point J tiles.  TMEM: O0, O1, five 64-column groups
+//     from 192 of one tile each (S: 64 fp32 columns, overwritten by the packed
+//     k1 | k2 pairs); A_I stays in shared memory (SS MMA-1).
+// The Gram (MMA-1) is 3xTF32 in both, over 64 points per instruction.
+constexpr bool kTfSingleO = true;
+constexpr int kTfGroups = kTfSingleO ? 3 : 2;
 template <bool BF>
 struct Cfg {
-  static constexpr int kTJ = BF ? 64 : 32;        // points per J tile
-  static constexpr int kBufs = BF ? 5 : 4;
-  static constexpr uint32_t kOStride = 96;
-  static constexpr uint32_t kAhi = 192, kAlo = 224;  // BF = false only
-  static constexpr uint32_t kBufFirst = BF ? 192u : 256u;
-  static constexpr uint32_t kBStage = 2u * kTJ * 128u;  // B_hi | B_lo planes
-  static __device__ __forceinline__ uint32_t buf_col(int b) { return kBufFirst + 64u * static_cast<uint32_t>(b); }
+  static constexpr int kTJ = BF ? 64 : 32;        // points per J tile (MMA-2 K, epilogue)
+  static constexpr int kP = BF ? 1 : 2;           // tiles per MMA-1 group
+  static constexpr int kN1 = kP * kTJ;            // MMA-1 N = points per B stage (64)
+  static constexpr int kGroups = BF ? 5 : kTfGroups;  // MMA-1 groups in flight (TMEM)
+  static constexpr int kTilesInFlight = kP * kGroups;
+  static constexpr uint32_t kGW = BF ? 64u : 128u;  // TMEM columns per group
+  // tf32 layout variant (kTfSingleO): one O accumulator [0, 96) whose chunk
+  // drains stall MMA-2, A_I in shared memory (SS Gram), three groups from 96
+  // (6 tiles in flight); otherwise O0 | O1, A_I in TMEM, two groups from 256.
+  static constexpr bool kATmem = !BF && !kTfSingleO;
+  static constexpr int kOBufs = (BF || !kTfSingleO) ? 2 : 1;
+  static constexpr uint32_t kOStride = kOBufs == 2 ? 96u : 0u;
+  static constexpr uint32_t kAhi = 192, kAlo = 224;  // kATmem only
+  static constexpr uint32_t kBufFirst = BF ? 192u : (kTfSingleO ? 96u : 256u);
+  static constexpr uint32_t kBStage = 2u * kN1 * 128u;  // B_hi | B_lo planes
+  static constexpr uint32_t kLoOff = 64;                // BF = false: k_lo column offset
+  static __device__ __forceinline__ uint32_t grp_col(int gi) { return kBufFirst + kGW * static_cast<uint32_t>(gi); }
+  // TMEM column of tile t's S / k_hi (BF: S / packed k1 | k2)
+  static __device__ __forceinline__ uint32_t tile_col(int t) {
+    return grp_col((t / kP) % kGroups) + 32u * static_cast<uint32_t>(t % kP);
+  }
 };
 
 constexpr int kEpiGroups = 3;
@@ -315,9 +335,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                  const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
                  const TcArgs p) {
   using K = Cfg<BF>;
-  constexpr int NBUF = K::kBufs;
+  constexpr int NBUF = K::kTilesInFlight;  // kfull ring
   constexpr int TJ = K::kTJ;
+  constexpr int P = K::kP;
   if (p.done && *p.done) return;
+  long long gt0 = 0;
+  if (p.ctatime && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // m1done[t % 8]: MMA-1(t) complete (S_t ready; B slot of t free);
   // m2done[t % 8]: MMA-2(t) complete (K buffer and V slot of t free).  One
@@ -334,9 +357,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sAlo = smem + 16384;
   // R: [s_pad][128] fp32 running sum; with A_I in TMEM (BF = false) it reuses
   // A's staging area, which is dead once A has been copied to TMEM.
-  float* sR = reinterpret_cast<float*>(BF ? smem + 32768 : smem);
+  float* sR = reinterpret_cast<float*>(K::kATmem ? smem : smem + 32768);
   uint8_t* sB = smem + p.a_region;                            // nb x [B_hi | B_lo]
   uint8_t* sV = sB + static_cast<size_t>(p.nb) * K::kBStage;  // nv x vstage
+  // [s_pad][128] fp32: V[g_row, c] of this CTA's rows for the exact diagonal
+  // term, prefetched with cp.async at the start (splits == 1 only)
+  float* sVd = reinterpret_cast<float*>(sV + static_cast<size_t>(p.nv) * p.vstage_bytes);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rt = blockIdx.x / p.splits, sp = blockIdx.x % p.splits;
@@ -380,16 +406,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_expect_tx_warp(&bar_a, 2 * 16384);
       tma_load_2d_warp(sAhi, &mAhi, &bar_a, 0, arow);
       tma_load_2d_warp(sAlo, &mAlo, &bar_a, 0, arow);
+      // one stage per MMA-1 group (kN1 = 64 points)
+      const int G = (T + P - 1) / P;
       int st = 0;
-      for (int t = 0; t < T; ++t, st = (st + 1 == NB) ? 0 : st + 1) {
-        if (t >= NB) mbar_wait(&bar_m1done[(t - NB) & (kDoneRing - 1)], ((t - NB) >> 3) & 1);
+      for (int gr = 0; gr < G; ++gr, st = (st + 1 == NB) ? 0 : st + 1) {
+        if (gr >= NB) mbar_wait(&bar_m1done[(gr - NB) & (kDoneRing - 1)], ((gr - NB) >> 3) & 1);
         uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
         if (p.dbg & 32) {
           mbar_arrive_warp(&bar_bfull[st]);
           continue;
         }
         mbar_expect_tx_warp(&bar_bfull[st], K::kBStage);
-        const int pt = static_cast<int>(p.j0) + (jt_begin + t) * TJ;
+        const int pt = static_cast<int>(p.j0) + (jt_begin + gr * P) * TJ;
         tma_load_2d_warp(base, &mBhi, &bar_bfull[st], 0, pt);
         tma_load_2d_warp(base + K::kBStage / 2, &mBlo, &bar_bfull[st], 0, pt);
       }
@@ -425,39 +453,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     // m2done.  The whole warp runs the loop (uniform operands); elect.sync
     // picks the issuing lane.
     if (T > 0) {
-      constexpr uint32_t id1 = idesc_tf32(kTI, TJ);
-      if constexpr (BF) {
+      constexpr uint32_t id1 = idesc_tf32(kTI, K::kN1);
+      if constexpr (!K::kATmem) {
         mbar_wait(&bar_a, 0);
       } else {
         mbar_wait(&bar_atm, 0);  // A_I copied into TMEM by epilogue group 0
       }
       tc_after();
       const uint64_t dAhi = umma_desc(sAhi), dAlo = umma_desc(sAlo);
-      int st = 0, b = 0;
+      const int G = (T + P - 1) / P;
+      int st = 0, gi = 0;
       uint32_t bph = 0;
-      for (int t = 0; t < T; ++t) {
+      for (int gr = 0; gr < G; ++gr) {
+        const int t = gr * P;  // first tile of the group (trace index)
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 6] = clock64();
-        if (t >= NBUF) mbar_wait(&bar_m2done[(t - NBUF) & (kDoneRing - 1)], ((t - NBUF) >> 3) & 1);
+        // the group's columns are free once MMA-2 read the last tile of group gr - kGroups
+        if (gr >= K::kGroups) {
+          const int u = (gr - K::kGroups) * P + P - 1;
+          mbar_wait(&bar_m2done[u & (kDoneRing - 1)], (u >> 3) & 1);
+        }
         mbar_wait(&bar_bfull[st], bph);
         tc_after();
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 7] = clock64();
         uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
         const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + K::kBStage / 2);
-        const uint32_t d = tmem + K::buf_col(b);
+        const uint32_t d = tmem + K::grp_col(gi);
         if (!(p.dbg & 4)) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            if constexpr (BF)
+            if constexpr (!K::kATmem)
               mma3_ss(d, dAhi + 2 * k, dAlo + 2 * k, dBhi + 2 * k, dBlo + 2 * k, id1, k > 0);
             else
               mma3_ts(d, tmem + K::kAhi + 8 * k, tmem + K::kAlo + 8 * k, dBhi + 2 * k, dBlo + 2 * k, id1,
                       k > 0);
           }
         }
-        mma_commit(&bar_m1done[t & (kDoneRing - 1)]);
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 0] = clock64();
+        mma_commit(&bar_m1done[gr & (kDoneRing - 1)]);
+        if (p.trace && blockIdx.x == 0 && lane == 0)
+          for (int h = 0; h < P; ++h) p.trace[(t + h) * 16 + 0] = clock64();
         if (++st == NB) st = 0, bph ^= 1u;
-        if (++b == NBUF) b = 0;
+        if (++gi == K::kGroups) gi = 0;
       }
     }
   } else if (warp == kWarpM2) {
@@ -469,15 +504,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t kph = 0, vph = 0;
       for (int t = 0; t < T; ++t) {
         const uint32_t o = tmem + static_cast<uint32_t>(c & 1) * K::kOStride;
-        // chunk c reuses O[c & 1] once the epilogue drained chunk c - 2
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 4] = clock64();
-        if (tc == 0 && c >= 2) mbar_wait(&bar_odrained[c & 1], ((c >> 1) - 1) & 1);
+        // chunk c reuses its accumulator once the epilogue drained chunk c - kOBufs
+        if (tc == 0 && c >= K::kOBufs) {
+          const int cp = c - K::kOBufs;
+          mbar_wait(&bar_odrained[cp & 1], (cp >> 1) & 1);
+        }
         mbar_wait(&bar_vfull[st], vph);
         mbar_wait(&bar_kfull[b], kph);
         tc_after();
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 3] = clock64();
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
-        const uint32_t kb = tmem + K::buf_col(b);
+        const uint32_t kb = tmem + K::tile_col(t);
         const uint64_t dv = umma_desc(base);
         if (!(p.dbg & 2)) {
 #pragma unroll
@@ -489,8 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma3_ts_bf16(o, kb + c1, kb + c1 + 16, dv + 2 * k, dv + box + 2 * k, id2,
                            (tc > 0 || k > 0) ? 1u : 0u);
             } else {
-              // k_hi in columns [0, 32), k_lo in [32, 64); an 8-point K step is 8 columns
-              mma3_ts(o, kb + 8 * k, kb + 32 + 8 * k, dv + 2 * k, dv + box + 2 * k, id2,
+              // k_hi in the tile's 32 columns, k_lo kLoOff further; an 8-point K step is 8 columns
+              mma3_ts(o, kb + 8 * k, kb + K::kLoOff + 8 * k, dv + 2 * k, dv + box + 2 * k, id2,
                       (tc > 0 || k > 0) ? 1u : 0u);
             }
           }
@@ -498,6 +536,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 5] = clock64();
         mma_commit(&bar_m2done[t & (kDoneRing - 1)]);
         if (tc == C - 1 || t == T - 1) mma_commit(&bar_ofull[c & 1]);
+        if (t == T - 1 && p.ctatime && lane == 0) {
+          long long gt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+          p.ctatime[blockIdx.x * 8 + 6] = gt;  // last MMA-2 issued
+        }
         if (++st == NV) st = 0, vph ^= 1u;
         if (++b == NBUF) b = 0, kph ^= 1u;
         if (++tc == C) tc = 0, ++c;
@@ -505,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    // Warpgroup w handles tiles t = w, w+3, ... (buffer t % NBUF); warp w%4
+    // Warpgroup w handles tiles t = w, w+3, ...; warp w%4
     // of the group reads TMEM lanes 32 (w%4) .. +31 (= its 32 output rows).
     const int ew = warp, q = ew & 3, w = ew >> 2;
     const int row = q * 32 + lane;
@@ -518,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool nomath = p.dbg & 1;
     const int nch = (T + C - 1) / C;
     const bool diag = g >= p.j0 && g < p.j1;
-    if (!BF && w == 0 && T > 0) {
+    if (K::kATmem && w == 0 && T > 0) {
       // Copy this row of A_I (hi, lo: 32 fp32 each) from the 128B-swizzled
       // TMA tile into TMEM: MMA-1 then reads A from TMEM (with A in shared
       // memory MMA-1 is smem-bandwidth bound, 48 clk per MMA, measured).
@@ -551,28 +594,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     double* F = p.flush + static_cast<int64_t>(sp) * spad * p.m_pad + lr;  // column c at F[c * m_pad]
     float* R = sR + row;                                                   // column c at R[c * 128]
     const int FE = p.flush_every;
+    float* Vd = sVd + row;  // column c at Vd[c * 128]
     // Group w owns the contiguous column block [cb, ce) (<= 32 columns,
     // multiples of 8): one TMEM round trip per drain.
     const int cpg = ((spad + 3 * 8 - 1) / (3 * 8)) * 8;
     const int cb = min(spad, w * cpg), ce = min(spad, (w + 1) * cpg);
+    // Intermediate chunk c: R (+)= O[c & 1] (every flush_every chunks R moves
+    // into the fp64 sum F instead); O[c & 1] is released to MMA-2 once read.
     auto drain = [&](int c) {
       mbar_wait(&bar_ofull[c & 1], (c >> 1) & 1);
       tc_after();
       const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
-      const bool last = c == nch - 1;
       const bool fresh = c % FE == 0;  // R starts over with this chunk
-      const bool flush = !last && (c + 1) % FE == 0;
+      const bool flush = (c + 1) % FE == 0;
       uint32_t o[4][8];
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (cb + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + cb + 8 * k, o[k]);
       tmem_wait_ld();
-      if (!last) {  // O[c & 1] is free for chunk c + 2 once read
-        tc_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_odrained[c & 1]);
-      }
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_odrained[c & 1]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (cb + 8 * k >= ce) break;
@@ -580,48 +623,86 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 8; ++i) {
           const int col = cb + 8 * k + i;
           const float r = (fresh ? 0.f : R[col * 128]) + __uint_as_float(o[k][i]);
-          if (!last) {
-            if (flush) {
-              if (valid && col < p.s) {
-                double* f = F + static_cast<int64_t>(col) * p.m_pad;
-                *f = (c + 1 == FE ? 0.0 : *f) + static_cast<double>(r);
-              }
-            } else {
-              R[col * 128] = r;
-            }
-            continue;
+          if (!flush) {
+            R[col * 128] = r;
+          } else if (valid && col < p.s) {
+            double* f = F + static_cast<int64_t>(col) * p.m_pad;
+            *f = (c + 1 == FE ? 0.0 : *f) + static_cast<double>(r);
           }
-          if (!valid || col >= p.s) continue;
-          float v = r;
-          if (c >= FE) v = static_cast<float>(F[static_cast<int64_t>(col) * p.m_pad] + static_cast<double>(r));
-          if (p.splits > 1) {
-            p.part[(static_cast<int64_t>(sp) * spad + col) * p.m_pad + lr] = v;
-            continue;
-          }
-          if (diag) v = fmaf(p.diag, p.V[g + col * p.ldv], v);
-          float* dst = p.out + lr + col * p.ldo;
-          if (p.mode == kHvStore)
-            *dst = v;
-          else if (p.mode == kHvResidual)
-            *dst = p.B[g + col * p.ldb] - v;
-          else
-            *dst -= v;
         }
       }
     };
+    // Last chunk c: this row's outputs -- the exact diagonal term and the
+    // output mode, or the fp32 partial when the J tiles are split across CTAs.
+    // Kept compact and free of dependent global loads on the common path: it
+    // runs once per CTA from a cold instruction cache, and an unrolled version
+    // with per-column global loads cost 8-12 us per CTA (measured).  The
+    // diagonal's V entries come from sVd (cp.async prefetch at the start).
+    auto finish = [&](int c) {
+      mbar_wait(&bar_ofull[c & 1], (c >> 1) & 1);
+      tc_after();
+      if (p.ctatime && threadIdx.x == 0) {
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.ctatime[blockIdx.x * 8 + 4] = gt;  // last ofull observed
+      }
+      const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
+      const bool fresh = c % FE == 0;
+      uint32_t o[4][8];
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (cb + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + cb + 8 * k, o[k]);
+      tmem_wait_ld();
+      if (!valid) return;
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      const int cend = min(ce, p.s);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int col = cb + 8 * k + i;
+          if (col >= cend) continue;
+          float r = (fresh ? 0.f : R[col * 128]) + __uint_as_float(o[k][i]);
+          if (c >= FE) r = static_cast<float>(__ldcg(F + static_cast<int64_t>(col) * p.m_pad) + static_cast<double>(r));
+          if (p.splits > 1) {
+            p.part[(static_cast<int64_t>(sp) * spad + col) * p.m_pad + lr] = r;
+            continue;
+          }
+          if (diag) r = fmaf(p.diag, Vd[col * 128], r);
+          float* dst = p.out + lr + static_cast<int64_t>(col) * p.ldo;
+          if (p.mode == kHvStore)
+            *dst = r;
+          else if (p.mode == kHvResidual)
+            *dst = p.B[g + static_cast<int64_t>(col) * p.ldb] - r;
+          else
+            *dst -= r;
+        }
+      }
+    };
+    // prefetch the diagonal's V entries (overlaps the whole tile loop)
+    if (valid && diag && p.splits == 1) {
+      for (int col = cb; col < ce && col < p.s; ++col)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(Vd + col * 128)),
+                     "l"(p.V + g + static_cast<int64_t>(col) * p.ldv)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     // Chunk dc is drained `lag` tiles after it ended, so its last MMA-2 has
     // retired by then; every group still drains it before MMA-2 reaches
     // chunk dc + 2 (lag + 2 <= C), so MMA-2 never waits for a drain.
-    const int lag = max(2, C / 2);
+    // (single O: drained as soon as possible, MMA-2 waits for it)
+    const int lag = K::kOBufs == 1 ? 0 : max(2, C / 2);
     int dc = 0;  // next chunk to drain
     for (int t = w; t < T; t += kEpiGroups) {
       while (dc < nch - 1 && t >= (dc + 1) * C + lag) drain(dc++);
       const int b = t % NBUF;
-      const uint32_t bcol = K::buf_col(b);
+      const uint32_t bcol = K::tile_col(t);
+      const int gr = t / P;
       const int64_t tstart = p.j0 + static_cast<int64_t>(jt_begin + t) * TJ;
       const int64_t dg = valid ? g - tstart : -1;
       const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < TJ);
-      mbar_wait(&bar_m1done[t & (kDoneRing - 1)], (t >> 3) & 1);
+      mbar_wait(&bar_m1done[gr & (kDoneRing - 1)], (gr >> 3) & 1);
       tc_after();
       if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 16 + 1] = clock64();
       const int dgi = static_cast<int>(dg < 0 || dg >= TJ ? -1 : dg);
@@ -652,7 +733,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st32(tmem + lanes + bcol + 32 * half, wds);
           }
         } else {
-          // S (32 columns) -> k_hi in place, k_lo in the next 32 columns
+          // S (32 columns) -> k_hi in place, k_lo kLoOff columns further
           uint32_t r[32], khi[32], klo[32];
           __syncwarp();
           tmem_ld32(tmem + lanes + bcol, r);
@@ -667,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
           tmem_st32(tmem + lanes + bcol, khi);
-          tmem_st32(tmem + lanes + bcol + 32, klo);
+          tmem_st32(tmem + lanes + bcol + K::kLoOff, klo);
         }
       }
       tmem_wait_st();
@@ -677,11 +758,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 16 + 2] = clock64();
       if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 8 + q] = clock64();
     }
-    while (dc < nch) drain(dc++);
+    if (p.ctatime && threadIdx.x == 0) {
+      long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      p.ctatime[blockIdx.x * 8 + 2] = gt;  // epilogue tile loop done (before the last drain)
+    }
+    while (dc < nch - 1) drain(dc++);
+    if (nch > 0) {
+      finish(dc++);
+      if (p.ctatime && threadIdx.x == 0) {
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.ctatime[blockIdx.x * 8 + 5] = gt;  // final drain done
+      }
+    }
   }
   tc_before();
   __syncthreads();
   tc_after();
+  if (p.ctatime && threadIdx.x == 0) {
+    uint32_t smid;
+    long long gt;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.ctatime[blockIdx.x * 8 + 0] = smid;
+    p.ctatime[blockIdx.x * 8 + 1] = gt0;
+    p.ctatime[blockIdx.x * 8 + 3] = gt;
+  }
   if (warp == kWarpVProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
@@ -810,13 +913,18 @@ CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t 
   return m;
 }
 
+// J-split count: waves x (tiles per CTA + a fixed per-CTA cost of ~16 tile
+// times for the pipeline fill, the final drain and the CTA turnover,
+// measured), plus the split-reduction pass.
 int choose_splits(int64_t row_tiles, int jt, int sms) {
+  constexpr double kCtaOverheadTiles = 16.0;
   int best = 1;
   double best_cost = 1e300;
   for (int sp = 1; sp <= 16; ++sp) {
-    if (sp > 1 && jt / sp < 4) break;
+    if (sp > 1 && jt / sp < 8) break;
     const double waves = std::ceil(static_cast<double>(row_tiles * sp) / sms);
-    const double cost = waves * std::ceil(static_cast<double>(jt) / sp) + (sp > 1 ? 1.0 + 0.25 * sp : 0.0);
+    const double cost = waves * (std::ceil(static_cast<double>(jt) / sp) + kCtaOverheadTiles) +
+                        (sp > 1 ? 4.0 + 0.5 * sp : 0.0);
     if (cost < best_cost - 1e-9) {
       best_cost = cost;
       best = sp;
@@ -973,8 +1081,8 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   }
   const CUtensorMap mAhi = make_map(ahi, kKA, a_rows, kKA * 4, kKA, kTI);
   const CUtensorMap mAlo = make_map(alo, kKA, a_rows, kKA * 4, kKA, kTI);
-  const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, TJ);
-  const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, TJ);
+  const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, 64);  // MMA-1 N = 64 points
+  const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, 64);
   // one TJ-point x s_pad box per plane (128-byte rows: 32 tf32 / 64 bf16 points)
   const CUtensorMapDataType vt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const CUtensorMap mVhi = make_map(vhi, nv, s, ldw * esz, TJ, spad, vt);
@@ -1001,10 +1109,11 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   }();
   a.vstage_bytes = 2u * static_cast<uint32_t>(spad) * 128u;
   // A_I (32 KB) + the running sum R (512 s_pad bytes; aliases A when A lives in TMEM)
-  a.a_region = bf16 ? 32768u + 512u * spad : std::max(32768u, 512u * spad);
-  const int bstage = 2 * TJ * 128;
-  a.nb = env_nb > 0 ? std::min(env_nb, kMaxStages) : (bf16 ? 3 : 4);
-  a.nv = std::min<int>(kMaxStages, (kSmemLimit - static_cast<int>(a.a_region) - 1024 - a.nb * bstage) /
+  const bool a_tmem = bf16 ? Cfg<true>::kATmem : Cfg<false>::kATmem;
+  a.a_region = a_tmem ? std::max(32768u, 512u * spad) : 32768u + 512u * spad;
+  const int bstage = 2 * 64 * 128;
+  a.nb = env_nb > 0 ? std::min(env_nb, kMaxStages) : 3;
+  a.nv = std::min<int>(kMaxStages, (kSmemLimit - static_cast<int>(a.a_region) - 512 * spad - 1024 - a.nb * bstage) /
                                        static_cast<int>(a.vstage_bytes));
   if (env_nv > 0) a.nv = std::min(a.nv, env_nv);
   if (a.nv < 2 || a.nb < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
@@ -1060,8 +1169,12 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   char* pw = static_cast<char*>(ws_part.ensure(round_up(part_bytes, 256) + flush_bytes + 256));
   a.part = reinterpret_cast<float*>(pw);
   a.flush = reinterpret_cast<double*>(pw + round_up(part_bytes, 256));
-  const int smem = static_cast<int>(a.a_region) + 1024 + a.nb * bstage + a.nv * static_cast<int>(a.vstage_bytes);
+  const int smem = static_cast<int>(a.a_region) + 1024 + a.nb * bstage + a.nv * static_cast<int>(a.vstage_bytes) +
+                   512 * spad;  // + sVd
   const unsigned grid = static_cast<unsigned>(row_tiles * a.splits);
+  static Workspace ws_cta;
+  a.ctatime = nullptr;
+  if (tracing) a.ctatime = static_cast<long long*>(ws_cta.ensure(sizeof(long long) * 8 * grid));
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (ops.profiling) {
     WGP_CUDA(cudaEventCreate(&ev0));
@@ -1109,6 +1222,38 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
               "issue %.0f + commit %.0f | MMA-1 period %.0f: wait %.0f issue+commit %.0f clk\n",
               cnt, v[0] / cnt, v[1] / cnt, v[2] / cnt, v[3] / cnt, v[4] / cnt, v[5] / cnt, v[6] / cnt, v[9] / cnt,
               v[7] / cnt, v[8] / cnt);
+    {
+      std::vector<long long> c(8 * grid);
+      WGP_CUDA(cudaMemcpy(c.data(), a.ctatime, sizeof(long long) * c.size(), cudaMemcpyDeviceToHost));
+      long long t0 = c[1], t1 = c[3];
+      double dur = 0, tail = 0, s_m2 = 0, s_of = 0, s_dr = 0, s_ex = 0;
+      for (unsigned b = 0; b < grid; ++b) {
+        t0 = std::min(t0, c[8 * b + 1]);
+        t1 = std::max(t1, c[8 * b + 3]);
+        dur += c[8 * b + 3] - c[8 * b + 1];
+        tail += c[8 * b + 3] - c[8 * b + 2];
+        s_m2 += c[8 * b + 6] - c[8 * b + 2];
+        s_of += c[8 * b + 4] - c[8 * b + 2];
+        s_dr += c[8 * b + 5] - c[8 * b + 4];
+        s_ex += c[8 * b + 3] - c[8 * b + 5];
+      }
+      fprintf(stderr, "[hv_tc trace] tail from epilogue loop end: last MMA-2 issued %+.1f us, ofull seen %.1f, "
+              "final drain %.1f, sync+exit %.1f us\n", s_m2 / grid / 1e3, s_of / grid / 1e3, s_dr / grid / 1e3,
+              s_ex / grid / 1e3);
+      // gaps between consecutive CTAs on one SM
+      std::vector<std::vector<std::pair<long long, long long>>> per_sm(256);
+      for (unsigned b = 0; b < grid; ++b) per_sm[c[8 * b] & 255].push_back({c[8 * b + 1], c[8 * b + 3]});
+      double gap = 0;
+      int ng = 0;
+      for (auto& v : per_sm) {
+        std::sort(v.begin(), v.end());
+        for (size_t i = 1; i < v.size(); ++i) gap += v[i].first - v[i - 1].second, ++ng;
+      }
+      fprintf(stderr,
+              "[hv_tc trace] grid %u: span %.1f us, CTA mean %.1f us (last drain+exit %.1f us), "
+              "SM gap between CTAs %.1f us (%d)\n",
+              grid, (t1 - t0) / 1e3, dur / grid / 1e3, tail / grid / 1e3, ng ? gap / ng / 1e3 : 0.0, ng);
+    }
     if (cnt)  // quarter q shares SMSP q with control warp 12 + q (measured: the MMA-warp SMSPs lag)
       fprintf(stderr, "[hv_tc trace] epilogue per lane quarter (SMSP): %.0f %.0f %.0f %.0f clk\n", v[10] / cnt,
               v[11] / cnt, v[12] / cnt, v[13] / cnt);
