@@ -160,6 +160,7 @@ typedef struct {
   double init_noise;      /* <= 0: init_constrained */
   double init_signal;     /* <= 0: init_constrained */
   int warm_start_distance;/* 1: compute the diagnostic (+1 H.V per warm step) */
+  int exact_gradients;    /* 1: train_exact (optimizer.hpp:83-86): exact Cholesky gradient */
 } wgp_train_cfg;
 
 /* StepRecord fields (proj/include/warmgp/optimizer.hpp:54-67), caller-owned,
@@ -182,6 +183,13 @@ typedef struct {
  *  device-resident previous solutions, gradients, Adam on the host.
  *  Uses the context's data (wgp_set_data); y host n. */
 int wgp_train(wgp_ctx* ctx, const float* y_host, const wgp_train_cfg* cfg, wgp_trace* trace);
+
+/** exact_mll / exact_gradient (proj/src/exact.cpp:25-50) in fp64 on the device
+ *  (dense H, cuSOLVER Cholesky; n <= 20000 = kDenseGuard, exact.hpp:23) for the
+ *  context's data, y host n, raw (d+2) in `transform`'s space.  mll / grad
+ *  (raw-space gradient, d+2) may be NULL; errors as the reference's
+ *  ("...: system matrix is not positive definite", "...: n exceeds the dense guard"). */
+int wgp_exact(wgp_ctx* ctx, int transform, const double* raw, const float* y, double* mll, double* grad);
 
 /** adam_step (proj/src/optimizer.cpp:48-65). */
 int wgp_adam_step(double* raw, const double* grad, double* m, double* v, int p, int t,

@@ -179,9 +179,44 @@ struct OptTrace {
   const StepRecord& back() const { return steps.back(); }
 };
 
+namespace detail {
+inline OptTrace run_loop(b200::Device& dev, const std::vector<float>& X, const std::vector<float>& y,
+                         std::int64_t n, int d, const TrainConfig& c, bool exact_gradients);
+}  // namespace detail
+
 /// train(X, y, config) -- proj/src/optimizer.cpp:175-177.
 inline OptTrace train(b200::Device& dev, const std::vector<float>& X, const std::vector<float>& y,
                       std::int64_t n, int d, const TrainConfig& c) {
+  return detail::run_loop(dev, X, y, n, d, c, false);
+}
+
+/// train_exact(X, y, config) -- proj/src/optimizer.cpp:179-181: the same loop
+/// with the exact Cholesky gradient (fp64 on the device, n <= 20000).
+inline OptTrace train_exact(b200::Device& dev, const std::vector<float>& X, const std::vector<float>& y,
+                            std::int64_t n, int d, const TrainConfig& c) {
+  return detail::run_loop(dev, X, y, n, d, c, true);
+}
+
+/// exact_mll / exact_gradient -- proj/src/exact.cpp:25-50 (raw-space gradient;
+/// `transform` as TrainConfig::transform).
+inline double exact_mll(b200::Device& dev, const std::vector<float>& X, const std::vector<float>& y,
+                        std::int64_t n, int d, const std::vector<double>& raw, int transform = WGP_TRANSFORM_SOFTPLUS) {
+  b200::check(wgp_set_data(dev.get(), X.data(), n, d));
+  double m = 0.0;
+  b200::check(wgp_exact(dev.get(), transform, raw.data(), y.data(), &m, nullptr));
+  return m;
+}
+inline std::vector<double> exact_gradient(b200::Device& dev, const std::vector<float>& X,
+                                          const std::vector<float>& y, std::int64_t n, int d,
+                                          const std::vector<double>& raw, int transform = WGP_TRANSFORM_SOFTPLUS) {
+  b200::check(wgp_set_data(dev.get(), X.data(), n, d));
+  std::vector<double> g(d + 2);
+  b200::check(wgp_exact(dev.get(), transform, raw.data(), y.data(), nullptr, g.data()));
+  return g;
+}
+
+inline OptTrace detail::run_loop(b200::Device& dev, const std::vector<float>& X, const std::vector<float>& y,
+                                 std::int64_t n, int d, const TrainConfig& c, bool exact_gradients) {
   if (static_cast<std::int64_t>(y.size()) != n) throw std::invalid_argument("train: X and y disagree on n");
   b200::check(wgp_set_data(dev.get(), X.data(), n, d));
   const int T = c.steps, p = d + 2, sp = c.num_probes + 1;
@@ -191,7 +226,7 @@ inline OptTrace train(b200::Device& dev, const std::vector<float>& X, const std:
   wgp_train_cfg cfg{c.steps, c.learning_rate, c.adam_beta1, c.adam_beta2, c.adam_eps, c.num_probes,
                     c.probe_distribution, static_cast<int>(c.mode), c.solver.c(), c.init_constrained,
                     c.seed, c.transform, c.estimator, c.rff_features, c.init_noise, c.init_signal,
-                    c.warm_start_distance ? 1 : 0};
+                    c.warm_start_distance ? 1 : 0, exact_gradients ? 1 : 0};
   wgp_trace tr{raw.data(), con.data(), grad.data(), it.data(), pcr.data(), wsd.data(), seeds.data(),
                sms.data(), tms.data(), nullptr};
   b200::check(wgp_train(dev.get(), y.data(), &cfg, &tr));

@@ -21,7 +21,8 @@ __all__ = [
     "NumericalError", "DeviceError", "Context", "Hyperparameters", "SolverConfig", "SolveState",
     "TrainConfig", "StepRecord", "OptTrace", "KernelOperator", "solve", "train",
     "sample_probes", "GradientEstimate", "assemble_gradient_streamed", "warm_start_distance",
-    "adam_step", "derive_seed", "library_path", "load", "device_count",
+    "adam_step", "derive_seed", "library_path", "load", "device_count", "train_exact",
+    "exact_mll", "exact_gradient",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -68,7 +69,8 @@ class _TrainCfg(C.Structure):
                 ("probe_distribution", C.c_int), ("mode", C.c_int), ("solver", _SolverCfg),
                 ("init_constrained", C.c_double), ("seed", C.c_uint64), ("transform", C.c_int),
                 ("estimator", C.c_int), ("rff_features", C.c_int), ("init_noise", C.c_double),
-                ("init_signal", C.c_double), ("warm_start_distance", C.c_int)]
+                ("init_signal", C.c_double), ("warm_start_distance", C.c_int),
+                ("exact_gradients", C.c_int)]
 
 
 class _Trace(C.Structure):
@@ -86,6 +88,7 @@ EXPORTS = [
     "wgp_set_hv_impl", "wgp_stream", "wgp_set_data", "wgp_set_hyper", "wgp_set_rows", "wgp_hv",
     "wgp_hv_device", "wgp_solve", "wgp_grad", "wgp_sample_probes", "wgp_rff_probes", "wgp_train",
     "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
+    "wgp_exact",
 ]
 
 
@@ -126,6 +129,7 @@ def load():
     lib.wgp_sample_probes.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
     lib.wgp_rff_probes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
     lib.wgp_train.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.wgp_exact.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.wgp_adam_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                   C.c_double, C.c_double, C.c_double, C.c_double]
     _lib = lib
@@ -295,6 +299,7 @@ class TrainConfig:
     init_noise: float = 0.0
     init_signal: float = 0.0
     warm_start_distance: bool = True
+    exact_gradients: bool = False  # train_exact (optimizer.hpp:83-86)
 
     def validate(self):
         if self.steps < 1:
@@ -309,7 +314,7 @@ class TrainConfig:
                          _MODES[self.mode], self.solver._c(), self.init_constrained, self.seed,
                          _TRANSFORMS[self.transform], _ESTIMATORS[self.estimator],
                          self.rff_features, self.init_noise, self.init_signal,
-                         int(self.warm_start_distance))
+                         int(self.warm_start_distance), int(self.exact_gradients))
 
 
 @dataclass
@@ -440,6 +445,25 @@ class Context:
                                    _ptr(init) if init is not None else None, s, C.byref(st)))
         return SolveState(sol, res, pcr, [bool(c) for c in conv], st.iterations_used)
 
+    def exact_mll(self, y, raw, transform="softplus"):
+        """exact_mll (exact.cpp:25-36) on the device in fp64 for the context's data."""
+        return self._exact(y, raw, transform, want_grad=False)[0]
+
+    def exact_gradient(self, y, raw, transform="softplus"):
+        """exact_gradient (exact.cpp:38-50): raw-space gradient of the exact MLL."""
+        return self._exact(y, raw, transform, want_grad=True)[1]
+
+    def _exact(self, y, raw, transform, want_grad):
+        y = np.ascontiguousarray(y, dtype=np.float32).ravel()
+        r = np.ascontiguousarray(raw, dtype=np.float64)
+        if r.size != self.d + 2:
+            raise ValueError("Hyperparameters: raw vector must have input_dim + 2 entries")
+        mll = C.c_double(0.0)
+        g = np.zeros(self.d + 2)
+        _check(self._lib.wgp_exact(self._h, _TRANSFORMS[transform], _ptr(r), _ptr(y), C.byref(mll),
+                                   _ptr(g) if want_grad else None))
+        return float(mll.value), g
+
     def grad(self, transform, raw, vy, L, R, coef_b):
         raw = np.ascontiguousarray(raw, dtype=np.float64)
         vy = np.ascontiguousarray(vy, dtype=np.float32)
@@ -513,6 +537,27 @@ def train(X, y, config: TrainConfig, device: int = 0, ctx: Optional[Context] = N
     ctx = ctx or Context(device, hv_impl)
     ctx.set_data(X)
     return ctx.train(y, config)
+
+
+def train_exact(X, y, config: TrainConfig, device: int = 0, ctx: Optional[Context] = None) -> OptTrace:
+    """optimizer.cpp:179-181: the same loop with the exact Cholesky gradient
+    (fp64, dense, on the device; n <= 20000)."""
+    import dataclasses
+    return train(X, y, dataclasses.replace(config, exact_gradients=True), device, ctx)
+
+
+def exact_mll(X, y, hyper: "Hyperparameters", device: int = 0, ctx: Optional[Context] = None) -> float:
+    """exact.cpp:25-36 on the device (fp64)."""
+    ctx = ctx or Context(device)
+    ctx.set_data(_f32(X))
+    return ctx.exact_mll(y, hyper.raw, hyper.transform)
+
+
+def exact_gradient(X, y, hyper: "Hyperparameters", device: int = 0, ctx: Optional[Context] = None) -> np.ndarray:
+    """exact.cpp:38-50 on the device (fp64): raw-space gradient."""
+    ctx = ctx or Context(device)
+    ctx.set_data(_f32(X))
+    return ctx.exact_gradient(y, hyper.raw, hyper.transform)
 
 
 def sample_probes(n: int, s: int, distribution: str = "gaussian", seed: int = 0) -> np.ndarray:

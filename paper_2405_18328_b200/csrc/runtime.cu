@@ -17,6 +17,7 @@
 
 #include "../../include/warmgp_b200.h"
 #include "common.cuh"
+#include "exact.cuh"
 #include "host_rng.hpp"
 #include "hv_tc.cuh"
 #include "kernels.cuh"
@@ -85,6 +86,7 @@ struct Ctx {
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum;
   Buf P, HP, Rtmp, vel, batch, idx, hbuf, Rb, D64, D32, lapack_work, info;
   Buf gpart, gout;
+  Buf hx, hx_ws, exv;  // exact path: dense H (fp64), cuSOLVER workspace, vectors
   Buf io_in, io_out;  // staging for the host-pointer entry points
   PinnedCtrl hctrl;
 
@@ -606,6 +608,71 @@ struct Ctx {
     return softplus_inverse(v);
   }
 
+  // ---------------------------------------------------------------- exact path
+  // exact_mll / exact_gradient (proj/src/exact.cpp:25-50) in fp64 on the device:
+  // dense H (lower triangle), cuSOLVER potrf / potrs / potri, fused derivative
+  // contractions.  grad (raw space, d + 2) may be null (mll only).
+  void exact(int transform, const double* raw, const float* yh, double* mll, double* grad_out) {
+    if (n < 1) throw std::invalid_argument("no training inputs: call wgp_set_data first");
+    const char* who = grad_out ? "exact_gradient" : "exact_mll";
+    if (n > kDenseGuard) throw std::invalid_argument(std::string(who) + ": n exceeds the dense guard");
+    const int p = d + 2;
+    std::vector<double> cons(p);
+    for (int k = 0; k < p; ++k) cons[k] = to_c(transform, raw[k]);
+    const double sfe = cons[d], sge = cons[d + 1];
+    lazy_handles();
+    const int parts = exact_grad_parts();
+    // device vectors: inv_ls [d] | y -> alpha [n] | logdiag [1] | sums [p] | parts [parts x p]
+    const size_t nv = static_cast<size_t>(d) + n + 1 + p + static_cast<size_t>(parts) * p;
+    exv.ensure(sizeof(double) * nv);
+    double* inv_ls = exv.as<double>();
+    double* alpha = inv_ls + d;
+    double* logd = alpha + n;
+    double* sums = logd + 1;
+    double* part = sums + p;
+    std::vector<double> hv(d + n);
+    for (int k = 0; k < d; ++k) hv[k] = 1.0 / cons[k];
+    for (int64_t i = 0; i < n; ++i) hv[d + i] = static_cast<double>(yh[i]);
+    WGP_CUDA(cudaMemcpyAsync(inv_ls, hv.data(), sizeof(double) * (d + n), cudaMemcpyHostToDevice, st));
+    hx.ensure(sizeof(double) * static_cast<size_t>(n) * n);
+    double* H = hx.as<double>();
+    exact_build(X.as<float>(), n, d, inv_ls, sfe * sfe, sge * sge, H, st);
+    const int ni = static_cast<int>(n);
+    int lw1 = 0, lw2 = 0;
+    cusolverDnDpotrf_bufferSize(cusolver, CUBLAS_FILL_MODE_LOWER, ni, H, ni, &lw1);
+    if (grad_out) cusolverDnDpotri_bufferSize(cusolver, CUBLAS_FILL_MODE_LOWER, ni, H, ni, &lw2);
+    hx_ws.ensure(sizeof(double) * std::max(std::max(lw1, lw2), 1) + sizeof(int));
+    int* dinfo = reinterpret_cast<int*>(hx_ws.as<double>() + std::max(std::max(lw1, lw2), 1));
+    cusolverDnDpotrf(cusolver, CUBLAS_FILL_MODE_LOWER, ni, H, ni, hx_ws.as<double>(), std::max(lw1, 1), dinfo);
+    int hinfo = 0;
+    WGP_CUDA(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    if (hinfo != 0) throw NumericalError(std::string(who) + ": system matrix is not positive definite");
+    cusolverDnDpotrs(cusolver, CUBLAS_FILL_MODE_LOWER, ni, 1, H, ni, alpha, ni, dinfo);
+    exact_logdiag(H, n, logd, st);
+    std::vector<double> ha(n + 1);
+    WGP_CUDA(cudaMemcpyAsync(ha.data(), alpha, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    if (mll) {
+      double ya = 0.0;
+      for (int64_t i = 0; i < n; ++i) ya += hv[d + i] * ha[i];
+      *mll = -0.5 * ya - ha[n] - 0.5 * static_cast<double>(n) * 1.8378770664093453;
+    }
+    if (!grad_out) return;
+    cusolverDnDpotri(cusolver, CUBLAS_FILL_MODE_LOWER, ni, H, ni, hx_ws.as<double>(), std::max(lw2, 1), dinfo);
+    WGP_CUDA(cudaMemcpyAsync(&hinfo, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    exact_grad_sums(X.as<float>(), n, d, inv_ls, sfe * sfe, alpha, H, part, parts, sums, st);
+    std::vector<double> acc(p);
+    WGP_CUDA(cudaMemcpyAsync(acc.data(), sums, sizeof(double) * p, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    if (hinfo != 0) throw NumericalError(std::string(who) + ": system matrix is not positive definite");
+    auto chain = [&](double r) { return transform == 1 ? std::exp(r) : softplus_derivative(r); };
+    // dk/dl_k = 3 sf^2 e^{-sqrt3 r} dx_k^2 / l_k^3; dH/dsf = 2 k / sf; dH/dsigma = 2 sigma I
+    for (int k = 0; k < d; ++k) grad_out[k] = 3.0 * sfe * sfe / cons[k] * acc[k] * chain(raw[k]);
+    grad_out[d] = 2.0 / sfe * acc[d] * chain(raw[d]);
+    grad_out[d + 1] = 2.0 * sge * acc[d + 1] * chain(raw[d + 1]);
+  }
+
   void train(const float* yh, const wgp_train_cfg& cfg, wgp_trace* tr) {  // optimizer.cpp:81-171
     if (cfg.steps < 1) throw std::invalid_argument("TrainConfig: steps must be >= 1");
     if (cfg.num_probes < 1) throw std::invalid_argument("TrainConfig: num_probes must be >= 1");
@@ -645,7 +712,7 @@ struct Ctx {
         WGP_CUDA(cudaStreamSynchronize(st));
       }
     };
-    if (fixed) draw(derive_seed(cfg.seed, 1));
+    if (fixed && !cfg.exact_gradients) draw(derive_seed(cfg.seed, 1));  // optimizer.cpp:99
     float* cur = sol0.as<float>();
     float* prev = sol1.as<float>();
     bool have_prev = false;
@@ -659,6 +726,34 @@ struct Ctx {
           std::vector<double> cons(p);
           for (int k = 0; k < p; ++k) cons[k] = to_c(T, raw[k]);
           WGP_CUDA(cudaEventRecord(e0, st));
+          if (cfg.exact_gradients) {  // train_exact: the exact Cholesky gradient (optimizer.cpp:117-118)
+            std::vector<double> g(p);
+            exact(T, raw.data(), yh, nullptr, g.data());
+            WGP_CUDA(cudaEventRecord(e1, st));
+            adam(raw.data(), g.data(), m.data(), v.data(), p, t, cfg.learning_rate, cfg.adam_beta1,
+                 cfg.adam_beta2, cfg.adam_eps);
+            WGP_CUDA(cudaEventRecord(e2, st));
+            WGP_CUDA(cudaEventSynchronize(e2));
+            if (tr) {
+              const size_t off = static_cast<size_t>(t - 1) * p;
+              if (tr->raw_params) std::memcpy(tr->raw_params + off, raw.data(), sizeof(double) * p);
+              if (tr->constrained_params)
+                for (int k = 0; k < p; ++k) tr->constrained_params[off + k] = to_c(T, raw[k]);
+              if (tr->gradient) std::memcpy(tr->gradient + off, g.data(), sizeof(double) * p);
+              if (tr->solver_iterations) tr->solver_iterations[t - 1] = 0;
+              if (tr->per_column_relative_residual)
+                std::fill(tr->per_column_relative_residual + static_cast<size_t>(t - 1) * sp,
+                          tr->per_column_relative_residual + static_cast<size_t>(t) * sp, 0.0);
+              if (tr->warm_start_distance) tr->warm_start_distance[t - 1] = 0.0;
+              if (tr->probe_seed) tr->probe_seed[t - 1] = 0;
+              float ms_a = 0.f, ms_b = 0.f;
+              WGP_CUDA(cudaEventElapsedTime(&ms_a, e0, e1));
+              WGP_CUDA(cudaEventElapsedTime(&ms_b, e0, e2));
+              if (tr->solver_ms) tr->solver_ms[t - 1] = ms_a;
+              if (tr->step_ms) tr->step_ms[t - 1] = ms_b;
+            }
+            continue;
+          }
           set_hyper(cons.data());
           if (!fixed) draw(derive_seed(cfg.seed, static_cast<uint64_t>(t)));
           if (pathwise) rff_eval(rff, Z);
@@ -983,6 +1078,16 @@ int wgp_train(wgp_ctx* ctx, const float* y, const wgp_train_cfg* cfg, wgp_trace*
     WGP_CUDA(cudaSetDevice(ctx->c.device));
     if (ctx->c.n < 1) throw std::invalid_argument("train: dataset is empty");
     ctx->c.train(y, *cfg, trace);
+  });
+}
+
+int wgp_exact(wgp_ctx* ctx, int transform, const double* raw, const float* y, double* mll, double* grad) {
+  return guarded([&] {
+    if (!ctx || !raw || !y) throw std::invalid_argument("wgp_exact: null argument");
+    WGP_CUDA(cudaSetDevice(ctx->c.device));
+    if (transform != WGP_TRANSFORM_SOFTPLUS && transform != WGP_TRANSFORM_LOG)
+      throw std::invalid_argument("unknown hyperparameter transform");
+    ctx->c.exact(transform, raw, y, mll, grad);
   });
 }
 

@@ -40,6 +40,23 @@ int main() {
     for (auto& v : y) v = static_cast<float>(normal(rng));
     const warmgp::OptTrace tr = warmgp::train(dev, X, y, n, d, tc);
     std::printf("train: %zu steps, noise %.4f\n", tr.steps.size(), tr.back().constrained_params[d + 1]);
+    // exact path (proj/src/exact.cpp:25-50): the gradient matches central
+    // differences of the exact MLL (proj/tests/kernel_test.cpp FD checks)
+    const std::vector<double> raw0 = {0.1, -0.2, 0.3, 0.05, -0.4};
+    const std::vector<double> g = warmgp::exact_gradient(dev, X, y, n, d, raw0);
+    for (int k = 0; k < d + 2; ++k) {
+      std::vector<double> rp = raw0, rm = raw0;
+      const double h = 1e-5;
+      rp[k] += h;
+      rm[k] -= h;
+      const double fd = (warmgp::exact_mll(dev, X, y, n, d, rp) - warmgp::exact_mll(dev, X, y, n, d, rm)) / (2 * h);
+      if (std::fabs(fd - g[k]) > 1e-5 * (1.0 + std::fabs(g[k]))) {
+        std::fprintf(stderr, "exact gradient %d: %.10g vs finite difference %.10g\n", k, g[k], fd);
+        return 1;
+      }
+    }
+    const warmgp::OptTrace te = warmgp::train_exact(dev, X, y, n, d, tc);
+    std::printf("train_exact: %zu steps, noise %.4f\n", te.steps.size(), te.back().constrained_params[d + 1]);
     // non-finite inputs are std::invalid_argument (proj/src/solvers.cpp:58-67)
     rhs[0] = NAN;
     try {

@@ -366,3 +366,43 @@ def test_cg_unreachable_tolerance_stays_bounded(ctx):
     assert st.iterations_used == 2000 and not st.all_converged()
     assert np.all(np.isfinite(st.solutions))
     assert max(st.per_column_relative_residual) < 1e-3
+
+
+@pytest.mark.parametrize("transform", ["softplus", "log"])
+@pytest.mark.parametrize("n", [1024, 2048])
+def test_exact_path_matches_oracle(ctx, transform, n):
+    """exact_mll / exact_gradient (exact.cpp:25-50) on the device in fp64
+    against the oracle's dense restatement (same fp32-rounded inputs)."""
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, 5)).astype(np.float32)
+    y = np.sin(X.sum(1)).astype(np.float32)
+    raw = rng.uniform(-0.5, 0.8, 7)
+    ctx.set_data(X)
+    g = ctx.exact_gradient(y, raw, transform)
+    m = ctx.exact_mll(y, raw, transform)
+    go = orc.exact_gradient(X, y, transform, raw)
+    mo = orc.exact_mll(X, y, transform, raw)
+    assert abs(m - mo) <= 1e-9 * abs(mo)
+    assert np.max(np.abs(g - go)) <= 1e-8 * np.max(np.abs(go))
+
+
+def test_train_exact_matches_oracle(ctx):
+    """train_exact (optimizer.cpp:179-181): config-0 generator at n=1024, 5 Adam
+    steps with the exact gradient; trajectories equal to the oracle's to fp64
+    rounding (the oracle's dense inverse bounds the size)."""
+    p = datasets.config0(n=1024)
+    ctx.set_data(p.X)
+    cfg = c0_config(wg, steps=5)
+    cfg.exact_gradients = True
+    g = ctx.train(p.y, cfg)
+    ocfg = c0_config(orc, steps=5)
+    ocfg.exact_gradients = True
+    o = orc.train(p.X, p.y, ocfg)
+    assert max_rel(g, o) <= 1e-9
+    assert all(r.solver_iterations == 0 for r in g.steps)
+
+
+def test_exact_dense_guard(ctx):
+    ctx.set_data(np.zeros((20001, 2), np.float32))
+    with pytest.raises(ValueError, match="dense guard"):
+        ctx.exact_mll(np.zeros(20001, np.float32), np.zeros(4))
