@@ -29,6 +29,9 @@ struct DeviceError : std::runtime_error {
 // Every kernel launch of the library is followed by WGP_LAUNCH_CHECK, which
 // also counts it (wgp_launch_count: bench.py's gpu_launches).
 std::atomic<uint64_t>& launch_counter();
+// Bumped whenever a device workspace is (re)allocated: captured CUDA graphs
+// bake buffer addresses in and are re-captured when this changes.
+std::atomic<uint64_t>& alloc_generation();
 #define WGP_LAUNCH_CHECK()                                                   \
   do {                                                                       \
     ::wgp::launch_counter().fetch_add(1, std::memory_order_relaxed);         \

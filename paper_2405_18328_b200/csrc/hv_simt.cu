@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(NT) hv_simt_kernel(HvParams p) {
   __shared__ int64_t grow_s[TM];
 
   const int tid = threadIdx.x;
+  const float hsf2 = p.hyp ? p.hyp[0] : p.sf2, ha = p.hyp ? p.hyp[1] : p.a, hdiag = p.hyp ? p.hyp[2] : p.diag;
   const int64_t rbase = static_cast<int64_t>(blockIdx.x) * TM;
   for (int r = tid; r < TM; r += NT) {
     const int64_t lr = rbase + r;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(NT) hv_simt_kernel(HvParams p) {
       const bool valid = gj < p.j1;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        const float kv = matern_from_u(sqrt_approx(r2[a][b]), p.sf2, p.a);
+        const float kv = matern_from_u(sqrt_approx(r2[a][b]), hsf2, ha);
         ks[(jj + b) * (TM + 4) + ii + a] = (valid && gj != grow_s[ii + a]) ? kv : 0.f;
       }
     }
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(NT) hv_simt_kernel(HvParams p) {
       const int c = tx + 16 * q;
       if (c >= p.s) continue;
       float v = static_cast<float>(acc[a][q]);
-      if (diag) v = fmaf(p.diag, p.V[g + c * p.ldv], v);
+      if (diag) v = fmaf(hdiag, p.V[g + c * p.ldv], v);
       float* o = p.out + lr + c * p.ldo;
       if (p.mode == kHvStore)
         *o = v;

@@ -254,6 +254,7 @@ struct TcArgs {
   int64_t ldb;
   int mode;
   float sf2, a, diag;
+  const float* hyp;  // device [sf2, a, diag] (overrides the three above when set)
   float* part;       // [splits][s_pad][m_pad] fp32 split partials (splits > 1)
   double* flush;     // [splits][s_pad][m_pad] fp64 running sums (T > flush_every * chunk)
   int flush_every;   // chunks per fp32 running sum before it is flushed to fp64
@@ -557,7 +558,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool valid = lr < p.m;
     int64_t g = -1;
     if (valid) g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
-    const float sf2 = p.sf2, ac = p.a;
+    const float sf2 = p.hyp ? p.hyp[0] : p.sf2, ac = p.hyp ? p.hyp[1] : p.a;
+    const float hdiag = p.hyp ? p.hyp[2] : p.diag;
     const bool nomath = p.dbg & 1;
     const int nch = (T + C - 1) / C;
     const bool diag = g >= p.j0 && g < p.j1;
@@ -669,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.part[(static_cast<int64_t>(sp) * spad + col) * p.m_pad + lr] = r;
             continue;
           }
-          if (diag) r = fmaf(p.diag, Vd[col * 128], r);
+          if (diag) r = fmaf(hdiag, Vd[col * 128], r);
           float* dst = p.out + lr + static_cast<int64_t>(col) * p.ldo;
           if (p.mode == kHvStore)
             *dst = r;
@@ -799,7 +801,7 @@ __global__ void tc_reduce_kernel(const TcArgs p) {
     acc += static_cast<double>(p.part[(static_cast<int64_t>(sp) * p.s_pad + c) * p.m_pad + lr]);
   float v = static_cast<float>(acc);
   const int64_t g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
-  if (g >= p.j0 && g < p.j1) v = fmaf(p.diag, p.V[g + c * p.ldv], v);
+  if (g >= p.j0 && g < p.j1) v = fmaf(p.hyp ? p.hyp[2] : p.diag, p.V[g + c * p.ldv], v);
   float* dst = p.out + lr + c * p.ldo;
   if (p.mode == kHvStore)
     *dst = v;
@@ -944,6 +946,7 @@ struct Workspace {
       p = nullptr;
       WGP_CUDA(cudaMalloc(&p, b));
       bytes = b;
+      alloc_generation().fetch_add(1);
     }
     return p;
   }
@@ -1129,6 +1132,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   a.sf2 = hp.sf2;
   a.a = hp.a;
   a.diag = hp.diag;
+  a.hyp = hp.hyp;
   a.m_pad = m_pad;
   a.done = hp.done;
   static const int dbg = [] {

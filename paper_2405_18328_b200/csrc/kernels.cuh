@@ -41,6 +41,8 @@ struct HvParams {
   float diag;            // sf^2 + sigma^2: the diagonal H_ii, applied in the epilogue
                          // (the streamed sum skips j == row so fp32 accumulation
                          // never carries the dominant diagonal term)
+  const float* hyp;      // optional device [sf2, a, diag] overriding the three fields above
+                         // (lets a captured CUDA graph follow hyperparameter changes)
   const int* done;       // optional device flag: skip the launch body when *done != 0
   int64_t split_rows;    // rows that key the J-split decomposition (0: m).  Row shards
                          // pass the global row count so every shard sums in the same

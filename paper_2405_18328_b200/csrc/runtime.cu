@@ -46,6 +46,7 @@ struct Buf {
     bytes = 0;
     WGP_CUDA(cudaMalloc(&p, b));
     bytes = b;
+    alloc_generation().fetch_add(1);
   }
   template <class T>
   T* as() const {
@@ -86,11 +87,14 @@ struct Ctx {
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum;
   Buf P, HP, Rtmp, vel, batch, idx, hbuf, Rb, D64, D32, lapack_work, info;
   Buf gpart, gout;
+  Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
+  Buf hyper_tmp;  // set_hyper staging (centres, scales)
   Buf hx, hx_ws, exv;  // exact path: dense H (fp64), cuSOLVER workspace, vectors
   Buf io_in, io_out;  // staging for the host-pointer entry points
   PinnedCtrl hctrl;
 
   ~Ctx() {
+    drop_cg_graphs();
     if (cublas) cublasDestroy(cublas);
     if (cusolver) cusolverDnDestroy(cusolver);
     if (st) cudaStreamDestroy(st);
@@ -108,6 +112,7 @@ struct Ctx {
   // ---------------------------------------------------------------- data
   void set_data(const float* Xh, int64_t n_, int d_) {
     if (n_ < 1) throw std::invalid_argument("build_kernel_matrices: need at least one row");
+    drop_cg_graphs();  // n and the leading dimension are baked into captured launches
     if (d_ < 1 || d_ > 64) throw std::invalid_argument("input dimension must lie in [1, 64]");
     for (int64_t e = 0; e < n_ * d_; ++e)
       if (!std::isfinite(Xh[e])) throw std::invalid_argument("build_kernel_matrices: non-finite input");
@@ -142,7 +147,7 @@ struct Ctx {
     sigma = c[d + 1];
     std::vector<double> scale(d);
     for (int k = 0; k < d; ++k) scale[k] = kUScale / ls[k];
-    Buf tmp;
+    Buf& tmp = hyper_tmp;  // persistent: a fresh allocation would invalidate the cached CG graphs
     tmp.ensure(sizeof(double) * 2 * d);
     std::vector<double> h(2 * d);
     std::copy(mu.begin(), mu.end(), h.begin());
@@ -151,6 +156,9 @@ struct Ctx {
     prepare_points(X.as<float>(), n, d, tmp.as<double>(), tmp.as<double>() + d, xs.as<float>(), n_pad,
                    dp, st);
     tc.invalidate();
+    const float hh[4] = {sf2(), a_coef(), static_cast<float>(sf * sf + sigma * sigma), 0.f};
+    dhyp.ensure(sizeof(float) * 4);
+    WGP_CUDA(cudaMemcpyAsync(dhyp.p, hh, sizeof(hh), cudaMemcpyHostToDevice, st));
     WGP_CUDA(cudaStreamSynchronize(st));
     have_hyper = true;
   }
@@ -180,6 +188,7 @@ struct Ctx {
     p.a = a_coef();
     p.noise2 = noise2();
     p.diag = static_cast<float>(sf * sf + sigma * sigma);
+    p.hyp = dhyp.as<float>();
     p.done = done;
     p.split_rows = row_idx ? 0 : n;  // shards of the full operator decompose like the whole
     if ((hv_impl == WGP_HV_TC || hv_impl == WGP_HV_TC_BF16) && hv_tc_supported(d, s)) {
@@ -322,6 +331,29 @@ struct Ctx {
     return out;
   }
 
+  // CG iterations as CUDA graphs: after the first 10 iterations (eager, which
+  // also sizes every workspace) the loop replays a captured 10-iteration chunk
+  // (or its variant whose last iteration is the residual refresh, :111).  At
+  // small n a CG iteration is launch-bound (~150 us eager at config 0 for
+  // ~10 us of GPU work).  Graphs are cached per (B, X, R, s, hv_impl) across
+  // solves -- the H.V kernels read the hyperparameter scalars from device
+  // memory -- and re-captured when any device workspace was reallocated.
+  struct CgGraph {
+    const float* B;
+    float* Xo;
+    float* R;
+    int s, impl;
+    uint64_t gen;
+    cudaGraphExec_t exec[2];
+  };
+  std::vector<CgGraph> cg_graphs;
+  void drop_cg_graphs() {
+    for (auto& g : cg_graphs)
+      for (auto e : g.exec)
+        if (e) cudaGraphExecDestroy(e);
+    cg_graphs.clear();
+  }
+
   void cg(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {
     const int max_it = cfg.max_iterations > 0 ? cfg.max_iterations : static_cast<int>(10 * n);
     reset_ctrl(max_it);
@@ -333,8 +365,60 @@ struct Ctx {
     double* pt = part.as<double>();
     cg_init(Pp, R, ld, n, s, cs, pt, c, st);
     const int* done = &c->done;
+    auto iteration = [&](bool refresh) {
+      hv_all(Pp, s, HPp, kHvStore, nullptr, done);
+      cg_alpha(Pp, HPp, ld, n, s, cs, pt, c, st);
+      if (!refresh) {
+        cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, false, st);
+      } else {
+        cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, true, st);
+        hv_all(Xo, s, Rt, kHvResidual, B, done);
+        cg_refresh_norm(R, Rt, ld, n, s, cs, pt, c, st);
+      }
+      cg_direction(Pp, R, ld, n, s, cs, pt, c, st);
+    };
+    static const bool no_graphs = getenv("WGP_NO_GRAPHS") != nullptr;
+    constexpr int kChunk = 10;
     int launched = 0;
-    int chunk = 2;
+    const int eager[3] = {2, 4, 4};  // first kChunk iterations, polled early
+    for (int e = 0; e < 3; ++e) {
+      const SolveCtrl& h = poll();
+      if (h.done) {
+        if (h.status != kStatusOk) fail(h, 0);
+        out.iterations = h.it;
+        return;
+      }
+      for (int k = 0; k < eager[e]; ++k) iteration(++launched % 50 == 0);
+    }
+    CgGraph* gr = nullptr;
+    if (!no_graphs) {
+      const uint64_t gen = alloc_generation().load();
+      for (auto& g : cg_graphs)
+        if (g.B == B && g.Xo == Xo && g.R == R && g.s == s && g.impl == hv_impl) gr = &g;
+      if (gr && gr->gen != gen) {
+        drop_cg_graphs();
+        gr = nullptr;
+      }
+      if (!gr) {
+        if (cg_graphs.size() >= 8) drop_cg_graphs();
+        CgGraph g{B, Xo, R, s, hv_impl, gen, {nullptr, nullptr}};
+        for (int v = 0; v < 2; ++v) {
+          cudaGraph_t graph;
+          WGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          for (int k = 0; k < kChunk; ++k) iteration(v == 1 && k == kChunk - 1);
+          WGP_CUDA(cudaStreamEndCapture(st, &graph));
+          const cudaError_t ie = cudaGraphInstantiate(&g.exec[v], graph, 0);
+          cudaGraphDestroy(graph);
+          WGP_CUDA(ie);
+        }
+        if (alloc_generation().load() != gen) {  // a workspace moved while capturing
+          for (auto e : g.exec) cudaGraphExecDestroy(e);
+        } else {
+          cg_graphs.push_back(g);
+          gr = &cg_graphs.back();
+        }
+      }
+    }
     while (true) {
       const SolveCtrl& h = poll();
       if (h.done) {
@@ -342,21 +426,13 @@ struct Ctx {
         out.iterations = h.it;
         return;
       }
-      for (int k = 0; k < chunk; ++k) {
-        const int it = ++launched;
-        const bool refresh = it % 50 == 0;  // :111
-        hv_all(Pp, s, HPp, kHvStore, nullptr, done);
-        cg_alpha(Pp, HPp, ld, n, s, cs, pt, c, st);
-        if (!refresh) {
-          cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, false, st);
-        } else {
-          cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, true, st);
-          hv_all(Xo, s, Rt, kHvResidual, B, done);
-          cg_refresh_norm(R, Rt, ld, n, s, cs, pt, c, st);
-        }
-        cg_direction(Pp, R, ld, n, s, cs, pt, c, st);
+      if (gr) {
+        const bool refresh = (launched + kChunk) % 50 == 0;
+        WGP_CUDA(cudaGraphLaunch(gr->exec[refresh ? 1 : 0], st));
+        launched += kChunk;
+      } else {
+        for (int k = 0; k < kChunk; ++k) iteration(++launched % 50 == 0);
       }
-      chunk = std::min(chunk * 2, 8);
     }
   }
 
@@ -844,6 +920,10 @@ int guarded(F&& f) {
 }
 
 std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> c{0};
+  return c;
+}
+std::atomic<uint64_t>& alloc_generation() {
   static std::atomic<uint64_t> c{0};
   return c;
 }

@@ -35,8 +35,14 @@ struct ColState {
   const double* tol;
 };
 
-constexpr int kRowsPerBlock = 2048;
-inline int reduce_blocks(int64_t n) { return static_cast<int>((n + kRowsPerBlock - 1) / kRowsPerBlock); }
+// Rows per CTA of the reduction kernels: 256 (one per thread) up to a grid of
+// ~2 CTAs per SM; the same function on host and device.
+__host__ __device__ inline int64_t rows_per_block(int64_t n) {
+  const int64_t want = (n + 295) / 296;  // 2 x 148 SMs
+  const int64_t r = ((want + 255) / 256) * 256;
+  return r < 256 ? 256 : r;
+}
+inline int reduce_blocks(int64_t n) { return static_cast<int>((n + rows_per_block(n) - 1) / rows_per_block(n)); }
 
 // out[c] = sum_i A[i,c] * B[i,c]  (fp64, fixed order), all columns.
 void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, double* part,
