@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t == T - 1 && p.ctatime && lane == 0) {
           long long gt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-          p.ctatime[blockIdx.x * 8 + 6] = gt;  // last MMA-2 issued
+          p.ctatime[blockIdx.x * 12 + 6] = gt;  // last MMA-2 issued
         }
         if (++st == NV) st = 0, vph ^= 1u;
         if (++b == NBUF) b = 0, kph ^= 1u;
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.ctatime && threadIdx.x == 0) {
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.ctatime[blockIdx.x * 8 + 4] = gt;  // last ofull observed
+        p.ctatime[blockIdx.x * 12 + 4] = gt;  // last ofull observed
       }
       const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
       const bool fresh = c % FE == 0;
@@ -656,30 +656,58 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < 4; ++k)
         if (cb + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + cb + 8 * k, o[k]);
       tmem_wait_ld();
+      if (p.ctatime && threadIdx.x == 0) {
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.ctatime[blockIdx.x * 12 + 7] = gt;  // last accumulator read
+      }
       if (!valid) return;
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      const int cend = min(ce, p.s);
+      // Fold the accumulator into R (one short unrolled block), then a rolled
+      // loop over the row's columns: this code runs once per CTA from a cold
+      // instruction cache, so its length, not its arithmetic, sets its time
+      // (measured: ~4 us for the fully unrolled form, ~40 clk per instruction).
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 4; ++k)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int col = cb + 8 * k + i;
-          if (col >= cend) continue;
-          float r = (fresh ? 0.f : R[col * 128]) + __uint_as_float(o[k][i]);
-          if (c >= FE) r = static_cast<float>(__ldcg(F + static_cast<int64_t>(col) * p.m_pad) + static_cast<double>(r));
-          if (p.splits > 1) {
-            p.part[(static_cast<int64_t>(sp) * spad + col) * p.m_pad + lr] = r;
-            continue;
-          }
-          if (diag) r = fmaf(hdiag, Vd[col * 128], r);
-          float* dst = p.out + lr + static_cast<int64_t>(col) * p.ldo;
-          if (p.mode == kHvStore)
-            *dst = r;
-          else if (p.mode == kHvResidual)
-            *dst = p.B[g + static_cast<int64_t>(col) * p.ldb] - r;
-          else
-            *dst -= r;
+          if (col < ce) R[col * 128] = (fresh ? 0.f : R[col * 128]) + __uint_as_float(o[k][i]);
         }
+      if (p.ctatime && threadIdx.x == 0) {
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.ctatime[blockIdx.x * 12 + 8] = gt;  // folded into R
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      if (p.ctatime && threadIdx.x == 0) {
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        p.ctatime[blockIdx.x * 12 + 9] = gt;  // prefetch complete
+      }
+      const int cend = min(ce, p.s);
+      if (p.splits > 1) {
+        float* part = p.part + static_cast<int64_t>(sp) * spad * p.m_pad + lr;
+#pragma unroll 1
+        for (int col = cb; col < cend; ++col) {
+          float r = R[col * 128];
+          if (c >= FE) r = static_cast<float>(__ldcg(F + static_cast<int64_t>(col) * p.m_pad) + static_cast<double>(r));
+          part[static_cast<int64_t>(col) * p.m_pad] = r;
+        }
+        return;
+      }
+      const float dscale = diag ? hdiag : 0.f;
+#pragma unroll 1
+      for (int col = cb; col < cend; ++col) {
+        float r = R[col * 128];
+        if (c >= FE) r = static_cast<float>(__ldcg(F + static_cast<int64_t>(col) * p.m_pad) + static_cast<double>(r));
+        r = fmaf(dscale, diag ? Vd[col * 128] : 0.f, r);
+        float* dst = p.out + lr + static_cast<int64_t>(col) * p.ldo;
+        if (p.mode == kHvStore)
+          *dst = r;
+        else if (p.mode == kHvResidual)
+          *dst = p.B[g + static_cast<int64_t>(col) * p.ldb] - r;
+        else
+          *dst -= r;
       }
     };
     // prefetch the diagonal's V entries (overlaps the whole tile loop)
@@ -763,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.ctatime && threadIdx.x == 0) {
       long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      p.ctatime[blockIdx.x * 8 + 2] = gt;  // epilogue tile loop done (before the last drain)
+      p.ctatime[blockIdx.x * 12 + 2] = gt;  // epilogue tile loop done (before the last drain)
     }
     while (dc < nch - 1) drain(dc++);
     if (nch > 0) {
@@ -771,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.ctatime && threadIdx.x == 0) {
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.ctatime[blockIdx.x * 8 + 5] = gt;  // final drain done
+        p.ctatime[blockIdx.x * 12 + 5] = gt;  // final drain done
       }
     }
   }
@@ -783,9 +811,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long gt;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.ctatime[blockIdx.x * 8 + 0] = smid;
-    p.ctatime[blockIdx.x * 8 + 1] = gt0;
-    p.ctatime[blockIdx.x * 8 + 3] = gt;
+    p.ctatime[blockIdx.x * 12 + 0] = smid;
+    p.ctatime[blockIdx.x * 12 + 1] = gt0;
+    p.ctatime[blockIdx.x * 12 + 3] = gt;
   }
   if (warp == kWarpVProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
@@ -1178,7 +1206,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   const unsigned grid = static_cast<unsigned>(row_tiles * a.splits);
   static Workspace ws_cta;
   a.ctatime = nullptr;
-  if (tracing) a.ctatime = static_cast<long long*>(ws_cta.ensure(sizeof(long long) * 8 * grid));
+  if (tracing) a.ctatime = static_cast<long long*>(ws_cta.ensure(sizeof(long long) * 12 * grid));
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (ops.profiling) {
     WGP_CUDA(cudaEventCreate(&ev0));
@@ -1227,26 +1255,30 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
               cnt, v[0] / cnt, v[1] / cnt, v[2] / cnt, v[3] / cnt, v[4] / cnt, v[5] / cnt, v[6] / cnt, v[9] / cnt,
               v[7] / cnt, v[8] / cnt);
     {
-      std::vector<long long> c(8 * grid);
+      std::vector<long long> c(12 * grid);
       WGP_CUDA(cudaMemcpy(c.data(), a.ctatime, sizeof(long long) * c.size(), cudaMemcpyDeviceToHost));
       long long t0 = c[1], t1 = c[3];
-      double dur = 0, tail = 0, s_m2 = 0, s_of = 0, s_dr = 0, s_ex = 0;
+      double dur = 0, tail = 0, s_m2 = 0, s_of = 0, s_dr = 0, s_ex = 0, s_tl = 0, s_fo = 0, s_cw = 0;
       for (unsigned b = 0; b < grid; ++b) {
-        t0 = std::min(t0, c[8 * b + 1]);
-        t1 = std::max(t1, c[8 * b + 3]);
-        dur += c[8 * b + 3] - c[8 * b + 1];
-        tail += c[8 * b + 3] - c[8 * b + 2];
-        s_m2 += c[8 * b + 6] - c[8 * b + 2];
-        s_of += c[8 * b + 4] - c[8 * b + 2];
-        s_dr += c[8 * b + 5] - c[8 * b + 4];
-        s_ex += c[8 * b + 3] - c[8 * b + 5];
+        t0 = std::min(t0, c[12 * b + 1]);
+        t1 = std::max(t1, c[12 * b + 3]);
+        dur += c[12 * b + 3] - c[12 * b + 1];
+        tail += c[12 * b + 3] - c[12 * b + 2];
+        s_m2 += c[12 * b + 6] - c[12 * b + 2];
+        s_of += c[12 * b + 4] - c[12 * b + 2];
+        s_dr += c[12 * b + 5] - c[12 * b + 4];
+        s_tl += c[12 * b + 7] - c[12 * b + 4];
+        s_fo += c[12 * b + 8] - c[12 * b + 7];
+        s_cw += c[12 * b + 9] - c[12 * b + 8];
+        s_ex += c[12 * b + 3] - c[12 * b + 5];
       }
       fprintf(stderr, "[hv_tc trace] tail from epilogue loop end: last MMA-2 issued %+.1f us, ofull seen %.1f, "
-              "final drain %.1f, sync+exit %.1f us\n", s_m2 / grid / 1e3, s_of / grid / 1e3, s_dr / grid / 1e3,
-              s_ex / grid / 1e3);
+              "final drain %.1f (TMEM read %.1f, fold %.1f, cp.async wait %.1f), sync+exit %.1f us\n",
+              s_m2 / grid / 1e3, s_of / grid / 1e3, s_dr / grid / 1e3, s_tl / grid / 1e3, s_fo / grid / 1e3,
+              s_cw / grid / 1e3, s_ex / grid / 1e3);
       // gaps between consecutive CTAs on one SM
       std::vector<std::vector<std::pair<long long, long long>>> per_sm(256);
-      for (unsigned b = 0; b < grid; ++b) per_sm[c[8 * b] & 255].push_back({c[8 * b + 1], c[8 * b + 3]});
+      for (unsigned b = 0; b < grid; ++b) per_sm[c[8 * b] & 255].push_back({c[12 * b + 1], c[12 * b + 3]});
       double gap = 0;
       int ng = 0;
       for (auto& v : per_sm) {
