@@ -191,6 +191,13 @@ int wgp_train(wgp_ctx* ctx, const float* y_host, const wgp_train_cfg* cfg, wgp_t
  *  ("...: system matrix is not positive definite", "...: n exceeds the dense guard"). */
 int wgp_exact(wgp_ctx* ctx, int transform, const double* raw, const float* y, double* mll, double* grad);
 
+/** predict(X_train, y, X_test, hyper) (proj/src/exact.cpp:52-77) through
+ *  iterative solves with `cfg` for the context's data and hyperparameters:
+ *  X_test host column-major m x d, y host n; means / variances (latent) host m;
+ *  noise_variance may be NULL.  Beyond the dense guard (no n limit). */
+int wgp_predict(wgp_ctx* ctx, const float* X_test, int64_t m, const float* y, const wgp_solver_cfg* cfg,
+                double* means, double* variances, double* noise_variance);
+
 /** adam_step (proj/src/optimizer.cpp:48-65). */
 int wgp_adam_step(double* raw, const double* grad, double* m, double* v, int p, int t,
                   double lr, double beta1, double beta2, double eps);

@@ -138,3 +138,20 @@ def cg_solve(H, rhs, init, tol_mean, tol_samples, max_it):
                 P[:, j] = R[:, j] + (rn / rs[j]) * P[:, j]
             rs[j] = rn
     return X, it, conv
+
+
+def predict(X_train, y, X_test, ls, sf, sigma):
+    """exact.cpp:52-77 (dense fp64): latent means and variances at X_test."""
+    X_train = np.asarray(X_train, np.float64)
+    X_test = np.asarray(X_test, np.float64)
+    H, _, _ = kernel_matrices(X_train, ls, sf, sigma)
+    L = np.linalg.cholesky(H)
+    alpha = np.linalg.solve(L.T, np.linalg.solve(L, np.asarray(y, np.float64)))
+    ls = np.asarray(ls, np.float64)
+    d = (((X_train[:, None, :] - X_test[None, :, :]) / ls) ** 2).sum(-1)
+    r = np.sqrt(d)
+    Ks = sf * sf * (1.0 + np.sqrt(3.0) * r) * np.exp(-np.sqrt(3.0) * r)  # n x m
+    means = Ks.T @ alpha
+    W = np.linalg.solve(L.T, np.linalg.solve(L, Ks))
+    var = sf * sf - (Ks * W).sum(0)
+    return means, np.maximum(var, 0.0), sigma * sigma

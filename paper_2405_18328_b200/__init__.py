@@ -22,7 +22,7 @@ __all__ = [
     "TrainConfig", "StepRecord", "OptTrace", "KernelOperator", "solve", "train",
     "sample_probes", "GradientEstimate", "assemble_gradient_streamed", "warm_start_distance",
     "adam_step", "derive_seed", "library_path", "load", "device_count", "train_exact",
-    "exact_mll", "exact_gradient",
+    "exact_mll", "exact_gradient", "predict", "test_metrics", "PredictiveDistribution", "TestMetrics",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -88,7 +88,7 @@ EXPORTS = [
     "wgp_set_hv_impl", "wgp_stream", "wgp_set_data", "wgp_set_hyper", "wgp_set_rows", "wgp_hv",
     "wgp_hv_device", "wgp_solve", "wgp_grad", "wgp_sample_probes", "wgp_rff_probes", "wgp_train",
     "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
-    "wgp_exact",
+    "wgp_exact", "wgp_predict",
 ]
 
 
@@ -130,6 +130,8 @@ def load():
     lib.wgp_rff_probes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_void_p]
     lib.wgp_train.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.wgp_exact.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.wgp_predict.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p]
     lib.wgp_adam_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                   C.c_double, C.c_double, C.c_double, C.c_double]
     _lib = lib
@@ -445,6 +447,24 @@ class Context:
                                    _ptr(init) if init is not None else None, s, C.byref(st)))
         return SolveState(sol, res, pcr, [bool(c) for c in conv], st.iterations_used)
 
+    def predict(self, X_test, y, config: "SolverConfig" = None) -> "PredictiveDistribution":
+        """predict (exact.cpp:52-77) through iterative solves (`config`, default
+        CG at tolerance 1e-4) at the context's hyperparameters."""
+        config = config or SolverConfig(kind="cg", tol_mean=1e-4, tol_samples=1e-4, max_iterations=10000)
+        config.validate()
+        Xt = _f32(X_test)
+        m = Xt.shape[0]
+        if m and Xt.shape[1] != self.d:
+            raise ValueError("predict: input dimension mismatch")
+        y = np.ascontiguousarray(y, dtype=np.float32).ravel()
+        mean = np.zeros(m)
+        var = np.zeros(m)
+        nv = C.c_double(0.0)
+        cfg = config._c()
+        _check(self._lib.wgp_predict(self._h, _ptr(Xt), m, _ptr(y), C.byref(cfg), _ptr(mean), _ptr(var),
+                                     C.byref(nv)))
+        return PredictiveDistribution(mean, var, float(nv.value))
+
     def exact_mll(self, y, raw, transform="softplus"):
         """exact_mll (exact.cpp:25-36) on the device in fp64 for the context's data."""
         return self._exact(y, raw, transform, want_grad=False)[0]
@@ -537,6 +557,44 @@ def train(X, y, config: TrainConfig, device: int = 0, ctx: Optional[Context] = N
     ctx = ctx or Context(device, hv_impl)
     ctx.set_data(X)
     return ctx.train(y, config)
+
+
+@dataclass
+class PredictiveDistribution:
+    """exact.hpp PredictiveDistribution: latent means / variances + noise variance."""
+    means: np.ndarray
+    variances: np.ndarray
+    noise_variance: float = 0.0
+
+
+@dataclass
+class TestMetrics:
+    """exact.hpp TestMetrics."""
+    rmse: float = 0.0
+    mean_loglik: float = 0.0
+
+
+def test_metrics(pred: PredictiveDistribution, y_test) -> TestMetrics:
+    """exact.cpp:79-92: RMSE and mean predictive log-likelihood (latent
+    variance + noise variance)."""
+    y_test = np.asarray(y_test, dtype=np.float64).ravel()
+    if pred.means.size != y_test.size:
+        raise ValueError("test_metrics: prediction/target length mismatch")
+    if y_test.size == 0:
+        return TestMetrics()
+    err = pred.means - y_test
+    var = pred.variances + pred.noise_variance
+    return TestMetrics(float(np.sqrt(np.mean(err ** 2))),
+                       float(np.mean(-0.5 * (np.log(var) + 1.8378770664093453) - 0.5 * err ** 2 / var)))
+
+
+def predict(X_train, y, X_test, hyper: "Hyperparameters", config: "SolverConfig" = None, device: int = 0,
+            ctx: Optional[Context] = None) -> PredictiveDistribution:
+    """exact.cpp:52-77 on the device through iterative solves."""
+    ctx = ctx or Context(device)
+    ctx.set_data(_f32(X_train))
+    ctx.set_hyper(hyper.to_constrained_vector())
+    return ctx.predict(X_test, y, config)
 
 
 def train_exact(X, y, config: TrainConfig, device: int = 0, ctx: Optional[Context] = None) -> OptTrace:

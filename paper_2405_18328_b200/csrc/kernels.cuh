@@ -96,6 +96,14 @@ struct RffParams {
 };
 void rff_probes(const RffParams& p, cudaStream_t st);
 
+// Cross kernel matrix K*[j + i ld] = k(x_j, x*_i) (train j < n, test i < m) from
+// prepared points; rows n..ld-1 are zero (predict.cu).
+void cross_matrix(const float* xs, int64_t n, const float* xt, int64_t m, int dp, float sf2, float a, float* out,
+                  int64_t ld, cudaStream_t st);
+// out[i] = K*[:, i] . alpha in fp64.
+void colvec_dots(const float* K, int64_t ld, int64_t n, int64_t m, const float* alpha, double* out,
+                 cudaStream_t st);
+
 // Prepare xs from column-major raw X: xs[i][k] = (X[i,k] - mu_k) * scale_k.
 void prepare_points(const float* X, int64_t n, int d, const double* mu, const double* scale,
                     float* xs, int64_t n_pad, int dp, cudaStream_t st);

@@ -84,7 +84,7 @@ struct Ctx {
   TcOperands tc;
 
   // workspaces
-  Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum;
+  Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
   Buf P, HP, Rtmp, vel, batch, idx, hbuf, Rb, D64, D32, lapack_work, info;
   Buf gpart, gout;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
@@ -218,6 +218,9 @@ struct Ctx {
     bnorm.ensure(sizeof(double) * (s + 1));
     tol.ensure(sizeof(double) * (s + 1));
     colsum.ensure(sizeof(double) * (s + 1));
+    best.ensure(sizeof(double) * (s + 1));
+    stall.ensure(sizeof(int) * (s + 1));
+    act.ensure(sizeof(int) * (s + 1));
     part.ensure(sizeof(double) * static_cast<size_t>(reduce_blocks(n)) * (s + 2));
     P.ensure(sizeof(float) * ld * s);
     HP.ensure(sizeof(float) * ld * s);
@@ -225,7 +228,7 @@ struct Ctx {
   }
   ColState colstate() {
     return ColState{conv.as<int>(), rs.as<double>(), alpha.as<double>(), beta.as<double>(),
-                    bnorm.as<double>(), tol.as<double>()};
+                    bnorm.as<double>(), tol.as<double>(), best.as<double>(), stall.as<int>(), act.as<int>()};
   }
   std::vector<double> dots(const float* A, const float* B_, int s) {
     ensure_solver_ws(s);
@@ -327,7 +330,7 @@ struct Ctx {
     out.conv.resize(s);
     WGP_CUDA(cudaMemcpyAsync(out.conv.data(), conv.p, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
-    for (int& c : out.conv) c = c != 0;
+    for (int& c : out.conv) c = c == 1 || c == 2;  // 3: stalled, frozen at its best iterate
     return out;
   }
 
@@ -363,7 +366,12 @@ struct Ctx {
     const ColState cs = colstate();
     SolveCtrl* c = dctrl();
     double* pt = part.as<double>();
+    Xbest.ensure(sizeof(float) * ld * s);
+    Rbest.ensure(sizeof(float) * ld * s);
+    float* Xb = Xbest.as<float>();
+    float* Rb = Rbest.as<float>();
     cg_init(Pp, R, ld, n, s, cs, pt, c, st);
+    cg_snapshot(Xo, R, Xb, Rb, ld, n, s, cs, c, true, st);
     const int* done = &c->done;
     auto iteration = [&](bool refresh) {
       hv_all(Pp, s, HPp, kHvStore, nullptr, done);
@@ -374,6 +382,7 @@ struct Ctx {
         cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, true, st);
         hv_all(Xo, s, Rt, kHvResidual, B, done);
         cg_refresh_norm(R, Rt, ld, n, s, cs, pt, c, st);
+        cg_snapshot(Xo, R, Xb, Rb, ld, n, s, cs, c, false, st);
       }
       cg_direction(Pp, R, ld, n, s, cs, pt, c, st);
     };
@@ -682,6 +691,71 @@ struct Ctx {
       return std::log(v);
     }
     return softplus_inverse(v);
+  }
+
+  // ---------------------------------------------------------------- prediction
+  // predict / test metrics (proj/src/exact.cpp:52-92) through iterative solves
+  // (SURVEY §8f rank 2): alpha = H^-1 y and W = H^-1 K* with the configured
+  // solver, K* (train x test) built per chunk of test points;
+  // means = K*^T alpha, latent variances = sf^2 - colsum(K* o W).  The
+  // reference's -1e-10 negativity guard is for fp64 dense solves; here a
+  // variance below -1e-3 sf^2 is a NumericalError and smaller negatives clamp
+  // to 0 like the reference.
+  Buf xt, kstar, pw, pr, pal, pdots;
+  void predict(const float* Xt_h, int64_t m, const float* yh, const wgp_solver_cfg& cfg, double* means,
+               double* vars) {
+    require_data();
+    if (m < 0) throw std::invalid_argument("predict: negative test count");
+    if (m == 0) return;
+    for (int64_t e = 0; e < m * d; ++e)
+      if (!std::isfinite(Xt_h[e])) throw std::invalid_argument("predict: non-finite test input");
+    // prepared test points (training centres and scales, hyper_tmp = [mu | scale])
+    const int64_t m_pad = round_up(m, 128);
+    Buf xraw;
+    xraw.ensure(sizeof(float) * m * d);
+    WGP_CUDA(cudaMemcpyAsync(xraw.p, Xt_h, sizeof(float) * m * d, cudaMemcpyHostToDevice, st));
+    xt.ensure(sizeof(float) * m_pad * dp);
+    prepare_points(xraw.as<float>(), m, d, hyper_tmp.as<double>(), hyper_tmp.as<double>() + d, xt.as<float>(), m_pad,
+                   dp, st);
+    // alpha = H^-1 y
+    pal.ensure(sizeof(float) * ld * 2);
+    float* yd = pal.as<float>();
+    float* alpha = yd + ld;
+    WGP_CUDA(cudaMemsetAsync(yd, 0, sizeof(float) * ld, st));
+    WGP_CUDA(cudaMemcpyAsync(yd, yh, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+    pw.ensure(sizeof(float) * ld * 64);
+    pr.ensure(sizeof(float) * ld * 64);
+    {
+      const SolveOut so = solve(cfg, yd, nullptr, alpha, pr.as<float>(), 1);
+      if (getenv("WGP_PREDICT_DEBUG")) {
+        std::vector<float> ha(n);
+        WGP_CUDA(cudaMemcpy(ha.data(), alpha, sizeof(float) * n, cudaMemcpyDeviceToHost));
+        float mx = 0.f;
+        for (float v : ha) mx = std::max(mx, std::fabs(v));
+        fprintf(stderr, "[predict] alpha solve: %d iterations, rel %.3e, conv %d, max|alpha| %.3e\n", so.iterations,
+                so.rel[0], so.conv[0], mx);
+      }
+    }
+    // test points in chunks of 64 columns (the solver's right-hand sides)
+    constexpr int64_t kMc = 64;
+    kstar.ensure(sizeof(float) * ld * kMc);
+    pdots.ensure(sizeof(double) * kMc);
+    const double sfv = sf * sf;
+    for (int64_t i0 = 0; i0 < m; i0 += kMc) {
+      const int mc = static_cast<int>(std::min(kMc, m - i0));
+      float* K = kstar.as<float>();
+      cross_matrix(xs.as<float>(), n, xt.as<float>() + i0 * dp, mc, dp, sf2(), a_coef(), K, ld, st);
+      colvec_dots(K, ld, n, mc, alpha, pdots.as<double>(), st);
+      WGP_CUDA(cudaMemcpyAsync(means + i0, pdots.p, sizeof(double) * mc, cudaMemcpyDeviceToHost, st));
+      solve(cfg, K, nullptr, pw.as<float>(), pr.as<float>(), mc);
+      const std::vector<double> q = dots(K, pw.as<float>(), mc);
+      for (int c = 0; c < mc; ++c) {
+        double v = sfv - q[c];
+        if (v < -1e-3 * sfv) throw NumericalError("predict: negative predictive variance beyond tolerance");
+        vars[i0 + c] = v < 0.0 ? 0.0 : v;
+      }
+    }
+    WGP_CUDA(cudaStreamSynchronize(st));
   }
 
   // ---------------------------------------------------------------- exact path
@@ -1158,6 +1232,17 @@ int wgp_train(wgp_ctx* ctx, const float* y, const wgp_train_cfg* cfg, wgp_trace*
     WGP_CUDA(cudaSetDevice(ctx->c.device));
     if (ctx->c.n < 1) throw std::invalid_argument("train: dataset is empty");
     ctx->c.train(y, *cfg, trace);
+  });
+}
+
+int wgp_predict(wgp_ctx* ctx, const float* X_test, int64_t m, const float* y, const wgp_solver_cfg* cfg,
+                double* means, double* variances, double* noise_variance) {
+  return guarded([&] {
+    if (!ctx || !y || !cfg || (m > 0 && (!X_test || !means || !variances)))
+      throw std::invalid_argument("wgp_predict: null argument");
+    WGP_CUDA(cudaSetDevice(ctx->c.device));
+    ctx->c.predict(X_test, m, y, *cfg, means, variances);
+    if (noise_variance) *noise_variance = ctx->c.sigma * ctx->c.sigma;
   });
 }
 

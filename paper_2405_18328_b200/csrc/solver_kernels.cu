@@ -132,6 +132,9 @@ __global__ void cg_init_kernel(float* P, const float* R, int64_t ld, int64_t n, 
     cs.rs[c] = rs;
     const bool conv = cs.bnorm[c] == 0.0 || sqrt(rs) <= cs.tol[c] * cs.bnorm[c];
     cs.conv[c] = conv ? 1 : 0;
+    cs.best[c] = rs;
+    cs.stall[c] = 0;
+    cs.act[c] = 1;
   }
   loop_check(s, cs, ctrl, true);
 }
@@ -185,11 +188,23 @@ __device__ void beta_epilogue(int s, ColState cs, const double* part, SolveCtrl*
       atomicCAS(&ctrl->status, kStatusOk, kStatusNaN);
       ctrl->fail_it = ctrl->it;
     }
+    if (restart) cs.act[c] = 0;
     if (sqrt(rs_new) <= cs.tol[c] * cs.bnorm[c]) {
       cs.conv[c] = 2;
       cs.beta[c] = 0.0;
     } else {
       cs.beta[c] = (restart && rs_new > 4.0 * cs.rs[c]) ? 0.0 : rs_new / cs.rs[c];
+      if (restart) {  // rs_new is the exact residual: keep the best iterate
+        if (rs_new < cs.best[c]) {
+          cs.best[c] = rs_new;
+          cs.stall[c] = 0;
+          cs.act[c] = 1;
+        } else if (++cs.stall[c] >= 3 || rs_new > 1e4 * cs.best[c]) {
+          cs.act[c] = 2;  // below the attainable accuracy: restore the best, freeze
+          cs.conv[c] = 3;
+          cs.beta[c] = 0.0;
+        }
+      }
     }
     cs.rs[c] = rs_new;
   }
@@ -243,7 +258,7 @@ __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_
 #pragma unroll 4
     for (int c = 0; c < s; ++c) {
       const int st = cs.conv[c];
-      if (st == 1) continue;
+      if (st == 1 || st == 3) continue;
       const int64_t e = i + c * ld;
       P[e] = st == 2 ? 0.f : fmaf(static_cast<float>(cs.beta[c]), P[e], R[e]);
     }
@@ -258,6 +273,29 @@ __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_
   for (int c = threadIdx.x; c < s; c += NT)
     if (cs.conv[c] == 2) cs.conv[c] = 1;
   loop_check(s, cs, ctrl, true);
+}
+
+// restart comment: see beta_epilogue.  The reference iterates to max_iterations
+// regardless; in fp64 the tolerances it is used with are reachable, in fp32
+// an unreachable one let the iterate drift and blow up between refreshes
+// (measured: relative residual 7e10 after 5000 iterations at tol 1e-6), so a
+// column whose exact residual has not improved for three refreshes (or grew
+// 1e4x past its best) is restored to its best iterate and frozen.
+__global__ void cg_snapshot_kernel(float* X, float* R, float* Xb, float* Rb, int64_t ld, int64_t n, int s,
+                                   ColState cs, const SolveCtrl* ctrl, int at_start) {
+  if (!at_start && ctrl->done) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= n) return;
+  const int a = cs.act[c];
+  const int64_t e = i + static_cast<int64_t>(c) * ld;
+  if (a == 1) {
+    Xb[e] = X[e];
+    Rb[e] = R[e];
+  } else if (a == 2) {
+    X[e] = Xb[e];
+    R[e] = Rb[e];
+  }
 }
 
 __global__ void norms_convergence_kernel(const float* R, int64_t ld, int64_t n, int s, ColState cs,
@@ -386,6 +424,13 @@ void check_s(int s) {
 }
 
 }  // namespace
+
+void cg_snapshot(float* X, float* R, float* Xb, float* Rb, int64_t ld, int64_t n, int s, ColState cs,
+                 const SolveCtrl* ctrl, bool at_start, cudaStream_t st) {
+  cg_snapshot_kernel<<<dim3(static_cast<unsigned>(ceil_div(n, NT)), s), NT, 0, st>>>(X, R, Xb, Rb, ld, n, s, cs,
+                                                                                     ctrl, at_start ? 1 : 0);
+  WGP_LAUNCH_CHECK();
+}
 
 void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, double* part,
               unsigned* ticket, double* out, cudaStream_t st) {

@@ -25,7 +25,9 @@ struct SolveCtrl {
 
 enum : int { kStatusOk = 0, kStatusNotPd = 1, kStatusNaN = 2, kStatusDiverged = 3 };
 
-// Column state: 0 active, 1 converged (frozen), 2 converged in this iteration.
+// Column state: 0 active, 1 converged (frozen), 2 converged in this iteration,
+// 3 stalled below the fp32 attainable accuracy (frozen at its best iterate,
+// reported not converged; CG only).
 struct ColState {
   int* conv;
   double* rs;      // CG: ||r||^2
@@ -33,6 +35,9 @@ struct ColState {
   double* beta;    // CG
   const double* bnorm;
   const double* tol;
+  double* best;    // CG: smallest exact ||r||^2 seen at a refresh (or the start)
+  int* stall;      // CG: refreshes since the last improvement
+  int* act;        // CG: 1 snapshot the iterate, 2 restore the snapshot (refresh steps)
 };
 
 // Rows per CTA of the reduction kernels: 256 (one per thread) up to a grid of
@@ -61,6 +66,10 @@ void cg_update(float* X, float* R, const float* P, const float* HP, int64_t ld, 
 // refresh: r = rtmp for active columns; then ||r||^2, convergence, beta.
 void cg_refresh_norm(float* R, const float* Rtmp, int64_t ld, int64_t n, int s, ColState cs,
                      double* part, SolveCtrl* ctrl, cudaStream_t st);
+// Refresh steps: per column, act 1 copies X, R -> Xb, Rb (new best iterate),
+// act 2 copies Xb, Rb -> X, R (stalled column restored to its best).
+void cg_snapshot(float* X, float* R, float* Xb, float* Rb, int64_t ld, int64_t n, int s, ColState cs,
+                 const SolveCtrl* ctrl, bool at_start, cudaStream_t st);
 // p = r + beta p (active) / 0 (just converged); then the next-iteration check.
 void cg_direction(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs,
                   double* part, SolveCtrl* ctrl, cudaStream_t st);

@@ -10,6 +10,7 @@ import pytest
 
 import paper_2405_18328_b200 as wg
 from paper_2405_18328_b200 import datasets
+from oracle import dense_ref
 from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -355,17 +356,28 @@ def test_hv_accumulation_knobs_subprocess():
 
 
 def test_cg_unreachable_tolerance_stays_bounded(ctx):
-    """A tolerance below the fp32 attainable accuracy runs to max_iterations
-    without converging, and the iterate must stay bounded (the residual
-    refresh restarts the direction instead of inflating it)."""
+    """A tolerance below the fp32 attainable accuracy never converges: every
+    column stalls, is restored to its best iterate (exact residual at a
+    refresh) and frozen, so the solve ends before max_iterations with bounded
+    iterates and residuals at the fp32 floor."""
     X, ls, sf, sig, rhs = kernel_problem(700, 3, 4, seed=12)
     ctx.set_data(X)
     ctx.set_hyper([*ls, sf, sig])
-    cfg = wg.SolverConfig(kind="cg", tol_mean=1e-9, tol_samples=1e-9, max_iterations=2000)
+    cfg = wg.SolverConfig(kind="cg", tol_mean=1e-9, tol_samples=1e-9, max_iterations=20000)
     st = ctx.solve(rhs, cfg)
-    assert st.iterations_used == 2000 and not st.all_converged()
+    assert st.iterations_used < 20000 and not any(st.converged)
     assert np.all(np.isfinite(st.solutions))
-    assert max(st.per_column_relative_residual) < 1e-3
+    assert max(st.per_column_relative_residual) < 1e-4
+    # the data that used to diverge (residual 7e10 at tol 1e-6, 5000 iterations)
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((1500, 4)).astype(np.float32)
+    rng.standard_normal((300, 4))
+    y = (np.sin(X[:, 0]) + 0.5 * X[:, 1] + 0.1 * rng.standard_normal(1500)).astype(np.float32)
+    ctx.set_data(X)
+    ctx.set_hyper([1.2, 0.9, 1.5, 2.0, 1.1, 0.3])
+    st = ctx.solve(y.reshape(-1, 1), wg.SolverConfig(kind="cg", tol_mean=1e-8, tol_samples=1e-8,
+                                                     max_iterations=5000))
+    assert st.per_column_relative_residual[0] < 1e-4
 
 
 @pytest.mark.parametrize("transform", ["softplus", "log"])
@@ -406,3 +418,25 @@ def test_exact_dense_guard(ctx):
     ctx.set_data(np.zeros((20001, 2), np.float32))
     with pytest.raises(ValueError, match="dense guard"):
         ctx.exact_mll(np.zeros(20001, np.float32), np.zeros(4))
+
+
+def test_predict_matches_dense_oracle(ctx):
+    """predict (exact.cpp:52-77) through iterative solves against the dense
+    fp64 oracle: posterior means and latent variances at 300 test points."""
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((1500, 4)).astype(np.float32)
+    Xt = rng.standard_normal((300, 4)).astype(np.float32)
+    y = (np.sin(X[:, 0]) + 0.5 * X[:, 1] + 0.1 * rng.standard_normal(1500)).astype(np.float32)
+    ls, sf, sig = np.array([1.2, 0.9, 1.5, 2.0]), 1.1, 0.3
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, sf, sig])
+    cfg = wg.SolverConfig(kind="cg", tol_mean=1e-5, tol_samples=1e-5, max_iterations=5000)
+    pred = ctx.predict(Xt, y, cfg)
+    means, var, nv = dense_ref.predict(X, y, Xt, ls, sf, sig)
+    assert np.max(np.abs(pred.means - means)) <= 1e-4 * np.max(np.abs(means))
+    assert np.max(np.abs(pred.variances - var)) <= 1e-4 * sf * sf
+    assert pred.noise_variance == pytest.approx(sig * sig, rel=1e-6)
+    m = wg.test_metrics(pred, np.sin(Xt[:, 0]) + 0.5 * Xt[:, 1])
+    mo = wg.test_metrics(wg.PredictiveDistribution(means, var, nv), np.sin(Xt[:, 0]) + 0.5 * Xt[:, 1])
+    assert m.rmse == pytest.approx(mo.rmse, rel=1e-4) and m.mean_loglik == pytest.approx(mo.mean_loglik, rel=1e-4)
+    assert ctx.predict(np.zeros((0, 4), np.float32), y, cfg).means.size == 0
