@@ -950,7 +950,7 @@ int choose_splits(int64_t row_tiles, int jt, int sms) {
   constexpr double kCtaOverheadTiles = 16.0;
   int best = 1;
   double best_cost = 1e300;
-  for (int sp = 1; sp <= 16; ++sp) {
+  for (int sp = 1; sp <= 64; ++sp) {
     if (sp > 1 && jt / sp < 8) break;
     const double waves = std::ceil(static_cast<double>(row_tiles * sp) / sms);
     const double cost = waves * (std::ceil(static_cast<double>(jt) / sp) + kCtaOverheadTiles) +

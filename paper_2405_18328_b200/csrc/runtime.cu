@@ -85,7 +85,7 @@ struct Ctx {
 
   // workspaces
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
-  Buf P, HP, Rtmp, vel, batch, idx, hbuf, Rb, D64, D32, lapack_work, info;
+  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, D32, lapack_work, info;
   Buf gpart, gout;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
@@ -166,7 +166,7 @@ struct Ctx {
   // ---------------------------------------------------------------- H.V
   void hv(const float* V, int64_t ldv, int s, float* out, int64_t ldo, int mode, const float* B,
           int64_t ldb, int64_t j0, int64_t j1, const int* row_idx, int64_t rr0, int64_t m,
-          const int* done = nullptr) {
+          const int* done = nullptr, bool shard_invariant = true) {
     HvParams p{};
     p.xs = xs.as<float>();
     p.n = n;
@@ -190,7 +190,9 @@ struct Ctx {
     p.diag = static_cast<float>(sf * sf + sigma * sigma);
     p.hyp = dhyp.as<float>();
     p.done = done;
-    p.split_rows = row_idx ? 0 : n;  // shards of the full operator decompose like the whole
+    // shards of the full operator decompose like the whole (bitwise-equal
+    // rows); internal row blocks (AP) split for their own size instead
+    p.split_rows = (row_idx || !shard_invariant) ? 0 : n;
     if ((hv_impl == WGP_HV_TC || hv_impl == WGP_HV_TC_BF16) && hv_tc_supported(d, s)) {
       if (!tc.valid) tc.build(xs.as<float>(), n, dp, d, st);
       hv_tc(tc, p, st, hv_impl == WGP_HV_TC_BF16);
@@ -450,40 +452,58 @@ struct Ctx {
     const int max_ep = cfg.max_iterations > 0 ? cfg.max_iterations : 1000;
     const int64_t bs = std::min<int64_t>(std::max(cfg.block_size, 1), n);
     const int64_t nb = ceil_div(n, bs);
-    // Factor every diagonal block once per solve (:151-165): H[b,b] in fp64,
-    // Cholesky, explicit inverse, so each Gauss-Seidel step is one symmetric
-    // GEMM on the tensor-free fp64 path.
+    // Factor every diagonal block once per solve (:151-165): H[b,b] in fp64
+    // (the last, partial block padded with the identity), one batched
+    // cuSOLVER Cholesky over all blocks, then the explicit inverses below.
+    // (Per-block potrf + potri and a symm per step cost ~20 small launches per
+    // block and 0.4 ms per symm, measured.)
     hbuf.ensure(sizeof(double) * static_cast<size_t>(nb) * bs * bs);
     info.ensure(sizeof(int) * nb);
     WGP_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int) * nb, st));
-    int lw1 = 0, lw2 = 0;
-    cusolverDnDpotrf_bufferSize(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(bs), hbuf.as<double>(),
-                                static_cast<int>(bs), &lw1);
-    cusolverDnDpotri_bufferSize(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(bs), hbuf.as<double>(),
-                                static_cast<int>(bs), &lw2);
-    const int lw = std::max(lw1, lw2);
-    lapack_work.ensure(sizeof(double) * std::max(lw, 1));
     const double sf2d = sf * sf, ad = sf * sf * kLn2, n2d = sigma * sigma;
+    std::vector<double*> hptr(nb);
     for (int64_t b = 0; b < nb; ++b) {
       const int64_t start = b * bs, size = std::min(bs, n - start);
-      double* Hb = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
-      build_block(xs.as<float>(), dp, start, size, sf2d, ad, n2d, Hb, st);
-      cusolverDnDpotrf(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(size), Hb, static_cast<int>(size),
-                       lapack_work.as<double>(), lw, info.as<int>() + b);
+      hptr[b] = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
+      build_block(xs.as<float>(), dp, start, size, bs, sf2d, ad, n2d, hptr[b], st);
     }
+    lapack_work.ensure(sizeof(double*) * nb);
+    WGP_CUDA(cudaMemcpyAsync(lapack_work.p, hptr.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice, st));
+    if (cusolverDnDpotrfBatched(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(bs),
+                                reinterpret_cast<double**>(lapack_work.p), static_cast<int>(bs), info.as<int>(),
+                                static_cast<int>(nb)) != CUSOLVER_STATUS_SUCCESS)
+      throw DeviceError("cusolverDnDpotrfBatched failed");
     std::vector<int> hinfo(nb);
     WGP_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
     for (int v : hinfo)
       if (v != 0)
         throw NumericalError("ap_solve: diagonal block factorization failed, H is not positive definite");
-    for (int64_t b = 0; b < nb; ++b) {
-      const int64_t start = b * bs, size = std::min(bs, n - start);
-      double* Hb = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
-      cusolverDnDpotri(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(size), Hb, static_cast<int>(size),
-                       lapack_work.as<double>(), lw, info.as<int>() + b);
-      (void)start;
-    }
+    // H_bb^-1 = L^-T L^-1 for all blocks: batched triangular solve against the
+    // identity, then a strided-batched GEMM (per-block cublasDtrsm in the
+    // epoch loop expanded to ~30 kernels, ~0.5 ms per block, measured); each
+    // Gauss-Seidel step is then one DGEMM.
+    const size_t bb = static_cast<size_t>(bs) * bs;
+    linv.ensure(sizeof(double) * bb * nb);
+    identities(linv.as<double>(), bs, nb, st);
+    std::vector<double*> lptr(nb);
+    for (int64_t b = 0; b < nb; ++b) lptr[b] = linv.as<double>() + b * bb;
+    Buf lp;
+    lp.ensure(sizeof(double*) * nb);
+    WGP_CUDA(cudaMemcpyAsync(lp.p, lptr.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice, st));
+    const double one_ = 1.0, zero_ = 0.0;
+    if (cublasDtrsmBatched(cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                           static_cast<int>(bs), static_cast<int>(bs), &one_,
+                           reinterpret_cast<const double* const*>(lapack_work.p), static_cast<int>(bs),
+                           reinterpret_cast<double* const*>(lp.p), static_cast<int>(bs),
+                           static_cast<int>(nb)) != CUBLAS_STATUS_SUCCESS)
+      throw DeviceError("cublasDtrsmBatched failed");
+    if (cublasDgemmStridedBatched(cublas, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(bs), static_cast<int>(bs),
+                                  static_cast<int>(bs), &one_, linv.as<double>(), static_cast<int>(bs),
+                                  static_cast<long long>(bb), linv.as<double>(), static_cast<int>(bs),
+                                  static_cast<long long>(bb), &zero_, hbuf.as<double>(), static_cast<int>(bs),
+                                  static_cast<long long>(bb), static_cast<int>(nb)) != CUBLAS_STATUS_SUCCESS)
+      throw DeviceError("cublasDgemmStridedBatched failed");
     Rb.ensure(sizeof(double) * bs * s);
     D64.ensure(sizeof(double) * bs * s);
     D32.ensure(sizeof(float) * bs * s);
@@ -503,14 +523,20 @@ struct Ctx {
       for (int64_t b = 0; b < nb; ++b) {  // :183-187
         const int64_t start = b * bs, size = std::min(bs, n - start);
         const double* Hinv = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
+        // Left-looking block residual R_b = B_b - H[b, :] X from the current X
+        // (= the reference's incrementally updated R_b in exact arithmetic:
+        // R is exact at the epoch start and every earlier block's update is in
+        // X).  One H.V of `size` rows against all n points splits into long
+        // J ranges; the right-looking R -= H[:, b] delta over n rows with only
+        // `size` contracted points ran ~32 tiles per CTA, dominated by the
+        // per-CTA fixed cost (measured 0.75 s per config-3 epoch).
+        hv(Xo, ld, s, R + start, ld, kHvResidual, B, ld, 0, n, nullptr, start, size, &c->done, false);
         ap_gather(R, ld, start, size, s, Rb.as<double>(), c, st);
-        cublasDsymm(cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, static_cast<int>(size), s, &one,
-                    Hinv, static_cast<int>(size), Rb.as<double>(), static_cast<int>(size), &zero,
-                    D64.as<double>(), static_cast<int>(size));
+        // delta = H_bb^-1 R_b (:185)
+        cublasDgemm(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, static_cast<int>(size), &one, Hinv,
+                    static_cast<int>(bs), Rb.as<double>(), static_cast<int>(size), &zero, D64.as<double>(),
+                    static_cast<int>(size));
         ap_apply(Xo, ld, start, size, s, D64.as<double>(), D32.as<float>(), c, st);
-        // R -= H[:, blk] delta : contracted points [start, start + size)
-        hv(D32.as<float>() - start, size, s, R, ld, kHvSubtract, nullptr, 0, start, start + size,
-           nullptr, 0, n, &c->done);
       }
       hv_all(Xo, s, R, kHvResidual, B);                            // :188
       norms_convergence(R, ld, n, s, cs, pt, c, true, true, st);  // :189-191

@@ -340,11 +340,17 @@ __global__ void ap_apply_kernel(float* X, int64_t ld, int64_t start, int64_t b, 
   d32[i + c * b] = static_cast<float>(dv);
 }
 
-__global__ void build_block_kernel(const float* xs, int dp, int64_t start, int64_t b, double sf2,
+// H[b, b] (fp64) padded to `full` x `full` with the identity (so a partial last
+// block joins the uniform batched factorisation without changing its solve).
+__global__ void build_block_kernel(const float* xs, int dp, int64_t start, int64_t b, int64_t full, double sf2,
                                    double a, double noise2, double* out) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= b * b) return;
-  const int64_t i = e % b, j = e / b;
+  if (e >= full * full) return;
+  const int64_t i = e % full, j = e / full;
+  if (i >= b || j >= b) {
+    out[e] = i == j ? 1.0 : 0.0;
+    return;
+  }
   const float* xa = xs + (start + i) * dp;
   const float* xb = xs + (start + j) * dp;
   double r2 = 0.0;
@@ -356,6 +362,14 @@ __global__ void build_block_kernel(const float* xs, int dp, int64_t start, int64
   double v = (a * u + sf2) * exp2(-u);
   if (i == j) v += noise2;
   out[e] = v;
+}
+
+// nb identity matrices of size b x b (column-major, contiguous)
+__global__ void identity_kernel(double* A, int64_t b, int64_t total) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const int64_t r = e % (b * b);
+  A[e] = (r % b == r / b) ? 1.0 : 0.0;
 }
 
 __global__ void sgd_scatter_kernel(float* X, float* R, float* vel, int64_t ld, const int* idx,
@@ -493,10 +507,16 @@ void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const doubl
   WGP_LAUNCH_CHECK();
 }
 
-void build_block(const float* xs, int dp, int64_t start, int64_t b, double sf2, double a,
+void identities(double* A, int64_t b, int64_t nb, cudaStream_t st) {
+  const int64_t total = b * b * nb;
+  identity_kernel<<<static_cast<unsigned>(ceil_div(total, NT)), NT, 0, st>>>(A, b, total);
+  WGP_LAUNCH_CHECK();
+}
+
+void build_block(const float* xs, int dp, int64_t start, int64_t b, int64_t full, double sf2, double a,
                  double noise2, double* out, cudaStream_t st) {
-  build_block_kernel<<<static_cast<unsigned>(ceil_div(b * b, NT)), NT, 0, st>>>(
-      xs, dp, start, b, sf2, a, noise2, out);
+  build_block_kernel<<<static_cast<unsigned>(ceil_div(full * full, NT)), NT, 0, st>>>(
+      xs, dp, start, b, full, sf2, a, noise2, out);
   WGP_LAUNCH_CHECK();
 }
 

@@ -85,8 +85,10 @@ void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, doub
                const SolveCtrl* ctrl, cudaStream_t st);
 void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
               float* delta32, const SolveCtrl* ctrl, cudaStream_t st);
-// H[b, b] in fp64 from the prepared points.
-void build_block(const float* xs, int dp, int64_t start, int64_t b, double sf2, double a,
+// nb contiguous b x b identity matrices (fp64, column-major).
+void identities(double* A, int64_t b, int64_t nb, cudaStream_t st);
+// H[b, b] in fp64 from the prepared points, padded with the identity to full x full.
+void build_block(const float* xs, int dp, int64_t start, int64_t b, int64_t full, double sf2, double a,
                  double noise2, double* out, cudaStream_t st);
 
 // SGD: vel/X/R row scatter (proj/src/solvers.cpp:247-252) then divergence and
