@@ -35,6 +35,7 @@
 
 #include "common.cuh"
 #include "hv_tc.cuh"
+#include "tc_ptx.cuh"
 
 namespace wgp {
 namespace {
@@ -46,146 +47,6 @@ constexpr uint32_t kTfMask = 0xFFFFE000u;  // keep sign, exponent, 10 mantissa b
 constexpr int kSmemLimit = 232448 - 2048;  // 227 KB opt-in minus static smem (barriers)
 constexpr int kMaxStages = 8;              // smem ring depth cap (barrier arrays)
 constexpr int kDoneRing = 8;               // MMA completion rings (>= kMaxStages, NBUF)
-
-// ------------------------------------------------------------------ PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  const uint32_t addr = smem_u32(b);
-  uint32_t ok = 0;
-  while (true) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    if (ok) break;
-  }
-}
-__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// MMA issue helpers are called by a whole converged warp with warp-uniform
-// operands (so descriptors live in uniform registers); one lane, chosen by
-// elect.sync, issues.
-// The three 3xTF32 partial products of one K step from a single asm block
-// (one elect): D (+)= A_hi B_hi + A_hi B_lo + A_lo B_hi.
-__device__ __forceinline__ void mma3_ss(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
-                                        uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p, t, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %6, 0;\n"
-      " setp.eq.u32 t, 0, 0;\n"
-      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n"
-      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, t;\n}\n" ::"r"(d),
-      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma3_ts(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
-                                        uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p, t, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %6, 0;\n"
-      " setp.eq.u32 t, 0, 0;\n"
-      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, p;\n"
-      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, t;\n}\n" ::"r"(d),
-      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-// TMA issue by one elected lane of a converged warp.
-__device__ __forceinline__ void tma_load_2d_warp(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                                 int c1) {
-  asm volatile(
-      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-      " @e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
-      "[%2];\n}\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_warp(uint64_t* b, uint32_t bytes) {
-  asm volatile(
-      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-      " @e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(b)),
-      "r"(bytes)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_warp(uint64_t* b) {
-  asm volatile(
-      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-      " @e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(smem_u32(b))
-      : "memory");
-}
-
-#define R8(i) "=r"(r[i + 0]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3]), "=r"(r[i + 4]), \
-              "=r"(r[i + 5]), "=r"(r[i + 6]), "=r"(r[i + 7])
-#define W8(i) "r"(r[i + 0]), "r"(r[i + 1]), "r"(r[i + 2]), "r"(r[i + 3]), "r"(r[i + 4]), \
-              "r"(r[i + 5]), "r"(r[i + 6]), "r"(r[i + 7])
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : R8(0), R8(8), R8(16), R8(24)
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : R8(0)
-               : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      W8(0), W8(8), W8(16), W8(24)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms of
-// 1024 bytes (SBO), version 1 (sm_100), LBO unused for swizzled K-major.
-__device__ __forceinline__ uint64_t umma_desc(const void* p) {
-  const uint32_t a = smem_u32(p);
-  return static_cast<uint64_t>((a >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
-         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
-         (static_cast<uint64_t>(2) << 61);
-}
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(M >> 4) << 24);
-}
-
-// bf16 x 3 MMA-2 (kind::f16, K = 16 per instruction): D (+)= k1 v1 + k1 v2 + k2 v1.
-__device__ __forceinline__ void mma3_ts_bf16(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
-                                             uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p, t, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %6, 0;\n"
-      " setp.eq.u32 t, 0, 0;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n}\n" ::"r"(d),
-      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
-}
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(M >> 4) << 24);
-}
 
 // 32 squared scaled distances -> tf32 hi / lo planes of k (k_hi keeps sign,
 // exponent and 10 mantissa bits; k_lo = k - k_hi is exact); the diagonal
@@ -1055,6 +916,12 @@ void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorM
   hv_tc_kernel<BF><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a);
   WGP_LAUNCH_CHECK();
 }
+
+CUtensorMap tc_tensor_map(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
+                          uint32_t box_out) {
+  return make_map(base, inner, outer, row_bytes, box_in, box_out);
+}
+int tc_sm_count() { return sm_count(); }
 
 bool hv_tc_supported(int d, int s) { return d + 2 <= kKA && s >= 1 && s <= 128; }
 

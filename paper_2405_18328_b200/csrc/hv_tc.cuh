@@ -1,6 +1,7 @@
 // hv_tc.cuh — tcgen05 / TMEM / TMA fused H.V, see hv_tc.cu.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -40,5 +41,11 @@ bool hv_tc_supported(int d, int s);
 // product) or bf16x3 (bf16 = true, ~2^-17, half the tensor work); fp32
 // accumulation in chunks of 1024 points summed at higher precision.
 void hv_tc(TcOperands& ops, const HvParams& p, cudaStream_t st, bool bf16);
+
+// Shared host helpers of the tcgen05 kernels (hv_tc.cu, grad_tc.cu): a 2D
+// fp32 TMA map with 128-byte swizzle (box_in x box_out elements) and the SM count.
+CUtensorMap tc_tensor_map(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
+                          uint32_t box_out);
+int tc_sm_count();
 
 }  // namespace wgp

@@ -77,6 +77,16 @@ struct GradParams {
 };
 int grad_blocks(int64_t n);
 void grad_simt(const GradParams& p, cudaStream_t st);
+// Tensor-core gradient (grad_tc.cu): W^B on tcgen05, O(d) epilogue; same
+// partial format as grad_simt ([plan.nblk][2 (d + 1)]).
+struct GradTcPlan {
+  int64_t n_pad = 0;
+  int spk = 0, ep = 0, splits = 1, nblk = 0;
+  size_t ws_bytes = 0;
+};
+bool grad_tc_supported(int d, int s);
+GradTcPlan grad_tc_plan(int64_t n, int d, int s);
+void grad_tc(const GradParams& p, const GradTcPlan& plan, void* ws, cudaStream_t st);
 // out[0..2(d+1)) = sum over blocks in block order.
 void grad_finalize(const double* part, int nblk, int width, double* out, cudaStream_t st);
 

@@ -86,7 +86,7 @@ struct Ctx {
   // workspaces
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
   Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, D32, lapack_work, info;
-  Buf gpart, gout;
+  Buf gpart, gout, gtc_ws;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
   Buf hx, hx_ws, exv;  // exact path: dense H (fp64), cuSOLVER workspace, vectors
@@ -609,9 +609,19 @@ struct Ctx {
     std::vector<double> cons(d + 2);
     for (int k = 0; k < d + 2; ++k) cons[k] = transform == 1 ? std::exp(raw[k]) : softplus(raw[k]);
     set_hyper(cons.data());
-    const int nblk = grad_blocks(n);
+    // tensor-core engines (TC, TC_BF16) use the tcgen05 gradient where it
+    // applies; WGP_GRAD_IMPL=simt forces the CUDA-core kernel
+    static const bool force_simt = [] {
+      const char* e = getenv("WGP_GRAD_IMPL");
+      return e && std::string(e) == "simt";
+    }();
+    const bool use_tc = hv_impl != WGP_HV_SIMT && !force_simt && grad_tc_supported(d, s);
+    GradTcPlan plan;
+    if (use_tc) plan = grad_tc_plan(n, d, s);
+    const int nblk = use_tc ? plan.nblk : grad_blocks(n);
     const int W = 2 * (d + 1);
     gpart.ensure(sizeof(double) * nblk * W);
+    if (use_tc) gtc_ws.ensure(plan.ws_bytes);
     gout.ensure(sizeof(double) * W);
     GradParams gp{};
     gp.xs = xs.as<float>();
@@ -627,7 +637,10 @@ struct Ctx {
     gp.sf2 = sf2();
     gp.a = a_coef();
     gp.part = gpart.as<double>();
-    grad_simt(gp, st);
+    if (use_tc)
+      grad_tc(gp, plan, gtc_ws.p, st);
+    else
+      grad_simt(gp, st);
     grad_finalize(gpart.as<double>(), nblk, W, gout.as<double>(), st);
     std::vector<double> acc(W);
     WGP_CUDA(cudaMemcpyAsync(acc.data(), gout.p, sizeof(double) * W, cudaMemcpyDeviceToHost, st));

@@ -188,10 +188,18 @@ def test_sgd_divergence_message(ctx):
         ctx.solve(rhs, wg.SolverConfig(kind="sgd", learning_rate=1e9, max_iterations=10000))
 
 
-@pytest.mark.parametrize("transform", ["softplus", "log"])
-def test_gradient_contractions_match_oracle(ctx, transform):
-    rng = np.random.default_rng(21)
-    n, d, s = 900, 5, 8
+@pytest.mark.parametrize("impl", ["tc", "simt"])
+@pytest.mark.parametrize("transform,n,d,s", [("softplus", 900, 5, 8), ("log", 900, 5, 8), ("log", 1, 1, 1),
+                                             ("softplus", 130, 3, 64), ("log", 2048, 8, 17),
+                                             ("softplus", 1000, 9, 33), ("log", 300, 12, 40),
+                                             ("softplus", 500, 13, 8), ("log", 400, 4, 65)])
+def test_gradient_contractions_match_oracle(ctx, impl, transform, n, d, s):
+    """derivative_contractions (kernel.cpp:199-262) through both gradient
+    engines: tcgen05 (hv impl tc: W^B on the tensor core, 1 <= d <= 12,
+    s <= 64) and the CUDA-core kernel (simt; also what tc falls back to for
+    d = 13 and s = 65)."""
+    ctx.set_hv_impl(impl)
+    rng = np.random.default_rng(21 + n + d + s)
     X = rng.standard_normal((n, d)).astype(np.float32)
     ctx.set_data(X)
     raw = np.array([orc.to_raw(transform, v) for v in (*rng.uniform(0.6, 1.6, d), 1.2, 0.3)])
@@ -200,8 +208,37 @@ def test_gradient_contractions_match_oracle(ctx, transform):
     R = rng.standard_normal((n, s)).astype(np.float32)
     ga, gb = ctx.grad(transform, raw, vy, L, R, 0.5 / s)
     oa, ob = orc.grad_contractions(X, transform, raw, vy, L, R, 0.5 / s)
+    ctx.set_hv_impl("tc")
     assert np.allclose(ga, oa, rtol=2e-5, atol=1e-5 * np.abs(oa).max())
     assert np.allclose(gb, ob, rtol=2e-5, atol=1e-5 * np.abs(ob).max())
+
+
+def test_gradient_tc_full_size_config3(ctx):
+    """BASELINE config 3 at full size (n=391,386, d=3, 64 probes): the
+    tcgen05 gradient against the CUDA-core one (the oracle's O(n^2 s) pass
+    does not finish in test time), plus linearity in L and determinism."""
+    p = datasets.config3()
+    n, d, s = p.X.shape[0], p.X.shape[1], 64
+    rng = np.random.default_rng(5)
+    ctx.set_data(p.X)
+    raw = np.array([orc.to_raw("softplus", v) for v in (*p.lengthscales, p.signal, p.noise)])
+    vy = rng.standard_normal(n).astype(np.float32)
+    L = rng.standard_normal((n, s)).astype(np.float32)
+    R = rng.standard_normal((n, s)).astype(np.float32)
+    ctx.set_hv_impl("simt")
+    sa, sb = ctx.grad("softplus", raw, vy, L, R, 0.5 / s)
+    ctx.set_hv_impl("tc")
+    ta, tb = ctx.grad("softplus", raw, vy, L, R, 0.5 / s)
+    ta2, tb2 = ctx.grad("softplus", raw, vy, L, R, 0.5 / s)
+    assert np.array_equal(ta, ta2) and np.array_equal(tb, tb2)
+    assert np.allclose(ta, sa, rtol=1e-5, atol=1e-6 * np.abs(sa).max())
+    assert np.allclose(tb, sb, rtol=1e-4, atol=1e-5 * np.abs(sb).max())
+    # B contraction is linear in L: split L into two halves of its columns' mass
+    L1 = (0.25 * L).astype(np.float32)
+    L2 = (L - L1).astype(np.float32)
+    _, b1 = ctx.grad("softplus", raw, vy, L1, R, 0.5 / s)
+    _, b2 = ctx.grad("softplus", raw, vy, L2, R, 0.5 / s)
+    assert np.allclose(b1 + b2, tb, rtol=1e-4, atol=1e-5 * np.abs(tb).max())
 
 
 def test_rff_probes_match_oracle(ctx):
