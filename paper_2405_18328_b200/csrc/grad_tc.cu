@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 namespace wgp {
@@ -41,30 +42,166 @@ constexpr int gTI = 128;             // rows per CTA (MMA M, TMEM lanes)
 constexpr int gTJ = 64;              // points per J tile (MMA N)
 constexpr int gThreads = 512;
 constexpr int gEpiGroups = 3, gEpiWarps = 12, gEpiThreads = 384;
-constexpr int gWarpProd = 12, gWarpMma = 13, gWarpAlloc = 14;
+// Warp roles.  Every SMSP (warp % 4) runs three epilogue warps (4..15; warp
+// w reads TMEM lanes 32 (w % 4) .. +31) and one issuer warp (0..3): issuer q
+// loads and multiplies the tiles t = q (mod 4).  The issue work of the loads
+// and MMAs costs the hosting SMSP's epilogue warps issue slots, and each
+// epilogue group advances at the pace of its slowest lane quarter, so it is
+// spread evenly (measured with WGP_GRAD_TRACE: a single issuer warp left its
+// SMSP's epilogue warps the bottleneck of the whole pipeline).
+constexpr int gEpiBase = 4;
+constexpr int gIssuers = 4;
+constexpr int gWarpAlloc = 1;
 constexpr int gBufs = 6;                    // W buffers (64 TMEM columns each)
 constexpr uint32_t gLhi = 384, gLlo = 448;  // L_I planes, <= 64 columns each
-constexpr int gRing = 8;                    // MMA-done barrier ring (> gBufs)
-constexpr int gNE = 8;                      // epilogue-data ring (>= gBufs + 2)
-constexpr int gMaxNM = 6;
+constexpr int gNM = 4;                      // R_J ring: stage t % 4, owned by issuer t % 4
+constexpr int gMaxNE = 8;                   // epilogue-data ring: 8 (or 4 when shared memory is short)
 constexpr int gFlushTiles = 4;              // fp32 row sums span 4 tiles (256 entries)
 constexpr int gSmemLimit = 232448 - 4096;   // 227 KB opt-in minus static smem
 constexpr uint32_t gTfMask = 0xFFFFE000u;
 
-__host__ __device__ constexpr int ep_of(int d) { return ((d + 1 + 3) / 4) * 4; }  // x_j[0..d) | vy_j | 0..
+// Epilogue stage of one tile: [d + 1][64] fp32, coordinate-major (rows 0..d-1:
+// -x_jk, row d: vy_j), so one 16-byte shared load yields 4 points of one
+// coordinate (two float2 pairs) and x_ik - x_jk is one FADD2.
+__host__ __device__ constexpr int ep_of(int d) { return d + 1; }
+
+// After tcgen05.wait::ld: the registers of the completed load are redefined
+// here for the compiler, so no use or copy of them is scheduled before the wait.
+__device__ __forceinline__ void pin(uint32_t (&r)[16]) {
+  asm volatile("" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+               "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+               "+r"(r[14]), "+r"(r[15]));
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+
+// Per-entry work of two points j, j+1 (one row i per lane) in packed fp32x2
+// (FADD2 / FMUL2 / FFMA2 halve the issue slots of the FMA-pipe work, which
+// bounds this epilogue): nx[k] = -x_jk pair, vy pair, w = W^B pair.
+template <int D>
+__device__ __forceinline__ void entry_pair(const float2 (&xi)[D], const float2 (&nx)[D], float2 vy, float2 w,
+                                           float2 sf2, float2 ac, float2 (&A)[D + 1], float2 (&B)[D + 1]) {
+  float2 dq[D];
+  float2 r2;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float2 df = __fadd2_rn(xi[k], nx[k]);
+    dq[k] = __fmul2_rn(df, df);
+    r2 = k == 0 ? dq[0] : __fadd2_rn(r2, dq[k]);
+  }
+  float2 u, dec;
+  u.x = sqrt_approx(r2.x);
+  u.y = sqrt_approx(r2.y);
+  dec.x = ex2_approx(-u.x);
+  dec.y = ex2_approx(-u.y);
+  const float2 pk = __ffma2_rn(ac, u, sf2);  // k = pk * dec
+  const float2 dA = __fmul2_rn(dec, vy), dB = __fmul2_rn(dec, w);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    A[k] = __ffma2_rn(dq[k], dA, A[k]);
+    B[k] = __ffma2_rn(dq[k], dB, B[k]);
+  }
+  A[D] = __ffma2_rn(pk, dA, A[D]);
+  B[D] = __ffma2_rn(pk, dB, B[D]);
+}
+
+// W(t) = L_I R_J^T in 3xTF32 over K = 32 (4 K steps): all 12 MMAs of a tile from one
+// asm block and one elect (per-k A / B addresses by immediate adds), so the
+// issuing warp costs its SMSP ~34 instructions per tile instead of ~180.
+// a: TMEM address of L_I hi column 0 (lo 64 columns further); bh / bl: B
+// descriptors of the stage's hi / lo plane (boxes of 32 K, 8192 bytes apart).
+__device__ __forceinline__ void mma_w_k32(uint32_t d, uint32_t a, uint64_t bh, uint64_t bl, uint32_t idesc) {
+  asm volatile(
+      "{\n .reg .pred e, f, t;\n .reg .b32 ah, al;\n .reg .b64 dh, dl;\n"
+      " setp.ne.b32 f, 0, 0;\n setp.eq.b32 t, 0, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " add.u32 ah, %1, 0;\n add.u32 al, %1, 64;\n add.s64 dh, %2, 0;\n add.s64 dl, %3, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, f;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 8;\n add.u32 al, %1, 72;\n add.s64 dh, %2, 2;\n add.s64 dl, %3, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 16;\n add.u32 al, %1, 80;\n add.s64 dh, %2, 4;\n add.s64 dl, %3, 4;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 24;\n add.u32 al, %1, 88;\n add.s64 dh, %2, 6;\n add.s64 dl, %3, 6;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      "}\n"
+      ::"r"(d), "r"(a), "l"(bh), "l"(bl), "r"(idesc));
+}
+// W(t) = L_I R_J^T in 3xTF32 over K = 64 (8 K steps): all 24 MMAs of a tile from one
+// asm block and one elect (per-k A / B addresses by immediate adds), so the
+// issuing warp costs its SMSP ~62 instructions per tile instead of ~360.
+// a: TMEM address of L_I hi column 0 (lo 64 columns further); bh / bl: B
+// descriptors of the stage's hi / lo plane (boxes of 32 K, 8192 bytes apart).
+__device__ __forceinline__ void mma_w_k64(uint32_t d, uint32_t a, uint64_t bh, uint64_t bl, uint32_t idesc) {
+  asm volatile(
+      "{\n .reg .pred e, f, t;\n .reg .b32 ah, al;\n .reg .b64 dh, dl;\n"
+      " setp.ne.b32 f, 0, 0;\n setp.eq.b32 t, 0, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " add.u32 ah, %1, 0;\n add.u32 al, %1, 64;\n add.s64 dh, %2, 0;\n add.s64 dl, %3, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, f;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 8;\n add.u32 al, %1, 72;\n add.s64 dh, %2, 2;\n add.s64 dl, %3, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 16;\n add.u32 al, %1, 80;\n add.s64 dh, %2, 4;\n add.s64 dl, %3, 4;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 24;\n add.u32 al, %1, 88;\n add.s64 dh, %2, 6;\n add.s64 dl, %3, 6;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 32;\n add.u32 al, %1, 96;\n add.s64 dh, %2, 512;\n add.s64 dl, %3, 512;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 40;\n add.u32 al, %1, 104;\n add.s64 dh, %2, 514;\n add.s64 dl, %3, 514;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 48;\n add.u32 al, %1, 112;\n add.s64 dh, %2, 516;\n add.s64 dl, %3, 516;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      " add.u32 ah, %1, 56;\n add.u32 al, %1, 120;\n add.s64 dh, %2, 518;\n add.s64 dl, %3, 518;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], dl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], dh, %4, t;\n"
+      "}\n"
+      ::"r"(d), "r"(a), "l"(bh), "l"(bl), "r"(idesc));
+}
 
 struct GradTcArgs {
   int64_t n;
   int d, dp, s, spk;  // spk: K extent of W^B (32 or 64: multiples of one 128-byte swizzle row)
-  int num_jt, splits, nm;
+  int num_jt, splits, ne;
+  int cs, rt_pad;     // cluster size (CTAs sharing each R_J stage by TMA multicast), row tiles padded to cs
   uint32_t mstage, estage, acc_off;
   const float* xs;   // prepared points [n][dp]
   const float* vy;   // [n]
-  const float* xv;   // [n_pad][ep]: x_j | vy_j, zero rows past n
+  const float* xv;   // [n_pad / 64][d + 1][64]: -x_jk rows, vy_j row (zero past n)
   const float* L;
   int64_t ld;
   float sf2, a, coef_b;
   double* part;      // [gridDim.x][2 (d + 1)]
+  int dbg;           // WGP_GRAD_DEBUG ablation bits: 1 no MMA, 2 no epilogue math, 4 no R loads
+  unsigned long long* trace;  // WGP_GRAD_TRACE: per warp {total, wait A, wait B, wait C} clk, summed over CTAs
 };
 
 template <int D>
@@ -74,34 +211,47 @@ __global__ void __launch_bounds__(gThreads, 1)
   constexpr int EP = ep_of(D);
   constexpr int NW = 2 * (D + 1);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // rfull[s]: R_J planes of stage s landed; efull[s]: x_j | vy_j of stage s
-  // landed; mdone[t % 8]: W(t) in TMEM and R stage of t free; wfree[b]: the
-  // epilogue read W buffer b; efree[s]: the epilogue read stage s; lready: L_I in TMEM.
-  __shared__ __align__(8) uint64_t bar_rfull[gMaxNM], bar_efull[gNE], bar_mdone[gRing], bar_wfree[gBufs],
-      bar_efree[gNE], bar_lready;
+  // rfull[s]: R_J planes of stage s landed (all cs slices); rempty[s]: the
+  // MMAs of all cs CTAs of the cluster released stage s; efull[s]: x_j | vy_j
+  // of stage s landed; mdone[b]: W of the tile in buffer b ready; wfree[b]:
+  // the epilogue read W buffer b; efree[s]: the epilogue read stage s;
+  // lready: L_I in TMEM.  mdone shares the W-buffer ring: MMA(t) completes
+  // phase t / 6 of mdone[t % 6] only after the epilogue of t - 6 consumed the
+  // previous one, so no waiter can miss a phase whatever the issue order.
+  __shared__ __align__(8) uint64_t bar_rfull[gNM], bar_rempty[gNM], bar_efull[gMaxNE], bar_mdone[gBufs],
+      bar_wfree[gBufs], bar_efree[gMaxNE], bar_lready;
   __shared__ double wacc[gEpiWarps][NW];
   __shared__ uint32_t tmem_slot;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sR = smem;                                                 // nm x [R_hi | R_lo]
-  const float* sE = reinterpret_cast<const float*>(sR + static_cast<size_t>(p.nm) * p.mstage);  // gNE x [64][EP]
+  const float* sE = reinterpret_cast<const float*>(sR + static_cast<size_t>(gNM) * p.mstage);  // ne x [EP][64]
   double* sAcc = reinterpret_cast<double*>(smem + p.acc_off);        // [NW][384] per-row fp64 sums
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rt = blockIdx.x / p.splits, sp = blockIdx.x % p.splits;
+  // clusters of cs consecutive row tiles share one J range (and its R_J stream)
+  const int rt = blockIdx.x % p.rt_pad, sp = blockIdx.x / p.rt_pad;
+  const int CS = p.cs;
+  const uint32_t crank = CS > 1 ? cluster_ctarank() : 0u;
+  const uint16_t cmask = static_cast<uint16_t>((1u << CS) - 1u);
   const int jt_begin = static_cast<int>(static_cast<int64_t>(p.num_jt) * sp / p.splits);
   const int jt_end = static_cast<int>(static_cast<int64_t>(p.num_jt) * (sp + 1) / p.splits);
   const int T = jt_end - jt_begin;
-  const int NM = p.nm;
+  const int NE = p.ne;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NM; ++i) mbar_init(&bar_rfull[i], 1);
-    for (int i = 0; i < gNE; ++i) {
+    for (int i = 0; i < gNM; ++i) {
+      mbar_init(&bar_rfull[i], 1);
+      mbar_init(&bar_rempty[i], CS);
+    }
+    for (int i = 0; i < NE; ++i) {
       mbar_init(&bar_efull[i], 1);
       mbar_init(&bar_efree[i], 4);
     }
-    for (int i = 0; i < gRing; ++i) mbar_init(&bar_mdone[i], 1);
-    for (int i = 0; i < gBufs; ++i) mbar_init(&bar_wfree[i], 4);
+    for (int i = 0; i < gBufs; ++i) {
+      mbar_init(&bar_mdone[i], 1);
+      mbar_init(&bar_wfree[i], 4);
+    }
     mbar_init(&bar_lready, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -111,70 +261,100 @@ __global__ void __launch_bounds__(gThreads, 1)
   }
   tc_before();
   __syncthreads();
+  if (CS > 1) cluster_sync_all();  // peers multicast into this CTA's ring and barriers
   tc_after();
   const uint32_t tmem = tmem_slot;
 
-  if (warp == gWarpProd) {
-    // ------------------------------------------------------------ producer
-    // Ring slots / phases advance incrementally (no runtime divisions in the
-    // single-warp loops).
-    int sm = 0, se = 0, eround = 0;
+  if (warp < gIssuers) {
+    // ------------------------------------------------------------ issuer q
+    // Tiles t = q, q + 4, ...: R_J stage t % 4 and W buffer t % 6.  R_J stage
+    // = nbox boxes of 64 points x 128 bytes (hi / lo planes x spk / 32); CTA
+    // rank r of the cluster loads boxes r, r + cs, ... multicast to every
+    // CTA, so the cluster reads R once.  The next own tile's loads are issued
+    // as soon as every CTA's MMA released the stage (3 tiles of lead).
+    const int q = warp;
+    constexpr uint32_t idesc = idesc_tf32(gTI, gTJ);
     const uint32_t plane = p.mstage / 2;
-    for (int t = 0; t < T; ++t) {
+    const int nbox = 2 * (p.spk / 32);
+    long long tw1 = 0, tw2 = 0;
+    const long long tstart = clock64();
+    auto load = [&](int t) {
+      const int sm = t & (gNM - 1);
       const int pt = (jt_begin + t) * gTJ;
-      if (t >= NM) mbar_wait(&bar_mdone[(t - NM) & (gRing - 1)], ((t - NM) >> 3) & 1);
       uint8_t* rb = sR + static_cast<size_t>(sm) * p.mstage;
-      mbar_expect_tx_warp(&bar_rfull[sm], p.mstage);
-      for (int kb = 0; kb < p.spk / 32; ++kb) {
-        tma_load_2d_warp(rb + kb * 8192, &mRhi, &bar_rfull[sm], 32 * kb, pt);
-        tma_load_2d_warp(rb + plane + kb * 8192, &mRlo, &bar_rfull[sm], 32 * kb, pt);
+      if (p.dbg & 4) {
+        mbar_arrive_warp(&bar_rfull[sm]);
+      } else {
+        mbar_expect_tx_warp(&bar_rfull[sm], p.mstage);
+        for (int bi = static_cast<int>(crank); bi < nbox; bi += CS) {
+          const int kb = bi >> 1;
+          uint8_t* dst = rb + (bi & 1) * plane + kb * 8192;
+          const CUtensorMap* map = (bi & 1) ? &mRlo : &mRhi;
+          if (CS > 1)
+            tma_load_2d_mc_warp(dst, map, &bar_rfull[sm], 32 * kb, pt, cmask);
+          else
+            tma_load_2d_warp(dst, map, &bar_rfull[sm], 32 * kb, pt);
+        }
       }
-      if (eround > 0) mbar_wait(&bar_efree[se], (eround - 1) & 1);
+      const int se = t % NE;
+      const long long c1 = p.trace ? clock64() : 0;
+      if (t >= NE) mbar_wait(&bar_efree[se], ((t - NE) / NE) & 1);
+      if (p.trace) tw2 += clock64() - c1;
       mbar_expect_tx_warp(&bar_efull[se], p.estage);
       bulk_load_warp(const_cast<float*>(sE) + se * (p.estage / 4), p.xv + static_cast<int64_t>(pt) * EP, p.estage,
                      &bar_efull[se]);
-      if (++sm == NM) sm = 0;
-      if (++se == gNE) se = 0, ++eround;
-    }
-  } else if (warp == gWarpMma) {
-    // ------------------------------------------------------------ MMA issuer
-    // W(t) = L_I R_J^T into buffer t % 6: spk / 8 K steps of 3xTF32, A (L_I
-    // hi / lo) from TMEM, B (R_J hi / lo, 64 points x 8 K, 128-byte swizzle) from shared memory.
-    if (T > 0) {
-      constexpr uint32_t idesc = idesc_tf32(gTI, gTJ);
+    };
+    if (q < T) {
+      load(q);
       mbar_wait(&bar_lready, 0);
       tc_after();
-      const int nk = p.spk / 8;
-      const uint32_t plane = p.mstage / 2;
-      int sm = 0, b = 0, bround = 0;
-      uint32_t rph = 0;
-      for (int t = 0; t < T; ++t) {
-        if (bround > 0) mbar_wait(&bar_wfree[b], (bround - 1) & 1);
-        mbar_wait(&bar_rfull[sm], rph);
-        tc_after();
-        const uint8_t* rb = sR + static_cast<size_t>(sm) * p.mstage;
-        const uint32_t dcol = tmem + static_cast<uint32_t>(b) * gTJ;
-#pragma unroll 8
-        for (int k = 0; k < nk; ++k) {
-          const uint64_t dh = umma_desc(rb + (k >> 2) * 8192) + 2 * (k & 3);
-          const uint64_t dl = umma_desc(rb + plane + (k >> 2) * 8192) + 2 * (k & 3);
-          mma3_ts(dcol, tmem + gLhi + 8 * k, tmem + gLlo + 8 * k, dh, dl, idesc, k > 0 ? 1u : 0u);
-        }
-        mma_commit(&bar_mdone[t & (gRing - 1)]);
-        if (++sm == NM) sm = 0, rph ^= 1u;
-        if (++b == gBufs) b = 0, ++bround;
-      }
     }
-  } else if (warp < gEpiWarps) {
+    for (int t = q; t < T; t += gIssuers) {
+      const int sm = t & (gNM - 1), b = t % gBufs;
+      const long long c0 = p.trace ? clock64() : 0;
+      if (t >= gBufs) mbar_wait(&bar_wfree[b], ((t - gBufs) / gBufs) & 1);
+      mbar_wait(&bar_rfull[sm], (t >> 2) & 1);
+      if (p.trace) tw1 += clock64() - c0;
+      tc_after();
+      if (!(p.dbg & 1)) {
+        const uint8_t* rb = sR + static_cast<size_t>(sm) * p.mstage;
+        const uint64_t dh = umma_desc(rb), dl = umma_desc(rb + plane);
+        const uint32_t dcol = tmem + static_cast<uint32_t>(b) * gTJ;
+        if (p.spk == 64)
+          mma_w_k64(dcol, tmem + gLhi, dh, dl, idesc);
+        else
+          mma_w_k32(dcol, tmem + gLhi, dh, dl, idesc);
+      }
+      mma_commit(&bar_mdone[b]);
+      if (CS > 1)
+        mma_commit_mc(&bar_rempty[sm], cmask);
+      else
+        mma_commit(&bar_rempty[sm]);
+      // the stage's next use (own tile t + 4) once all cs CTAs released it;
+      // after the last own tile this wait drains the peers' arrivals before exit
+      mbar_wait(&bar_rempty[sm], (t >> 2) & 1);
+      if (t + gIssuers < T) load(t + gIssuers);
+    }
+    if (p.trace && lane == 0) {
+      unsigned long long* tr = p.trace + warp * 4;
+      atomicAdd(tr + 0, static_cast<unsigned long long>(clock64() - tstart));
+      atomicAdd(tr + 1, static_cast<unsigned long long>(tw1));
+      atomicAdd(tr + 2, static_cast<unsigned long long>(tw2));
+    }
+  } else if (warp >= gEpiBase) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3, w = warp >> 2;
+    const int ew = warp - gEpiBase;  // epilogue warp index 0..11
+    const int q = warp & 3, w = ew >> 2;
     const int row = q * 32 + lane;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
     const int64_t gi = static_cast<int64_t>(rt) * gTI + row;
     const bool valid = gi < p.n;
-    float xi[D];
+    float2 xi[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) xi[k] = valid ? p.xs[gi * p.dp + k] : 0.f;
+    for (int k = 0; k < D; ++k) {
+      const float v = valid ? p.xs[gi * p.dp + k] : 0.f;
+      xi[k] = make_float2(v, v);
+    }
     const float hvy = valid ? 0.5f * p.vy[gi] : 0.f;
     if (w == 0 && T > 0) {
       // L_I (row gi, columns [0, spk), zero past s and past n) -> TMEM hi / lo planes
@@ -196,66 +376,93 @@ __global__ void __launch_bounds__(gThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_lready);
     }
-    double* acc64 = sAcc + warp * 32 + lane;  // slot k at acc64[k * 384]
+    double* acc64 = sAcc + ew * 32 + lane;  // slot k at acc64[k * 384]
 #pragma unroll
     for (int k = 0; k < NW; ++k) acc64[k * gEpiThreads] = 0.0;
-    const float sf2 = p.sf2, ac = p.a;
-    float A[D + 1], B[D + 1];
+    const float2 sf2 = make_float2(p.sf2, p.sf2), ac = make_float2(p.a, p.a);
+    float2 A[D + 1], B[D + 1];
 #pragma unroll
-    for (int k = 0; k <= D; ++k) A[k] = B[k] = 0.f;
+    for (int k = 0; k <= D; ++k) A[k] = B[k] = make_float2(0.f, 0.f);
     auto flush = [&]() {
 #pragma unroll
       for (int k = 0; k <= D; ++k) {
-        acc64[k * gEpiThreads] += static_cast<double>(A[k]);
-        acc64[(D + 1 + k) * gEpiThreads] += static_cast<double>(B[k]);
-        A[k] = B[k] = 0.f;
+        acc64[k * gEpiThreads] += static_cast<double>(A[k].x) + static_cast<double>(A[k].y);
+        acc64[(D + 1 + k) * gEpiThreads] += static_cast<double>(B[k].x) + static_cast<double>(B[k].y);
+        A[k] = B[k] = make_float2(0.f, 0.f);
       }
     };
+    // points per shared load: 4 (two pairs) while the registers allow it
+    constexpr int QP = D <= 6 ? 4 : 2;
+    const uint32_t sE_u32 = smem_u32(sE);
     int since = 0;
+    long long tw1 = 0, tw2 = 0, tw3 = 0;
+    const long long tstart = clock64();
     for (int t = w; t < T; t += gEpiGroups) {
-      const int b = t % gBufs, se = t % gNE;
-      mbar_wait(&bar_mdone[t & (gRing - 1)], (t >> 3) & 1);
-      mbar_wait(&bar_efull[se], (t / gNE) & 1);
-      tc_after();
-      const float* ev = sE + se * (p.estage / 4);
-#pragma unroll 1
-      for (int h = 0; h < gTJ / 16; ++h) {
-        uint32_t wr[16];
-        __syncwarp();
-        tmem_ld16(tmem + lanes + static_cast<uint32_t>(b * gTJ + 16 * h), wr);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float* xj = ev + (16 * h + e) * EP;  // warp-uniform: shared-memory broadcast
-          float xv[EP];
-#pragma unroll
-          for (int c = 0; c < EP / 4; ++c) {
-            const float4 v = *reinterpret_cast<const float4*>(xj + 4 * c);
-            xv[4 * c] = v.x, xv[4 * c + 1] = v.y, xv[4 * c + 2] = v.z, xv[4 * c + 3] = v.w;
-          }
-          float dq[D];
-          float r2 = 0.f;
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            const float df = xi[k] - xv[k];
-            r2 = fmaf(df, df, r2);
-            dq[k] = df * df;
-          }
-          const float u = sqrt_approx(r2);
-          const float dec = ex2_approx(-u);
-          const float kv = fmaf(ac, u, sf2) * dec;
-          const float vyj = xv[D];
-          const float wb = __uint_as_float(wr[e]);
-          const float dA = dec * vyj, dB = dec * wb;
-#pragma unroll
-          for (int k = 0; k < D; ++k) {
-            A[k] = fmaf(dq[k], dA, A[k]);
-            B[k] = fmaf(dq[k], dB, B[k]);
-          }
-          A[D] = fmaf(kv, vyj, A[D]);
-          B[D] = fmaf(kv, wb, B[D]);
-        }
+      const int b = t % gBufs, se = t % NE;
+      long long c0 = p.trace ? clock64() : 0;
+      mbar_wait(&bar_mdone[b], (t / gBufs) & 1);
+      long long c1 = p.trace ? clock64() : 0;
+      mbar_wait(&bar_efull[se], (t / NE) & 1);
+      if (p.trace) {
+        const long long c2 = clock64();
+        tw1 += c1 - c0;
+        tw2 += c2 - c1;
       }
+      tc_after();
+      const uint32_t ev = sE_u32 + static_cast<uint32_t>(se) * p.estage;  // [D + 1][64] fp32
+      // 16-column chunks of W(t); the TMEM load of chunk h + 1 is in flight
+      // while chunk h is processed (tcgen05.wait::ld waits for all loads, so
+      // two register buffers alternate)
+      auto chunk = [&](int h, const uint32_t(&wr)[16]) {
+        if (p.dbg & 2) {
+          A[0].x += __uint_as_float(wr[h]);
+          return;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; e += QP) {
+          const uint32_t col = ev + static_cast<uint32_t>(16 * h + e) * 4u;  // warp-uniform: broadcast loads
+          if constexpr (QP == 4) {
+            float2 n0[D], n1[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              const float4 v = lds128(col + k * 256);
+              n0[k] = make_float2(v.x, v.y);
+              n1[k] = make_float2(v.z, v.w);
+            }
+            const float4 vy = lds128(col + D * 256);
+            entry_pair<D>(xi, n0, make_float2(vy.x, vy.y),
+                          make_float2(__uint_as_float(wr[e]), __uint_as_float(wr[e + 1])), sf2, ac, A, B);
+            entry_pair<D>(xi, n1, make_float2(vy.z, vy.w),
+                          make_float2(__uint_as_float(wr[e + 2]), __uint_as_float(wr[e + 3])), sf2, ac, A, B);
+          } else {
+            float2 n0[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) n0[k] = lds64(col + k * 256);
+            entry_pair<D>(xi, n0, lds64(col + D * 256),
+                          make_float2(__uint_as_float(wr[e]), __uint_as_float(wr[e + 1])), sf2, ac, A, B);
+          }
+        }
+      };
+      const uint32_t wcol = tmem + lanes + static_cast<uint32_t>(b * gTJ);
+      uint32_t w0[16], w1[16];
+      __syncwarp();
+      const long long c3 = p.trace ? clock64() : 0;
+      tmem_ld16(wcol, w0);
+      tmem_wait_ld();
+      if (p.trace) tw3 += clock64() - c3;
+      tmem_ld16(wcol + 16, w1);
+      chunk(0, w0);
+      tmem_wait_ld();
+      pin(w1);
+      tmem_ld16(wcol + 32, w0);
+      chunk(1, w1);
+      tmem_wait_ld();
+      pin(w0);
+      tmem_ld16(wcol + 48, w1);
+      chunk(2, w0);
+      tmem_wait_ld();
+      pin(w1);
+      chunk(3, w1);
       tc_before();
       __syncwarp();
       if (lane == 0) {
@@ -268,13 +475,20 @@ __global__ void __launch_bounds__(gThreads, 1)
       }
     }
     flush();
+    if (p.trace && lane == 0) {
+      unsigned long long* tr = p.trace + warp * 4;
+      atomicAdd(tr + 0, static_cast<unsigned long long>(clock64() - tstart));
+      atomicAdd(tr + 1, static_cast<unsigned long long>(tw1));
+      atomicAdd(tr + 2, static_cast<unsigned long long>(tw2));
+      atomicAdd(tr + 3, static_cast<unsigned long long>(tw3));
+    }
     // row scale (W^A = vy_i vy_j / 2: the vy_i / 2 factor; coef_b for W^B),
     // then the fixed-order warp sums
 #pragma unroll
     for (int k = 0; k < NW; ++k) {
       double v = acc64[k * gEpiThreads] * (k <= D ? static_cast<double>(hvy) : static_cast<double>(p.coef_b));
       v = warp_sum(v);
-      if (lane == 0) wacc[warp][k] = v;
+      if (lane == 0) wacc[ew][k] = v;
     }
   }
   tc_before();
@@ -285,11 +499,12 @@ __global__ void __launch_bounds__(gThreads, 1)
     for (int w = 0; w < gEpiWarps; ++w) s += wacc[w][threadIdx.x];
     p.part[static_cast<int64_t>(blockIdx.x) * NW + threadIdx.x] = s;
   }
+  if (CS > 1) cluster_sync_all();
   if (warp == gWarpAlloc) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // R (column-major, ld) -> tf32 hi / lo planes [n_pad][spk] (point-major, K
-// contiguous: the MMA's K-major B operand), and xv [n_pad][ep] = x_j | vy_j.
+// contiguous: the MMA's K-major B operand), and the epilogue stages xv.
 // 32 points per CTA through a shared-memory transpose (coalesced both ways).
 __global__ void grad_tc_prep_kernel(const float* R, int64_t ld, int s, const float* xs, int dp, int d,
                                     const float* vy, int64_t n, int spk, int ep, float* rhi, float* rlo, float* xv) {
@@ -305,12 +520,13 @@ __global__ void grad_tc_prep_kernel(const float* R, int64_t ld, int s, const flo
       rhi[(i0 + r) * spk + c] = h;
       rlo[(i0 + r) * spk + c] = v - h;
     }
-    for (int k = tx; k < ep; k += 32) {
-      const int64_t i = i0 + r;
-      float v = 0.f;
-      if (i < n) v = k < d ? xs[i * dp + k] : (k == d ? vy[i] : 0.f);
-      xv[i * ep + k] = v;
-    }
+  }
+  // epilogue stage: tile-major [n_pad / 64][ep][64], rows -x_jk (k < d) and vy_j
+  for (int k = ty; k < ep; k += 8) {
+    const int64_t i = i0 + tx;
+    float v = 0.f;
+    if (i < n) v = k < d ? -xs[i * dp + k] : vy[i];
+    xv[(i / 64) * (ep * 64) + k * 64 + (i % 64)] = v;
   }
 }
 
@@ -338,7 +554,19 @@ void launch_grad_tc(const CUtensorMap& mh, const CUtensorMap& ml, const GradTcAr
     WGP_CUDA(cudaFuncSetAttribute(grad_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, gSmemLimit));
     configured = true;
   }
-  grad_tc_kernel<D><<<grid, gThreads, smem, st>>>(mh, ml, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(gThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(a.cs);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  WGP_CUDA(cudaLaunchKernelEx(&cfg, grad_tc_kernel<D>, mh, ml, a));
   WGP_LAUNCH_CHECK();
 }
 
@@ -351,14 +579,23 @@ GradTcPlan grad_tc_plan(int64_t n, int d, int s) {
   pl.n_pad = round_up(std::max<int64_t>(n, 1), gTJ);
   pl.spk = s <= 32 ? 32 : 64;
   pl.ep = ep_of(d);
+  // cluster size: CTAs sharing the R_J stream (<= boxes per stage)
+  static const int env_cs = [] {
+    const char* e = getenv("WGP_GRAD_CLUSTER");
+    return e ? atoi(e) : 0;
+  }();
+  const int nbox = 2 * (pl.spk / 32);
+  pl.cs = std::min(nbox, env_cs == 1 || env_cs == 2 || env_cs == 4 ? env_cs : 2);
   const int64_t row_tiles = ceil_div(n, gTI);
+  if (row_tiles < pl.cs) pl.cs = 1;
+  pl.rt_pad = static_cast<int>(round_up(row_tiles, pl.cs));
   const int jt = static_cast<int>(ceil_div(n, gTJ));
   static const int force = [] {
     const char* e = getenv("WGP_GRAD_SPLITS");
     return e ? atoi(e) : 0;
   }();
-  pl.splits = force > 0 ? std::min(force, jt) : choose_grad_splits(row_tiles, jt, tc_sm_count());
-  pl.nblk = static_cast<int>(row_tiles * pl.splits);
+  pl.splits = force > 0 ? std::min(force, jt) : choose_grad_splits(pl.rt_pad, jt, tc_sm_count());
+  pl.nblk = static_cast<int>(pl.rt_pad * pl.splits);
   pl.ws_bytes = sizeof(float) * static_cast<size_t>(pl.n_pad) * (2 * pl.spk + pl.ep);
   return pl;
 }
@@ -381,14 +618,16 @@ void grad_tc(const GradParams& p, const GradTcPlan& pl, void* ws, cudaStream_t s
   a.spk = pl.spk;
   a.num_jt = static_cast<int>(ceil_div(p.n, gTJ));
   a.splits = pl.splits;
+  a.cs = pl.cs;
+  a.rt_pad = pl.rt_pad;
   a.mstage = 2u * static_cast<uint32_t>(pl.spk / 32) * 8192u;
   a.estage = static_cast<uint32_t>(gTJ * pl.ep * 4);
   const int acc_bytes = 2 * (p.d + 1) * gEpiThreads * 8;
-  const int fixed = gNE * static_cast<int>(a.estage) + acc_bytes + 1024;
-  a.nm = std::min(gMaxNM, (gSmemLimit - fixed) / static_cast<int>(a.mstage));
-  if (a.nm < 2) throw DeviceError("grad_tc: shared memory too small for the R ring");
-  a.acc_off = static_cast<uint32_t>(a.nm) * a.mstage + gNE * a.estage;
+  a.ne = gMaxNE;
+  if (gNM * static_cast<int>(a.mstage) + a.ne * static_cast<int>(a.estage) + acc_bytes + 1024 > gSmemLimit) a.ne = 4;
+  a.acc_off = gNM * a.mstage + static_cast<uint32_t>(a.ne) * a.estage;
   const int smem = static_cast<int>(a.acc_off) + acc_bytes + 1024;
+  if (smem > gSmemLimit) throw DeviceError("grad_tc: shared memory too small");
   a.xs = p.xs;
   a.vy = p.vy;
   a.xv = xv;
@@ -398,11 +637,25 @@ void grad_tc(const GradParams& p, const GradTcPlan& pl, void* ws, cudaStream_t s
   a.a = p.a;
   a.coef_b = p.coef_b;
   a.part = p.part;
+  static const int dbg = [] {
+    const char* e = getenv("WGP_GRAD_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  a.dbg = dbg;
+  static const bool tracing = getenv("WGP_GRAD_TRACE") != nullptr;
+  static unsigned long long* trace = nullptr;
+  a.trace = nullptr;
+  if (tracing) {
+    if (!trace) WGP_CUDA(cudaMalloc(&trace, sizeof(unsigned long long) * 64));
+    WGP_CUDA(cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 64, st));
+    a.trace = trace;
+  }
   const unsigned grid = static_cast<unsigned>(pl.nblk);
   switch (p.d) {
 #define WGP_GRAD_CASE(D) \
   case D:                \
-    return launch_grad_tc<D>(mh, ml, a, grid, smem, st);
+    launch_grad_tc<D>(mh, ml, a, grid, smem, st); \
+    break;
     WGP_GRAD_CASE(1)
     WGP_GRAD_CASE(2)
     WGP_GRAD_CASE(3)
@@ -418,6 +671,20 @@ void grad_tc(const GradParams& p, const GradTcPlan& pl, void* ws, cudaStream_t s
 #undef WGP_GRAD_CASE
     default:
       throw std::invalid_argument("grad_tc: unsupported d");
+  }
+  if (tracing) {
+    // per warp: {total, wait A, wait B, wait C} clk summed over CTAs.  Epilogue
+    // warps: A = mdone (W ready), B = efull (x_j | vy_j), C = first TMEM load;
+    // MMA warp: A = wfree, B = rfull; producer: A = rempty, B = efree.
+    unsigned long long h[64];
+    WGP_CUDA(cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    for (int w = 0; w < 16; ++w) {
+      const double tot = static_cast<double>(h[4 * w]);
+      if (tot <= 0) continue;
+      fprintf(stderr, "[grad_tc trace] warp %2d: total %.3e clk  waitA %5.1f%%  waitB %5.1f%%  waitC %5.1f%%\n", w, tot,
+              100.0 * h[4 * w + 1] / tot, 100.0 * h[4 * w + 2] / tot, 100.0 * h[4 * w + 3] / tot);
+    }
   }
 }
 

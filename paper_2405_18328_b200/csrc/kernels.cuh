@@ -82,6 +82,7 @@ void grad_simt(const GradParams& p, cudaStream_t st);
 struct GradTcPlan {
   int64_t n_pad = 0;
   int spk = 0, ep = 0, splits = 1, nblk = 0;
+  int cs = 1, rt_pad = 0;  // cluster size sharing the R stream, row tiles padded to it
   size_t ws_bytes = 0;
 };
 bool grad_tc_supported(int d, int s);
