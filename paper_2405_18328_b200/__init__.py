@@ -93,7 +93,9 @@ EXPORTS = [
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, _LIB_NAME)
+    # WGP_LIBRARY: an alternative build of the same library (A/B timing of
+    # kernel variants in one process tree); default the in-tree build
+    return os.environ.get("WGP_LIBRARY") or os.path.join(_HERE, _LIB_NAME)
 
 
 def load():

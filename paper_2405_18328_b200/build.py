@@ -34,7 +34,7 @@ def nvcc() -> str:
 def flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                    "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-                   "-Xptxas", "-warn-spills"]
+                   "-Xptxas", "-warn-spills"] + os.environ.get("WGP_NVCC_DEFS", "").split()  # dev A/B variants
 
 
 def _stale(target, deps):

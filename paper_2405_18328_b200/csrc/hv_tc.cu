@@ -142,7 +142,15 @@ struct TcArgs {
 //     from 192 of one tile each (S: 64 fp32 columns, overwritten by the packed
 //     k1 | k2 pairs); A_I stays in shared memory (SS MMA-1).
 // The Gram (MMA-1) is 3xTF32 in both, over 64 points per instruction.
-constexpr bool kTfSingleO = true;
+// tf32 TMEM layout (compile-time WGP_TC_LAYOUT): 0 = single O [0, 96), A_I in
+// shared memory, three groups from 96; 1 = O0 | O1 [0, 192), A_I in shared
+// memory, two groups from 192 (4 tiles in flight, no chunk-drain stall of
+// MMA-2); 2 = O0 | O1, A_I in TMEM [192, 256), two groups from 256.
+#ifndef WGP_TC_LAYOUT
+#define WGP_TC_LAYOUT 2
+#endif
+constexpr bool kTfSingleO = WGP_TC_LAYOUT == 0;
+constexpr bool kTfATmem = WGP_TC_LAYOUT == 2;
 constexpr int kTfGroups = kTfSingleO ? 3 : 2;
 template <bool BF>
 struct Cfg {
@@ -155,11 +163,11 @@ struct Cfg {
   // tf32 layout variant (kTfSingleO): one O accumulator [0, 96) whose chunk
   // drains stall MMA-2, A_I in shared memory (SS Gram), three groups from 96
   // (6 tiles in flight); otherwise O0 | O1, A_I in TMEM, two groups from 256.
-  static constexpr bool kATmem = !BF && !kTfSingleO;
+  static constexpr bool kATmem = !BF && kTfATmem;
   static constexpr int kOBufs = (BF || !kTfSingleO) ? 2 : 1;
   static constexpr uint32_t kOStride = kOBufs == 2 ? 96u : 0u;
   static constexpr uint32_t kAhi = 192, kAlo = 224;  // kATmem only
-  static constexpr uint32_t kBufFirst = BF ? 192u : (kTfSingleO ? 96u : 256u);
+  static constexpr uint32_t kBufFirst = BF ? 192u : (kTfSingleO ? 96u : (kATmem ? 256u : 192u));
   static constexpr uint32_t kBStage = 2u * kN1 * 128u;  // B_hi | B_lo planes
   static constexpr uint32_t kLoOff = 64;                // BF = false: k_lo column offset
   static __device__ __forceinline__ uint32_t grp_col(int gi) { return kBufFirst + kGW * static_cast<uint32_t>(gi); }
@@ -341,11 +349,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + K::kBStage / 2);
         const uint32_t d = tmem + K::grp_col(gi);
         if (!(p.dbg & 4)) {
+          if constexpr (!K::kATmem) {
+            mma1_group_tf32(d, dAhi, dAlo, dBhi, dBlo, id1);
+          } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if constexpr (!K::kATmem)
-              mma3_ss(d, dAhi + 2 * k, dAlo + 2 * k, dBhi + 2 * k, dBlo + 2 * k, id1, k > 0);
-            else
+            for (int k = 0; k < 4; ++k)
               mma3_ts(d, tmem + K::kAhi + 8 * k, tmem + K::kAlo + 8 * k, dBhi + 2 * k, dBlo + 2 * k, id1,
                       k > 0);
           }
@@ -372,14 +380,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int cp = c - K::kOBufs;
           mbar_wait(&bar_odrained[cp & 1], (cp >> 1) & 1);
         }
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 12] = clock64();
         mbar_wait(&bar_vfull[st], vph);
+        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 13] = clock64();
         mbar_wait(&bar_kfull[b], kph);
         tc_after();
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 3] = clock64();
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const uint32_t kb = tmem + K::tile_col(t);
         const uint64_t dv = umma_desc(base);
-        if (!(p.dbg & 2)) {
+        if (!(p.dbg & 2) && !BF) {
+          static_assert(BF || K::kLoOff == 64, "mma2_tile_tf32 assumes k_lo 64 columns after k_hi");
+          mma2_tile_tf32(o, kb, dv, dv + box, id2, tc > 0 ? 1u : 0u);
+        } else if (!(p.dbg & 2)) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             if constexpr (BF) {
@@ -1114,6 +1127,20 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
       v[8] += r[0] - r[7];   // MMA-1 issuing + commits
       v[9] += n[6] - r[6];   // MMA-1 period
       ++cnt;
+    }
+    {
+      double w_od = 0, w_v = 0, w_k = 0;
+      int m = 0;
+      for (int t = 8; t + 2 < T0; ++t) {
+        const long long* r = &h[16 * t];
+        w_od += r[12] - r[4];
+        w_v += r[13] - r[12];
+        w_k += r[3] - r[13];
+        ++m;
+      }
+      if (m)
+        fprintf(stderr, "[hv_tc trace] MMA-2 waits per tile: odrained %.0f  vfull %.0f  kfull %.0f clk\n", w_od / m,
+                w_v / m, w_k / m);
     }
     if (cnt)
       fprintf(stderr,

@@ -32,6 +32,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     if (ok) break;
   }
 }
+// Non-blocking phase test (whole warp, uniform).
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// One try_wait probe: suspends the warp for up to a hardware time limit
+// while the phase is incomplete (no issue-slot spinning), then reports.
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -165,6 +186,95 @@ __device__ __forceinline__ void bulk_load_warp(void* dst, const void* src, uint3
       : "memory");
 }
 
+// The 12 MMAs of one MMA-1 group (Gram, 4 K steps of 3xTF32, A and B from
+// shared memory) from one asm block and one elect: per-k descriptors by
+// immediate adds.  Per-k-step helper calls cost the issuing warp ~45
+// instructions each (elect, uniform-register moves, descriptor math), taken
+// from the epilogue warps of the same SMSP (measured in grad_tc).
+__device__ __forceinline__ void mma1_group_tf32(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                                uint32_t idesc) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b64 xh, xl, yh, yl;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.s64 xh, %1, 0;\n"
+      " add.s64 xl, %2, 0;\n"
+      " add.s64 yh, %3, 0;\n"
+      " add.s64 yl, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xh, yh, %5, f;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xh, yl, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xl, yh, %5, t;\n"
+      " add.s64 xh, %1, 2;\n"
+      " add.s64 xl, %2, 2;\n"
+      " add.s64 yh, %3, 2;\n"
+      " add.s64 yl, %4, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xh, yh, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xh, yl, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xl, yh, %5, t;\n"
+      " add.s64 xh, %1, 4;\n"
+      " add.s64 xl, %2, 4;\n"
+      " add.s64 yh, %3, 4;\n"
+      " add.s64 yl, %4, 4;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xh, yh, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xh, yl, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xl, yh, %5, t;\n"
+      " add.s64 xh, %1, 6;\n"
+      " add.s64 xl, %2, 6;\n"
+      " add.s64 yh, %3, 6;\n"
+      " add.s64 yl, %4, 6;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xh, yh, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xh, yl, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], xl, yh, %5, t;\n"
+      "}\n"
+      ::"r"(d), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc));
+}
+// The 12 MMAs of one MMA-2 tile (K.V, 4 K steps of 3xTF32: k_hi / k_lo in
+// TMEM at kcol / kcol + 64, V hi / lo descriptors vh / vl) from one asm block
+// and one elect; acc = 0 starts the accumulator (first tile of a chunk).
+__device__ __forceinline__ void mma2_tile_tf32(uint32_t o, uint32_t kcol, uint64_t vh, uint64_t vl, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, p, t;\n"
+      " .reg .b32 ah, al;\n"
+      " .reg .b64 yh, yl;\n"
+      " setp.ne.b32 p, %5, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 ah, %1, 0;\n"
+      " add.u32 al, %1, 64;\n"
+      " add.s64 yh, %2, 0;\n"
+      " add.s64 yl, %3, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], yh, %4, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], yh, %4, t;\n"
+      " add.u32 ah, %1, 8;\n"
+      " add.u32 al, %1, 72;\n"
+      " add.s64 yh, %2, 2;\n"
+      " add.s64 yl, %3, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], yh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], yh, %4, t;\n"
+      " add.u32 ah, %1, 16;\n"
+      " add.u32 al, %1, 80;\n"
+      " add.s64 yh, %2, 4;\n"
+      " add.s64 yl, %3, 4;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], yh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], yh, %4, t;\n"
+      " add.u32 ah, %1, 24;\n"
+      " add.u32 al, %1, 88;\n"
+      " add.s64 yh, %2, 6;\n"
+      " add.s64 yl, %3, 6;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], yh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], yh, %4, t;\n"
+      "}\n"
+      ::"r"(o), "r"(kcol), "l"(vh), "l"(vl), "r"(idesc), "r"(acc));
+}
 // TMA 2D load multicast to the CTAs of `mask` in the cluster: the box lands at
 // the same shared-memory offset in each and completes tx bytes on the
 // mbarrier at the same offset in each (one elected lane).

@@ -23,7 +23,7 @@ for impl in ("tc", "tc_bf16"):
 # Gram-only error: V = e_j columns pick single entries of K
 c.set_hv_impl("tc")
 """ % ROOT
-for chunk in ("8", "16", "32", "100000"):
+for chunk in (sys.argv[1:] or ["8", "16", "32", "100000"]):
     env = dict(os.environ, WGP_TC_CHUNK=chunk, WGP_TC_SPLITS="1")
     r = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True)
     print("chunk", chunk, r.stdout.replace("\n", "  "), r.stderr[-300:])
