@@ -352,10 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (!K::kATmem) {
             mma1_group_tf32(d, dAhi, dAlo, dBhi, dBlo, id1);
           } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma3_ts(d, tmem + K::kAhi + 8 * k, tmem + K::kAlo + 8 * k, dBhi + 2 * k, dBlo + 2 * k, id1,
-                      k > 0);
+            mma1_group_tf32_ts(d, tmem + K::kAhi, tmem + K::kAlo, dBhi, dBlo, id1);
           }
         }
         mma_commit(&bar_m1done[gr & (kDoneRing - 1)]);

@@ -231,6 +231,49 @@ __device__ __forceinline__ void mma1_group_tf32(uint32_t d, uint64_t ah, uint64_
       "}\n"
       ::"r"(d), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc));
 }
+// MMA-1 group with A_I in TMEM (hi at column ah, lo at al): 12 MMAs, one
+// asm block and one elect, as mma1_group_tf32.
+__device__ __forceinline__ void mma1_group_tf32_ts(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+                                                   uint32_t idesc) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t;\n"
+      " .reg .b32 xh, xl;\n"
+      " .reg .b64 yh, yl;\n"
+      " setp.ne.b32 f, 0, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 xh, %1, 0;\n"
+      " add.u32 xl, %2, 0;\n"
+      " add.s64 yh, %3, 0;\n"
+      " add.s64 yl, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xh], yh, %5, f;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xh], yl, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xl], yh, %5, t;\n"
+      " add.u32 xh, %1, 8;\n"
+      " add.u32 xl, %2, 8;\n"
+      " add.s64 yh, %3, 2;\n"
+      " add.s64 yl, %4, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xh], yh, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xh], yl, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xl], yh, %5, t;\n"
+      " add.u32 xh, %1, 16;\n"
+      " add.u32 xl, %2, 16;\n"
+      " add.s64 yh, %3, 4;\n"
+      " add.s64 yl, %4, 4;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xh], yh, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xh], yl, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xl], yh, %5, t;\n"
+      " add.u32 xh, %1, 24;\n"
+      " add.u32 xl, %2, 24;\n"
+      " add.s64 yh, %3, 6;\n"
+      " add.s64 yl, %4, 6;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xh], yh, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xh], yl, %5, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [xl], yh, %5, t;\n"
+      "}\n"
+      ::"r"(d), "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc));
+}
 // The 12 MMAs of one MMA-2 tile (K.V, 4 K steps of 3xTF32: k_hi / k_lo in
 // TMEM at kcol / kcol + 64, V hi / lo descriptors vh / vl) from one asm block
 // and one elect; acc = 0 starts the accumulator (first tile of a chunk).
