@@ -205,6 +205,12 @@ int wgp_adam_step(double* raw, const double* grad, double* m, double* v, int p, 
 /** Utilities of the reference's common.hpp:25-36. */
 uint64_t wgp_derive_seed(uint64_t base, uint64_t stream);
 
+/** Row permutation of split_standardize (proj/src/dataset.cpp:118-124):
+ *  order = 0..n-1 shuffled by Fisher-Yates from the back with
+ *  mt19937_64(derive_seed(split_seed, 0x5b117)) and uniform_below -- bitwise
+ *  the reference's permutation (host-only, no device work). */
+int wgp_split_order(int64_t n, uint64_t split_seed, int64_t* order);
+
 #ifdef __cplusplus
 }
 #endif

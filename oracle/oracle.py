@@ -87,6 +87,7 @@ def lib():
             getattr(_lib, name).restype = C.c_uint64
         _lib.or_splitmix64.argtypes = [C.c_uint64]
         _lib.or_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        _lib.or_split_order.argtypes = [C.c_int64, C.c_uint64, C.c_void_p]
         for name in ("or_softplus", "or_softplus_inverse", "or_softplus_derivative"):
             getattr(_lib, name).restype = C.c_double
             getattr(_lib, name).argtypes = [C.c_double]
@@ -125,6 +126,13 @@ def splitmix64(x: int) -> int:
 
 def derive_seed(base: int, stream: int) -> int:
     return int(lib().or_derive_seed(C.c_uint64(base), C.c_uint64(stream)))
+
+
+def split_order(n: int, split_seed: int) -> np.ndarray:
+    """dataset.cpp:118-124: split_standardize's row permutation."""
+    out = np.empty(int(n), dtype=np.int64)
+    _check(lib().or_split_order(int(n), C.c_uint64(split_seed), out.ctypes.data))
+    return out
 
 
 def softplus(x):

@@ -919,6 +919,18 @@ uint64_t or_derive_seed(uint64_t base, uint64_t stream) {  // common.hpp:34-36
   return or_splitmix64(or_splitmix64(base) ^ or_splitmix64(stream + 0x51ed2701ab0a3c11ULL));
 }
 
+// dataset.cpp:118-124 (split_standardize's permutation)
+int or_split_order(int64_t n, uint64_t split_seed, int64_t* order) {
+  if (n < 1) return 2;
+  for (int64_t i = 0; i < n; ++i) order[i] = i;
+  std::mt19937_64 rng(or_derive_seed(split_seed, 0x5b117ULL));
+  for (int64_t i = n - 1; i > 0; --i) {
+    const int64_t j = static_cast<int64_t>(uniform_below(rng, static_cast<uint64_t>(i) + 1));
+    std::swap(order[i], order[j]);
+  }
+  return 0;
+}
+
 double or_softplus(double x) { return softplus(x); }
 double or_softplus_inverse(double v) {
   double r = std::numeric_limits<double>::quiet_NaN();

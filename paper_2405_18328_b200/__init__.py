@@ -88,7 +88,7 @@ EXPORTS = [
     "wgp_set_hv_impl", "wgp_stream", "wgp_set_data", "wgp_set_hyper", "wgp_set_rows", "wgp_hv",
     "wgp_hv_device", "wgp_solve", "wgp_grad", "wgp_sample_probes", "wgp_rff_probes", "wgp_train",
     "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
-    "wgp_exact", "wgp_predict",
+    "wgp_exact", "wgp_predict", "wgp_split_order",
 ]
 
 
@@ -117,6 +117,7 @@ def load():
     lib.wgp_profile_read.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.wgp_derive_seed.restype = C.c_uint64
     lib.wgp_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+    lib.wgp_split_order.argtypes = [C.c_int64, C.c_uint64, C.c_void_p]
     lib.wgp_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     lib.wgp_destroy.argtypes = [C.c_void_p]
     lib.wgp_set_hv_impl.argtypes = [C.c_void_p, C.c_int]
@@ -158,6 +159,14 @@ def launch_count() -> int:
 
 def device_count() -> int:
     return int(load().wgp_device_count())
+
+
+def split_order(n: int, split_seed: int) -> np.ndarray:
+    """dataset.cpp:118-124: split_standardize's row permutation (host
+    mt19937_64 Fisher-Yates, bitwise the reference's)."""
+    out = np.empty(int(n), dtype=np.int64)
+    _check(load().wgp_split_order(int(n), C.c_uint64(split_seed), out.ctypes.data))
+    return out
 
 
 def derive_seed(base: int, stream: int) -> int:

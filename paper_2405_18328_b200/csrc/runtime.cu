@@ -1302,4 +1302,18 @@ int wgp_adam_step(double* raw, const double* grad, double* m, double* v, int p, 
 
 uint64_t wgp_derive_seed(uint64_t base, uint64_t stream) { return wgp::derive_seed(base, stream); }
 
+// split_standardize's row permutation (dataset.cpp:118-124): Fisher-Yates
+// from the back with mt19937_64(derive_seed(split_seed, 0x5b117)).
+int wgp_split_order(int64_t n, uint64_t split_seed, int64_t* order) {
+  return guarded([&] {
+    if (n < 1 || !order) throw std::invalid_argument("split_order: n must be >= 1");
+    for (int64_t i = 0; i < n; ++i) order[i] = i;
+    std::mt19937_64 rng(wgp::derive_seed(split_seed, 0x5b117ULL));
+    for (int64_t i = n - 1; i > 0; --i) {
+      const int64_t j = static_cast<int64_t>(wgp::uniform_below(rng, static_cast<uint64_t>(i) + 1));
+      std::swap(order[i], order[j]);
+    }
+  });
+}
+
 }  // extern "C"
