@@ -117,6 +117,7 @@ struct TcArgs {
   float sf2, a, diag;
   const float* hyp;  // device [sf2, a, diag] (overrides the three above when set)
   float* part;       // [splits][s_pad][m_pad] fp32 split partials (splits > 1)
+  int tma_part;      // 1: the final partial tile goes out as one TMA store (mPart)
   double* flush;     // [splits][s_pad][m_pad] fp64 running sums (T > flush_every * chunk)
   int flush_every;   // chunks per fp32 running sum before it is flushed to fp64
   int64_t m_pad;
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     hv_tc_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                  const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                  const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
-                 const TcArgs p) {
+                 const __grid_constant__ CUtensorMap mPart, const TcArgs p) {
   using K = Cfg<BF>;
   constexpr int NBUF = K::kTilesInFlight;  // kfull ring
   constexpr int TJ = K::kTJ;
@@ -532,7 +533,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
         p.ctatime[blockIdx.x * 12 + 7] = gt;  // last accumulator read
       }
-      if (!valid) return;
+      // split partial as one TMA store of R (all 384 epilogue threads fold
+      // their rows first; rows past m land in the padding rows of `part`)
+      const bool tma_out = p.tma_part && c < FE;
+      if (!valid && !tma_out) return;
       // Fold the accumulator into R (one short unrolled block), then a rolled
       // loop over the row's columns: this code runs once per CTA from a cold
       // instruction cache, so its length, not its arithmetic, sets its time
@@ -549,13 +553,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
         p.ctatime[blockIdx.x * 12 + 8] = gt;  // folded into R
       }
+      if (tma_out) {
+        // 27 coalesced column stores per thread cost ~3 us per CTA, 4% of the
+        // kernel (measured, WGP_TC_DEBUG 256); one bulk tensor store of the
+        // [s_pad][128] tile replaces them.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (warp == 0 && lane == 0) {
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&mPart),
+                       "r"(rt * kTI), "r"(sp * spad), "r"(smem_u32(sR))
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // sR is read before the CTA exits
+        }
+        return;
+      }
       asm volatile("cp.async.wait_all;" ::: "memory");
       if (p.ctatime && threadIdx.x == 0) {
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
         p.ctatime[blockIdx.x * 12 + 9] = gt;  // prefetch complete
       }
-      const int cend = min(ce, p.s);
+      const int cend = min(ce, p.dbg & 256 ? cb : p.s);  // dbg 256: no final stores (ablation)
       if (p.splits > 1) {
         float* part = p.part + static_cast<int64_t>(sp) * spad * p.m_pad + lr;
 #pragma unroll 1
@@ -801,14 +820,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes, uint32_t box_in,
-                     uint32_t box_out, CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
+                     uint32_t box_out, CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_bytes};
   cuuint32_t box[2] = {box_in, box_out};
   cuuint32_t es[2] = {1, 1};
   const CUresult r = encode_fn()(&m, dtype, 2, const_cast<void*>(base), dims, strides,
-                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   return m;
@@ -916,6 +936,7 @@ void TcOperands::build(const float* xs, int64_t n_, int dp, int d_, cudaStream_t
 
 template <bool BF>
 void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorMap& mBhi, const CUtensorMap& mBlo,
+               const CUtensorMap& mPart,
                const CUtensorMap& mVhi, const CUtensorMap& mVlo, const TcArgs& a, unsigned grid, int smem,
                cudaStream_t st) {
   static bool configured = false;
@@ -923,7 +944,7 @@ void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorM
     WGP_CUDA(cudaFuncSetAttribute(hv_tc_kernel<BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
     configured = true;
   }
-  hv_tc_kernel<BF><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a);
+  hv_tc_kernel<BF><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart, a);
   WGP_LAUNCH_CHECK();
 }
 
@@ -1078,6 +1099,15 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   char* pw = static_cast<char*>(ws_part.ensure(round_up(part_bytes, 256) + flush_bytes + 256));
   a.part = reinterpret_cast<float*>(pw);
   a.flush = reinterpret_cast<double*>(pw + round_up(part_bytes, 256));
+  // The split partial of a CTA, R = [s_pad][128] fp32 in shared memory, is one
+  // box of the partial buffer viewed as [splits * s_pad] columns x [m_pad] rows.
+  CUtensorMap mPart = mAhi;  // unused unless tma_part
+  a.tma_part = 0;
+  if (a.splits > 1) {
+    mPart = make_map(a.part, static_cast<uint64_t>(m_pad), static_cast<uint64_t>(a.splits) * spad, m_pad * 4, kTI,
+                     static_cast<uint32_t>(spad), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.tma_part = 1;
+  }
   const int smem = static_cast<int>(a.a_region) + 1024 + a.nb * bstage + a.nv * static_cast<int>(a.vstage_bytes) +
                    512 * spad;  // + sVd
   const unsigned grid = static_cast<unsigned>(row_tiles * a.splits);
@@ -1091,9 +1121,9 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
     WGP_CUDA(cudaEventRecord(ev0, st));
   }
   if (bf16)
-    launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a, grid, smem, st);
+    launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st);
   else
-    launch_tc<false>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, a, grid, smem, st);
+    launch_tc<false>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st);
   if (ops.profiling) {
     WGP_CUDA(cudaEventRecord(ev1, st));
     ops.events.emplace_back(ev0, ev1);
