@@ -126,7 +126,9 @@ int wgp_solve(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const float* rhs, const f
  *     A = 1/2 vy vy^T,  B = coef_b L R^T      (vy: n, L/R: n x s; host)
  *  out_a/out_b (d+2): raw-space <dH/dtheta_k, A>, <dH/dtheta_k, B>, with the
  *  chain rule of `transform` at `raw`.  Uses the context's X; the context's
- *  hyperparameters are set from `raw`. */
+ *  hyperparameters are set from `raw`.  The row sums run over the context's
+ *  row range (wgp_set_rows; default all rows) against all n points: the
+ *  outputs of a row partition add up to the full contraction (row sharding). */
 int wgp_grad(wgp_ctx* ctx, int transform, const double* raw, const float* vy, const float* L,
              const float* R, int s, double coef_b, double* out_a, double* out_b);
 
@@ -210,6 +212,24 @@ uint64_t wgp_derive_seed(uint64_t base, uint64_t stream);
  *  mt19937_64(derive_seed(split_seed, 0x5b117)) and uniform_below -- bitwise
  *  the reference's permutation (host-only, no device work). */
 int wgp_split_order(int64_t n, uint64_t split_seed, int64_t* order);
+
+/* ---- row-sharded solver building blocks (paper_2405_18328_b200/sharded.py) ---- */
+
+/** out[r, :] (rows r of the context's row range, wgp_set_rows) =
+ *  mode 0: H[row, j0:j1] V[j0:j1, :];  1: B[row, :] - (that);  2: out -= (that).
+ *  V holds the block's rows (V[(j - j0) + c ldv], ldv >= j1 - j0), B and out
+ *  the context's rows (B[(row - r0) + c ldb]).  Device pointers.
+ *  The column block of the right-looking AP residual update
+ *  R_I -= H[I, b] delta_b (proj/src/solvers.cpp:186). */
+int wgp_hv_cols(wgp_ctx* ctx, const float* V, int64_t ldv, int s, int64_t j0, int64_t j1, float* out, int64_t ldo,
+                int mode, const float* B, int64_t ldb);
+/** Factor every diagonal block of size block_size at the current
+ *  hyperparameters (proj/src/solvers.cpp:151-165: Cholesky, errors as
+ *  ap_solve's) and keep the inverses; *nblocks = ceil(n / block_size). */
+int wgp_ap_factor(wgp_ctx* ctx, int block_size, int64_t* nblocks);
+/** delta_b = H_bb^-1 R_b for block b of the last wgp_ap_factor
+ *  (proj/src/solvers.cpp:185); device fp64, column-major size x s, ld = size. */
+int wgp_ap_block_solve(wgp_ctx* ctx, int64_t block, const double* Rb, int s, double* delta);
 
 #ifdef __cplusplus
 }

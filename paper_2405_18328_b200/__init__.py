@@ -88,7 +88,7 @@ EXPORTS = [
     "wgp_set_hv_impl", "wgp_stream", "wgp_set_data", "wgp_set_hyper", "wgp_set_rows", "wgp_hv",
     "wgp_hv_device", "wgp_solve", "wgp_grad", "wgp_sample_probes", "wgp_rff_probes", "wgp_train",
     "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
-    "wgp_exact", "wgp_predict", "wgp_split_order",
+    "wgp_exact", "wgp_predict", "wgp_split_order", "wgp_hv_cols", "wgp_ap_factor", "wgp_ap_block_solve",
 ]
 
 
@@ -126,6 +126,10 @@ def load():
     lib.wgp_set_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
     lib.wgp_hv.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.wgp_hv_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64]
+    lib.wgp_hv_cols.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int64, C.c_void_p,
+                                C.c_int64, C.c_int, C.c_void_p, C.c_int64]
+    lib.wgp_ap_factor.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    lib.wgp_ap_block_solve.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int, C.c_void_p]
     lib.wgp_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.wgp_grad.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                              C.c_int, C.c_double, C.c_void_p, C.c_void_p]
@@ -437,6 +441,23 @@ class Context:
     def hv_device(self, V_ptr: int, ldv: int, s: int, out_ptr: int, ldo: int):
         """Device-pointer H V on the context stream (asynchronous)."""
         _check(self._lib.wgp_hv_device(self._h, C.c_void_p(V_ptr), ldv, s, C.c_void_p(out_ptr), ldo))
+
+    def hv_cols_device(self, V_ptr: int, ldv: int, s: int, j0: int, j1: int, out_ptr: int, ldo: int,
+                       mode: int = 0, B_ptr: int = 0, ldb: int = 0):
+        """Device-pointer column block over the set_rows rows: out = (mode 0) H[rows, j0:j1] V,
+        (1) B - that, (2) out -= that; V holds the block's j1 - j0 rows, B / out the local rows."""
+        _check(self._lib.wgp_hv_cols(self._h, C.c_void_p(V_ptr), ldv, s, j0, j1, C.c_void_p(out_ptr), ldo, mode,
+                                     C.c_void_p(B_ptr or None), ldb))
+
+    def ap_factor(self, block_size: int) -> int:
+        """Factor and invert every diagonal block (solvers.cpp:151-165); returns the block count."""
+        nb = C.c_int64(0)
+        _check(self._lib.wgp_ap_factor(self._h, int(block_size), C.byref(nb)))
+        return int(nb.value)
+
+    def ap_block_solve_device(self, block: int, Rb_ptr: int, s: int, delta_ptr: int):
+        """delta_b = H_bb^-1 R_b (fp64 device, size x s column-major)."""
+        _check(self._lib.wgp_ap_block_solve(self._h, int(block), C.c_void_p(Rb_ptr), s, C.c_void_p(delta_ptr)))
 
     def solve(self, rhs, config: SolverConfig, init=None) -> SolveState:
         rhs = _f32(rhs)

@@ -35,16 +35,17 @@ __global__ void __launch_bounds__(NT) grad_kernel(GradParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W = 2 * (p.d + 1);
   for (int e = tid; e < (NT / 32) * 2 * (DMAX + 1); e += NT) (&wacc[0][0])[e] = 0.0;
-  const int64_t ib = static_cast<int64_t>(blockIdx.x) * TM;
+  const int64_t ib = p.r0 + static_cast<int64_t>(blockIdx.x) * TM;
+  const int64_t iend = p.r0 + (p.m < 0 ? p.n : p.m);  // rows [r0, iend)
   for (int e = tid; e < TM * p.dp; e += NT) {
     const int r = e / p.dp, k = e % p.dp;
-    xi[r * dps + k] = ib + r < p.n ? p.xs[(ib + r) * p.dp + k] : 0.f;
+    xi[r * dps + k] = ib + r < iend ? p.xs[(ib + r) * p.dp + k] : 0.f;
   }
   for (int e = tid; e < TM * p.s; e += NT) {
     const int c = e / TM, r = e % TM;
-    li[r * sp + c] = ib + r < p.n ? p.L[ib + r + c * p.ld] : 0.f;
+    li[r * sp + c] = ib + r < iend ? p.L[ib + r + c * p.ld] : 0.f;
   }
-  for (int r = tid; r < TM; r += NT) vyi[r] = ib + r < p.n ? p.vy[ib + r] : 0.f;
+  for (int r = tid; r < TM; r += NT) vyi[r] = ib + r < iend ? p.vy[ib + r] : 0.f;
 
   const int ii = (tid / 16) * 4, jj = (tid % 16) * 4;
   float accA[DMAX + 1], accB[DMAX + 1];
@@ -157,7 +158,7 @@ void launch_grad(const GradParams& p, cudaStream_t st) {
                                   200 * 1024));
     configured = true;
   }
-  grad_kernel<DMAX><<<grad_blocks(p.n), NT, smem, st>>>(p);
+  grad_kernel<DMAX><<<grad_blocks(p.m < 0 ? p.n : p.m), NT, smem, st>>>(p);
   WGP_LAUNCH_CHECK();
 }
 
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(NT) rff_kernel(RffParams p) {
 
 }  // namespace
 
-int grad_blocks(int64_t n) { return static_cast<int>(ceil_div(n, TM)); }
+int grad_blocks(int64_t m) { return static_cast<int>(ceil_div(m, TM)); }
 
 void grad_simt(const GradParams& p, cudaStream_t st) {
   if (p.d <= 4) return launch_grad<4>(p, st);

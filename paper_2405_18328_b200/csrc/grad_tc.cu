@@ -189,6 +189,7 @@ __device__ __forceinline__ void mma_w_k64(uint32_t d, uint32_t a, uint64_t bh, u
 
 struct GradTcArgs {
   int64_t n;
+  int64_t r0, r1;  // rows [r0, r1)
   int d, dp, s, spk;  // spk: K extent of W^B (32 or 64: multiples of one 128-byte swizzle row)
   int num_jt, splits, ne;
   int cs, rt_pad;     // cluster size (CTAs sharing each R_J stage by TMA multicast), row tiles padded to cs
@@ -347,8 +348,8 @@ __global__ void __launch_bounds__(gThreads, 1)
     const int q = warp & 3, w = ew >> 2;
     const int row = q * 32 + lane;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
-    const int64_t gi = static_cast<int64_t>(rt) * gTI + row;
-    const bool valid = gi < p.n;
+    const int64_t gi = p.r0 + static_cast<int64_t>(rt) * gTI + row;
+    const bool valid = gi < p.r1;
     float2 xi[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -574,7 +575,7 @@ void launch_grad_tc(const CUtensorMap& mh, const CUtensorMap& ml, const GradTcAr
 
 bool grad_tc_supported(int d, int s) { return d >= 1 && d <= 12 && s >= 1 && s <= 64; }
 
-GradTcPlan grad_tc_plan(int64_t n, int d, int s) {
+GradTcPlan grad_tc_plan(int64_t n, int64_t m, int d, int s) {
   GradTcPlan pl;
   pl.n_pad = round_up(std::max<int64_t>(n, 1), gTJ);
   pl.spk = s <= 32 ? 32 : 64;
@@ -586,7 +587,7 @@ GradTcPlan grad_tc_plan(int64_t n, int d, int s) {
   }();
   const int nbox = 2 * (pl.spk / 32);
   pl.cs = std::min(nbox, env_cs == 1 || env_cs == 2 || env_cs == 4 ? env_cs : 2);
-  const int64_t row_tiles = ceil_div(n, gTI);
+  const int64_t row_tiles = ceil_div(m, gTI);
   if (row_tiles < pl.cs) pl.cs = 1;
   pl.rt_pad = static_cast<int>(round_up(row_tiles, pl.cs));
   const int jt = static_cast<int>(ceil_div(n, gTJ));
@@ -612,6 +613,8 @@ void grad_tc(const GradParams& p, const GradTcPlan& pl, void* ws, cudaStream_t s
   const CUtensorMap ml = tc_tensor_map(rlo, pl.spk, pl.n_pad, pl.spk * 4, 32, gTJ);
   GradTcArgs a{};
   a.n = p.n;
+  a.r0 = p.r0;
+  a.r1 = p.r0 + (p.m < 0 ? p.n : p.m);
   a.d = p.d;
   a.dp = p.dp;
   a.s = p.s;

@@ -74,8 +74,9 @@ struct GradParams {
   float coef_b;
   float sf2, a;
   double* part;   // [gridDim.x][2 (d+1)]
+  int64_t r0 = 0, m = -1;  // rows [r0, r0 + m) against all n points (m < 0: all rows)
 };
-int grad_blocks(int64_t n);
+int grad_blocks(int64_t m);  // rows
 void grad_simt(const GradParams& p, cudaStream_t st);
 // Tensor-core gradient (grad_tc.cu): W^B on tcgen05, O(d) epilogue; same
 // partial format as grad_simt ([plan.nblk][2 (d + 1)]).
@@ -86,7 +87,7 @@ struct GradTcPlan {
   size_t ws_bytes = 0;
 };
 bool grad_tc_supported(int d, int s);
-GradTcPlan grad_tc_plan(int64_t n, int d, int s);
+GradTcPlan grad_tc_plan(int64_t n, int64_t m, int d, int s);  // n points, m rows
 void grad_tc(const GradParams& p, const GradTcPlan& plan, void* ws, cudaStream_t st);
 // out[0..2(d+1)) = sum over blocks in block order.
 void grad_finalize(const double* part, int nblk, int width, double* out, cudaStream_t st);

@@ -81,6 +81,7 @@ struct Ctx {
   double sf = 1.0, sigma = 1.0;
   bool have_hyper = false;
   int64_t r0 = 0, r1 = -1;
+  int64_t ap_bs = 0;  // block size of the cached AP factors (hbuf), 0: none
   TcOperands tc;
 
   // workspaces
@@ -138,6 +139,7 @@ struct Ctx {
   }
 
   void set_hyper(const double* c) {
+    ap_bs = 0;  // cached AP block factors belong to the previous hyperparameters
     if (n < 1) throw std::invalid_argument("no training inputs: call wgp_set_data first");
     for (int k = 0; k < d + 2; ++k)
       if (!(c[k] > 0.0) || !std::isfinite(c[k]))
@@ -231,6 +233,15 @@ struct Ctx {
   ColState colstate() {
     return ColState{conv.as<int>(), rs.as<double>(), alpha.as<double>(), beta.as<double>(),
                     bnorm.as<double>(), tol.as<double>(), best.as<double>(), stall.as<int>(), act.as<int>()};
+  }
+  // column dots over rows [r, r + m)
+  std::vector<double> dots_rows(const float* A, const float* B_, int s, int64_t r, int64_t m) {
+    ensure_solver_ws(s);
+    col_dots(A + r, B_ + r, ld, m, s, part.as<double>(), &dctrl()->ticket, colsum.as<double>(), st);
+    std::vector<double> h(s);
+    WGP_CUDA(cudaMemcpyAsync(h.data(), colsum.p, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    return h;
   }
   std::vector<double> dots(const float* A, const float* B_, int s) {
     ensure_solver_ws(s);
@@ -447,10 +458,12 @@ struct Ctx {
     }
   }
 
-  void ap(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {
+  // Factor every diagonal block of size bs once (solvers.cpp:151-165): H[b,b]
+  // in fp64 (the last, partial block padded with the identity), one batched
+  // cuSOLVER Cholesky over all blocks, then the explicit inverses H_bb^-1
+  // (hbuf, ap_bs): each Gauss-Seidel step is one DGEMM.  Returns the count.
+  int64_t ap_factor(int64_t bs) {
     lazy_handles();
-    const int max_ep = cfg.max_iterations > 0 ? cfg.max_iterations : 1000;
-    const int64_t bs = std::min<int64_t>(std::max(cfg.block_size, 1), n);
     const int64_t nb = ceil_div(n, bs);
     // Factor every diagonal block once per solve (:151-165): H[b,b] in fp64
     // (the last, partial block padded with the identity), one batched
@@ -504,6 +517,29 @@ struct Ctx {
                                   static_cast<long long>(bb), &zero_, hbuf.as<double>(), static_cast<int>(bs),
                                   static_cast<long long>(bb), static_cast<int>(nb)) != CUBLAS_STATUS_SUCCESS)
       throw DeviceError("cublasDgemmStridedBatched failed");
+    ap_bs = bs;
+    return nb;
+  }
+  // delta = H_bb^-1 R_b for block b of the last ap_factor (device fp64,
+  // column-major size x s, leading dimension size).
+  void ap_block_solve(int64_t b, const double* Rbp, int s, double* delta) {
+    if (ap_bs <= 0) throw std::invalid_argument("ap_block_solve: call ap_factor first");
+    const int64_t nb = ceil_div(n, ap_bs);
+    if (b < 0 || b >= nb) throw std::invalid_argument("ap_block_solve: block index out of range");
+    const int64_t start = b * ap_bs, size = std::min(ap_bs, n - start);
+    const double one = 1.0, zero = 0.0;
+    const double* Hinv = hbuf.as<double>() + static_cast<size_t>(b) * ap_bs * ap_bs;
+    if (cublasDgemm(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, static_cast<int>(size), &one, Hinv,
+                    static_cast<int>(ap_bs), Rbp, static_cast<int>(size), &zero, delta,
+                    static_cast<int>(size)) != CUBLAS_STATUS_SUCCESS)
+      throw DeviceError("cublasDgemm failed");
+  }
+
+  void ap(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {
+    lazy_handles();
+    const int max_ep = cfg.max_iterations > 0 ? cfg.max_iterations : 1000;
+    const int64_t bs = std::min<int64_t>(std::max(cfg.block_size, 1), n);
+    const int64_t nb = ap_factor(bs);
     Rb.ensure(sizeof(double) * bs * s);
     D64.ensure(sizeof(double) * bs * s);
     D32.ensure(sizeof(float) * bs * s);
@@ -604,8 +640,12 @@ struct Ctx {
   // ---------------------------------------------------------------- gradient
   // derivative_contractions for A = vy vy^T / 2, B = coef L R^T (device
   // inputs, ld); raw-space outputs on the host.
+  // Rows [gr0, gr0 + gm) against all n points (gm < 0: all rows): a row
+  // shard's share of every contraction; the shares of a row partition sum to
+  // the full gradient (all outputs are linear in the row sums).
   void grad(int transform, const double* raw, const float* vy, const float* L, const float* R,
-            int s, double coef_b, double* out_a, double* out_b) {
+            int s, double coef_b, double* out_a, double* out_b, int64_t gr0 = 0, int64_t gm = -1) {
+    if (gm < 0) gm = n - gr0;
     std::vector<double> cons(d + 2);
     for (int k = 0; k < d + 2; ++k) cons[k] = transform == 1 ? std::exp(raw[k]) : softplus(raw[k]);
     set_hyper(cons.data());
@@ -617,8 +657,8 @@ struct Ctx {
     }();
     const bool use_tc = hv_impl != WGP_HV_SIMT && !force_simt && grad_tc_supported(d, s);
     GradTcPlan plan;
-    if (use_tc) plan = grad_tc_plan(n, d, s);
-    const int nblk = use_tc ? plan.nblk : grad_blocks(n);
+    if (use_tc) plan = grad_tc_plan(n, gm, d, s);
+    const int nblk = use_tc ? plan.nblk : grad_blocks(gm);
     const int W = 2 * (d + 1);
     gpart.ensure(sizeof(double) * nblk * W);
     if (use_tc) gtc_ws.ensure(plan.ws_bytes);
@@ -637,6 +677,8 @@ struct Ctx {
     gp.sf2 = sf2();
     gp.a = a_coef();
     gp.part = gpart.as<double>();
+    gp.r0 = gr0;
+    gp.m = gm;
     if (use_tc)
       grad_tc(gp, plan, gtc_ws.p, st);
     else
@@ -644,8 +686,8 @@ struct Ctx {
     grad_finalize(gpart.as<double>(), nblk, W, gout.as<double>(), st);
     std::vector<double> acc(W);
     WGP_CUDA(cudaMemcpyAsync(acc.data(), gout.p, sizeof(double) * W, cudaMemcpyDeviceToHost, st));
-    const std::vector<double> yy = dots(vy, vy, 1);
-    const std::vector<double> lr = dots(L, R, s);
+    const std::vector<double> yy = dots_rows(vy, vy, 1, gr0, gm);
+    const std::vector<double> lr = dots_rows(L, R, s, gr0, gm);
     double tb = 0.0;
     for (double v : lr) tb += v;
     auto chain = [&](double r) { return transform == 1 ? std::exp(r) : softplus_derivative(r); };
@@ -1241,7 +1283,9 @@ int wgp_grad(wgp_ctx* ctx, int transform, const double* raw, const float* vy, co
                                cudaMemcpyHostToDevice, c.st));
     WGP_CUDA(cudaMemcpy2DAsync(dR.p, sizeof(float) * c.ld, R, sizeof(float) * c.n, sizeof(float) * c.n, s,
                                cudaMemcpyHostToDevice, c.st));
-    c.grad(transform, raw, dvy.as<float>(), dL.as<float>(), dR.as<float>(), s, coef_b, out_a, out_b);
+    // rows of the context's row range (wgp_set_rows) against all points
+    c.grad(transform, raw, dvy.as<float>(), dL.as<float>(), dR.as<float>(), s, coef_b, out_a, out_b, c.r0,
+           c.r1 - c.r0);
   });
 }
 
@@ -1301,6 +1345,39 @@ int wgp_adam_step(double* raw, const double* grad, double* m, double* v, int p, 
 }
 
 uint64_t wgp_derive_seed(uint64_t base, uint64_t stream) { return wgp::derive_seed(base, stream); }
+
+int wgp_hv_cols(wgp_ctx* ctx, const float* V, int64_t ldv, int s, int64_t j0, int64_t j1, float* out, int64_t ldo,
+                int mode, const float* B, int64_t ldb) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    c.require_data();
+    if (s < 1) throw std::invalid_argument("wgp_hv_cols: s must be >= 1");
+    if (j0 < 0 || j1 > c.n || j1 <= j0) throw std::invalid_argument("wgp_hv_cols: bad column range");
+    if (mode < wgp::kHvStore || mode > wgp::kHvSubtract) throw std::invalid_argument("wgp_hv_cols: bad mode");
+    if (mode == wgp::kHvResidual && !B) throw std::invalid_argument("wgp_hv_cols: residual mode needs B");
+    if (ldv < j1 - j0 || ldo < c.r1 - c.r0 || (B && ldb < c.r1 - c.r0))
+      throw std::invalid_argument("wgp_hv_cols: leading dimension too small");
+    // the kernels index V by global point and B by global row
+    c.hv(V - j0, ldv, s, out, ldo, mode, B ? B - c.r0 : nullptr, ldb, j0, j1, nullptr, c.r0, c.r1 - c.r0);
+  });
+}
+
+int wgp_ap_factor(wgp_ctx* ctx, int block_size, int64_t* nblocks) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    c.require_data();
+    if (block_size < 1) throw std::invalid_argument("SolverConfig: block_size must be >= 1");
+    const int64_t nb = c.ap_factor(std::min<int64_t>(block_size, c.n));
+    if (nblocks) *nblocks = nb;
+  });
+}
+
+int wgp_ap_block_solve(wgp_ctx* ctx, int64_t block, const double* Rb, int s, double* delta) {
+  return guarded([&] {
+    if (s < 1) throw std::invalid_argument("wgp_ap_block_solve: s must be >= 1");
+    ctx->c.ap_block_solve(block, Rb, s, delta);
+  });
+}
 
 // split_standardize's row permutation (dataset.cpp:118-124): Fisher-Yates
 // from the back with mt19937_64(derive_seed(split_seed, 0x5b117)).

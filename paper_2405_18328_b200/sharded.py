@@ -141,3 +141,132 @@ def device_local_hv(ctx, r0: int, r1: int):
         return out.t()
 
     return f
+
+
+# ------------------------------------------------------------------ AP
+@dataclass
+class ApOps:
+    """Local operators of the row-sharded AP for this rank's rows I = [r0, r1).
+
+    rows_residual(B_local, X_full)   -> B_local - H[I, :] X_full
+    cols_subtract(R_local, delta, j0, j1) -> R_local - H[I, j0:j1] delta
+    factor(block_size)               -> number of blocks (factors kept)
+    block_solve(b, R_b)              -> H_bb^-1 R_b   (fp64, size x s)
+    """
+    rows_residual: Callable
+    cols_subtract: Callable
+    factor: Callable
+    block_solve: Callable
+
+
+def _allreduce_exact(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """Sum of disjoint contributions (every element nonzero on at most one rank): exact."""
+    if world > 1:
+        dist.all_reduce(x, group=group)
+    return x
+
+
+def sharded_ap(ops: ApOps, B_local: torch.Tensor, n: int, r0: int, r1: int, block_size: int = 2000,
+               tol_mean: float = 0.01, tol_samples: float = 0.1, max_iterations: int = 0,
+               init_local: torch.Tensor | None = None, group=None) -> ShardedSolveState:
+    """ap_solve (proj/src/solvers.cpp:141-196) over row shards.
+
+    Blocks of `block_size` consecutive points in fixed order (they may straddle
+    ranks).  Per block: R_b from the ranks' overlapping rows (one all-reduce of
+    disjoint b x s contributions, exact), delta_b = H_bb^-1 R_b on every rank
+    (identical inputs, identical result), own rows of X += delta_b, own rows of
+    R -= H[I, b] delta_b (the reference's right-looking update, :186).  Each
+    epoch ends with the exact refresh R = B - H X from the all-gathered X
+    (:188) and the per-column norms summed in rank order (:189-191)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    s = B_local.shape[1]
+    dt = B_local.dtype
+    bs = min(max(int(block_size), 1), n)
+    max_ep = max_iterations if max_iterations > 0 else 1000
+    nb = ops.factor(bs)
+    X = torch.zeros_like(B_local) if init_local is None else init_local.clone()
+    bn = torch.sqrt(_sum_ranks((B_local.double() ** 2).sum(0), world, group))
+    tols = torch.tensor([tol_mean] + [tol_samples] * (s - 1), dtype=torch.float64, device=bn.device)
+    R = ops.rows_residual(B_local, _gather_rows(X, n, world, group))
+
+    def converged(R):
+        rs = _sum_ranks((R.double() ** 2).sum(0), world, group)
+        return rs, (bn == 0) | (torch.sqrt(rs) <= tols * bn)
+
+    _, conv = converged(R)
+    epoch = 0
+    while not bool(conv.all()) and epoch < max_ep:
+        epoch += 1
+        for b in range(nb):
+            j0, j1 = b * bs, min(n, (b + 1) * bs)
+            o0, o1 = max(j0, r0), min(j1, r1)
+            Rb = torch.zeros((j1 - j0, s), dtype=torch.float64, device=B_local.device)
+            if o0 < o1:
+                Rb[o0 - j0:o1 - j0] = R[o0 - r0:o1 - r0].double()
+            Rb = _allreduce_exact(Rb, world, group)
+            delta = ops.block_solve(b, Rb)
+            if o0 < o1:
+                X[o0 - r0:o1 - r0] += delta[o0 - j0:o1 - j0].to(dt)
+            R = ops.cols_subtract(R, delta, j0, j1)
+        R = ops.rows_residual(B_local, _gather_rows(X, n, world, group))
+        rs, conv = converged(R)
+        if not bool(torch.isfinite(rs).all()):
+            raise NumericalError(f"ap_solve: NaN in iterate at epoch {epoch}")
+    en = torch.sqrt(_sum_ranks((R.double() ** 2).sum(0), world, group))
+    rel = torch.where(bn > 0, en / torch.where(bn > 0, bn, torch.ones_like(bn)), torch.zeros_like(bn))
+    return ShardedSolveState(X, R, rel.tolist(), conv.tolist(), epoch)
+
+
+def device_ap_ops(ctx, r0: int, r1: int) -> ApOps:
+    """ApOps backed by the library (device tensors, rows [r0, r1)): the fused
+    H.V for the row and column blocks (wgp_hv_cols) and the cached fp64
+    block inverses (wgp_ap_factor / wgp_ap_block_solve)."""
+    ctx.set_rows(r0, r1)
+    n, m = ctx.n, r1 - r0
+
+    def on_ctx(fn):
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        cur = torch.cuda.current_stream()
+        stream.wait_stream(cur)
+        out = fn()
+        cur.wait_stream(stream)
+        return out
+
+    def rows_residual(B_local, X_full):
+        Bt = B_local.t().contiguous()                 # [s][m]: column-major m x s
+        Xt = X_full.t().contiguous()                  # [s][n]
+        out = torch.empty_like(Bt)
+        on_ctx(lambda: ctx.hv_cols_device(Xt.data_ptr(), n, Xt.shape[0], 0, n, out.data_ptr(), m, 1,
+                                          Bt.data_ptr(), m))
+        return out.t()
+
+    def cols_subtract(R_local, delta, j0, j1):
+        Rt = R_local.t().contiguous()
+        Dt = delta.to(R_local.dtype).t().contiguous()  # [s][size]
+        on_ctx(lambda: ctx.hv_cols_device(Dt.data_ptr(), j1 - j0, Dt.shape[0], j0, j1, Rt.data_ptr(), m, 2))
+        return Rt.t()
+
+    def block_solve(b, Rb):
+        Rt = Rb.t().contiguous()                      # [s][size] fp64
+        Dt = torch.empty_like(Rt)
+        on_ctx(lambda: ctx.ap_block_solve_device(b, Rt.data_ptr(), Rt.shape[0], Dt.data_ptr()))
+        return Dt.t()
+
+    return ApOps(rows_residual, cols_subtract, lambda bs: ctx.ap_factor(bs), block_solve)
+
+
+# ------------------------------------------------------------------ gradient
+def sharded_grad(local_grad: Callable[[], tuple], group=None):
+    """Row-sharded gradient contractions: every rank contracts its
+    rows against all points (``Context.set_rows`` + ``Context.grad``; the
+    outputs are linear in the row sums), the (d + 2)-vectors are gathered and
+    summed in rank order (fp64): identical on every rank, deterministic."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    qa, qb = local_grad()
+    nccl = world > 1 and dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    both = torch.tensor(list(qa) + list(qb), dtype=torch.float64, device=dev)
+    tot = _sum_ranks(both, world, group)
+    p = len(qa)
+    tot = tot.cpu()
+    return tot[:p].numpy(), tot[p:].numpy()

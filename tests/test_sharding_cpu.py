@@ -85,3 +85,91 @@ def test_two_ranks_gloo_match_single_process():
         assert abs(it - ref.iterations_used) <= 1  # fp64 summation order differs per shard
         assert np.all(np.array(rel) <= 1e-6 * 1.0001)
     assert np.abs(sol - ref.solutions.numpy()).max() <= 1e-5
+
+
+# ------------------------------------------------------------------ AP + gradient
+def host_ap_ops(H, r0, r1):
+    """ApOps over a host fp64 matrix (the device path: sharded.device_ap_ops)."""
+    Ht = torch.from_numpy(H)
+    HI = Ht[r0:r1]
+    chol = {}
+
+    def factor(bs):
+        chol.clear()
+        n = H.shape[0]
+        nb = -(-n // bs)
+        for b in range(nb):
+            j0, j1 = b * bs, min(n, (b + 1) * bs)
+            chol[b] = torch.linalg.cholesky(Ht[j0:j1, j0:j1])
+        return nb
+
+    return sharded.ApOps(lambda B, X: B - HI @ X, lambda R, d, j0, j1: R - HI[:, j0:j1] @ d, factor,
+                         lambda b, Rb: torch.cholesky_solve(Rb, chol[b]))
+
+
+def _worker_ap(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    H, B = _problem()
+    n = H.shape[0]
+    r0, r1 = sharded.row_range(n, rank, world)
+    st = sharded.sharded_ap(host_ap_ops(H, r0, r1), torch.from_numpy(B[r0:r1]).clone(), n, r0, r1,
+                            block_size=100, tol_mean=1e-8, tol_samples=1e-8)
+    # gradient: rank partials of the B contraction (rows of L masked to the shard)
+    from oracle import oracle as orc
+
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((n, 3))
+    raw = np.array([orc.to_raw("softplus", v) for v in (0.9, 1.2, 1.0, 1.1, 0.5)])
+    vy, L, R = rng.standard_normal(n), rng.standard_normal((n, 4)), rng.standard_normal((n, 4))
+    Lm = np.zeros_like(L)
+    Lm[r0:r1] = L[r0:r1]
+    ga, gb = sharded.sharded_grad(lambda: orc.grad_contractions(X, "softplus", raw, vy, Lm, R, 0.125))
+    out[rank] = (r0, r1, st.solutions.numpy().copy(), st.iterations_used, st.per_column_relative_residual, gb)
+    dist.destroy_process_group()
+
+
+def test_sharded_ap_single_process_matches_oracle():
+    """Right-looking block Gauss-Seidel with exact epoch refresh = ap_solve."""
+    from oracle import oracle as orc
+
+    H, B = _problem()
+    n = H.shape[0]
+    st = sharded.sharded_ap(host_ap_ops(H, 0, n), torch.from_numpy(B), n, 0, n, block_size=100,
+                            tol_mean=1e-8, tol_samples=1e-8)
+    o = orc.solve(B, orc.SolverConfig(kind="ap", tol_mean=1e-8, tol_samples=1e-8, block_size=100), H=H)
+    assert st.iterations_used == o.iterations_used
+    assert np.abs(st.solutions.numpy() - o.solutions).max() <= 1e-8 * np.abs(o.solutions).max() * 100
+    assert np.all(np.array(st.per_column_relative_residual) <= 1e-8)
+
+
+@pytest.mark.timeout(300)
+def test_two_ranks_gloo_sharded_ap_and_gradient():
+    """Blocks of 100 straddle the rank boundary at 128: R_b is assembled across
+    ranks; both ranks reproduce the single-process AP, and the rank partials of
+    the gradient contraction sum to the full one."""
+    from oracle import oracle as orc
+
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_ap, args=(world, _free_port(), out), nprocs=world, join=True)
+    H, B = _problem()
+    n = H.shape[0]
+    ref = sharded.sharded_ap(host_ap_ops(H, 0, n), torch.from_numpy(B), n, 0, n, block_size=100,
+                             tol_mean=1e-8, tol_samples=1e-8)
+    sol = np.zeros_like(B)
+    for rank in range(world):
+        r0, r1, x, it, rel, gb = out[rank]
+        sol[r0:r1] = x
+        assert it == ref.iterations_used
+        assert np.all(np.array(rel) <= 1e-8)
+    assert np.abs(sol - ref.solutions.numpy()).max() <= 1e-10 * np.abs(sol).max() + 1e-12
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((n, 3))
+    raw = np.array([orc.to_raw("softplus", v) for v in (0.9, 1.2, 1.0, 1.1, 0.5)])
+    vy, L, R = rng.standard_normal(n), rng.standard_normal((n, 4)), rng.standard_normal((n, 4))
+    _, full = orc.grad_contractions(X, "softplus", raw, vy, L, R, 0.125)
+    assert np.array_equal(out[0][5], out[1][5])  # identical on every rank
+    assert np.allclose(out[0][5], full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
