@@ -39,7 +39,8 @@ def make(n, d, s, seed, scale=1.0):
 
 @pytest.mark.parametrize("impl", ["tc", "simt"])
 @pytest.mark.parametrize("n,d,s", [(1, 2, 1), (2, 1, 3), (129, 3, 16), (300, 3, 5), (1000, 9, 17),
-                                   (2048, 8, 17), (777, 26, 65), (513, 11, 128)])
+                                   (2048, 8, 17), (777, 26, 65), (513, 11, 128), (400, 5, 18), (901, 4, 34),
+                                   (650, 7, 66), (333, 6, 97), (70, 3, 33)])
 def test_hv_matches_oracle(ctx, impl, n, d, s):
     ctx.set_hv_impl(impl)
     X, V, ls = make(n, d, s, seed=n + d + s)
