@@ -806,17 +806,7 @@ struct Ctx {
     WGP_CUDA(cudaMemcpyAsync(yd, yh, sizeof(float) * n, cudaMemcpyHostToDevice, st));
     pw.ensure(sizeof(float) * ld * 64);
     pr.ensure(sizeof(float) * ld * 64);
-    {
-      const SolveOut so = solve(cfg, yd, nullptr, alpha, pr.as<float>(), 1);
-      if (getenv("WGP_PREDICT_DEBUG")) {
-        std::vector<float> ha(n);
-        WGP_CUDA(cudaMemcpy(ha.data(), alpha, sizeof(float) * n, cudaMemcpyDeviceToHost));
-        float mx = 0.f;
-        for (float v : ha) mx = std::max(mx, std::fabs(v));
-        fprintf(stderr, "[predict] alpha solve: %d iterations, rel %.3e, conv %d, max|alpha| %.3e\n", so.iterations,
-                so.rel[0], so.conv[0], mx);
-      }
-    }
+    solve(cfg, yd, nullptr, alpha, pr.as<float>(), 1);
     // test points in chunks of 64 columns (the solver's right-hand sides)
     constexpr int64_t kMc = 64;
     kstar.ensure(sizeof(float) * ld * kMc);
