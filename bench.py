@@ -235,6 +235,10 @@ def main():
     r0, r1 = min(n, t0_ * 128), min(n, t1_ * 128)
     m = r1 - r0
     ctx.set_rows(r0, r1)
+    if ws > 1:
+        # strong scaling of one H.V: J splits keyed on the shard's rows (more
+        # CTAs per GPU on small shards; rows equal to fp32 rounding, not bitwise)
+        ctx.set_split_global(False)
     stream = torch.cuda.ExternalStream(ctx.stream)
     dev = torch.device("cuda", local)
     Vt = torch.from_numpy(np.ascontiguousarray(p.V.T)).to(dev)  # [s][n] = column-major n x s

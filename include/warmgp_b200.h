@@ -215,6 +215,12 @@ int wgp_split_order(int64_t n, uint64_t split_seed, int64_t* order);
 
 /* ---- row-sharded solver building blocks (paper_2405_18328_b200/sharded.py) ---- */
 
+/** J-split decomposition of the fused H.V for a row range: keyed on the global
+ *  n (global != 0, the default: a row shard reproduces the full operator's rows
+ *  bitwise at any GPU count) or on the shard's own rows (global == 0: more
+ *  CTAs per GPU on small shards; rows equal to fp32 rounding). */
+int wgp_set_split_global(wgp_ctx* ctx, int global);
+
 /** out[r, :] (rows r of the context's row range, wgp_set_rows) =
  *  mode 0: H[row, j0:j1] V[j0:j1, :];  1: B[row, :] - (that);  2: out -= (that).
  *  V holds the block's rows (V[(j - j0) + c ldv], ldv >= j1 - j0), B and out

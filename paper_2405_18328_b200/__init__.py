@@ -89,6 +89,7 @@ EXPORTS = [
     "wgp_hv_device", "wgp_solve", "wgp_grad", "wgp_sample_probes", "wgp_rff_probes", "wgp_train",
     "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
     "wgp_exact", "wgp_predict", "wgp_split_order", "wgp_hv_cols", "wgp_ap_factor", "wgp_ap_block_solve",
+    "wgp_set_split_global",
 ]
 
 
@@ -448,6 +449,10 @@ class Context:
         (1) B - that, (2) out -= that; V holds the block's j1 - j0 rows, B / out the local rows."""
         _check(self._lib.wgp_hv_cols(self._h, C.c_void_p(V_ptr), ldv, s, j0, j1, C.c_void_p(out_ptr), ldo, mode,
                                      C.c_void_p(B_ptr or None), ldb))
+
+    def set_split_global(self, flag: bool):
+        """J splits keyed on the global n (bitwise shard-invariant rows) or on the local rows."""
+        _check(self._lib.wgp_set_split_global(self._h, int(bool(flag))))
 
     def ap_factor(self, block_size: int) -> int:
         """Factor and invert every diagonal block (solvers.cpp:151-165); returns the block count."""

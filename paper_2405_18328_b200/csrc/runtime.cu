@@ -82,6 +82,10 @@ struct Ctx {
   bool have_hyper = false;
   int64_t r0 = 0, r1 = -1;
   int64_t ap_bs = 0;  // block size of the cached AP factors (hbuf), 0: none
+  // J splits keyed on the global n (row shards reproduce the full operator's
+  // rows bitwise) or on the local rows (wgp_set_split_global(ctx, 0): more
+  // CTAs per rank on small row shards, rows equal to fp32 tolerance)
+  bool split_global = true;
   TcOperands tc;
 
   // workspaces
@@ -194,7 +198,7 @@ struct Ctx {
     p.done = done;
     // shards of the full operator decompose like the whole (bitwise-equal
     // rows); internal row blocks (AP) split for their own size instead
-    p.split_rows = (row_idx || !shard_invariant) ? 0 : n;
+    p.split_rows = (row_idx || !shard_invariant || !split_global) ? 0 : n;
     if ((hv_impl == WGP_HV_TC || hv_impl == WGP_HV_TC_BF16) && hv_tc_supported(d, s)) {
       if (!tc.valid) tc.build(xs.as<float>(), n, dp, d, st);
       hv_tc(tc, p, st, hv_impl == WGP_HV_TC_BF16);
@@ -1335,6 +1339,10 @@ int wgp_adam_step(double* raw, const double* grad, double* m, double* v, int p, 
 }
 
 uint64_t wgp_derive_seed(uint64_t base, uint64_t stream) { return wgp::derive_seed(base, stream); }
+
+int wgp_set_split_global(wgp_ctx* ctx, int global) {
+  return guarded([&] { ctx->c.split_global = global != 0; });
+}
 
 int wgp_hv_cols(wgp_ctx* ctx, const float* V, int64_t ldv, int s, int64_t j0, int64_t j1, float* out, int64_t ldo,
                 int mode, const float* B, int64_t ldb) {

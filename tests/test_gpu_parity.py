@@ -109,7 +109,11 @@ def test_hv_row_sharding(ctx):
     for r0, r1 in ((0, 700), (700, 1500), (128, 256)):
         ctx.set_rows(r0, r1)
         part = ctx.hv(V, rows=r1 - r0)
-        assert np.array_equal(part, full[r0:r1])
+        assert np.array_equal(part, full[r0:r1])  # J splits keyed on the global n: bitwise
+        ctx.set_split_global(False)  # keyed on the shard's rows: fp32 rounding
+        part = ctx.hv(V, rows=r1 - r0)
+        ctx.set_split_global(True)
+        assert rel(part, full[r0:r1].astype(np.float64)) <= 1e-6
     ctx.set_rows(0, 1500)
 
 
