@@ -43,6 +43,7 @@ const char* or_last_error(void);
 uint64_t or_splitmix64(uint64_t x);
 uint64_t or_derive_seed(uint64_t base, uint64_t stream);
 int or_split_order(int64_t n, uint64_t split_seed, int64_t* order);  // dataset.cpp:118-124
+int or_synthesize_draws(int n, int d, uint64_t seed, double* X, double* xi);  // dataset.cpp:167-190
 
 /* kernel.cpp:14-31 (softplus) plus the log transform BASELINE asks for.
  * transform: 0 = softplus (reference), 1 = log. */

@@ -88,6 +88,7 @@ def lib():
         _lib.or_splitmix64.argtypes = [C.c_uint64]
         _lib.or_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
         _lib.or_split_order.argtypes = [C.c_int64, C.c_uint64, C.c_void_p]
+        _lib.or_synthesize_draws.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_void_p]
         for name in ("or_softplus", "or_softplus_inverse", "or_softplus_derivative"):
             getattr(_lib, name).restype = C.c_double
             getattr(_lib, name).argtypes = [C.c_double]
@@ -133,6 +134,17 @@ def split_order(n: int, split_seed: int) -> np.ndarray:
     out = np.empty(int(n), dtype=np.int64)
     _check(lib().or_split_order(int(n), C.c_uint64(split_seed), out.ctypes.data))
     return out
+
+
+def synthesize(n, d, lengthscales, signal, noise, seed):
+    """dataset.cpp:167-190: X ~ U[0,1]^d and y = chol(K + noise^2 I) xi with the
+    reference's draws (bitwise X and xi; y up to Cholesky rounding).
+    The 4-argument form synthesize(n, d, noise, seed) is lengthscales = 1, signal = 1."""
+    X = np.empty((n, d))
+    xi = np.empty(n)
+    _check(lib().or_synthesize_draws(int(n), int(d), C.c_uint64(seed), X.ctypes.data, xi.ctypes.data))
+    H = kernel_matrices(X, np.broadcast_to(np.asarray(lengthscales, dtype=np.float64), (d,)), signal, noise)[0]
+    return X, np.linalg.cholesky(H) @ xi
 
 
 def softplus(x):

@@ -919,6 +919,19 @@ uint64_t or_derive_seed(uint64_t base, uint64_t stream) {  // common.hpp:34-36
   return or_splitmix64(or_splitmix64(base) ^ or_splitmix64(stream + 0x51ed2701ab0a3c11ULL));
 }
 
+// dataset.cpp:167-190 (synthesize): the random draws -- X ~ U[0,1]^d row by
+// row (uniform_unit) and xi ~ N(0,1) (libstdc++ normal_distribution) from
+// mt19937_64(derive_seed(seed, 0xda7a)); y = chol(H) xi is formed by the caller.
+int or_synthesize_draws(int n, int d, uint64_t seed, double* X, double* xi) {
+  if (n < 1 || d < 1) return 2;
+  std::mt19937_64 rng(or_derive_seed(seed, 0xda7aULL));
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < d; ++k) X[static_cast<size_t>(i) * d + k] = uniform_unit(rng);
+  std::normal_distribution<double> normal(0.0, 1.0);
+  for (int i = 0; i < n; ++i) xi[i] = normal(rng);
+  return 0;
+}
+
 // dataset.cpp:118-124 (split_standardize's permutation)
 int or_split_order(int64_t n, uint64_t split_seed, int64_t* order) {
   if (n < 1) return 2;
