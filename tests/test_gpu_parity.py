@@ -87,6 +87,38 @@ def test_hv_full_size_dense_accumulation(ctx, cfg, impl, s):
         assert rel(out[r0:r1], ref) <= HV_TOL, (r0, rel(out[r0:r1], ref))
 
 
+@pytest.mark.parametrize("impl", ["tc", "simt"])
+@pytest.mark.parametrize("d", [30, 31, 32])
+def test_hv_maximum_dimension(ctx, impl, d):
+    """d = 30 is the largest the tcgen05 kernel takes (augmented K = d + 2 <= 32);
+    d = 31, 32 run on the CUDA-core kernel under either engine."""
+    ctx.set_hv_impl(impl)
+    X, V, ls = make(500, d, 17, seed=d)
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, 1.3, 0.4])
+    out = ctx.hv(V)
+    ctx.set_hv_impl("tc")
+    assert rel(out, orc.hv(X, ls, 1.3, 0.4, V)) <= HV_TOL
+
+
+@pytest.mark.parametrize("impl", ["tc", "simt"])
+def test_hv_duplicate_points(ctx, impl):
+    """Collisions: duplicated inputs (u = 0 off the diagonal, the Gram's
+    cancellation at its worst) and a constant column."""
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal((400, 5)).astype(np.float32)
+    X[200:300] = X[:100]          # 100 exact duplicates
+    X[:, 3] = 0.7                 # a constant dimension
+    V = rng.standard_normal((400, 9)).astype(np.float32)
+    ls = np.array([0.8, 1.1, 0.9, 1.3, 1.0])
+    ctx.set_hv_impl(impl)
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, 1.2, 0.3])
+    out = ctx.hv(V)
+    ctx.set_hv_impl("tc")
+    assert rel(out, orc.hv(X, ls, 1.2, 0.3, V)) <= HV_TOL
+
+
 def test_hv_impls_agree_and_deterministic(ctx):
     X, V, ls = make(3000, 6, 33, seed=3)
     ctx.set_data(X)
