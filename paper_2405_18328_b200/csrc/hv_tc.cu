@@ -357,6 +357,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         mma_commit(&bar_m1done[gr & (kDoneRing - 1)]);
+        if (gr == 0 && p.ctatime && lane == 0) {
+          long long gt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+          p.ctatime[blockIdx.x * 12 + 11] = gt;  // first Gram group issued
+        }
         if (p.trace && blockIdx.x == 0 && lane == 0)
           for (int h = 0; h < P; ++h) p.trace[(t + h) * 16 + 0] = clock64();
         if (++st == NB) st = 0, bph ^= 1u;
@@ -407,6 +412,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 5] = clock64();
+        if (t == 0 && p.ctatime && lane == 0) {
+          long long gt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+          p.ctatime[blockIdx.x * 12 + 10] = gt;  // first MMA-2 issued
+        }
         mma_commit(&bar_m2done[t & (kDoneRing - 1)]);
         if (tc == C - 1 || t == T - 1) mma_commit(&bar_ofull[c & 1]);
         if (t == T - 1 && p.ctatime && lane == 0) {
@@ -1193,13 +1203,20 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
         s_cw += c[12 * b + 9] - c[12 * b + 8];
         s_ex += c[12 * b + 3] - c[12 * b + 5];
       }
+      double f1 = 0, f2 = 0;
+      for (unsigned b = 0; b < grid; ++b) {
+        f1 += c[12 * b + 11] - c[12 * b + 1];
+        f2 += c[12 * b + 10] - c[12 * b + 1];
+      }
+      fprintf(stderr, "[hv_tc trace] fill from CTA start: first Gram group issued %.1f us, first K.V tile issued %.1f us\n",
+              f1 / grid / 1e3, f2 / grid / 1e3);
       fprintf(stderr, "[hv_tc trace] tail from epilogue loop end: last MMA-2 issued %+.1f us, ofull seen %.1f, "
               "final drain %.1f (TMEM read %.1f, fold %.1f, cp.async wait %.1f), sync+exit %.1f us\n",
               s_m2 / grid / 1e3, s_of / grid / 1e3, s_dr / grid / 1e3, s_tl / grid / 1e3, s_fo / grid / 1e3,
               s_cw / grid / 1e3, s_ex / grid / 1e3);
       // gaps between consecutive CTAs on one SM
       std::vector<std::vector<std::pair<long long, long long>>> per_sm(256);
-      for (unsigned b = 0; b < grid; ++b) per_sm[c[8 * b] & 255].push_back({c[12 * b + 1], c[12 * b + 3]});
+      for (unsigned b = 0; b < grid; ++b) per_sm[c[12 * b] & 255].push_back({c[12 * b + 1], c[12 * b + 3]});
       double gap = 0;
       int ng = 0;
       for (auto& v : per_sm) {
