@@ -254,7 +254,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&bar_a, 1);
     mbar_init(&bar_atm, 4);
-    for (int i = 0; i < NBUF; ++i) mbar_init(&bar_kfull[i], 4);
+    // tf32: the V tile of slot b completes on kfull[b] too (NV == NBUF): 4
+    // epilogue arrivals + the producer's expect_tx arrival, so MMA-2 checks
+    // one barrier per tile (each check costs ~90 clk of its loop, measured)
+    for (int i = 0; i < NBUF; ++i) mbar_init(&bar_kfull[i], BF ? 4 : 5);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar_ofull[i], 1);
       mbar_init(&bar_odrained[i], kEpiWarps);
@@ -305,13 +308,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t >= NV) mbar_wait(&bar_m2done[(t - NV) & (kDoneRing - 1)], ((t - NV) >> 3) & 1);
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const int vp = (jt_begin + t) * TJ;
+        uint64_t* vbar = BF ? &bar_vfull[st] : &bar_kfull[st];  // tf32: st == t % NBUF
         if (p.dbg & 8) {
-          mbar_arrive_warp(&bar_vfull[st]);
+          mbar_arrive_warp(vbar);
           continue;
         }
-        mbar_expect_tx_warp(&bar_vfull[st], p.vstage_bytes);
-        tma_load_2d_warp(base, &mVhi, &bar_vfull[st], vp, 0);
-        tma_load_2d_warp(base + vbox, &mVlo, &bar_vfull[st], vp, 0);
+        mbar_expect_tx_warp(vbar, p.vstage_bytes);
+        tma_load_2d_warp(base, &mVhi, vbar, vp, 0);
+        tma_load_2d_warp(base + vbox, &mVlo, vbar, vp, 0);
       }
     }
   } else if (warp == kWarpM1) {
@@ -384,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bar_odrained[cp & 1], (cp >> 1) & 1);
         }
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 12] = clock64();
-        mbar_wait(&bar_vfull[st], vph);
+        if (BF) mbar_wait(&bar_vfull[st], vph);
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 13] = clock64();
         mbar_wait(&bar_kfull[b], kph);
         tc_after();
@@ -1055,6 +1059,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   a.nv = std::min<int>(kMaxStages, (kSmemLimit - static_cast<int>(a.a_region) - 512 * spad - 1024 - a.nb * bstage) /
                                        static_cast<int>(a.vstage_bytes));
   if (env_nv > 0) a.nv = std::min(a.nv, env_nv);
+  if (!bf16) a.nv = Cfg<false>::kTilesInFlight;  // V slots share the K slots' barriers
   if (a.nv < 2 || a.nb < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
   a.row_idx = hp.row_idx;
   a.r0 = hp.r0;
