@@ -23,16 +23,24 @@ __device__ __forceinline__ void deposit(Red& red, int c, double v) {
 }
 
 // Writes this CTA's partials and returns true in the last CTA to finish.
+// Small n: the grid's y dimension splits the columns into groups of 4 (CTA
+// (x, y) takes row block x and column groups y, y + gridDim.y, ...), so each
+// CTA makes one pass instead of s / 4 serial ones.  Each (row block, column)
+// partial is still produced by one CTA in the same order: results are
+// identical to the one-dimensional grid.
+__device__ __forceinline__ bool my_col(int c) { return ((c >> 2) % gridDim.y) == blockIdx.y; }
+
 __device__ bool publish(Red& red, int s, double* part, SolveCtrl* ctrl) {
   __syncthreads();
   for (int c = threadIdx.x; c < s; c += blockDim.x) {
+    if (!my_col(c)) continue;
     double t = 0.0;
     for (int w = 0; w < NT / 32; ++w) t += red.v[w][c];
     part[static_cast<int64_t>(blockIdx.x) * s + c] = t;
   }
   __threadfence();
   __shared__ bool last;
-  if (threadIdx.x == 0) last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (!last) return false;
   __threadfence();
@@ -58,7 +66,7 @@ __device__ __forceinline__ double total_of(const double* part, int c, int s) {
 // n = 2048, measured).  f(c, e) returns element e's contribution to column c.
 template <class F>
 __device__ __forceinline__ void cols4(int s, int64_t rb, int64_t re, int64_t ld, Red& red, F f) {
-  for (int c0 = 0; c0 < s; c0 += 4) {
+  for (int c0 = 4 * static_cast<int>(blockIdx.y); c0 < s; c0 += 4 * static_cast<int>(gridDim.y)) {
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
 #pragma unroll
@@ -104,13 +112,14 @@ __global__ void col_dots_kernel(const float* A, const float* B, int64_t ld, int6
   cols4(s, rb, re, ld, red, [&](int, int64_t e) { return static_cast<double>(A[e]) * static_cast<double>(B[e]); });
   __syncthreads();
   for (int c = threadIdx.x; c < s; c += NT) {
+    if (!my_col(c)) continue;
     double t = 0.0;
     for (int w = 0; w < NT / 32; ++w) t += red.v[w][c];
     part[static_cast<int64_t>(blockIdx.x) * s + c] = t;
   }
   __threadfence();
   __shared__ bool last;
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -255,18 +264,21 @@ __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_
   if (ctrl->done) return;
   ROWS_OF_BLOCK
   for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
-#pragma unroll 4
-    for (int c = 0; c < s; ++c) {
-      const int st = cs.conv[c];
-      if (st == 1 || st == 3) continue;
-      const int64_t e = i + c * ld;
-      P[e] = st == 2 ? 0.f : fmaf(static_cast<float>(cs.beta[c]), P[e], R[e]);
+    for (int c0 = 4 * static_cast<int>(blockIdx.y); c0 < s; c0 += 4 * static_cast<int>(gridDim.y)) {
+#pragma unroll
+      for (int c = c0; c < c0 + 4; ++c) {
+        if (c >= s) break;
+        const int st = cs.conv[c];
+        if (st == 1 || st == 3) continue;
+        const int64_t e = i + c * ld;
+        P[e] = st == 2 ? 0.f : fmaf(static_cast<float>(cs.beta[c]), P[e], R[e]);
+      }
     }
   }
   __syncthreads();
   __threadfence();
   __shared__ bool last;
-  if (threadIdx.x == 0) last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -432,6 +444,12 @@ __global__ void copy_kernel(const float* A, int64_t lda, float* B, int64_t ldb, 
 }
 
 inline dim3 grid2(int64_t n, int s) { return dim3(static_cast<unsigned>(ceil_div(n, NT)), s); }
+// reduction kernels: row blocks x column groups of 4 while the row blocks alone
+// leave SMs idle (config 0: 8 row blocks for n = 2048)
+inline dim3 cgrid(int64_t n, int s) {
+  const int rb = reduce_blocks(n);
+  return dim3(static_cast<unsigned>(rb), rb < 148 ? static_cast<unsigned>((s + 3) / 4) : 1u);
+}
 
 void check_s(int s) {
   if (s < 1 || s >= SMAX) throw std::invalid_argument("solver kernels support 1 <= s < 256 columns");
@@ -449,14 +467,14 @@ void cg_snapshot(float* X, float* R, float* Xb, float* Rb, int64_t ld, int64_t n
 void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, double* part,
               unsigned* ticket, double* out, cudaStream_t st) {
   check_s(s);
-  col_dots_kernel<<<reduce_blocks(n), NT, 0, st>>>(A, B, ld, n, s, part, ticket, out);
+  col_dots_kernel<<<cgrid(n, s), NT, 0, st>>>(A, B, ld, n, s, part, ticket, out);
   WGP_LAUNCH_CHECK();
 }
 
 void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
              SolveCtrl* ctrl, cudaStream_t st) {
   check_s(s);
-  cg_init_kernel<<<reduce_blocks(n), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
+  cg_init_kernel<<<cgrid(n, s), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
   cg_seed_direction_kernel<<<grid2(n, s), NT, 0, st>>>(P, R, ld, n, s, cs.conv);
   WGP_LAUNCH_CHECK();
@@ -464,33 +482,33 @@ void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs
 
 void cg_alpha(const float* P, const float* HP, int64_t ld, int64_t n, int s, ColState cs,
               double* part, SolveCtrl* ctrl, cudaStream_t st) {
-  cg_alpha_kernel<<<reduce_blocks(n), NT, 0, st>>>(P, HP, ld, n, s, cs, part, ctrl);
+  cg_alpha_kernel<<<cgrid(n, s), NT, 0, st>>>(P, HP, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
 }
 
 void cg_update(float* X, float* R, const float* P, const float* HP, int64_t ld, int64_t n, int s,
                ColState cs, double* part, SolveCtrl* ctrl, bool refresh, cudaStream_t st) {
-  cg_update_kernel<<<reduce_blocks(n), NT, 0, st>>>(X, R, P, HP, ld, n, s, cs, part, ctrl,
+  cg_update_kernel<<<cgrid(n, s), NT, 0, st>>>(X, R, P, HP, ld, n, s, cs, part, ctrl,
                                                     refresh ? 1 : 0);
   WGP_LAUNCH_CHECK();
 }
 
 void cg_refresh_norm(float* R, const float* Rtmp, int64_t ld, int64_t n, int s, ColState cs,
                      double* part, SolveCtrl* ctrl, cudaStream_t st) {
-  cg_refresh_norm_kernel<<<reduce_blocks(n), NT, 0, st>>>(R, Rtmp, ld, n, s, cs, part, ctrl);
+  cg_refresh_norm_kernel<<<cgrid(n, s), NT, 0, st>>>(R, Rtmp, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
 }
 
 void cg_direction(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs,
                   double* part, SolveCtrl* ctrl, cudaStream_t st) {
-  cg_direction_kernel<<<reduce_blocks(n), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
+  cg_direction_kernel<<<cgrid(n, s), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
 }
 
 void norms_convergence(const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
                        SolveCtrl* ctrl, bool check_nan, bool begin_next, cudaStream_t st) {
   check_s(s);
-  norms_convergence_kernel<<<reduce_blocks(n), NT, 0, st>>>(R, ld, n, s, cs, part, ctrl,
+  norms_convergence_kernel<<<cgrid(n, s), NT, 0, st>>>(R, ld, n, s, cs, part, ctrl,
                                                             check_nan ? 1 : 0, begin_next ? 1 : 0);
   WGP_LAUNCH_CHECK();
 }
