@@ -38,6 +38,21 @@ std::atomic<uint64_t>& alloc_generation();
     WGP_CUDA(cudaGetLastError());                                            \
   } while (0)
 
+// Opt a kernel into `bytes` of dynamic shared memory once per device (the
+// attribute belongs to the device's copy of the kernel: a process driving two
+// GPUs through two contexts must set it on each).
+#define WGP_SMEM_ATTR(kernel, bytes)                                                            \
+  do {                                                                                          \
+    static std::atomic<unsigned long long> mask__{0};                                           \
+    int dev__ = 0;                                                                              \
+    WGP_CUDA(cudaGetDevice(&dev__));                                                            \
+    const unsigned long long bit__ = 1ull << (dev__ & 63);                                      \
+    if (!(mask__.load(std::memory_order_acquire) & bit__)) {                                    \
+      WGP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)); \
+      mask__.fetch_or(bit__, std::memory_order_acq_rel);                                        \
+    }                                                                                           \
+  } while (0)
+
 constexpr double kSqrt3 = 1.7320508075688772;
 constexpr double kLog2e = 1.4426950408889634;
 constexpr double kLn2 = 0.6931471805599453;

@@ -152,12 +152,7 @@ template <int DMAX>
 void launch_grad(const GradParams& p, cudaStream_t st) {
   const int dps = p.dp + 1, sp = p.s + 1;
   const size_t smem = sizeof(float) * (2 * 64 * dps + 2 * 64 * sp + 2 * 64);
-  static bool configured = false;
-  if (!configured) {
-    WGP_CUDA(cudaFuncSetAttribute(grad_kernel<DMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
-    configured = true;
-  }
+  WGP_SMEM_ATTR(grad_kernel<DMAX>, 200 * 1024);
   grad_kernel<DMAX><<<grad_blocks(p.m < 0 ? p.n : p.m), NT, smem, st>>>(p);
   WGP_LAUNCH_CHECK();
 }
@@ -253,11 +248,7 @@ void rff_probes(const RffParams& p, cudaStream_t st) {
   if (p.s > 128) throw std::invalid_argument("rff_probes: at most 128 probes per launch");
   const int SP = ((p.s + 15) / 16) * 16;
   const size_t smem = sizeof(float) * (RF * (RT + 4) + RF * SP);
-  static bool configured = false;
-  if (!configured) {
-    WGP_CUDA(cudaFuncSetAttribute(rff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    configured = true;
-  }
+  WGP_SMEM_ATTR(rff_kernel, 64 * 1024);
   rff_kernel<<<static_cast<unsigned>(ceil_div(p.n, RT)), NT, smem, st>>>(p);
   WGP_LAUNCH_CHECK();
 }

@@ -550,11 +550,7 @@ int choose_grad_splits(int64_t row_tiles, int jt, int sms) {
 template <int D>
 void launch_grad_tc(const CUtensorMap& mh, const CUtensorMap& ml, const GradTcArgs& a, unsigned grid, int smem,
                     cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    WGP_CUDA(cudaFuncSetAttribute(grad_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, gSmemLimit));
-    configured = true;
-  }
+  WGP_SMEM_ATTR(grad_tc_kernel<D>, gSmemLimit);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(gThreads);

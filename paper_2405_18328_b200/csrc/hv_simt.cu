@@ -157,12 +157,7 @@ template <int CPT>
 void launch(const HvParams& p, cudaStream_t st) {
   const int dps = p.dp + 1;
   const size_t smem = sizeof(float) * (TM * dps + TJ * dps + TJ * (TM + 4) + TJ * 16 * CPT);
-  static bool configured = false;
-  if (!configured) {
-    WGP_CUDA(cudaFuncSetAttribute(hv_simt_kernel<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  96 * 1024));
-    configured = true;
-  }
+  WGP_SMEM_ATTR(hv_simt_kernel<CPT>, 96 * 1024);
   const unsigned grid = static_cast<unsigned>(ceil_div(p.m, TM));
   if (grid == 0) return;
   hv_simt_kernel<CPT><<<grid, NT, smem, st>>>(p);

@@ -953,11 +953,7 @@ void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorM
                const CUtensorMap& mPart,
                const CUtensorMap& mVhi, const CUtensorMap& mVlo, const TcArgs& a, unsigned grid, int smem,
                cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    WGP_CUDA(cudaFuncSetAttribute(hv_tc_kernel<BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-    configured = true;
-  }
+  WGP_SMEM_ATTR(hv_tc_kernel<BF>, kSmemLimit);
   hv_tc_kernel<BF><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart, a);
   WGP_LAUNCH_CHECK();
 }
