@@ -355,6 +355,23 @@ def test_train_modes(ctx):
     assert outs["warm"].steps[1].warm_start_distance > 0
 
 
+@pytest.mark.parametrize("kind", ["cg", "sgd"])
+def test_training_is_deterministic(ctx, kind):
+    """optimizer_test.cpp:137-151: two runs of the same configuration give
+    bitwise-identical parameters, gradients and solver iteration counts
+    (fixed-order reductions everywhere, no float atomics)."""
+    p = datasets.config0(n=400, d=3)
+    ctx.set_data(p.X)
+    cfg = wg.TrainConfig(steps=5, num_probes=4, mode="warm", seed=3,
+                         solver=wg.SolverConfig(kind=kind, learning_rate=1.0, minibatch_size=100,
+                                                max_iterations=2000))
+    a, b = ctx.train(p.y, cfg), ctx.train(p.y, cfg)
+    for ra, rb in zip(a.steps, b.steps):
+        assert np.array_equal(ra.raw_params, rb.raw_params)
+        assert np.array_equal(ra.gradient, rb.gradient)
+        assert ra.solver_iterations == rb.solver_iterations
+
+
 def test_train_solver_failure_names_step(ctx):
     p = datasets.config0(n=100, d=2)
     ctx.set_data(p.X)
