@@ -446,6 +446,24 @@ def test_hv_accumulation_knobs_subprocess():
         assert r.returncode == 0, (chunk, flush, splits, r.stdout, r.stderr[-2000:])
 
 
+def test_hv_output_modes_forced_splits_subprocess():
+    """The store / residual / subtract epilogues with the exact diagonal inside
+    a column block, under forced J-split counts (WGP_TC_SPLITS is read once
+    per process): 1 runs the kernel's own row epilogue, 3 the split partials
+    plus tc_reduce_kernel."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for splits in ("1", "3"):
+        for extra in ({}, {"WGP_TC_CHUNK": "4", "WGP_TC_FLUSH": "1"}):
+            env = dict(os.environ, WGP_TC_SPLITS=splits, PYTHONPATH=root, **extra)
+            r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x",
+                                "tests/test_gpu_sharded.py::test_hv_cols_matches_dense_oracle"],
+                               env=env, cwd=root, capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, (splits, extra, r.stdout[-2000:], r.stderr[-2000:])
+
+
 def test_cg_unreachable_tolerance_stays_bounded(ctx):
     """A tolerance below the fp32 attainable accuracy never converges: every
     column stalls, is restored to its best iterate (exact residual at a
