@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--hv-impl", default="tc", choices=["tc", "tc_bf16", "simt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--outer", action="store_true", help="also time config-2 outer steps")
+    ap.add_argument("--outer", action="store_true",
+                    help="also time config-2 outer steps (row-sharded over the ranks under torchrun)")
     return ap.parse_args()
 
 
@@ -166,6 +167,47 @@ def outer_steps(wg, datasets, device, args):
         except Exception as e:  # report, keep the other solvers' numbers
             out[name] = {"error": str(e)[:200]}
         ctx.close()
+    return out
+
+
+def outer_sharded(wg, datasets, device, args, ws, rank):
+    """BASELINE config 2 outer loop row-sharded over `ws` GPUs
+    (sharded.sharded_train on the library's operators: CG with per-iteration
+    all-gathers of the direction, AP with per-block exchanges, the gradient
+    summed in rank order).  Per-step time: host clock around each step with
+    the device synchronised, maximum over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_18328_b200 import sharded
+
+    p = datasets.config2()
+    n = p.X.shape[0]
+    r0, r1 = sharded.row_range(n, rank, ws)
+    ctx = wg.Context(device, hv_impl=args.hv_impl)
+    ctx.set_data(p.X)
+    ctx.set_split_global(False)  # strong scaling: J splits keyed on the shard's rows
+    ops = sharded.device_train_ops(ctx, r0, r1)
+    n_steps = args.warmup + max(args.steps, 1)
+    out = {"workload": "config2 n=41157 d=9 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start",
+           "sharding": f"rows{ws}", "timing": "host clock per outer step (device synchronised), max over ranks",
+           "steps": max(args.steps, 1), "warmup_steps": args.warmup}
+    for name, sc in {"cg": dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=1000),
+                     "ap": dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=100,
+                                block_size=1000)}.items():
+        cfg = wg.TrainConfig(steps=n_steps, learning_rate=0.1, num_probes=64, mode="warm", seed=0,
+                             transform="log", estimator="pathwise", rff_features=1000, init_noise=0.5,
+                             init_constrained=1.0, solver=wg.SolverConfig(**sc))
+        torch.cuda.synchronize()
+        steps = sharded.sharded_train(ops, p.y, cfg)
+        timed = steps[args.warmup:]
+        t = torch.tensor([1e3 * float(np.mean([s.step_seconds for s in timed]))], device=f"cuda:{device}")
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out[name] = {"ms_per_step": float(t.item()),
+                     "iterations_mean": float(np.mean([s.solver_iterations for s in timed])),
+                     "config": {k: v for k, v in sc.items() if k != "kind"}}
+    ctx.close()
     return out
 
 
@@ -314,6 +356,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # multi-GPU outer steps run on every rank (collectives), before rank 0 reports
+    outer_multi = outer_sharded(wg, datasets, local, args, ws, rank) if (args.outer and ws > 1) else None
     if rank != 0:
         if ws > 1:
             dist.barrier()
@@ -372,7 +416,7 @@ def main():
         "clocks": clocks,
     }
     if args.outer:
-        line["outer"] = outer_steps(wg, datasets, local, args)
+        line["outer"] = outer_multi if ws > 1 else outer_steps(wg, datasets, local, args)
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(p, args.cpu_seconds)
     print(json.dumps(line), flush=True)

@@ -270,3 +270,136 @@ def sharded_grad(local_grad: Callable[[], tuple], group=None):
     p = len(qa)
     tot = tot.cpu()
     return tot[:p].numpy(), tot[p:].numpy()
+
+
+# ------------------------------------------------------------------ outer loop
+@dataclass
+class TrainOps:
+    """Rank-local operations of the row-sharded outer loop (rows [r0, r1)).
+
+    set_hyper(constrained)                 -> None (operators and probes follow theta)
+    probes(seed, s, F, pathwise, dist)      -> full n x s float32 probes
+    local_hv                                -> CG's H[I, :] V_full (torch)
+    ap_ops                                  -> ApOps of the current theta
+    grad(transform, raw, vy, L, R, coef)    -> (qa, qb): this rank's rows against all points
+    """
+    n: int
+    d: int
+    r0: int
+    r1: int
+    set_hyper: Callable
+    probes: Callable
+    local_hv: Callable
+    ap_ops: Callable
+    grad: Callable
+    device: object = None
+
+
+@dataclass
+class ShardedStep:
+    step: int
+    raw_params: list
+    constrained_params: list
+    gradient: list
+    solver_iterations: int
+    per_column_relative_residual: List[float]
+    step_seconds: float
+
+
+_SOLVER_STREAM = 0x736F6C7665  # proj/src/optimizer.cpp:15
+
+
+def sharded_train(ops: TrainOps, y, cfg, group=None) -> List[ShardedStep]:
+    """run_loop (proj/src/optimizer.cpp:81-171) over row shards, with the
+    semantics of the single-GPU wgp_train: initial raw theta, probe draws
+    (fixed: derive_seed(seed, 1) once; resampled: derive_seed(seed, t)),
+    pathwise RFF or Gaussian / Rademacher probes, the solver seed
+    derive_seed(derive_seed(seed, solver stream), t), warm starts from the
+    previous step's solutions (mode "warm"), gradient = quadratic - trace
+    from the row-sharded contractions (coefficient 1 / (2 s)), Adam on the
+    host (identical on every rank).  Solvers: CG and AP (SGD has no sharded
+    driver; SURVEY §8e marks it optional)."""
+    import time
+
+    import numpy as np
+
+    from . import Hyperparameters, NumericalError as LibNumericalError, adam_step, derive_seed
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    kind = cfg.solver.kind
+    if kind not in ("cg", "ap"):
+        raise ValueError("sharded_train: CG and AP only")
+    n, d, r0, r1 = ops.n, ops.d, ops.r0, ops.r1
+    s = cfg.num_probes
+    T = cfg.transform
+    init = [cfg.init_constrained] * d + [cfg.init_signal if cfg.init_signal > 0 else cfg.init_constrained,
+                                         cfg.init_noise if cfg.init_noise > 0 else cfg.init_constrained]
+    raw = Hyperparameters.from_constrained(init[:d], init[d], init[d + 1], T).raw.astype(np.float64).copy()
+    m, v = np.zeros_like(raw), np.zeros_like(raw)
+    fixed, warm = cfg.mode != "cold", cfg.mode == "warm"
+    pathwise = cfg.estimator == "pathwise"
+    F = cfg.rff_features if cfg.rff_features > 0 else 1000
+    y = np.asarray(y, dtype=np.float32).reshape(-1)
+    probe_seed = derive_seed(cfg.seed, 1) if fixed else None
+    dev = ops.device
+    prev = None
+    out: List[ShardedStep] = []
+    for t in range(1, cfg.steps + 1):
+        t0 = time.perf_counter()
+        try:
+            cons = Hyperparameters(raw.copy(), T).to_constrained_vector()
+            ops.set_hyper(cons)
+            if not fixed:
+                probe_seed = derive_seed(cfg.seed, t)
+            Z = ops.probes(probe_seed, s, F, pathwise, cfg.probe_distribution)
+            rhs = np.empty((n, s + 1), dtype=np.float32)
+            rhs[:, 0] = y
+            rhs[:, 1:] = Z
+            B_local = torch.from_numpy(rhs[r0:r1].copy()).to(dev)
+            sc = cfg.solver
+            init_local = prev if (warm and prev is not None) else None
+            if kind == "cg":
+                st = sharded_cg(ops.local_hv, B_local, n, sc.tol_mean, sc.tol_samples, sc.max_iterations,
+                                init_local=init_local, group=group)
+            else:
+                st = sharded_ap(ops.ap_ops(), B_local, n, r0, r1, sc.block_size, sc.tol_mean, sc.tol_samples,
+                                sc.max_iterations, init_local=init_local, group=group)
+            Vf = _gather_rows(st.solutions, n, world, group).cpu().numpy()
+            vy = np.ascontiguousarray(Vf[:, 0])
+            Vp = np.asfortranarray(Vf[:, 1:])
+            R = Vp if pathwise else np.asfortranarray(Z)
+            qa, qb = sharded_grad(lambda: ops.grad(T, raw, vy, Vp, R, 0.5 / s), group)
+            g = np.ascontiguousarray(qa - qb)
+            adam_step(raw, g, m, v, t, cfg)
+        except (NumericalError, LibNumericalError) as e:
+            raise NumericalError(f"step {t}: {e}") from e
+        prev = st.solutions
+        out.append(ShardedStep(t, raw.tolist(), Hyperparameters(raw.copy(), T).to_constrained_vector().tolist(),
+                               g.tolist(), st.iterations_used, st.per_column_relative_residual,
+                               time.perf_counter() - t0))
+    return out
+
+
+def device_train_ops(ctx, r0: int, r1: int) -> TrainOps:
+    """TrainOps backed by the library on this rank's device: the fused H.V and
+    AP block inverses over rows [r0, r1), the RFF / host probe generators and
+    the row-range gradient (all indices global)."""
+    import numpy as np
+
+    from . import sample_probes
+
+    n = ctx.n
+    local = device_local_hv(ctx, r0, r1)
+
+    def set_hyper(cons):
+        ctx.set_hyper(np.asarray(cons, dtype=np.float64))
+
+    def probes(seed, s, F, pathwise, dist_name):
+        return ctx.rff_probes(F, s, seed) if pathwise else sample_probes(n, s, dist_name, seed)
+
+    def grad(T, raw, vy, L, R, coef):
+        ctx.set_rows(r0, r1)
+        return ctx.grad(T, raw, vy, L, R, coef)
+
+    return TrainOps(n, ctx.d, r0, r1, set_hyper, probes, local, lambda: device_ap_ops(ctx, r0, r1), grad,
+                    torch.device("cuda", torch.cuda.current_device()))

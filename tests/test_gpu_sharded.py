@@ -110,3 +110,25 @@ def test_row_range_gradient_partials_sum_to_full(impl):
 
 def sharded_rows(n, world):
     return [sharded.row_range(n, r, world) for r in range(world)]
+
+
+@pytest.mark.parametrize("kind", ["cg", "ap"])
+def test_sharded_train_on_device_matches_train(kind):
+    """The row-sharded outer loop on the device operators (world 1) follows
+    the library's own training loop (wgp_train) at a tight solver tolerance:
+    the same probes, seeds, warm starts and Adam; trajectories within 1e-3."""
+    from paper_2405_18328_b200 import datasets
+
+    p = datasets.config0(n=1024, d=4)
+    ctx = wg.Context(0)
+    ctx.set_data(p.X)
+    cfg = wg.TrainConfig(steps=5, num_probes=8, mode="warm", seed=0, transform="log", estimator="pathwise",
+                         rff_features=256, init_noise=0.5,
+                         solver=wg.SolverConfig(kind=kind, tol_mean=1e-4, tol_samples=1e-4, block_size=256,
+                                                max_iterations=5000))
+    ref = ctx.train(p.y, cfg)
+    steps = sharded.sharded_train(sharded.device_train_ops(ctx, 0, p.X.shape[0]), p.y, cfg)
+    got = np.array([s.constrained_params for s in steps])
+    exp = np.array([r.constrained_params for r in ref.steps])
+    assert np.max(np.abs(got - exp) / np.abs(exp)) <= 1e-3
+    ctx.close()

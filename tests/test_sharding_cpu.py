@@ -173,3 +173,104 @@ def test_two_ranks_gloo_sharded_ap_and_gradient():
     _, full = orc.grad_contractions(X, "softplus", raw, vy, L, R, 0.125)
     assert np.array_equal(out[0][5], out[1][5])  # identical on every rank
     assert np.allclose(out[0][5], full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
+
+
+# ------------------------------------------------------------------ outer loop
+def host_train_ops(X, r0, r1):
+    """TrainOps over host fp64 matrices (the device path: sharded.device_train_ops)."""
+    from oracle import oracle as orc
+
+    n, d = X.shape
+    state = {}
+
+    def set_hyper(cons):
+        state["c"] = np.asarray(cons, dtype=np.float64)
+        state["H"] = orc.kernel_matrices(X, state["c"][:d], state["c"][d], state["c"][d + 1])[0]
+
+    def probes(seed, s, F, pathwise, dist_name):
+        c = state["c"]
+        if pathwise:
+            return orc.rff_probes(X, c[:d], c[d], c[d + 1], orc.rff_base(n, d, F, s, seed)).astype(np.float32)
+        return orc.sample_probes(n, s, dist_name, seed).astype(np.float32)
+
+    def local_hv(V):
+        return (torch.from_numpy(state["H"][r0:r1]) @ V.double()).to(V.dtype)
+
+    def ap_ops():
+        ops = host_ap_ops(state["H"], r0, r1)
+        return sharded.ApOps(lambda B, Xf: (B.double() - torch.from_numpy(state["H"][r0:r1]) @ Xf.double()).to(B.dtype),
+                             lambda R, dl, j0, j1: (R.double() - torch.from_numpy(state["H"][r0:r1, j0:j1]) @ dl).to(R.dtype),
+                             ops.factor, ops.block_solve)
+
+    def grad(T, raw, vy, L, R, coef):
+        m = np.zeros((n, 1))
+        m[r0:r1] = 1.0
+        z = np.zeros(n)
+        _, qa = orc.grad_contractions(X, T, raw, z, vy[:, None] * m, vy[:, None], 0.5)
+        _, qb = orc.grad_contractions(X, T, raw, z, np.asarray(L) * m, np.asarray(R), coef)
+        return qa, qb
+
+    return sharded.TrainOps(n, d, r0, r1, set_hyper, probes, local_hv, ap_ops, grad, torch.device("cpu"))
+
+
+def _train_problem():
+    from oracle import oracle as orc
+
+    rng = np.random.default_rng(9)
+    X = rng.standard_normal((200, 2)).astype(np.float32).astype(np.float64)
+    y = (np.sin(2 * X).sum(1) + 0.1 * rng.standard_normal(200)).astype(np.float32)
+    return X, y
+
+
+def _train_cfg(mod, kind, estimator):
+    return mod.TrainConfig(steps=4, num_probes=4, mode="warm", seed=5, transform="log", estimator=estimator,
+                           rff_features=64, init_noise=0.5,
+                           solver=mod.SolverConfig(kind=kind, tol_mean=1e-6, tol_samples=1e-6, block_size=64,
+                                                   max_iterations=5000))
+
+
+def _worker_train(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2405_18328_b200 as wg
+
+    X, y = _train_problem()
+    r0, r1 = sharded.row_range(200, rank, world)
+    res = {}
+    for kind in ("cg", "ap"):
+        steps = sharded.sharded_train(host_train_ops(X, r0, r1), y, _train_cfg(wg, kind, "pathwise"))
+        res[kind] = [s.constrained_params for s in steps]
+    out[rank] = res
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,estimator", [("cg", "pathwise"), ("cg", "hutchinson"), ("ap", "pathwise")])
+def test_sharded_train_single_process_matches_oracle_train(kind, estimator):
+    """The sharded outer loop restates wgp_train's semantics (seeds, probes,
+    warm starts, gradient assembly, Adam): with host operators it follows the
+    oracle's training loop (optimizer.cpp:81-171) to 1e-5."""
+    import paper_2405_18328_b200 as wg
+    from oracle import oracle as orc
+
+    X, y = _train_problem()
+    steps = sharded.sharded_train(host_train_ops(X, 0, 200), y, _train_cfg(wg, kind, estimator))
+    o = orc.train(X, y.astype(np.float64), _train_cfg(orc, kind, estimator))
+    got = np.array([s.constrained_params for s in steps])
+    assert np.allclose(got, o["constrained_params"], rtol=1e-5), (got, o["constrained_params"])
+
+
+@pytest.mark.timeout(300)
+def test_two_ranks_gloo_sharded_train():
+    import paper_2405_18328_b200 as wg
+
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_train, args=(world, _free_port(), out), nprocs=world, join=True)
+    X, y = _train_problem()
+    for kind in ("cg", "ap"):
+        ref = sharded.sharded_train(host_train_ops(X, 0, 200), y, _train_cfg(wg, kind, "pathwise"))
+        refc = np.array([s.constrained_params for s in ref])
+        assert out[0][kind] == out[1][kind]  # identical on every rank
+        assert np.allclose(np.array(out[0][kind]), refc, rtol=1e-6), kind
