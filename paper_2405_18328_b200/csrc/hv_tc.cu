@@ -124,6 +124,7 @@ struct TcArgs {
   const int* done;
   long long* trace;  // WGP_TC_TRACE: per-tile clock64 stamps of CTA 0 ([T][16])
   long long* ctatime;  // WGP_TC_TRACE: per CTA {smid, globaltimer at start, after the tile loop, at exit}
+  int nk1;  // packed Gram K steps (TcOperands::nk1), 0: 12 hi / lo MMAs
   int dbg;  // ablation bits (WGP_TC_DEBUG): 1 no epilogue math, 2 no MMA-2, 4 no MMA-1, 8 no V loads,
             // 16 no epilogue TMEM traffic, 32 no B loads, 128 (bf16) FMA-pipe ex2 for odd entries
 };
@@ -355,9 +356,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t d = tmem + K::grp_col(gi);
         if (!(p.dbg & 4)) {
           if constexpr (!K::kATmem) {
-            mma1_group_tf32(d, dAhi, dAlo, dBhi, dBlo, id1);
+            if (p.nk1)
+              mma1_packed_tf32(d, dAhi, dAlo, dBhi, dBlo, id1, p.nk1);
+            else
+              mma1_group_tf32(d, dAhi, dAlo, dBhi, dBlo, id1);
           } else {
-            mma1_group_tf32_ts(d, tmem + K::kAhi, tmem + K::kAlo, dBhi, dBlo, id1);
+            static_assert(K::kAlo == K::kAhi + 32, "packed Gram: A K columns contiguous in TMEM");
+            if (p.nk1)
+              mma1_packed_tf32_ts(d, tmem + K::kAhi, dBhi, dBlo, id1, p.nk1);
+            else
+              mma1_group_tf32_ts(d, tmem + K::kAhi, tmem + K::kAlo, dBhi, dBlo, id1);
           }
         }
         mma_commit(&bar_m1done[gr & (kDoneRing - 1)]);
@@ -768,7 +776,7 @@ __global__ void split_v_bf16_kernel(const float* V, int64_t ldv, int64_t j0, int
 }
 
 // Augmented operand rows from the prepared points (see TcOperands).
-__global__ void build_ops_kernel(const float* xs, int64_t n, int64_t n_pad, int dp, int d, float* ahi,
+__global__ void build_ops_kernel(const float* xs, int64_t n, int64_t n_pad, int dp, int d, bool packed, float* ahi,
                                  float* alo, float* bhi, float* blo) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_pad) return;
@@ -792,14 +800,33 @@ __global__ void build_ops_kernel(const float* xs, int64_t n, int64_t n_pad, int 
     b[d] = 1.f;
     b[d + 1] = static_cast<float>(sq);
   }
+  if (!packed) {
 #pragma unroll
-  for (int k = 0; k < kKA; ++k) {
-    const float ah = __uint_as_float(__float_as_uint(a[k]) & kTfMask);
-    const float bh = __uint_as_float(__float_as_uint(b[k]) & kTfMask);
-    ahi[i * kKA + k] = ah;
-    alo[i * kKA + k] = a[k] - ah;
-    bhi[i * kKA + k] = bh;
-    blo[i * kKA + k] = b[k] - bh;
+    for (int k = 0; k < kKA; ++k) {
+      const float ah = __uint_as_float(__float_as_uint(a[k]) & kTfMask);
+      const float bh = __uint_as_float(__float_as_uint(b[k]) & kTfMask);
+      ahi[i * kKA + k] = ah;
+      alo[i * kKA + k] = a[k] - ah;
+      bhi[i * kKA + k] = bh;
+      blo[i * kKA + k] = b[k] - bh;
+    }
+    return;
+  }
+  // packed (TcOperands::nk1): [a_hi | a_hi | a_lo] . [b_hi | b_lo | b_hi]
+  const int w = d + 2;
+  for (int k = 0; k < 2 * kKA; ++k) {
+    const int seg = k / w, e = k - seg * w;
+    float av = 0.f, bv = 0.f;
+    if (seg < 3) {
+      const float ah = __uint_as_float(__float_as_uint(a[e]) & kTfMask);
+      const float bh = __uint_as_float(__float_as_uint(b[e]) & kTfMask);
+      av = seg < 2 ? ah : a[e] - ah;
+      bv = seg == 1 ? b[e] - bh : bh;
+    }
+    float* pa = k < kKA ? ahi : alo;
+    float* pb = k < kKA ? bhi : blo;
+    pa[i * kKA + (k & (kKA - 1))] = av;
+    pb[i * kKA + (k & (kKA - 1))] = bv;
   }
 }
 
@@ -941,8 +968,10 @@ void TcOperands::build(const float* xs, int64_t n_, int dp, int d_, cudaStream_t
   a_lo = static_cast<char*>(a_hi) + plane;
   b_hi = static_cast<char*>(a_hi) + 2 * plane;
   b_lo = static_cast<char*>(a_hi) + 3 * plane;
+  static const bool no_pack = getenv("WGP_TC_NOPACK") != nullptr;  // A/B switch
+  nk1 = (!no_pack && 3 * (d + 2) <= 2 * kKA) ? static_cast<int>(ceil_div(3 * (d + 2), 8)) : 0;
   build_ops_kernel<<<static_cast<unsigned>(ceil_div(n_pad, 128)), 128, 0, st>>>(
-      xs, n, n_pad, dp, d, static_cast<float*>(a_hi), static_cast<float*>(a_lo), static_cast<float*>(b_hi),
+      xs, n, n_pad, dp, d, nk1 > 0, static_cast<float*>(a_hi), static_cast<float*>(a_lo), static_cast<float*>(b_hi),
       static_cast<float*>(b_lo));
   WGP_LAUNCH_CHECK();
   valid = true;
@@ -1077,6 +1106,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
     return e ? atoi(e) : 0;
   }();
   a.dbg = dbg;
+  a.nk1 = ops.nk1;
   static const bool tracing = getenv("WGP_TC_TRACE") != nullptr;
   static Workspace ws_trace;
   a.trace = nullptr;

@@ -25,6 +25,11 @@ struct TcOperands {
   void* b_hi = nullptr;
   void* b_lo = nullptr;
   void* sq = nullptr;    // [n_pad] fp32 |x|^2 (diagonal fix)
+  // Packed Gram (d + 2 <= 21): the 64 floats [a_hi | a_hi | a_lo] (A) and
+  // [b_hi | b_lo | b_hi] (B), each segment d + 2 wide, split over the two
+  // planes (K 0..31 in *_hi, 32..63 in *_lo); MMA-1 then takes nk1 =
+  // ceil(3 (d + 2) / 8) K steps instead of 12 MMAs.  0: the hi / lo planes.
+  int nk1 = 0;
   size_t bytes = 0;
   TcWorkspaces* ws = nullptr;  // per-launch scratch (V planes, gathered rows, split partials)
   // Kernel timing (wgp_profile): CUDA events around every hv_tc_kernel launch.

@@ -231,6 +231,72 @@ __device__ __forceinline__ void mma1_group_tf32(uint32_t d, uint64_t ah, uint64_
       "}\n"
       ::"r"(d), "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc));
 }
+// Packed Gram (small d): the three 3xTF32 passes concatenated along K,
+// a' = [a_hi | a_hi | a_lo], b' = [b_hi | b_lo | b_hi] (each d + 2 wide), so
+// a'.b' = hi.hi + hi.lo + lo.hi in nk = ceil(3 (d + 2) / 8) <= 8 K steps
+// instead of 12 MMAs.  K columns 0..31 live in the "hi" plane, 32..63 in
+// the "lo" plane; steps past nk are predicated off (one elect, one block).
+#define WGP_PACKED_PREDS                                  \
+  " setp.ne.b32 f, 0, 0;\n"                               \
+  " setp.eq.b32 t, 0, 0;\n"                               \
+  " elect.sync _|e, 0xffffffff;\n"                        \
+  " setp.gt.u32 q, %6, 1;\n and.pred p1, e, q;\n"         \
+  " setp.gt.u32 q, %6, 2;\n and.pred p2, e, q;\n"         \
+  " setp.gt.u32 q, %6, 3;\n and.pred p3, e, q;\n"         \
+  " setp.gt.u32 q, %6, 4;\n and.pred p4, e, q;\n"         \
+  " setp.gt.u32 q, %6, 5;\n and.pred p5, e, q;\n"         \
+  " setp.gt.u32 q, %6, 6;\n and.pred p6, e, q;\n"         \
+  " setp.gt.u32 q, %6, 7;\n and.pred p7, e, q;\n"
+__device__ __forceinline__ void mma1_packed_tf32(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                                 uint32_t idesc, uint32_t nk) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t, q, p1, p2, p3, p4, p5, p6, p7;\n"
+      " .reg .b64 x, y;\n" WGP_PACKED_PREDS
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, f;\n"
+      " add.s64 x, %1, 2;\n add.s64 y, %3, 2;\n"
+      " @p1 tcgen05.mma.cta_group::1.kind::tf32 [%0], x, y, %5, t;\n"
+      " add.s64 x, %1, 4;\n add.s64 y, %3, 4;\n"
+      " @p2 tcgen05.mma.cta_group::1.kind::tf32 [%0], x, y, %5, t;\n"
+      " add.s64 x, %1, 6;\n add.s64 y, %3, 6;\n"
+      " @p3 tcgen05.mma.cta_group::1.kind::tf32 [%0], x, y, %5, t;\n"
+      " @p4 tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %4, %5, t;\n"
+      " add.s64 x, %2, 2;\n add.s64 y, %4, 2;\n"
+      " @p5 tcgen05.mma.cta_group::1.kind::tf32 [%0], x, y, %5, t;\n"
+      " add.s64 x, %2, 4;\n add.s64 y, %4, 4;\n"
+      " @p6 tcgen05.mma.cta_group::1.kind::tf32 [%0], x, y, %5, t;\n"
+      " add.s64 x, %2, 6;\n add.s64 y, %4, 6;\n"
+      " @p7 tcgen05.mma.cta_group::1.kind::tf32 [%0], x, y, %5, t;\n"
+      "}\n" ::"r"(d),
+      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(nk));
+}
+// As mma1_packed_tf32 with A_I in TMEM: K column k at TMEM column a0 + k.
+__device__ __forceinline__ void mma1_packed_tf32_ts(uint32_t d, uint32_t a0, uint64_t bh, uint64_t bl,
+                                                    uint32_t idesc, uint32_t nk) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, f, t, q, p1, p2, p3, p4, p5, p6, p7;\n"
+      " .reg .b32 x;\n"
+      " .reg .b64 y;\n" WGP_PACKED_PREDS
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, f;\n"
+      " add.u32 x, %1, 8;\n add.s64 y, %3, 2;\n"
+      " @p1 tcgen05.mma.cta_group::1.kind::tf32 [%0], [x], y, %5, t;\n"
+      " add.u32 x, %1, 16;\n add.s64 y, %3, 4;\n"
+      " @p2 tcgen05.mma.cta_group::1.kind::tf32 [%0], [x], y, %5, t;\n"
+      " add.u32 x, %1, 24;\n add.s64 y, %3, 6;\n"
+      " @p3 tcgen05.mma.cta_group::1.kind::tf32 [%0], [x], y, %5, t;\n"
+      " add.u32 x, %1, 32;\n"
+      " @p4 tcgen05.mma.cta_group::1.kind::tf32 [%0], [x], %4, %5, t;\n"
+      " add.u32 x, %1, 40;\n add.s64 y, %4, 2;\n"
+      " @p5 tcgen05.mma.cta_group::1.kind::tf32 [%0], [x], y, %5, t;\n"
+      " add.u32 x, %1, 48;\n add.s64 y, %4, 4;\n"
+      " @p6 tcgen05.mma.cta_group::1.kind::tf32 [%0], [x], y, %5, t;\n"
+      " add.u32 x, %1, 56;\n add.s64 y, %4, 6;\n"
+      " @p7 tcgen05.mma.cta_group::1.kind::tf32 [%0], [x], y, %5, t;\n"
+      "}\n" ::"r"(d),
+      "r"(a0), "l"(0ull), "l"(bh), "l"(bl), "r"(idesc), "r"(nk));
+}
+#undef WGP_PACKED_PREDS
 // MMA-1 group with A_I in TMEM (hi at column ah, lo at al): 12 MMAs, one
 // asm block and one elect, as mma1_group_tf32.
 __device__ __forceinline__ void mma1_group_tf32_ts(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,

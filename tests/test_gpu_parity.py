@@ -464,6 +464,57 @@ def test_hv_output_modes_forced_splits_subprocess():
             assert r.returncode == 0, (splits, extra, r.stdout[-2000:], r.stderr[-2000:])
 
 
+@pytest.mark.parametrize("d", [1, 3, 9, 19, 20])
+def test_hv_tc_entries_across_gram_packing(ctx, d):
+    """Kernel entries straight from the tcgen05 path (identity right-hand
+    sides give columns of H) against the fp64 oracle on both sides of the
+    packed-Gram limit (d + 2 <= 21 concatenates the three 3xTF32 passes along
+    K, TcOperands::nk1), with a near-duplicate pair for the cancellation in
+    |x_i|^2 + |x_j|^2 - 2 x_i.x_j."""
+    rng = np.random.default_rng(100 + d)
+    n = 1500
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    X[1] = X[0] + 1e-3
+    ls = np.exp(rng.uniform(np.log(0.5), np.log(2.0), d))
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, 1.0, 0.1])
+    E = np.zeros((n, 48), np.float32)
+    E[np.arange(48), np.arange(48)] = 1.0
+    assert np.abs(ctx.hv(E) - orc.hv(X, ls, 1.0, 0.1, E)).max() <= 5e-5
+    V = rng.standard_normal((n, 17)).astype(np.float32)
+    ref = orc.hv(X, ls, 1.0, 0.1, V)
+    assert np.linalg.norm(ctx.hv(V) - ref) / np.linalg.norm(ref) <= 1e-5
+
+
+def test_hv_tc_packed_gram_matches_hi_lo_subprocess():
+    """WGP_TC_NOPACK=1 (read once per process) forces the 12-MMA hi / lo
+    Gram; both Gram forms agree to 2e-6 on a small-d problem."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, paper_2405_18328_b200 as wg\n"
+        "rng = np.random.default_rng(8)\n"
+        "X = rng.standard_normal((5000, 7)).astype(np.float32)\n"
+        "V = rng.standard_normal((5000, 33)).astype(np.float32)\n"
+        "c = wg.Context(0)\n"
+        "c.set_data(X); c.set_hyper([0.8] * 7 + [1.0, 0.3])\n"
+        "np.save('gpurun_out/_pack_' + ('hilo' if __import__('os').environ.get('WGP_TC_NOPACK') else 'packed') + '.npy', c.hv(V))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    outs = []
+    for extra in ({}, {"WGP_TC_NOPACK": "1"}):
+        env = dict(os.environ, PYTHONPATH=root, **extra)
+        env.pop("WGP_TC_NOPACK", None) if not extra else None
+        r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, (extra, r.stderr[-2000:])
+        path = os.path.join(root, "gpurun_out", "_pack_" + ("hilo" if extra else "packed") + ".npy")
+        outs.append(np.load(path))
+        os.remove(path)
+    assert np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[1]) <= 2e-6
+
+
 def test_cg_unreachable_tolerance_stays_bounded(ctx):
     """A tolerance below the fp32 attainable accuracy never converges: every
     column stalls, is restored to its best iterate (exact residual at a
