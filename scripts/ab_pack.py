@@ -1,6 +1,8 @@
-"""Packed vs hi/lo Gram (WGP_TC_NOPACK=1 selects the latter): entry accuracy
+"""A/B of an hv_tc variant switch (default WGP_TC_NOPACK: packed vs hi/lo
+Gram; WGP_TC_NODIRECT: direct distances vs Gram for d <= 4): entry accuracy
 (H columns through identity right-hand sides vs the fp64 oracle), H.V accuracy
-and kernel time at the config-2 / config-3 shapes.  usage: ab_pack.py"""
+and kernel time at the config-2 / config-3 shapes.
+usage: ab_pack.py [SWITCH [d,d,..]]"""
 import os
 import subprocess
 import sys
@@ -9,14 +11,16 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+SWITCH = sys.argv[1] if len(sys.argv) > 1 and sys.argv[1] != "child" else os.environ.get("AB_SWITCH", "WGP_TC_NOPACK")
+DIMS = [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else os.environ.get("AB_DIMS", "1,3,8,9,19,20,26")).split(",")]
 
 
 def child():
     import paper_2405_18328_b200 as wg
     from oracle import oracle as orc
-    tag = "nopack" if os.environ.get("WGP_TC_NOPACK") else "packed"
+    tag = "off" if os.environ.get(SWITCH) else "on"
     ctx = wg.Context(0, hv_impl="tc")
-    for d in (1, 3, 8, 9, 19, 20, 26):
+    for d in DIMS:
         rng = np.random.default_rng(d)
         n = 2000
         X = rng.standard_normal((n, d)).astype(np.float32)
@@ -39,10 +43,11 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "child":
         child()
         sys.exit(0)
-    for env in ({}, {"WGP_TC_NOPACK": "1"}):
-        e = dict(os.environ, **env)
+    for env in ({}, {SWITCH: "1"}):
+        e = dict(os.environ, AB_SWITCH=SWITCH, AB_DIMS=",".join(map(str, DIMS)), **env)
         subprocess.run([sys.executable, __file__, "child"], env=e, check=True)
-        for args in (["41157", "9", "65", "20"], ["100000", "3", "65", "5"], ["13500", "26", "65", "30"]):
+        for args in (["41157", "9", "65", "20"], ["100000", "3", "65", "5"], ["100000", "1", "65", "5"],
+                     ["13500", "26", "65", "30"]):
             out = subprocess.run([sys.executable, os.path.join(ROOT, "scripts/time_hv.py"), "tc", *args], env=e,
                                  capture_output=True, text=True, check=True).stdout.strip().splitlines()[-1]
-            print(("nopack " if env else "packed ") + out, flush=True)
+            print(("off " if env else "on  ") + out, flush=True)
