@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--outer", action="store_true",
-                    help="also time config-2 outer steps (row-sharded over the ranks under torchrun)")
+                    help="also time outer steps (row-sharded over the ranks under torchrun)")
+    ap.add_argument("--outer-config", type=int, default=2, choices=[2, 3],
+                    help="BASELINE config of --outer: 2 (CG / AP / SGD) or 3 (AP, 10-epoch budget)")
     return ap.parse_args()
 
 
@@ -133,23 +135,42 @@ def cpu_baseline(p, seconds):
                       f"s=65), {elapsed:.1f} s"}
 
 
-def outer_steps(wg, datasets, device, args):
-    """BASELINE config 2 outer loop (n=41,157, d=9, 64 pathwise probes + y,
-    1000 RFF features, log-space Adam lr 0.1, warm start): device time per
-    outer step (solve + gradient + probes, from the library's per-step CUDA
-    events) for CG (tol 0.01), AP (blocks of 1000) and SGD (minibatch 1000,
-    momentum 0.9), each over `steps` steps after `warmup` steps."""
+def outer_spec(datasets, args, sharded_run=False):
+    """The outer-loop workload of `--outer-config`:
+    2: BASELINE config 2 (n=41,157, d=9, 64 pathwise probes + y, 1000 RFF
+       features, log-space Adam lr 0.1, warm start) with CG (tol 0.01), AP
+       (blocks of 1000) and SGD (minibatch 1000, momentum 0.9), `steps` timed
+       steps after `warmup`;
+    3: BASELINE config 3 (n=391,386, d=3, s=65, AP blocks of 1000 with a
+       budget of 10 epochs per outer step, warm start): ~10 s per step on one
+       GPU, so at most 3 timed steps after 1 warm-up step.
+    Returns (problem, workload, solvers, timed steps, warm-up steps)."""
+    if args.outer_config == 3:
+        p = datasets.config3()
+        solvers = {"ap": dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=10, block_size=1000)}
+        return (p, "config3 n=391386 d=3 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start, "
+                   "AP 10-epoch budget", solvers, max(1, min(args.steps, 3)), 1)
     p = datasets.config2()
-    n_steps = args.warmup + max(args.steps, 1)
     solvers = {
         "cg": dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=1000),
         "ap": dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=100, block_size=1000),
-        "sgd": dict(kind="sgd", tol_mean=0.01, tol_samples=0.01, max_iterations=3000,
-                    minibatch_size=1000, momentum=0.9, learning_rate=10.0),
     }
-    out = {"workload": "config2 n=41157 d=9 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start",
+    if not sharded_run:
+        solvers["sgd"] = dict(kind="sgd", tol_mean=0.01, tol_samples=0.01, max_iterations=3000,
+                              minibatch_size=1000, momentum=0.9, learning_rate=10.0)
+    return (p, "config2 n=41157 d=9 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start", solvers,
+            max(args.steps, 1), args.warmup)
+
+
+def outer_steps(wg, datasets, device, args):
+    """The `--outer-config` outer loop on one GPU (outer_spec): device time
+    per outer step (solve + gradient + probes, from the library's per-step
+    CUDA events) per solver."""
+    p, workload, solvers, k_steps, w_steps = outer_spec(datasets, args)
+    n_steps = w_steps + k_steps
+    out = {"workload": workload,
            "timing": "CUDA events on the context stream around each outer step (device time)",
-           "steps": max(args.steps, 1), "warmup_steps": args.warmup}
+           "steps": k_steps, "warmup_steps": w_steps}
     for name, sc in solvers.items():
         ctx = wg.Context(device, hv_impl=args.hv_impl)
         ctx.set_data(p.X)
@@ -159,7 +180,7 @@ def outer_steps(wg, datasets, device, args):
                              solver=wg.SolverConfig(**sc))
         try:
             tr = ctx.train(p.y, cfg)
-            timed = tr.steps[args.warmup:]
+            timed = tr.steps[w_steps:]
             out[name] = {"ms_per_step": float(np.mean([r.step_ms for r in timed])),
                          "solver_ms_per_step": float(np.mean([r.solver_ms for r in timed])),
                          "iterations_mean": float(np.mean([r.solver_iterations for r in timed])),
@@ -171,7 +192,7 @@ def outer_steps(wg, datasets, device, args):
 
 
 def outer_sharded(wg, datasets, device, args, ws, rank):
-    """BASELINE config 2 outer loop row-sharded over `ws` GPUs
+    """The `--outer-config` outer loop (outer_spec; CG and AP) row-sharded over `ws` GPUs
     (sharded.sharded_train on the library's operators: CG with per-iteration
     all-gathers of the direction, AP with per-block exchanges, the gradient
     summed in rank order).  Per-step time: host clock around each step with
@@ -181,26 +202,24 @@ def outer_sharded(wg, datasets, device, args, ws, rank):
 
     from paper_2405_18328_b200 import sharded
 
-    p = datasets.config2()
+    p, workload, solvers, k_steps, w_steps = outer_spec(datasets, args, sharded_run=True)
     n = p.X.shape[0]
     r0, r1 = sharded.row_range(n, rank, ws)
     ctx = wg.Context(device, hv_impl=args.hv_impl)
     ctx.set_data(p.X)
     ctx.set_split_global(False)  # strong scaling: J splits keyed on the shard's rows
     ops = sharded.device_train_ops(ctx, r0, r1)
-    n_steps = args.warmup + max(args.steps, 1)
-    out = {"workload": "config2 n=41157 d=9 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start",
+    n_steps = w_steps + k_steps
+    out = {"workload": workload,
            "sharding": f"rows{ws}", "timing": "host clock per outer step (device synchronised), max over ranks",
-           "steps": max(args.steps, 1), "warmup_steps": args.warmup}
-    for name, sc in {"cg": dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=1000),
-                     "ap": dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=100,
-                                block_size=1000)}.items():
+           "steps": k_steps, "warmup_steps": w_steps}
+    for name, sc in solvers.items():
         cfg = wg.TrainConfig(steps=n_steps, learning_rate=0.1, num_probes=64, mode="warm", seed=0,
                              transform="log", estimator="pathwise", rff_features=1000, init_noise=0.5,
                              init_constrained=1.0, solver=wg.SolverConfig(**sc))
         torch.cuda.synchronize()
         steps = sharded.sharded_train(ops, p.y, cfg)
-        timed = steps[args.warmup:]
+        timed = steps[w_steps:]
         t = torch.tensor([1e3 * float(np.mean([s.step_seconds for s in timed]))], device=f"cuda:{device}")
         if ws > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -90,7 +90,7 @@ struct Ctx {
 
   // workspaces
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
-  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, D32, lapack_work, info;
+  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, lapack_work, info;
   Buf gpart, gout, gtc_ws;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
@@ -546,7 +546,7 @@ struct Ctx {
     const int64_t nb = ap_factor(bs);
     Rb.ensure(sizeof(double) * bs * s);
     D64.ensure(sizeof(double) * bs * s);
-    D32.ensure(sizeof(float) * bs * s);
+    DX.ensure(sizeof(float) * ld * s);
     reset_ctrl(max_ep);
     const ColState cs = colstate();
     SolveCtrl* c = dctrl();
@@ -563,20 +563,25 @@ struct Ctx {
       for (int64_t b = 0; b < nb; ++b) {  // :183-187
         const int64_t start = b * bs, size = std::min(bs, n - start);
         const double* Hinv = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
-        // Left-looking block residual R_b = B_b - H[b, :] X from the current X
-        // (= the reference's incrementally updated R_b in exact arithmetic:
-        // R is exact at the epoch start and every earlier block's update is in
-        // X).  One H.V of `size` rows against all n points splits into long
-        // J ranges; the right-looking R -= H[:, b] delta over n rows with only
-        // `size` contracted points ran ~32 tiles per CTA, dominated by the
-        // per-CTA fixed cost (measured 0.75 s per config-3 epoch).
-        hv(Xo, ld, s, R + start, ld, kHvResidual, B, ld, 0, n, nullptr, start, size, &c->done, false);
+        // Block residual, left-looking over the earlier blocks only: R is the
+        // exact residual at the epoch start (R0), and this epoch changed X
+        // only in blocks < b, by DX = their deltas, so
+        //   R_b = R0_b - H[b, 0:start] DX[0:start]
+        // -- the reference's incrementally updated R_b (R -= H[:, b'] delta
+        // after every block b', :186) computed when it is needed.  Contracting
+        // `size` rows against the `start` earlier points splits into long J
+        // ranges (the right-looking update over n rows with only `size`
+        // contracted points ran ~32 tiles per CTA, dominated by the per-CTA
+        // fixed cost: 0.75 s per config-3 epoch), and the triangle costs
+        // n^2 / 2 entries per epoch where B_b - H[b, :] X cost n^2.
+        if (b > 0) hv(DX.as<float>(), ld, s, R + start, ld, kHvResidual, R, ld, 0, start, nullptr, start, size,
+                      &c->done, false);
         ap_gather(R, ld, start, size, s, Rb.as<double>(), c, st);
         // delta = H_bb^-1 R_b (:185)
         cublasDgemm(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, static_cast<int>(size), &one, Hinv,
                     static_cast<int>(bs), Rb.as<double>(), static_cast<int>(size), &zero, D64.as<double>(),
                     static_cast<int>(size));
-        ap_apply(Xo, ld, start, size, s, D64.as<double>(), D32.as<float>(), c, st);
+        ap_apply(Xo, ld, start, size, s, D64.as<double>(), DX.as<float>(), c, st);
       }
       hv_all(Xo, s, R, kHvResidual, B);                            // :188
       norms_convergence(R, ld, n, s, cs, pt, c, true, true, st);  // :189-191

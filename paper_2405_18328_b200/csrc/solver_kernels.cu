@@ -342,14 +342,14 @@ __global__ void ap_gather_kernel(const float* R, int64_t ld, int64_t start, int6
 }
 
 __global__ void ap_apply_kernel(float* X, int64_t ld, int64_t start, int64_t b, int s,
-                                const double* delta, float* d32, const SolveCtrl* ctrl) {
+                                const double* delta, float* dx, const SolveCtrl* ctrl) {
   if (ctrl->done) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (i >= b) return;
   const double dv = delta[i + c * b];
   X[start + i + c * ld] = static_cast<float>(static_cast<double>(X[start + i + c * ld]) + dv);
-  d32[i + c * b] = static_cast<float>(dv);
+  dx[start + i + c * ld] = static_cast<float>(dv);  // this epoch's change of block b (Delta X)
 }
 
 // H[b, b] (fp64) padded to `full` x `full` with the identity (so a partial last
@@ -520,8 +520,8 @@ void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, doub
 }
 
 void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
-              float* delta32, const SolveCtrl* ctrl, cudaStream_t st) {
-  ap_apply_kernel<<<grid2(b, s), NT, 0, st>>>(X, ld, start, b, s, delta, delta32, ctrl);
+              float* dx, const SolveCtrl* ctrl, cudaStream_t st) {
+  ap_apply_kernel<<<grid2(b, s), NT, 0, st>>>(X, ld, start, b, s, delta, dx, ctrl);
   WGP_LAUNCH_CHECK();
 }
 

@@ -83,8 +83,9 @@ void norms_convergence(const float* R, int64_t ld, int64_t n, int s, ColState cs
 // AP block step helpers.
 void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, double* Rb,
                const SolveCtrl* ctrl, cudaStream_t st);
+// X[start:start+b] += delta, and dx[start:start+b] = delta (fp32, same ld as X).
 void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
-              float* delta32, const SolveCtrl* ctrl, cudaStream_t st);
+              float* dx, const SolveCtrl* ctrl, cudaStream_t st);
 // nb contiguous b x b identity matrices (fp64, column-major).
 void identities(double* A, int64_t b, int64_t nb, cudaStream_t st);
 // H[b, b] in fp64 from the prepared points, padded with the identity to full x full.
