@@ -229,6 +229,14 @@ int wgp_set_split_global(wgp_ctx* ctx, int global);
  *  R_I -= H[I, b] delta_b (proj/src/solvers.cpp:186). */
 int wgp_hv_cols(wgp_ctx* ctx, const float* V, int64_t ldv, int s, int64_t j0, int64_t j1, float* out, int64_t ldo,
                 int mode, const float* B, int64_t ldb);
+/** out = H[i0:i1, j0:j1] V for any block of the full operator (independent of
+ *  wgp_set_rows): V holds rows j0..j1-1 (V[(j - j0) + c ldv]), out rows
+ *  i0..i1-1 (out[(i - i0) + c ldo]); the diagonal term where the ranges
+ *  overlap.  Device pointers; J splits keyed on the block's own rows.  The
+ *  row-sharded AP's block residual R_b = R0_b - sum over ranks of
+ *  H[b, own columns before b] dX (proj/src/solvers.cpp:186 applied lazily). */
+int wgp_hv_block(wgp_ctx* ctx, int64_t i0, int64_t i1, int64_t j0, int64_t j1, const float* V, int64_t ldv, int s,
+                 float* out, int64_t ldo);
 /** Factor every diagonal block of size block_size at the current
  *  hyperparameters (proj/src/solvers.cpp:151-165: Cholesky, errors as
  *  ap_solve's) and keep the inverses; *nblocks = ceil(n / block_size). */

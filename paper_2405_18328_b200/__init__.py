@@ -88,7 +88,7 @@ EXPORTS = [
     "wgp_set_hv_impl", "wgp_stream", "wgp_set_data", "wgp_set_hyper", "wgp_set_rows", "wgp_hv",
     "wgp_hv_device", "wgp_solve", "wgp_grad", "wgp_sample_probes", "wgp_rff_probes", "wgp_train",
     "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
-    "wgp_exact", "wgp_predict", "wgp_split_order", "wgp_hv_cols", "wgp_ap_factor", "wgp_ap_block_solve",
+    "wgp_exact", "wgp_predict", "wgp_split_order", "wgp_hv_cols", "wgp_hv_block", "wgp_ap_factor", "wgp_ap_block_solve",
     "wgp_set_split_global",
 ]
 
@@ -127,6 +127,8 @@ def load():
     lib.wgp_set_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
     lib.wgp_hv.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.wgp_hv_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64]
+    lib.wgp_hv_block.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                 C.c_int, C.c_void_p, C.c_int64]
     lib.wgp_hv_cols.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int64, C.c_void_p,
                                 C.c_int64, C.c_int, C.c_void_p, C.c_int64]
     lib.wgp_ap_factor.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
@@ -442,6 +444,12 @@ class Context:
     def hv_device(self, V_ptr: int, ldv: int, s: int, out_ptr: int, ldo: int):
         """Device-pointer H V on the context stream (asynchronous)."""
         _check(self._lib.wgp_hv_device(self._h, C.c_void_p(V_ptr), ldv, s, C.c_void_p(out_ptr), ldo))
+
+    def hv_block_device(self, i0: int, i1: int, j0: int, j1: int, V_ptr: int, ldv: int, s: int, out_ptr: int,
+                        ldo: int) -> None:
+        """out = H[i0:i1, j0:j1] V (wgp_hv_block; device pointers, column-major,
+        V rows j0.., out rows i0..)."""
+        _check(self._lib.wgp_hv_block(self._h, i0, i1, j0, j1, C.c_void_p(V_ptr), ldv, s, C.c_void_p(out_ptr), ldo))
 
     def hv_cols_device(self, V_ptr: int, ldv: int, s: int, j0: int, j1: int, out_ptr: int, ldo: int,
                        mode: int = 0, B_ptr: int = 0, ldb: int = 0):

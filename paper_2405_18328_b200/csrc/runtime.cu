@@ -1365,6 +1365,20 @@ int wgp_hv_cols(wgp_ctx* ctx, const float* V, int64_t ldv, int s, int64_t j0, in
   });
 }
 
+int wgp_hv_block(wgp_ctx* ctx, int64_t i0, int64_t i1, int64_t j0, int64_t j1, const float* V, int64_t ldv, int s,
+                 float* out, int64_t ldo) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    c.require_data();
+    if (s < 1) throw std::invalid_argument("wgp_hv_block: s must be >= 1");
+    if (i0 < 0 || i1 > c.n || i1 <= i0 || j0 < 0 || j1 > c.n || j1 <= j0)
+      throw std::invalid_argument("wgp_hv_block: bad row or column range");
+    if (ldv < j1 - j0 || ldo < i1 - i0) throw std::invalid_argument("wgp_hv_block: leading dimension too small");
+    // the kernels index V by global point
+    c.hv(V - j0, ldv, s, out, ldo, wgp::kHvStore, nullptr, 0, j0, j1, nullptr, i0, i1 - i0, nullptr, false);
+  });
+}
+
 int wgp_ap_factor(wgp_ctx* ctx, int block_size, int64_t* nblocks) {
   return guarded([&] {
     wgp::Ctx& c = ctx->c;

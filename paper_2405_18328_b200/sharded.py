@@ -149,21 +149,15 @@ class ApOps:
     """Local operators of the row-sharded AP for this rank's rows I = [r0, r1).
 
     rows_residual(B_local, X_full)   -> B_local - H[I, :] X_full
-    cols_subtract(R_local, delta, j0, j1) -> R_local - H[I, j0:j1] delta
+    block_rows(i0, i1, c0, c1, V)    -> H[i0:i1, c0:c1] V   (V: (c1 - c0) x s rows of
+                                        this rank's columns, c0 >= r0, c1 <= r1)
     factor(block_size)               -> number of blocks (factors kept)
     block_solve(b, R_b)              -> H_bb^-1 R_b   (fp64, size x s)
     """
     rows_residual: Callable
-    cols_subtract: Callable
+    block_rows: Callable
     factor: Callable
     block_solve: Callable
-
-
-def _allreduce_exact(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """Sum of disjoint contributions (every element nonzero on at most one rank): exact."""
-    if world > 1:
-        dist.all_reduce(x, group=group)
-    return x
 
 
 def sharded_ap(ops: ApOps, B_local: torch.Tensor, n: int, r0: int, r1: int, block_size: int = 2000,
@@ -172,12 +166,19 @@ def sharded_ap(ops: ApOps, B_local: torch.Tensor, n: int, r0: int, r1: int, bloc
     """ap_solve (proj/src/solvers.cpp:141-196) over row shards.
 
     Blocks of `block_size` consecutive points in fixed order (they may straddle
-    ranks).  Per block: R_b from the ranks' overlapping rows (one all-reduce of
-    disjoint b x s contributions, exact), delta_b = H_bb^-1 R_b on every rank
-    (identical inputs, identical result), own rows of X += delta_b, own rows of
-    R -= H[I, b] delta_b (the reference's right-looking update, :186).  Each
-    epoch ends with the exact refresh R = B - H X from the all-gathered X
-    (:188) and the per-column norms summed in rank order (:189-191)."""
+    ranks).  R holds the exact residual R0 of the epoch start and dX this
+    epoch's deltas of the own rows; the reference's incrementally updated
+    R_b (R -= H[:, b'] delta_b' after every block b', :186) is formed when
+    block b needs it:
+        R_b = R0_b - sum over ranks of H[b, own columns before b] dX
+    (each rank's contraction over its own columns < j0 plus R0 of its own
+    rows of b; the partials summed in rank order, one b x s exchange per
+    block).  delta_b = H_bb^-1 R_b on every rank (identical inputs, identical
+    result); own rows of X += delta_b.  The triangle costs n^2 / 2 entries
+    per epoch over all ranks, with long contractions instead of the
+    right-looking update's n x b ones.  Each epoch ends with the exact
+    refresh R = B - H X from the all-gathered X (:188) and the per-column
+    norms summed in rank order (:189-191)."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     s = B_local.shape[1]
     dt = B_local.dtype
@@ -188,6 +189,9 @@ def sharded_ap(ops: ApOps, B_local: torch.Tensor, n: int, r0: int, r1: int, bloc
     bn = torch.sqrt(_sum_ranks((B_local.double() ** 2).sum(0), world, group))
     tols = torch.tensor([tol_mean] + [tol_samples] * (s - 1), dtype=torch.float64, device=bn.device)
     R = ops.rows_residual(B_local, _gather_rows(X, n, world, group))
+    # this epoch's deltas of the own rows, column-major (a row slice is one
+    # strided device operand)
+    dX = torch.zeros((s, r1 - r0), dtype=dt, device=B_local.device).t()
 
     def converged(R):
         rs = _sum_ranks((R.double() ** 2).sum(0), world, group)
@@ -203,11 +207,14 @@ def sharded_ap(ops: ApOps, B_local: torch.Tensor, n: int, r0: int, r1: int, bloc
             Rb = torch.zeros((j1 - j0, s), dtype=torch.float64, device=B_local.device)
             if o0 < o1:
                 Rb[o0 - j0:o1 - j0] = R[o0 - r0:o1 - r0].double()
-            Rb = _allreduce_exact(Rb, world, group)
+            c1 = min(r1, j0)  # own columns of the earlier blocks
+            if c1 > r0:
+                Rb -= ops.block_rows(j0, j1, r0, c1, dX[:c1 - r0]).double()
+            Rb = _sum_ranks(Rb, world, group)
             delta = ops.block_solve(b, Rb)
             if o0 < o1:
                 X[o0 - r0:o1 - r0] += delta[o0 - j0:o1 - j0].to(dt)
-            R = ops.cols_subtract(R, delta, j0, j1)
+                dX[o0 - r0:o1 - r0] = delta[o0 - j0:o1 - j0].to(dt)
         R = ops.rows_residual(B_local, _gather_rows(X, n, world, group))
         rs, conv = converged(R)
         if not bool(torch.isfinite(rs).all()):
@@ -240,11 +247,14 @@ def device_ap_ops(ctx, r0: int, r1: int) -> ApOps:
                                           Bt.data_ptr(), m))
         return out.t()
 
-    def cols_subtract(R_local, delta, j0, j1):
-        Rt = R_local.t().contiguous()
-        Dt = delta.to(R_local.dtype).t().contiguous()  # [s][size]
-        on_ctx(lambda: ctx.hv_cols_device(Dt.data_ptr(), j1 - j0, Dt.shape[0], j0, j1, Rt.data_ptr(), m, 2))
-        return Rt.t()
+    def block_rows(i0, i1, c0, c1, V):
+        # V: (c1 - c0) x s, column-major (a row slice of sharded_ap's dX) or copied to it
+        if V.stride(0) != 1:
+            V = V.t().contiguous().t()
+        out = torch.empty((V.shape[1], i1 - i0), dtype=V.dtype, device=V.device)  # [s][size]
+        on_ctx(lambda: ctx.hv_block_device(i0, i1, c0, c1, V.data_ptr(), V.stride(1), V.shape[1], out.data_ptr(),
+                                           i1 - i0))
+        return out.t()
 
     def block_solve(b, Rb):
         Rt = Rb.t().contiguous()                      # [s][size] fp64
@@ -252,7 +262,7 @@ def device_ap_ops(ctx, r0: int, r1: int) -> ApOps:
         on_ctx(lambda: ctx.ap_block_solve_device(b, Rt.data_ptr(), Rt.shape[0], Dt.data_ptr()))
         return Dt.t()
 
-    return ApOps(rows_residual, cols_subtract, lambda bs: ctx.ap_factor(bs), block_solve)
+    return ApOps(rows_residual, block_rows, lambda bs: ctx.ap_factor(bs), block_solve)
 
 
 # ------------------------------------------------------------------ gradient

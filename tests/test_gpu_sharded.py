@@ -50,9 +50,33 @@ def test_hv_cols_matches_dense_oracle(mode):
     ctx.close()
 
 
+@pytest.mark.parametrize("rows,cols", [((300, 700), (0, 300)), ((128, 512), (100, 450)), ((0, 640), (500, 640))])
+def test_hv_block_matches_dense_oracle(rows, cols):
+    """wgp_hv_block: any block H[i0:i1, j0:j1] V of the full operator, with
+    the diagonal term where the ranges overlap, independent of set_rows."""
+    X, ls, sf, sig, B = problem()
+    s = B.shape[1]
+    H = orc.kernel_matrices(X.astype(np.float64), ls, sf, sig)[0]
+    ctx = wg.Context(0)
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, sf, sig])
+    ctx.set_rows(64, 200)  # must not matter
+    (i0, i1), (j0, j1) = rows, cols
+    Vb = np.random.default_rng(2).standard_normal((j1 - j0, s)).astype(np.float32)
+    Vt = torch.from_numpy(np.ascontiguousarray(Vb.T)).cuda()
+    Ot = torch.empty((s, i1 - i0), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ctx.hv_block_device(i0, i1, j0, j1, Vt.data_ptr(), j1 - j0, s, Ot.data_ptr(), i1 - i0)
+    torch.cuda.synchronize()
+    ref = H[i0:i1, j0:j1] @ Vb.astype(np.float64)
+    assert np.linalg.norm(Ot.cpu().numpy().T - ref) / np.linalg.norm(ref) <= 1e-5
+    ctx.close()
+
+
 def test_sharded_ap_on_device_matches_oracle():
-    """sharded_ap with the device ops (world 1): the reference's right-looking
-    AP in fp32 storage with fp64 block solves; epochs within 10% of the fp64
+    """sharded_ap with the device ops (world 1): the reference's AP (block
+    residuals formed lazily from the epoch-start residual) in fp32 storage
+    with fp64 block solves; epochs within 10% of the fp64
     oracle's and the exact residual at the tolerance."""
     # config-0-like conditioning (d = 8, sigma 0.5), as the solver parity tests:
     # fp32 residual floors stay well below the tolerance

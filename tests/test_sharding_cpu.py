@@ -103,7 +103,7 @@ def host_ap_ops(H, r0, r1):
             chol[b] = torch.linalg.cholesky(Ht[j0:j1, j0:j1])
         return nb
 
-    return sharded.ApOps(lambda B, X: B - HI @ X, lambda R, d, j0, j1: R - HI[:, j0:j1] @ d, factor,
+    return sharded.ApOps(lambda B, X: B - HI @ X, lambda i0, i1, c0, c1, V: Ht[i0:i1, c0:c1] @ V, factor,
                          lambda b, Rb: torch.cholesky_solve(Rb, chol[b]))
 
 
@@ -199,7 +199,7 @@ def host_train_ops(X, r0, r1):
     def ap_ops():
         ops = host_ap_ops(state["H"], r0, r1)
         return sharded.ApOps(lambda B, Xf: (B.double() - torch.from_numpy(state["H"][r0:r1]) @ Xf.double()).to(B.dtype),
-                             lambda R, dl, j0, j1: (R.double() - torch.from_numpy(state["H"][r0:r1, j0:j1]) @ dl).to(R.dtype),
+                             lambda i0, i1, c0, c1, V: (torch.from_numpy(state["H"][i0:i1, c0:c1]) @ V.double()).to(V.dtype),
                              ops.factor, ops.block_solve)
 
     def grad(T, raw, vy, L, R, coef):
