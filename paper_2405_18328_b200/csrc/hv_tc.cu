@@ -237,7 +237,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sVd = reinterpret_cast<float*>(sV + static_cast<size_t>(p.nv) * p.vstage_bytes);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rt = blockIdx.x / p.splits, sp = blockIdx.x % p.splits;
+  // split-major grid: the CTAs running together share one J range (split),
+  // which stays L2-resident while all row tiles pass over it
+  const int row_tiles = static_cast<int>(gridDim.x) / p.splits;
+  const int rt = blockIdx.x % row_tiles, sp = blockIdx.x / row_tiles;
   const int jt_begin = static_cast<int>(static_cast<int64_t>(p.num_jt) * sp / p.splits);
   const int jt_end = static_cast<int>(static_cast<int64_t>(p.num_jt) * (sp + 1) / p.splits);
   const int T = jt_end - jt_begin;
@@ -878,12 +881,14 @@ CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t 
 // J-split count: waves x (tiles per CTA + a fixed per-CTA cost of ~16 tile
 // times for the pipeline fill, the final drain and the CTA turnover,
 // measured), plus the split-reduction pass.
-int choose_splits(int64_t row_tiles, int jt, int sms) {
+// min_sp: the smallest split count whose J range fits the L2 budget (below).
+int choose_splits(int64_t row_tiles, int jt, int sms, int min_sp = 1) {
   constexpr double kCtaOverheadTiles = 16.0;
   int best = 1;
   double best_cost = 1e300;
   for (int sp = 1; sp <= 64; ++sp) {
     if (sp > 1 && jt / sp < 8) break;
+    if (sp < min_sp) continue;
     const double waves = std::ceil(static_cast<double>(row_tiles * sp) / sms);
     const double cost = waves * (std::ceil(static_cast<double>(jt) / sp) + kCtaOverheadTiles) +
                         (sp > 1 ? 4.0 + 0.5 * sp : 0.0);
@@ -1116,7 +1121,27 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   }
   const int64_t row_tiles = ceil_div(hp.m, kTI);
   const int64_t key_tiles = hp.split_rows > 0 ? ceil_div(hp.split_rows, kTI) : row_tiles;
-  a.splits = choose_splits(key_tiles, a.num_jt, sm_count());
+  // L2 rasterisation: every CTA streams the operand planes of its J range
+  // (B hi / lo + V hi / lo: 256 + 2 esz s_pad bytes per point).  With one
+  // split the concurrently running row tiles drift apart along J over the
+  // waves, and once the planes outgrow L2 they re-read them from HBM
+  // (config 3, n = 391k: 463 GB of DRAM reads per H.V at a 53% L2 hit rate,
+  // ncu).  Splits whose J range fits the budget, with the split-major grid,
+  // keep the range L2-resident across all row tiles; the fp32 partials are
+  // capped at 8 GB.
+  static const double l2_budget = [] {
+    const char* e = getenv("WGP_TC_L2MB");
+    return (e ? atof(e) : 48.0) * 1e6;
+  }();
+  int min_sp = 1;
+  if (l2_budget > 0) {
+    const double plane_bytes = static_cast<double>(nv) * (256.0 + 2.0 * static_cast<double>(esz) * spad);
+    min_sp = static_cast<int>(std::ceil(plane_bytes / l2_budget));
+    // the cap uses the split key's rows, so a row shard picks the full operator's splits
+    const double part_row = 4.0 * spad * static_cast<double>(key_tiles * kTI);
+    min_sp = std::max(1, std::min({min_sp, static_cast<int>(8e9 / part_row), 64}));
+  }
+  a.splits = choose_splits(key_tiles, a.num_jt, sm_count(), min_sp);
   static const int force_splits = [] {
     const char* e = getenv("WGP_TC_SPLITS");
     return e ? atoi(e) : 0;
