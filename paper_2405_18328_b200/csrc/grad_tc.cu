@@ -531,12 +531,15 @@ __global__ void grad_tc_prep_kernel(const float* R, int64_t ld, int s, const flo
   }
 }
 
-int choose_grad_splits(int64_t row_tiles, int jt, int sms) {
+// min_sp: the smallest split count whose J range fits the L2 budget (the
+// grid is split-major, as hv_tc's: see choose_splits there).
+int choose_grad_splits(int64_t row_tiles, int jt, int sms, int min_sp = 1) {
   constexpr double kCtaOverheadTiles = 8.0;
   int best = 1;
   double best_cost = 1e300;
   for (int sp = 1; sp <= 64; ++sp) {
     if (sp > 1 && jt / sp < 8) break;
+    if (sp < min_sp) continue;
     const double waves = std::ceil(static_cast<double>(row_tiles * sp) / sms);
     const double cost = waves * (std::ceil(static_cast<double>(jt) / sp) + kCtaOverheadTiles);
     if (cost < best_cost - 1e-9) {
@@ -591,7 +594,17 @@ GradTcPlan grad_tc_plan(int64_t n, int64_t m, int d, int s) {
     const char* e = getenv("WGP_GRAD_SPLITS");
     return e ? atoi(e) : 0;
   }();
-  pl.splits = force > 0 ? std::min(force, jt) : choose_grad_splits(pl.rt_pad, jt, tc_sm_count());
+  // L2 rasterisation: the R_J / coordinate planes of a split's J range
+  // (4 (2 spk + ep) bytes per point) within a 48 MB budget
+  static const double l2_budget = [] {
+    const char* e = getenv("WGP_TC_L2MB");
+    return (e ? atof(e) : 48.0) * 1e6;
+  }();
+  int min_sp = 1;
+  if (l2_budget > 0)
+    min_sp = std::max(1, std::min(64, static_cast<int>(std::ceil(static_cast<double>(pl.n_pad) * 4.0 *
+                                                                 (2 * pl.spk + pl.ep) / l2_budget))));
+  pl.splits = force > 0 ? std::min(force, jt) : choose_grad_splits(pl.rt_pad, jt, tc_sm_count(), min_sp);
   pl.nblk = static_cast<int>(pl.rt_pad * pl.splits);
   pl.ws_bytes = sizeof(float) * static_cast<size_t>(pl.n_pad) * (2 * pl.spk + pl.ep);
   return pl;
