@@ -1010,6 +1010,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
       q.V = hp.V + c0 * hp.ldv;
       q.out = hp.out + c0 * hp.ldo;
       if (hp.B) q.B = hp.B + c0 * hp.ldb;
+      q.vplanes = nullptr;
       hv_tc(ops, q, st, bf16);
     }
     return;
@@ -1026,10 +1027,16 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   const int TJ = bf16 ? Cfg<true>::kTJ : Cfg<false>::kTJ;
   // hi / lo planes of V[j0:j1]: tf32 (fp32 storage) or bf16 v1 = bf16(v), v2 = bf16(v - v1)
   const size_t esz = bf16 ? 2 : 4;
-  char* vhi = static_cast<char*>(ws_v.ensure(esz * ldw * s * 2));
-  char* vlo = vhi + esz * ldw * s;
+  // caller-maintained planes (16-byte aligned rows for TMA) or this launch's split
+  const bool pre = !bf16 && hp.vplanes && hp.j0 % 4 == 0 && hp.vplanes_ld % 4 == 0 && hp.vplanes_ld >= hp.j1;
+  char* vhi = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0))
+                  : static_cast<char*>(ws_v.ensure(esz * ldw * s * 2));
+  char* vlo = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0 + hp.vplanes_ld * s))
+                  : vhi + esz * ldw * s;
+  const int64_t ldp = pre ? hp.vplanes_ld : ldw;  // plane leading dimension
   const dim3 vgrid(static_cast<unsigned>(ceil_div(nv, 256)), s);
-  if (bf16)
+  if (pre) {
+  } else if (bf16)
     split_v_bf16_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<__nv_bfloat16*>(vhi),
                                                reinterpret_cast<__nv_bfloat16*>(vlo), ldw);
   else
@@ -1058,8 +1065,8 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, 64);
   // one TJ-point x s_pad box per plane (128-byte rows: 32 tf32 / 64 bf16 points)
   const CUtensorMapDataType vt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  const CUtensorMap mVhi = make_map(vhi, nv, s, ldw * esz, TJ, spad, vt);
-  const CUtensorMap mVlo = make_map(vlo, nv, s, ldw * esz, TJ, spad, vt);
+  const CUtensorMap mVhi = make_map(vhi, nv, s, ldp * esz, TJ, spad, vt);
+  const CUtensorMap mVlo = make_map(vlo, nv, s, ldp * esz, TJ, spad, vt);
 
   TcArgs a{};
   a.m = hp.m;

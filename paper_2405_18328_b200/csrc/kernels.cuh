@@ -47,6 +47,9 @@ struct HvParams {
   int64_t split_rows;    // rows that key the J-split decomposition (0: m).  Row shards
                          // pass the global row count so every shard sums in the same
                          // order as the single-GPU launch (bitwise identical rows).
+  const float* vplanes;  // optional caller-maintained tf32 planes of V (hv_tc, s <= 96):
+  int64_t vplanes_ld;    // hi[j + c ld], lo[j + (s + c) ld] for global j, bitwise
+                         // split_v's; the launch then skips its own split of V
 };
 
 // SIMT fp32 fused H.V (direct differences; any d, s <= 128).

@@ -90,7 +90,7 @@ struct Ctx {
 
   // workspaces
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
-  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, lapack_work, info;
+  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, DXP, lapack_work, info;
   Buf gpart, gout, gtc_ws;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
@@ -172,8 +172,11 @@ struct Ctx {
   // ---------------------------------------------------------------- H.V
   void hv(const float* V, int64_t ldv, int s, float* out, int64_t ldo, int mode, const float* B,
           int64_t ldb, int64_t j0, int64_t j1, const int* row_idx, int64_t rr0, int64_t m,
-          const int* done = nullptr, bool shard_invariant = true) {
+          const int* done = nullptr, bool shard_invariant = true, const float* vplanes = nullptr,
+          int64_t vplanes_ld = 0) {
     HvParams p{};
+    p.vplanes = vplanes;
+    p.vplanes_ld = vplanes_ld;
     p.xs = xs.as<float>();
     p.n = n;
     p.dp = dp;
@@ -547,6 +550,7 @@ struct Ctx {
     Rb.ensure(sizeof(double) * bs * s);
     D64.ensure(sizeof(double) * bs * s);
     DX.ensure(sizeof(float) * ld * s);
+    DXP.ensure(sizeof(float) * 2 * ld * s);  // tf32 planes of DX (no per-block re-split)
     reset_ctrl(max_ep);
     const ColState cs = colstate();
     SolveCtrl* c = dctrl();
@@ -575,13 +579,13 @@ struct Ctx {
         // fixed cost: 0.75 s per config-3 epoch), and the triangle costs
         // n^2 / 2 entries per epoch where B_b - H[b, :] X cost n^2.
         if (b > 0) hv(DX.as<float>(), ld, s, R + start, ld, kHvResidual, R, ld, 0, start, nullptr, start, size,
-                      &c->done, false);
+                      &c->done, false, DXP.as<float>(), ld);
         ap_gather(R, ld, start, size, s, Rb.as<double>(), c, st);
         // delta = H_bb^-1 R_b (:185)
         cublasDgemm(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, static_cast<int>(size), &one, Hinv,
                     static_cast<int>(bs), Rb.as<double>(), static_cast<int>(size), &zero, D64.as<double>(),
                     static_cast<int>(size));
-        ap_apply(Xo, ld, start, size, s, D64.as<double>(), DX.as<float>(), c, st);
+        ap_apply(Xo, ld, start, size, s, D64.as<double>(), DX.as<float>(), DXP.as<float>(), c, st);
       }
       hv_all(Xo, s, R, kHvResidual, B);                            // :188
       norms_convergence(R, ld, n, s, cs, pt, c, true, true, st);  // :189-191

@@ -342,14 +342,20 @@ __global__ void ap_gather_kernel(const float* R, int64_t ld, int64_t start, int6
 }
 
 __global__ void ap_apply_kernel(float* X, int64_t ld, int64_t start, int64_t b, int s,
-                                const double* delta, float* dx, const SolveCtrl* ctrl) {
+                                const double* delta, float* dx, float* dxp, const SolveCtrl* ctrl) {
   if (ctrl->done) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (i >= b) return;
   const double dv = delta[i + c * b];
   X[start + i + c * ld] = static_cast<float>(static_cast<double>(X[start + i + c * ld]) + dv);
-  dx[start + i + c * ld] = static_cast<float>(dv);  // this epoch's change of block b (Delta X)
+  const float d32 = static_cast<float>(dv);
+  dx[start + i + c * ld] = d32;  // this epoch's change of block b (Delta X)
+  if (dxp) {  // and its tf32 hi / lo planes (hv_tc's split of V, bitwise)
+    const float hi = __uint_as_float(__float_as_uint(d32) & 0xFFFFE000u);
+    dxp[start + i + c * ld] = hi;
+    dxp[start + i + (s + c) * ld] = d32 - hi;
+  }
 }
 
 // H[b, b] (fp64) padded to `full` x `full` with the identity (so a partial last
@@ -520,8 +526,8 @@ void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, doub
 }
 
 void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
-              float* dx, const SolveCtrl* ctrl, cudaStream_t st) {
-  ap_apply_kernel<<<grid2(b, s), NT, 0, st>>>(X, ld, start, b, s, delta, dx, ctrl);
+              float* dx, float* dxp, const SolveCtrl* ctrl, cudaStream_t st) {
+  ap_apply_kernel<<<grid2(b, s), NT, 0, st>>>(X, ld, start, b, s, delta, dx, dxp, ctrl);
   WGP_LAUNCH_CHECK();
 }
 

@@ -83,9 +83,11 @@ void norms_convergence(const float* R, int64_t ld, int64_t n, int s, ColState cs
 // AP block step helpers.
 void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, double* Rb,
                const SolveCtrl* ctrl, cudaStream_t st);
-// X[start:start+b] += delta, and dx[start:start+b] = delta (fp32, same ld as X).
+// X[start:start+b] += delta, and dx[start:start+b] = delta (fp32, same ld as X);
+// dxp (optional): the tf32 hi / lo planes of dx (hi at dxp[j + c ld], lo at
+// dxp[j + (s + c) ld]), for hv with HvParams::vplanes.
 void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
-              float* dx, const SolveCtrl* ctrl, cudaStream_t st);
+              float* dx, float* dxp, const SolveCtrl* ctrl, cudaStream_t st);
 // nb contiguous b x b identity matrices (fp64, column-major).
 void identities(double* A, int64_t b, int64_t nb, cudaStream_t st);
 // H[b, b] in fp64 from the prepared points, padded with the identity to full x full.
