@@ -1135,7 +1135,8 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   // (config 3, n = 391k: 463 GB of DRAM reads per H.V at a 53% L2 hit rate,
   // ncu).  Splits whose J range fits the budget, with the split-major grid,
   // keep the range L2-resident across all row tiles; the fp32 partials are
-  // capped at 8 GB.
+  // capped at WGP_TC_PART_GB (default 32 GB, keyed like the splits: a row
+  // shard allocates its share).
   static const double l2_budget = [] {
     const char* e = getenv("WGP_TC_L2MB");
     return (e ? atof(e) : 48.0) * 1e6;
@@ -1146,7 +1147,11 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
     min_sp = static_cast<int>(std::ceil(plane_bytes / l2_budget));
     // the cap uses the split key's rows, so a row shard picks the full operator's splits
     const double part_row = 4.0 * spad * static_cast<double>(key_tiles * kTI);
-    min_sp = std::max(1, std::min({min_sp, static_cast<int>(8e9 / part_row), 64}));
+    static const double part_cap = [] {
+      const char* e = getenv("WGP_TC_PART_GB");
+      return (e ? atof(e) : 32.0) * 1e9;
+    }();
+    min_sp = std::max(1, std::min({min_sp, static_cast<int>(part_cap / part_row), 64}));
   }
   a.splits = choose_splits(key_tiles, a.num_jt, sm_count(), min_sp);
   static const int force_splits = [] {
