@@ -90,7 +90,7 @@ struct Ctx {
 
   // workspaces
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
-  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, DXP, lapack_work, info;
+  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, DXP, XP, lapack_work, info;
   Buf gpart, gout, gtc_ws;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
@@ -232,7 +232,7 @@ struct Ctx {
     best.ensure(sizeof(double) * (s + 1));
     stall.ensure(sizeof(int) * (s + 1));
     act.ensure(sizeof(int) * (s + 1));
-    part.ensure(sizeof(double) * static_cast<size_t>(reduce_blocks(n)) * (s + 2));
+    part.ensure(sizeof(double) * static_cast<size_t>(reduce_blocks(n)) * std::max(s + 2, 2 * s));
     P.ensure(sizeof(float) * ld * s);
     HP.ensure(sizeof(float) * ld * s);
     Rtmp.ensure(sizeof(float) * ld * s);
@@ -597,6 +597,10 @@ struct Ctx {
     const int max_steps = cfg.max_iterations > 0 ? cfg.max_iterations : static_cast<int>((100 * n) / m);
     vel.ensure(sizeof(float) * ld * s);
     fill_zero(vel.as<float>(), ld, n, s, st);
+    // X's tf32 planes, kept current by sgd_scatter: the minibatch H.V then
+    // skips re-splitting all of X every step (10 us per config-2 step)
+    XP.ensure(sizeof(float) * 2 * ld * s);
+    tf32_planes(Xo, ld, n, s, XP.as<float>(), st);
     batch.ensure(sizeof(float) * m * s);
     constexpr int K = 8;  // steps per host round trip
     idx.ensure(sizeof(int) * m * K);
@@ -629,9 +633,10 @@ struct Ctx {
       for (int k = 0; k < K; ++k) {
         const int* ik = idx.as<int>() + static_cast<size_t>(k) * m;
         // batch = B[I] - H[I, :] X  (:241-243)
-        hv(Xo, ld, s, batch.as<float>(), m, kHvResidual, B, ld, 0, n, ik, 0, m, &c->done);
+        hv(Xo, ld, s, batch.as<float>(), m, kHvResidual, B, ld, 0, n, ik, 0, m, &c->done, true, XP.as<float>(),
+           ld);
         sgd_scatter(Xo, R, vel.as<float>(), ld, ik, m, s, batch.as<float>(),
-                    static_cast<float>(cfg.momentum), gs, ss, c, st);
+                    static_cast<float>(cfg.momentum), gs, ss, XP.as<float>(), c, st);
         sgd_check(Xo, R, ld, n, s, cs, pt, c, st);
       }
     }

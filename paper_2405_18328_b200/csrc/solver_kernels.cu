@@ -30,6 +30,8 @@ __device__ __forceinline__ void deposit(Red& red, int c, double v) {
 // identical to the one-dimensional grid.
 __device__ __forceinline__ bool my_col(int c) { return ((c >> 2) % gridDim.y) == blockIdx.y; }
 
+__device__ void block_totals(const double* part, int w, double* tot);
+
 __device__ bool publish(Red& red, int s, double* part, SolveCtrl* ctrl) {
   __syncthreads();
   for (int c = threadIdx.x; c < s; c += blockDim.x) {
@@ -44,20 +46,30 @@ __device__ bool publish(Red& red, int s, double* part, SolveCtrl* ctrl) {
   __syncthreads();
   if (!last) return false;
   __threadfence();
+  block_totals(part, s, red.v[0]);  // red's deposits are in part: reuse it
   return true;
 }
 
-// Column total over the CTAs' partials: four interleaved fixed-order
-// accumulators (independent loads in flight), combined in fixed order.
-__device__ __forceinline__ double total_of(const double* part, int c, int s) {
-  double t[4] = {0.0, 0.0, 0.0, 0.0};
-  unsigned b = 0;
-  for (; b + 4 <= gridDim.x; b += 4) {
+// All column totals at once in the last CTA: warp w takes columns w, w + 8,
+// ...; its lanes stride over the CTAs' partials and a fixed shuffle tree
+// combines them (fixed order: deterministic).  A thread per column walking
+// ~160 partials was a chain of L2 round trips (~25 us per reduction kernel,
+// 65 us for sgd_check's two, config 2).
+__device__ void block_totals(const double* part, int w, double* tot) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned nb = gridDim.x;
+  for (int c = warp; c < w; c += NT / 32) {
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+    unsigned b = lane;
+    for (; b + 96 < nb; b += 128) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) t[u] += __ldcg(part + static_cast<int64_t>(b + u) * s + c);
+      for (int u = 0; u < 4; ++u) t[u] += __ldcg(part + static_cast<int64_t>(b + 32 * u) * w + c);
+    }
+    for (; b < nb; b += 32) t[0] += __ldcg(part + static_cast<int64_t>(b) * w + c);
+    const double v = warp_sum((t[0] + t[1]) + (t[2] + t[3]));
+    if (lane == 0) tot[c] = v;
   }
-  for (; b < gridDim.x; ++b) t[0] += __ldcg(part + static_cast<int64_t>(b) * s + c);
-  return (t[0] + t[1]) + (t[2] + t[3]);
+  __syncthreads();
 }
 
 // Per-column partials of the CTA's rows, four columns at a time with the row
@@ -123,7 +135,8 @@ __global__ void col_dots_kernel(const float* A, const float* B, int64_t ld, int6
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int c = threadIdx.x; c < s; c += NT) out[c] = total_of(part, c, s);
+  block_totals(part, s, red.v[0]);
+  for (int c = threadIdx.x; c < s; c += NT) out[c] = red.v[0][c];
   if (threadIdx.x == 0) *ticket = 0;
 }
 
@@ -137,7 +150,7 @@ __global__ void cg_init_kernel(float* P, const float* R, int64_t ld, int64_t n, 
   });
   if (!publish(red, s, part, ctrl)) return;
   for (int c = threadIdx.x; c < s; c += NT) {
-    const double rs = total_of(part, c, s);
+    const double rs = red.v[0][c];
     cs.rs[c] = rs;
     const bool conv = cs.bnorm[c] == 0.0 || sqrt(rs) <= cs.tol[c] * cs.bnorm[c];
     cs.conv[c] = conv ? 1 : 0;
@@ -168,7 +181,7 @@ __global__ void cg_alpha_kernel(const float* P, const float* HP, int64_t ld, int
   if (!publish(red, s, part, ctrl)) return;
   for (int c = threadIdx.x; c < s; c += NT) {
     if (cs.conv[c]) continue;
-    const double pHp = total_of(part, c, s);
+    const double pHp = red.v[0][c];
     if (!(pHp > 0.0)) {
       atomicCAS(&ctrl->status, kStatusOk, kStatusNotPd);
       ctrl->fail_it = ctrl->it;
@@ -189,10 +202,10 @@ __global__ void cg_alpha_kernel(const float* P, const float* HP, int64_t ld, int
 // inflated beta derails the iteration (measured: residuals 1e17 at tol 1e-6).
 // So when the replaced residual exceeds 4x the previous one, the direction
 // restarts (beta = 0); at reachable tolerances this does not trigger.
-__device__ void beta_epilogue(int s, ColState cs, const double* part, SolveCtrl* ctrl, bool restart = false) {
+__device__ void beta_epilogue(int s, ColState cs, const double* tot, SolveCtrl* ctrl, bool restart = false) {
   for (int c = threadIdx.x; c < s; c += NT) {
     if (cs.conv[c]) continue;
-    const double rs_new = total_of(part, c, s);
+    const double rs_new = tot[c];
     if (!isfinite(rs_new)) {
       atomicCAS(&ctrl->status, kStatusOk, kStatusNaN);
       ctrl->fail_it = ctrl->it;
@@ -241,7 +254,7 @@ __global__ void cg_update_kernel(float* X, float* R, const float* P, const float
   });
   if (refresh) return;
   if (!publish(red, s, part, ctrl)) return;
-  beta_epilogue(s, cs, part, ctrl);
+  beta_epilogue(s, cs, red.v[0], ctrl);
 }
 
 __global__ void cg_refresh_norm_kernel(float* R, const float* Rtmp, int64_t ld, int64_t n, int s,
@@ -256,7 +269,7 @@ __global__ void cg_refresh_norm_kernel(float* R, const float* Rtmp, int64_t ld, 
     return static_cast<double>(r) * r;
   });
   if (!publish(red, s, part, ctrl)) return;
-  beta_epilogue(s, cs, part, ctrl, true);
+  beta_epilogue(s, cs, red.v[0], ctrl, true);
 }
 
 __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
@@ -322,7 +335,7 @@ __global__ void norms_convergence_kernel(const float* R, int64_t ld, int64_t n, 
   });
   if (!publish(red, s, part, ctrl)) return;
   for (int c = threadIdx.x; c < s; c += NT) {
-    const double t = total_of(part, c, s);
+    const double t = red.v[0][c];
     if (check_nan && !isfinite(t)) {
       atomicCAS(&ctrl->status, kStatusOk, kStatusNaN);
       ctrl->fail_it = ctrl->it;
@@ -392,7 +405,7 @@ __global__ void identity_kernel(double* A, int64_t b, int64_t total) {
 
 __global__ void sgd_scatter_kernel(float* X, float* R, float* vel, int64_t ld, const int* idx,
                                    int64_t m, int s, const float* batch, float mu, float gs,
-                                   float ss, const SolveCtrl* ctrl) {
+                                   float ss, float* xp, const SolveCtrl* ctrl) {
   if (ctrl->done) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
@@ -402,8 +415,25 @@ __global__ void sgd_scatter_kernel(float* X, float* R, float* vel, int64_t ld, c
   const float br = batch[i + c * m];
   const float v = mu * vel[e] - gs * br;
   vel[e] = v;
-  X[e] -= ss * v;
+  const float x = X[e] - ss * v;
+  X[e] = x;
   R[e] = br;
+  if (xp) {  // X's tf32 hi / lo planes (hv's split of V, bitwise) follow the update
+    const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    xp[e] = hi;
+    xp[e + static_cast<int64_t>(s) * ld] = x - hi;
+  }
+}
+
+__global__ void tf32_planes_kernel(const float* X, int64_t ld, int64_t n, int s, float* xp) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (i >= n) return;
+  const int64_t e = i + c * ld;
+  const float x = X[e];
+  const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  xp[e] = hi;
+  xp[e + static_cast<int64_t>(s) * ld] = x - hi;
 }
 
 __global__ void sgd_check_kernel(const float* X, const float* R, int64_t ld, int64_t n, int s,
@@ -411,22 +441,41 @@ __global__ void sgd_check_kernel(const float* X, const float* R, int64_t ld, int
   if (ctrl->done) return;
   __shared__ Red red;
   ROWS_OF_BLOCK
-  // columns 0..s-1: ||R_c||^2 ; column s: ||X||_F^2 (part has s+1 columns)
-  double xs = 0.0;
-  cols4(s, rb, re, ld, red, [&](int, int64_t e) {
-    const double r = R[e];
-    const double x = X[e];
-    xs += x * x;
-    return r * r;
-  });
-  deposit(red, s, xs);
-  if (!publish(red, s + 1, part, ctrl)) return;
+  // 2s virtual columns: c < s ||R_c||^2, s + c ||X_c||^2 (summed to ||X||_F^2
+  // in fixed order), so the column groups of the 2D grid each publish their
+  // own share (a per-CTA X sum deposited once ran 65 us per step in a 1D
+  // grid of ~160 CTAs walking all columns, config 2)
+  // (1D grid -- enough row blocks, or s >= SMAX / 2: s + 1 columns,
+  // ||X||_F^2 per CTA in column s)
+  const bool split_x = gridDim.y > 1;
+  const int w = split_x ? 2 * s : s + 1;
+  if (split_x) {
+    cols4(2 * s, rb, re, ld, red, [&](int c, int64_t e) {
+      const double v = c < s ? static_cast<double>(R[e]) : static_cast<double>(X[e - static_cast<int64_t>(s) * ld]);
+      return v * v;
+    });
+  } else {
+    double xs = 0.0;
+    cols4(s, rb, re, ld, red, [&](int, int64_t e) {
+      const double r = R[e];
+      const double x = X[e];
+      xs += x * x;
+      return r * r;
+    });
+    deposit(red, s, xs);
+  }
+  if (!publish(red, w, part, ctrl)) return;
   for (int c = threadIdx.x; c < s; c += NT) {
-    const double t = total_of(part, c, s + 1);
+    const double t = red.v[0][c];
     cs.conv[c] = (cs.bnorm[c] == 0.0 || sqrt(t) <= cs.tol[c] * cs.bnorm[c]) ? 1 : 0;
   }
   if (threadIdx.x == 0) {
-    const double xn = sqrt(total_of(part, s, s + 1));
+    double x2 = 0.0;
+    if (split_x)
+      for (int c = 0; c < s; ++c) x2 += red.v[0][s + c];
+    else
+      x2 = red.v[0][s];
+    const double xn = sqrt(x2);
     if (!isfinite(xn) || xn > 1e12) {
       ctrl->status = kStatusDiverged;
       ctrl->fail_it = ctrl->it;
@@ -545,17 +594,25 @@ void build_block(const float* xs, int dp, int64_t start, int64_t b, int64_t full
 }
 
 void sgd_scatter(float* X, float* R, float* vel, int64_t ld, const int* idx, int64_t m, int s,
-                 const float* batch, float momentum, float grad_scale, float step_scale,
+                 const float* batch, float momentum, float grad_scale, float step_scale, float* xp,
                  const SolveCtrl* ctrl, cudaStream_t st) {
   sgd_scatter_kernel<<<grid2(m, s), NT, 0, st>>>(X, R, vel, ld, idx, m, s, batch, momentum,
-                                                 grad_scale, step_scale, ctrl);
+                                                 grad_scale, step_scale, xp, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void tf32_planes(const float* X, int64_t ld, int64_t n, int s, float* xp, cudaStream_t st) {
+  tf32_planes_kernel<<<grid2(n, s), NT, 0, st>>>(X, ld, n, s, xp);
   WGP_LAUNCH_CHECK();
 }
 
 void sgd_check(const float* X, const float* R, int64_t ld, int64_t n, int s, ColState cs,
                double* part, SolveCtrl* ctrl, cudaStream_t st) {
   check_s(s + 1);
-  sgd_check_kernel<<<reduce_blocks(n), NT, 0, st>>>(X, R, ld, n, s, cs, part, ctrl);
+  // part holds reduce_blocks(n) x max(s + 2, 2 s) doubles (Ctx::ensure_solver_ws)
+  const int rb = reduce_blocks(n);
+  const dim3 grid = (rb < 148 && 2 * s < SMAX) ? cgrid(n, 2 * s) : dim3(static_cast<unsigned>(rb));
+  sgd_check_kernel<<<grid, NT, 0, st>>>(X, R, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
 }
 

@@ -96,9 +96,13 @@ void build_block(const float* xs, int dp, int64_t start, int64_t b, int64_t full
 
 // SGD: vel/X/R row scatter (proj/src/solvers.cpp:247-252) then divergence and
 // convergence on the stored residual estimate (:254-258).
+// xp (optional): X's tf32 hi / lo planes (tf32_planes layout), updated with X.
 void sgd_scatter(float* X, float* R, float* vel, int64_t ld, const int* idx, int64_t m, int s,
-                 const float* batch, float momentum, float grad_scale, float step_scale,
+                 const float* batch, float momentum, float grad_scale, float step_scale, float* xp,
                  const SolveCtrl* ctrl, cudaStream_t st);
+// xp[j + c ld] = tf32 hi of X[j + c ld], xp[j + (s + c) ld] = the lo part
+// (bitwise hv_tc's split of V; for HvParams::vplanes).
+void tf32_planes(const float* X, int64_t ld, int64_t n, int s, float* xp, cudaStream_t st);
 void sgd_check(const float* X, const float* R, int64_t ld, int64_t n, int s, ColState cs,
                double* part, SolveCtrl* ctrl, cudaStream_t st);
 
