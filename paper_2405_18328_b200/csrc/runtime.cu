@@ -96,6 +96,7 @@ struct Ctx {
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
   Buf hx, hx_ws, exv;  // exact path: dense H (fp64), cuSOLVER workspace, vectors
   Buf io_in, io_out;  // staging for the host-pointer entry points
+  Buf cublas_ws;  // explicit cuBLAS workspace: no allocation inside a captured AP epoch
   PinnedCtrl hctrl;
 
   ~Ctx() {
@@ -272,6 +273,9 @@ struct Ctx {
     if (!cublas) {
       if (cublasCreate(&cublas) != CUBLAS_STATUS_SUCCESS) throw DeviceError("cublasCreate failed");
       cublasSetStream(cublas, st);
+      constexpr size_t kWs = size_t(32) << 20;
+      cublas_ws.ensure(kWs);
+      cublasSetWorkspace(cublas, cublas_ws.p, kWs);
     }
     if (!cusolver) {
       if (cusolverDnCreate(&cusolver) != CUSOLVER_STATUS_SUCCESS) throw DeviceError("cusolverDnCreate failed");
@@ -370,11 +374,28 @@ struct Ctx {
     cudaGraphExec_t exec[2];
   };
   std::vector<CgGraph> cg_graphs;
-  void drop_cg_graphs() {
+  // One AP epoch (every block step + the exact residual + the convergence
+  // check) as a graph, cached like the CG ones and keyed on the block size:
+  // at config 2 an epoch is 42 blocks of ~6 launches each with only a few us
+  // of GPU work per launch.
+  struct ApGraph {
+    const float* B;
+    float* Xo;
+    float* R;
+    int s, impl;
+    int64_t bs;
+    uint64_t gen;
+    cudaGraphExec_t exec;
+  };
+  std::vector<ApGraph> ap_graphs;
+  void drop_cg_graphs() {  // and the AP epoch graphs
     for (auto& g : cg_graphs)
       for (auto e : g.exec)
         if (e) cudaGraphExecDestroy(e);
     cg_graphs.clear();
+    for (auto& g : ap_graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    ap_graphs.clear();
   }
 
   void cg(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {
@@ -557,13 +578,7 @@ struct Ctx {
     double* pt = part.as<double>();
     norms_convergence(R, ld, n, s, cs, pt, c, false, true, st);  // :172-178
     const double one = 1.0, zero = 0.0;
-    while (true) {
-      const SolveCtrl& h = poll();
-      if (h.done) {
-        if (h.status != kStatusOk) fail(h, 1);
-        out.iterations = h.it;
-        return;
-      }
+    auto epoch = [&]() {
       for (int64_t b = 0; b < nb; ++b) {  // :183-187
         const int64_t start = b * bs, size = std::min(bs, n - start);
         const double* Hinv = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
@@ -589,7 +604,60 @@ struct Ctx {
       }
       hv_all(Xo, s, R, kHvResidual, B);                            // :188
       norms_convergence(R, ld, n, s, cs, pt, c, true, true, st);  // :189-191
+    };
+    static const bool no_graphs = getenv("WGP_NO_GRAPHS") != nullptr;
+    bool eager_done = false;  // one eager epoch first: every workspace exists before a capture
+    bool tried = false;       // one capture attempt per solve
+    ApGraph* gr = nullptr;
+    while (true) {
+      const SolveCtrl& h = poll();
+      if (h.done) {
+        if (h.status != kStatusOk) fail(h, 1);
+        out.iterations = h.it;
+        return;
+      }
+      if (!gr && !tried && eager_done && !no_graphs && !tc.profiling) {
+        tried = true;
+        gr = ap_graph(B, Xo, R, s, bs, epoch);
+      }
+      if (gr)
+        WGP_CUDA(cudaGraphLaunch(gr->exec, st));
+      else
+        epoch();
+      eager_done = true;
     }
+  }
+  template <class F>
+  ApGraph* ap_graph(const float* B, float* Xo, float* R, int s, int64_t bs, F& epoch) {
+    const uint64_t gen = alloc_generation().load();
+    for (auto& g : ap_graphs)
+      if (g.B == B && g.Xo == Xo && g.R == R && g.s == s && g.impl == hv_impl && g.bs == bs && g.gen == gen) return &g;
+    if (ap_graphs.size() >= 4) {
+      for (auto& g : ap_graphs) cudaGraphExecDestroy(g.exec);
+      ap_graphs.clear();
+    }
+    cudaGraph_t graph = nullptr;
+    WGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    bool ok = true;
+    try {
+      epoch();
+    } catch (...) {
+      ok = false;
+    }
+    const cudaError_t ee = cudaStreamEndCapture(st, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (ok && ee == cudaSuccess && graph && alloc_generation().load() == gen)
+      ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    else
+      ok = false;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {  // eager epochs from here on (capture unsupported for a library call, or a workspace moved)
+      if (exec) cudaGraphExecDestroy(exec);
+      cudaGetLastError();
+      return nullptr;
+    }
+    ap_graphs.push_back(ApGraph{B, Xo, R, s, hv_impl, bs, gen, exec});
+    return &ap_graphs.back();
   }
 
   void sgd(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {

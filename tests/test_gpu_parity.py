@@ -515,6 +515,29 @@ def test_hv_tc_packed_gram_matches_hi_lo_subprocess():
     assert np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[1]) <= 2e-6
 
 
+def test_ap_epoch_graph_matches_eager_subprocess():
+    """The captured AP epoch (Ctx::ap_graph) reproduces the eager epochs
+    bitwise (WGP_NO_GRAPHS=1 is read once per process), including a second
+    solve that replays the cached graph."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    outs = []
+    for extra in ({}, {"WGP_NO_GRAPHS": "1"}):
+        path = os.path.join(root, "gpurun_out", "_apg_%d.npy" % len(outs))
+        env = dict(os.environ, PYTHONPATH=root, **extra)
+        if not extra:
+            env.pop("WGP_NO_GRAPHS", None)
+        r = subprocess.run([sys.executable, os.path.join(root, "scripts", "ap_graph_check.py"), path], env=env,
+                           cwd=root, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, (extra, r.stderr[-2000:])
+        outs.append(np.load(path))
+        os.remove(path)
+    assert np.array_equal(outs[0], outs[1])
+
+
 def test_cg_unreachable_tolerance_stays_bounded(ctx):
     """A tolerance below the fp32 attainable accuracy never converges: every
     column stalls, is restored to its best iterate (exact residual at a
