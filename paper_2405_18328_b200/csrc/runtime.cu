@@ -62,6 +62,30 @@ struct PinnedCtrl {
   }
 };
 
+// Page-locked host staging that grows on demand (async host -> device copies).
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) WGP_CUDA(cudaFreeHost(p));
+    p = nullptr;
+    bytes = 0;
+    WGP_CUDA(cudaMallocHost(&p, b));
+    bytes = b;
+  }
+  template <class T>
+  T* as() {
+    return static_cast<T*>(p);
+  }
+};
+
 const char* solver_name(int kind) { return kind == 0 ? "cg_solve" : kind == 1 ? "ap_solve" : "sgd_solve"; }
 
 }  // namespace
@@ -98,6 +122,7 @@ struct Ctx {
   Buf io_in, io_out;  // staging for the host-pointer entry points
   Buf cublas_ws;  // explicit cuBLAS workspace: no allocation inside a captured AP epoch
   PinnedCtrl hctrl;
+  PinnedBuf sgd_hidx;  // SGD minibatch indices, two rounds (double buffer)
 
   ~Ctx() {
     drop_cg_graphs();
@@ -671,8 +696,10 @@ struct Ctx {
     tf32_planes(Xo, ld, n, s, XP.as<float>(), st);
     batch.ensure(sizeof(float) * m * s);
     constexpr int K = 8;  // steps per host round trip
-    idx.ensure(sizeof(int) * m * K);
-    std::vector<int> hidx(static_cast<size_t>(m) * K);
+    // two rounds of indices: round r + 1 is drawn on the host (pinned) while
+    // the device runs round r, then copied asynchronously
+    idx.ensure(sizeof(int) * m * K * 2);
+    sgd_hidx.ensure(sizeof(int) * m * K * 2);
     reset_ctrl(max_steps);
     const ColState cs = colstate();
     SolveCtrl* c = dctrl();
@@ -683,6 +710,18 @@ struct Ctx {
     std::mt19937_64 rng(cfg.seed);
     const float gs = static_cast<float>(static_cast<double>(n) / static_cast<double>(m));
     const float ss = static_cast<float>(cfg.learning_rate / static_cast<double>(n));
+    // minibatch index stream, partial Fisher-Yates on the persistent pool
+    // (:237-240), in the reference's draw order
+    auto draw = [&](int* hidx) {
+      for (int k = 0; k < K; ++k)
+        for (int64_t i = 0; i < m; ++i) {
+          const int64_t j = i + static_cast<int64_t>(uniform_below(rng, static_cast<uint64_t>(n - i)));
+          std::swap(pool[i], pool[j]);
+          hidx[static_cast<size_t>(k) * m + i] = static_cast<int>(pool[i]);
+        }
+    };
+    int cur = 0;
+    draw(sgd_hidx.as<int>());
     while (true) {
       const SolveCtrl& h = poll();
       if (h.done) {
@@ -690,16 +729,11 @@ struct Ctx {
         out.iterations = h.it;
         return;
       }
-      // minibatch index stream, partial Fisher-Yates on the persistent pool (:237-240)
-      for (int k = 0; k < K; ++k)
-        for (int64_t i = 0; i < m; ++i) {
-          const int64_t j = i + static_cast<int64_t>(uniform_below(rng, static_cast<uint64_t>(n - i)));
-          std::swap(pool[i], pool[j]);
-          hidx[static_cast<size_t>(k) * m + i] = static_cast<int>(pool[i]);
-        }
-      WGP_CUDA(cudaMemcpyAsync(idx.p, hidx.data(), sizeof(int) * m * K, cudaMemcpyHostToDevice, st));
+      const size_t off = static_cast<size_t>(cur) * m * K;
+      WGP_CUDA(cudaMemcpyAsync(idx.as<int>() + off, sgd_hidx.as<int>() + off, sizeof(int) * m * K,
+                               cudaMemcpyHostToDevice, st));
       for (int k = 0; k < K; ++k) {
-        const int* ik = idx.as<int>() + static_cast<size_t>(k) * m;
+        const int* ik = idx.as<int>() + off + static_cast<size_t>(k) * m;
         // batch = B[I] - H[I, :] X  (:241-243)
         hv(Xo, ld, s, batch.as<float>(), m, kHvResidual, B, ld, 0, n, ik, 0, m, &c->done, true, XP.as<float>(),
            ld);
@@ -707,6 +741,10 @@ struct Ctx {
                     static_cast<float>(cfg.momentum), gs, ss, XP.as<float>(), c, st);
         sgd_check(Xo, R, ld, n, s, cs, pt, c, st);
       }
+      // the next round's indices while the device runs this one (its pinned
+      // half was last read by the copy two rounds ago, complete at the poll)
+      cur ^= 1;
+      draw(sgd_hidx.as<int>() + static_cast<size_t>(cur) * m * K);
     }
   }
 

@@ -73,6 +73,23 @@ def test_hv_block_matches_dense_oracle(rows, cols):
     ctx.close()
 
 
+def test_hv_block_rejects_bad_ranges():
+    """wgp_hv_block validates its ranges and leading dimensions like
+    wgp_hv_cols (status 2, std::invalid_argument's text)."""
+    X, ls, sf, sig, B = problem()
+    n = X.shape[0]
+    ctx = wg.Context(0)
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, sf, sig])
+    V = torch.zeros((4, n), device="cuda")
+    out = torch.zeros((4, n), device="cuda")
+    for i0, i1, j0, j1, ldv, ldo in ((0, 0, 0, 10, n, n), (5, 3, 0, 10, n, n), (0, 10, 0, n + 1, n + 1, n),
+                                     (-1, 10, 0, 10, n, n), (0, 10, 0, 10, 5, n), (0, 10, 0, 10, n, 5)):
+        with pytest.raises(ValueError):
+            ctx.hv_block_device(i0, i1, j0, j1, V.data_ptr(), ldv, 4, out.data_ptr(), ldo)
+    ctx.close()
+
+
 def test_sharded_ap_on_device_matches_oracle():
     """sharded_ap with the device ops (world 1): the reference's AP (block
     residuals formed lazily from the epoch-start residual) in fp32 storage
