@@ -594,7 +594,8 @@ struct Ctx {
     const int64_t bs = std::min<int64_t>(std::max(cfg.block_size, 1), n);
     const int64_t nb = ap_factor(bs);
     Rb.ensure(sizeof(double) * bs * s);
-    D64.ensure(sizeof(double) * bs * s);
+    constexpr int kSplitK = 4;  // block solve as 4 K-slices (a 1000 x 65 output is only 64 cuBLAS tiles)
+    D64.ensure(sizeof(double) * bs * s * kSplitK);
     DX.ensure(sizeof(float) * ld * s);
     DXP.ensure(sizeof(float) * 2 * ld * s);  // tf32 planes of DX (no per-block re-split)
     reset_ctrl(max_ep);
@@ -621,11 +622,23 @@ struct Ctx {
         if (b > 0) hv(DX.as<float>(), ld, s, R + start, ld, kHvResidual, R, ld, 0, start, nullptr, start, size,
                       &c->done, false, DXP.as<float>(), ld);
         ap_gather(R, ld, start, size, s, Rb.as<double>(), c, st);
-        // delta = H_bb^-1 R_b (:185)
-        cublasDgemm(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, static_cast<int>(size), &one, Hinv,
-                    static_cast<int>(bs), Rb.as<double>(), static_cast<int>(size), &zero, D64.as<double>(),
-                    static_cast<int>(size));
-        ap_apply(Xo, ld, start, size, s, D64.as<double>(), DX.as<float>(), DXP.as<float>(), c, st);
+        // delta = H_bb^-1 R_b (:185); full blocks as kSplitK K-slices in one
+        // strided-batched DGEMM (partials summed in fixed order by ap_apply):
+        // the single DGEMM ran 64 CTAs over K = 1000, ~16 us per block
+        int kparts = 1;
+        if (size == bs && bs % kSplitK == 0) {
+          const int kc = static_cast<int>(bs / kSplitK);
+          kparts = kSplitK;
+          cublasDgemmStridedBatched(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, kc, &one, Hinv,
+                                    static_cast<int>(bs), static_cast<long long>(kc) * bs, Rb.as<double>(),
+                                    static_cast<int>(size), kc, &zero, D64.as<double>(), static_cast<int>(size),
+                                    static_cast<long long>(size) * s, kSplitK);
+        } else {
+          cublasDgemm(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, static_cast<int>(size), &one, Hinv,
+                      static_cast<int>(bs), Rb.as<double>(), static_cast<int>(size), &zero, D64.as<double>(),
+                      static_cast<int>(size));
+        }
+        ap_apply(Xo, ld, start, size, s, D64.as<double>(), kparts, DX.as<float>(), DXP.as<float>(), c, st);
       }
       hv_all(Xo, s, R, kHvResidual, B);                            // :188
       norms_convergence(R, ld, n, s, cs, pt, c, true, true, st);  // :189-191

@@ -355,12 +355,13 @@ __global__ void ap_gather_kernel(const float* R, int64_t ld, int64_t start, int6
 }
 
 __global__ void ap_apply_kernel(float* X, int64_t ld, int64_t start, int64_t b, int s,
-                                const double* delta, float* dx, float* dxp, const SolveCtrl* ctrl) {
+                                const double* delta, int kparts, float* dx, float* dxp, const SolveCtrl* ctrl) {
   if (ctrl->done) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (i >= b) return;
-  const double dv = delta[i + c * b];
+  double dv = delta[i + c * b];  // split-K partials of the block solve, summed in fixed order
+  for (int k = 1; k < kparts; ++k) dv += delta[static_cast<int64_t>(k) * b * s + i + c * b];
   X[start + i + c * ld] = static_cast<float>(static_cast<double>(X[start + i + c * ld]) + dv);
   const float d32 = static_cast<float>(dv);
   dx[start + i + c * ld] = d32;  // this epoch's change of block b (Delta X)
@@ -574,9 +575,9 @@ void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, doub
   WGP_LAUNCH_CHECK();
 }
 
-void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
+void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta, int kparts,
               float* dx, float* dxp, const SolveCtrl* ctrl, cudaStream_t st) {
-  ap_apply_kernel<<<grid2(b, s), NT, 0, st>>>(X, ld, start, b, s, delta, dx, dxp, ctrl);
+  ap_apply_kernel<<<grid2(b, s), NT, 0, st>>>(X, ld, start, b, s, delta, kparts, dx, dxp, ctrl);
   WGP_LAUNCH_CHECK();
 }
 

@@ -86,7 +86,8 @@ void ap_gather(const float* R, int64_t ld, int64_t start, int64_t b, int s, doub
 // X[start:start+b] += delta, and dx[start:start+b] = delta (fp32, same ld as X);
 // dxp (optional): the tf32 hi / lo planes of dx (hi at dxp[j + c ld], lo at
 // dxp[j + (s + c) ld]), for hv with HvParams::vplanes.
-void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta,
+// delta: kparts partials of b x s (ld b) at stride b s, summed in fixed order.
+void ap_apply(float* X, int64_t ld, int64_t start, int64_t b, int s, const double* delta, int kparts,
               float* dx, float* dxp, const SolveCtrl* ctrl, cudaStream_t st);
 // nb contiguous b x b identity matrices (fp64, column-major).
 void identities(double* A, int64_t b, int64_t nb, cudaStream_t st);
