@@ -1029,8 +1029,10 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   const size_t esz = bf16 ? 2 : 4;
   // caller-maintained planes (16-byte aligned rows for TMA) or this launch's split
   const bool pre = !bf16 && hp.vplanes && hp.j0 % 4 == 0 && hp.vplanes_ld % 4 == 0 && hp.vplanes_ld >= hp.j1;
-  char* vhi = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0))
-                  : static_cast<char*>(ws_v.ensure(esz * ldw * s * 2));
+  // (the split workspace is sized even when unused: a later launch in a CUDA
+  // graph capture, e.g. CG's refresh H.V of X, must not allocate)
+  char* wsv = static_cast<char*>(ws_v.ensure(esz * ldw * s * 2));
+  char* vhi = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0)) : wsv;
   char* vlo = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0 + hp.vplanes_ld * s))
                   : vhi + esz * ldw * s;
   const int64_t ldp = pre ? hp.vplanes_ld : ldw;  // plane leading dimension

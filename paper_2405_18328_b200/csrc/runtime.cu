@@ -114,7 +114,7 @@ struct Ctx {
 
   // workspaces
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
-  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, DXP, XP, lapack_work, info;
+  Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, DXP, XP, PP, lapack_work, info;
   Buf gpart, gout, gtc_ws;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
@@ -237,8 +237,8 @@ struct Ctx {
   }
   // full-operator convenience: out (rows all) = H V
   void hv_all(const float* V, int s, float* out, int mode = kHvStore, const float* B = nullptr,
-              const int* done = nullptr) {
-    hv(V, ld, s, out, ld, mode, B, ld, 0, n, nullptr, 0, n, done);
+              const int* done = nullptr, const float* vplanes = nullptr) {
+    hv(V, ld, s, out, ld, mode, B, ld, 0, n, nullptr, 0, n, done, true, vplanes, vplanes ? ld : 0);
   }
 
   // ---------------------------------------------------------------- workspace
@@ -436,11 +436,13 @@ struct Ctx {
     Rbest.ensure(sizeof(float) * ld * s);
     float* Xb = Xbest.as<float>();
     float* Rb = Rbest.as<float>();
-    cg_init(Pp, R, ld, n, s, cs, pt, c, st);
+    PP.ensure(sizeof(float) * 2 * ld * s);  // P's tf32 planes: the H.V skips its split of P
+    float* PPp = PP.as<float>();
+    cg_init(Pp, R, ld, n, s, cs, pt, c, st, PPp);
     cg_snapshot(Xo, R, Xb, Rb, ld, n, s, cs, c, true, st);
     const int* done = &c->done;
     auto iteration = [&](bool refresh) {
-      hv_all(Pp, s, HPp, kHvStore, nullptr, done);
+      hv_all(Pp, s, HPp, kHvStore, nullptr, done, PPp);
       cg_alpha(Pp, HPp, ld, n, s, cs, pt, c, st);
       if (!refresh) {
         cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, false, st);
@@ -450,7 +452,7 @@ struct Ctx {
         cg_refresh_norm(R, Rt, ld, n, s, cs, pt, c, st);
         cg_snapshot(Xo, R, Xb, Rb, ld, n, s, cs, c, false, st);
       }
-      cg_direction(Pp, R, ld, n, s, cs, pt, c, st);
+      cg_direction(Pp, R, ld, n, s, cs, pt, c, st, PPp);
     };
     static const bool no_graphs = getenv("WGP_NO_GRAPHS") != nullptr;
     constexpr int kChunk = 10;

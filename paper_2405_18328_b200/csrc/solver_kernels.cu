@@ -162,12 +162,22 @@ __global__ void cg_init_kernel(float* P, const float* R, int64_t ld, int64_t n, 
 }
 
 // P = R for active columns, 0 otherwise (separate pass: needs conv flags).
+// P's tf32 hi / lo planes (HvParams::vplanes) written with P, bitwise hv_tc's split.
+__device__ __forceinline__ void put_planes(float* pp, int64_t e, int64_t plane, float v) {
+  if (!pp) return;
+  const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  pp[e] = hi;
+  pp[e + plane] = v - hi;
+}
+
 __global__ void cg_seed_direction_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
-                                         const int* conv) {
+                                         const int* conv, float* pp) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (i >= n) return;
-  P[i + c * ld] = conv[c] ? 0.f : R[i + c * ld];
+  const float v = conv[c] ? 0.f : R[i + c * ld];
+  P[i + c * ld] = v;
+  put_planes(pp, i + c * ld, static_cast<int64_t>(s) * ld, v);
 }
 
 __global__ void cg_alpha_kernel(const float* P, const float* HP, int64_t ld, int64_t n, int s,
@@ -273,7 +283,7 @@ __global__ void cg_refresh_norm_kernel(float* R, const float* Rtmp, int64_t ld, 
 }
 
 __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
-                                    ColState cs, double* part, SolveCtrl* ctrl) {
+                                    ColState cs, double* part, SolveCtrl* ctrl, float* pp) {
   if (ctrl->done) return;
   ROWS_OF_BLOCK
   for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
@@ -284,7 +294,9 @@ __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_
         const int st = cs.conv[c];
         if (st == 1 || st == 3) continue;
         const int64_t e = i + c * ld;
-        P[e] = st == 2 ? 0.f : fmaf(static_cast<float>(cs.beta[c]), P[e], R[e]);
+        const float v = st == 2 ? 0.f : fmaf(static_cast<float>(cs.beta[c]), P[e], R[e]);
+        P[e] = v;
+        put_planes(pp, e, static_cast<int64_t>(s) * ld, v);  // skipped columns keep P and its planes
       }
     }
   }
@@ -528,11 +540,11 @@ void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, doub
 }
 
 void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
-             SolveCtrl* ctrl, cudaStream_t st) {
+             SolveCtrl* ctrl, cudaStream_t st, float* pp) {
   check_s(s);
   cg_init_kernel<<<cgrid(n, s), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
-  cg_seed_direction_kernel<<<grid2(n, s), NT, 0, st>>>(P, R, ld, n, s, cs.conv);
+  cg_seed_direction_kernel<<<grid2(n, s), NT, 0, st>>>(P, R, ld, n, s, cs.conv, pp);
   WGP_LAUNCH_CHECK();
 }
 
@@ -556,8 +568,8 @@ void cg_refresh_norm(float* R, const float* Rtmp, int64_t ld, int64_t n, int s, 
 }
 
 void cg_direction(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs,
-                  double* part, SolveCtrl* ctrl, cudaStream_t st) {
-  cg_direction_kernel<<<cgrid(n, s), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
+                  double* part, SolveCtrl* ctrl, cudaStream_t st, float* pp) {
+  cg_direction_kernel<<<cgrid(n, s), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl, pp);
   WGP_LAUNCH_CHECK();
 }
 

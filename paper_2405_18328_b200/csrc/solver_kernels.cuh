@@ -55,8 +55,10 @@ void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, doub
 
 // CG: before the loop.  R = rhs - H X0 must already be in R; computes
 // rs = ||r||^2, convergence, P = R (active) / 0, and the loop-entry check.
+// pp (optional, here and in cg_direction): P's tf32 planes, written with P
+// (hi at pp[j + c ld], lo at pp[j + (s + c) ld]; for HvParams::vplanes).
 void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
-             SolveCtrl* ctrl, cudaStream_t st);
+             SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
 // alpha_c = rs_c / (p_c . hp_c); non-positive curvature -> kStatusNotPd.
 void cg_alpha(const float* P, const float* HP, int64_t ld, int64_t n, int s, ColState cs,
               double* part, SolveCtrl* ctrl, cudaStream_t st);
@@ -72,7 +74,7 @@ void cg_snapshot(float* X, float* R, float* Xb, float* Rb, int64_t ld, int64_t n
                  const SolveCtrl* ctrl, bool at_start, cudaStream_t st);
 // p = r + beta p (active) / 0 (just converged); then the next-iteration check.
 void cg_direction(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs,
-                  double* part, SolveCtrl* ctrl, cudaStream_t st);
+                  double* part, SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
 
 // Convergence from exact residual norms (AP epochs, SGD init): conv_c =
 // bnorm_c == 0 || ||R_c|| <= tol_c bnorm_c; NaN -> kStatusNaN (when check_nan);
