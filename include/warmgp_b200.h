@@ -51,6 +51,14 @@ typedef struct wgp_ctx wgp_ctx;
 #define WGP_HV_TC 0
 #define WGP_HV_SIMT 1
 #define WGP_HV_TC_BF16 2
+/* Precision of CG's solver state and operator (proj/src/solvers.cpp:81-139):
+ *   WGP_CG_F64  fp64 x / r / p / Hp over the fp64-accumulating symmetric
+ *               operator (hv_f64.cu): iteration counts of the fp64 reference
+ *               (default)
+ *   WGP_CG_F32  fp32 vectors over the selected fp32 H.V engine (faster; needs
+ *               up to ~40% more iterations on ill-conditioned systems) */
+#define WGP_CG_F64 0
+#define WGP_CG_F32 1
 
 /** Thread-local message of the last failing call. */
 const char* wgp_last_error(void);
@@ -67,6 +75,9 @@ int wgp_create(int device, wgp_ctx** out);
 int wgp_destroy(wgp_ctx* ctx);
 /** Select the H.V kernel (WGP_HV_TC / WGP_HV_SIMT). */
 int wgp_set_hv_impl(wgp_ctx* ctx, int impl);
+/** Select CG's precision (WGP_CG_F64 / WGP_CG_F32); AP and SGD always run
+ *  on fp32 state over the selected H.V engine. */
+int wgp_set_cg_precision(wgp_ctx* ctx, int precision);
 /** The cudaStream_t the context launches on (for event timing by callers). */
 void* wgp_stream(wgp_ctx* ctx);
 /** Kernel timing: while enabled, CUDA events bracket every tensor-core H.V
@@ -90,6 +101,11 @@ int wgp_set_rows(wgp_ctx* ctx, int64_t r0, int64_t r1);
  *  products H * P / H * X at proj/src/solvers.cpp:71,92,110,120,169,188,211
  *  and proj/src/estimator.cpp:90. */
 int wgp_hv(wgp_ctx* ctx, const float* V_host, int s, float* out_host);
+/** fp64 H V on host fp64 V / out (n x s; rows of wgp_set_rows): the operator
+ *  of the fp64 CG path -- entries evaluated in fp32 (bitwise symmetric),
+ *  products and sums in fp64.  The Eigen::MatrixXd-facing form of the
+ *  products H * X the reference writes in fp64 (same sites as wgp_hv). */
+int wgp_hv_f64(wgp_ctx* ctx, const double* V_host, int s, double* out_host);
 /** Device-pointer variant; `stream` may be NULL (context stream). */
 int wgp_hv_device(wgp_ctx* ctx, const float* V, int64_t ldv, int s, float* out, int64_t ldo);
 
@@ -120,6 +136,22 @@ typedef struct {
  *  (init may be NULL = zeros). */
 int wgp_solve(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const float* rhs, const float* init, int s,
               wgp_solve_state* state);
+
+/* SolveState in fp64 (the reference's MatrixXd / VectorXd members). */
+typedef struct {
+  double* solutions;                     /* n x s */
+  double* residuals;                     /* n x s, solver-tracked */
+  double* per_column_relative_residual;  /* s, exact at exit */
+  int* converged;                        /* s */
+  int iterations_used;
+} wgp_solve_state_f64;
+
+/** wgp_solve for fp64 host buffers (Eigen::MatrixXd's column-major storage:
+ *  rhs.data(), init.data()).  With fp64 CG (WGP_CG_F64, the default) the fp64
+ *  init and the fp64 solutions pass through unrounded; AP / SGD run on fp32
+ *  state (rounded in, widened out). */
+int wgp_solve_f64(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const double* rhs, const double* init, int s,
+                  wgp_solve_state_f64* state);
 
 /** derivative_contractions (proj/src/kernel.cpp:216-252) for the estimator's
  *  low-rank contractions (proj/src/estimator.cpp:63-82):

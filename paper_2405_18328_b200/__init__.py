@@ -34,6 +34,8 @@ HV_TC, HV_SIMT, HV_TC_BF16 = 0, 1, 2
 # tc: tcgen05 3xTF32 (default); simt: CUDA-core fp32; tc_bf16: tcgen05 with
 # bf16x3 K.V (faster, ~5e-6 relative: not for tight solver tolerances)
 _HV_IMPLS = {"tc": HV_TC, "simt": HV_SIMT, "tc_bf16": HV_TC_BF16}
+CG_F64, CG_F32 = 0, 1
+_CG_PRECISIONS = {"f64": CG_F64, "f32": CG_F32}
 _KINDS = {"cg": 0, "ap": 1, "sgd": 2}
 _MODES = {"warm": 0, "cold": 1, "cold-fixed": 2}
 _TRANSFORMS = {"softplus": 0, "log": 1}
@@ -59,6 +61,12 @@ class _SolverCfg(C.Structure):
 
 class _SolveState(C.Structure):
     _fields_ = [("solutions", C.POINTER(C.c_float)), ("residuals", C.POINTER(C.c_float)),
+                ("per_column_relative_residual", C.POINTER(C.c_double)),
+                ("converged", C.POINTER(C.c_int)), ("iterations_used", C.c_int)]
+
+
+class _SolveStateF64(C.Structure):
+    _fields_ = [("solutions", C.POINTER(C.c_double)), ("residuals", C.POINTER(C.c_double)),
                 ("per_column_relative_residual", C.POINTER(C.c_double)),
                 ("converged", C.POINTER(C.c_int)), ("iterations_used", C.c_int)]
 
@@ -89,7 +97,7 @@ EXPORTS = [
     "wgp_hv_device", "wgp_solve", "wgp_grad", "wgp_sample_probes", "wgp_rff_probes", "wgp_train",
     "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
     "wgp_exact", "wgp_predict", "wgp_split_order", "wgp_hv_cols", "wgp_hv_block", "wgp_ap_factor", "wgp_ap_block_solve",
-    "wgp_set_split_global",
+    "wgp_set_split_global", "wgp_set_cg_precision", "wgp_hv_f64", "wgp_solve_f64",
 ]
 
 
@@ -122,6 +130,9 @@ def load():
     lib.wgp_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     lib.wgp_destroy.argtypes = [C.c_void_p]
     lib.wgp_set_hv_impl.argtypes = [C.c_void_p, C.c_int]
+    lib.wgp_set_cg_precision.argtypes = [C.c_void_p, C.c_int]
+    lib.wgp_hv_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    lib.wgp_solve_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.wgp_set_data.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
     lib.wgp_set_hyper.argtypes = [C.c_void_p, C.c_void_p]
     lib.wgp_set_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
@@ -181,10 +192,14 @@ def derive_seed(base: int, stream: int) -> int:
     return int(load().wgp_derive_seed(C.c_uint64(base), C.c_uint64(stream)))
 
 
-def _f32(a, n=None):
+def _f32(a, n=None, what="solve: rhs row count mismatch"):
+    """fp32 column-major n x s; with n given, the row count must match (the
+    reference's check_shapes, solvers.cpp:58-67, raises the same way)."""
     a = np.asfortranarray(np.asarray(a, dtype=np.float32))
     if a.ndim == 1:
         a = a.reshape(-1, 1, order="F")
+    if n is not None and a.shape[0] != n:
+        raise ValueError(what)
     return a
 
 
@@ -373,7 +388,7 @@ class Context:
     """One device context (C-ABI ``wgp_ctx``): owns the stream, the points and
     every device buffer, including the warm-start state of ``train``."""
 
-    def __init__(self, device: int = 0, hv_impl: str = "tc"):
+    def __init__(self, device: int = 0, hv_impl: str = "tc", cg_precision: str = "f64"):
         self._lib = load()
         h = C.c_void_p()
         _check(self._lib.wgp_create(device, C.byref(h)))
@@ -381,6 +396,7 @@ class Context:
         self.n = 0
         self.d = 0
         self.set_hv_impl(hv_impl)
+        self.set_cg_precision(cg_precision)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -418,6 +434,14 @@ class Context:
             raise ValueError(f"unknown H.V implementation {impl!r}; one of {sorted(_HV_IMPLS)}")
         _check(self._lib.wgp_set_hv_impl(self._h, _HV_IMPLS[impl]))
 
+    def set_cg_precision(self, precision: str):
+        """CG on fp64 state over the fp64-accumulating operator ("f64", default:
+        the reference's iteration counts) or on fp32 state over the H.V engine
+        ("f32": faster, more iterations on ill-conditioned systems)."""
+        if precision not in _CG_PRECISIONS:
+            raise ValueError(f"unknown CG precision {precision!r}; one of {sorted(_CG_PRECISIONS)}")
+        _check(self._lib.wgp_set_cg_precision(self._h, _CG_PRECISIONS[precision]))
+
     def set_data(self, X):
         X = _f32(X)
         self.n, self.d = X.shape
@@ -435,10 +459,22 @@ class Context:
 
     def hv(self, V, rows=None):
         """H V for host V (n x s) -> host (rows x s)."""
-        V = _f32(V)
+        V = _f32(V, self.n, "hv: V row count mismatch")
         m = self.n if rows is None else rows
         out = np.empty((m, V.shape[1]), dtype=np.float32, order="F")
         _check(self._lib.wgp_hv(self._h, _ptr(V), V.shape[1], _ptr(out)))
+        return out
+
+    def hv_f64(self, V, rows=None):
+        """fp64 H V (the fp64 CG operator) for host V (n x s) -> host fp64 (rows x s)."""
+        V = np.asfortranarray(np.asarray(V, dtype=np.float64))
+        if V.ndim == 1:
+            V = V.reshape(-1, 1, order="F")
+        if V.shape[0] != self.n:
+            raise ValueError("hv: V row count mismatch")
+        m = self.n if rows is None else rows
+        out = np.empty((m, V.shape[1]), dtype=np.float64, order="F")
+        _check(self._lib.wgp_hv_f64(self._h, _ptr(V), V.shape[1], _ptr(out)))
         return out
 
     def hv_device(self, V_ptr: int, ldv: int, s: int, out_ptr: int, ldo: int):
@@ -473,8 +509,10 @@ class Context:
         _check(self._lib.wgp_ap_block_solve(self._h, int(block), C.c_void_p(Rb_ptr), s, C.c_void_p(delta_ptr)))
 
     def solve(self, rhs, config: SolverConfig, init=None) -> SolveState:
-        rhs = _f32(rhs)
+        rhs = _f32(rhs, self.n)
         n, s = rhs.shape
+        if s < 1:
+            raise ValueError("solve: rhs needs at least one column")
         if init is not None:
             init = _f32(init)
             if init.shape != rhs.shape:
@@ -492,6 +530,33 @@ class Context:
                                    _ptr(init) if init is not None else None, s, C.byref(st)))
         return SolveState(sol, res, pcr, [bool(c) for c in conv], st.iterations_used)
 
+    def solve_f64(self, rhs, config: SolverConfig, init=None) -> SolveState:
+        """wgp_solve_f64: fp64 rhs / init / solutions (the reference's MatrixXd);
+        with fp64 CG nothing is rounded to fp32 on the way."""
+        def f64(a):
+            a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+            return a.reshape(-1, 1, order="F") if a.ndim == 1 else a
+        rhs = f64(rhs)
+        if rhs.shape[0] != self.n:
+            raise ValueError("solve: rhs row count mismatch")
+        n, s = rhs.shape
+        if s < 1:
+            raise ValueError("solve: rhs needs at least one column")
+        if init is not None:
+            init = f64(init)
+            if init.shape != rhs.shape:
+                raise ValueError("solve: init shape must match rhs")
+        sol = np.empty((n, s), order="F")
+        res = np.empty((n, s), order="F")
+        pcr = np.empty(s)
+        conv = np.zeros(s, dtype=np.int32)
+        dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+        st = _SolveStateF64(dp(sol), dp(res), dp(pcr), conv.ctypes.data_as(C.POINTER(C.c_int)), 0)
+        cfg = config._c()
+        _check(self._lib.wgp_solve_f64(self._h, C.byref(cfg), _ptr(rhs),
+                                       _ptr(init) if init is not None else None, s, C.byref(st)))
+        return SolveState(sol, res, pcr, [bool(c) for c in conv], st.iterations_used)
+
     def predict(self, X_test, y, config: "SolverConfig" = None) -> "PredictiveDistribution":
         """predict (exact.cpp:52-77) through iterative solves (`config`, default
         CG at tolerance 1e-4) at the context's hyperparameters."""
@@ -502,6 +567,8 @@ class Context:
         if m and Xt.shape[1] != self.d:
             raise ValueError("predict: input dimension mismatch")
         y = np.ascontiguousarray(y, dtype=np.float32).ravel()
+        if y.size != self.n:
+            raise ValueError("predict: X_train and y disagree on n")
         mean = np.zeros(m)
         var = np.zeros(m)
         nv = C.c_double(0.0)
@@ -520,6 +587,8 @@ class Context:
 
     def _exact(self, y, raw, transform, want_grad):
         y = np.ascontiguousarray(y, dtype=np.float32).ravel()
+        if y.size != self.n:
+            raise ValueError(("exact_gradient" if want_grad else "exact_mll") + ": X and y disagree on n")
         r = np.ascontiguousarray(raw, dtype=np.float64)
         if r.size != self.d + 2:
             raise ValueError("Hyperparameters: raw vector must have input_dim + 2 entries")
@@ -532,7 +601,12 @@ class Context:
     def grad(self, transform, raw, vy, L, R, coef_b):
         raw = np.ascontiguousarray(raw, dtype=np.float64)
         vy = np.ascontiguousarray(vy, dtype=np.float32)
-        L, R = _f32(L), _f32(R)
+        if vy.size != self.n:
+            raise ValueError("assemble_gradient_streamed: shape mismatch")
+        L = _f32(L, self.n, "assemble_gradient_streamed: shape mismatch")
+        R = _f32(R, self.n, "assemble_gradient_streamed: shape mismatch")
+        if L.shape[1] != R.shape[1]:
+            raise ValueError("assemble_gradient_streamed: shape mismatch")
         oa, ob = np.empty(raw.size), np.empty(raw.size)
         _check(self._lib.wgp_grad(self._h, _TRANSFORMS.get(transform, transform), _ptr(raw),
                                   _ptr(vy), _ptr(L), _ptr(R), L.shape[1], coef_b, _ptr(oa), _ptr(ob)))
@@ -545,7 +619,9 @@ class Context:
 
     def train(self, y, config: TrainConfig) -> OptTrace:
         config.validate()
-        y = np.ascontiguousarray(y, dtype=np.float32)
+        y = np.ascontiguousarray(y, dtype=np.float32).ravel()
+        if y.size != self.n:
+            raise ValueError("train: X and y disagree on n")
         T, p, sp = config.steps, self.d + 2, config.num_probes + 1
         arr = dict(raw=np.zeros((T, p)), con=np.zeros((T, p)), grad=np.zeros((T, p)),
                    it=np.zeros(T, dtype=np.int32), pcr=np.zeros((T, sp)), wsd=np.zeros(T),

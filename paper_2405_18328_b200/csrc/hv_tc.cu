@@ -2,28 +2,35 @@
 //
 // Replaces the dense products H * V of the reference solvers
 // (proj/src/solvers.cpp:71,92,110,120,169,186,188,211,242) without forming H.
-// One CTA owns a 128-row tile I and streams 64-point tiles J (FlashAttention
-// shape, no online-softmax state):
+// One CTA owns a 128-row tile I and streams 32-point tiles J (FlashAttention
+// shape, no online-softmax state); the default engine is 3xTF32 throughout:
 //
-//   MMA-1  S[I,J]  = A_I . B_J^T           (tcgen05.mma kind::tf32, 3xTF32,
-//                    a_i = [x_i, |x_i|^2, 1], b_j = [-2 x_j, 1, |x_j|^2]
-//                    so S = u^2, the squared scaled distance, lands in TMEM)
+//   MMA-1  S[I,J]  = A_I . B_J^T           (tcgen05.mma kind::tf32, M=128, N=64:
+//                    two J tiles per instruction, 3xTF32 hi.hi + hi.lo + lo.hi;
+//                    a_i = [x_i, |x_i|^2, 1], b_j = [-2 x_j, 1, |x_j|^2] so
+//                    S = u^2, the squared scaled distance, lands in TMEM; for
+//                    d <= 19 the three passes are packed along K)
 //   epilogue       k = sf^2 (1 + u ln2) 2^-u from S (tcgen05.ld -> registers,
 //                    sqrt + ex2 on the MUFU), the diagonal entry zeroed
 //                    (H_ii V_i = (sf^2 + sigma^2) V_i is added exactly at the end),
-//                    split k = k1 + k2 into two bf16, tcgen05.st back to TMEM
-//   MMA-2  O[I,:] += K[I,J] . V[J,:]       (kind::f16, A = K from TMEM, bf16x3:
-//                    k1 v1 + k1 v2 + k2 v1 with V = v1 + v2 split likewise)
+//                    k split into tf32 k_hi | k_lo, tcgen05.st back to TMEM in place
+//   MMA-2  O[I,:] += K[I,J] . V[J,:]       (kind::tf32, A = K from TMEM, N = s
+//                    padded to 16, 3xTF32 k_hi v_hi + k_hi v_lo + k_lo v_hi)
 //
 // Warp roles (512 threads): warps 0..11 epilogue (three warpgroups; group w
 // takes tiles t = w, w+3, ...), warp 12 TMA producer of A_I and the B_J ring,
 // 13 MMA-1 issuer, 14 TMA producer of the V_J ring (+ TMEM allocation), 15
-// MMA-2 issuer.  Five 64-column TMEM buffers hold S and then, in place, the
-// packed K, so MMA-1 runs ahead of MMA-2 and the epilogue latency of one tile
-// hides behind the MMAs of the next.  MMA-2 accumulates in fp32 chunks of 16
-// tiles that the epilogue drains into fp64 (accumulation error independent of
-// n).  J tiles of a row tile may be split across CTAs (split count fixed per
-// launch shape, fp64 partials summed in fixed order -> deterministic).
+// MMA-2 issuer.  TMEM (layout 2): two fp32 accumulators O0 | O1
+// (double-buffered chunk drains), A_I hi/lo, and two 128-column groups each
+// holding S(t) | S(t+1) and then, in place, their K planes -- 4 tiles in
+// flight, so MMA-1 runs ahead of MMA-2 and one tile's epilogue hides behind
+// the MMAs of the next.  MMA-2 accumulates in fp32 chunks of 32 tiles that the
+// epilogue folds into a shared-memory fp32 sum and an fp64 CTA sum (error
+// independent of n).  J tiles of a row tile may be split across CTAs (split
+// count keyed on the global n, partials summed in fixed order ->
+// deterministic and shard-invariant).  WGP_HV_TC_BF16 selects the opt-in
+// bf16x3 K.V variant (kind::f16, 64-point tiles).
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>

@@ -13,12 +13,14 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/warmgp_b200.h"
 #include "common.cuh"
 #include "exact.cuh"
 #include "host_rng.hpp"
+#include "hv_f64.cuh"
 #include "hv_tc.cuh"
 #include "kernels.cuh"
 #include "solver_kernels.cuh"
@@ -116,6 +118,12 @@ struct Ctx {
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
   Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, DXP, XP, PP, lapack_work, info;
   Buf gpart, gout, gtc_ws;
+  // fp64 CG (cg_precision == WGP_CG_F64): solver state and the hv_f64 split partials
+  Buf B64, X64, R64, P64, HP64, Rt64, Xbest64, Rbest64, hv64_ws;
+  Buf linv_ptrs;  // AP: device pointer array of the batched inverse
+  Buf tr_rhs, tr_sol0, tr_sol1, tr_res, tr_sol64a, tr_sol64b;  // train(): solver state across steps
+  Buf api_B, api_X0, api_Xs, api_Rs;  // wgp_solve staging
+  int cg_precision = WGP_CG_F64;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
   Buf hx, hx_ws, exv;  // exact path: dense H (fp64), cuSOLVER workspace, vectors
@@ -276,7 +284,8 @@ struct Ctx {
     WGP_CUDA(cudaStreamSynchronize(st));
     return h;
   }
-  std::vector<double> dots(const float* A, const float* B_, int s) {
+  template <class T>
+  std::vector<double> dots(const T* A, const T* B_, int s) {
     ensure_solver_ws(s);
     col_dots(A, B_, ld, n, s, part.as<double>(), &dctrl()->ticket, colsum.as<double>(), st);
     std::vector<double> h(s);
@@ -339,8 +348,13 @@ struct Ctx {
 
   // solve(H, rhs, init, config), proj/src/solvers.cpp:265-279.  Device
   // pointers with leading dimension ld; init == nullptr means zeros.
+  // CG with cg_precision == WGP_CG_F64 runs on fp64 solver state over the
+  // fp64-accumulating operator (hv_f64.cu) and rounds X / R to fp32 at exit;
+  // init64 (optional) is an fp64 initial guess taking precedence over init,
+  // and Xo64 (optional) receives the fp64 solutions (the outer loop's warm
+  // start keeps them, proj/src/optimizer.cpp:133-135,158).
   SolveOut solve(const wgp_solver_cfg& cfg, const float* B, const float* init, float* Xo, float* Ro,
-                 int s) {
+                 int s, const double* init64 = nullptr, double* Xo64 = nullptr) {
     require_data();
     validate(cfg);
     if (s < 1) throw std::invalid_argument("solve: rhs needs at least one column");
@@ -358,22 +372,53 @@ struct Ctx {
     for (int c = 0; c < s; ++c) tl[c] = c == 0 ? cfg.tol_mean : cfg.tol_samples;  // :49-56
     WGP_CUDA(cudaMemcpyAsync(bnorm.p, bn.data(), sizeof(double) * s, cudaMemcpyHostToDevice, st));
     WGP_CUDA(cudaMemcpyAsync(tol.p, tl.data(), sizeof(double) * s, cudaMemcpyHostToDevice, st));
-    // X = init; R = rhs - H X (exactly rhs for a zero init)
-    if (init) {
-      copy_cols(init, ld, Xo, ld, n, s, st);
-      hv_all(Xo, s, Ro, kHvResidual, B);
-    } else {
-      fill_zero(Xo, ld, n, s, st);
-      copy_cols(B, ld, Ro, ld, n, s, st);
-    }
     SolveOut out;
-    if (cfg.kind == WGP_SOLVER_CG) cg(cfg, B, Xo, Ro, s, out);
-    else if (cfg.kind == WGP_SOLVER_AP) ap(cfg, B, Xo, Ro, s, out);
-    else sgd(cfg, B, Xo, Ro, s, out);
-    // finalize_exact_residuals, :69-77
-    float* E = Rtmp.as<float>();
-    hv_all(Xo, s, E, kHvResidual, B);
-    std::vector<double> en = dots(E, E, s);
+    std::vector<double> en;
+    if (cfg.kind == WGP_SOLVER_CG && cg_precision == WGP_CG_F64) {
+      const size_t bytes = sizeof(double) * ld * s;
+      B64.ensure(bytes);
+      X64.ensure(bytes);
+      R64.ensure(bytes);
+      double* b64 = B64.as<double>();
+      double* x64 = X64.as<double>();
+      double* r64 = R64.as<double>();
+      widen(B, ld, b64, ld, n, s, st);
+      if (init64 || init) {
+        if (init64) WGP_CUDA(cudaMemcpy2DAsync(x64, sizeof(double) * ld, init64, sizeof(double) * ld,
+                                               sizeof(double) * n, s, cudaMemcpyDeviceToDevice, st));
+        else widen(init, ld, x64, ld, n, s, st);
+        hv64_all(x64, s, r64, kHv64Residual, b64, nullptr);
+      } else {
+        WGP_CUDA(cudaMemsetAsync(x64, 0, bytes, st));
+        WGP_CUDA(cudaMemcpyAsync(r64, b64, bytes, cudaMemcpyDeviceToDevice, st));
+      }
+      cg<double>(cfg, b64, x64, r64, s, out);
+      // finalize_exact_residuals (:69-77) on the fp64 iterate
+      Rt64.ensure(bytes);
+      double* e64 = Rt64.as<double>();
+      hv64_all(x64, s, e64, kHv64Residual, b64, nullptr);
+      en = dots(e64, e64, s);
+      narrow(x64, ld, Xo, ld, n, s, st);
+      narrow(r64, ld, Ro, ld, n, s, st);
+      if (Xo64) WGP_CUDA(cudaMemcpy2DAsync(Xo64, sizeof(double) * ld, x64, sizeof(double) * ld,
+                                           sizeof(double) * n, s, cudaMemcpyDeviceToDevice, st));
+    } else {
+      // X = init; R = rhs - H X (exactly rhs for a zero init)
+      if (init) {
+        copy_cols(init, ld, Xo, ld, n, s, st);
+        hv_all(Xo, s, Ro, kHvResidual, B);
+      } else {
+        fill_zero(Xo, ld, n, s, st);
+        copy_cols(B, ld, Ro, ld, n, s, st);
+      }
+      if (cfg.kind == WGP_SOLVER_CG) cg<float>(cfg, B, Xo, Ro, s, out);
+      else if (cfg.kind == WGP_SOLVER_AP) ap(cfg, B, Xo, Ro, s, out);
+      else sgd(cfg, B, Xo, Ro, s, out);
+      // finalize_exact_residuals, :69-77
+      float* E = Rtmp.as<float>();
+      hv_all(Xo, s, E, kHvResidual, B);
+      en = dots(E, E, s);
+    }
     out.rel.resize(s);
     for (int c = 0; c < s; ++c) out.rel[c] = bn[c] > 0.0 ? std::sqrt(en[c]) / bn[c] : 0.0;
     out.conv.resize(s);
@@ -391,9 +436,9 @@ struct Ctx {
   // solves -- the H.V kernels read the hyperparameter scalars from device
   // memory -- and re-captured when any device workspace was reallocated.
   struct CgGraph {
-    const float* B;
-    float* Xo;
-    float* R;
+    const void* B;
+    const void* Xo;
+    const void* R;
     int s, impl;
     uint64_t gen;
     cudaGraphExec_t exec[2];
@@ -423,32 +468,88 @@ struct Ctx {
     ap_graphs.clear();
   }
 
-  void cg(const wgp_solver_cfg& cfg, const float* B, float* Xo, float* R, int s, SolveOut& out) {
+  // fp64 CG operator: out = H V (store) or B - H V (residual) for output rows
+  // [rr0, rr0 + m), fp64 V (all n rows) / out / B (hv_f64.cu).
+  void hv64_rows(const double* V, int64_t ldv, int s, double* out, int64_t ldo, int mode, const double* B,
+                 int64_t ldb, int64_t rr0, int64_t m, const int* done) {
+    Hv64Params q{};
+    q.xs = xs.as<float>();
+    q.n = n;
+    q.dp = dp;
+    q.d = d;
+    q.r0 = rr0;
+    q.m = m;
+    q.ldv = ldv;
+    q.ldo = ldo;
+    q.ldb = ldb;
+    q.mode = mode;
+    q.hyp = dhyp.as<float>();
+    q.done = done;
+    for (int c0 = 0; c0 < s; c0 += 80) {  // one workspace per chunk of <= 80 columns
+      const int sc = std::min(80, s - c0);
+      hv64_ws.ensure(hv64_workspace_bytes(n, m, sc));
+      Hv64Params r = q;
+      r.s = sc;
+      r.V = V + c0 * ldv;
+      r.out = out + c0 * ldo;
+      r.B = B ? B + c0 * ldb : nullptr;
+      r.part = hv64_ws.as<double>();
+      hv64(r, st);
+    }
+  }
+  void hv64_all(const double* V, int s, double* out, int mode, const double* B, const int* done) {
+    hv64_rows(V, ld, s, out, ld, mode, B, ld, 0, n, done);
+  }
+
+  // The operator of a CG iteration in the solver-state precision T: float
+  // runs the configured fp32 engine (P's tf32 planes kept by the direction
+  // kernels), double the fp64-accumulating symmetric engine (hv_f64.cu).
+  void cg_hv(const float* V, int s, float* out, int mode, const float* B, const int* done, const float* vplanes) {
+    hv_all(V, s, out, mode, B, done, vplanes);
+  }
+  void cg_hv(const double* V, int s, double* out, int mode, const double* B, const int* done, const float*) {
+    hv64_all(V, s, out, mode == kHvResidual ? kHv64Residual : kHv64Store, B, done);
+  }
+
+  template <class T>
+  void cg(const wgp_solver_cfg& cfg, const T* B, T* Xo, T* R, int s, SolveOut& out) {
+    constexpr bool f64 = std::is_same<T, double>::value;
     const int max_it = cfg.max_iterations > 0 ? cfg.max_iterations : static_cast<int>(10 * n);
     reset_ctrl(max_it);
-    float* Pp = P.as<float>();
-    float* HPp = HP.as<float>();
-    float* Rt = Rtmp.as<float>();
+    Buf& Pbuf = f64 ? P64 : P;
+    Buf& HPbuf = f64 ? HP64 : HP;
+    Buf& Rtbuf = f64 ? Rt64 : Rtmp;
+    Pbuf.ensure(sizeof(T) * ld * s);
+    HPbuf.ensure(sizeof(T) * ld * s);
+    Rtbuf.ensure(sizeof(T) * ld * s);
+    T* Pp = Pbuf.as<T>();
+    T* HPp = HPbuf.as<T>();
+    T* Rt = Rtbuf.as<T>();
     const ColState cs = colstate();
     SolveCtrl* c = dctrl();
     double* pt = part.as<double>();
-    Xbest.ensure(sizeof(float) * ld * s);
-    Rbest.ensure(sizeof(float) * ld * s);
-    float* Xb = Xbest.as<float>();
-    float* Rb = Rbest.as<float>();
-    PP.ensure(sizeof(float) * 2 * ld * s);  // P's tf32 planes: the H.V skips its split of P
-    float* PPp = PP.as<float>();
+    Buf& Xbbuf = f64 ? Xbest64 : Xbest;
+    Buf& Rbbuf = f64 ? Rbest64 : Rbest;
+    Xbbuf.ensure(sizeof(T) * ld * s);
+    Rbbuf.ensure(sizeof(T) * ld * s);
+    T* Xb = Xbbuf.as<T>();
+    T* Rb = Rbbuf.as<T>();
+    float* PPp = nullptr;
+    if (!f64) {
+      PP.ensure(sizeof(float) * 2 * ld * s);  // P's tf32 planes: the H.V skips its split of P
+      PPp = PP.as<float>();
+    }
     cg_init(Pp, R, ld, n, s, cs, pt, c, st, PPp);
     cg_snapshot(Xo, R, Xb, Rb, ld, n, s, cs, c, true, st);
     const int* done = &c->done;
     auto iteration = [&](bool refresh) {
-      hv_all(Pp, s, HPp, kHvStore, nullptr, done, PPp);
+      cg_hv(Pp, s, HPp, kHvStore, nullptr, done, PPp);
       cg_alpha(Pp, HPp, ld, n, s, cs, pt, c, st);
       if (!refresh) {
         cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, false, st);
       } else {
         cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, true, st);
-        hv_all(Xo, s, Rt, kHvResidual, B, done);
+        cg_hv(Xo, s, Rt, kHvResidual, B, done, nullptr);
         cg_refresh_norm(R, Rt, ld, n, s, cs, pt, c, st);
         cg_snapshot(Xo, R, Xb, Rb, ld, n, s, cs, c, false, st);
       }
@@ -456,6 +557,7 @@ struct Ctx {
     };
     static const bool no_graphs = getenv("WGP_NO_GRAPHS") != nullptr;
     constexpr int kChunk = 10;
+    const int impl = f64 ? -1 : hv_impl;
     int launched = 0;
     const int eager[3] = {2, 4, 4};  // first kChunk iterations, polled early
     for (int e = 0; e < 3; ++e) {
@@ -471,14 +573,14 @@ struct Ctx {
     if (!no_graphs) {
       const uint64_t gen = alloc_generation().load();
       for (auto& g : cg_graphs)
-        if (g.B == B && g.Xo == Xo && g.R == R && g.s == s && g.impl == hv_impl) gr = &g;
+        if (g.B == B && g.Xo == Xo && g.R == R && g.s == s && g.impl == impl) gr = &g;
       if (gr && gr->gen != gen) {
         drop_cg_graphs();
         gr = nullptr;
       }
       if (!gr) {
         if (cg_graphs.size() >= 8) drop_cg_graphs();
-        CgGraph g{B, Xo, R, s, hv_impl, gen, {nullptr, nullptr}};
+        CgGraph g{B, Xo, R, s, impl, gen, {nullptr, nullptr}};
         for (int v = 0; v < 2; ++v) {
           cudaGraph_t graph;
           WGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -556,7 +658,7 @@ struct Ctx {
     identities(linv.as<double>(), bs, nb, st);
     std::vector<double*> lptr(nb);
     for (int64_t b = 0; b < nb; ++b) lptr[b] = linv.as<double>() + b * bb;
-    Buf lp;
+    Buf& lp = linv_ptrs;  // persistent: a fresh allocation would invalidate the cached graphs
     lp.ensure(sizeof(double*) * nb);
     WGP_CUDA(cudaMemcpyAsync(lp.p, lptr.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice, st));
     const double one_ = 1.0, zero_ = 0.0;
@@ -631,14 +733,16 @@ struct Ctx {
         if (size == bs && bs % kSplitK == 0) {
           const int kc = static_cast<int>(bs / kSplitK);
           kparts = kSplitK;
-          cublasDgemmStridedBatched(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, kc, &one, Hinv,
-                                    static_cast<int>(bs), static_cast<long long>(kc) * bs, Rb.as<double>(),
-                                    static_cast<int>(size), kc, &zero, D64.as<double>(), static_cast<int>(size),
-                                    static_cast<long long>(size) * s, kSplitK);
+          if (cublasDgemmStridedBatched(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, kc, &one, Hinv,
+                                        static_cast<int>(bs), static_cast<long long>(kc) * bs, Rb.as<double>(),
+                                        static_cast<int>(size), kc, &zero, D64.as<double>(), static_cast<int>(size),
+                                        static_cast<long long>(size) * s, kSplitK) != CUBLAS_STATUS_SUCCESS)
+            throw DeviceError("cublasDgemmStridedBatched failed (AP block solve)");
         } else {
-          cublasDgemm(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, static_cast<int>(size), &one, Hinv,
-                      static_cast<int>(bs), Rb.as<double>(), static_cast<int>(size), &zero, D64.as<double>(),
-                      static_cast<int>(size));
+          if (cublasDgemm(cublas, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(size), s, static_cast<int>(size), &one,
+                          Hinv, static_cast<int>(bs), Rb.as<double>(), static_cast<int>(size), &zero,
+                          D64.as<double>(), static_cast<int>(size)) != CUBLAS_STATUS_SUCCESS)
+            throw DeviceError("cublasDgemm failed (AP block solve)");
         }
         ap_apply(Xo, ld, start, size, s, D64.as<double>(), kparts, DX.as<float>(), DXP.as<float>(), c, st);
       }
@@ -770,6 +874,24 @@ struct Ctx {
     float* HD = HP.as<float>();
     sub_into(init, sol, D, ld, n, s, st);
     hv_all(D, s, HD);
+    const std::vector<double> q = dots(D, HD, s);
+    double acc = 0.0;
+    for (double v : q) acc += v;
+    return std::sqrt(std::max(acc / s / static_cast<double>(n), 0.0));
+  }
+
+  // the same on fp64 solver state over the fp64 operator (fp64 CG)
+  double warm_distance64(const double* init, const double* sol, int s) {
+    ensure_solver_ws(s);
+    const size_t bytes = sizeof(double) * ld * s;
+    P64.ensure(bytes);
+    HP64.ensure(bytes);
+    double* D = P64.as<double>();
+    double* HD = HP64.as<double>();
+    // D = init - sol
+    WGP_CUDA(cudaMemcpyAsync(D, init, bytes, cudaMemcpyDeviceToDevice, st));
+    axpy_cols(-1.0, sol, D, ld, n, s, st);
+    hv64_all(D, s, HD, kHv64Store, nullptr, nullptr);
     const std::vector<double> q = dots(D, HD, s);
     double acc = 0.0;
     for (double v : q) acc += v;
@@ -1050,7 +1172,12 @@ struct Ctx {
     const bool fixed = cfg.mode != 1, warm = cfg.mode == 0, pathwise = cfg.estimator == 1;
     const int F = cfg.rff_features > 0 ? cfg.rff_features : 1000;
 
-    Buf rhs, sol0, sol1, Rres;
+    // persistent across calls (Ctx members): fresh allocations would bump the
+    // allocation generation and force every cached CG / AP graph to re-capture
+    Buf& rhs = tr_rhs;
+    Buf& sol0 = tr_sol0;
+    Buf& sol1 = tr_sol1;
+    Buf& Rres = tr_res;
     rhs.ensure(sizeof(float) * ld * sp);
     sol0.ensure(sizeof(float) * ld * sp);
     sol1.ensure(sizeof(float) * ld * sp);
@@ -1075,6 +1202,19 @@ struct Ctx {
     if (fixed && !cfg.exact_gradients) draw(derive_seed(cfg.seed, 1));  // optimizer.cpp:99
     float* cur = sol0.as<float>();
     float* prev = sol1.as<float>();
+    // fp64 CG keeps the warm-start solutions in fp64 as well (the reference's
+    // prev_solutions are MatrixXd, optimizer.cpp:133-135,158)
+    const bool keep64 = cfg.solver.kind == WGP_SOLVER_CG && cg_precision == WGP_CG_F64;
+    Buf& s64a = tr_sol64a;
+    Buf& s64b = tr_sol64b;
+    double* cur64 = nullptr;
+    double* prev64 = nullptr;
+    if (keep64) {
+      s64a.ensure(sizeof(double) * ld * sp);
+      s64b.ensure(sizeof(double) * ld * sp);
+      cur64 = s64a.as<double>();
+      prev64 = s64b.as<double>();
+    }
     bool have_prev = false;
     cudaEvent_t e0, e1, e2;
     WGP_CUDA(cudaEventCreate(&e0));
@@ -1120,10 +1260,12 @@ struct Ctx {
           wgp_solver_cfg sc = cfg.solver;
           sc.seed = derive_seed(derive_seed(cfg.seed, kSolverStream), static_cast<uint64_t>(t));
           const bool have_warm = warm && have_prev;
-          SolveOut so = solve(sc, rhs.as<float>(), have_warm ? prev : nullptr, cur, Rres.as<float>(), sp);
+          SolveOut so = solve(sc, rhs.as<float>(), have_warm ? prev : nullptr, cur, Rres.as<float>(), sp,
+                              have_warm ? prev64 : nullptr, cur64);
           WGP_CUDA(cudaEventRecord(e1, st));
           double wsd = 0.0;
-          if (have_warm && cfg.warm_start_distance) wsd = warm_distance(prev, cur, sp);
+          if (have_warm && cfg.warm_start_distance)
+            wsd = keep64 ? warm_distance64(prev64, cur64, sp) : warm_distance(prev, cur, sp);
           std::vector<double> qa(p), qb(p), g(p);
           grad(T, raw.data(), cur, cur + ld, pathwise ? cur + ld : Z, s, 0.5 / s, qa.data(), qb.data());
           for (int k = 0; k < p; ++k) g[k] = qa[k] - qb[k];
@@ -1150,6 +1292,7 @@ struct Ctx {
             if (tr->step_ms) tr->step_ms[t - 1] = ms_step;
           }
           std::swap(cur, prev);
+          std::swap(cur64, prev64);
           have_prev = true;
         } catch (const NumericalError& e) {
           throw NumericalError("step " + std::to_string(t) + ": " + e.what());
@@ -1220,6 +1363,98 @@ struct wgp_ctx {
 
 using wgp::guarded;
 
+namespace {
+// wgp_solve / wgp_solve_f64: host rhs / init (fp32 or fp64) -> device, solve,
+// solutions / residuals back in the caller's precision.  With fp64 CG an fp64
+// init and the fp64 solutions pass through unrounded.
+template <class H, class S>
+int solve_host(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const H* rhs, const H* init, int s, S* state) {
+  constexpr bool f64 = std::is_same<H, double>::value;
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    WGP_CUDA(cudaSetDevice(c.device));
+    c.require_data();
+    if (!cfg) throw std::invalid_argument("solve: null config");
+    if (s < 1) throw std::invalid_argument("solve: rhs needs at least one column");
+    if (!rhs) throw std::invalid_argument("solve: rhs row count mismatch");
+    for (int64_t e = 0; e < c.n * s; ++e)
+      if (!std::isfinite(rhs[e]) || (init && !std::isfinite(init[e])))
+        throw std::invalid_argument("solve: non-finite right-hand side or init");
+    const size_t bytes = sizeof(float) * c.ld * s;
+    c.api_B.ensure(bytes);
+    c.api_Xs.ensure(bytes);
+    c.api_Rs.ensure(bytes);
+    float* B = c.api_B.as<float>();
+    float* Xs = c.api_Xs.as<float>();
+    float* Rs = c.api_Rs.as<float>();
+    float* X0 = nullptr;
+    double* X0_64 = nullptr;
+    double* Xo64 = nullptr;
+    // host fp64 -> device fp64 staging, rounded to fp32 where the solver state is fp32
+    auto upload = [&](const H* src, float* dst32, double** dst64) {
+      WGP_CUDA(cudaMemsetAsync(dst32, 0, bytes, c.st));
+      if constexpr (f64) {
+        c.io_in.ensure(sizeof(double) * c.ld * s);
+        double* tmp = c.io_in.as<double>();
+        WGP_CUDA(cudaMemcpy2DAsync(tmp, sizeof(double) * c.ld, src, sizeof(double) * c.n, sizeof(double) * c.n, s,
+                                   cudaMemcpyHostToDevice, c.st));
+        wgp::narrow(tmp, c.ld, dst32, c.ld, c.n, s, c.st);
+        if (dst64) *dst64 = tmp;
+      } else {
+        WGP_CUDA(cudaMemcpy2DAsync(dst32, sizeof(float) * c.ld, src, sizeof(float) * c.n, sizeof(float) * c.n, s,
+                                   cudaMemcpyHostToDevice, c.st));
+      }
+    };
+    upload(rhs, B, nullptr);
+    if (init) {
+      c.api_X0.ensure(bytes);
+      X0 = c.api_X0.as<float>();
+      upload(init, X0, &X0_64);
+    }
+    const bool keep64 = f64 && cfg->kind == WGP_SOLVER_CG && c.cg_precision == WGP_CG_F64;
+    if (keep64) {
+      c.io_out.ensure(sizeof(double) * c.ld * s);
+      Xo64 = c.io_out.as<double>();
+    }
+    const wgp::Ctx::SolveOut so = c.solve(*cfg, B, X0, Xs, Rs, s, keep64 ? X0_64 : nullptr, Xo64);
+    if (state) {
+      if constexpr (f64) {
+        // solutions in fp64 (fp64 CG: unrounded), residuals widened from fp32
+        c.io_in.ensure(sizeof(double) * c.ld * s);
+        double* w = c.io_in.as<double>();
+        if (state->solutions) {
+          const double* src = Xo64;
+          if (!src) {
+            wgp::widen(Xs, c.ld, w, c.ld, c.n, s, c.st);
+            src = w;
+          }
+          WGP_CUDA(cudaMemcpy2DAsync(state->solutions, sizeof(double) * c.n, src, sizeof(double) * c.ld,
+                                     sizeof(double) * c.n, s, cudaMemcpyDeviceToHost, c.st));
+          WGP_CUDA(cudaStreamSynchronize(c.st));
+        }
+        if (state->residuals) {
+          wgp::widen(Rs, c.ld, w, c.ld, c.n, s, c.st);
+          WGP_CUDA(cudaMemcpy2DAsync(state->residuals, sizeof(double) * c.n, w, sizeof(double) * c.ld,
+                                     sizeof(double) * c.n, s, cudaMemcpyDeviceToHost, c.st));
+        }
+      } else {
+        if (state->solutions)
+          WGP_CUDA(cudaMemcpy2DAsync(state->solutions, sizeof(float) * c.n, Xs, sizeof(float) * c.ld,
+                                     sizeof(float) * c.n, s, cudaMemcpyDeviceToHost, c.st));
+        if (state->residuals)
+          WGP_CUDA(cudaMemcpy2DAsync(state->residuals, sizeof(float) * c.n, Rs, sizeof(float) * c.ld,
+                                     sizeof(float) * c.n, s, cudaMemcpyDeviceToHost, c.st));
+      }
+      WGP_CUDA(cudaStreamSynchronize(c.st));
+      if (state->per_column_relative_residual)
+        std::copy(so.rel.begin(), so.rel.end(), state->per_column_relative_residual);
+      if (state->converged) std::copy(so.conv.begin(), so.conv.end(), state->converged);
+      state->iterations_used = so.iterations;
+    }
+  });
+}
+}  // namespace
+
 extern "C" {
 
 const char* wgp_last_error(void) { return wgp::g_last_error.c_str(); }
@@ -1282,6 +1517,13 @@ int wgp_set_hv_impl(wgp_ctx* ctx, int impl) {
   });
 }
 
+int wgp_set_cg_precision(wgp_ctx* ctx, int precision) {
+  return guarded([&] {
+    if (precision != WGP_CG_F64 && precision != WGP_CG_F32) throw std::invalid_argument("unknown CG precision");
+    ctx->c.cg_precision = precision;
+  });
+}
+
 int wgp_profile(wgp_ctx* ctx, int enable) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("null context");
@@ -1340,6 +1582,25 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
   });
 }
 
+int wgp_hv_f64(wgp_ctx* ctx, const double* V, int s, double* out) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    WGP_CUDA(cudaSetDevice(c.device));
+    c.require_data();
+    if (s < 1) throw std::invalid_argument("wgp_hv: s must be >= 1");
+    const int64_t m = c.r1 - c.r0;
+    wgp::Buf& dv = c.io_in;
+    wgp::Buf& dout = c.io_out;
+    dv.ensure(sizeof(double) * c.ld * s);
+    dout.ensure(sizeof(double) * m * s);
+    WGP_CUDA(cudaMemcpy2DAsync(dv.p, sizeof(double) * c.ld, V, sizeof(double) * c.n, sizeof(double) * c.n, s,
+                               cudaMemcpyHostToDevice, c.st));
+    c.hv64_rows(dv.as<double>(), c.ld, s, dout.as<double>(), m, wgp::kHv64Store, nullptr, 0, c.r0, m, nullptr);
+    WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double) * m * s, cudaMemcpyDeviceToHost, c.st));
+    WGP_CUDA(cudaStreamSynchronize(c.st));
+  });
+}
+
 int wgp_hv_device(wgp_ctx* ctx, const float* V, int64_t ldv, int s, float* out, int64_t ldo) {
   return guarded([&] {
     wgp::Ctx& c = ctx->c;
@@ -1352,44 +1613,12 @@ int wgp_hv_device(wgp_ctx* ctx, const float* V, int64_t ldv, int s, float* out, 
 
 int wgp_solve(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const float* rhs, const float* init, int s,
               wgp_solve_state* state) {
-  return guarded([&] {
-    wgp::Ctx& c = ctx->c;
-    WGP_CUDA(cudaSetDevice(c.device));
-    c.require_data();
-    if (s < 1) throw std::invalid_argument("solve: rhs needs at least one column");
-    for (int64_t e = 0; e < c.n * s; ++e)
-      if (!std::isfinite(rhs[e]) || (init && !std::isfinite(init[e])))
-        throw std::invalid_argument("solve: non-finite right-hand side or init");
-    wgp::Buf B, X0, Xs, Rs;
-    const size_t bytes = sizeof(float) * c.ld * s;
-    B.ensure(bytes);
-    Xs.ensure(bytes);
-    Rs.ensure(bytes);
-    WGP_CUDA(cudaMemsetAsync(B.p, 0, bytes, c.st));
-    WGP_CUDA(cudaMemcpy2DAsync(B.p, sizeof(float) * c.ld, rhs, sizeof(float) * c.n, sizeof(float) * c.n, s,
-                               cudaMemcpyHostToDevice, c.st));
-    if (init) {
-      X0.ensure(bytes);
-      WGP_CUDA(cudaMemsetAsync(X0.p, 0, bytes, c.st));
-      WGP_CUDA(cudaMemcpy2DAsync(X0.p, sizeof(float) * c.ld, init, sizeof(float) * c.n, sizeof(float) * c.n,
-                                 s, cudaMemcpyHostToDevice, c.st));
-    }
-    const wgp::Ctx::SolveOut so =
-        c.solve(*cfg, B.as<float>(), init ? X0.as<float>() : nullptr, Xs.as<float>(), Rs.as<float>(), s);
-    if (state) {
-      if (state->solutions)
-        WGP_CUDA(cudaMemcpy2DAsync(state->solutions, sizeof(float) * c.n, Xs.p, sizeof(float) * c.ld,
-                                   sizeof(float) * c.n, s, cudaMemcpyDeviceToHost, c.st));
-      if (state->residuals)
-        WGP_CUDA(cudaMemcpy2DAsync(state->residuals, sizeof(float) * c.n, Rs.p, sizeof(float) * c.ld,
-                                   sizeof(float) * c.n, s, cudaMemcpyDeviceToHost, c.st));
-      WGP_CUDA(cudaStreamSynchronize(c.st));
-      if (state->per_column_relative_residual)
-        std::copy(so.rel.begin(), so.rel.end(), state->per_column_relative_residual);
-      if (state->converged) std::copy(so.conv.begin(), so.conv.end(), state->converged);
-      state->iterations_used = so.iterations;
-    }
-  });
+  return solve_host(ctx, cfg, rhs, init, s, state);
+}
+
+int wgp_solve_f64(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const double* rhs, const double* init, int s,
+                  wgp_solve_state_f64* state) {
+  return solve_host(ctx, cfg, rhs, init, s, state);
 }
 
 int wgp_grad(wgp_ctx* ctx, int transform, const double* raw, const float* vy, const float* L,

@@ -117,7 +117,8 @@ __device__ void loop_check(int s, ColState cs, SolveCtrl* ctrl, bool begin_next)
   const int64_t rb = static_cast<int64_t>(blockIdx.x) * rpb_;         \
   const int64_t re = rb + rpb_ < n ? rb + rpb_ : n;
 
-__global__ void col_dots_kernel(const float* A, const float* B, int64_t ld, int64_t n, int s,
+template <class T>
+__global__ void col_dots_kernel(const T* A, const T* B, int64_t ld, int64_t n, int s,
                                 double* part, unsigned* ticket, double* out) {
   __shared__ Red red;
   ROWS_OF_BLOCK
@@ -140,7 +141,8 @@ __global__ void col_dots_kernel(const float* A, const float* B, int64_t ld, int6
   if (threadIdx.x == 0) *ticket = 0;
 }
 
-__global__ void cg_init_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
+template <class T>
+__global__ void cg_init_kernel(T* P, const T* R, int64_t ld, int64_t n, int s,
                                ColState cs, double* part, SolveCtrl* ctrl) {
   __shared__ Red red;
   ROWS_OF_BLOCK
@@ -163,6 +165,7 @@ __global__ void cg_init_kernel(float* P, const float* R, int64_t ld, int64_t n, 
 
 // P = R for active columns, 0 otherwise (separate pass: needs conv flags).
 // P's tf32 hi / lo planes (HvParams::vplanes) written with P, bitwise hv_tc's split.
+__device__ __forceinline__ void put_planes(float*, int64_t, int64_t, double) {}  // fp64 CG: no planes
 __device__ __forceinline__ void put_planes(float* pp, int64_t e, int64_t plane, float v) {
   if (!pp) return;
   const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
@@ -170,17 +173,19 @@ __device__ __forceinline__ void put_planes(float* pp, int64_t e, int64_t plane, 
   pp[e + plane] = v - hi;
 }
 
-__global__ void cg_seed_direction_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
+template <class T>
+__global__ void cg_seed_direction_kernel(T* P, const T* R, int64_t ld, int64_t n, int s,
                                          const int* conv, float* pp) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (i >= n) return;
-  const float v = conv[c] ? 0.f : R[i + c * ld];
+  const T v = conv[c] ? T(0) : R[i + c * ld];
   P[i + c * ld] = v;
   put_planes(pp, i + c * ld, static_cast<int64_t>(s) * ld, v);
 }
 
-__global__ void cg_alpha_kernel(const float* P, const float* HP, int64_t ld, int64_t n, int s,
+template <class T>
+__global__ void cg_alpha_kernel(const T* P, const T* HP, int64_t ld, int64_t n, int s,
                                 ColState cs, double* part, SolveCtrl* ctrl) {
   if (ctrl->done) return;
   __shared__ Red red;
@@ -247,7 +252,11 @@ __device__ void beta_epilogue(int s, ColState cs, const double* tot, SolveCtrl* 
   }
 }
 
-__global__ void cg_update_kernel(float* X, float* R, const float* P, const float* HP, int64_t ld,
+__device__ __forceinline__ float axpy(double a, float x, float y) { return fmaf(static_cast<float>(a), x, y); }
+__device__ __forceinline__ double axpy(double a, double x, double y) { return fma(a, x, y); }
+
+template <class T>
+__global__ void cg_update_kernel(T* X, T* R, const T* P, const T* HP, int64_t ld,
                                  int64_t n, int s, ColState cs, double* part, SolveCtrl* ctrl,
                                  int refresh) {
   if (ctrl->done) return;
@@ -255,10 +264,10 @@ __global__ void cg_update_kernel(float* X, float* R, const float* P, const float
   ROWS_OF_BLOCK
   cols4(s, rb, re, ld, red, [&](int c, int64_t e) {
     if (cs.conv[c]) return 0.0;
-    const float a = static_cast<float>(cs.alpha[c]);
-    X[e] = fmaf(a, P[e], X[e]);
+    const double a = cs.alpha[c];
+    X[e] = axpy(a, P[e], X[e]);
     if (refresh) return 0.0;
-    const float r = fmaf(-a, HP[e], R[e]);
+    const T r = axpy(-a, HP[e], R[e]);
     R[e] = r;
     return static_cast<double>(r) * r;
   });
@@ -267,14 +276,15 @@ __global__ void cg_update_kernel(float* X, float* R, const float* P, const float
   beta_epilogue(s, cs, red.v[0], ctrl);
 }
 
-__global__ void cg_refresh_norm_kernel(float* R, const float* Rtmp, int64_t ld, int64_t n, int s,
+template <class T>
+__global__ void cg_refresh_norm_kernel(T* R, const T* Rtmp, int64_t ld, int64_t n, int s,
                                        ColState cs, double* part, SolveCtrl* ctrl) {
   if (ctrl->done) return;
   __shared__ Red red;
   ROWS_OF_BLOCK
   cols4(s, rb, re, ld, red, [&](int c, int64_t e) {
     if (cs.conv[c]) return 0.0;
-    const float r = Rtmp[e];
+    const T r = Rtmp[e];
     R[e] = r;
     return static_cast<double>(r) * r;
   });
@@ -282,7 +292,8 @@ __global__ void cg_refresh_norm_kernel(float* R, const float* Rtmp, int64_t ld, 
   beta_epilogue(s, cs, red.v[0], ctrl, true);
 }
 
-__global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_t n, int s,
+template <class T>
+__global__ void cg_direction_kernel(T* P, const T* R, int64_t ld, int64_t n, int s,
                                     ColState cs, double* part, SolveCtrl* ctrl, float* pp) {
   if (ctrl->done) return;
   ROWS_OF_BLOCK
@@ -294,7 +305,7 @@ __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_
         const int st = cs.conv[c];
         if (st == 1 || st == 3) continue;
         const int64_t e = i + c * ld;
-        const float v = st == 2 ? 0.f : fmaf(static_cast<float>(cs.beta[c]), P[e], R[e]);
+        const T v = st == 2 ? T(0) : axpy(cs.beta[c], P[e], R[e]);
         P[e] = v;
         put_planes(pp, e, static_cast<int64_t>(s) * ld, v);  // skipped columns keep P and its planes
       }
@@ -318,7 +329,8 @@ __global__ void cg_direction_kernel(float* P, const float* R, int64_t ld, int64_
 // (measured: relative residual 7e10 after 5000 iterations at tol 1e-6), so a
 // column whose exact residual has not improved for three refreshes (or grew
 // 1e4x past its best) is restored to its best iterate and frozen.
-__global__ void cg_snapshot_kernel(float* X, float* R, float* Xb, float* Rb, int64_t ld, int64_t n, int s,
+template <class T>
+__global__ void cg_snapshot_kernel(T* X, T* R, T* Xb, T* Rb, int64_t ld, int64_t n, int s,
                                    ColState cs, const SolveCtrl* ctrl, int at_start) {
   if (!at_start && ctrl->done) return;
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -525,21 +537,24 @@ void check_s(int s) {
 
 }  // namespace
 
-void cg_snapshot(float* X, float* R, float* Xb, float* Rb, int64_t ld, int64_t n, int s, ColState cs,
+template <class T>
+void cg_snapshot(T* X, T* R, T* Xb, T* Rb, int64_t ld, int64_t n, int s, ColState cs,
                  const SolveCtrl* ctrl, bool at_start, cudaStream_t st) {
   cg_snapshot_kernel<<<dim3(static_cast<unsigned>(ceil_div(n, NT)), s), NT, 0, st>>>(X, R, Xb, Rb, ld, n, s, cs,
                                                                                      ctrl, at_start ? 1 : 0);
   WGP_LAUNCH_CHECK();
 }
 
-void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, double* part,
+template <class T>
+void col_dots(const T* A, const T* B, int64_t ld, int64_t n, int s, double* part,
               unsigned* ticket, double* out, cudaStream_t st) {
   check_s(s);
   col_dots_kernel<<<cgrid(n, s), NT, 0, st>>>(A, B, ld, n, s, part, ticket, out);
   WGP_LAUNCH_CHECK();
 }
 
-void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
+template <class T>
+void cg_init(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
              SolveCtrl* ctrl, cudaStream_t st, float* pp) {
   check_s(s);
   cg_init_kernel<<<cgrid(n, s), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
@@ -548,28 +563,76 @@ void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs
   WGP_LAUNCH_CHECK();
 }
 
-void cg_alpha(const float* P, const float* HP, int64_t ld, int64_t n, int s, ColState cs,
+template <class T>
+void cg_alpha(const T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs,
               double* part, SolveCtrl* ctrl, cudaStream_t st) {
   cg_alpha_kernel<<<cgrid(n, s), NT, 0, st>>>(P, HP, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
 }
 
-void cg_update(float* X, float* R, const float* P, const float* HP, int64_t ld, int64_t n, int s,
+template <class T>
+void cg_update(T* X, T* R, const T* P, const T* HP, int64_t ld, int64_t n, int s,
                ColState cs, double* part, SolveCtrl* ctrl, bool refresh, cudaStream_t st) {
   cg_update_kernel<<<cgrid(n, s), NT, 0, st>>>(X, R, P, HP, ld, n, s, cs, part, ctrl,
                                                     refresh ? 1 : 0);
   WGP_LAUNCH_CHECK();
 }
 
-void cg_refresh_norm(float* R, const float* Rtmp, int64_t ld, int64_t n, int s, ColState cs,
+template <class T>
+void cg_refresh_norm(T* R, const T* Rtmp, int64_t ld, int64_t n, int s, ColState cs,
                      double* part, SolveCtrl* ctrl, cudaStream_t st) {
   cg_refresh_norm_kernel<<<cgrid(n, s), NT, 0, st>>>(R, Rtmp, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
 }
 
-void cg_direction(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs,
+template <class T>
+void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
                   double* part, SolveCtrl* ctrl, cudaStream_t st, float* pp) {
   cg_direction_kernel<<<cgrid(n, s), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl, pp);
+  WGP_LAUNCH_CHECK();
+}
+
+#define WGP_CG_INSTANTIATE(T)                                                                                  \
+  template void cg_snapshot<T>(T*, T*, T*, T*, int64_t, int64_t, int, ColState, const SolveCtrl*, bool,     \
+                               cudaStream_t);                                                                \
+  template void col_dots<T>(const T*, const T*, int64_t, int64_t, int, double*, unsigned*, double*,         \
+                            cudaStream_t);                                                                   \
+  template void cg_init<T>(T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*, cudaStream_t, \
+                           float*);                                                                          \
+  template void cg_alpha<T>(const T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,       \
+                            cudaStream_t);                                                                   \
+  template void cg_update<T>(T*, T*, const T*, const T*, int64_t, int64_t, int, ColState, double*,          \
+                             SolveCtrl*, bool, cudaStream_t);                                                \
+  template void cg_refresh_norm<T>(T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,      \
+                                   cudaStream_t);                                                            \
+  template void cg_direction<T>(T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,         \
+                                cudaStream_t, float*);
+WGP_CG_INSTANTIATE(float)
+WGP_CG_INSTANTIATE(double)
+#undef WGP_CG_INSTANTIATE
+
+__global__ void widen_kernel(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) B[i + blockIdx.y * ldb] = A[i + blockIdx.y * lda];
+}
+__global__ void narrow_kernel(const double* A, int64_t lda, float* B, int64_t ldb, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) B[i + blockIdx.y * ldb] = static_cast<float>(A[i + blockIdx.y * lda]);
+}
+__global__ void axpy_cols_kernel(double a, const double* X, double* Y, int64_t ld, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) Y[i + blockIdx.y * ld] = fma(a, X[i + blockIdx.y * ld], Y[i + blockIdx.y * ld]);
+}
+void axpy_cols(double a, const double* X, double* Y, int64_t ld, int64_t n, int s, cudaStream_t st) {
+  axpy_cols_kernel<<<grid2(n, s), NT, 0, st>>>(a, X, Y, ld, n);
+  WGP_LAUNCH_CHECK();
+}
+void widen(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n, int s, cudaStream_t st) {
+  widen_kernel<<<grid2(n, s), NT, 0, st>>>(A, lda, B, ldb, n);
+  WGP_LAUNCH_CHECK();
+}
+void narrow(const double* A, int64_t lda, float* B, int64_t ldb, int64_t n, int s, cudaStream_t st) {
+  narrow_kernel<<<grid2(n, s), NT, 0, st>>>(A, lda, B, ldb, n);
   WGP_LAUNCH_CHECK();
 }
 

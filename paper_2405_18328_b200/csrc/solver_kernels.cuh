@@ -49,32 +49,46 @@ __host__ __device__ inline int64_t rows_per_block(int64_t n) {
 }
 inline int reduce_blocks(int64_t n) { return static_cast<int>((n + rows_per_block(n) - 1) / rows_per_block(n)); }
 
+// The CG kernels run on fp32 (the tf32 engines' solver state) or fp64 vectors
+// (the fp64 CG path over hv_f64); scalars are fp64 either way.
 // out[c] = sum_i A[i,c] * B[i,c]  (fp64, fixed order), all columns.
-void col_dots(const float* A, const float* B, int64_t ld, int64_t n, int s, double* part,
+template <class T>
+void col_dots(const T* A, const T* B, int64_t ld, int64_t n, int s, double* part,
               unsigned* ticket, double* out, cudaStream_t st);
 
 // CG: before the loop.  R = rhs - H X0 must already be in R; computes
 // rs = ||r||^2, convergence, P = R (active) / 0, and the loop-entry check.
-// pp (optional, here and in cg_direction): P's tf32 planes, written with P
-// (hi at pp[j + c ld], lo at pp[j + (s + c) ld]; for HvParams::vplanes).
-void cg_init(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
+// pp (optional, fp32 only, here and in cg_direction): P's tf32 planes, written
+// with P (hi at pp[j + c ld], lo at pp[j + (s + c) ld]; for HvParams::vplanes).
+template <class T>
+void cg_init(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
              SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
 // alpha_c = rs_c / (p_c . hp_c); non-positive curvature -> kStatusNotPd.
-void cg_alpha(const float* P, const float* HP, int64_t ld, int64_t n, int s, ColState cs,
+template <class T>
+void cg_alpha(const T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs,
               double* part, SolveCtrl* ctrl, cudaStream_t st);
 // x += alpha p; r -= alpha hp (refresh=false) or x += alpha p only (refresh=true).
-void cg_update(float* X, float* R, const float* P, const float* HP, int64_t ld, int64_t n, int s,
+template <class T>
+void cg_update(T* X, T* R, const T* P, const T* HP, int64_t ld, int64_t n, int s,
                ColState cs, double* part, SolveCtrl* ctrl, bool refresh, cudaStream_t st);
 // refresh: r = rtmp for active columns; then ||r||^2, convergence, beta.
-void cg_refresh_norm(float* R, const float* Rtmp, int64_t ld, int64_t n, int s, ColState cs,
+template <class T>
+void cg_refresh_norm(T* R, const T* Rtmp, int64_t ld, int64_t n, int s, ColState cs,
                      double* part, SolveCtrl* ctrl, cudaStream_t st);
 // Refresh steps: per column, act 1 copies X, R -> Xb, Rb (new best iterate),
 // act 2 copies Xb, Rb -> X, R (stalled column restored to its best).
-void cg_snapshot(float* X, float* R, float* Xb, float* Rb, int64_t ld, int64_t n, int s, ColState cs,
+template <class T>
+void cg_snapshot(T* X, T* R, T* Xb, T* Rb, int64_t ld, int64_t n, int s, ColState cs,
                  const SolveCtrl* ctrl, bool at_start, cudaStream_t st);
 // p = r + beta p (active) / 0 (just converged); then the next-iteration check.
-void cg_direction(float* P, const float* R, int64_t ld, int64_t n, int s, ColState cs,
+template <class T>
+void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
                   double* part, SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
+// B = A (fp32 -> fp64) / B = A rounded to fp32, n x s column blocks.
+void widen(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n, int s, cudaStream_t st);
+// Y += a X (fp64, n x s column blocks, leading dimension ld).
+void axpy_cols(double a, const double* X, double* Y, int64_t ld, int64_t n, int s, cudaStream_t st);
+void narrow(const double* A, int64_t lda, float* B, int64_t ldb, int64_t n, int s, cudaStream_t st);
 
 // Convergence from exact residual norms (AP epochs, SGD init): conv_c =
 // bnorm_c == 0 || ||R_c|| <= tol_c bnorm_c; NaN -> kStatusNaN (when check_nan);
