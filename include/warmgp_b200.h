@@ -195,6 +195,7 @@ typedef struct {
   double init_signal;     /* <= 0: init_constrained */
   int warm_start_distance;/* 1: compute the diagnostic (+1 H.V per warm step) */
   int exact_gradients;    /* 1: train_exact (optimizer.hpp:83-86): exact Cholesky gradient */
+  int record_solver_state;/* 1: fill wgp_trace::solver_init / solver_solutions (optimizer.hpp:35) */
 } wgp_train_cfg;
 
 /* StepRecord fields (proj/include/warmgp/optimizer.hpp:54-67), caller-owned,
@@ -210,6 +211,11 @@ typedef struct {
   double* solver_ms;           /* steps: device time of the solve */
   double* step_ms;             /* steps: device time of the whole outer step */
   float* final_solutions;      /* n x (num_probes + 1) */
+  double* warm_distance_ms;    /* steps: device time of the warm-start-distance H.V
+                                  (included in step_ms; step_ms - this = the step without it) */
+  float* solver_init;          /* steps x n x (num_probes + 1), with record_solver_state
+                                  (StepRecord::solver_init, optimizer.hpp:65) */
+  float* solver_solutions;     /* steps x n x (num_probes + 1) (StepRecord::solver_solutions, :66) */
 } wgp_trace;
 
 /** train(X, y, config) (proj/src/optimizer.cpp:175-177, run_loop :81-171):

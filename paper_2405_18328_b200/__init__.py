@@ -78,7 +78,7 @@ class _TrainCfg(C.Structure):
                 ("init_constrained", C.c_double), ("seed", C.c_uint64), ("transform", C.c_int),
                 ("estimator", C.c_int), ("rff_features", C.c_int), ("init_noise", C.c_double),
                 ("init_signal", C.c_double), ("warm_start_distance", C.c_int),
-                ("exact_gradients", C.c_int)]
+                ("exact_gradients", C.c_int), ("record_solver_state", C.c_int)]
 
 
 class _Trace(C.Structure):
@@ -88,7 +88,9 @@ class _Trace(C.Structure):
                 ("per_column_relative_residual", C.POINTER(C.c_double)),
                 ("warm_start_distance", C.POINTER(C.c_double)),
                 ("probe_seed", C.POINTER(C.c_uint64)), ("solver_ms", C.POINTER(C.c_double)),
-                ("step_ms", C.POINTER(C.c_double)), ("final_solutions", C.POINTER(C.c_float))]
+                ("step_ms", C.POINTER(C.c_double)), ("final_solutions", C.POINTER(C.c_float)),
+                ("warm_distance_ms", C.POINTER(C.c_double)), ("solver_init", C.POINTER(C.c_float)),
+                ("solver_solutions", C.POINTER(C.c_float))]
 
 
 EXPORTS = [
@@ -335,6 +337,7 @@ class TrainConfig:
     init_signal: float = 0.0
     warm_start_distance: bool = True
     exact_gradients: bool = False  # train_exact (optimizer.hpp:83-86)
+    record_solver_state: bool = False  # keep per-step init / solutions (optimizer.hpp:35)
 
     def validate(self):
         if self.steps < 1:
@@ -349,7 +352,8 @@ class TrainConfig:
                          _MODES[self.mode], self.solver._c(), self.init_constrained, self.seed,
                          _TRANSFORMS[self.transform], _ESTIMATORS[self.estimator],
                          self.rff_features, self.init_noise, self.init_signal,
-                         int(self.warm_start_distance), int(self.exact_gradients))
+                         int(self.warm_start_distance), int(self.exact_gradients),
+                         int(self.record_solver_state))
 
 
 @dataclass
@@ -365,6 +369,9 @@ class StepRecord:
     per_column_relative_residual: np.ndarray
     warm_start_distance: float
     probe_seed: int
+    warm_distance_ms: float = 0.0  # device time of the warm-start-distance H.V (inside step_ms)
+    solver_init: Optional[np.ndarray] = None       # with record_solver_state (optimizer.hpp:65)
+    solver_solutions: Optional[np.ndarray] = None  # (optimizer.hpp:66)
 
 
 @dataclass
@@ -378,6 +385,11 @@ class OptTrace:
 
     def total_solver_iterations(self, first=1, last=1 << 30):
         return sum(r.solver_iterations for r in self.steps if first <= r.step <= last)
+
+    def final_hyperparameters(self, input_dim, transform="softplus"):
+        """optimizer.cpp:67-70: the last step's parameters."""
+        c = np.asarray(self.steps[-1].constrained_params)
+        return Hyperparameters.from_constrained(c[:input_dim], c[input_dim], c[input_dim + 1], transform)
 
     def raw_params(self):
         return np.array([r.raw_params for r in self.steps])
@@ -626,17 +638,26 @@ class Context:
         arr = dict(raw=np.zeros((T, p)), con=np.zeros((T, p)), grad=np.zeros((T, p)),
                    it=np.zeros(T, dtype=np.int32), pcr=np.zeros((T, sp)), wsd=np.zeros(T),
                    seed=np.zeros(T, dtype=np.uint64), sms=np.zeros(T), tms=np.zeros(T),
-                   fin=np.zeros((self.n, sp), dtype=np.float32, order="F"))
+                   fin=np.zeros((self.n, sp), dtype=np.float32, order="F"), wms=np.zeros(T))
+        rec = config.record_solver_state
+        if rec:  # steps x (n x sp column-major)
+            arr["sinit"] = np.zeros((T, sp, self.n), dtype=np.float32)
+            arr["ssol"] = np.zeros((T, sp, self.n), dtype=np.float32)
         dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+        fp = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))
         tr = _Trace(dp(arr["raw"]), dp(arr["con"]), dp(arr["grad"]),
                     arr["it"].ctypes.data_as(C.POINTER(C.c_int)), dp(arr["pcr"]), dp(arr["wsd"]),
                     arr["seed"].ctypes.data_as(C.POINTER(C.c_uint64)), dp(arr["sms"]),
-                    dp(arr["tms"]), arr["fin"].ctypes.data_as(C.POINTER(C.c_float)))
+                    dp(arr["tms"]), fp(arr["fin"]), dp(arr["wms"]),
+                    fp(arr["sinit"]) if rec else None, fp(arr["ssol"]) if rec else None)
         cfg = config._c()
         _check(self._lib.wgp_train(self._h, _ptr(y), C.byref(cfg), C.byref(tr)))
         steps = [StepRecord(t + 1, arr["raw"][t].copy(), arr["con"][t].copy(), arr["grad"][t].copy(),
                             int(arr["it"][t]), float(arr["sms"][t]), float(arr["tms"][t]),
-                            arr["pcr"][t].copy(), float(arr["wsd"][t]), int(arr["seed"][t]))
+                            arr["pcr"][t].copy(), float(arr["wsd"][t]), int(arr["seed"][t]),
+                            float(arr["wms"][t]),
+                            arr["sinit"][t].T.copy(order="F") if rec else None,
+                            arr["ssol"][t].T.copy(order="F") if rec else None)
                  for t in range(T)]
         return OptTrace(steps, arr["fin"])
 

@@ -1216,9 +1216,10 @@ struct Ctx {
       prev64 = s64b.as<double>();
     }
     bool have_prev = false;
-    cudaEvent_t e0, e1, e2;
+    cudaEvent_t e0, e1, e1w, e2;
     WGP_CUDA(cudaEventCreate(&e0));
     WGP_CUDA(cudaEventCreate(&e1));
+    WGP_CUDA(cudaEventCreate(&e1w));
     WGP_CUDA(cudaEventCreate(&e2));
     try {
       for (int t = 1; t <= cfg.steps; ++t) {
@@ -1251,6 +1252,7 @@ struct Ctx {
               WGP_CUDA(cudaEventElapsedTime(&ms_b, e0, e2));
               if (tr->solver_ms) tr->solver_ms[t - 1] = ms_a;
               if (tr->step_ms) tr->step_ms[t - 1] = ms_b;
+              if (tr->warm_distance_ms) tr->warm_distance_ms[t - 1] = 0.0;
             }
             continue;
           }
@@ -1266,6 +1268,20 @@ struct Ctx {
           double wsd = 0.0;
           if (have_warm && cfg.warm_start_distance)
             wsd = keep64 ? warm_distance64(prev64, cur64, sp) : warm_distance(prev, cur, sp);
+          WGP_CUDA(cudaEventRecord(e1w, st));
+          if (tr && cfg.record_solver_state) {  // optimizer.cpp:148-151 (fp32 copies)
+            const size_t off = static_cast<size_t>(t - 1) * n * sp;
+            if (tr->solver_init) {
+              if (have_warm)
+                WGP_CUDA(cudaMemcpy2DAsync(tr->solver_init + off, sizeof(float) * n, prev, sizeof(float) * ld,
+                                           sizeof(float) * n, sp, cudaMemcpyDeviceToHost, st));
+              else
+                std::fill(tr->solver_init + off, tr->solver_init + off + static_cast<size_t>(n) * sp, 0.f);
+            }
+            if (tr->solver_solutions)
+              WGP_CUDA(cudaMemcpy2DAsync(tr->solver_solutions + off, sizeof(float) * n, cur, sizeof(float) * ld,
+                                         sizeof(float) * n, sp, cudaMemcpyDeviceToHost, st));
+          }
           std::vector<double> qa(p), qb(p), g(p);
           grad(T, raw.data(), cur, cur + ld, pathwise ? cur + ld : Z, s, 0.5 / s, qa.data(), qb.data());
           for (int k = 0; k < p; ++k) g[k] = qa[k] - qb[k];
@@ -1290,6 +1306,11 @@ struct Ctx {
             WGP_CUDA(cudaEventElapsedTime(&ms_step, e0, e2));
             if (tr->solver_ms) tr->solver_ms[t - 1] = ms_solve;
             if (tr->step_ms) tr->step_ms[t - 1] = ms_step;
+            if (tr->warm_distance_ms) {
+              float ms_w = 0.f;
+              WGP_CUDA(cudaEventElapsedTime(&ms_w, e1, e1w));
+              tr->warm_distance_ms[t - 1] = ms_w;
+            }
           }
           std::swap(cur, prev);
           std::swap(cur64, prev64);
@@ -1305,14 +1326,10 @@ struct Ctx {
         WGP_CUDA(cudaStreamSynchronize(st));
       }
     } catch (...) {
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
-      cudaEventDestroy(e2);
+      for (cudaEvent_t e : {e0, e1, e1w, e2}) cudaEventDestroy(e);
       throw;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
+    for (cudaEvent_t e : {e0, e1, e1w, e2}) cudaEventDestroy(e);
   }
 
   static void adam(double* raw, const double* g, double* m, double* v, int p, int t, double lr,

@@ -7,6 +7,22 @@
 
 #include "warmgp_b200.hpp"
 
+// Minimal stand-in for Eigen::MatrixXd / VectorXd (Eigen is not in this
+// image): column-major doubles with rows(), cols(), data() and (r, c)
+// construction -- the surface the adapter's fp64 entry points use.
+struct MatrixXd {
+  long r = 0, c = 0;
+  std::vector<double> v;
+  MatrixXd() = default;
+  MatrixXd(long rows, long cols) : r(rows), c(cols), v(static_cast<size_t>(rows * cols)) {}
+  long rows() const { return r; }
+  long cols() const { return c; }
+  double* data() { return v.data(); }
+  const double* data() const { return v.data(); }
+  double& operator()(long i, long j) { return v[static_cast<size_t>(i + j * r)]; }
+  double operator()(long i, long j) const { return v[static_cast<size_t>(i + j * r)]; }
+};
+
 int main() {
   try {
     const int n = 600, d = 3, s = 4;
@@ -63,6 +79,59 @@ int main() {
       warmgp::solve(H, rhs, s, warmgp::SolverConfig{});
       return 1;
     } catch (const std::invalid_argument&) {
+    }
+    // the reference's own signatures on fp64 matrices (solvers.hpp:50-55,
+    // optimizer.hpp:81): solve(H, rhs, init, config), train(X, y, config)
+    MatrixXd Xd(n, d), Bd(n, s), yd(n, 1);
+    for (long e = 0; e < n * d; ++e) Xd.v[e] = X[e];
+    for (long e = 0; e < n * s; ++e) Bd.v[e] = normal(rng);
+    for (long e = 0; e < n; ++e) yd.v[e] = y[e];
+    warmgp::KernelOperator H64(dev, Xd, {1.0, 0.8, 1.3, 1.1, 0.5});
+    warmgp::SolverConfig c64;
+    c64.tol_mean = c64.tol_samples = 1e-6;
+    c64.max_iterations = 5000;
+    const warmgp::SolveStateT<MatrixXd> s64 = warmgp::solve(H64, Bd, c64);
+    if (!s64.all_converged() || s64.solutions.rows() != n || s64.solutions.cols() != s) return 1;
+    // the fp64 operator reproduces rhs from the fp64 solutions to the tolerance
+    const MatrixXd HX = H64.apply(s64.solutions);
+    for (int j = 0; j < s; ++j) {
+      double num = 0, den = 0;
+      for (long i = 0; i < n; ++i) {
+        num += (Bd(i, j) - HX(i, j)) * (Bd(i, j) - HX(i, j));
+        den += Bd(i, j) * Bd(i, j);
+      }
+      if (std::sqrt(num / den) > 1.01e-6) return 1;
+    }
+    const warmgp::SolveStateT<MatrixXd> w64 = warmgp::solve(H64, Bd, s64.solutions, c64);
+    if (w64.iterations_used != 0) return 1;
+    warmgp::TrainConfig rc;
+    rc.steps = 4;
+    rc.num_probes = 3;
+    rc.record_solver_state = true;
+    const warmgp::OptTrace tw = warmgp::train(Xd, yd, rc);
+    // optimizer_test.cpp:113-124: warm init of step t = solutions of step t-1, zero at step 1
+    for (float v : tw.steps[0].solver_init)
+      if (v != 0.f) return 1;
+    for (int t = 1; t < rc.steps; ++t)
+      if (tw.steps[t].solver_init != tw.steps[t - 1].solver_solutions) return 1;
+    rc.mode = warmgp::TrainMode::ColdStartFixedProbes;  // :130-134: cold init is zero every step
+    const warmgp::OptTrace tc0 = warmgp::train(Xd, yd, rc);
+    for (const auto& r : tc0.steps)
+      for (float v : r.solver_init)
+        if (v != 0.f) return 1;
+    const warmgp::Hyperparameters fh = tw.final_hyperparameters(d);
+    if (fh.input_dim() != d || fh.noise_scale() != tw.back().constrained_params[d + 1]) return 1;
+    if (tw.total_solver_iterations() != tw.total_solver_iterations(1, rc.steps) ||
+        tw.total_solver_iterations(2, 3) != tw.steps[1].solver_iterations + tw.steps[2].solver_iterations)
+      return 1;
+    std::printf("fp64 solve: %d iterations; train(X, y, config): noise %.4f, %ld iterations\n", s64.iterations_used,
+                fh.noise_scale(), tw.total_solver_iterations());
+    // shape errors are std::invalid_argument with the reference's messages
+    try {
+      warmgp::solve(H64, MatrixXd(n - 1, s), c64);
+      return 1;
+    } catch (const std::invalid_argument& e) {
+      if (std::string(e.what()) != "solve: rhs row count mismatch") return 1;
     }
     std::printf("adapter ok\n");
     return 0;

@@ -740,3 +740,26 @@ def test_solve_f64_boundary(ctx):
     assert ap.all_converged()
     with pytest.raises(ValueError, match="row count mismatch"):
         ctx.solve_f64(rhs[:10].astype(np.float64), cfg)
+
+
+@pytest.mark.parametrize("kind", ["cg", "ap"])
+def test_record_solver_state_warm_chaining(ctx, kind):
+    """optimizer_test.cpp:113-135: with record_solver_state, a warm step's init
+    is the previous step's solutions (bitwise), the first init is zero, and in
+    cold mode every init is zero; final_hyperparameters / total_solver_iterations
+    (optimizer.cpp:67-78) read the trace."""
+    p = datasets.config0(n=400, d=3)
+    ctx.set_data(p.X)
+    sc = wg.SolverConfig(kind=kind, tol_mean=1e-3, tol_samples=1e-3, block_size=100, max_iterations=2000)
+    cfg = wg.TrainConfig(steps=4, num_probes=3, record_solver_state=True, solver=sc)
+    tr = ctx.train(p.y, cfg)
+    assert np.all(tr.steps[0].solver_init == 0)
+    for t in range(1, 4):
+        assert np.array_equal(tr.steps[t].solver_init, tr.steps[t - 1].solver_solutions)
+    assert np.array_equal(tr.steps[-1].solver_solutions, tr.final_solutions)
+    cfg.mode = "cold-fixed"
+    tc = ctx.train(p.y, cfg)
+    assert all(np.all(r.solver_init == 0) for r in tc.steps)
+    h = tr.final_hyperparameters(3)
+    assert np.allclose(h.to_constrained_vector(), tr.steps[-1].constrained_params)
+    assert tr.total_solver_iterations(2, 3) == tr.steps[1].solver_iterations + tr.steps[2].solver_iterations
