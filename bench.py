@@ -47,7 +47,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--outer", action="store_true",
-                    help="also time outer steps (row-sharded over the ranks under torchrun)")
+                    help="legacy torch-driven row-sharded outer steps under torchrun")
+    ap.add_argument("--no-outer", action="store_true", help="skip the per-outer-step timings")
+    ap.add_argument("--no-c3", action="store_true", help="skip the config-3 outer steps")
+    ap.add_argument("--outer-steps", type=int, default=5, help="timed outer steps per solver (config 2)")
+    ap.add_argument("--outer-warmup", type=int, default=1, help="untimed outer steps before them")
     ap.add_argument("--outer-config", type=int, default=2, choices=[2, 3],
                     help="BASELINE config of --outer: 2 (CG / AP / SGD) or 3 (AP, 10-epoch budget)")
     return ap.parse_args()
@@ -136,15 +140,9 @@ def cpu_baseline(p, seconds):
 
 
 def outer_spec(datasets, args, sharded_run=False):
-    """The outer-loop workload of `--outer-config`:
-    2: BASELINE config 2 (n=41,157, d=9, 64 pathwise probes + y, 1000 RFF
-       features, log-space Adam lr 0.1, warm start) with CG (tol 0.01), AP
-       (blocks of 1000) and SGD (minibatch 1000, momentum 0.9), `steps` timed
-       steps after `warmup`;
-    3: BASELINE config 3 (n=391,386, d=3, s=65, AP blocks of 1000 with a
-       budget of 10 epochs per outer step, warm start): ~10 s per step on one
-       GPU, so at most 3 timed steps after 1 warm-up step.
-    Returns (problem, workload, solvers, timed steps, warm-up steps)."""
+    """The outer-loop workload of `--outer-config` (legacy torch-driven sharded
+    run, `--outer` under torchrun): 2 = BASELINE config 2 with CG and AP,
+    3 = config 3 with AP and a 10-epoch budget."""
     if args.outer_config == 3:
         p = datasets.config3()
         solvers = {"ap": dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=10, block_size=1000)}
@@ -155,40 +153,138 @@ def outer_spec(datasets, args, sharded_run=False):
         "cg": dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=1000),
         "ap": dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=100, block_size=1000),
     }
-    if not sharded_run:
-        solvers["sgd"] = dict(kind="sgd", tol_mean=0.01, tol_samples=0.01, max_iterations=3000,
-                              minibatch_size=1000, momentum=0.9, learning_rate=10.0)
     return (p, "config2 n=41157 d=9 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start", solvers,
             max(args.steps, 1), args.warmup)
 
 
-def outer_steps(wg, datasets, device, args):
-    """The `--outer-config` outer loop on one GPU (outer_spec): device time
-    per outer step (solve + gradient + probes, from the library's per-step
-    CUDA events) per solver."""
-    p, workload, solvers, k_steps, w_steps = outer_spec(datasets, args)
-    n_steps = w_steps + k_steps
-    out = {"workload": workload,
-           "timing": "CUDA events on the context stream around each outer step (device time)",
-           "steps": k_steps, "warmup_steps": w_steps}
-    for name, sc in solvers.items():
-        ctx = wg.Context(device, hv_impl=args.hv_impl)
-        ctx.set_data(p.X)
-        cfg = wg.TrainConfig(steps=n_steps, learning_rate=0.1, num_probes=64, mode="warm", seed=0,
-                             transform="log", estimator="pathwise", rff_features=1000, init_noise=0.5,
-                             init_constrained=1.0, warm_start_distance=False,
-                             solver=wg.SolverConfig(**sc))
+def sgd_learning_rate(wg, ds_X, ds_y, device):
+    """The reference's grid search (proj/src/experiment.cpp:133-168, default
+    candidates and budget proj/tools/main.cpp:53-54) at config 2's start."""
+    from paper_2405_18328_b200 import experiment as ex
+
+    ds = ex.Dataset("c2", ds_X, ds_y)
+    base = wg.TrainConfig(init_constrained=1.0, seed=0,
+                          solver=wg.SolverConfig(kind="sgd", minibatch_size=1000, momentum=0.9))
+    cands = [1.0, 3.0, 10.0, 30.0, 100.0, 300.0]
+    t0 = time.perf_counter()
+    lr = ex.grid_search_sgd_lr(ds, cands, 60, base, device=device)
+    return lr, {"candidates": cands, "budget_steps": 60, "chosen": lr, "seconds": time.perf_counter() - t0}
+
+
+def run_outer(wg, ctx, p, sc, steps, warmup, precision="f64"):
+    """One warm-started training run on the device; per-step device times of
+    the timed steps (CUDA events around each outer step: probes, solve,
+    warm-start-distance H.V, gradient, Adam) and what the solver did."""
+    ctx.set_cg_precision(precision)
+    cfg = wg.TrainConfig(steps=warmup + steps, learning_rate=0.1, num_probes=64, mode="warm", seed=0,
+                         transform="log", estimator="pathwise", rff_features=1000, init_noise=0.5,
+                         init_constrained=1.0, warm_start_distance=True, solver=wg.SolverConfig(**sc))
+    tr = ctx.train(p.y, cfg)
+    timed = tr.steps[warmup:]
+    tol = np.array([sc["tol_mean"]] + [sc["tol_samples"]] * 64)
+    conv = [bool(np.all(r.per_column_relative_residual <= tol * (1 + 1e-9))) for r in timed]
+    step = np.array([r.step_ms for r in timed])
+    wsd = np.array([r.warm_distance_ms for r in timed])
+    return {"ms_per_step": float(step.mean()),
+            "ms_per_step_without_warm_start_distance": float((step - wsd).mean()),
+            "solver_ms_per_step": float(np.mean([r.solver_ms for r in timed])),
+            "iterations": [int(r.solver_iterations) for r in timed],
+            "iterations_mean": float(np.mean([r.solver_iterations for r in timed])),
+            "converged_steps": f"{sum(conv)}/{len(conv)}",
+            "max_final_relative_residual": float(max(r.per_column_relative_residual.max() for r in timed)),
+            "cg_precision": precision if sc["kind"] == "cg" else None,
+            "config": {k: v for k, v in sc.items() if k != "kind"}}
+
+
+def outer_bench(wg, datasets, device, args):
+    """ms per marginal-likelihood step (the second half of BASELINE.json's
+    metric) on one GPU through the library's wgp_train:
+      config 2 (n=41,157, d=9, 64 pathwise probes + y, RFF 1000, log-space
+      Adam lr 0.1, warm start): CG (tol 0.01, fp64 and fp32), AP (blocks of
+      1000, tol 0.01), SGD (minibatch 1000, momentum 0.9, tol 0.01, learning
+      rate from the reference's grid search), reference default iteration caps
+      (solvers.cpp:88,148,206);
+      config 3 (n=391,386, d=3): AP, blocks of 1000, 10-epoch budget.
+    Each run starts cold at step 1; `outer_warmup` steps are untimed, the
+    next `outer_steps` are timed."""
+    out = {"timing": "CUDA events on the context stream around each outer step (device time; the "
+                     "warm-start-distance H.V included, and subtracted in the *_without_* field)",
+           "steps_timed": args.outer_steps, "warmup_steps": args.outer_warmup}
+    p = datasets.config2()
+    ctx = wg.Context(device, hv_impl=args.hv_impl)
+    ctx.set_data(p.X)
+    c2 = {"workload": "config2 n=41157 d=9 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start"}
+    runs = [("cg_f64", dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=0), "f64"),
+            ("cg_f32", dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=0), "f32"),
+            ("ap", dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=0, block_size=1000), "f64")]
+    try:
+        lr, grid = sgd_learning_rate(wg, p.X, p.y, device)
+        runs.append(("sgd", dict(kind="sgd", tol_mean=0.01, tol_samples=0.01, max_iterations=0,
+                                 minibatch_size=1000, momentum=0.9, learning_rate=lr, seed=0), "f64"))
+        c2["sgd_lr_grid_search"] = grid
+    except Exception as e:
+        c2["sgd_lr_grid_search"] = {"error": str(e)[:200]}
+    for name, sc, prec in runs:
         try:
-            tr = ctx.train(p.y, cfg)
-            timed = tr.steps[w_steps:]
-            out[name] = {"ms_per_step": float(np.mean([r.step_ms for r in timed])),
-                         "solver_ms_per_step": float(np.mean([r.solver_ms for r in timed])),
-                         "iterations_mean": float(np.mean([r.solver_iterations for r in timed])),
-                         "config": {k: v for k, v in sc.items() if k != "kind"}}
+            c2[name] = run_outer(wg, ctx, p, sc, args.outer_steps, args.outer_warmup, prec)
         except Exception as e:  # report, keep the other solvers' numbers
-            out[name] = {"error": str(e)[:200]}
+            c2[name] = {"error": str(e)[:200]}
+    ctx.close()
+    out["c2"] = c2
+    if not args.no_c3:
+        p3 = datasets.config3()
+        ctx = wg.Context(device, hv_impl=args.hv_impl)
+        ctx.set_data(p3.X)
+        c3 = {"workload": "config3 n=391386 d=3 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start, "
+                          "AP blocks of 1000 with a 10-epoch budget"}
+        try:
+            c3["ap"] = run_outer(wg, ctx, p3, dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=10,
+                                                   block_size=1000), min(args.outer_steps, 2), 1)
+        except Exception as e:
+            c3["ap"] = {"error": str(e)[:200]}
         ctx.close()
+        out["c3"] = c3
     return out
+
+
+def cpu_outer_baseline(datasets, outer, seconds):
+    """The reference's CPU path for outer steps:
+    config 0's whole 20-step training run by the fp64 oracle (timed), and a
+    config-2 CG step extrapolated from a timed oracle fp64 H.V row sample x
+    the H.V products the step needs (iterations + 2, the iteration count of
+    the fp64 device run, which matches the reference's)."""
+    from oracle import oracle as orc
+
+    res = {"cores": os.cpu_count(), "kind": "port"}
+    p0 = datasets.config0()
+    cfg = orc.TrainConfig(steps=20, learning_rate=0.1, num_probes=16, mode="warm", seed=0, transform="log",
+                          estimator="pathwise", rff_features=1000, init_noise=0.5, init_constrained=1.0,
+                          solver=orc.SolverConfig(kind="cg", tol_mean=0.01, tol_samples=0.01,
+                                                  max_iterations=1000))
+    t0 = time.perf_counter()
+    o = orc.train(p0.X, p0.y, cfg)
+    dt = time.perf_counter() - t0
+    res["c0_train"] = {"ms_per_step": 1e3 * dt / 20, "seconds": dt, "iterations_total": int(o["solver_iterations"].sum()),
+                       "sample": "oracle fp64 train, BASELINE config 0, 20 steps (timed)"}
+    p2 = datasets.config2()
+    n = p2.X.shape[0]
+    V = np.random.default_rng(0).standard_normal((n, 65))
+    rows, el = 64, 0.0
+    while True:
+        t0 = time.perf_counter()
+        orc.hv_rows(p2.X, p2.lengthscales, p2.signal, p2.noise, V, 0, rows)
+        el = time.perf_counter() - t0
+        if el >= seconds / 4 or rows >= n:
+            break
+        rows = min(n, rows * 4)
+    rate = rows * n / el
+    cg = (outer or {}).get("c2", {}).get("cg_f64", {})
+    it = cg.get("iterations_mean")
+    if it:
+        res["c2_cg_step"] = {"ms_per_step": 1e3 * (it + 2) * n * n / rate, "extrapolated": True,
+                             "sample": f"oracle fp64 H.V rows 0..{rows} x {n} points, s=65 ({el:.1f} s), "
+                                       f"x {it + 2:.1f} H.V per step (device fp64 CG iterations + 2)"}
+    return res
 
 
 def outer_sharded(wg, datasets, device, args, ws, rank):
@@ -255,6 +351,22 @@ def run_reference(args):
             times.append(dt)
     ms = 1e3 * float(np.mean(times))
     value = n * n / (ms / 1e3)
+    # the reference itself is single-threaded Eigen (no OpenMP,
+    # proj/src/CMakeLists.txt:14): the same GEMM on one core, on a row block
+    single = None
+    try:
+        from threadpoolctl import threadpool_limits
+        rows = 2000
+        with threadpool_limits(limits=1):
+            Hb = np.asfortranarray(H[:rows])
+            Hb @ V
+            t0 = time.perf_counter()
+            Hb @ V
+            dt1 = time.perf_counter() - t0
+        single = {"value": rows * n / dt1, "unit": UNIT, "cores": 1, "kind": "port",
+                  "sample": f"dense fp64 H[0:{rows}, :] @ V (n={n}, s=65), one BLAS thread, {dt1:.2f} s"}
+    except Exception as e:
+        single = {"error": str(e)[:200]}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -266,6 +378,11 @@ def run_reference(args):
                          "sample": "full config-1 dense H.V per step (H built once, "
                                    f"{build_s:.1f} s, outside the timed region)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("a LOWER BOUND on the reference's time per H.V: multi-threaded BLAS on all host cores "
+                 "stands in for the reference's single-threaded Eigen GEMM, and the dense H is built once "
+                 "outside the timed region (the reference rebuilds it every outer step, "
+                 "proj/src/optimizer.cpp:121)"),
+        "single_thread": single,
     }
     print(json.dumps(line), flush=True)
 
@@ -316,6 +433,11 @@ def main():
                 chunk[:, :m] = out_local[:, :m]
                 dist.all_gather_into_tensor(gathered, chunk)
 
+    # clocks are sampled from the warm-up through the timed H.V steps and the
+    # outer-step timings (a 20-step H.V region lasts ~5 ms, shorter than one
+    # nvidia-smi sample); reported per phase
+    clk = ClockSampler(local)
+    clk.__enter__()
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             one_step()
@@ -328,13 +450,14 @@ def main():
         launches0 = wg.launch_count()
         if args.hv_impl != "simt":
             ctx.profile(True)
-        with ClockSampler(local) as clk:
-            for a, b in evs:
-                flush.zero_()
-                a.record(stream)
-                one_step()
-                b.record(stream)
-            stream.synchronize()
+        n_samples0 = len(clk.samples)
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            one_step()
+            b.record(stream)
+        stream.synchronize()
+        hv_samples = len(clk.samples) - n_samples0
     launches = wg.launch_count() - launches0
     kernel_ms, kernel_launches = ctx.profile_read() if args.hv_impl != "simt" else (0.0, 0)
     ctx.profile(False)
@@ -377,6 +500,10 @@ def main():
 
     # multi-GPU outer steps run on every rank (collectives), before rank 0 reports
     outer_multi = outer_sharded(wg, datasets, local, args, ws, rank) if (args.outer and ws > 1) else None
+    outer = None
+    if ws == 1 and not args.no_outer:
+        outer = outer_bench(wg, datasets, local, args)
+    clk.__exit__()
     if rank != 0:
         if ws > 1:
             dist.barrier()
@@ -384,38 +511,44 @@ def main():
         return
     pk = peaks()
     clocks = clk.summary()
+    clocks["samples_during_hv_steps"] = hv_samples
     f_entry = 2 * d + 2 * s + 8                       # SURVEY §8d F_hv
     flops = f_entry * n * n
+    # T_roof = max(sum over pipes of FLOPs_pipe / P_pipe,
+    # 2 n^2 / P_MUFU) on ALGORITHMIC work: the 2d (Gram) + 2s (K.V) flops on
+    # the tensor pipe at P_TF32 / 3 (3xTF32), the 8 Matern flops on the FMA
+    # pipe (P_FFMA = 128 FMA/clk/SM, scripts/ubench/ubench_ffma2.cu), 2 MUFU ops.
+    p_bf16 = pk["bf16"] * 1e12
+    p_tf32 = p_bf16 / 2                                # TF32 = half the bf16 rate
+    p_ffma = 2 * 128 * 148 * pk["mhz"] * 1e6
+    p_mufu = 16 * 148 * pk["mhz"] * 1e6                # ex2 / sqrt per s (16/clk/SM)
     if args.hv_impl in ("tc", "tc_bf16"):
-        # issued tensor work per entry: 3xTF32 Gram over the 32-wide augmented
-        # rows + 3-pass K.V over s_pad columns (3xTF32 for "tc", bf16x3 for
-        # "tc_bf16"); the epilogue needs one sqrt and one ex2 per entry on the
-        # MUFU (16/clk/SM).  The binding resource sets the peak.
+        p_tc = p_tf32 / 3 if args.hv_impl == "tc" else p_bf16 / 3
+        t_pipes = (2 * d + 2 * s) / p_tc + 8 / p_ffma
+        basis = (f"sum-of-pipes: {2 * d + 2 * s} tensor flop/entry at {'P_TF32' if args.hv_impl == 'tc' else 'P_BF16'}/3 "
+                 f"+ 8 FMA-pipe flop/entry at P_FFMA; MUFU 2 ops/entry at 16/clk/SM")
+        # the padded work the kernel actually issues (Gram K = 32, K.V N = s
+        # padded to 16), for reference: not the roofline
         spad = 16 * -(-s // 16)
-        p_bf16 = pk["bf16"] * 1e12
-        p_tf32 = p_bf16 / 2                            # TF32 = half the bf16 rate
-        p_mufu = 16 * 148 * pk["mhz"] * 1e6            # ex2/sqrt per s (nominal)
-        p_kv = p_tf32 if args.hv_impl == "tc" else p_bf16
-        t_tensor = 3 * 2 * 32 / p_tf32 + 3 * 2 * spad / p_kv
-        t_entry = max(t_tensor, 2 / p_mufu)
-        bound = "tensor"
-        basis = (f"max(3xTF32 Gram (K=32) at bf16/2 + 3-pass K.V (N={spad}) at "
-                 f"{'bf16/2' if args.hv_impl == 'tc' else 'bf16'}, 2 MUFU ops at 16/clk/SM) per entry; "
-                 f"{'tensor' if t_tensor >= 2 / p_mufu else 'MUFU'} binds")
+        t_issued = 3 * 2 * 32 / p_tf32 + 3 * 2 * spad / (p_tf32 if args.hv_impl == "tc" else p_bf16)
     else:
-        p_ffma = 2 * 128 * 148 * pk["mhz"] * 1e6
-        t_entry = max(f_entry / p_ffma, 2 / (16 * 148 * pk["mhz"] * 1e6))
-        bound = "tensor"  # compute (FFMA) bound; contract field admits hbm|tensor only
+        t_pipes = f_entry / p_ffma
         basis = "FFMA 256 flop/clk/SM"
+        t_issued = t_pipes
+    t_entry = max(t_pipes, 2 / p_mufu)
+    bound = "tensor"  # compute-bound (contract field admits hbm|tensor only)
     peak = f_entry / t_entry / 1e12
     achieved = flops / ws / (kernel_ms / 1e3) / 1e12  # this rank's rows per launch
+    # DRAM traffic is only measurable under ncu (profiles/): not from this run
     traffic = None
+    traffic_profile = None
     prof = os.path.join(ROOT, "profiles", "hv_tc_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            traffic_profile = {"dram_bytes_per_launch": json.load(open(prof)).get("dram_bytes_per_launch"),
+                               "source": "profiles/hv_tc_traffic.json (ncu --set full, config 1; not this run)"}
         except Exception:
-            traffic = None
+            traffic_profile = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -428,16 +561,24 @@ def main():
                 "h2d_bytes_per_step": int(n * s * 4), "d2h_bytes_per_step": int(m * s * 4),
                 "ms_per_step": e2e_ms},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_profile": traffic_profile,
                      "peak_basis": f"{pk['src']} peaks: F_hv={f_entry} flop/entry; " + basis,
-                     "kernel_ms": kernel_ms},
+                     "kernel_ms": kernel_ms, "t_roof_ms": t_entry * n * n / ws * 1e3,
+                     "frac_of_issued_work": (t_issued * n * n / ws * 1e3) / kernel_ms},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
-    if args.outer:
-        line["outer"] = outer_multi if ws > 1 else outer_steps(wg, datasets, local, args)
+    if outer is not None:
+        line["outer"] = outer
+    if outer_multi is not None:
+        line["outer_sharded"] = outer_multi
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(p, args.cpu_seconds)
+        if outer is not None:
+            try:
+                line["cpu_baseline"]["outer"] = cpu_outer_baseline(datasets, outer, args.cpu_seconds)
+            except Exception as e:
+                line["cpu_baseline"]["outer"] = {"error": str(e)[:200]}
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
