@@ -251,7 +251,34 @@ uint64_t wgp_derive_seed(uint64_t base, uint64_t stream);
  *  the reference's permutation (host-only, no device work). */
 int wgp_split_order(int64_t n, uint64_t split_seed, int64_t* order);
 
-/* ---- row-sharded solver building blocks (paper_2405_18328_b200/sharded.py) ---- */
+/* ---- row sharding inside the library: one process per GPU, NCCL ----
+ * Every rank creates a context on its GPU and attaches a communicator before
+ * wgp_set_data (all ranks pass the same full inputs).  Rank r then owns rows
+ * [own0, own1) = [r blk, (r + 1) blk) of every solver vector (blk = the
+ * 128-row tiles dealt in contiguous blocks); vectors keep all rows (leading
+ * dimension nranks blk), so the exchanges are in-place all-gathers:
+ *   wgp_hv / wgp_hv_f64 / wgp_hv_device: the rank's rows of H V, then the
+ *     all-gather of the n x s result;
+ *   wgp_solve (CG, AP; SGD is single-GPU): CG all-gathers the direction every
+ *     iteration and finishes its column reductions on the ranks' rank-order
+ *     sums; AP sums each block's residual shares with an all-reduce; the
+ *     solutions end with all rows on every rank (these collectives are
+ *     captured into the CG / AP CUDA graphs);
+ *   wgp_grad, wgp_train: the rank's rows of every contraction, summed over
+ *     the ranks; the outer loop (Adam) runs identically on every rank.
+ * Without wgp_set_comm nothing changes (the whole operator on one GPU). */
+/** ncclGetUniqueId (rank 0 calls it and broadcasts the 128 bytes). */
+int wgp_nccl_unique_id(unsigned char id[128]);
+/** Attach a communicator (ncclCommInitRank; collective over the ranks) to the
+ *  context; wgp_set_data must follow. */
+int wgp_set_comm(wgp_ctx* ctx, int rank, int nranks, const unsigned char id[128]);
+/** The context's rank, rank count, own rows and vector leading dimension. */
+int wgp_shard_info(wgp_ctx* ctx, int* rank, int* nranks, int64_t* own0, int64_t* own1, int64_t* ld);
+/** The row partition of n points over nranks (host only): own rows and ld. */
+int wgp_shard_rows(int64_t n, int rank, int nranks, int64_t* own0, int64_t* own1, int64_t* ld);
+
+/* ---- row-sharded solver building blocks for callers driving their own exchanges
+ *      (paper_2405_18328_b200/sharded.py, torch.distributed) ---- */
 
 /** J-split decomposition of the fused H.V for a row range: keyed on the global
  *  n (global != 0, the default: a row shard reproduces the full operator's rows

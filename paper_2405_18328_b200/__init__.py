@@ -100,6 +100,7 @@ EXPORTS = [
     "wgp_adam_step", "wgp_derive_seed", "wgp_launch_count", "wgp_profile", "wgp_profile_read",
     "wgp_exact", "wgp_predict", "wgp_split_order", "wgp_hv_cols", "wgp_hv_block", "wgp_ap_factor", "wgp_ap_block_solve",
     "wgp_set_split_global", "wgp_set_cg_precision", "wgp_hv_f64", "wgp_solve_f64",
+    "wgp_nccl_unique_id", "wgp_set_comm", "wgp_shard_info", "wgp_shard_rows",
 ]
 
 
@@ -135,6 +136,10 @@ def load():
     lib.wgp_set_cg_precision.argtypes = [C.c_void_p, C.c_int]
     lib.wgp_hv_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
     lib.wgp_solve_f64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    lib.wgp_nccl_unique_id.argtypes = [C.c_void_p]
+    lib.wgp_set_comm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    lib.wgp_shard_info.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+    lib.wgp_shard_rows.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.wgp_set_data.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
     lib.wgp_set_hyper.argtypes = [C.c_void_p, C.c_void_p]
     lib.wgp_set_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
@@ -187,6 +192,20 @@ def split_order(n: int, split_seed: int) -> np.ndarray:
     out = np.empty(int(n), dtype=np.int64)
     _check(load().wgp_split_order(int(n), C.c_uint64(split_seed), out.ctypes.data))
     return out
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0; broadcast the bytes)."""
+    buf = (C.c_ubyte * 128)()
+    _check(load().wgp_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def shard_rows(n: int, rank: int, nranks: int):
+    """The library's row partition (wgp_shard_rows): (own0, own1, ld)."""
+    a, b, ld = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+    _check(load().wgp_shard_rows(n, rank, nranks, C.byref(a), C.byref(b), C.byref(ld)))
+    return int(a.value), int(b.value), int(ld.value)
 
 
 def derive_seed(base: int, stream: int) -> int:
@@ -453,6 +472,22 @@ class Context:
         if precision not in _CG_PRECISIONS:
             raise ValueError(f"unknown CG precision {precision!r}; one of {sorted(_CG_PRECISIONS)}")
         _check(self._lib.wgp_set_cg_precision(self._h, _CG_PRECISIONS[precision]))
+
+    def set_comm(self, rank: int, nranks: int, unique_id: bytes):
+        """Attach an NCCL communicator (one process per GPU): the context's
+        solvers, H.V and outer loop then run row-sharded over the ranks
+        (wgp_set_comm; call before set_data)."""
+        if len(unique_id) != 128:
+            raise ValueError("unique id must be 128 bytes")
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        _check(self._lib.wgp_set_comm(self._h, rank, nranks, buf))
+
+    def shard_info(self):
+        """(rank, nranks, own0, own1, ld) of the context's row sharding."""
+        r, nr = C.c_int(0), C.c_int(0)
+        a, b, ld = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+        _check(self._lib.wgp_shard_info(self._h, C.byref(r), C.byref(nr), C.byref(a), C.byref(b), C.byref(ld)))
+        return int(r.value), int(nr.value), int(a.value), int(b.value), int(ld.value)
 
     def set_data(self, X):
         X = _f32(X)

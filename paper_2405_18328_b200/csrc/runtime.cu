@@ -6,6 +6,8 @@
 // (warm-start solutions, residuals, directions) resident in HBM across steps.
 #include <cublas_v2.h>
 #include <cusolverDn.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the entry points are resolved from libnccl.so.2 at run time
 
 #include <algorithm>
 #include <cmath>
@@ -90,6 +92,85 @@ struct PinnedBuf {
 
 const char* solver_name(int kind) { return kind == 0 ? "cg_solve" : kind == 1 ? "ap_solve" : "sgd_solve"; }
 
+// NCCL, resolved at run time from libnccl.so.2 (the copy torch already
+// loaded, when it did, else the system's): a context without a communicator
+// never touches it, and the library has no link-time NCCL dependency.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclAllReduce) all_reduce = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  static const NcclApi& get() {
+    static const NcclApi api = [] {
+      NcclApi a;
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) return a;
+      a.get_unique_id = reinterpret_cast<decltype(&ncclGetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+      a.comm_init_rank = reinterpret_cast<decltype(&ncclCommInitRank)>(dlsym(h, "ncclCommInitRank"));
+      a.comm_destroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(h, "ncclCommDestroy"));
+      a.all_gather = reinterpret_cast<decltype(&ncclAllGather)>(dlsym(h, "ncclAllGather"));
+      a.all_reduce = reinterpret_cast<decltype(&ncclAllReduce)>(dlsym(h, "ncclAllReduce"));
+      a.group_start = reinterpret_cast<decltype(&ncclGroupStart)>(dlsym(h, "ncclGroupStart"));
+      a.group_end = reinterpret_cast<decltype(&ncclGroupEnd)>(dlsym(h, "ncclGroupEnd"));
+      a.error_string = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(h, "ncclGetErrorString"));
+      return a;
+    }();
+    if (!api.comm_init_rank || !api.all_gather || !api.all_reduce || !api.group_start)
+      throw DeviceError("NCCL (libnccl.so.2) is not available");
+    return api;
+  }
+  void check(ncclResult_t r, const char* what) const {
+    if (r != ncclSuccess)
+      throw DeviceError(std::string(what) + ": " + (error_string ? error_string(r) : "NCCL error"));
+  }
+};
+
+// One rank's communicator (one process per GPU).  Collectives
+// are enqueued on the context stream (and so are captured into the CG / AP
+// CUDA graphs with the kernels around them).
+struct Comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  Comm(int r, int nr, const ncclUniqueId& id) : rank(r), nranks(nr) {
+    const NcclApi& a = NcclApi::get();
+    a.check(a.comm_init_rank(&comm, nr, id, r), "ncclCommInitRank");
+  }
+  ~Comm() {
+    if (comm) NcclApi::get().comm_destroy(comm);
+  }
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+  static ncclDataType_t type(size_t elem) { return elem == 8 ? ncclFloat64 : ncclFloat32; }
+  // In-place all-gather of row blocks of s columns (column c at base + c ld,
+  // rank r's rows at [r blk, (r + 1) blk)): one grouped launch.
+  void gather_rows(void* base, int64_t ld, int64_t blk, int s, size_t elem, cudaStream_t st) const {
+    const NcclApi& a = NcclApi::get();
+    char* b = static_cast<char*>(base);
+    a.check(a.group_start(), "ncclGroupStart");
+    for (int c = 0; c < s; ++c) {
+      char* col = b + static_cast<size_t>(c) * ld * elem;
+      a.check(a.all_gather(col + static_cast<size_t>(rank) * blk * elem, col, static_cast<size_t>(blk), type(elem),
+                           comm, st),
+              "ncclAllGather");
+    }
+    a.check(a.group_end(), "ncclGroupEnd");
+  }
+  // recv[r * count + k] = rank r's send[k]
+  void all_gather(const double* send, double* recv, size_t count, cudaStream_t st) const {
+    const NcclApi& a = NcclApi::get();
+    a.check(a.all_gather(send, recv, count, ncclFloat64, comm, st), "ncclAllGather");
+  }
+  void all_reduce_sum(double* buf, size_t count, cudaStream_t st) const {
+    const NcclApi& a = NcclApi::get();
+    a.check(a.all_reduce(buf, buf, count, ncclFloat64, ncclSum, comm, st), "ncclAllReduce");
+  }
+};
+
 }  // namespace
 
 struct Ctx {
@@ -114,6 +195,16 @@ struct Ctx {
   bool split_global = true;
   TcOperands tc;
 
+  // Row sharding (one process per GPU, wgp_set_comm): rank r owns rows
+  // [own0, own1) = [r blk, (r + 1) blk) ∩ [0, n) of every solver vector;
+  // vectors keep all n rows (ld = nranks blk) so the all-gathers are in place.
+  std::unique_ptr<Comm> comm;
+  int rank = 0, nranks = 1;
+  int64_t blk = 0, own0 = 0, own1 = 0;
+  bool sharded() const { return comm != nullptr; }
+  int64_t own_m() const { return own1 - own0; }
+  Buf dloc, dall;  // per-rank column totals and their all-gather (dist reductions)
+
   // workspaces
   Buf ctrl, conv, rs, alpha, beta, bnorm, tol, part, colsum, best, stall, act, Xbest, Rbest;
   Buf P, HP, Rtmp, vel, batch, idx, hbuf, linv, Rb, D64, DX, DXP, XP, PP, lapack_work, info;
@@ -121,6 +212,7 @@ struct Ctx {
   // fp64 CG (cg_precision == WGP_CG_F64): solver state and the hv_f64 split partials
   Buf B64, X64, R64, P64, HP64, Rt64, Xbest64, Rbest64, hv64_ws;
   Buf linv_ptrs;  // AP: device pointer array of the batched inverse
+  Buf Rpart;      // row-sharded AP: this rank's share of a block residual
   Buf tr_rhs, tr_sol0, tr_sol1, tr_res, tr_sol64a, tr_sol64b;  // train(): solver state across steps
   Buf api_B, api_X0, api_Xs, api_Rs;  // wgp_solve staging
   int cg_precision = WGP_CG_F64;
@@ -160,6 +252,15 @@ struct Ctx {
     dp = static_cast<int>(round_up(d, 4));
     n_pad = round_up(n, 128);
     ld = n_pad;
+    blk = ld;
+    own0 = 0;
+    own1 = n;
+    if (comm) {  // 128-row tiles dealt to the ranks in contiguous blocks
+      blk = ceil_div(ceil_div(n, 128), nranks) * 128;
+      ld = std::max(n_pad, blk * nranks);
+      own0 = std::min<int64_t>(n, rank * blk);
+      own1 = std::min<int64_t>(n, (rank + 1) * blk);
+    }
     X.ensure(sizeof(float) * n * d);
     WGP_CUDA(cudaMemcpyAsync(X.p, Xh, sizeof(float) * n * d, cudaMemcpyHostToDevice, st));
     mu.assign(d, 0.0);
@@ -270,10 +371,62 @@ struct Ctx {
     P.ensure(sizeof(float) * ld * s);
     HP.ensure(sizeof(float) * ld * s);
     Rtmp.ensure(sizeof(float) * ld * s);
+    if (sharded()) {
+      dloc.ensure(sizeof(double) * 2 * std::max(s + 2, 2 * s));
+      dall.ensure(sizeof(double) * 2 * std::max(s + 2, 2 * s) * nranks);
+    }
   }
   ColState colstate() {
-    return ColState{conv.as<int>(), rs.as<double>(), alpha.as<double>(), beta.as<double>(),
-                    bnorm.as<double>(), tol.as<double>(), best.as<double>(), stall.as<int>(), act.as<int>()};
+    ColState c{conv.as<int>(), rs.as<double>(), alpha.as<double>(), beta.as<double>(),
+               bnorm.as<double>(), tol.as<double>(), best.as<double>(), stall.as<int>(), act.as<int>()};
+    c.dist_loc = sharded() ? dloc.as<double>() : nullptr;
+    return c;
+  }
+  // Row-sharded reduction epilogue: the ranks' column totals (left in dloc by
+  // the reduction kernel) are all-gathered and summed in rank order, then
+  // `kind`'s epilogue runs -- identically on every rank.
+  void dist_reduce(int kind, int w, int s, bool fa = false, bool fb = false, double* out = nullptr) {
+    comm->all_gather(dloc.as<double>(), dall.as<double>(), static_cast<size_t>(w), st);
+    dist_finish(kind, dall.as<double>(), nranks, w, s, colstate(), dctrl(), out, fa, fb, st);
+  }
+  // all-gather the own rows of s columns (in place; no-op unsharded)
+  template <class T>
+  void gather_rows(T* base, int s) {
+    if (sharded()) comm->gather_rows(base, ld, blk, s, sizeof(T), st);
+  }
+  // column dots over the own rows, summed over the ranks
+  template <class T>
+  std::vector<double> dots_own(const T* A, const T* B_, int s) {
+    ensure_solver_ws(s);
+    col_dots(A + own0, B_ + own0, ld, own_m(), s, part.as<double>(), &dctrl()->ticket, colsum.as<double>(), st);
+    if (sharded()) {
+      comm->all_gather(colsum.as<double>(), dall.as<double>(), static_cast<size_t>(s), st);
+      dist_finish(kDistSum, dall.as<double>(), nranks, s, s, colstate(), dctrl(), colsum.as<double>(), false,
+                  false, st);
+    }
+    std::vector<double> h(s);
+    WGP_CUDA(cudaMemcpyAsync(h.data(), colsum.p, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    return h;
+  }
+  // host vector summed over the ranks in rank order (identical on every rank)
+  void sum_over_ranks(std::vector<double>& v) {
+    if (!sharded() || v.empty()) return;
+    const size_t w = v.size();
+    Buf& sb = dloc;
+    Buf& rb = dall;
+    sb.ensure(sizeof(double) * w);
+    rb.ensure(sizeof(double) * w * nranks);
+    WGP_CUDA(cudaMemcpyAsync(sb.p, v.data(), sizeof(double) * w, cudaMemcpyHostToDevice, st));
+    comm->all_gather(sb.as<double>(), rb.as<double>(), w, st);
+    std::vector<double> all(w * nranks);
+    WGP_CUDA(cudaMemcpyAsync(all.data(), rb.p, sizeof(double) * w * nranks, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    for (size_t k = 0; k < w; ++k) {
+      double t = 0.0;
+      for (int r = 0; r < nranks; ++r) t += all[r * w + k];
+      v[k] = t;
+    }
   }
   // column dots over rows [r, r + m)
   std::vector<double> dots_rows(const float* A, const float* B_, int s, int64_t r, int64_t m) {
@@ -374,6 +527,12 @@ struct Ctx {
     WGP_CUDA(cudaMemcpyAsync(tol.p, tl.data(), sizeof(double) * s, cudaMemcpyHostToDevice, st));
     SolveOut out;
     std::vector<double> en;
+    // Row-sharded contexts: rhs and init hold all rows on every rank; the
+    // residuals are formed for the rank's rows [own0, own1) only and the
+    // solutions end with all rows on every rank.
+    const int64_t r = own0, m = own_m();
+    if (sharded() && cfg.kind == WGP_SOLVER_SGD)
+      throw std::invalid_argument("sgd_solve: not available on a row-sharded context (use CG or AP)");
     if (cfg.kind == WGP_SOLVER_CG && cg_precision == WGP_CG_F64) {
       const size_t bytes = sizeof(double) * ld * s;
       B64.ensure(bytes);
@@ -387,7 +546,7 @@ struct Ctx {
         if (init64) WGP_CUDA(cudaMemcpy2DAsync(x64, sizeof(double) * ld, init64, sizeof(double) * ld,
                                                sizeof(double) * n, s, cudaMemcpyDeviceToDevice, st));
         else widen(init, ld, x64, ld, n, s, st);
-        hv64_all(x64, s, r64, kHv64Residual, b64, nullptr);
+        hv64_rows(x64, ld, s, r64 + r, ld, kHv64Residual, b64, ld, r, m, nullptr);
       } else {
         WGP_CUDA(cudaMemsetAsync(x64, 0, bytes, st));
         WGP_CUDA(cudaMemcpyAsync(r64, b64, bytes, cudaMemcpyDeviceToDevice, st));
@@ -396,17 +555,17 @@ struct Ctx {
       // finalize_exact_residuals (:69-77) on the fp64 iterate
       Rt64.ensure(bytes);
       double* e64 = Rt64.as<double>();
-      hv64_all(x64, s, e64, kHv64Residual, b64, nullptr);
-      en = dots(e64, e64, s);
+      hv64_rows(x64, ld, s, e64 + r, ld, kHv64Residual, b64, ld, r, m, nullptr);
+      en = dots_own(e64, e64, s);
       narrow(x64, ld, Xo, ld, n, s, st);
-      narrow(r64, ld, Ro, ld, n, s, st);
+      narrow(r64 + r, ld, Ro + r, ld, m, s, st);
       if (Xo64) WGP_CUDA(cudaMemcpy2DAsync(Xo64, sizeof(double) * ld, x64, sizeof(double) * ld,
                                            sizeof(double) * n, s, cudaMemcpyDeviceToDevice, st));
     } else {
       // X = init; R = rhs - H X (exactly rhs for a zero init)
       if (init) {
         copy_cols(init, ld, Xo, ld, n, s, st);
-        hv_all(Xo, s, Ro, kHvResidual, B);
+        hv(Xo, ld, s, Ro + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);
       } else {
         fill_zero(Xo, ld, n, s, st);
         copy_cols(B, ld, Ro, ld, n, s, st);
@@ -416,8 +575,8 @@ struct Ctx {
       else sgd(cfg, B, Xo, Ro, s, out);
       // finalize_exact_residuals, :69-77
       float* E = Rtmp.as<float>();
-      hv_all(Xo, s, E, kHvResidual, B);
-      en = dots(E, E, s);
+      hv(Xo, ld, s, E + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);
+      en = dots_own(E, E, s);
     }
     out.rel.resize(s);
     for (int c = 0; c < s; ++c) out.rel[c] = bn[c] > 0.0 ? std::sqrt(en[c]) / bn[c] : 0.0;
@@ -504,11 +663,14 @@ struct Ctx {
   // The operator of a CG iteration in the solver-state precision T: float
   // runs the configured fp32 engine (P's tf32 planes kept by the direction
   // kernels), double the fp64-accumulating symmetric engine (hv_f64.cu).
+  // (output rows [own0, own1): the rank's rows; out / B indexed by global row)
   void cg_hv(const float* V, int s, float* out, int mode, const float* B, const int* done, const float* vplanes) {
-    hv_all(V, s, out, mode, B, done, vplanes);
+    hv(V, ld, s, out + own0, ld, mode, B, ld, 0, n, nullptr, own0, own_m(), done, true, vplanes,
+       vplanes ? ld : 0);
   }
   void cg_hv(const double* V, int s, double* out, int mode, const double* B, const int* done, const float*) {
-    hv64_all(V, s, out, mode == kHvResidual ? kHv64Residual : kHv64Store, B, done);
+    hv64_rows(V, ld, s, out + own0, ld, mode == kHvResidual ? kHv64Residual : kHv64Store, B, ld, own0, own_m(),
+              done);
   }
 
   template <class T>
@@ -539,22 +701,53 @@ struct Ctx {
       PP.ensure(sizeof(float) * 2 * ld * s);  // P's tf32 planes: the H.V skips its split of P
       PPp = PP.as<float>();
     }
-    cg_init(Pp, R, ld, n, s, cs, pt, c, st, PPp);
-    cg_snapshot(Xo, R, Xb, Rb, ld, n, s, cs, c, true, st);
+    // Vector work on the rank's rows [own0, own1) (all rows unsharded); a
+    // sharded iteration all-gathers the direction before its H.V and the
+    // iterate before a residual refresh, and finishes every column reduction
+    // on the ranks' rank-order sum (dist_reduce).
+    const int64_t r = own0, m = own_m();
+    const bool sh = sharded();
+    float* PPr = PPp ? PPp + r : nullptr;
+    cg_init(R + r, ld, m, s, cs, pt, c, st);
+    if (sh) dist_reduce(kDistInit, s, s);
+    cg_seed(Pp + r, R + r, ld, m, s, cs.conv, st, PPr);
+    cg_snapshot(Xo + r, R + r, Xb + r, Rb + r, ld, m, s, cs, c, true, st);
     const int* done = &c->done;
     auto iteration = [&](bool refresh) {
-      cg_hv(Pp, s, HPp, kHvStore, nullptr, done, PPp);
-      cg_alpha(Pp, HPp, ld, n, s, cs, pt, c, st);
-      if (!refresh) {
-        cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, false, st);
-      } else {
-        cg_update(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, true, st);
-        cg_hv(Xo, s, Rt, kHvResidual, B, done, nullptr);
-        cg_refresh_norm(R, Rt, ld, n, s, cs, pt, c, st);
-        cg_snapshot(Xo, R, Xb, Rb, ld, n, s, cs, c, false, st);
+      if (sh) {
+        gather_rows(Pp, s);
+        if (PPp) gather_rows(PPp, 2 * s);
       }
-      cg_direction(Pp, R, ld, n, s, cs, pt, c, st, PPp);
+      cg_hv(Pp, s, HPp, kHvStore, nullptr, done, PPp);
+      cg_alpha(Pp + r, HPp + r, ld, m, s, cs, pt, c, st);
+      if (sh) dist_reduce(kDistAlpha, s, s);
+      if (!refresh) {
+        cg_update(Xo + r, R + r, Pp + r, HPp + r, ld, m, s, cs, pt, c, false, st);
+        if (sh) dist_reduce(kDistBeta, s, s);
+      } else {
+        cg_update(Xo + r, R + r, Pp + r, HPp + r, ld, m, s, cs, pt, c, true, st);
+        if (sh) gather_rows(Xo, s);
+        cg_hv(Xo, s, Rt, kHvResidual, B, done, nullptr);
+        cg_refresh_norm(R + r, Rt + r, ld, m, s, cs, pt, c, st);
+        if (sh) dist_reduce(kDistRefresh, s, s);
+        cg_snapshot(Xo + r, R + r, Xb + r, Rb + r, ld, m, s, cs, c, false, st);
+      }
+      cg_direction(Pp + r, R + r, ld, m, s, cs, pt, c, st, PPr);
     };
+    // every rank ends with all rows of the solutions
+    struct GatherAtExit {
+      Ctx* self;
+      T* X;
+      int s;
+      ~GatherAtExit() {
+        if (self->sharded()) {
+          try {
+            self->gather_rows(X, s);
+          } catch (...) {
+          }
+        }
+      }
+    } gather_at_exit{this, Xo, s};
     static const bool no_graphs = getenv("WGP_NO_GRAPHS") != nullptr;
     constexpr int kChunk = 10;
     const int impl = f64 ? -1 : hv_impl;
@@ -706,12 +899,35 @@ struct Ctx {
     const ColState cs = colstate();
     SolveCtrl* c = dctrl();
     double* pt = part.as<double>();
-    norms_convergence(R, ld, n, s, cs, pt, c, false, true, st);  // :172-178
+    // Row-sharded AP: R holds the exact residual of the rank's rows; X and
+    // the epoch's deltas DX stay replicated (every rank applies the same
+    // delta_b); block b's residual R_b = R0_b - H[b, 0:start] DX[0:start] is
+    // a sum of per-rank shares -- the R0 rows the rank owns minus the
+    // contraction over its 1/nranks slice of the columns [0, start) -- summed
+    // by an all-reduce, so every rank solves the same delta_b = H_bb^-1 R_b.
+    const bool sh = sharded();
+    const int64_t r = own0, m = own_m();
+    if (sh) {
+      Rpart.ensure(sizeof(float) * bs * s);
+      fill_zero(DX.as<float>(), ld, n, s, st);  // the column slices read DX rows of any rank
+    }
+    norms_convergence(R + r, ld, m, s, cs, pt, c, false, true, st);  // :172-178
+    if (sh) dist_reduce(kDistNorms, s, s, false, true);
     const double one = 1.0, zero = 0.0;
     auto epoch = [&]() {
       for (int64_t b = 0; b < nb; ++b) {  // :183-187
         const int64_t start = b * bs, size = std::min(bs, n - start);
         const double* Hinv = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
+        if (sh) {
+          float* rp = Rpart.as<float>();
+          masked_rows(R, ld, start, size, own0, own1, s, rp, c, st);
+          const int64_t j0 = start * rank / nranks, j1 = start * (rank + 1) / nranks;
+          if (j1 > j0)
+            hv(DX.as<float>(), ld, s, rp, size, kHvSubtract, nullptr, 0, j0, j1, nullptr, start, size, &c->done,
+               false, DXP.as<float>(), ld);
+          widen_block(rp, Rb.as<double>(), size, s, c, st);
+          comm->all_reduce_sum(Rb.as<double>(), static_cast<size_t>(size) * s, st);
+        } else {
         // Block residual, left-looking over the earlier blocks only: R is the
         // exact residual at the epoch start (R0), and this epoch changed X
         // only in blocks < b, by DX = their deltas, so
@@ -726,6 +942,7 @@ struct Ctx {
         if (b > 0) hv(DX.as<float>(), ld, s, R + start, ld, kHvResidual, R, ld, 0, start, nullptr, start, size,
                       &c->done, false, DXP.as<float>(), ld);
         ap_gather(R, ld, start, size, s, Rb.as<double>(), c, st);
+        }
         // delta = H_bb^-1 R_b (:185); full blocks as kSplitK K-slices in one
         // strided-batched DGEMM (partials summed in fixed order by ap_apply):
         // the single DGEMM ran 64 CTAs over K = 1000, ~16 us per block
@@ -746,8 +963,9 @@ struct Ctx {
         }
         ap_apply(Xo, ld, start, size, s, D64.as<double>(), kparts, DX.as<float>(), DXP.as<float>(), c, st);
       }
-      hv_all(Xo, s, R, kHvResidual, B);                            // :188
-      norms_convergence(R, ld, n, s, cs, pt, c, true, true, st);  // :189-191
+      hv(Xo, ld, s, R + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);  // :188
+      norms_convergence(R + r, ld, m, s, cs, pt, c, true, true, st);       // :189-191
+      if (sh) dist_reduce(kDistNorms, s, s, true, true);
     };
     static const bool no_graphs = getenv("WGP_NO_GRAPHS") != nullptr;
     bool eager_done = false;  // one eager epoch first: every workspace exists before a capture
@@ -873,8 +1091,8 @@ struct Ctx {
     float* D = P.as<float>();
     float* HD = HP.as<float>();
     sub_into(init, sol, D, ld, n, s, st);
-    hv_all(D, s, HD);
-    const std::vector<double> q = dots(D, HD, s);
+    hv(D, ld, s, HD + own0, ld, kHvStore, nullptr, 0, 0, n, nullptr, own0, own_m());
+    const std::vector<double> q = dots_own(D, HD, s);
     double acc = 0.0;
     for (double v : q) acc += v;
     return std::sqrt(std::max(acc / s / static_cast<double>(n), 0.0));
@@ -891,8 +1109,8 @@ struct Ctx {
     // D = init - sol
     WGP_CUDA(cudaMemcpyAsync(D, init, bytes, cudaMemcpyDeviceToDevice, st));
     axpy_cols(-1.0, sol, D, ld, n, s, st);
-    hv64_all(D, s, HD, kHv64Store, nullptr, nullptr);
-    const std::vector<double> q = dots(D, HD, s);
+    hv64_rows(D, ld, s, HD + own0, ld, kHv64Store, nullptr, ld, own0, own_m(), nullptr);
+    const std::vector<double> q = dots_own(D, HD, s);
     double acc = 0.0;
     for (double v : q) acc += v;
     return std::sqrt(std::max(acc / s / static_cast<double>(n), 0.0));
@@ -904,12 +1122,31 @@ struct Ctx {
   // Rows [gr0, gr0 + gm) against all n points (gm < 0: all rows): a row
   // shard's share of every contraction; the shares of a row partition sum to
   // the full gradient (all outputs are linear in the row sums).
+  // Row-sharded contexts (reduce_ranks): each rank contracts its rows and
+  // the (d + 2)-vectors are summed over the ranks in rank order.
   void grad(int transform, const double* raw, const float* vy, const float* L, const float* R,
-            int s, double coef_b, double* out_a, double* out_b, int64_t gr0 = 0, int64_t gm = -1) {
+            int s, double coef_b, double* out_a, double* out_b, int64_t gr0 = 0, int64_t gm = -1,
+            bool reduce_ranks = false) {
     if (gm < 0) gm = n - gr0;
     std::vector<double> cons(d + 2);
     for (int k = 0; k < d + 2; ++k) cons[k] = transform == 1 ? std::exp(raw[k]) : softplus(raw[k]);
     set_hyper(cons.data());
+    if (gm <= 0) {  // a rank without rows contributes zeros
+      std::fill(out_a, out_a + d + 2, 0.0);
+      std::fill(out_b, out_b + d + 2, 0.0);
+    } else {
+      grad_rows(transform, raw, vy, L, R, s, coef_b, out_a, out_b, gr0, gm);
+    }
+    if (reduce_ranks && sharded()) {
+      std::vector<double> v(out_a, out_a + d + 2);
+      v.insert(v.end(), out_b, out_b + d + 2);
+      sum_over_ranks(v);
+      std::copy(v.begin(), v.begin() + d + 2, out_a);
+      std::copy(v.begin() + d + 2, v.end(), out_b);
+    }
+  }
+  void grad_rows(int transform, const double* raw, const float* vy, const float* L, const float* R,
+                 int s, double coef_b, double* out_a, double* out_b, int64_t gr0, int64_t gm) {
     // tensor-core engines (TC, TC_BF16) use the tcgen05 gradient where it
     // applies; WGP_GRAD_IMPL=simt forces the CUDA-core kernel
     static const bool force_simt = [] {
@@ -1283,7 +1520,8 @@ struct Ctx {
                                          sizeof(float) * n, sp, cudaMemcpyDeviceToHost, st));
           }
           std::vector<double> qa(p), qb(p), g(p);
-          grad(T, raw.data(), cur, cur + ld, pathwise ? cur + ld : Z, s, 0.5 / s, qa.data(), qb.data());
+          grad(T, raw.data(), cur, cur + ld, pathwise ? cur + ld : Z, s, 0.5 / s, qa.data(), qb.data(), own0,
+               own_m(), true);
           for (int k = 0; k < p; ++k) g[k] = qa[k] - qb[k];
           adam(raw.data(), g.data(), m.data(), v.data(), p, t, cfg.learning_rate, cfg.adam_beta1,
                cfg.adam_beta2, cfg.adam_eps);
@@ -1572,6 +1810,55 @@ int wgp_set_hyper(wgp_ctx* ctx, const double* c) {
   });
 }
 
+int wgp_nccl_unique_id(unsigned char* id) {
+  return guarded([&] {
+    if (!id) throw std::invalid_argument("wgp_nccl_unique_id: null id");
+    const wgp::NcclApi& a = wgp::NcclApi::get();
+    ncclUniqueId u;
+    a.check(a.get_unique_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, u.internal, sizeof(u.internal));
+  });
+}
+
+int wgp_set_comm(wgp_ctx* ctx, int rank, int nranks, const unsigned char* id) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("wgp_set_comm: bad rank / nranks");
+    if (!id) throw std::invalid_argument("wgp_set_comm: null id");
+    WGP_CUDA(cudaSetDevice(c.device));
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, sizeof(u.internal));
+    c.drop_cg_graphs();  // captured launches bake in the layout
+    c.comm.reset();
+    c.comm = std::make_unique<wgp::Comm>(rank, nranks, u);
+    c.rank = rank;
+    c.nranks = nranks;
+    c.n = 0;  // the row layout depends on the rank count: wgp_set_data follows
+    c.have_hyper = false;
+  });
+}
+
+int wgp_shard_info(wgp_ctx* ctx, int* rank, int* nranks, int64_t* own0, int64_t* own1, int64_t* ld) {
+  return guarded([&] {
+    const wgp::Ctx& c = ctx->c;
+    if (rank) *rank = c.rank;
+    if (nranks) *nranks = c.nranks;
+    if (own0) *own0 = c.own0;
+    if (own1) *own1 = c.own1;
+    if (ld) *ld = c.ld;
+  });
+}
+
+int wgp_shard_rows(int64_t n, int rank, int nranks, int64_t* own0, int64_t* own1, int64_t* ld) {
+  return guarded([&] {
+    if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("wgp_shard_rows: bad arguments");
+    const int64_t blk = wgp::ceil_div(wgp::ceil_div(n, 128), nranks) * 128;
+    if (own0) *own0 = std::min<int64_t>(n, rank * blk);
+    if (own1) *own1 = std::min<int64_t>(n, (rank + 1) * blk);
+    if (ld) *ld = std::max<int64_t>(wgp::round_up(n, 128), blk * nranks);
+  });
+}
+
 int wgp_set_rows(wgp_ctx* ctx, int64_t r0, int64_t r1) {
   return guarded([&] {
     if (r0 < 0 || r1 > ctx->c.n || r1 <= r0) throw std::invalid_argument("wgp_set_rows: bad row range");
@@ -1586,15 +1873,25 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
     WGP_CUDA(cudaSetDevice(c.device));
     c.require_data();
     if (s < 1) throw std::invalid_argument("wgp_hv: s must be >= 1");
-    const int64_t m = c.r1 - c.r0;
     wgp::Buf& dv = c.io_in;
     wgp::Buf& dout = c.io_out;
     dv.ensure(sizeof(float) * c.ld * s);
-    dout.ensure(sizeof(float) * m * s);
     WGP_CUDA(cudaMemcpy2DAsync(dv.p, sizeof(float) * c.ld, V, sizeof(float) * c.n, sizeof(float) * c.n, s,
                                cudaMemcpyHostToDevice, c.st));
-    c.hv(dv.as<float>(), c.ld, s, dout.as<float>(), m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, m);
-    WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(float) * m * s, cudaMemcpyDeviceToHost, c.st));
+    if (c.sharded()) {  // the rank's rows, then the all-gather of the n x s result
+      dout.ensure(sizeof(float) * c.ld * s);
+      float* o = dout.as<float>();
+      c.hv(dv.as<float>(), c.ld, s, o + c.own0, c.ld, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.own0,
+           c.own_m());
+      c.gather_rows(o, s);
+      WGP_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * c.n, o, sizeof(float) * c.ld, sizeof(float) * c.n, s,
+                                 cudaMemcpyDeviceToHost, c.st));
+    } else {
+      const int64_t m = c.r1 - c.r0;
+      dout.ensure(sizeof(float) * m * s);
+      c.hv(dv.as<float>(), c.ld, s, dout.as<float>(), m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, m);
+      WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(float) * m * s, cudaMemcpyDeviceToHost, c.st));
+    }
     WGP_CUDA(cudaStreamSynchronize(c.st));
   });
 }
@@ -1605,15 +1902,25 @@ int wgp_hv_f64(wgp_ctx* ctx, const double* V, int s, double* out) {
     WGP_CUDA(cudaSetDevice(c.device));
     c.require_data();
     if (s < 1) throw std::invalid_argument("wgp_hv: s must be >= 1");
-    const int64_t m = c.r1 - c.r0;
     wgp::Buf& dv = c.io_in;
     wgp::Buf& dout = c.io_out;
     dv.ensure(sizeof(double) * c.ld * s);
-    dout.ensure(sizeof(double) * m * s);
     WGP_CUDA(cudaMemcpy2DAsync(dv.p, sizeof(double) * c.ld, V, sizeof(double) * c.n, sizeof(double) * c.n, s,
                                cudaMemcpyHostToDevice, c.st));
-    c.hv64_rows(dv.as<double>(), c.ld, s, dout.as<double>(), m, wgp::kHv64Store, nullptr, 0, c.r0, m, nullptr);
-    WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double) * m * s, cudaMemcpyDeviceToHost, c.st));
+    if (c.sharded()) {
+      dout.ensure(sizeof(double) * c.ld * s);
+      double* o = dout.as<double>();
+      c.hv64_rows(dv.as<double>(), c.ld, s, o + c.own0, c.ld, wgp::kHv64Store, nullptr, 0, c.own0, c.own_m(),
+                  nullptr);
+      c.gather_rows(o, s);
+      WGP_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * c.n, o, sizeof(double) * c.ld, sizeof(double) * c.n, s,
+                                 cudaMemcpyDeviceToHost, c.st));
+    } else {
+      const int64_t m = c.r1 - c.r0;
+      dout.ensure(sizeof(double) * m * s);
+      c.hv64_rows(dv.as<double>(), c.ld, s, dout.as<double>(), m, wgp::kHv64Store, nullptr, 0, c.r0, m, nullptr);
+      WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(double) * m * s, cudaMemcpyDeviceToHost, c.st));
+    }
     WGP_CUDA(cudaStreamSynchronize(c.st));
   });
 }
@@ -1623,6 +1930,13 @@ int wgp_hv_device(wgp_ctx* ctx, const float* V, int64_t ldv, int s, float* out, 
     wgp::Ctx& c = ctx->c;
     c.require_data();
     if (s < 1) throw std::invalid_argument("wgp_hv: s must be >= 1");
+    if (c.sharded()) {  // rows [own0, own1) into out, then the in-place all-gather: out holds all rows
+      if (ldv < c.n || ldo != c.ld)
+        throw std::invalid_argument("wgp_hv: a row-sharded context needs ldo == its leading dimension");
+      c.hv(V, ldv, s, out + c.own0, ldo, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.own0, c.own_m());
+      c.gather_rows(out, s);
+      return;
+    }
     if (ldv < c.n || ldo < c.r1 - c.r0) throw std::invalid_argument("wgp_hv: leading dimension too small");
     c.hv(V, ldv, s, out, ldo, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, c.r1 - c.r0);
   });
@@ -1658,9 +1972,14 @@ int wgp_grad(wgp_ctx* ctx, int transform, const double* raw, const float* vy, co
                                cudaMemcpyHostToDevice, c.st));
     WGP_CUDA(cudaMemcpy2DAsync(dR.p, sizeof(float) * c.ld, R, sizeof(float) * c.n, sizeof(float) * c.n, s,
                                cudaMemcpyHostToDevice, c.st));
-    // rows of the context's row range (wgp_set_rows) against all points
-    c.grad(transform, raw, dvy.as<float>(), dL.as<float>(), dR.as<float>(), s, coef_b, out_a, out_b, c.r0,
-           c.r1 - c.r0);
+    // rows of the context's row range (wgp_set_rows) against all points;
+    // a row-sharded context contracts its rows and sums over the ranks
+    if (c.sharded())
+      c.grad(transform, raw, dvy.as<float>(), dL.as<float>(), dR.as<float>(), s, coef_b, out_a, out_b, c.own0,
+             c.own_m(), true);
+    else
+      c.grad(transform, raw, dvy.as<float>(), dL.as<float>(), dR.as<float>(), s, coef_b, out_a, out_b, c.r0,
+             c.r1 - c.r0);
   });
 }
 

@@ -32,7 +32,11 @@ __device__ __forceinline__ bool my_col(int c) { return ((c >> 2) % gridDim.y) ==
 
 __device__ void block_totals(const double* part, int w, double* tot);
 
-__device__ bool publish(Red& red, int s, double* part, SolveCtrl* ctrl) {
+// Row-sharded solves (ColState::dist_loc set): the last CTA stores this
+// rank's column totals in dist_loc and stops; the host exchanges the ranks'
+// totals (allgather) and dist_finish runs the epilogue on their rank-order
+// sum, identically on every rank.
+__device__ bool publish(Red& red, int s, double* part, SolveCtrl* ctrl, double* dist_loc = nullptr) {
   __syncthreads();
   for (int c = threadIdx.x; c < s; c += blockDim.x) {
     if (!my_col(c)) continue;
@@ -47,6 +51,11 @@ __device__ bool publish(Red& red, int s, double* part, SolveCtrl* ctrl) {
   if (!last) return false;
   __threadfence();
   block_totals(part, s, red.v[0]);  // red's deposits are in part: reuse it
+  if (dist_loc) {
+    for (int c = threadIdx.x; c < s; c += blockDim.x) dist_loc[c] = red.v[0][c];
+    if (threadIdx.x == 0) ctrl->ticket = 0;
+    return false;
+  }
   return true;
 }
 
@@ -141,18 +150,9 @@ __global__ void col_dots_kernel(const T* A, const T* B, int64_t ld, int64_t n, i
   if (threadIdx.x == 0) *ticket = 0;
 }
 
-template <class T>
-__global__ void cg_init_kernel(T* P, const T* R, int64_t ld, int64_t n, int s,
-                               ColState cs, double* part, SolveCtrl* ctrl) {
-  __shared__ Red red;
-  ROWS_OF_BLOCK
-  cols4(s, rb, re, ld, red, [&](int, int64_t e) {
-    const double r = R[e];
-    return r * r;
-  });
-  if (!publish(red, s, part, ctrl)) return;
+__device__ void cg_init_epi(int s, ColState cs, const double* tot, SolveCtrl* ctrl) {
   for (int c = threadIdx.x; c < s; c += NT) {
-    const double rs = red.v[0][c];
+    const double rs = tot[c];
     cs.rs[c] = rs;
     const bool conv = cs.bnorm[c] == 0.0 || sqrt(rs) <= cs.tol[c] * cs.bnorm[c];
     cs.conv[c] = conv ? 1 : 0;
@@ -161,6 +161,19 @@ __global__ void cg_init_kernel(T* P, const T* R, int64_t ld, int64_t n, int s,
     cs.act[c] = 1;
   }
   loop_check(s, cs, ctrl, true);
+}
+
+template <class T>
+__global__ void cg_init_kernel(const T* R, int64_t ld, int64_t n, int s,
+                               ColState cs, double* part, SolveCtrl* ctrl) {
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  cols4(s, rb, re, ld, red, [&](int, int64_t e) {
+    const double r = R[e];
+    return r * r;
+  });
+  if (!publish(red, s, part, ctrl, cs.dist_loc)) return;
+  cg_init_epi(s, cs, red.v[0], ctrl);
 }
 
 // P = R for active columns, 0 otherwise (separate pass: needs conv flags).
@@ -184,19 +197,10 @@ __global__ void cg_seed_direction_kernel(T* P, const T* R, int64_t ld, int64_t n
   put_planes(pp, i + c * ld, static_cast<int64_t>(s) * ld, v);
 }
 
-template <class T>
-__global__ void cg_alpha_kernel(const T* P, const T* HP, int64_t ld, int64_t n, int s,
-                                ColState cs, double* part, SolveCtrl* ctrl) {
-  if (ctrl->done) return;
-  __shared__ Red red;
-  ROWS_OF_BLOCK
-  cols4(s, rb, re, ld, red, [&](int c, int64_t e) {
-    return cs.conv[c] ? 0.0 : static_cast<double>(P[e]) * static_cast<double>(HP[e]);
-  });
-  if (!publish(red, s, part, ctrl)) return;
+__device__ void cg_alpha_epi(int s, ColState cs, const double* tot, SolveCtrl* ctrl) {
   for (int c = threadIdx.x; c < s; c += NT) {
     if (cs.conv[c]) continue;
-    const double pHp = red.v[0][c];
+    const double pHp = tot[c];
     if (!(pHp > 0.0)) {
       atomicCAS(&ctrl->status, kStatusOk, kStatusNotPd);
       ctrl->fail_it = ctrl->it;
@@ -208,6 +212,19 @@ __global__ void cg_alpha_kernel(const T* P, const T* HP, int64_t ld, int64_t n, 
     ctrl->ticket = 0;
     if (ctrl->status != kStatusOk) ctrl->done = 1;
   }
+}
+
+template <class T>
+__global__ void cg_alpha_kernel(const T* P, const T* HP, int64_t ld, int64_t n, int s,
+                                ColState cs, double* part, SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  cols4(s, rb, re, ld, red, [&](int c, int64_t e) {
+    return cs.conv[c] ? 0.0 : static_cast<double>(P[e]) * static_cast<double>(HP[e]);
+  });
+  if (!publish(red, s, part, ctrl, cs.dist_loc)) return;
+  cg_alpha_epi(s, cs, red.v[0], ctrl);
 }
 
 // restart: a refresh step (:119-120).  The reference keeps the direction
@@ -272,7 +289,7 @@ __global__ void cg_update_kernel(T* X, T* R, const T* P, const T* HP, int64_t ld
     return static_cast<double>(r) * r;
   });
   if (refresh) return;
-  if (!publish(red, s, part, ctrl)) return;
+  if (!publish(red, s, part, ctrl, cs.dist_loc)) return;
   beta_epilogue(s, cs, red.v[0], ctrl);
 }
 
@@ -288,7 +305,7 @@ __global__ void cg_refresh_norm_kernel(T* R, const T* Rtmp, int64_t ld, int64_t 
     R[e] = r;
     return static_cast<double>(r) * r;
   });
-  if (!publish(red, s, part, ctrl)) return;
+  if (!publish(red, s, part, ctrl, cs.dist_loc)) return;
   beta_epilogue(s, cs, red.v[0], ctrl, true);
 }
 
@@ -347,6 +364,19 @@ __global__ void cg_snapshot_kernel(T* X, T* R, T* Xb, T* Rb, int64_t ld, int64_t
   }
 }
 
+__device__ void norms_epi(int s, ColState cs, const double* tot, SolveCtrl* ctrl, int check_nan, int begin_next) {
+  for (int c = threadIdx.x; c < s; c += NT) {
+    const double t = tot[c];
+    if (check_nan && !isfinite(t)) {
+      atomicCAS(&ctrl->status, kStatusOk, kStatusNaN);
+      ctrl->fail_it = ctrl->it;
+    }
+    cs.rs[c] = t;
+    cs.conv[c] = (cs.bnorm[c] == 0.0 || sqrt(t) <= cs.tol[c] * cs.bnorm[c]) ? 1 : 0;
+  }
+  loop_check(s, cs, ctrl, begin_next != 0);
+}
+
 __global__ void norms_convergence_kernel(const float* R, int64_t ld, int64_t n, int s, ColState cs,
                                          double* part, SolveCtrl* ctrl, int check_nan,
                                          int begin_next) {
@@ -357,17 +387,35 @@ __global__ void norms_convergence_kernel(const float* R, int64_t ld, int64_t n, 
     const double r = R[e];
     return r * r;
   });
-  if (!publish(red, s, part, ctrl)) return;
-  for (int c = threadIdx.x; c < s; c += NT) {
-    const double t = red.v[0][c];
-    if (check_nan && !isfinite(t)) {
-      atomicCAS(&ctrl->status, kStatusOk, kStatusNaN);
-      ctrl->fail_it = ctrl->it;
-    }
-    cs.rs[c] = t;
-    cs.conv[c] = (cs.bnorm[c] == 0.0 || sqrt(t) <= cs.tol[c] * cs.bnorm[c]) ? 1 : 0;
+  if (!publish(red, s, part, ctrl, cs.dist_loc)) return;
+  norms_epi(s, cs, red.v[0], ctrl, check_nan, begin_next);
+}
+
+// The epilogue of a row-sharded reduction: column totals = the ranks'
+// totals (all[r * w + c]) summed in rank order, then the kind's epilogue.
+__global__ void dist_finish_kernel(int kind, const double* all, int nranks, int w, int s, ColState cs,
+                                   SolveCtrl* ctrl, double* out, int flag_a, int flag_b) {
+  if (kind == kDistAlpha || kind == kDistBeta || kind == kDistRefresh) {
+    if (ctrl->done) return;
+  } else if (kind == kDistNorms && flag_b && ctrl->done) {
+    return;
   }
-  loop_check(s, cs, ctrl, begin_next != 0);
+  __shared__ double tot[SMAX];
+  for (int c = threadIdx.x; c < w; c += NT) {
+    double t = 0.0;
+    for (int r = 0; r < nranks; ++r) t += all[static_cast<int64_t>(r) * w + c];
+    tot[c] = t;
+  }
+  __syncthreads();
+  switch (kind) {
+    case kDistInit: cg_init_epi(s, cs, tot, ctrl); break;
+    case kDistAlpha: cg_alpha_epi(s, cs, tot, ctrl); break;
+    case kDistBeta: beta_epilogue(s, cs, tot, ctrl); break;
+    case kDistRefresh: beta_epilogue(s, cs, tot, ctrl, true); break;
+    case kDistNorms: norms_epi(s, cs, tot, ctrl, flag_a, flag_b); break;
+    default:
+      for (int c = threadIdx.x; c < w; c += NT) out[c] = tot[c];
+  }
 }
 
 __global__ void ap_gather_kernel(const float* R, int64_t ld, int64_t start, int64_t b, int s,
@@ -540,6 +588,7 @@ void check_s(int s) {
 template <class T>
 void cg_snapshot(T* X, T* R, T* Xb, T* Rb, int64_t ld, int64_t n, int s, ColState cs,
                  const SolveCtrl* ctrl, bool at_start, cudaStream_t st) {
+  if (n <= 0) return;
   cg_snapshot_kernel<<<dim3(static_cast<unsigned>(ceil_div(n, NT)), s), NT, 0, st>>>(X, R, Xb, Rb, ld, n, s, cs,
                                                                                      ctrl, at_start ? 1 : 0);
   WGP_LAUNCH_CHECK();
@@ -554,12 +603,17 @@ void col_dots(const T* A, const T* B, int64_t ld, int64_t n, int s, double* part
 }
 
 template <class T>
-void cg_init(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
-             SolveCtrl* ctrl, cudaStream_t st, float* pp) {
+void cg_init(const T* R, int64_t ld, int64_t n, int s, ColState cs, double* part, SolveCtrl* ctrl,
+             cudaStream_t st) {
   check_s(s);
-  cg_init_kernel<<<cgrid(n, s), NT, 0, st>>>(P, R, ld, n, s, cs, part, ctrl);
+  cg_init_kernel<<<cgrid(n, s), NT, 0, st>>>(R, ld, n, s, cs, part, ctrl);
   WGP_LAUNCH_CHECK();
-  cg_seed_direction_kernel<<<grid2(n, s), NT, 0, st>>>(P, R, ld, n, s, cs.conv, pp);
+}
+
+template <class T>
+void cg_seed(T* P, const T* R, int64_t ld, int64_t n, int s, const int* conv, cudaStream_t st, float* pp) {
+  if (n <= 0) return;
+  cg_seed_direction_kernel<<<grid2(n, s), NT, 0, st>>>(P, R, ld, n, s, conv, pp);
   WGP_LAUNCH_CHECK();
 }
 
@@ -597,8 +651,8 @@ void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
                                cudaStream_t);                                                                \
   template void col_dots<T>(const T*, const T*, int64_t, int64_t, int, double*, unsigned*, double*,         \
                             cudaStream_t);                                                                   \
-  template void cg_init<T>(T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*, cudaStream_t, \
-                           float*);                                                                          \
+  template void cg_init<T>(const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*, cudaStream_t);     \
+  template void cg_seed<T>(T*, const T*, int64_t, int64_t, int, const int*, cudaStream_t, float*);             \
   template void cg_alpha<T>(const T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,       \
                             cudaStream_t);                                                                   \
   template void cg_update<T>(T*, T*, const T*, const T*, int64_t, int64_t, int, ColState, double*,          \
@@ -610,6 +664,29 @@ void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
 WGP_CG_INSTANTIATE(float)
 WGP_CG_INSTANTIATE(double)
 #undef WGP_CG_INSTANTIATE
+
+__global__ void masked_rows_kernel(const float* R, int64_t ld, int64_t start, int64_t size, int64_t own0,
+                                   int64_t own1, float* out, const SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= size) return;
+  const int64_t g = start + i;
+  out[i + blockIdx.y * size] = (g >= own0 && g < own1) ? R[g + blockIdx.y * ld] : 0.f;
+}
+void masked_rows(const float* R, int64_t ld, int64_t start, int64_t size, int64_t own0, int64_t own1, int s,
+                 float* out, const SolveCtrl* ctrl, cudaStream_t st) {
+  masked_rows_kernel<<<grid2(size, s), NT, 0, st>>>(R, ld, start, size, own0, own1, out, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+__global__ void widen_block_kernel(const float* A, double* B, int64_t size, const SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < size) B[i + blockIdx.y * size] = A[i + blockIdx.y * size];
+}
+void widen_block(const float* A, double* B, int64_t size, int s, const SolveCtrl* ctrl, cudaStream_t st) {
+  widen_block_kernel<<<grid2(size, s), NT, 0, st>>>(A, B, size, ctrl);
+  WGP_LAUNCH_CHECK();
+}
 
 __global__ void widen_kernel(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -624,15 +701,25 @@ __global__ void axpy_cols_kernel(double a, const double* X, double* Y, int64_t l
   if (i < n) Y[i + blockIdx.y * ld] = fma(a, X[i + blockIdx.y * ld], Y[i + blockIdx.y * ld]);
 }
 void axpy_cols(double a, const double* X, double* Y, int64_t ld, int64_t n, int s, cudaStream_t st) {
+  if (n <= 0) return;
   axpy_cols_kernel<<<grid2(n, s), NT, 0, st>>>(a, X, Y, ld, n);
   WGP_LAUNCH_CHECK();
 }
 void widen(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n, int s, cudaStream_t st) {
+  if (n <= 0) return;
   widen_kernel<<<grid2(n, s), NT, 0, st>>>(A, lda, B, ldb, n);
   WGP_LAUNCH_CHECK();
 }
 void narrow(const double* A, int64_t lda, float* B, int64_t ldb, int64_t n, int s, cudaStream_t st) {
+  if (n <= 0) return;
   narrow_kernel<<<grid2(n, s), NT, 0, st>>>(A, lda, B, ldb, n);
+  WGP_LAUNCH_CHECK();
+}
+
+void dist_finish(int kind, const double* all, int nranks, int w, int s, ColState cs, SolveCtrl* ctrl,
+                 double* out, bool flag_a, bool flag_b, cudaStream_t st) {
+  if (w > SMAX) throw std::invalid_argument("dist_finish: too many columns");
+  dist_finish_kernel<<<1, NT, 0, st>>>(kind, all, nranks, w, s, cs, ctrl, out, flag_a ? 1 : 0, flag_b ? 1 : 0);
   WGP_LAUNCH_CHECK();
 }
 
@@ -693,16 +780,19 @@ void sgd_check(const float* X, const float* R, int64_t ld, int64_t n, int s, Col
 }
 
 void fill_zero(float* A, int64_t ld, int64_t n, int s, cudaStream_t st) {
+  if (n <= 0) return;
   fill_zero_kernel<<<grid2(n, s), NT, 0, st>>>(A, ld, n);
   WGP_LAUNCH_CHECK();
 }
 void sub_into(const float* A, const float* B, float* out, int64_t ld, int64_t n, int s,
               cudaStream_t st) {
+  if (n <= 0) return;
   sub_kernel<<<grid2(n, s), NT, 0, st>>>(A, B, out, ld, n);
   WGP_LAUNCH_CHECK();
 }
 void copy_cols(const float* A, int64_t lda, float* B, int64_t ldb, int64_t n, int s,
                cudaStream_t st) {
+  if (n <= 0) return;
   copy_kernel<<<grid2(n, s), NT, 0, st>>>(A, lda, B, ldb, n);
   WGP_LAUNCH_CHECK();
 }

@@ -38,7 +38,17 @@ struct ColState {
   double* best;    // CG: smallest exact ||r||^2 seen at a refresh (or the start)
   int* stall;      // CG: refreshes since the last improvement
   int* act;        // CG: 1 snapshot the iterate, 2 restore the snapshot (refresh steps)
+  double* dist_loc = nullptr;  // row-sharded solve: this rank's column totals (see dist_finish)
 };
+
+// Row-sharded reductions: with ColState::dist_loc set, a reduction kernel
+// (cg_init, cg_alpha, cg_update, cg_refresh_norm, norms_convergence) leaves
+// this rank's column totals in dist_loc and skips its epilogue; after the
+// ranks' totals are gathered into all[nranks][w], dist_finish sums them in
+// rank order and runs the epilogue of `kind` (kDistSum: out[c] = total).
+enum : int { kDistSum = 0, kDistInit = 1, kDistAlpha = 2, kDistBeta = 3, kDistRefresh = 4, kDistNorms = 5 };
+void dist_finish(int kind, const double* all, int nranks, int w, int s, ColState cs, SolveCtrl* ctrl,
+                 double* out, bool flag_a, bool flag_b, cudaStream_t st);
 
 // Rows per CTA of the reduction kernels: 256 (one per thread) up to a grid of
 // ~2 CTAs per SM; the same function on host and device.
@@ -47,7 +57,11 @@ __host__ __device__ inline int64_t rows_per_block(int64_t n) {
   const int64_t r = ((want + 255) / 256) * 256;
   return r < 256 ? 256 : r;
 }
-inline int reduce_blocks(int64_t n) { return static_cast<int>((n + rows_per_block(n) - 1) / rows_per_block(n)); }
+// (at least one CTA: a rank without rows still publishes zero totals)
+inline int reduce_blocks(int64_t n) {
+  const int b = static_cast<int>((n + rows_per_block(n) - 1) / rows_per_block(n));
+  return b < 1 ? 1 : b;
+}
 
 // The CG kernels run on fp32 (the tf32 engines' solver state) or fp64 vectors
 // (the fp64 CG path over hv_f64); scalars are fp64 either way.
@@ -56,13 +70,17 @@ template <class T>
 void col_dots(const T* A, const T* B, int64_t ld, int64_t n, int s, double* part,
               unsigned* ticket, double* out, cudaStream_t st);
 
-// CG: before the loop.  R = rhs - H X0 must already be in R; computes
-// rs = ||r||^2, convergence, P = R (active) / 0, and the loop-entry check.
+// CG: before the loop.  R = rhs - H X0 must already be in R; cg_init
+// computes rs = ||r||^2, convergence and the loop-entry check (row-sharded:
+// dist_finish(kDistInit)); cg_seed then sets P = R (active) / 0.
 // pp (optional, fp32 only, here and in cg_direction): P's tf32 planes, written
 // with P (hi at pp[j + c ld], lo at pp[j + (s + c) ld]; for HvParams::vplanes).
 template <class T>
-void cg_init(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs, double* part,
-             SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
+void cg_init(const T* R, int64_t ld, int64_t n, int s, ColState cs, double* part, SolveCtrl* ctrl,
+             cudaStream_t st);
+template <class T>
+void cg_seed(T* P, const T* R, int64_t ld, int64_t n, int s, const int* conv, cudaStream_t st,
+             float* pp = nullptr);
 // alpha_c = rs_c / (p_c . hp_c); non-positive curvature -> kStatusNotPd.
 template <class T>
 void cg_alpha(const T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs,
@@ -89,6 +107,12 @@ void widen(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n, int s
 // Y += a X (fp64, n x s column blocks, leading dimension ld).
 void axpy_cols(double a, const double* X, double* Y, int64_t ld, int64_t n, int s, cudaStream_t st);
 void narrow(const double* A, int64_t lda, float* B, int64_t ldb, int64_t n, int s, cudaStream_t st);
+// out[i + c size] = R[start + i + c ld] for rows start + i in [own0, own1), 0 elsewhere
+// (a rank's share of an AP block residual, row-sharded AP).
+void masked_rows(const float* R, int64_t ld, int64_t start, int64_t size, int64_t own0, int64_t own1, int s,
+                 float* out, const SolveCtrl* ctrl, cudaStream_t st);
+// B[i + c size] = (double) A[i + c size] for an AP block (size x s, contiguous).
+void widen_block(const float* A, double* B, int64_t size, int s, const SolveCtrl* ctrl, cudaStream_t st);
 
 // Convergence from exact residual norms (AP epochs, SGD init): conv_c =
 // bnorm_c == 0 || ||R_c|| <= tol_c bnorm_c; NaN -> kStatusNaN (when check_nan);
