@@ -8,9 +8,16 @@ inputs resident in HBM, timed per launch with CUDA events on the launching
 stream; ``e2e`` is the same H.V through the C-ABI host-pointer entry point
 (``wgp_hv``: pinned host V in, host H.V out, copies inside the timed region).
 Between timed iterations L2 is flushed (a 512 MiB write; the inputs, 3.5 MB,
-would otherwise stay L2-resident).  With --gpus N under torchrun the rows of
-H.V are sharded across ranks (row-block sharding) and the n x s
-result is all-gathered over NCCL; timing is the max over ranks.
+would otherwise stay L2-resident).  With --gpus N under torchrun every rank's
+library context joins one NCCL communicator (wgp_set_comm): the library
+computes the rank's rows of H.V and all-gathers the n x s result itself
+(SURVEY §8e); timing is the max over ranks.
+
+The line also carries ``outer``: ms per marginal-likelihood step (the second
+half of the metric) at configs 2 and 3 through the library's wgp_train --
+row-sharded inside the library under torchrun -- with iterations, converged
+steps and final residuals per solver, and the CPU path's outer-step figures
+under ``cpu_baseline.outer`` (N=1).
 
 ``--impl reference`` times the reference's CPU path -- the CPU oracle's
 restatement of build_kernel_matrices (proj/src/kernel.cpp:120-139) plus the
@@ -46,14 +53,12 @@ def parse():
     ap.add_argument("--hv-impl", default="tc", choices=["tc", "tc_bf16", "simt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--outer", action="store_true",
-                    help="legacy torch-driven row-sharded outer steps under torchrun")
     ap.add_argument("--no-outer", action="store_true", help="skip the per-outer-step timings")
+    ap.add_argument("--comm", action="store_true",
+                    help="N=1: attach a one-rank NCCL communicator (runs the library's sharded code path)")
     ap.add_argument("--no-c3", action="store_true", help="skip the config-3 outer steps")
     ap.add_argument("--outer-steps", type=int, default=5, help="timed outer steps per solver (config 2)")
     ap.add_argument("--outer-warmup", type=int, default=1, help="untimed outer steps before them")
-    ap.add_argument("--outer-config", type=int, default=2, choices=[2, 3],
-                    help="BASELINE config of --outer: 2 (CG / AP / SGD) or 3 (AP, 10-epoch budget)")
     return ap.parse_args()
 
 
@@ -139,24 +144,6 @@ def cpu_baseline(p, seconds):
                       f"s=65), {elapsed:.1f} s"}
 
 
-def outer_spec(datasets, args, sharded_run=False):
-    """The outer-loop workload of `--outer-config` (legacy torch-driven sharded
-    run, `--outer` under torchrun): 2 = BASELINE config 2 with CG and AP,
-    3 = config 3 with AP and a 10-epoch budget."""
-    if args.outer_config == 3:
-        p = datasets.config3()
-        solvers = {"ap": dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=10, block_size=1000)}
-        return (p, "config3 n=391386 d=3 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start, "
-                   "AP 10-epoch budget", solvers, max(1, min(args.steps, 3)), 1)
-    p = datasets.config2()
-    solvers = {
-        "cg": dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=1000),
-        "ap": dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=100, block_size=1000),
-    }
-    return (p, "config2 n=41157 d=9 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start", solvers,
-            max(args.steps, 1), args.warmup)
-
-
 def sgd_learning_rate(wg, ds_X, ds_y, device):
     """The reference's grid search (proj/src/experiment.cpp:133-168, default
     candidates and budget proj/tools/main.cpp:53-54) at config 2's start."""
@@ -171,7 +158,7 @@ def sgd_learning_rate(wg, ds_X, ds_y, device):
     return lr, {"candidates": cands, "budget_steps": 60, "chosen": lr, "seconds": time.perf_counter() - t0}
 
 
-def run_outer(wg, ctx, p, sc, steps, warmup, precision="f64"):
+def run_outer(wg, ctx, p, sc, steps, warmup, precision="f64", ws=1):
     """One warm-started training run on the device; per-step device times of
     the timed steps (CUDA events around each outer step: probes, solve,
     warm-start-distance H.V, gradient, Adam) and what the solver did."""
@@ -185,6 +172,13 @@ def run_outer(wg, ctx, p, sc, steps, warmup, precision="f64"):
     conv = [bool(np.all(r.per_column_relative_residual <= tol * (1 + 1e-9))) for r in timed]
     step = np.array([r.step_ms for r in timed])
     wsd = np.array([r.warm_distance_ms for r in timed])
+    if ws > 1:  # per-step maximum over the ranks
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(np.concatenate([step, step - wsd]), device=f"cuda:{torch.cuda.current_device()}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        both = t.cpu().numpy()
+        step, wsd = both[:len(step)], both[:len(step)] - both[len(step):]
     return {"ms_per_step": float(step.mean()),
             "ms_per_step_without_warm_start_distance": float((step - wsd).mean()),
             "solver_ms_per_step": float(np.mean([r.solver_ms for r in timed])),
@@ -196,7 +190,7 @@ def run_outer(wg, ctx, p, sc, steps, warmup, precision="f64"):
             "config": {k: v for k, v in sc.items() if k != "kind"}}
 
 
-def outer_bench(wg, datasets, device, args):
+def outer_bench(wg, datasets, device, args, ws=1, rank=0):
     """ms per marginal-likelihood step (the second half of BASELINE.json's
     metric) on one GPU through the library's wgp_train:
       config 2 (n=41,157, d=9, 64 pathwise probes + y, RFF 1000, log-space
@@ -206,40 +200,45 @@ def outer_bench(wg, datasets, device, args):
       (solvers.cpp:88,148,206);
       config 3 (n=391,386, d=3): AP, blocks of 1000, 10-epoch budget.
     Each run starts cold at step 1; `outer_warmup` steps are untimed, the
-    next `outer_steps` are timed."""
+    next `outer_steps` are timed.  Under torchrun every context joins an NCCL
+    communicator and the library row-shards the whole outer loop (SGD is
+    single-GPU and skipped); times are the per-step maximum over the ranks."""
     out = {"timing": "CUDA events on the context stream around each outer step (device time; the "
                      "warm-start-distance H.V included, and subtracted in the *_without_* field)",
            "steps_timed": args.outer_steps, "warmup_steps": args.outer_warmup}
+    if ws > 1 or args.comm:
+        out["sharding"] = f"rows over {ws} GPU(s) inside the library (wgp_set_comm, NCCL)"
     p = datasets.config2()
-    ctx = wg.Context(device, hv_impl=args.hv_impl)
+    ctx = make_ctx(wg, device, args, ws, rank)
     ctx.set_data(p.X)
     c2 = {"workload": "config2 n=41157 d=9 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start"}
     runs = [("cg_f64", dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=0), "f64"),
             ("cg_f32", dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=0), "f32"),
             ("ap", dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=0, block_size=1000), "f64")]
-    try:
-        lr, grid = sgd_learning_rate(wg, p.X, p.y, device)
-        runs.append(("sgd", dict(kind="sgd", tol_mean=0.01, tol_samples=0.01, max_iterations=0,
-                                 minibatch_size=1000, momentum=0.9, learning_rate=lr, seed=0), "f64"))
-        c2["sgd_lr_grid_search"] = grid
-    except Exception as e:
-        c2["sgd_lr_grid_search"] = {"error": str(e)[:200]}
+    if ws == 1 and not args.comm:  # SGD is single-GPU
+        try:
+            lr, grid = sgd_learning_rate(wg, p.X, p.y, device)
+            runs.append(("sgd", dict(kind="sgd", tol_mean=0.01, tol_samples=0.01, max_iterations=0,
+                                     minibatch_size=1000, momentum=0.9, learning_rate=lr, seed=0), "f64"))
+            c2["sgd_lr_grid_search"] = grid
+        except Exception as e:
+            c2["sgd_lr_grid_search"] = {"error": str(e)[:200]}
     for name, sc, prec in runs:
         try:
-            c2[name] = run_outer(wg, ctx, p, sc, args.outer_steps, args.outer_warmup, prec)
+            c2[name] = run_outer(wg, ctx, p, sc, args.outer_steps, args.outer_warmup, prec, ws)
         except Exception as e:  # report, keep the other solvers' numbers
             c2[name] = {"error": str(e)[:200]}
     ctx.close()
     out["c2"] = c2
     if not args.no_c3:
         p3 = datasets.config3()
-        ctx = wg.Context(device, hv_impl=args.hv_impl)
+        ctx = make_ctx(wg, device, args, ws, rank)
         ctx.set_data(p3.X)
         c3 = {"workload": "config3 n=391386 d=3 s=65, pathwise RFF 1000, log-space Adam lr 0.1, warm start, "
                           "AP blocks of 1000 with a 10-epoch budget"}
         try:
             c3["ap"] = run_outer(wg, ctx, p3, dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=10,
-                                                   block_size=1000), min(args.outer_steps, 2), 1)
+                                                   block_size=1000), min(args.outer_steps, 2), 1, "f64", ws)
         except Exception as e:
             c3["ap"] = {"error": str(e)[:200]}
         ctx.close()
@@ -287,43 +286,39 @@ def cpu_outer_baseline(datasets, outer, seconds):
     return res
 
 
-def outer_sharded(wg, datasets, device, args, ws, rank):
-    """The `--outer-config` outer loop (outer_spec; CG and AP) row-sharded over `ws` GPUs
-    (sharded.sharded_train on the library's operators: CG with per-iteration
-    all-gathers of the direction, AP with per-block exchanges, the gradient
-    summed in rank order).  Per-step time: host clock around each step with
-    the device synchronised, maximum over ranks."""
-    import torch
-    import torch.distributed as dist
+class _StdoutToStderr:
+    """fd-level redirect of stdout into stderr (NCCL prints its version banner
+    on stdout at communicator creation; rank 0's stdout is the JSON line)."""
 
-    from paper_2405_18328_b200 import sharded
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
 
-    p, workload, solvers, k_steps, w_steps = outer_spec(datasets, args, sharded_run=True)
-    n = p.X.shape[0]
-    r0, r1 = sharded.row_range(n, rank, ws)
-    ctx = wg.Context(device, hv_impl=args.hv_impl)
-    ctx.set_data(p.X)
-    ctx.set_split_global(False)  # strong scaling: J splits keyed on the shard's rows
-    ops = sharded.device_train_ops(ctx, r0, r1)
-    n_steps = w_steps + k_steps
-    out = {"workload": workload,
-           "sharding": f"rows{ws}", "timing": "host clock per outer step (device synchronised), max over ranks",
-           "steps": k_steps, "warmup_steps": w_steps}
-    for name, sc in solvers.items():
-        cfg = wg.TrainConfig(steps=n_steps, learning_rate=0.1, num_probes=64, mode="warm", seed=0,
-                             transform="log", estimator="pathwise", rff_features=1000, init_noise=0.5,
-                             init_constrained=1.0, solver=wg.SolverConfig(**sc))
-        torch.cuda.synchronize()
-        steps = sharded.sharded_train(ops, p.y, cfg)
-        timed = steps[w_steps:]
-        t = torch.tensor([1e3 * float(np.mean([s.step_seconds for s in timed]))], device=f"cuda:{device}")
-        if ws > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        out[name] = {"ms_per_step": float(t.item()),
-                     "iterations_mean": float(np.mean([s.solver_iterations for s in timed])),
-                     "config": {k: v for k, v in sc.items() if k != "kind"}}
-    ctx.close()
-    return out
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
+def make_ctx(wg, device, args, ws, rank, **kw):
+    """A library context; under torchrun it joins an NCCL communicator of the
+    ws ranks (wgp_set_comm: the library row-shards H.V, the solvers and the
+    outer loop itself).  torch.distributed only carries the 128-byte NCCL id."""
+    ctx = wg.Context(device, hv_impl=args.hv_impl, **kw)
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{device}")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(wg.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        with _StdoutToStderr():
+            ctx.set_comm(rank, ws, bytes(uid.cpu().numpy().tobytes()))
+    elif args.comm:  # the sharded code path on a one-rank communicator (plumbing check)
+        with _StdoutToStderr():
+            ctx.set_comm(0, 1, wg.nccl_unique_id())
+    return ctx
 
 
 def run_reference(args):
@@ -397,22 +392,20 @@ def main():
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with _StdoutToStderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
     import paper_2405_18328_b200 as wg
     from paper_2405_18328_b200 import datasets
 
     p = datasets.config1()
     n, d = p.X.shape
     s = p.V.shape[1]
-    ctx = wg.Context(local, hv_impl=args.hv_impl)
+    ctx = make_ctx(wg, local, args, ws, rank)
     ctx.set_data(p.X)
     ctx.set_hyper([*p.lengthscales, p.signal, p.noise])
-    # row shard of this rank (aligned to the 128-row tile grid)
-    tiles = -(-n // 128)
-    t0_, t1_ = tiles * rank // ws, tiles * (rank + 1) // ws
-    r0, r1 = min(n, t0_ * 128), min(n, t1_ * 128)
+    _, _, r0, r1, ldc = ctx.shard_info()
     m = r1 - r0
-    ctx.set_rows(r0, r1)
     if ws > 1:
         # strong scaling of one H.V: J splits keyed on the shard's rows (more
         # CTAs per GPU on small shards; rows equal to fp32 rounding, not bitwise)
@@ -420,18 +413,14 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream)
     dev = torch.device("cuda", local)
     Vt = torch.from_numpy(np.ascontiguousarray(p.V.T)).to(dev)  # [s][n] = column-major n x s
-    out_local = torch.empty((s, max(m, 1)), device=dev)
-    gathered = torch.empty((ws, s, tiles * 128 // ws + 128), device=dev) if ws > 1 else None
+    # sharded: the library computes this rank's rows and all-gathers the n x s
+    # result over NCCL inside wgp_hv_device (out holds all rows, leading dim ldc)
+    sharded = ws > 1 or args.comm
+    out_dev = torch.empty((s, ldc if sharded else max(m, 1)), device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, device=dev)
 
     def one_step():
-        ctx.hv_device(Vt.data_ptr(), n, s, out_local.data_ptr(), max(m, 1))
-        if ws > 1:
-            import torch.distributed as dist
-            with torch.cuda.stream(stream):
-                chunk = torch.zeros((s, gathered.shape[2]), device=dev)
-                chunk[:, :m] = out_local[:, :m]
-                dist.all_gather_into_tensor(gathered, chunk)
+        ctx.hv_device(Vt.data_ptr(), n, s, out_dev.data_ptr(), out_dev.shape[1])
 
     # clocks are sampled from the warm-up through the timed H.V steps and the
     # outer-step timings (a 20-step H.V region lasts ~5 ms, shorter than one
@@ -475,7 +464,8 @@ def main():
 
     # e2e through the C-ABI with host buffers (pinned), copies in the timed region
     Vh = torch.from_numpy(np.asfortranarray(p.V).T.copy()).pin_memory()
-    outh = torch.empty((s, m), pin_memory=True)
+    m_out = n if sharded else m  # sharded wgp_hv returns the all-gathered n x s
+    outh = torch.empty((s, m_out), pin_memory=True)
     lib = wg.load()
     import ctypes as C
     e2e_times = []
@@ -498,11 +488,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    # multi-GPU outer steps run on every rank (collectives), before rank 0 reports
-    outer_multi = outer_sharded(wg, datasets, local, args, ws, rank) if (args.outer and ws > 1) else None
+    # outer steps run on every rank (collectives inside the library), before rank 0 reports
     outer = None
-    if ws == 1 and not args.no_outer:
-        outer = outer_bench(wg, datasets, local, args)
+    if not args.no_outer:
+        outer = outer_bench(wg, datasets, local, args, ws, rank)
     clk.__exit__()
     if rank != 0:
         if ws > 1:
@@ -558,7 +547,7 @@ def main():
                    "n": n, "d": d, "s": s, "hv_impl": args.hv_impl, "l2": "flushed (512 MiB write)",
                    "parallelism": f"rows{ws}" if ws > 1 else "single"},
         "e2e": {"value": n * n / (e2e_ms / 1e3), "unit": UNIT,
-                "h2d_bytes_per_step": int(n * s * 4), "d2h_bytes_per_step": int(m * s * 4),
+                "h2d_bytes_per_step": int(n * s * 4), "d2h_bytes_per_step": int(m_out * s * 4),
                 "ms_per_step": e2e_ms},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_profile": traffic_profile,
@@ -570,8 +559,6 @@ def main():
     }
     if outer is not None:
         line["outer"] = outer
-    if outer_multi is not None:
-        line["outer_sharded"] = outer_multi
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(p, args.cpu_seconds)
         if outer is not None:
