@@ -32,13 +32,20 @@
 namespace wgp {
 namespace {
 
-constexpr int TM = 64;   // output rows per CTA (4 warps x 16 rows)
-constexpr int TJ = 32;   // contracted points per tile
-constexpr int NT = 128;  // threads
-constexpr int KS = TM + 8;   // fp64 row stride of the K^T tile: conflict-free A fragments
+#ifndef WGP_HV64_TM
+#define WGP_HV64_TM 128
+#endif
+constexpr int TM = WGP_HV64_TM;  // output rows per CTA: one warp per 16 rows
+constexpr int TJ = 32;           // contracted points per tile
+constexpr int NT = 2 * TM;       // threads (TM / 16 warps)
+constexpr int NW = NT / 32;
+constexpr int KS = TM + 8;   // fp32 row stride of the K^T tile: conflict-free A fragments
 constexpr int VJ = TJ + 4;   // fp64 column stride of the V tile: conflict-free B fragments
 constexpr int kMaxNF = 10;   // <= 80 columns per launch (8 per DMMA fragment)
-constexpr int kCtasPerSm = 3;
+// residency: <= 128 registers per thread (2 x 256 or 4 x 128 threads)
+constexpr int kCtasPerSm = TM == 128 ? 2 : 3;
+constexpr int RA = TM / 32;        // K phase: rows lane + 32 a, a < RA
+constexpr int PB = TJ / NW;        // K phase: points PB w + b, b < PB
 
 __host__ __device__ inline int64_t jtiles(int64_t n) { return (n + TJ - 1) / TJ; }
 
@@ -79,23 +86,23 @@ __device__ __forceinline__ void load_tile(const Hv64Params& p, int64_t jt, doubl
   cp_async_commit();
 }
 
-// Per tile: (1) the K tile, 64 x 32 entries, 16 per thread, in fp32 from
-// direct differences, stored as fp64 K^T (thread (ty, tx) takes rows tx + 16a
-// and points 4 ty + b: a warp's stores are two contiguous 128-byte runs);
-// (2) the product on the fp64 tensor core: warp w owns rows 16w..16w+15 and
-// every column, 2 x NF m8n8k4 DMMAs per 4 points.  The next tile's V and
-// coordinates stream in with cp.async during the current tile (double
-// buffered); three CTAs per SM overlap one CTA's K phase (FP32 / MUFU) with
-// the others' DMMAs.
+// Per tile: (1) the K tile, TM x 32 entries, 16 per thread, in fp32 from
+// direct differences, stored as K^T (fp32; lane takes rows lane + 32 a, warp
+// w points PB w + b: a warp's stores are 128-byte runs); (2) the product on
+// the fp64 tensor core: warp w owns rows 16 w .. 16 w + 15 and every column,
+// 2 x NF m8n8k4 DMMAs per 4 points, K widened to fp64 in the A fragment.
+// The next tile's V and coordinates stream in with cp.async during the
+// current tile (double buffered); two CTAs per SM overlap one CTA's K phase
+// (FP32 / MUFU) with the other's DMMAs.
 template <int NF>
 __global__ void __launch_bounds__(NT, kCtasPerSm) hv64_kernel(Hv64Params p, int64_t m_pad, int splits) {
   if (p.done && *p.done) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int dps = p.dp + 1;  // odd stride: conflict-free row reads of xi
-  double* ks = reinterpret_cast<double*>(smem_raw);   // [TJ][KS]
-  double* vsb = ks + TJ * KS;                          // 2 x [8 NF][VJ]
-  float* xjb = reinterpret_cast<float*>(vsb + 2 * 8 * NF * VJ);  // 2 x [TJ][dp]
-  float* xi = xjb + 2 * TJ * p.dp;                     // [TM][dps]
+  double* vsb = reinterpret_cast<double*>(smem_raw);            // 2 x [8 NF][VJ]
+  float* ks = reinterpret_cast<float*>(vsb + 2 * 8 * NF * VJ);  // [TJ][KS]
+  float* xjb = ks + TJ * KS;                                     // 2 x [TJ][dp]
+  float* xi = xjb + 2 * TJ * p.dp;                               // [TM][dps]
   __shared__ int64_t grow_s[TM];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -117,7 +124,6 @@ __global__ void __launch_bounds__(NT, kCtasPerSm) hv64_kernel(Hv64Params p, int6
     xi[r * dps + k] = g >= 0 ? p.xs[g * p.dp + k] : 0.f;
   }
 
-  const int ty = tid / 16, tx = tid % 16;
   double acc[2][NF][2];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
@@ -131,35 +137,34 @@ __global__ void __launch_bounds__(NT, kCtasPerSm) hv64_kernel(Hv64Params p, int6
     const float* xj = xjb + buf * TJ * p.dp;
     cp_async_wait_all();
     __syncthreads();  // tile t landed; every warp is done with tile t - 1 (ks, other buffers)
-    {  // K tile: rows tx + 16 a, points 4 ty + b; bitwise symmetric in (i, j)
-      float r2[4][4];
+    {  // K tile: rows lane + 32 a, points PB warp + b; bitwise symmetric in (i, j)
+      float r2[RA][PB];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < RA; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) r2[a][b] = 0.f;
+        for (int b = 0; b < PB; ++b) r2[a][b] = 0.f;
       for (int k = 0; k < p.d; ++k) {  // the padded coordinates are zero: skip them
-        float xa[4], xb[4];
+        float xa[RA], xb[PB];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) xa[a] = xi[(tx + 16 * a) * dps + k];
+        for (int a = 0; a < RA; ++a) xa[a] = xi[(lane + 32 * a) * dps + k];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) xb[b] = xj[(4 * ty + b) * p.dp + k];
+        for (int b = 0; b < PB; ++b) xb[b] = xj[(PB * warp + b) * p.dp + k];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < RA; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
+          for (int b = 0; b < PB; ++b) {
             const float df = xa[a] - xb[b];
             r2[a][b] = fmaf(df, df, r2[a][b]);
           }
       }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int64_t gj = jt + 4 * ty + b;
+      for (int b = 0; b < PB; ++b) {
+        const int64_t gj = jt + PB * warp + b;
         const bool valid = gj < p.n;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < RA; ++a) {
           const float kv = matern_from_u(sqrt_approx(r2[a][b]), hsf2, ha);
-          ks[(4 * ty + b) * KS + tx + 16 * a] =
-              (valid && gj != grow_s[tx + 16 * a]) ? static_cast<double>(kv) : 0.0;
+          ks[(PB * warp + b) * KS + lane + 32 * a] = (valid && gj != grow_s[lane + 32 * a]) ? kv : 0.f;
         }
       }
     }
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(NT, kCtasPerSm) hv64_kernel(Hv64Params p, int6
     if (t + 1 < t1) load_tile<NF>(p, jt + TJ, vsb + (buf ^ 1) * 8 * NF * VJ, xjb + (buf ^ 1) * TJ * p.dp);
     // product: A = K rows (16 w + 8 r + lane / 4), points 4 kk + lane % 4;
     // B = V points 4 kk + lane % 4, columns 8 f + lane / 4
-    const double* ka = ks + (lane & 3) * KS + 16 * warp + (lane >> 2);
+    const float* ka = ks + (lane & 3) * KS + 16 * warp + (lane >> 2);
     const double* vb = vs + (lane >> 2) * VJ + (lane & 3);
 #pragma unroll 2
     for (int kk = 0; kk < TJ / 4; ++kk) {
@@ -214,7 +219,7 @@ __global__ void hv64_reduce_kernel(Hv64Params p, int64_t m_pad, int splits) {
 
 template <int NF>
 size_t smem_bytes(int dp) {
-  return sizeof(double) * (TJ * KS + 2 * 8 * NF * VJ) + sizeof(float) * (2 * TJ * dp + TM * (dp + 1));
+  return sizeof(double) * 2 * 8 * NF * VJ + sizeof(float) * (TJ * KS + 2 * TJ * dp + TM * (dp + 1));
 }
 
 template <int NF>
@@ -242,7 +247,9 @@ int hv64_splits(int64_t n) {
     const double waves = static_cast<double>(ctas) / wave;
     if (waves / std::ceil(waves) >= 0.9) return static_cast<int>(s);
   }
-  return static_cast<int>(std::min<int64_t>(smax, std::max<int64_t>(1, ceil_div(2 * wave, rt))));
+  // small operators (fewer than two waves even at 4 tiles per split): one
+  // wave, as many CTAs as fit (config 0: 32 row tiles x 13 splits = 416 of 444)
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(smax, wave / rt)));
 }
 
 size_t hv64_workspace_bytes(int64_t n, int64_t m, int s) {

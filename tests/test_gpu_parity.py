@@ -68,7 +68,7 @@ def test_hv_config1_full_size_row_samples(ctx, impl):
     assert rel(out2, 2 * out[:, :5].astype(np.float64) - out[:, 5:10]) <= 1e-5
 
 
-@pytest.mark.parametrize("cfg,impl,s", [("c3", "tc", 65), ("c3", "simt", 65), ("c4", "tc", 17)])
+@pytest.mark.parametrize("cfg,impl,s", [("c3", "tc", 65), ("c3", "simt", 65), ("c3", "f64", 65), ("c4", "tc", 65)])
 def test_hv_full_size_dense_accumulation(ctx, cfg, impl, s):
     """Full-size BASELINE configs 3 (n=391,386, d=3, unit lengthscales on the
     unit cube: every entry of K is large) and 4 (n=1,844,352): the fp32
@@ -77,10 +77,10 @@ def test_hv_full_size_dense_accumulation(ctx, cfg, impl, s):
     p = datasets.CONFIGS[cfg]()
     n = p.X.shape[0]
     V = np.random.default_rng(7).standard_normal((n, s)).astype(np.float32)
-    ctx.set_hv_impl(impl)
+    ctx.set_hv_impl(impl if impl != "f64" else "tc")
     ctx.set_data(p.X)
     ctx.set_hyper([*p.lengthscales, p.signal, p.noise])
-    out = ctx.hv(V)
+    out = ctx.hv_f64(V.astype(np.float64)) if impl == "f64" else ctx.hv(V)
     ctx.set_hv_impl("tc")
     for r0, r1 in ((0, 128), (n // 2, n // 2 + 64), (n - 64, n)):
         ref = orc.hv_rows(p.X, p.lengthscales, p.signal, p.noise, V, r0, r1)
