@@ -212,6 +212,7 @@ struct Ctx {
   // fp64 CG (cg_precision == WGP_CG_F64): solver state and the hv_f64 split partials
   Buf B64, X64, R64, P64, HP64, Rt64, Xbest64, Rbest64, hv64_ws;
   Buf linv_ptrs;  // AP: device pointer array of the batched inverse
+  Buf sgd_xsq;    // SGD: running ||X||_F^2
   Buf Rpart;      // row-sharded AP: this rank's share of a block residual
   Buf tr_rhs, tr_sol0, tr_sol1, tr_res, tr_sol64a, tr_sol64b;  // train(): solver state across steps
   Buf api_B, api_X0, api_Xs, api_Rs;  // wgp_solve staging
@@ -713,12 +714,18 @@ struct Ctx {
     cg_seed(Pp + r, R + r, ld, m, s, cs.conv, st, PPr);
     cg_snapshot(Xo + r, R + r, Xb + r, Rb + r, ld, m, s, cs, c, true, st);
     const int* done = &c->done;
+    static const bool no_fused = getenv("WGP_CG_NO_FUSED") != nullptr;
+    bool use_fused = !no_fused;
     auto iteration = [&](bool refresh) {
       if (sh) {
         gather_rows(Pp, s);
         if (PPp) gather_rows(PPp, 2 * s);
       }
       cg_hv(Pp, s, HPp, kHvStore, nullptr, done, PPp);
+      if (!refresh && !sh && use_fused) {  // alpha + update + direction in one cooperative kernel
+        if (cg_fused(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, st, PPp)) return;
+        use_fused = false;
+      }
       cg_alpha(Pp + r, HPp + r, ld, m, s, cs, pt, c, st);
       if (sh) dist_reduce(kDistAlpha, s, s);
       if (!refresh) {
@@ -774,15 +781,28 @@ struct Ctx {
       if (!gr) {
         if (cg_graphs.size() >= 8) drop_cg_graphs();
         CgGraph g{B, Xo, R, s, impl, gen, {nullptr, nullptr}};
-        for (int v = 0; v < 2; ++v) {
-          cudaGraph_t graph;
-          WGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-          for (int k = 0; k < kChunk; ++k) iteration(v == 1 && k == kChunk - 1);
-          WGP_CUDA(cudaStreamEndCapture(st, &graph));
-          const cudaError_t ie = cudaGraphInstantiate(&g.exec[v], graph, 0);
-          cudaGraphDestroy(graph);
-          WGP_CUDA(ie);
+        // capture; a failed capture with the cooperative fused kernel is
+        // retried once with the three-kernel iteration
+        bool ok = false;
+        for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+          ok = true;
+          for (int v = 0; v < 2 && ok; ++v) {
+            cudaGraph_t graph = nullptr;
+            WGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            for (int k = 0; k < kChunk; ++k) iteration(v == 1 && k == kChunk - 1);
+            const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+            ok = ce == cudaSuccess && graph && cudaGraphInstantiate(&g.exec[v], graph, 0) == cudaSuccess;
+            if (graph) cudaGraphDestroy(graph);
+          }
+          if (!ok) {
+            cudaGetLastError();
+            for (auto& e : g.exec)
+              if (e) cudaGraphExecDestroy(e), e = nullptr;
+            if (!use_fused) break;
+            use_fused = false;
+          }
         }
+        if (!ok) throw DeviceError("cg_solve: CUDA graph capture failed");
         if (alloc_generation().load() != gen) {  // a workspace moved while capturing
           for (auto e : g.exec) cudaGraphExecDestroy(e);
         } else {
@@ -1037,6 +1057,9 @@ struct Ctx {
     // the device runs round r, then copied asynchronously
     idx.ensure(sizeof(int) * m * K * 2);
     sgd_hidx.ensure(sizeof(int) * m * K * 2);
+    sgd_xsq.ensure(sizeof(double));
+    part.ensure(sizeof(double) * static_cast<size_t>(ceil_div(m, 256)) * 2 * s);  // sgd_step's partials
+    double* xsq = sgd_xsq.as<double>();
     reset_ctrl(max_steps);
     const ColState cs = colstate();
     SolveCtrl* c = dctrl();
@@ -1057,27 +1080,77 @@ struct Ctx {
           hidx[static_cast<size_t>(k) * m + i] = static_cast<int>(pool[i]);
         }
     };
-    int cur = 0;
-    draw(sgd_hidx.as<int>());
-    while (true) {
-      const SolveCtrl& h = poll();
-      if (h.done) {
-        if (h.status != kStatusOk) fail(h, 2);
-        out.iterations = h.it;
-        return;
-      }
-      const size_t off = static_cast<size_t>(cur) * m * K;
+    // One round = the copy of its K index vectors + K steps, each the
+    // minibatch residual H.V (batch = B[I] - H[I, :] X, :241-243) and one
+    // sgd_step (momentum scatter, :247-252, with the residual-estimate and
+    // iterate norms updated from the minibatch rows' changes, then the checks
+    // of :254-258).  The norms are recomputed exactly every kResync rounds.
+    // After one eager round sizes every workspace, the two rounds (index
+    // halves) replay as captured CUDA graphs: a step is launch-bound
+    // otherwise (~5 small launches for ~30 us of GPU work at config 2).
+    auto round = [&](int h) {
+      const size_t off = static_cast<size_t>(h) * m * K;
       WGP_CUDA(cudaMemcpyAsync(idx.as<int>() + off, sgd_hidx.as<int>() + off, sizeof(int) * m * K,
                                cudaMemcpyHostToDevice, st));
       for (int k = 0; k < K; ++k) {
         const int* ik = idx.as<int>() + off + static_cast<size_t>(k) * m;
-        // batch = B[I] - H[I, :] X  (:241-243)
         hv(Xo, ld, s, batch.as<float>(), m, kHvResidual, B, ld, 0, n, ik, 0, m, &c->done, true, XP.as<float>(),
            ld);
-        sgd_scatter(Xo, R, vel.as<float>(), ld, ik, m, s, batch.as<float>(),
-                    static_cast<float>(cfg.momentum), gs, ss, XP.as<float>(), c, st);
-        sgd_check(Xo, R, ld, n, s, cs, pt, c, st);
+        sgd_step(Xo, R, vel.as<float>(), ld, ik, m, s, batch.as<float>(), static_cast<float>(cfg.momentum), gs, ss,
+                 XP.as<float>(), cs, xsq, pt, c, st);
       }
+    };
+    static const bool no_graphs = getenv("WGP_NO_GRAPHS") != nullptr;
+    cudaGraphExec_t graphs[2] = {nullptr, nullptr};
+    struct Drop {
+      cudaGraphExec_t* g;
+      ~Drop() {
+        for (int h = 0; h < 2; ++h)
+          if (g[h]) cudaGraphExecDestroy(g[h]);
+      }
+    } drop{graphs};
+    bool eager_done = false, tried = false;
+    int cur = 0;
+    constexpr int kResync = 8;  // rounds between exact norm re-syncs (fp64 running sums drift ~1e-16 per step)
+    int64_t rounds = 0;
+    draw(sgd_hidx.as<int>());
+    while (true) {
+      const SolveCtrl& hc = poll();
+      if (hc.done) {
+        if (hc.status != kStatusOk) fail(hc, 2);
+        out.iterations = hc.it;
+        return;
+      }
+      if (eager_done && !tried && !no_graphs && !tc.profiling) {
+        tried = true;
+        const uint64_t gen = alloc_generation().load();
+        bool ok = true;
+        for (int h = 0; h < 2 && ok; ++h) {
+          cudaGraph_t graph = nullptr;
+          WGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          try {
+            round(h);
+          } catch (...) {
+            ok = false;
+          }
+          const cudaError_t ee = cudaStreamEndCapture(st, &graph);
+          ok = ok && ee == cudaSuccess && graph && alloc_generation().load() == gen &&
+               cudaGraphInstantiate(&graphs[h], graph, 0) == cudaSuccess;
+          if (graph) cudaGraphDestroy(graph);
+        }
+        if (!ok) {  // eager rounds from here on
+          for (int h = 0; h < 2; ++h)
+            if (graphs[h]) cudaGraphExecDestroy(graphs[h]);
+          graphs[0] = graphs[1] = nullptr;
+          cudaGetLastError();
+        }
+      }
+      if (rounds++ % kResync == 0) sgd_norms(Xo, R, ld, n, s, cs, xsq, pt, c, st);
+      if (graphs[cur])
+        WGP_CUDA(cudaGraphLaunch(graphs[cur], st));
+      else
+        round(cur);
+      eager_done = true;
       // the next round's indices while the device runs this one (its pinned
       // half was last read by the copy two rounds ago, complete at the poll)
       cur ^= 1;

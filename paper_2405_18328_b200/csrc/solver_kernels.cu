@@ -3,6 +3,8 @@
 // CG :81-139, AP :141-196, SGD :198-263; see solver_kernels.cuh.
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "solver_kernels.cuh"
 
@@ -340,6 +342,135 @@ __global__ void cg_direction_kernel(T* P, const T* R, int64_t ld, int64_t n, int
   loop_check(s, cs, ctrl, true);
 }
 
+// Grid-wide barrier for cooperatively launched kernels (all CTAs resident).
+__device__ void grid_sync(SolveCtrl* ctrl) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = &ctrl->bar_gen;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(&ctrl->bar_count, 1u) == gridDim.x * gridDim.y - 1) {
+      ctrl->bar_count = 0;
+      __threadfence();
+      atomicAdd(&ctrl->bar_gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// This CTA's column partials (its rows, its column groups) -> part[bx s + c].
+__device__ void store_partials(Red& red, int s, double* part) {
+  __syncthreads();
+  for (int c = threadIdx.x; c < s; c += blockDim.x) {
+    if (!my_col(c)) continue;
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t += red.v[w][c];
+    part[static_cast<int64_t>(blockIdx.x) * s + c] = t;
+  }
+}
+
+template <class T>
+__global__ void cg_fused_kernel(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs,
+                                double* part, SolveCtrl* ctrl, float* pp) {
+  if (ctrl->done) return;  // read once by every CTA; CTA 0 updates the control state last
+  __shared__ Red red;
+  __shared__ int sconv[SMAX], snew[SMAX];
+  __shared__ double scoef[SMAX], srs[SMAX];
+  __shared__ int sfail;
+  ROWS_OF_BLOCK
+  for (int c = threadIdx.x; c < s; c += NT) {  // CTA 0 rewrites the column state at the end
+    sconv[c] = cs.conv[c];
+    srs[c] = cs.rs[c];
+  }
+  if (threadIdx.x == 0) sfail = 0;
+  __syncthreads();
+  // alpha_c = rs_c / (p_c . Hp_c)  (cg_alpha)
+  cols4(s, rb, re, ld, red, [&](int c, int64_t e) {
+    return sconv[c] ? 0.0 : static_cast<double>(P[e]) * static_cast<double>(HP[e]);
+  });
+  store_partials(red, s, part);
+  grid_sync(ctrl);
+  block_totals(part, s, red.v[0]);
+  for (int c = threadIdx.x; c < s; c += NT) {
+    if (sconv[c]) continue;
+    const double pHp = red.v[0][c];
+    if (!(pHp > 0.0)) sfail = kStatusNotPd;
+    scoef[c] = srs[c] / pHp;
+  }
+  __syncthreads();
+  if (sfail) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+      ctrl->status = kStatusNotPd;
+      ctrl->fail_it = ctrl->it;
+      ctrl->done = 1;
+    }
+    return;
+  }
+  // x += alpha p, r -= alpha Hp, ||r||^2  (cg_update); rs_new totals in part + gridDim.x s
+  double* part2 = part + static_cast<int64_t>(gridDim.x) * s;
+  cols4(s, rb, re, ld, red, [&](int c, int64_t e) {
+    if (sconv[c]) return 0.0;
+    const double a = scoef[c];
+    X[e] = axpy(a, P[e], X[e]);
+    const T r = axpy(-a, HP[e], R[e]);
+    R[e] = r;
+    return static_cast<double>(r) * r;
+  });
+  store_partials(red, s, part2);
+  grid_sync(ctrl);
+  block_totals(part2, s, red.v[0]);
+  // beta / convergence (beta_epilogue without restart)
+  for (int c = threadIdx.x; c < s; c += NT) {
+    snew[c] = sconv[c];
+    if (sconv[c]) continue;
+    const double rs_new = red.v[0][c];
+    if (!isfinite(rs_new)) sfail = kStatusNaN;
+    if (sqrt(rs_new) <= cs.tol[c] * cs.bnorm[c]) {
+      snew[c] = 2;
+      scoef[c] = 0.0;
+    } else {
+      scoef[c] = rs_new / srs[c];
+    }
+  }
+  __syncthreads();
+  const bool lead = blockIdx.x == 0 && blockIdx.y == 0;
+  if (sfail) {
+    if (lead && threadIdx.x == 0) {
+      ctrl->status = kStatusNaN;
+      ctrl->fail_it = ctrl->it;
+      ctrl->done = 1;
+    }
+    return;
+  }
+  // p = r + beta p / 0 for the just-converged  (cg_direction)
+  for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
+    for (int c0 = 4 * static_cast<int>(blockIdx.y); c0 < s; c0 += 4 * static_cast<int>(gridDim.y)) {
+#pragma unroll
+      for (int c = c0; c < c0 + 4; ++c) {
+        if (c >= s) break;
+        const int stc = snew[c];
+        if (stc == 1 || stc == 3) continue;
+        const int64_t e = i + c * ld;
+        const T v = stc == 2 ? T(0) : axpy(scoef[c], P[e], R[e]);
+        P[e] = v;
+        put_planes(pp, e, static_cast<int64_t>(s) * ld, v);
+      }
+    }
+  }
+  if (!lead) return;
+  // the column state and the loop check, once
+  for (int c = threadIdx.x; c < s; c += NT) {
+    if (sconv[c]) continue;
+    cs.rs[c] = red.v[0][c];
+    cs.beta[c] = scoef[c];
+    cs.conv[c] = snew[c] == 2 ? 1 : 0;
+  }
+  loop_check(s, cs, ctrl, true);
+}
+
 // restart comment: see beta_epilogue.  The reference iterates to max_iterations
 // regardless; in fp64 the tolerances it is used with are reachable, in fp32
 // an unreachable one let the iterate drift and blow up between refreshes
@@ -498,6 +629,107 @@ __global__ void sgd_scatter_kernel(float* X, float* R, float* vel, int64_t ld, c
   }
 }
 
+// sgd_step: CTA (bx, c) scatters rows [256 bx, 256 bx + 256) of column c and
+// deposits its column-c change of ||R||^2 and ||X||^2; the last CTA folds the
+// changes in fixed order (column c: bx ascending; X: c, then bx) and runs the
+// checks of sgd_check_kernel.
+__global__ void sgd_step_kernel(float* X, float* R, float* vel, int64_t ld, const int* idx, int64_t m, int s,
+                                const float* batch, float mu, float gs, float ss, float* xp, ColState cs,
+                                double* xsq, double* part, SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  double dr = 0.0, dx = 0.0;
+  if (i < m) {
+    const int64_t row = idx[i];
+    const int64_t e = row + c * ld;
+    const float br = batch[i + c * m];
+    const float v = mu * vel[e] - gs * br;
+    vel[e] = v;
+    const float x0 = X[e], r0 = R[e];
+    const float x = x0 - ss * v;
+    X[e] = x;
+    R[e] = br;
+    if (xp) {
+      const float hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+      xp[e] = hi;
+      xp[e + static_cast<int64_t>(s) * ld] = x - hi;
+    }
+    dr = static_cast<double>(br) * br - static_cast<double>(r0) * r0;
+    dx = static_cast<double>(x) * x - static_cast<double>(x0) * x0;
+  }
+  __shared__ double sr[NT / 32], sx[NT / 32];
+  dr = warp_sum(dr);
+  dx = warp_sum(dx);
+  if ((threadIdx.x & 31) == 0) {
+    sr[threadIdx.x >> 5] = dr;
+    sx[threadIdx.x >> 5] = dx;
+  }
+  __syncthreads();
+  const unsigned gx = gridDim.x;
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < NT / 32; ++w) {
+      a += sr[w];
+      b += sx[w];
+    }
+    part[static_cast<int64_t>(c) * gx + blockIdx.x] = a;
+    part[static_cast<int64_t>(s) * gx + static_cast<int64_t>(c) * gx + blockIdx.x] = b;
+  }
+  __threadfence();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(&ctrl->ticket, 1u) == gx * gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // thread cc folds column cc's gx partials in order (column s + c: column
+  // c's change of ||X||^2); the loads of all columns are in flight together
+  __shared__ double sdx[SMAX];
+  for (int cc = threadIdx.x; cc < 2 * s; cc += NT) {
+    double t = 0.0;
+    for (unsigned b = 0; b < gx; ++b) t += __ldcg(part + static_cast<int64_t>(cc) * gx + b);
+    if (cc < s) {
+      const double r2 = cs.rs[cc] + t;
+      cs.rs[cc] = r2;
+      cs.conv[cc] = (cs.bnorm[cc] == 0.0 || sqrt(fmax(r2, 0.0)) <= cs.tol[cc] * cs.bnorm[cc]) ? 1 : 0;
+    } else {
+      sdx[cc - s] = t;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x2 = *xsq;
+    for (int cc = 0; cc < s; ++cc) x2 += sdx[cc];
+    *xsq = x2;
+    const double xn = sqrt(fmax(x2, 0.0));
+    if (!isfinite(xn) || xn > 1e12) {
+      ctrl->status = kStatusDiverged;
+      ctrl->fail_it = ctrl->it;
+    }
+  }
+  loop_check(s, cs, ctrl, true);
+}
+
+// exact re-sync of sgd_step's running norms (reduction pattern of sgd_check)
+__global__ void sgd_norms_kernel(const float* X, const float* R, int64_t ld, int64_t n, int s, ColState cs,
+                                 double* xsq, double* part, SolveCtrl* ctrl) {
+  if (ctrl->done) return;
+  __shared__ Red red;
+  ROWS_OF_BLOCK
+  cols4(2 * s, rb, re, ld, red, [&](int c, int64_t e) {
+    const double v = c < s ? static_cast<double>(R[e]) : static_cast<double>(X[e - static_cast<int64_t>(s) * ld]);
+    return v * v;
+  });
+  if (!publish(red, 2 * s, part, ctrl)) return;
+  for (int c = threadIdx.x; c < s; c += NT) cs.rs[c] = red.v[0][c];
+  if (threadIdx.x == 0) {
+    double x2 = 0.0;
+    for (int c = 0; c < s; ++c) x2 += red.v[0][s + c];
+    *xsq = x2;
+    ctrl->ticket = 0;
+  }
+}
+
 __global__ void tf32_planes_kernel(const float* X, int64_t ld, int64_t n, int s, float* xp) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
@@ -575,6 +807,15 @@ inline dim3 grid2(int64_t n, int s) { return dim3(static_cast<unsigned>(ceil_div
 // reduction kernels: row blocks x column groups of 4 while the row blocks alone
 // leave SMs idle (config 0: 8 row blocks for n = 2048)
 inline dim3 cgrid(int64_t n, int s) {
+  // ~4 CTAs per SM: at config 2 (161 row blocks, 130 columns) one column
+  // group per CTA walked 33 groups of 4 loads serially (88 us per pass)
+  const int rb = reduce_blocks(n);
+  const int groups = (s + 3) / 4;
+  const int y = std::max(1, std::min(groups, (592 + rb - 1) / rb));
+  return dim3(static_cast<unsigned>(rb), static_cast<unsigned>(y));
+}
+// the cooperative cg_fused kernel: every CTA resident (<= 2 per SM at 256 threads)
+inline dim3 coop_grid(int64_t n, int s) {
   const int rb = reduce_blocks(n);
   return dim3(static_cast<unsigned>(rb), rb < 148 ? static_cast<unsigned>((s + 3) / 4) : 1u);
 }
@@ -646,6 +887,29 @@ void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
   WGP_LAUNCH_CHECK();
 }
 
+template <class T>
+bool cg_fused(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs, double* part,
+              SolveCtrl* ctrl, cudaStream_t st, float* pp) {
+  check_s(s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = coop_grid(n, s);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, cg_fused_kernel<T>, X, R, P, HP, ld, n, s, cs, part, ctrl, pp);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  return true;
+}
+
 #define WGP_CG_INSTANTIATE(T)                                                                                  \
   template void cg_snapshot<T>(T*, T*, T*, T*, int64_t, int64_t, int, ColState, const SolveCtrl*, bool,     \
                                cudaStream_t);                                                                \
@@ -660,7 +924,9 @@ void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
   template void cg_refresh_norm<T>(T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,      \
                                    cudaStream_t);                                                            \
   template void cg_direction<T>(T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,         \
-                                cudaStream_t, float*);
+                                cudaStream_t, float*);                                                       \
+  template bool cg_fused<T>(T*, T*, T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,      \
+                            cudaStream_t, float*);
 WGP_CG_INSTANTIATE(float)
 WGP_CG_INSTANTIATE(double)
 #undef WGP_CG_INSTANTIATE
@@ -761,6 +1027,22 @@ void sgd_scatter(float* X, float* R, float* vel, int64_t ld, const int* idx, int
                  const SolveCtrl* ctrl, cudaStream_t st) {
   sgd_scatter_kernel<<<grid2(m, s), NT, 0, st>>>(X, R, vel, ld, idx, m, s, batch, momentum,
                                                  grad_scale, step_scale, xp, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void sgd_step(float* X, float* R, float* vel, int64_t ld, const int* idx, int64_t m, int s, const float* batch,
+              float momentum, float grad_scale, float step_scale, float* xp, ColState cs, double* xsq,
+              double* part, SolveCtrl* ctrl, cudaStream_t st) {
+  check_s(s);
+  sgd_step_kernel<<<grid2(m, s), NT, 0, st>>>(X, R, vel, ld, idx, m, s, batch, momentum, grad_scale, step_scale,
+                                              xp, cs, xsq, part, ctrl);
+  WGP_LAUNCH_CHECK();
+}
+
+void sgd_norms(const float* X, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* xsq,
+               double* part, SolveCtrl* ctrl, cudaStream_t st) {
+  check_s(2 * s);
+  sgd_norms_kernel<<<cgrid(n, 2 * s), NT, 0, st>>>(X, R, ld, n, s, cs, xsq, part, ctrl);
   WGP_LAUNCH_CHECK();
 }
 

@@ -21,6 +21,8 @@ struct SolveCtrl {
   int max_it;
   unsigned ticket;
   int pad;
+  unsigned bar_count;  // grid barrier of the cooperative cg_fused kernel
+  unsigned bar_gen;
 };
 
 enum : int { kStatusOk = 0, kStatusNotPd = 1, kStatusNaN = 2, kStatusDiverged = 3 };
@@ -102,6 +104,15 @@ void cg_snapshot(T* X, T* R, T* Xb, T* Rb, int64_t ld, int64_t n, int s, ColStat
 template <class T>
 void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
                   double* part, SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
+// One non-refresh CG iteration's vector work in ONE cooperative kernel:
+// cg_alpha + cg_update + cg_direction (solvers.cpp:112-134) with two grid
+// barriers; every CTA forms the column totals itself from the per-CTA
+// partials in the same fixed order, so results are bitwise those of the
+// three kernels.  Unsharded solves only.  Returns false (nothing launched)
+// when the cooperative launch is unavailable; the caller then runs the three.
+template <class T>
+bool cg_fused(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs, double* part,
+              SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
 // B = A (fp32 -> fp64) / B = A rounded to fp32, n x s column blocks.
 void widen(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n, int s, cudaStream_t st);
 // Y += a X (fp64, n x s column blocks, leading dimension ld).
@@ -144,6 +155,18 @@ void sgd_scatter(float* X, float* R, float* vel, int64_t ld, const int* idx, int
 // xp[j + c ld] = tf32 hi of X[j + c ld], xp[j + (s + c) ld] = the lo part
 // (bitwise hv_tc's split of V; for HvParams::vplanes).
 void tf32_planes(const float* X, int64_t ld, int64_t n, int s, float* xp, cudaStream_t st);
+// One SGD step's vector work in one kernel: the momentum scatter of
+// sgd_scatter, then the residual-estimate norms ||R_c||^2 (cs.rs) and ||X||_F^2
+// (*xsq) updated by the minibatch rows' changes (fp64, fixed order; the
+// minibatch rows are distinct), and sgd_check's convergence / divergence
+// tests and loop check on them.  part: >= ceil(m / 256) * (s + 1) doubles.
+void sgd_step(float* X, float* R, float* vel, int64_t ld, const int* idx, int64_t m, int s, const float* batch,
+              float momentum, float grad_scale, float step_scale, float* xp, ColState cs, double* xsq,
+              double* part, SolveCtrl* ctrl, cudaStream_t st);
+// Exact ||R_c||^2 -> cs.rs and ||X||_F^2 -> *xsq (no convergence or loop
+// check): re-synchronises sgd_step's running norms once per round.
+void sgd_norms(const float* X, const float* R, int64_t ld, int64_t n, int s, ColState cs, double* xsq,
+               double* part, SolveCtrl* ctrl, cudaStream_t st);
 void sgd_check(const float* X, const float* R, int64_t ld, int64_t n, int s, ColState cs,
                double* part, SolveCtrl* ctrl, cudaStream_t st);
 
