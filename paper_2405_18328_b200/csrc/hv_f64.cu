@@ -62,6 +62,16 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
+// D(16x8) += A(16x8, row) B(8x8, col): 4x the work of m8n8k4 per instruction.
+__device__ __forceinline__ void dmma1688(double (&c)[4], const double (&a)[4], double b0, double b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b0), "d"(b1));
+}
+#ifndef WGP_HV64_MMA
+#define WGP_HV64_MMA 16
+#endif
 
 // One tile's V (TJ points x 8 NF columns, column-major with stride VJ, zero
 // beyond n and s) and point coordinates (TJ x dp, row-major) -> shared memory
@@ -124,11 +134,17 @@ __global__ void __launch_bounds__(NT, kCtasPerSm) hv64_kernel(Hv64Params p, int6
     xi[r * dps + k] = g >= 0 ? p.xs[g * p.dp + k] : 0.f;
   }
 
+#if WGP_HV64_MMA == 16
+  double acc[NF][4];  // C fragment f: rows g, g + 8 (c0 c1 | c2 c3), columns 8 f + 2 t + {0, 1}
+#pragma unroll
+  for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = acc[f][2] = acc[f][3] = 0.0;
+#else
   double acc[2][NF][2];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
 #pragma unroll
     for (int f = 0; f < NF; ++f) acc[r][f][0] = acc[r][f][1] = 0.0;
+#endif
 
   int buf = 0;
   for (int64_t t = t0; t < t1; ++t, buf ^= 1) {
@@ -170,6 +186,24 @@ __global__ void __launch_bounds__(NT, kCtasPerSm) hv64_kernel(Hv64Params p, int6
     }
     __syncthreads();  // K^T tile complete
     if (t + 1 < t1) load_tile<NF>(p, jt + TJ, vsb + (buf ^ 1) * 8 * NF * VJ, xjb + (buf ^ 1) * TJ * p.dp);
+#if WGP_HV64_MMA == 16
+    // product, m16n8k8 (g = lane / 4, t = lane % 4): A = K rows 16 w + g (+ 8),
+    // points 8 kk + t (+ 4); B = V points 8 kk + t (+ 4), columns 8 f + g
+    const float* ka = ks + (lane & 3) * KS + 16 * warp + (lane >> 2);
+    const double* vb = vs + (lane >> 2) * VJ + (lane & 3);
+#pragma unroll
+    for (int kk = 0; kk < TJ / 8; ++kk) {
+      const double a[4] = {ka[8 * kk * KS], ka[8 * kk * KS + 8], ka[(8 * kk + 4) * KS], ka[(8 * kk + 4) * KS + 8]};
+      double b0[NF], b1[NF];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        b0[f] = vb[8 * f * VJ + 8 * kk];
+        b1[f] = vb[8 * f * VJ + 8 * kk + 4];
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) dmma1688(acc[f], a, b0[f], b1[f]);
+    }
+#else
     // product: A = K rows (16 w + 8 r + lane / 4), points 4 kk + lane % 4;
     // B = V points 4 kk + lane % 4, columns 8 f + lane / 4
     const float* ka = ks + (lane & 3) * KS + 16 * warp + (lane >> 2);
@@ -186,6 +220,7 @@ __global__ void __launch_bounds__(NT, kCtasPerSm) hv64_kernel(Hv64Params p, int6
         dmma884(acc[1][f], a1, b[f]);
       }
     }
+#endif
   }
   // partials: part[(split s + c) m_pad + local row]; C fragment: row lane / 4,
   // columns 2 (lane % 4) + {0, 1}
@@ -198,7 +233,11 @@ __global__ void __launch_bounds__(NT, kCtasPerSm) hv64_kernel(Hv64Params p, int6
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = 8 * f + 2 * (lane & 3) + e;
+#if WGP_HV64_MMA == 16
+        if (c < p.s) p.part[(static_cast<int64_t>(split) * p.s + c) * m_pad + lr] = acc[f][2 * r + e];
+#else
         if (c < p.s) p.part[(static_cast<int64_t>(split) * p.s + c) * m_pad + lr] = acc[r][f][e];
+#endif
       }
   }
 }
