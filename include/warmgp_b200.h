@@ -272,6 +272,15 @@ int wgp_nccl_unique_id(unsigned char id[128]);
 /** Attach a communicator (ncclCommInitRank; collective over the ranks) to the
  *  context; wgp_set_data must follow. */
 int wgp_set_comm(wgp_ctx* ctx, int rank, int nranks, const unsigned char id[128]);
+/** TEST INFRASTRUCTURE: a host-mediated communicator for N contexts on ONE
+ *  GPU driven by N host threads (each collective: a host barrier and device
+ *  copies between the contexts' buffers; no kernel waits on another rank's, no
+ *  CUDA graphs).  It runs the library's multi-rank sharding logic where only
+ *  one GPU is available; production uses wgp_set_comm (NCCL). */
+typedef struct wgp_local_group wgp_local_group;
+int wgp_local_group_create(int nranks, wgp_local_group** out);
+int wgp_local_group_destroy(wgp_local_group* g);
+int wgp_set_comm_local(wgp_ctx* ctx, wgp_local_group* g, int rank);
 /** The context's rank, rank count, own rows and vector leading dimension. */
 int wgp_shard_info(wgp_ctx* ctx, int* rank, int* nranks, int64_t* own0, int64_t* own1, int64_t* ld);
 /** The row partition of n points over nranks (host only): own rows and ld. */

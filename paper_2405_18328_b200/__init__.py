@@ -101,6 +101,7 @@ EXPORTS = [
     "wgp_exact", "wgp_predict", "wgp_split_order", "wgp_hv_cols", "wgp_hv_block", "wgp_ap_factor", "wgp_ap_block_solve",
     "wgp_set_split_global", "wgp_set_cg_precision", "wgp_hv_f64", "wgp_solve_f64",
     "wgp_nccl_unique_id", "wgp_set_comm", "wgp_shard_info", "wgp_shard_rows",
+    "wgp_local_group_create", "wgp_local_group_destroy", "wgp_set_comm_local",
 ]
 
 
@@ -140,6 +141,9 @@ def load():
     lib.wgp_set_comm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
     lib.wgp_shard_info.argtypes = [C.c_void_p] + [C.c_void_p] * 5
     lib.wgp_shard_rows.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.wgp_local_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    lib.wgp_local_group_destroy.argtypes = [C.c_void_p]
+    lib.wgp_set_comm_local.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
     lib.wgp_set_data.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int]
     lib.wgp_set_hyper.argtypes = [C.c_void_p, C.c_void_p]
     lib.wgp_set_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
@@ -199,6 +203,30 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     _check(load().wgp_nccl_unique_id(buf))
     return bytes(buf)
+
+
+class LocalGroup:
+    """TEST INFRASTRUCTURE (wgp_local_group_create): a host-mediated
+    communicator for `nranks` contexts on one GPU, each driven by its own
+    Python thread (ctypes releases the GIL in library calls)."""
+
+    def __init__(self, nranks: int):
+        self._lib = load()
+        h = C.c_void_p()
+        _check(self._lib.wgp_local_group_create(nranks, C.byref(h)))
+        self._h = h
+        self.nranks = nranks
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wgp_local_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def shard_rows(n: int, rank: int, nranks: int):
@@ -481,6 +509,11 @@ class Context:
             raise ValueError("unique id must be 128 bytes")
         buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
         _check(self._lib.wgp_set_comm(self._h, rank, nranks, buf))
+
+    def set_comm_local(self, group: "LocalGroup", rank: int):
+        """Join a LocalGroup as `rank` (test infrastructure: multi-rank sharding
+        on one GPU; call before set_data)."""
+        _check(self._lib.wgp_set_comm_local(self._h, group._h, rank))
 
     def shard_info(self):
         """(rank, nranks, own0, own1, ld) of the context's row sharding."""

@@ -11,8 +11,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <type_traits>
@@ -130,28 +132,41 @@ struct NcclApi {
   }
 };
 
-// One rank's communicator (one process per GPU).  Collectives
-// are enqueued on the context stream (and so are captured into the CG / AP
-// CUDA graphs with the kernels around them).
+// A rank's communicator.  NcclComm (one process per GPU) is the
+// product; LocalComm is a host-mediated stand-in for tests on one GPU: N
+// contexts driven by N host threads, each collective a host barrier plus
+// device copies between the contexts' buffers, so no kernel ever waits on
+// another rank's kernel.  Collectives run on the context stream (NCCL's are
+// captured into the CG / AP graphs; LocalComm's are not capturable).
 struct Comm {
-  ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
-  Comm(int r, int nr, const ncclUniqueId& id) : rank(r), nranks(nr) {
+  virtual ~Comm() = default;
+  virtual bool capturable() const = 0;
+  // In-place all-gather of row blocks of s columns (column c at base + c ld,
+  // rank r's rows at [r blk, (r + 1) blk)).
+  virtual void gather_rows(void* base, int64_t ld, int64_t blk, int s, size_t elem, cudaStream_t st) = 0;
+  // recv[r * count + k] = rank r's send[k]
+  virtual void all_gather(const double* send, double* recv, size_t count, cudaStream_t st) = 0;
+  virtual void all_reduce_sum(double* buf, size_t count, cudaStream_t st) = 0;
+};
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  NcclComm(int r, int nr, const ncclUniqueId& id) {
+    rank = r;
+    nranks = nr;
     const NcclApi& a = NcclApi::get();
     a.check(a.comm_init_rank(&comm, nr, id, r), "ncclCommInitRank");
   }
-  ~Comm() {
+  ~NcclComm() override {
     if (comm) NcclApi::get().comm_destroy(comm);
   }
-  Comm(const Comm&) = delete;
-  Comm& operator=(const Comm&) = delete;
   static ncclDataType_t type(size_t elem) { return elem == 8 ? ncclFloat64 : ncclFloat32; }
-  // In-place all-gather of row blocks of s columns (column c at base + c ld,
-  // rank r's rows at [r blk, (r + 1) blk)): one grouped launch.
-  void gather_rows(void* base, int64_t ld, int64_t blk, int s, size_t elem, cudaStream_t st) const {
+  bool capturable() const override { return true; }
+  void gather_rows(void* base, int64_t ld, int64_t blk, int s, size_t elem, cudaStream_t st) override {
     const NcclApi& a = NcclApi::get();
     char* b = static_cast<char*>(base);
-    a.check(a.group_start(), "ncclGroupStart");
+    a.check(a.group_start(), "ncclGroupStart");  // one grouped launch for all columns
     for (int c = 0; c < s; ++c) {
       char* col = b + static_cast<size_t>(c) * ld * elem;
       a.check(a.all_gather(col + static_cast<size_t>(rank) * blk * elem, col, static_cast<size_t>(blk), type(elem),
@@ -160,14 +175,82 @@ struct Comm {
     }
     a.check(a.group_end(), "ncclGroupEnd");
   }
-  // recv[r * count + k] = rank r's send[k]
-  void all_gather(const double* send, double* recv, size_t count, cudaStream_t st) const {
+  void all_gather(const double* send, double* recv, size_t count, cudaStream_t st) override {
     const NcclApi& a = NcclApi::get();
     a.check(a.all_gather(send, recv, count, ncclFloat64, comm, st), "ncclAllGather");
   }
-  void all_reduce_sum(double* buf, size_t count, cudaStream_t st) const {
+  void all_reduce_sum(double* buf, size_t count, cudaStream_t st) override {
     const NcclApi& a = NcclApi::get();
     a.check(a.all_reduce(buf, buf, count, ncclFloat64, ncclSum, comm, st), "ncclAllReduce");
+  }
+};
+
+}  // namespace
+
+// The shared state of a LocalComm group (wgp_local_group_create).
+struct LocalGroup {
+  int nranks = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  std::vector<const void*> slot;
+  explicit LocalGroup(int n) : nranks(n), slot(n, nullptr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = generation;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != g; });
+    }
+  }
+};
+
+namespace {
+struct LocalComm : Comm {
+  std::shared_ptr<LocalGroup> g;
+  LocalComm(std::shared_ptr<LocalGroup> grp, int r) : g(std::move(grp)) {
+    rank = r;
+    nranks = g->nranks;
+  }
+  bool capturable() const override { return false; }
+  // publish this rank's pointer once its stream is idle; returns after all did
+  void publish(const void* p, cudaStream_t st) {
+    WGP_CUDA(cudaStreamSynchronize(st));
+    g->slot[rank] = p;
+    g->barrier();
+  }
+  void gather_rows(void* base, int64_t ld, int64_t blk, int s, size_t elem, cudaStream_t st) override {
+    publish(base, st);
+    for (int r = 0; r < nranks; ++r) {
+      if (r == rank) continue;
+      const char* src = static_cast<const char*>(g->slot[r]) + static_cast<size_t>(r) * blk * elem;
+      char* dst = static_cast<char*>(base) + static_cast<size_t>(r) * blk * elem;
+      WGP_CUDA(cudaMemcpy2DAsync(dst, ld * elem, src, ld * elem, blk * elem, s, cudaMemcpyDeviceToDevice, st));
+    }
+    WGP_CUDA(cudaStreamSynchronize(st));
+    g->barrier();  // nobody overwrites its block before every rank copied it
+  }
+  void all_gather(const double* send, double* recv, size_t count, cudaStream_t st) override {
+    publish(send, st);
+    for (int r = 0; r < nranks; ++r)
+      WGP_CUDA(cudaMemcpyAsync(recv + r * count, g->slot[r], sizeof(double) * count, cudaMemcpyDeviceToDevice, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    g->barrier();
+  }
+  void all_reduce_sum(double* buf, size_t count, cudaStream_t st) override {
+    publish(buf, st);
+    std::vector<double> sum(count, 0.0), part(count);
+    for (int r = 0; r < nranks; ++r) {  // rank order
+      WGP_CUDA(cudaMemcpy(part.data(), g->slot[r], sizeof(double) * count, cudaMemcpyDeviceToHost));
+      for (size_t k = 0; k < count; ++k) sum[k] += part[k];
+    }
+    g->barrier();  // every rank has read every buffer
+    WGP_CUDA(cudaMemcpyAsync(buf, sum.data(), sizeof(double) * count, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
   }
 };
 
@@ -202,6 +285,7 @@ struct Ctx {
   int rank = 0, nranks = 1;
   int64_t blk = 0, own0 = 0, own1 = 0;
   bool sharded() const { return comm != nullptr; }
+  bool graphs_ok() const { return !comm || comm->capturable(); }
   int64_t own_m() const { return own1 - own0; }
   Buf dloc, dall;  // per-rank column totals and their all-gather (dist reductions)
 
@@ -770,7 +854,7 @@ struct Ctx {
       for (int k = 0; k < eager[e]; ++k) iteration(++launched % 50 == 0);
     }
     CgGraph* gr = nullptr;
-    if (!no_graphs) {
+    if (!no_graphs && graphs_ok()) {
       const uint64_t gen = alloc_generation().load();
       for (auto& g : cg_graphs)
         if (g.B == B && g.Xo == Xo && g.R == R && g.s == s && g.impl == impl) gr = &g;
@@ -998,7 +1082,7 @@ struct Ctx {
         out.iterations = h.it;
         return;
       }
-      if (!gr && !tried && eager_done && !no_graphs && !tc.profiling) {
+      if (!gr && !tried && eager_done && !no_graphs && !tc.profiling && graphs_ok()) {
         tried = true;
         gr = ap_graph(B, Xo, R, s, bs, epoch);
       }
@@ -1688,6 +1772,9 @@ std::atomic<uint64_t>& alloc_generation() {
 struct wgp_ctx {
   wgp::Ctx c;
 };
+struct wgp_local_group {
+  std::shared_ptr<wgp::LocalGroup> g;
+};
 
 using wgp::guarded;
 
@@ -1903,10 +1990,37 @@ int wgp_set_comm(wgp_ctx* ctx, int rank, int nranks, const unsigned char* id) {
     std::memcpy(u.internal, id, sizeof(u.internal));
     c.drop_cg_graphs();  // captured launches bake in the layout
     c.comm.reset();
-    c.comm = std::make_unique<wgp::Comm>(rank, nranks, u);
+    c.comm = std::make_unique<wgp::NcclComm>(rank, nranks, u);
     c.rank = rank;
     c.nranks = nranks;
     c.n = 0;  // the row layout depends on the rank count: wgp_set_data follows
+    c.have_hyper = false;
+  });
+}
+
+int wgp_local_group_create(int nranks, wgp_local_group** out) {
+  return guarded([&] {
+    if (nranks < 1 || !out) throw std::invalid_argument("wgp_local_group_create: bad arguments");
+    *out = new wgp_local_group{std::make_shared<wgp::LocalGroup>(nranks)};
+  });
+}
+
+int wgp_local_group_destroy(wgp_local_group* g) {
+  delete g;
+  return WGP_OK;
+}
+
+int wgp_set_comm_local(wgp_ctx* ctx, wgp_local_group* g, int rank) {
+  return guarded([&] {
+    wgp::Ctx& c = ctx->c;
+    if (!g || rank < 0 || rank >= g->g->nranks) throw std::invalid_argument("wgp_set_comm_local: bad rank");
+    WGP_CUDA(cudaSetDevice(c.device));
+    c.drop_cg_graphs();
+    c.comm.reset();
+    c.comm = std::make_unique<wgp::LocalComm>(g->g, rank);
+    c.rank = rank;
+    c.nranks = g->g->nranks;
+    c.n = 0;
     c.have_hyper = false;
   });
 }
