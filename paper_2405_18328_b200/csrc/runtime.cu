@@ -13,6 +13,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
+#include <list>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -698,10 +699,11 @@ struct Ctx {
     float* R;
     int s, impl;
     int64_t bs;
+    int exact;  // the epoch's closing residual from scratch
     uint64_t gen;
     cudaGraphExec_t exec;
   };
-  std::vector<ApGraph> ap_graphs;
+  std::list<ApGraph> ap_graphs;  // stable addresses: a solve holds pointers to two of them
   void drop_cg_graphs() {  // and the AP epoch graphs
     for (auto& g : cg_graphs)
       for (auto e : g.exec)
@@ -1018,7 +1020,14 @@ struct Ctx {
     norms_convergence(R + r, ld, m, s, cs, pt, c, false, true, st);  // :172-178
     if (sh) dist_reduce(kDistNorms, s, s, false, true);
     const double one = 1.0, zero = 0.0;
-    auto epoch = [&]() {
+    // The epoch's closing residual (:188).  `exact`: R = B - H X from scratch
+    // (n^2 entries).  Otherwise, unsharded: R = R0 - H dX, completed block by
+    // block -- R[b] already holds R0_b - H[b, 0:start] dX[0:start] from the
+    // block step, so R[b] -= H[b, start:n] dX[start:n] adds the rest: n^2 / 2
+    // entries, an epoch of n^2 instead of 1.5 n^2 (the triangle of the block
+    // steps plus this one).  Equal in exact arithmetic; every kApExact-th epoch
+    // is exact, so fp32 rounding cannot accumulate across epochs.
+    auto epoch = [&](bool exact) {
       for (int64_t b = 0; b < nb; ++b) {  // :183-187
         const int64_t start = b * bs, size = std::min(bs, n - start);
         const double* Hinv = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
@@ -1067,40 +1076,70 @@ struct Ctx {
         }
         ap_apply(Xo, ld, start, size, s, D64.as<double>(), kparts, DX.as<float>(), DXP.as<float>(), c, st);
       }
-      hv(Xo, ld, s, R + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);  // :188
-      norms_convergence(R + r, ld, m, s, cs, pt, c, true, true, st);       // :189-191
+      if (exact || sh) {
+        hv(Xo, ld, s, R + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);  // :188
+      } else {
+        for (int64_t b = 0; b < nb; ++b) {
+          const int64_t start = b * bs, size = std::min(bs, n - start);
+          hv(DX.as<float>(), ld, s, R + start, ld, kHvSubtract, nullptr, 0, start, n, nullptr, start, size,
+             &c->done, false, DXP.as<float>(), ld);
+        }
+      }
+      norms_convergence(R + r, ld, m, s, cs, pt, c, true, true, st);  // :189-191
       if (sh) dist_reduce(kDistNorms, s, s, true, true);
     };
+    static const int kApExact = [] {
+      const char* e = getenv("WGP_AP_EXACT_EVERY");  // 1: every epoch exact (the reference's form)
+      return e ? std::max(1, atoi(e)) : 10;
+    }();
     static const bool no_graphs = getenv("WGP_NO_GRAPHS") != nullptr;
-    bool eager_done = false;  // one eager epoch first: every workspace exists before a capture
-    bool tried = false;       // one capture attempt per solve
-    ApGraph* gr = nullptr;
-    while (true) {
+    bool eager_done[2] = {false, false};  // one eager epoch of each form first: every workspace exists
+    bool tried[2] = {false, false};       // one capture attempt per form and solve
+    ApGraph* gr[2] = {nullptr, nullptr};
+    for (int e = 0;; ++e) {
       const SolveCtrl& h = poll();
       if (h.done) {
         if (h.status != kStatusOk) fail(h, 1);
         out.iterations = h.it;
         return;
       }
-      if (!gr && !tried && eager_done && !no_graphs && !tc.profiling && graphs_ok()) {
-        tried = true;
-        gr = ap_graph(B, Xo, R, s, bs, epoch);
+      const int x = (e % kApExact == kApExact - 1) ? 1 : 0;  // exact closing residual
+      // a workspace grown by an eager epoch of the other form (e.g. the first
+      // exact residual over all rows) invalidates the graphs captured before it
+      for (int k = 0; k < 2; ++k)
+        if (gr[k] && gr[k]->gen != alloc_generation().load()) {
+          gr[k] = nullptr;
+          tried[k] = false;
+          eager_done[k] = false;
+        }
+      if (!gr[x] && !tried[x] && eager_done[x] && !no_graphs && !tc.profiling && graphs_ok()) {
+        tried[x] = true;
+        auto ep = [&]() { epoch(x == 1); };
+        gr[x] = ap_graph(B, Xo, R, s, bs, x, ep);
       }
-      if (gr)
-        WGP_CUDA(cudaGraphLaunch(gr->exec, st));
+      if (gr[x])
+        WGP_CUDA(cudaGraphLaunch(gr[x]->exec, st));
       else
-        epoch();
-      eager_done = true;
+        epoch(x == 1);
+      eager_done[x] = true;
     }
   }
   template <class F>
-  ApGraph* ap_graph(const float* B, float* Xo, float* R, int s, int64_t bs, F& epoch) {
+  ApGraph* ap_graph(const float* B, float* Xo, float* R, int s, int64_t bs, int exact, F& epoch) {
     const uint64_t gen = alloc_generation().load();
     for (auto& g : ap_graphs)
-      if (g.B == B && g.Xo == Xo && g.R == R && g.s == s && g.impl == hv_impl && g.bs == bs && g.gen == gen) return &g;
-    if (ap_graphs.size() >= 4) {
-      for (auto& g : ap_graphs) cudaGraphExecDestroy(g.exec);
-      ap_graphs.clear();
+      if (g.B == B && g.Xo == Xo && g.R == R && g.s == s && g.impl == hv_impl && g.bs == bs && g.exact == exact &&
+          g.gen == gen)
+        return &g;
+    if (ap_graphs.size() >= 6) {  // evict other solves' graphs (this solve may hold the other form's)
+      for (auto it = ap_graphs.begin(); it != ap_graphs.end();) {
+        if (it->B == B && it->Xo == Xo && it->R == R && it->s == s && it->bs == bs) {
+          ++it;
+        } else {
+          cudaGraphExecDestroy(it->exec);
+          it = ap_graphs.erase(it);
+        }
+      }
     }
     cudaGraph_t graph = nullptr;
     WGP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -1122,7 +1161,7 @@ struct Ctx {
       cudaGetLastError();
       return nullptr;
     }
-    ap_graphs.push_back(ApGraph{B, Xo, R, s, hv_impl, bs, gen, exec});
+    ap_graphs.push_back(ApGraph{B, Xo, R, s, hv_impl, bs, exact, gen, exec});
     return &ap_graphs.back();
   }
 
