@@ -73,29 +73,59 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed regions: NVML
+    (pynvml, ~every 2 ms -- a 20-step H.V region lasts ~5 ms) with nvidia-smi as
+    the fallback.  `phase(name)` labels the following samples."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []  # (phase, sm_mhz, max_mhz, reasons)
+        self._phase = "setup"
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._nvml = pynvml
+            self._bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                          "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                          "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                          "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+
+    def phase(self, name):
+        self._phase = name
+
+    def _sample_nvml(self):
+        n = self._nvml
+        sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+        r = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        self.samples.append((self._phase, float(sm), float(self._max),
+                             [k for k, bit in self._bits.items() if r & bit]))
+
+    def _sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip()
+        if out:
+            f = [x.strip() for x in out.split(",")]
+            self.samples.append((self._phase, float(f[0]), float(f[1]),
+                                 [self.NAMES[k] for k in range(4) if len(f) > 2 + k and f[2 + k].lower() == "active"]))
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self._sample_nvml() if self._nvml else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.002 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -109,14 +139,14 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        load = [x for x in self.samples if x[0] != "setup"] or self.samples
+        sm = [x[1] for x in load]
+        hv = [x for x in self.samples if x[0] == "hv"]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(x[2] for x in load),
+                "reasons": sorted({r for x in load for r in x[3]}), "samples": len(load),
+                "samples_during_hv_steps": len(hv),
+                "sm_mhz_during_hv_steps": float(np.median([x[1] for x in hv])) if hv else None,
+                "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def dist_env():
@@ -439,14 +469,14 @@ def main():
         launches0 = wg.launch_count()
         if args.hv_impl != "simt":
             ctx.profile(True)
-        n_samples0 = len(clk.samples)
+        clk.phase("hv")
         for a, b in evs:
             flush.zero_()
             a.record(stream)
             one_step()
             b.record(stream)
         stream.synchronize()
-        hv_samples = len(clk.samples) - n_samples0
+        clk.phase("e2e")
     launches = wg.launch_count() - launches0
     kernel_ms, kernel_launches = ctx.profile_read() if args.hv_impl != "simt" else (0.0, 0)
     ctx.profile(False)
@@ -491,6 +521,7 @@ def main():
     # outer steps run on every rank (collectives inside the library), before rank 0 reports
     outer = None
     if not args.no_outer:
+        clk.phase("outer")
         outer = outer_bench(wg, datasets, local, args, ws, rank)
     clk.__exit__()
     if rank != 0:
@@ -500,7 +531,6 @@ def main():
         return
     pk = peaks()
     clocks = clk.summary()
-    clocks["samples_during_hv_steps"] = hv_samples
     f_entry = 2 * d + 2 * s + 8                       # SURVEY §8d F_hv
     flops = f_entry * n * n
     # T_roof = max(sum over pipes of FLOPs_pipe / P_pipe,
