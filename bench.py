@@ -13,7 +13,9 @@ library context joins one NCCL communicator (wgp_set_comm): the library
 computes the rank's rows of H.V and all-gathers the n x s result itself
 (SURVEY §8e); timing is the max over ranks.
 
-The line also carries ``outer``: ms per marginal-likelihood step (the second
+The line also carries ``large_n``: config 3's full-size H.V (n = 391,386),
+row-sharded under torchrun, at every N -- the north star's scaling case -- and
+``outer``: ms per marginal-likelihood step (the second
 half of the metric) at configs 2 and 3 through the library's wgp_train --
 row-sharded inside the library under torchrun -- with iterations, converged
 steps and final residuals per solver, and the CPU path's outer-step figures
@@ -57,6 +59,7 @@ def parse():
     ap.add_argument("--comm", action="store_true",
                     help="N=1: attach a one-rank NCCL communicator (runs the library's sharded code path)")
     ap.add_argument("--no-c3", action="store_true", help="skip the config-3 outer steps")
+    ap.add_argument("--no-large", action="store_true", help="skip the config-3 full-size H.V (scaling case)")
     ap.add_argument("--outer-steps", type=int, default=5, help="timed outer steps per solver (config 2)")
     ap.add_argument("--outer-warmup", type=int, default=1, help="untimed outer steps before them")
     return ap.parse_args()
@@ -218,6 +221,48 @@ def run_outer(wg, ctx, p, sc, steps, warmup, precision="f64", ws=1):
             "max_final_relative_residual": float(max(r.per_column_relative_residual.max() for r in timed)),
             "cg_precision": precision if sc["kind"] == "cg" else None,
             "config": {k: v for k, v in sc.items() if k != "kind"}}
+
+
+def large_n_hv(wg, datasets, device, args, ws, rank, reps=5):
+    """The north star's scaling case: BASELINE config 3's full-size fused H.V
+    (n = 391,386, d = 3, s = 65, fp32 tc) row-sharded over the ranks by the
+    library (own rows + NCCL all-gather of the n x s result), CUDA events on the
+    context stream, maximum over the ranks -- reported at every N so the
+    scaling at n >= 390k can be read off the N = 1, 2, 4, 8 lines."""
+    import torch
+
+    p = datasets.config3()
+    n = p.X.shape[0]
+    ctx = make_ctx(wg, device, args, ws, rank)
+    ctx.set_data(p.X)
+    ctx.set_hyper([*p.lengthscales, p.signal, p.noise])
+    _, _, r0, r1, ldc = ctx.shard_info()
+    dev = torch.device("cuda", device)
+    V = torch.from_numpy(np.random.default_rng(7).standard_normal((65, n)).astype(np.float32)).to(dev)
+    sharded = ws > 1 or args.comm
+    out = torch.empty((65, ldc if sharded else n), device=dev)
+    st = torch.cuda.ExternalStream(ctx.stream)
+    times = []
+    with torch.cuda.stream(st):
+        for i in range(reps + 1):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            ctx.hv_device(V.data_ptr(), n, 65, out.data_ptr(), out.shape[1])
+            b.record(st)
+            b.synchronize()
+            if i:
+                times.append(a.elapsed_time(b))
+    ms = float(np.mean(times))
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ctx.close()
+    return {"workload": "config3 fused H.V n=391386 d=3 s=65 (fp32 tc), rows sharded over the ranks + NCCL "
+                        "all-gather of the result" if sharded else "config3 fused H.V n=391386 d=3 s=65 (fp32 tc)",
+            "value": n * n / (ms / 1e3), "unit": "entries/s", "ms_per_step": ms, "steps": reps,
+            "rows_per_rank": int(r1 - r0), "timing": "CUDA events, max over ranks"}
 
 
 def outer_bench(wg, datasets, device, args, ws=1, rank=0):
@@ -518,7 +563,15 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    # outer steps run on every rank (collectives inside the library), before rank 0 reports
+    # the large-n scaling case and the outer steps run on every rank
+    # (collectives inside the library), before rank 0 reports
+    large = None
+    if not args.no_large:
+        clk.phase("large_n")
+        try:
+            large = large_n_hv(wg, datasets, local, args, ws, rank)
+        except Exception as e:
+            large = {"error": str(e)[:200]}
     outer = None
     if not args.no_outer:
         clk.phase("outer")
@@ -587,6 +640,8 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if large is not None:
+        line["large_n"] = large
     if outer is not None:
         line["outer"] = outer
     if ws == 1 and not args.no_cpu_baseline:

@@ -11,7 +11,9 @@ BASELINE's pathwise RFF probes and log-space hyperparameters) at
       - AP, blocks of 1000, tol 0.01, with a 10-epoch budget per step (the
         reference cap of 1000 epochs costs the CPU oracle hours), 3 steps;
   * config 3's generator at n = 20,000 (the full 391,386 points are out of
-    the CPU oracle's reach): AP, blocks of 1000, 10-epoch budget, 3 steps.
+    the CPU oracle's reach): AP, blocks of 1000, 10-epoch budget, 3 steps;
+  * config 4's generator (d = 11, 2000 RFF features) at n = 20,000: CG, tol 0.01,
+    cap 1000 (config 4's settings), 3 steps.
 
 Stored per step: constrained theta, the gradient, solver iterations, the
 per-column relative residuals, the warm-start distance.  The inputs are
@@ -39,6 +41,8 @@ CASES = {
                                                      block_size=1000)),
     "c3_ap_n20000": dict(config="c3", n=20000, steps=3,
                          solver=dict(kind="ap", tol_mean=0.01, tol_samples=0.01, max_iterations=10, block_size=1000)),
+    "c4_cg_n20000": dict(config="c4", n=20000, steps=3, rff_features=2000,
+                         solver=dict(kind="cg", tol_mean=0.01, tol_samples=0.01, max_iterations=1000)),
 }
 
 
@@ -49,8 +53,8 @@ def problem(case):
 
 def train_config(mod, case):
     return mod.TrainConfig(steps=case["steps"], learning_rate=0.1, num_probes=64, mode="warm", seed=0,
-                           transform="log", estimator="pathwise", rff_features=1000, init_noise=0.5,
-                           init_constrained=1.0, solver=mod.SolverConfig(**case["solver"]))
+                           transform="log", estimator="pathwise", rff_features=case.get("rff_features", 1000),
+                           init_noise=0.5, init_constrained=1.0, solver=mod.SolverConfig(**case["solver"]))
 
 
 def main(names):

@@ -6,7 +6,8 @@ column's exact relative residual at the solver tolerance.
 
 Config 2 runs at its full size with bench.py's settings (CG and SGD with the
 reference's iteration caps; AP with a 10-epoch budget per step); config 3's
-generator at n = 20,000 (AP, 10-epoch budget)."""
+generator at n = 20,000 (AP, 10-epoch budget), config 4's at n = 20,000 (CG,
+2000 RFF features)."""
 import json
 import os
 
@@ -18,7 +19,7 @@ from paper_2405_18328_b200 import datasets
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-CASES = ["c2_cg", "c2_sgd", "c2_ap", "c3_ap_n20000"]
+CASES = ["c2_cg", "c2_sgd", "c2_ap", "c3_ap_n20000", "c4_cg_n20000"]
 
 
 def load(name):
@@ -44,7 +45,8 @@ def test_outer_loop_matches_oracle(ctx, name):
     p = gen(n=case["n"]) if "n" in case else gen()
     ctx.set_data(p.X)
     cfg = wg.TrainConfig(steps=case["steps"], learning_rate=0.1, num_probes=64, mode="warm", seed=0,
-                         transform="log", estimator="pathwise", rff_features=1000, init_noise=0.5,
+                         transform="log", estimator="pathwise", rff_features=case.get("rff_features", 1000),
+                         init_noise=0.5,
                          init_constrained=1.0, warm_start_distance=True, solver=wg.SolverConfig(**case["solver"]))
     tr = ctx.train(p.y, cfg)
     theta = np.array([r.constrained_params for r in tr.steps])
