@@ -561,6 +561,7 @@ struct Ctx {
     int iterations = 0;
     std::vector<double> rel;
     std::vector<int> conv;
+    bool r_exact = false;  // the solver's residual at exit is B - H X computed from scratch
   };
 
   static void validate(const wgp_solver_cfg& c) {  // proj/src/solvers.cpp:31-37
@@ -659,10 +660,15 @@ struct Ctx {
       if (cfg.kind == WGP_SOLVER_CG) cg<float>(cfg, B, Xo, Ro, s, out);
       else if (cfg.kind == WGP_SOLVER_AP) ap(cfg, B, Xo, Ro, s, out);
       else sgd(cfg, B, Xo, Ro, s, out);
-      // finalize_exact_residuals, :69-77
+      // finalize_exact_residuals, :69-77 (AP whose last epoch closed with the
+      // exact residual: that is this product, same kernel and arguments)
       float* E = Rtmp.as<float>();
-      hv(Xo, ld, s, E + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);
-      en = dots_own(E, E, s);
+      if (out.r_exact) {
+        en = dots_own(Ro, Ro, s);
+      } else {
+        hv(Xo, ld, s, E + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);
+        en = dots_own(E, E, s);
+      }
     }
     out.rel.resize(s);
     for (int c = 0; c < s; ++c) out.rel[c] = bn[c] > 0.0 ? std::sqrt(en[c]) / bn[c] : 0.0;
@@ -1096,14 +1102,19 @@ struct Ctx {
     bool eager_done[2] = {false, false};  // one eager epoch of each form first: every workspace exists
     bool tried[2] = {false, false};       // one capture attempt per form and solve
     ApGraph* gr[2] = {nullptr, nullptr};
+    bool last_exact = true;  // R at entry is exact (B - H X0, or B)
     for (int e = 0;; ++e) {
       const SolveCtrl& h = poll();
       if (h.done) {
         if (h.status != kStatusOk) fail(h, 1);
         out.iterations = h.it;
+        out.r_exact = last_exact;
         return;
       }
-      const int x = (e % kApExact == kApExact - 1) ? 1 : 0;  // exact closing residual
+      // exact closing residual every kApExact epochs and in the last epoch of
+      // the budget (finalize then reuses it instead of another product)
+      const int x = (e % kApExact == kApExact - 1 || e == max_ep - 1 || sh) ? 1 : 0;
+      last_exact = x == 1;
       // a workspace grown by an eager epoch of the other form (e.g. the first
       // exact residual over all rows) invalidates the graphs captured before it
       for (int k = 0; k < 2; ++k)
