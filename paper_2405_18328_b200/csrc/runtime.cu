@@ -634,6 +634,10 @@ struct Ctx {
                                                sizeof(double) * n, s, cudaMemcpyDeviceToDevice, st));
         else widen(init, ld, x64, ld, n, s, st);
         hv64_rows(x64, ld, s, r64 + r, ld, kHv64Residual, b64, ld, r, m, nullptr);
+        if (keep_residuals) {  // B - H X0 for warm_distance_res
+          wsd_r0.ensure(bytes);
+          WGP_CUDA(cudaMemcpyAsync(wsd_r0.p, r64, bytes, cudaMemcpyDeviceToDevice, st));
+        }
       } else {
         WGP_CUDA(cudaMemsetAsync(x64, 0, bytes, st));
         WGP_CUDA(cudaMemcpyAsync(r64, b64, bytes, cudaMemcpyDeviceToDevice, st));
@@ -644,6 +648,7 @@ struct Ctx {
       double* e64 = Rt64.as<double>();
       hv64_rows(x64, ld, s, e64 + r, ld, kHv64Residual, b64, ld, r, m, nullptr);
       en = dots_own(e64, e64, s);
+      wsd_res = WsdRes{e64, 64, init64 || init};
       narrow(x64, ld, Xo, ld, n, s, st);
       narrow(r64 + r, ld, Ro + r, ld, m, s, st);
       if (Xo64) WGP_CUDA(cudaMemcpy2DAsync(Xo64, sizeof(double) * ld, x64, sizeof(double) * ld,
@@ -653,6 +658,11 @@ struct Ctx {
       if (init) {
         copy_cols(init, ld, Xo, ld, n, s, st);
         hv(Xo, ld, s, Ro + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);
+        if (keep_residuals) {
+          const size_t bytes = sizeof(float) * ld * s;
+          wsd_r0.ensure(bytes);
+          WGP_CUDA(cudaMemcpyAsync(wsd_r0.p, Ro, bytes, cudaMemcpyDeviceToDevice, st));
+        }
       } else {
         fill_zero(Xo, ld, n, s, st);
         copy_cols(B, ld, Ro, ld, n, s, st);
@@ -665,9 +675,11 @@ struct Ctx {
       float* E = Rtmp.as<float>();
       if (out.r_exact) {
         en = dots_own(Ro, Ro, s);
+        wsd_res = WsdRes{Ro, 32, init != nullptr};
       } else {
         hv(Xo, ld, s, E + r, ld, kHvResidual, B, ld, 0, n, nullptr, r, m);
         en = dots_own(E, E, s);
+        wsd_res = WsdRes{E, 32, init != nullptr};
       }
     }
     out.rel.resize(s);
@@ -1305,6 +1317,33 @@ struct Ctx {
     return std::sqrt(std::max(acc / s / static_cast<double>(n), 0.0));
   }
 
+  // The warm-start distance without another product: H (x0 - x*) =
+  // (B - H x*) - (B - H x0) = R_end - R_0, both exact residuals the solve
+  // formed anyway (its initial residual, kept when keep_residuals, and the
+  // finalize_exact_residuals product).  Same quantity as estimator.cpp:84-95.
+  struct WsdRes {
+    const void* rend = nullptr;  // exact final residual of the last solve (own rows)
+    int prec = 0;                // 32 / 64, 0: none
+    bool warm = false;           // the last solve started from an init (R_0 kept)
+  };
+  WsdRes wsd_res;
+  bool keep_residuals = false;
+  Buf wsd_r0, wsd_d;
+  bool warm_distance_res_ok(int prec) const { return keep_residuals && wsd_res.warm && wsd_res.prec == prec; }
+  template <class T>
+  double warm_distance_res(const T* init, const T* sol, int s) {
+    const size_t bytes = sizeof(T) * ld * s;
+    wsd_d.ensure(2 * bytes);
+    T* D = wsd_d.as<T>();
+    T* HD = D + ld * s;
+    diff_cols(init, sol, D, ld, n, s, st);                                      // x0 - x*
+    diff_cols(static_cast<const T*>(wsd_res.rend), wsd_r0.as<T>(), HD, ld, n, s, st);  // R_end - R_0
+    const std::vector<double> q = dots_own(D, HD, s);
+    double acc = 0.0;
+    for (double v : q) acc += v;
+    return std::sqrt(std::max(acc / s / static_cast<double>(n), 0.0));
+  }
+
   // the same on fp64 solver state over the fp64 operator (fp64 CG)
   double warm_distance64(const double* init, const double* sol, int s) {
     ensure_solver_ws(s);
@@ -1614,6 +1653,7 @@ struct Ctx {
     raw[d] = to_r(T, cfg.init_signal > 0.0 ? cfg.init_signal : cfg.init_constrained);
     raw[d + 1] = to_r(T, cfg.init_noise > 0.0 ? cfg.init_noise : cfg.init_constrained);
     const bool fixed = cfg.mode != 1, warm = cfg.mode == 0, pathwise = cfg.estimator == 1;
+    static const bool no_wsd_res = getenv("WGP_WSD_PRODUCT") != nullptr;  // 1: the explicit H (x0 - x*) product
     const int F = cfg.rff_features > 0 ? cfg.rff_features : 1000;
 
     // persistent across calls (Ctx members): fresh allocations would bump the
@@ -1706,12 +1746,18 @@ struct Ctx {
           wgp_solver_cfg sc = cfg.solver;
           sc.seed = derive_seed(derive_seed(cfg.seed, kSolverStream), static_cast<uint64_t>(t));
           const bool have_warm = warm && have_prev;
+          keep_residuals = have_warm && cfg.warm_start_distance && !no_wsd_res;
+          wsd_res = WsdRes{};
           SolveOut so = solve(sc, rhs.as<float>(), have_warm ? prev : nullptr, cur, Rres.as<float>(), sp,
                               have_warm ? prev64 : nullptr, cur64);
           WGP_CUDA(cudaEventRecord(e1, st));
           double wsd = 0.0;
-          if (have_warm && cfg.warm_start_distance)
-            wsd = keep64 ? warm_distance64(prev64, cur64, sp) : warm_distance(prev, cur, sp);
+          if (have_warm && cfg.warm_start_distance) {
+            if (keep64)
+              wsd = warm_distance_res_ok(64) ? warm_distance_res(prev64, cur64, sp) : warm_distance64(prev64, cur64, sp);
+            else
+              wsd = warm_distance_res_ok(32) ? warm_distance_res(prev, cur, sp) : warm_distance(prev, cur, sp);
+          }
           WGP_CUDA(cudaEventRecord(e1w, st));
           if (tr && cfg.record_solver_state) {  // optimizer.cpp:148-151 (fp32 copies)
             const size_t off = static_cast<size_t>(t - 1) * n * sp;

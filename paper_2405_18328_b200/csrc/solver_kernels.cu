@@ -962,6 +962,21 @@ __global__ void narrow_kernel(const double* A, int64_t lda, float* B, int64_t ld
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) B[i + blockIdx.y * ldb] = static_cast<float>(A[i + blockIdx.y * lda]);
 }
+template <class T>
+__global__ void diff_cols_kernel(const T* A, const T* B, T* out, int64_t ld, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t e = i + blockIdx.y * ld;
+  if (i < n) out[e] = A[e] - B[e];
+}
+template <class T>
+void diff_cols(const T* A, const T* B, T* out, int64_t ld, int64_t n, int s, cudaStream_t st) {
+  if (n <= 0) return;
+  diff_cols_kernel<<<grid2(n, s), NT, 0, st>>>(A, B, out, ld, n);
+  WGP_LAUNCH_CHECK();
+}
+template void diff_cols<float>(const float*, const float*, float*, int64_t, int64_t, int, cudaStream_t);
+template void diff_cols<double>(const double*, const double*, double*, int64_t, int64_t, int, cudaStream_t);
+
 __global__ void axpy_cols_kernel(double a, const double* X, double* Y, int64_t ld, int64_t n) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) Y[i + blockIdx.y * ld] = fma(a, X[i + blockIdx.y * ld], Y[i + blockIdx.y * ld]);

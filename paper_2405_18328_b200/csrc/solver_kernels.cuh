@@ -115,6 +115,9 @@ bool cg_fused(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColSt
               SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
 // B = A (fp32 -> fp64) / B = A rounded to fp32, n x s column blocks.
 void widen(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n, int s, cudaStream_t st);
+// out = A - B (n x s column blocks, leading dimension ld; float or double).
+template <class T>
+void diff_cols(const T* A, const T* B, T* out, int64_t ld, int64_t n, int s, cudaStream_t st);
 // Y += a X (fp64, n x s column blocks, leading dimension ld).
 void axpy_cols(double a, const double* X, double* Y, int64_t ld, int64_t n, int s, cudaStream_t st);
 void narrow(const double* A, int64_t lda, float* B, int64_t ldb, int64_t n, int s, cudaStream_t st);
