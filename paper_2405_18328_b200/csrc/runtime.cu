@@ -2158,13 +2158,15 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
     if (s < 1) throw std::invalid_argument("wgp_hv: s must be >= 1");
     wgp::Buf& dv = c.io_in;
     wgp::Buf& dout = c.io_out;
+    // V uploaded as one contiguous copy (leading dimension n: the H.V kernels
+    // take any ldv), faster than a pitched copy into the padded layout
     dv.ensure(sizeof(float) * c.ld * s);
-    WGP_CUDA(cudaMemcpy2DAsync(dv.p, sizeof(float) * c.ld, V, sizeof(float) * c.n, sizeof(float) * c.n, s,
-                               cudaMemcpyHostToDevice, c.st));
+    WGP_CUDA(cudaMemcpyAsync(dv.p, V, sizeof(float) * c.n * s, cudaMemcpyHostToDevice, c.st));
+    const int64_t ldv = c.n;
     if (c.sharded()) {  // the rank's rows, then the all-gather of the n x s result
       dout.ensure(sizeof(float) * c.ld * s);
       float* o = dout.as<float>();
-      c.hv(dv.as<float>(), c.ld, s, o + c.own0, c.ld, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.own0,
+      c.hv(dv.as<float>(), ldv, s, o + c.own0, c.ld, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.own0,
            c.own_m());
       c.gather_rows(o, s);
       WGP_CUDA(cudaMemcpy2DAsync(out, sizeof(float) * c.n, o, sizeof(float) * c.ld, sizeof(float) * c.n, s,
@@ -2172,7 +2174,7 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
     } else {
       const int64_t m = c.r1 - c.r0;
       dout.ensure(sizeof(float) * m * s);
-      c.hv(dv.as<float>(), c.ld, s, dout.as<float>(), m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, m);
+      c.hv(dv.as<float>(), ldv, s, dout.as<float>(), m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, m);
       WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(float) * m * s, cudaMemcpyDeviceToHost, c.st));
     }
     WGP_CUDA(cudaStreamSynchronize(c.st));
