@@ -358,6 +358,36 @@ def cpu_outer_baseline(datasets, outer, seconds):
         res["c2_cg_step"] = {"ms_per_step": 1e3 * (it + 2) * n * n / rate, "extrapolated": True,
                              "sample": f"oracle fp64 H.V rows 0..{rows} x {n} points, s=65 ({el:.1f} s), "
                                        f"x {it + 2:.1f} H.V per step (device fp64 CG iterations + 2)"}
+
+    def rows_rate(p, budget):  # oracle fp64 H.V entries/s on a row sample of the full problem
+        n_ = p.X.shape[0]
+        V_ = np.random.default_rng(0).standard_normal((n_, 65))
+        r_, el_ = 8, 0.0
+        while True:
+            t0_ = time.perf_counter()
+            orc.hv_rows(p.X, p.lengthscales, p.signal, p.noise, V_, 0, r_)
+            el_ = time.perf_counter() - t0_
+            if el_ >= budget or r_ >= n_:
+                return r_ * n_ / el_, r_, el_
+            r_ = min(n_, r_ * 4)
+
+    # config 3 AP step as the reference runs it (proj/src/solvers.cpp:141-196):
+    # per epoch the right-looking updates (n x b per block: n^2) plus the exact
+    # residual (n^2), 10 epochs, + the initial residual, the final exact
+    # residual and the gradient (~1 H.V each): 23 H.V-equivalents per step.
+    p3 = datasets.config3()
+    rate3, r3, e3 = rows_rate(p3, seconds / 8)
+    n3 = p3.X.shape[0]
+    res["c3_ap_step"] = {"ms_per_step": 1e3 * 23 * n3 * n3 / rate3, "extrapolated": True,
+                         "sample": f"oracle fp64 H.V rows 0..{r3} x {n3} points, s=65 ({e3:.1f} s), x 23 "
+                                   "H.V-equivalents per AP step (10 epochs x 2 + 3)"}
+    # config 4 CG step: the device run's ~265 CG iterations per step (scripts/c4_outer.py) + 3
+    p4 = datasets.config4()
+    rate4, r4, e4 = rows_rate(p4, seconds / 8)
+    n4 = p4.X.shape[0]
+    res["c4_cg_step"] = {"ms_per_step": 1e3 * 268 * n4 * n4 / rate4, "extrapolated": True,
+                         "sample": f"oracle fp64 H.V rows 0..{r4} x {n4} points, s=65 ({e4:.1f} s), x 268 "
+                                   "H.V per CG step (~265 iterations, profiles/r2_c4_outer_f32_1gpu.json, + 3)"}
     return res
 
 
