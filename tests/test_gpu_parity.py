@@ -763,3 +763,33 @@ def test_record_solver_state_warm_chaining(ctx, kind):
     h = tr.final_hyperparameters(3)
     assert np.allclose(h.to_constrained_vector(), tr.steps[-1].constrained_params)
     assert tr.total_solver_iterations(2, 3) == tr.steps[1].solver_iterations + tr.steps[2].solver_iterations
+
+
+def _run_check(extra):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    path = os.path.join(root, "gpurun_out", "_apw_%d.npz" % len(extra))
+    env = dict(os.environ, PYTHONPATH=root, **extra)
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "ap_wsd_check.py"), path], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (extra, r.stderr[-2000:])
+    out = dict(np.load(path))
+    os.remove(path)
+    return out
+
+
+def test_ap_incremental_residual_and_wsd_from_residuals_subprocess():
+    """Two algebraic shortcuts against their explicit forms (the settings are
+    read once per process): AP epochs closed with R0 - H dX (exact every 10th)
+    vs B - H X every epoch (WGP_AP_EXACT_EVERY=1) -- same iterations, solutions
+    and residuals to rounding; the warm-start distance from R_end - R_0 vs the
+    explicit H (x0 - x*) product (WGP_WSD_PRODUCT=1), CG and AP, to 1e-4."""
+    fast = _run_check({})
+    ref = _run_check({"WGP_AP_EXACT_EVERY": "1", "WGP_WSD_PRODUCT": "1"})
+    assert abs(int(fast["it"]) - int(ref["it"])) <= 1
+    assert np.linalg.norm(fast["x"] - ref["x"]) <= 1e-4 * np.linalg.norm(ref["x"])
+    assert np.allclose(fast["rel"], ref["rel"], rtol=1e-2)
+    assert np.allclose(fast["wsd"], ref["wsd"], rtol=1e-4, atol=1e-9)
