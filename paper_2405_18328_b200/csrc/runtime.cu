@@ -906,8 +906,10 @@ struct Ctx {
             use_fused = false;
           }
         }
-        if (!ok) throw DeviceError("cg_solve: CUDA graph capture failed");
-        if (alloc_generation().load() != gen) {  // a workspace moved while capturing
+        if (!ok) {
+          // capture unavailable (e.g. a collective that cannot be captured):
+          // eager iterations from here on
+        } else if (alloc_generation().load() != gen) {  // a workspace moved while capturing
           for (auto e : g.exec) cudaGraphExecDestroy(e);
         } else {
           cg_graphs.push_back(g);
