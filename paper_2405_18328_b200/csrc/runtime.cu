@@ -300,7 +300,7 @@ struct Ctx {
   Buf sgd_xsq;    // SGD: running ||X||_F^2
   Buf Rpart;      // row-sharded AP: this rank's share of a block residual
   Buf tr_rhs, tr_sol0, tr_sol1, tr_res, tr_sol64a, tr_sol64b;  // train(): solver state across steps
-  Buf api_B, api_X0, api_Xs, api_Rs;  // wgp_solve staging
+  Buf api_B, api_X0, api_Xs, api_Rs, api_B64;  // wgp_solve staging
   int cg_precision = WGP_CG_F64;
   Buf dhyp;  // device [sf2, a, diag] for the H.V kernels (CUDA-graph friendly)
   Buf hyper_tmp;  // set_hyper staging (centres, scales)
@@ -594,7 +594,7 @@ struct Ctx {
   // and Xo64 (optional) receives the fp64 solutions (the outer loop's warm
   // start keeps them, proj/src/optimizer.cpp:133-135,158).
   SolveOut solve(const wgp_solver_cfg& cfg, const float* B, const float* init, float* Xo, float* Ro,
-                 int s, const double* init64 = nullptr, double* Xo64 = nullptr) {
+                 int s, const double* init64 = nullptr, double* Xo64 = nullptr, const double* B64in = nullptr) {
     require_data();
     validate(cfg);
     if (s < 1) throw std::invalid_argument("solve: rhs needs at least one column");
@@ -628,7 +628,10 @@ struct Ctx {
       double* b64 = B64.as<double>();
       double* x64 = X64.as<double>();
       double* r64 = R64.as<double>();
-      widen(B, ld, b64, ld, n, s, st);
+      if (B64in)  // an fp64 caller's rhs, unrounded
+        WGP_CUDA(cudaMemcpyAsync(b64, B64in, bytes, cudaMemcpyDeviceToDevice, st));
+      else
+        widen(B, ld, b64, ld, n, s, st);
       if (init64 || init) {
         if (init64) WGP_CUDA(cudaMemcpy2DAsync(x64, sizeof(double) * ld, init64, sizeof(double) * ld,
                                                sizeof(double) * n, s, cudaMemcpyDeviceToDevice, st));
@@ -1919,6 +1922,10 @@ int solve_host(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const H* rhs, const H* i
       }
     };
     upload(rhs, B, nullptr);
+    if constexpr (f64) {  // keep the fp64 rhs (io_in is reused for init below)
+      c.api_B64.ensure(sizeof(double) * c.ld * s);
+      WGP_CUDA(cudaMemcpyAsync(c.api_B64.p, c.io_in.p, sizeof(double) * c.ld * s, cudaMemcpyDeviceToDevice, c.st));
+    }
     if (init) {
       c.api_X0.ensure(bytes);
       X0 = c.api_X0.as<float>();
@@ -1929,7 +1936,8 @@ int solve_host(wgp_ctx* ctx, const wgp_solver_cfg* cfg, const H* rhs, const H* i
       c.io_out.ensure(sizeof(double) * c.ld * s);
       Xo64 = c.io_out.as<double>();
     }
-    const wgp::Ctx::SolveOut so = c.solve(*cfg, B, X0, Xs, Rs, s, keep64 ? X0_64 : nullptr, Xo64);
+    const wgp::Ctx::SolveOut so =
+        c.solve(*cfg, B, X0, Xs, Rs, s, keep64 ? X0_64 : nullptr, Xo64, keep64 ? c.api_B64.as<double>() : nullptr);
     if (state) {
       if constexpr (f64) {
         // solutions in fp64 (fp64 CG: unrounded), residuals widened from fp32
