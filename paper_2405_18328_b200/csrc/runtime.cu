@@ -805,7 +805,7 @@ struct Ctx {
     T* Xb = Xbbuf.as<T>();
     T* Rb = Rbbuf.as<T>();
     float* PPp = nullptr;
-    if (!f64) {
+    if (!f64 && !sharded()) {  // (sharded: the H.V splits the gathered P itself -- one all-gather, not three)
       PP.ensure(sizeof(float) * 2 * ld * s);  // P's tf32 planes: the H.V skips its split of P
       PPp = PP.as<float>();
     }
@@ -824,10 +824,7 @@ struct Ctx {
     static const bool no_fused = getenv("WGP_CG_NO_FUSED") != nullptr;
     bool use_fused = !no_fused;
     auto iteration = [&](bool refresh) {
-      if (sh) {
-        gather_rows(Pp, s);
-        if (PPp) gather_rows(PPp, 2 * s);
-      }
+      if (sh) gather_rows(Pp, s);
       cg_hv(Pp, s, HPp, kHvStore, nullptr, done, PPp);
       if (!refresh && !sh && use_fused) {  // alpha + update + direction in one cooperative kernel
         if (cg_fused(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, st, PPp)) return;
