@@ -480,6 +480,10 @@ struct Ctx {
   void gather_rows(T* base, int s) {
     if (sharded()) comm->gather_rows(base, ld, blk, s, sizeof(T), st);
   }
+  // in-place all-gather of equal contiguous chunks: rank r's at base + r chunk
+  void gather_rows_raw(double* base, int64_t chunk) {
+    if (sharded()) comm->gather_rows(base, chunk * nranks, chunk, 1, sizeof(double), st);
+  }
   // column dots over the own rows, summed over the ranks
   template <class T>
   std::vector<double> dots_own(const T* A, const T* B_, int s) {
@@ -945,54 +949,71 @@ struct Ctx {
     // (the last, partial block padded with the identity), one batched
     // cuSOLVER Cholesky over all blocks, then the explicit inverses below.
     // (Per-block potrf + potri and a symm per step cost ~20 small launches per
-    // block and 0.4 ms per symm, measured.)
-    hbuf.ensure(sizeof(double) * static_cast<size_t>(nb) * bs * bs);
-    info.ensure(sizeof(int) * nb);
-    WGP_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int) * nb, st));
+    // block and 0.4 ms per symm, measured.)  Row-sharded contexts factor
+    // their contiguous share of the blocks and all-gather the inverses (every
+    // rank applies every block's solve).
+    const bool sh = sharded();
+    const int64_t nbr = sh ? ceil_div(nb, nranks) : nb;  // blocks per rank
+    const int64_t b0 = sh ? std::min<int64_t>(nb, rank * nbr) : 0, b1 = sh ? std::min<int64_t>(nb, b0 + nbr) : nb;
+    const int64_t nown = b1 - b0;
+    const size_t bb = static_cast<size_t>(bs) * bs;
+    hbuf.ensure(sizeof(double) * bb * static_cast<size_t>(sh ? nbr * nranks : nb));
+    info.ensure(sizeof(int) * std::max<int64_t>(1, nown));
+    WGP_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int) * std::max<int64_t>(1, nown), st));
     const double sf2d = sf * sf, ad = sf * sf * kLn2, n2d = sigma * sigma;
-    std::vector<double*> hptr(nb);
-    for (int64_t b = 0; b < nb; ++b) {
+    std::vector<double*> hptr(std::max<int64_t>(1, nown));
+    for (int64_t b = b0; b < b1; ++b) {
       const int64_t start = b * bs, size = std::min(bs, n - start);
-      hptr[b] = hbuf.as<double>() + static_cast<size_t>(b) * bs * bs;
-      build_block(xs.as<float>(), dp, start, size, bs, sf2d, ad, n2d, hptr[b], st);
+      hptr[b - b0] = hbuf.as<double>() + static_cast<size_t>(b) * bb;
+      build_block(xs.as<float>(), dp, start, size, bs, sf2d, ad, n2d, hptr[b - b0], st);
     }
-    lapack_work.ensure(sizeof(double*) * nb);
-    WGP_CUDA(cudaMemcpyAsync(lapack_work.p, hptr.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice, st));
-    if (cusolverDnDpotrfBatched(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(bs),
-                                reinterpret_cast<double**>(lapack_work.p), static_cast<int>(bs), info.as<int>(),
-                                static_cast<int>(nb)) != CUSOLVER_STATUS_SUCCESS)
-      throw DeviceError("cusolverDnDpotrfBatched failed");
-    std::vector<int> hinfo(nb);
-    WGP_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
-    WGP_CUDA(cudaStreamSynchronize(st));
-    for (int v : hinfo)
-      if (v != 0)
-        throw NumericalError("ap_solve: diagonal block factorization failed, H is not positive definite");
+    bool failed = false;
+    if (nown > 0) {
+      lapack_work.ensure(sizeof(double*) * nown);
+      WGP_CUDA(cudaMemcpyAsync(lapack_work.p, hptr.data(), sizeof(double*) * nown, cudaMemcpyHostToDevice, st));
+      if (cusolverDnDpotrfBatched(cusolver, CUBLAS_FILL_MODE_LOWER, static_cast<int>(bs),
+                                  reinterpret_cast<double**>(lapack_work.p), static_cast<int>(bs), info.as<int>(),
+                                  static_cast<int>(nown)) != CUSOLVER_STATUS_SUCCESS)
+        throw DeviceError("cusolverDnDpotrfBatched failed");
+      std::vector<int> hinfo(nown);
+      WGP_CUDA(cudaMemcpyAsync(hinfo.data(), info.p, sizeof(int) * nown, cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaStreamSynchronize(st));
+      for (int v : hinfo) failed = failed || v != 0;
+    }
+    if (sh) {  // every rank raises the same error
+      std::vector<double> f{failed ? 1.0 : 0.0};
+      sum_over_ranks(f);
+      failed = f[0] > 0.0;
+    }
+    if (failed) throw NumericalError("ap_solve: diagonal block factorization failed, H is not positive definite");
     // H_bb^-1 = L^-T L^-1 for all blocks: batched triangular solve against the
     // identity, then a strided-batched GEMM (per-block cublasDtrsm in the
     // epoch loop expanded to ~30 kernels, ~0.5 ms per block, measured); each
     // Gauss-Seidel step is then one DGEMM.
-    const size_t bb = static_cast<size_t>(bs) * bs;
-    linv.ensure(sizeof(double) * bb * nb);
-    identities(linv.as<double>(), bs, nb, st);
-    std::vector<double*> lptr(nb);
-    for (int64_t b = 0; b < nb; ++b) lptr[b] = linv.as<double>() + b * bb;
-    Buf& lp = linv_ptrs;  // persistent: a fresh allocation would invalidate the cached graphs
-    lp.ensure(sizeof(double*) * nb);
-    WGP_CUDA(cudaMemcpyAsync(lp.p, lptr.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice, st));
-    const double one_ = 1.0, zero_ = 0.0;
-    if (cublasDtrsmBatched(cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
-                           static_cast<int>(bs), static_cast<int>(bs), &one_,
-                           reinterpret_cast<const double* const*>(lapack_work.p), static_cast<int>(bs),
-                           reinterpret_cast<double* const*>(lp.p), static_cast<int>(bs),
-                           static_cast<int>(nb)) != CUBLAS_STATUS_SUCCESS)
-      throw DeviceError("cublasDtrsmBatched failed");
-    if (cublasDgemmStridedBatched(cublas, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(bs), static_cast<int>(bs),
-                                  static_cast<int>(bs), &one_, linv.as<double>(), static_cast<int>(bs),
-                                  static_cast<long long>(bb), linv.as<double>(), static_cast<int>(bs),
-                                  static_cast<long long>(bb), &zero_, hbuf.as<double>(), static_cast<int>(bs),
-                                  static_cast<long long>(bb), static_cast<int>(nb)) != CUBLAS_STATUS_SUCCESS)
-      throw DeviceError("cublasDgemmStridedBatched failed");
+    if (nown > 0) {
+      linv.ensure(sizeof(double) * bb * nown);
+      identities(linv.as<double>(), bs, nown, st);
+      std::vector<double*> lptr(nown);
+      for (int64_t b = 0; b < nown; ++b) lptr[b] = linv.as<double>() + b * bb;
+      Buf& lp = linv_ptrs;  // persistent: a fresh allocation would invalidate the cached graphs
+      lp.ensure(sizeof(double*) * nown);
+      WGP_CUDA(cudaMemcpyAsync(lp.p, lptr.data(), sizeof(double*) * nown, cudaMemcpyHostToDevice, st));
+      const double one_ = 1.0, zero_ = 0.0;
+      if (cublasDtrsmBatched(cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                             static_cast<int>(bs), static_cast<int>(bs), &one_,
+                             reinterpret_cast<const double* const*>(lapack_work.p), static_cast<int>(bs),
+                             reinterpret_cast<double* const*>(lp.p), static_cast<int>(bs),
+                             static_cast<int>(nown)) != CUBLAS_STATUS_SUCCESS)
+        throw DeviceError("cublasDtrsmBatched failed");
+      if (cublasDgemmStridedBatched(cublas, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(bs), static_cast<int>(bs),
+                                    static_cast<int>(bs), &one_, linv.as<double>(), static_cast<int>(bs),
+                                    static_cast<long long>(bb), linv.as<double>(), static_cast<int>(bs),
+                                    static_cast<long long>(bb), &zero_, hbuf.as<double>() + b0 * bb,
+                                    static_cast<int>(bs), static_cast<long long>(bb),
+                                    static_cast<int>(nown)) != CUBLAS_STATUS_SUCCESS)
+        throw DeviceError("cublasDgemmStridedBatched failed");
+    }
+    if (sh) gather_rows_raw(hbuf.as<double>(), nbr * bb);  // rank r's blocks [r nbr, (r + 1) nbr)
     ap_bs = bs;
     return nb;
   }
