@@ -53,6 +53,11 @@ class Device {
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;
   wgp_ctx* get() const { return ctx_; }
+  /// CG's precision (WGP_CG_F64, the default: the reference's iteration counts;
+  /// WGP_CG_F32: fp32 vectors over the tensor-core operator, faster).
+  void set_cg_precision(int precision) { check(wgp_set_cg_precision(ctx_, precision)); }
+  /// Join an NCCL communicator (one process per GPU); call before the data is set.
+  void set_comm(int rank, int nranks, const unsigned char id[128]) { check(wgp_set_comm(ctx_, rank, nranks, id)); }
 
  private:
   wgp_ctx* ctx_ = nullptr;
