@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--hv-impl", default="tc", choices=["tc", "tc_bf16", "simt"])
+    ap.add_argument("--hv-impl", default="tc", choices=["tc", "tc_f16", "simt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-outer", action="store_true", help="skip the per-outer-step timings")
@@ -624,7 +624,7 @@ def main():
     p_tf32 = p_bf16 / 2                                # TF32 = half the bf16 rate
     p_ffma = 2 * 128 * 148 * pk["mhz"] * 1e6
     p_mufu = 16 * 148 * pk["mhz"] * 1e6                # ex2 / sqrt per s (16/clk/SM)
-    if args.hv_impl in ("tc", "tc_bf16"):
+    if args.hv_impl in ("tc", "tc_f16"):
         p_tc = p_tf32 / 3 if args.hv_impl == "tc" else p_bf16 / 3
         t_pipes = (2 * d + 2 * s) / p_tc + 8 / p_ffma
         basis = (f"sum-of-pipes: {2 * d + 2 * s} tensor flop/entry at {'P_TF32' if args.hv_impl == 'tc' else 'P_BF16'}/3 "

@@ -46,11 +46,11 @@ typedef struct wgp_ctx wgp_ctx;
  * at higher precision, so the error does not grow with n):
  *   WGP_HV_TC       tcgen05, Gram and K.V in 3xTF32 (default, ~1e-6 relative)
  *   WGP_HV_SIMT     CUDA-core fp32 kernel (direct differences, ~1e-7)
- *   WGP_HV_TC_BF16  tcgen05, K.V in bf16x3 (faster; ~5e-6 relative, too
- *                   coarse for tight solver tolerances) */
+ *   WGP_HV_TC_F16   tcgen05, K.V in fp16x3 over column-scaled V (half the
+ *                   K.V tensor work of 3xTF32, the same 22-bit operand split) */
 #define WGP_HV_TC 0
 #define WGP_HV_SIMT 1
-#define WGP_HV_TC_BF16 2
+#define WGP_HV_TC_F16 2
 /* Precision of CG's solver state and operator (proj/src/solvers.cpp:81-139):
  *   WGP_CG_F64  fp64 x / r / p / Hp over the fp64-accumulating symmetric
  *               operator (hv_f64.cu): iteration counts of the fp64 reference

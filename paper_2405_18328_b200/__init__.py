@@ -30,10 +30,10 @@ _LIB_NAME = "libwarmgp_b200.so"
 _lib = None
 
 WGP_OK, WGP_INVALID, WGP_NUMERICAL, WGP_DEVICE = 0, 2, 3, 4
-HV_TC, HV_SIMT, HV_TC_BF16 = 0, 1, 2
-# tc: tcgen05 3xTF32 (default); simt: CUDA-core fp32; tc_bf16: tcgen05 with
-# bf16x3 K.V (faster, ~5e-6 relative: not for tight solver tolerances)
-_HV_IMPLS = {"tc": HV_TC, "simt": HV_SIMT, "tc_bf16": HV_TC_BF16}
+HV_TC, HV_SIMT, HV_TC_F16 = 0, 1, 2
+# tc: tcgen05 3xTF32 (default); simt: CUDA-core fp32; tc_f16: tcgen05 with
+# fp16x3 K.V over column-scaled V (half the K.V tensor work, same operand split)
+_HV_IMPLS = {"tc": HV_TC, "simt": HV_SIMT, "tc_f16": HV_TC_F16}
 CG_F64, CG_F32 = 0, 1
 _CG_PRECISIONS = {"f64": CG_F64, "f32": CG_F32}
 _KINDS = {"cg": 0, "ap": 1, "sgd": 2}

@@ -28,12 +28,12 @@
 // epilogue folds into a shared-memory fp32 sum and an fp64 CTA sum (error
 // independent of n).  J tiles of a row tile may be split across CTAs (split
 // count keyed on the global n, partials summed in fixed order ->
-// deterministic and shard-invariant).  WGP_HV_TC_BF16 selects the opt-in
+// deterministic and shard-invariant).  WGP_HV_TC_F16 selects the opt-in
 // bf16x3 K.V variant (kind::f16, 64-point tiles).
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <mutex>
@@ -49,7 +49,12 @@ namespace {
 
 constexpr int kTI = 128;   // rows per tile (MMA M)
 constexpr int kKA = 32;    // augmented Gram dimension (d + 2 <= 32)
-constexpr int kThreads = 512;  // 3 epilogue warpgroups + 4 control warps
+#ifndef WGP_TC_EPI
+#define WGP_TC_EPI 3
+#endif
+constexpr int kEpiGroups = WGP_TC_EPI;          // epilogue warpgroups
+constexpr int kThreads = 128 * kEpiGroups + 128;  // + 4 control warps
+constexpr int kDrainK = (96 + 8 * kEpiGroups - 1) / (8 * kEpiGroups);  // 8-column pieces per group drain
 constexpr uint32_t kTfMask = 0xFFFFE000u;  // keep sign, exponent, 10 mantissa bits
 constexpr int kSmemLimit = 232448 - 2048;  // 227 KB opt-in minus static smem (barriers)
 constexpr int kMaxStages = 8;              // smem ring depth cap (barrier arrays)
@@ -73,29 +78,35 @@ __device__ __forceinline__ void to_k(const uint32_t (&r)[32], uint32_t (&khi)[32
   }
 }
 
-// 32 squared distances (one half of a 64-point tile) -> 32 packed bf16x2
-// words: w[c] = k1 pair c = bf16(k), w[16 + c] = k2 pair c = bf16(k - k1)
-// (lower K index in the low half).  POLY evaluates 2^-u of the odd entries on
-// the FMA pipe (ex2_poly) instead of the MUFU.  The squared distance from the
-// tensor core can be a tiny negative number for (near-)duplicate points;
-// sqrt(|u^2|) keeps it finite and folds the abs into the MUFU operand.  DIAG
-// is a separate instantiation for the rare tiles that contain the diagonal,
-// so the common path carries no per-entry index compares.
+// 32 squared distances (one half of a 64-point tile) -> 32 packed f16x2
+// words: w[c] = k1 pair c = f16(k'), w[16 + c] = k2 pair c = f16(k' - k1)
+// (lower K index in the low half), k' = 2^14 (1 + u ln2) 2^-u = 2^14 k / sf^2
+// in (0, 2^14]: the signal variance is applied to the output, and the 2^14
+// lifts k' so that k2 stays a normal fp16 number down to k' ~ 2^-3, i.e.
+// k / sf^2 >= 2^-17 (below that its absolute error is < 2^-39 sf^2).  fp16
+// keeps 11 significant bits like tf32, so k1 + k2 carries 22 bits.  POLY
+// evaluates 2^-u of the odd entries on the FMA pipe (ex2_poly) instead of the
+// MUFU.  The squared distance from the tensor core can be a tiny negative
+// number for (near-)duplicate points; sqrt(|u^2|) keeps it finite and folds
+// the abs into the MUFU operand.  DIAG is a separate instantiation for the
+// rare tiles that contain the diagonal, so the common path carries no
+// per-entry index compares.
+constexpr float kKScale = 16384.f;  // 2^14
 template <bool POLY, bool DIAG>
-__device__ __forceinline__ void to_k_bf16(const uint32_t (&r)[32], uint32_t (&w)[32], float sf2, float ac,
-                                          int dg) {
+__device__ __forceinline__ void to_k_f16(const uint32_t (&r)[32], uint32_t (&w)[32], int dg) {
+  constexpr float ks = kKScale, ka = kKScale * 0.69314718055994531f;
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
-    float ka = matern_from_u(sqrt_approx(fabsf(__uint_as_float(r[2 * c]))), sf2, ac);
+    float k0 = matern_from_u(sqrt_approx(fabsf(__uint_as_float(r[2 * c]))), ks, ka);
     const float ub = sqrt_approx(fabsf(__uint_as_float(r[2 * c + 1])));
-    float kb = POLY ? fmaf(ac, ub, sf2) * ex2_poly(-ub) : matern_from_u(ub, sf2, ac);
+    float k1 = POLY ? fmaf(ka, ub, ks) * ex2_poly(-ub) : matern_from_u(ub, ks, ka);
     if (DIAG) {
-      if (dg == 2 * c) ka = 0.f;
-      if (dg == 2 * c + 1) kb = 0.f;
+      if (dg == 2 * c) k0 = 0.f;
+      if (dg == 2 * c + 1) k1 = 0.f;
     }
-    const __nv_bfloat162 h = __floats2bfloat162_rn(ka, kb);
-    const float2 hf = __bfloat1622float2(h);
-    const __nv_bfloat162 l = __floats2bfloat162_rn(ka - hf.x, kb - hf.y);
+    const __half2 h = __floats2half2_rn(k0, k1);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(k0 - hf.x, k1 - hf.y);
     w[c] = *reinterpret_cast<const uint32_t*>(&h);
     w[16 + c] = *reinterpret_cast<const uint32_t*>(&l);
   }
@@ -123,6 +134,7 @@ struct TcArgs {
   int mode;
   float sf2, a, diag;
   const float* hyp;  // device [sf2, a, diag] (overrides the three above when set)
+  const float* vscale;  // H16: per column 2^-e_c, the inverse of the power of two that scaled V's fp16 planes
   float* part;       // [splits][s_pad][m_pad] fp32 split partials (splits > 1)
   int tma_part;      // 1: the final partial tile goes out as one TMA store (mPart)
   double* flush;     // [splits][s_pad][m_pad] fp64 running sums (T > flush_every * chunk)
@@ -133,11 +145,11 @@ struct TcArgs {
   long long* ctatime;  // WGP_TC_TRACE: per CTA {smid, globaltimer at start, after the tile loop, at exit}
   int nk1;  // packed Gram K steps (TcOperands::nk1), 0: 12 hi / lo MMAs
   int dbg;  // ablation bits (WGP_TC_DEBUG): 1 no epilogue math, 2 no MMA-2, 4 no MMA-1, 8 no V loads,
-            // 16 no epilogue TMEM traffic, 32 no B loads, 128 (bf16) FMA-pipe ex2 for odd entries
+            // 16 no epilogue TMEM traffic, 32 no B loads, 128 (H16) FMA-pipe ex2 for odd entries
 };
 
 // Two K.V precisions share the pipeline:
-//   BF = false (default, WGP_HV_TC): K.V in 3xTF32 (k_hi v_hi + k_hi v_lo +
+//   H16 = false (default, WGP_HV_TC): K.V in 3xTF32 (k_hi v_hi + k_hi v_lo +
 //     k_lo v_hi, ~2^-21 per product), 32-point J tiles.  TMEM: O0 [0, 96),
 //     O1 [96, 192), A_I hi/lo [192, 256) (MMA-1 reads A from TMEM), two
 //     128-column groups from 256.  A group serves two tiles: MMA-1 writes
@@ -145,7 +157,7 @@ struct TcArgs {
 //     tf32 MMA costs >= 35 clk whatever its size, so N = 32 ran at half the
 //     tensor rate, measured), the epilogue overwrites each S in place with
 //     k_hi and writes k_lo 64 columns further.
-//   BF = true (WGP_HV_TC_BF16): K.V in bf16x3 (k1 v1 + k1 v2 + k2 v1, ~2^-17
+//   H16 = true (WGP_HV_TC_F16): K.V in bf16x3 (k1 v1 + k1 v2 + k2 v1, ~2^-17
 //     per product: half the tensor work, too coarse for tight solver
 //     tolerances), 64-point J tiles.  TMEM: O0, O1, five 64-column groups
 //     from 192 of one tile each (S: 64 fp32 columns, overwritten by the packed
@@ -161,38 +173,37 @@ struct TcArgs {
 constexpr bool kTfSingleO = WGP_TC_LAYOUT == 0;
 constexpr bool kTfATmem = WGP_TC_LAYOUT == 2;
 constexpr int kTfGroups = kTfSingleO ? 3 : 2;
-template <bool BF>
+template <bool H16>
 struct Cfg {
-  static constexpr int kTJ = BF ? 64 : 32;        // points per J tile (MMA-2 K, epilogue)
-  static constexpr int kP = BF ? 1 : 2;           // tiles per MMA-1 group
+  static constexpr int kTJ = H16 ? 64 : 32;        // points per J tile (MMA-2 K, epilogue)
+  static constexpr int kP = H16 ? 1 : 2;           // tiles per MMA-1 group
   static constexpr int kN1 = kP * kTJ;            // MMA-1 N = points per B stage (64)
-  static constexpr int kGroups = BF ? 5 : kTfGroups;  // MMA-1 groups in flight (TMEM)
+  static constexpr int kGroups = H16 ? (kTfATmem ? 4 : 5) : kTfGroups;  // MMA-1 groups in flight (TMEM)
   static constexpr int kTilesInFlight = kP * kGroups;
-  static constexpr uint32_t kGW = BF ? 64u : 128u;  // TMEM columns per group
+  static constexpr uint32_t kGW = H16 ? 64u : 128u;  // TMEM columns per group
   // tf32 layout variant (kTfSingleO): one O accumulator [0, 96) whose chunk
   // drains stall MMA-2, A_I in shared memory (SS Gram), three groups from 96
   // (6 tiles in flight); otherwise O0 | O1, A_I in TMEM, two groups from 256.
-  static constexpr bool kATmem = !BF && kTfATmem;
-  static constexpr int kOBufs = (BF || !kTfSingleO) ? 2 : 1;
+  static constexpr bool kATmem = kTfATmem;
+  static constexpr int kOBufs = (H16 || !kTfSingleO) ? 2 : 1;
   static constexpr uint32_t kOStride = kOBufs == 2 ? 96u : 0u;
   static constexpr uint32_t kAhi = 192, kAlo = 224;  // kATmem only
-  static constexpr uint32_t kBufFirst = BF ? 192u : (kTfSingleO ? 96u : (kATmem ? 256u : 192u));
+  static constexpr uint32_t kBufFirst = kATmem ? 256u : (H16 || !kTfSingleO ? 192u : 96u);
   static constexpr uint32_t kBStage = 2u * kN1 * 128u;  // B_hi | B_lo planes
-  static constexpr uint32_t kLoOff = 64;                // BF = false: k_lo column offset
+  static constexpr uint32_t kLoOff = 64;                // H16 = false: k_lo column offset
   static __device__ __forceinline__ uint32_t grp_col(int gi) { return kBufFirst + kGW * static_cast<uint32_t>(gi); }
-  // TMEM column of tile t's S / k_hi (BF: S / packed k1 | k2)
+  // TMEM column of tile t's S / k_hi (H16: S / packed k1 | k2)
   static __device__ __forceinline__ uint32_t tile_col(int t) {
     return grp_col((t / kP) % kGroups) + 32u * static_cast<uint32_t>(t % kP);
   }
 };
 
-constexpr int kEpiGroups = 3;
 // Warp roles.  The warp scheduler prefers the highest warp id among eligible
 // warps, so the latency-critical control warps get the top ids and the 12
 // always-eligible epilogue warps (0..11; warp w reads TMEM lanes 32 (w % 4))
 // cannot starve them.
 constexpr int kEpiWarps = 4 * kEpiGroups;
-constexpr int kWarpBProd = 12, kWarpM1 = 13, kWarpVProd = 14, kWarpM2 = 15;
+constexpr int kWarpBProd = kEpiWarps, kWarpM1 = kEpiWarps + 1, kWarpVProd = kEpiWarps + 2, kWarpM2 = kEpiWarps + 3;
 
 // Accumulation precision.  MMA-2 accumulates into fp32 TMEM, and every
 // K-step instruction rounds the running sum: with ~3 n / 8 roundings per
@@ -207,13 +218,13 @@ constexpr int kWarpBProd = 12, kWarpM1 = 13, kWarpVProd = 14, kWarpM2 = 15;
 // per chunk) + sqrt(flush_every) roundings, independent of n; the
 // shared-memory drain costs no L2 traffic (an fp64 global drain per chunk
 // measured +20% time).
-template <bool BF>
+template <bool H16>
 __global__ void __launch_bounds__(kThreads, 1)
     hv_tc_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                  const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                  const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
                  const __grid_constant__ CUtensorMap mPart, const TcArgs p) {
-  using K = Cfg<BF>;
+  using K = Cfg<H16>;
   constexpr int NBUF = K::kTilesInFlight;  // kfull ring
   constexpr int TJ = K::kTJ;
   constexpr int P = K::kP;
@@ -230,11 +241,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       bar_m2done[kDoneRing];
   __shared__ __align__(8) uint64_t bar_a, bar_atm, bar_kfull[NBUF], bar_ofull[2], bar_odrained[2];
   __shared__ uint32_t tmem_slot;
+  // bar_turn[w][q]: epilogue warp q of group w may start its tile's math (the
+  // previous tile's warp q on the same SMSP is done with the MUFU)
+  __shared__ __align__(8) uint64_t bar_turn[kEpiGroups][4];
+  // H16: per epilogue warp, 2^-e of the columns [cb, ce) it finishes (cp.async prefetch)
+  __shared__ float sColScale[H16 ? kEpiWarps : 1][8 * kDrainK];
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAhi = smem;
   uint8_t* sAlo = smem + 16384;
-  // R: [s_pad][128] fp32 running sum; with A_I in TMEM (BF = false) it reuses
+  // R: [s_pad][128] fp32 running sum; with A_I in TMEM it reuses
   // A's staging area, which is dead once A has been copied to TMEM.
   float* sR = reinterpret_cast<float*>(K::kATmem ? smem : smem + 32768);
   uint8_t* sB = smem + p.a_region;                            // nb x [B_hi | B_lo]
@@ -264,11 +280,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_m2done[i], 1);
     }
     mbar_init(&bar_a, 1);
+    for (int i = 0; i < kEpiGroups * 4; ++i) mbar_init(&bar_turn[i / 4][i % 4], 1);
     mbar_init(&bar_atm, 4);
     // tf32: the V tile of slot b completes on kfull[b] too (NV == NBUF): 4
     // epilogue arrivals + the producer's expect_tx arrival, so MMA-2 checks
     // one barrier per tile (each check costs ~90 clk of its loop, measured)
-    for (int i = 0; i < NBUF; ++i) mbar_init(&bar_kfull[i], BF ? 4 : 5);
+    for (int i = 0; i < NBUF; ++i) mbar_init(&bar_kfull[i], H16 ? 4 : 5);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar_ofull[i], 1);
       mbar_init(&bar_odrained[i], kEpiWarps);
@@ -319,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t >= NV) mbar_wait(&bar_m2done[(t - NV) & (kDoneRing - 1)], ((t - NV) >> 3) & 1);
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const int vp = (jt_begin + t) * TJ;
-        uint64_t* vbar = BF ? &bar_vfull[st] : &bar_kfull[st];  // tf32: st == t % NBUF
+        uint64_t* vbar = H16 ? &bar_vfull[st] : &bar_kfull[st];  // tf32: st == t % NBUF
         if (p.dbg & 8) {
           mbar_arrive_warp(vbar);
           continue;
@@ -393,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kWarpM2) {
     // ------------------------------------------------------------ MMA-2 issuer
     if (T > 0) {
-      const uint32_t id2 = BF ? idesc_bf16(kTI, spad) : idesc_tf32(kTI, spad);
+      const uint32_t id2 = H16 ? idesc_f16(kTI, spad) : idesc_tf32(kTI, spad);
       const uint64_t box = vbox >> 4;
       int b = 0, st = 0, c = 0, tc = 0;
       uint32_t kph = 0, vph = 0;
@@ -406,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bar_odrained[cp & 1], (cp >> 1) & 1);
         }
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 12] = clock64();
-        if (BF) mbar_wait(&bar_vfull[st], vph);
+        if (H16) mbar_wait(&bar_vfull[st], vph);
         if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 13] = clock64();
         mbar_wait(&bar_kfull[b], kph);
         tc_after();
@@ -414,17 +431,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const uint32_t kb = tmem + K::tile_col(t);
         const uint64_t dv = umma_desc(base);
-        if (!(p.dbg & 2) && !BF) {
-          static_assert(BF || K::kLoOff == 64, "mma2_tile_tf32 assumes k_lo 64 columns after k_hi");
+        if (!(p.dbg & 2) && !H16) {
+          static_assert(H16 || K::kLoOff == 64, "mma2_tile_tf32 assumes k_lo 64 columns after k_hi");
           mma2_tile_tf32(o, kb, dv, dv + box, id2, tc > 0 ? 1u : 0u);
         } else if (!(p.dbg & 2)) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            if constexpr (BF) {
+            if constexpr (H16) {
               // per 32-point half h: k1 in columns [32h, 32h+16), k2 in
               // [32h+16, 32h+32); a 16-point K step is 8 columns
               const uint32_t c1 = 32u * (k >> 1) + 8u * (k & 1);
-              mma3_ts_bf16(o, kb + c1, kb + c1 + 16, dv + 2 * k, dv + box + 2 * k, id2,
+              mma3_ts_f16(o, kb + c1, kb + c1 + 16, dv + 2 * k, dv + box + 2 * k, id2,
                            (tc > 0 || k > 0) ? 1u : 0u);
             } else {
               // k_hi in the tile's 32 columns, k_lo kLoOff further; an 8-point K step is 8 columns
@@ -503,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* Vd = sVd + row;  // column c at Vd[c * 128]
     // Group w owns the contiguous column block [cb, ce) (<= 32 columns,
     // multiples of 8): one TMEM round trip per drain.
-    const int cpg = ((spad + 3 * 8 - 1) / (3 * 8)) * 8;
+    const int cpg = ((spad + kEpiGroups * 8 - 1) / (kEpiGroups * 8)) * 8;
     const int cb = min(spad, w * cpg), ce = min(spad, (w + 1) * cpg);
     // Intermediate chunk c: R (+)= O[c & 1] (every flush_every chunks R moves
     // into the fp64 sum F instead); O[c & 1] is released to MMA-2 once read.
@@ -513,17 +530,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
       const bool fresh = c % FE == 0;  // R starts over with this chunk
       const bool flush = (c + 1) % FE == 0;
-      uint32_t o[4][8];
+      uint32_t o[kDrainK][8];
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < kDrainK; ++k)
         if (cb + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + cb + 8 * k, o[k]);
       tmem_wait_ld();
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_odrained[c & 1]);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kDrainK; ++k) {
         if (cb + 8 * k >= ce) break;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -554,10 +571,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
       const bool fresh = c % FE == 0;
-      uint32_t o[4][8];
+      uint32_t o[kDrainK][8];
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < kDrainK; ++k)
         if (cb + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + cb + 8 * k, o[k]);
       tmem_wait_ld();
       if (p.ctatime && threadIdx.x == 0) {
@@ -568,17 +585,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       // split partial as one TMA store of R (all 384 epilogue threads fold
       // their rows first; rows past m land in the padding rows of `part`)
       const bool tma_out = p.tma_part && c < FE;
+      // H16: O carries sf^2-free k' = 2^14 k / sf^2 times V 2^e_c (to_k_f16, split_v_f16_kernel)
+      float osc = 1.f;
+      if constexpr (H16) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();  // (before any lane leaves: the column scales come from the whole warp)
+        osc = sf2 * (1.f / kKScale);
+      }
       if (!valid && !tma_out) return;
+      auto colsc = [&](int col) { return H16 ? osc * sColScale[warp][col - cb] : 1.f; };
       // Fold the accumulator into R (one short unrolled block), then a rolled
       // loop over the row's columns: this code runs once per CTA from a cold
       // instruction cache, so its length, not its arithmetic, sets its time
       // (measured: ~4 us for the fully unrolled form, ~40 clk per instruction).
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < kDrainK; ++k)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int col = cb + 8 * k + i;
-          if (col < ce) R[col * 128] = (fresh ? 0.f : R[col * 128]) + __uint_as_float(o[k][i]);
+          if (col < ce) {
+            const float r = (fresh ? 0.f : R[col * 128]) + __uint_as_float(o[k][i]);
+            R[col * 128] = (H16 && tma_out) ? r * colsc(col) : r;
+          }
         }
       if (p.ctatime && threadIdx.x == 0) {
         long long gt;
@@ -613,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int col = cb; col < cend; ++col) {
           float r = R[col * 128];
           if (c >= FE) r = static_cast<float>(__ldcg(F + static_cast<int64_t>(col) * p.m_pad) + static_cast<double>(r));
+          if (H16) r *= colsc(col);
           part[static_cast<int64_t>(col) * p.m_pad] = r;
         }
         return;
@@ -622,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int col = cb; col < cend; ++col) {
         float r = R[col * 128];
         if (c >= FE) r = static_cast<float>(__ldcg(F + static_cast<int64_t>(col) * p.m_pad) + static_cast<double>(r));
+        if (H16) r *= colsc(col);
         r = fmaf(dscale, diag ? Vd[col * 128] : 0.f, r);
         float* dst = p.out + lr + static_cast<int64_t>(col) * p.ldo;
         if (p.mode == kHvStore)
@@ -639,6 +669,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                      "l"(p.V + g + static_cast<int64_t>(col) * p.ldv)
                      : "memory");
     }
+    if constexpr (H16) {
+      for (int c = cb + lane; c < ce; c += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&sColScale[warp][c - cb])),
+                     "l"(p.vscale + c)
+                     : "memory");
+    }
     asm volatile("cp.async.commit_group;" ::: "memory");
     // Chunk dc is drained `lag` tiles after it ended, so its last MMA-2 has
     // retired by then; every group still drains it before MMA-2 reaches
@@ -646,6 +682,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (single O: drained as soon as possible, MMA-2 waits for it)
     const int lag = K::kOBufs == 1 ? 0 : max(2, C / 2);
     int dc = 0;  // next chunk to drain
+    const bool turns = p.dbg & 512;
+    uint32_t turn_ph = 0;
     for (int t = w; t < T; t += kEpiGroups) {
       while (dc < nch - 1 && t >= (dc + 1) * C + lag) drain(dc++);
       const int b = t % NBUF;
@@ -659,37 +697,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 16 + 1] = clock64();
       const int dgi = static_cast<int>(dg < 0 || dg >= TJ ? -1 : dg);
       if (!(p.dbg & 16)) {
-        if constexpr (BF) {
-          // both 32-column halves of S are read first; each half is then
-          // overwritten in place by [k1 pairs (16 cols) | k2 pairs (16 cols)]
-          uint32_t r0[32], r1[32], wds[32];
+        if constexpr (H16) {
+          // each 32-column half of S is read, converted and overwritten in
+          // place by [k1 pairs (16 cols) | k2 pairs (16 cols)]; the second
+          // half's load is issued before the first half's stores, and only
+          // one half's values are live at a time (the 128-register epilogue
+          // spilled with both)
+          uint32_t r[32], wds[32];
           __syncwarp();
-          tmem_ld32(tmem + lanes + bcol, r0);
-          tmem_ld32(tmem + lanes + bcol + 32, r1);
+          tmem_ld32(tmem + lanes + bcol, r);
           tmem_wait_ld();
-#pragma unroll
+          if (turns && t > 0) {
+            mbar_wait(&bar_turn[w][q], turn_ph & 1);
+            ++turn_ph;
+          }
+#pragma unroll 1
           for (int half = 0; half < 2; ++half) {
-            const uint32_t(&r)[32] = half ? r1 : r0;
             const int dh = dgi - 32 * half;
             if (nomath) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) wds[i] = r[i];
             } else if (diag_tile) {
-              to_k_bf16<false, true>(r, wds, sf2, ac, dh);
+              to_k_f16<false, true>(r, wds, dh);
             } else if (p.dbg & 128) {
-              to_k_bf16<true, false>(r, wds, sf2, ac, dh);
+              to_k_f16<true, false>(r, wds, dh);
             } else {
-              to_k_bf16<false, false>(r, wds, sf2, ac, dh);
+              to_k_f16<false, false>(r, wds, dh);
             }
             __syncwarp();
+            if (half == 0) tmem_ld32(tmem + lanes + bcol + 32, r);
             tmem_st32(tmem + lanes + bcol + 32 * half, wds);
+            if (half == 0) tmem_wait_ld();
           }
+          if (turns && lane == 0 && t + 1 < T) mbar_arrive(&bar_turn[w == kEpiGroups - 1 ? 0 : w + 1][q]);
         } else {
           // S (32 columns) -> k_hi in place, k_lo kLoOff columns further
           uint32_t r[32], khi[32], klo[32];
           __syncwarp();
           tmem_ld32(tmem + lanes + bcol, r);
           tmem_wait_ld();
+          if (turns && t > 0) {
+            mbar_wait(&bar_turn[w][q], turn_ph & 1);
+            ++turn_ph;
+          }
           if (nomath) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) khi[i] = r[i], klo[i] = 0u;
@@ -697,6 +747,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             to_k<true>(r, khi, klo, sf2, ac, dgi);
           } else {
             to_k<false>(r, khi, klo, sf2, ac, dgi);
+          }
+          if (turns && t + 1 < T) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_turn[w == kEpiGroups - 1 ? 0 : w + 1][q]);
           }
           __syncwarp();
           tmem_st32(tmem + lanes + bcol, khi);
@@ -773,16 +827,52 @@ __global__ void split_v_kernel(const float* V, int64_t ldv, int64_t j0, int64_t 
   lo[c * ldw + j] = v - vh;
 }
 
-// V[j0:j1, :s] -> bf16 planes v1 = bf16(v), v2 = bf16(v - v1) [s][ldw].
-__global__ void split_v_bf16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, __nv_bfloat16* v1,
-                                    __nv_bfloat16* v2, int64_t ldw) {
+// Column max |V[j0:j1, c]| as float bits (monotone for |v|) -> cmax[c]
+// (zeroed by the caller); NaN sorts above every finite value.
+__global__ void colmax_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, unsigned* cmax) {
+  const int c = blockIdx.y;
+  unsigned m = 0u;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < nv;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = max(m, __float_as_uint(V[j0 + j + c * ldv]) & 0x7FFFFFFFu);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ unsigned sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < blockDim.x / 32 ? sm[threadIdx.x] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0 && m) atomicMax(cmax + c, m);
+  }
+}
+
+// Power of two 2^e_c putting the column max into [2^14, 2^15): the fp16 planes
+// of the scaled column are then normal down to 2^-28 of its max (hi) and the
+// lo residual down to 2^-17 of it; below, their absolute error is < 2^-39 of
+// the max.  Zero and non-finite columns keep e = 0 (NaN / Inf propagate).
+__device__ __forceinline__ float col_scale(unsigned mbits) {
+  const int E = static_cast<int>(mbits >> 23);
+  int e = 0;
+  if (E == 0 && mbits) e = 100;
+  else if (E > 0 && E < 255) e = min(100, max(-100, 141 - E));
+  return __int_as_float((127 + e) << 23);
+}
+
+// V[j0:j1, :s] -> fp16 planes v1 = f16(2^e_c v), v2 = f16(2^e_c v - v1) [s][ldw];
+// vscale[c] = 2^-e_c (exact: |e_c| <= 100).
+__global__ void split_v_f16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, const unsigned* cmax,
+                                   __half* v1, __half* v2, int64_t ldw, float* vscale) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
+  const float sc = col_scale(cmax[c]);
+  if (j == 0) vscale[c] = 1.f / sc;
   if (j >= nv) return;
-  const float v = V[j0 + j + c * ldv];
-  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  const float v = V[j0 + j + c * ldv] * sc;
+  const __half h = __float2half_rn(v);
   v1[c * ldw + j] = h;
-  v2[c * ldw + j] = __float2bfloat16_rn(v - __bfloat162float(h));
+  v2[c * ldw + j] = __float2half_rn(v - __half2float(h));
 }
 
 // Augmented operand rows from the prepared points (see TcOperands).
@@ -989,13 +1079,13 @@ void TcOperands::build(const float* xs, int64_t n_, int dp, int d_, cudaStream_t
   valid = true;
 }
 
-template <bool BF>
+template <bool H16>
 void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorMap& mBhi, const CUtensorMap& mBlo,
                const CUtensorMap& mPart,
                const CUtensorMap& mVhi, const CUtensorMap& mVlo, const TcArgs& a, unsigned grid, int smem,
                cudaStream_t st) {
-  WGP_SMEM_ATTR(hv_tc_kernel<BF>, kSmemLimit);
-  hv_tc_kernel<BF><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart, a);
+  WGP_SMEM_ATTR(hv_tc_kernel<H16>, kSmemLimit);
+  hv_tc_kernel<H16><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart, a);
   WGP_LAUNCH_CHECK();
 }
 
@@ -1032,22 +1122,30 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   const int64_t nv = hp.j1 - hp.j0;
   const int64_t ldw = round_up(nv, 8);
   const int TJ = bf16 ? Cfg<true>::kTJ : Cfg<false>::kTJ;
-  // hi / lo planes of V[j0:j1]: tf32 (fp32 storage) or bf16 v1 = bf16(v), v2 = bf16(v - v1)
+  // hi / lo planes of V[j0:j1]: tf32 (fp32 storage) or column-scaled fp16 (split_v_f16_kernel)
   const size_t esz = bf16 ? 2 : 4;
   // caller-maintained planes (16-byte aligned rows for TMA) or this launch's split
   const bool pre = !bf16 && hp.vplanes && hp.j0 % 4 == 0 && hp.vplanes_ld % 4 == 0 && hp.vplanes_ld >= hp.j1;
   // (the split workspace is sized even when unused: a later launch in a CUDA
   // graph capture, e.g. CG's refresh H.V of X, must not allocate)
-  char* wsv = static_cast<char*>(ws_v.ensure(esz * ldw * s * 2));
+  const size_t plane_bytes = round_up(esz * ldw * s * 2, 256);
+  char* wsv = static_cast<char*>(ws_v.ensure(plane_bytes + 8 * 128));
+  unsigned* cmax = reinterpret_cast<unsigned*>(wsv + plane_bytes);  // [128] (H16)
+  float* vscale = reinterpret_cast<float*>(cmax + 128);             // [128] (H16)
   char* vhi = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0)) : wsv;
   char* vlo = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0 + hp.vplanes_ld * s))
                   : vhi + esz * ldw * s;
   const int64_t ldp = pre ? hp.vplanes_ld : ldw;  // plane leading dimension
   const dim3 vgrid(static_cast<unsigned>(ceil_div(nv, 256)), s);
   if (pre) {
-  } else if (bf16)
-    split_v_bf16_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<__nv_bfloat16*>(vhi),
-                                               reinterpret_cast<__nv_bfloat16*>(vlo), ldw);
+  } else if (bf16) {
+    WGP_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned) * s, st));
+    const unsigned mb = static_cast<unsigned>(std::min<int64_t>(ceil_div(nv, 256 * 8), std::max(1, 2 * sm_count() / s)));
+    colmax_kernel<<<dim3(mb, s), 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, cmax);
+    WGP_LAUNCH_CHECK();
+    split_v_f16_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, cmax, reinterpret_cast<__half*>(vhi),
+                                              reinterpret_cast<__half*>(vlo), ldw, vscale);
+  }
   else
     split_v_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<float*>(vhi),
                                           reinterpret_cast<float*>(vlo), ldw);
@@ -1073,7 +1171,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, 64);  // MMA-1 N = 64 points
   const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, 64);
   // one TJ-point x s_pad box per plane (128-byte rows: 32 tf32 / 64 bf16 points)
-  const CUtensorMapDataType vt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUtensorMapDataType vt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const CUtensorMap mVhi = make_map(vhi, nv, s, ldp * esz, TJ, spad, vt);
   const CUtensorMap mVlo = make_map(vlo, nv, s, ldp * esz, TJ, spad, vt);
 
@@ -1120,6 +1218,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   a.a = hp.a;
   a.diag = hp.diag;
   a.hyp = hp.hyp;
+  a.vscale = vscale;
   a.m_pad = m_pad;
   a.done = hp.done;
   static const int dbg = [] {

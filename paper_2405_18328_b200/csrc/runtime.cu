@@ -423,9 +423,9 @@ struct Ctx {
     // shards of the full operator decompose like the whole (bitwise-equal
     // rows); internal row blocks (AP) split for their own size instead
     p.split_rows = (row_idx || !shard_invariant || !split_global) ? 0 : n;
-    if ((hv_impl == WGP_HV_TC || hv_impl == WGP_HV_TC_BF16) && hv_tc_supported(d, s)) {
+    if ((hv_impl == WGP_HV_TC || hv_impl == WGP_HV_TC_F16) && hv_tc_supported(d, s)) {
       if (!tc.valid) tc.build(xs.as<float>(), n, dp, d, st);
-      hv_tc(tc, p, st, hv_impl == WGP_HV_TC_BF16);
+      hv_tc(tc, p, st, hv_impl == WGP_HV_TC_F16);
     } else {
       hv_simt(p, st);
     }
@@ -1416,7 +1416,7 @@ struct Ctx {
   }
   void grad_rows(int transform, const double* raw, const float* vy, const float* L, const float* R,
                  int s, double coef_b, double* out_a, double* out_b, int64_t gr0, int64_t gm) {
-    // tensor-core engines (TC, TC_BF16) use the tcgen05 gradient where it
+    // tensor-core engines (TC, TC_F16) use the tcgen05 gradient where it
     // applies; WGP_GRAD_IMPL=simt forces the CUDA-core kernel
     static const bool force_simt = [] {
       const char* e = getenv("WGP_GRAD_IMPL");
@@ -2050,7 +2050,7 @@ int wgp_destroy(wgp_ctx* ctx) {
 
 int wgp_set_hv_impl(wgp_ctx* ctx, int impl) {
   return guarded([&] {
-    if (impl != WGP_HV_TC && impl != WGP_HV_SIMT && impl != WGP_HV_TC_BF16)
+    if (impl != WGP_HV_TC && impl != WGP_HV_SIMT && impl != WGP_HV_TC_F16)
       throw std::invalid_argument("unknown H.V implementation");
     ctx->c.hv_impl = impl;
   });

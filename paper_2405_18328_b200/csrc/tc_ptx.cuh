@@ -153,8 +153,8 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-// bf16 x 3 MMA-2 (kind::f16, K = 16 per instruction): D (+)= k1 v1 + k1 v2 + k2 v1.
-__device__ __forceinline__ void mma3_ts_bf16(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+// 16-bit x 3 MMA-2 (kind::f16, K = 16 per instruction): D (+)= k1 v1 + k1 v2 + k2 v1.
+__device__ __forceinline__ void mma3_ts_f16(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
                                              uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p, t, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %6, 0;\n"
@@ -164,10 +164,9 @@ __device__ __forceinline__ void mma3_ts_bf16(uint32_t d, uint32_t ah, uint32_t a
       " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n}\n" ::"r"(d),
       "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
 }
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(M >> 4) << 24);
+// kind::f16 instruction descriptor: D f32, A/B fp16 (a/b format 0), both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {

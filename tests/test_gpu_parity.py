@@ -37,7 +37,7 @@ def make(n, d, s, seed, scale=1.0):
     return X, V, ls
 
 
-@pytest.mark.parametrize("impl", ["tc", "simt"])
+@pytest.mark.parametrize("impl", ["tc", "tc_f16", "simt"])
 @pytest.mark.parametrize("n,d,s", [(1, 2, 1), (2, 1, 3), (129, 3, 16), (300, 3, 5), (1000, 9, 17),
                                    (2048, 8, 17), (777, 26, 65), (513, 11, 128), (400, 5, 18), (901, 4, 34),
                                    (650, 7, 66), (333, 6, 97), (70, 3, 33)])
@@ -51,7 +51,7 @@ def test_hv_matches_oracle(ctx, impl, n, d, s):
     assert rel(out, ref) <= HV_TOL
 
 
-@pytest.mark.parametrize("impl", ["tc", "simt"])
+@pytest.mark.parametrize("impl", ["tc", "tc_f16", "simt"])
 def test_hv_config1_full_size_row_samples(ctx, impl):
     """BASELINE config 1 at full size (n=13,500, d=26, s=65), checked on row
     samples against the oracle, plus a size-independent linearity check."""
@@ -68,7 +68,8 @@ def test_hv_config1_full_size_row_samples(ctx, impl):
     assert rel(out2, 2 * out[:, :5].astype(np.float64) - out[:, 5:10]) <= 1e-5
 
 
-@pytest.mark.parametrize("cfg,impl,s", [("c3", "tc", 65), ("c3", "simt", 65), ("c3", "f64", 65), ("c4", "tc", 65)])
+@pytest.mark.parametrize("cfg,impl,s", [("c3", "tc", 65), ("c3", "tc_f16", 65), ("c3", "simt", 65), ("c3", "f64", 65),
+                                         ("c4", "tc", 65), ("c4", "tc_f16", 65)])
 def test_hv_full_size_dense_accumulation(ctx, cfg, impl, s):
     """Full-size BASELINE configs 3 (n=391,386, d=3, unit lengthscales on the
     unit cube: every entry of K is large) and 4 (n=1,844,352): the fp32
@@ -87,7 +88,7 @@ def test_hv_full_size_dense_accumulation(ctx, cfg, impl, s):
         assert rel(out[r0:r1], ref) <= HV_TOL, (r0, rel(out[r0:r1], ref))
 
 
-@pytest.mark.parametrize("impl", ["tc", "simt"])
+@pytest.mark.parametrize("impl", ["tc", "tc_f16", "simt"])
 @pytest.mark.parametrize("d", [30, 31, 32])
 def test_hv_maximum_dimension(ctx, impl, d):
     """d = 30 is the largest the tcgen05 kernel takes (augmented K = d + 2 <= 32);
@@ -101,7 +102,7 @@ def test_hv_maximum_dimension(ctx, impl, d):
     assert rel(out, orc.hv(X, ls, 1.3, 0.4, V)) <= HV_TOL
 
 
-@pytest.mark.parametrize("impl", ["tc", "simt"])
+@pytest.mark.parametrize("impl", ["tc", "tc_f16", "simt"])
 def test_hv_duplicate_points(ctx, impl):
     """Collisions: duplicated inputs (u = 0 off the diagonal, the Gram's
     cancellation at its worst) and a constant column."""
@@ -119,6 +120,31 @@ def test_hv_duplicate_points(ctx, impl):
     assert rel(out, orc.hv(X, ls, 1.2, 0.3, V)) <= HV_TOL
 
 
+@pytest.mark.parametrize("scale", [1e-30, 1e-8, 1e8, 1e30])
+def test_hv_f16_column_scales(ctx, scale):
+    """tc_f16 stores V in fp16 planes scaled per column by a power of two from
+    the column's max |v|: columns of any magnitude, a zero column, a single
+    nonzero and a ramp spanning 23 decades keep the 1e-5 bar per column."""
+    X, V, ls = make(1500, 7, 20, seed=11)
+    V = V.astype(np.float64)
+    V[:, 0] *= scale
+    V[:, 1] = 0.0
+    V[:, 2] = 0.0
+    V[5, 2] = 3.0 * scale
+    V[:, 3] = np.linspace(-1e-20, 1e3, 1500) * scale
+    V = V.astype(np.float32)
+    ctx.set_hv_impl("tc_f16")
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, 1.1, 0.3])
+    out = ctx.hv(V)
+    ctx.set_hv_impl("tc")
+    ref = orc.hv(X, ls, 1.1, 0.3, V)
+    assert not np.any(out[:, 1])
+    for c in range(V.shape[1]):
+        if c != 1:
+            assert rel(out[:, c], ref[:, c]) <= HV_TOL, (c, rel(out[:, c], ref[:, c]))
+
+
 def test_hv_impls_agree_and_deterministic(ctx):
     X, V, ls = make(3000, 6, 33, seed=3)
     ctx.set_data(X)
@@ -130,6 +156,10 @@ def test_hv_impls_agree_and_deterministic(ctx):
     ctx.set_hv_impl("simt")
     c = ctx.hv(V)
     assert rel(a, c.astype(np.float64)) <= HV_TOL
+    ctx.set_hv_impl("tc_f16")
+    e = ctx.hv(V)
+    assert np.array_equal(e, ctx.hv(V))
+    assert rel(e, c.astype(np.float64)) <= HV_TOL
     ctx.set_hv_impl("tc")
 
 
