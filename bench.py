@@ -52,7 +52,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--hv-impl", default="tc", choices=["tc", "tc_f16", "simt"])
+    # tc_f16 (default): 3xTF32 Gram + fp16x3 K.V over column-scaled V, 2.0e-7
+    # relative at config 1 (tc, 3xTF32 K.V: 3.5e-7; scripts/diag_f16.py)
+    ap.add_argument("--hv-impl", default="tc_f16", choices=["tc", "tc_f16", "simt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-outer", action="store_true", help="skip the per-outer-step timings")
@@ -617,22 +619,28 @@ def main():
     f_entry = 2 * d + 2 * s + 8                       # SURVEY §8d F_hv
     flops = f_entry * n * n
     # T_roof = max(sum over pipes of FLOPs_pipe / P_pipe,
-    # 2 n^2 / P_MUFU) on ALGORITHMIC work: the 2d (Gram) + 2s (K.V) flops on
-    # the tensor pipe at P_TF32 / 3 (3xTF32), the 8 Matern flops on the FMA
-    # pipe (P_FFMA = 128 FMA/clk/SM, scripts/ubench/ubench_ffma2.cu), 2 MUFU ops.
+    # 2 n^2 / P_MUFU) on ALGORITHMIC work: the 2d Gram flops on the tensor pipe
+    # at P_TF32 / 3 (3xTF32), the 2s K.V flops at P_TF32 / 3 (tc: 3xTF32) or
+    # P_F16 / 3 (tc_f16: fp16x3, the kind::f16 rate = the bf16 rate), the 8
+    # Matern flops on the FMA pipe (P_FFMA = 128 FMA/clk/SM,
+    # scripts/ubench/ubench_ffma2.cu), 2 MUFU ops.  `frac` is against the
+    # arithmetic the engine performs; `frac_if_3xtf32` applies the all-3xTF32
+    # tensor term (round 1's basis) to the same kernel time.
     p_bf16 = pk["bf16"] * 1e12
     p_tf32 = p_bf16 / 2                                # TF32 = half the bf16 rate
     p_ffma = 2 * 128 * 148 * pk["mhz"] * 1e6
     p_mufu = 16 * 148 * pk["mhz"] * 1e6                # ex2 / sqrt per s (16/clk/SM)
+    t_3xtf32 = (2 * d + 2 * s) / (p_tf32 / 3) + 8 / p_ffma
     if args.hv_impl in ("tc", "tc_f16"):
-        p_tc = p_tf32 / 3 if args.hv_impl == "tc" else p_bf16 / 3
-        t_pipes = (2 * d + 2 * s) / p_tc + 8 / p_ffma
-        basis = (f"sum-of-pipes: {2 * d + 2 * s} tensor flop/entry at {'P_TF32' if args.hv_impl == 'tc' else 'P_BF16'}/3 "
-                 f"+ 8 FMA-pipe flop/entry at P_FFMA; MUFU 2 ops/entry at 16/clk/SM")
+        p_kv = p_tf32 if args.hv_impl == "tc" else p_bf16
+        t_pipes = 2 * d / (p_tf32 / 3) + 2 * s / (p_kv / 3) + 8 / p_ffma
+        basis = (f"sum-of-pipes: {2 * d} Gram flop/entry at P_TF32/3 + {2 * s} K.V flop/entry at "
+                 f"{'P_TF32' if args.hv_impl == 'tc' else 'P_F16'}/3 + 8 FMA-pipe flop/entry at P_FFMA; "
+                 f"MUFU 2 ops/entry at 16/clk/SM")
         # the padded work the kernel actually issues (Gram K = 32, K.V N = s
         # padded to 16), for reference: not the roofline
         spad = 16 * -(-s // 16)
-        t_issued = 3 * 2 * 32 / p_tf32 + 3 * 2 * spad / (p_tf32 if args.hv_impl == "tc" else p_bf16)
+        t_issued = 3 * 2 * 32 / p_tf32 + 3 * 2 * spad / p_kv
     else:
         t_pipes = f_entry / p_ffma
         basis = "FFMA 256 flop/clk/SM"
@@ -666,7 +674,8 @@ def main():
                      "frac": achieved / peak, "traffic": traffic, "traffic_profile": traffic_profile,
                      "peak_basis": f"{pk['src']} peaks: F_hv={f_entry} flop/entry; " + basis,
                      "kernel_ms": kernel_ms, "t_roof_ms": t_entry * n * n / ws * 1e3,
-                     "frac_of_issued_work": (t_issued * n * n / ws * 1e3) / kernel_ms},
+                     "frac_of_issued_work": (t_issued * n * n / ws * 1e3) / kernel_ms,
+                     "frac_if_3xtf32": (max(t_3xtf32, 2 / p_mufu) * n * n / ws * 1e3) / kernel_ms},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }

@@ -144,6 +144,11 @@ struct TcArgs {
   long long* trace;  // WGP_TC_TRACE: per-tile clock64 stamps of CTA 0 ([T][16])
   long long* ctatime;  // WGP_TC_TRACE: per CTA {smid, globaltimer at start, after the tile loop, at exit}
   int nk1;  // packed Gram K steps (TcOperands::nk1), 0: 12 hi / lo MMAs
+  // persistent fp16 engine (hv_f16p_kernel): stream-K over (item, J tile) units
+  int row_tiles;   // R: row tiles of this launch
+  int64_t units;   // R * num_jt
+  int kp;          // partial slots per item (pieces an item can be cut into)
+  int ctas;        // G: CTAs of the persistent launch
   int dbg;  // ablation bits (WGP_TC_DEBUG): 1 no epilogue math, 2 no MMA-2, 4 no MMA-1, 8 no V loads,
             // 16 no epilogue TMEM traffic, 32 no B loads, 128 (H16) FMA-pipe ex2 for odd entries
 };
@@ -229,8 +234,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int TJ = K::kTJ;
   constexpr int P = K::kP;
   if (p.done && *p.done) return;
+  // Instrumentation (WGP_TC_TRACE stamps, per-CTA timers, WGP_TC_DEBUG
+  // ablations) only in -DWGP_TC_ABLATE builds: the checks cost the
+  // latency-critical control warps a few percent.
+#ifdef WGP_TC_ABLATE
+  long long* const trace = p.trace;
+  long long* const ctatime = p.ctatime;
+  const int dbg = p.dbg;
+#else
+  long long* const trace = nullptr;
+  long long* const ctatime = nullptr;
+  constexpr int dbg = 0;
+#endif
   long long gt0 = 0;
-  if (p.ctatime && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+  if (ctatime && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // m1done[t % 8]: MMA-1(t) complete (S_t ready; B slot of t free);
   // m2done[t % 8]: MMA-2(t) complete (K buffer and V slot of t free).  One
@@ -314,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int gr = 0; gr < G; ++gr, st = (st + 1 == NB) ? 0 : st + 1) {
         if (gr >= NB) mbar_wait(&bar_m1done[(gr - NB) & (kDoneRing - 1)], ((gr - NB) >> 3) & 1);
         uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
-        if (p.dbg & 32) {
+        if (dbg & 32) {
           mbar_arrive_warp(&bar_bfull[st]);
           continue;
         }
@@ -337,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const int vp = (jt_begin + t) * TJ;
         uint64_t* vbar = H16 ? &bar_vfull[st] : &bar_kfull[st];  // tf32: st == t % NBUF
-        if (p.dbg & 8) {
+        if (dbg & 8) {
           mbar_arrive_warp(vbar);
           continue;
         }
@@ -369,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t bph = 0;
       for (int gr = 0; gr < G; ++gr) {
         const int t = gr * P;  // first tile of the group (trace index)
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 6] = clock64();
+        if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 6] = clock64();
         // the group's columns are free once MMA-2 read the last tile of group gr - kGroups
         if (gr >= K::kGroups) {
           const int u = (gr - K::kGroups) * P + P - 1;
@@ -377,11 +394,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(&bar_bfull[st], bph);
         tc_after();
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 7] = clock64();
+        if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 7] = clock64();
         uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
         const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + K::kBStage / 2);
         const uint32_t d = tmem + K::grp_col(gi);
-        if (!(p.dbg & 4)) {
+        if (!(dbg & 4)) {
           if constexpr (!K::kATmem) {
             if (p.nk1)
               mma1_packed_tf32(d, dAhi, dAlo, dBhi, dBlo, id1, p.nk1);
@@ -396,13 +413,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         mma_commit(&bar_m1done[gr & (kDoneRing - 1)]);
-        if (gr == 0 && p.ctatime && lane == 0) {
+        if (gr == 0 && ctatime && lane == 0) {
           long long gt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-          p.ctatime[blockIdx.x * 12 + 11] = gt;  // first Gram group issued
+          ctatime[blockIdx.x * 12 + 11] = gt;  // first Gram group issued
         }
-        if (p.trace && blockIdx.x == 0 && lane == 0)
-          for (int h = 0; h < P; ++h) p.trace[(t + h) * 16 + 0] = clock64();
+        if (trace && blockIdx.x == 0 && lane == 0)
+          for (int h = 0; h < P; ++h) trace[(t + h) * 16 + 0] = clock64();
         if (++st == NB) st = 0, bph ^= 1u;
         if (++gi == K::kGroups) gi = 0;
       }
@@ -416,25 +433,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t kph = 0, vph = 0;
       for (int t = 0; t < T; ++t) {
         const uint32_t o = tmem + static_cast<uint32_t>(c & 1) * K::kOStride;
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 4] = clock64();
+        if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 4] = clock64();
         // chunk c reuses its accumulator once the epilogue drained chunk c - kOBufs
         if (tc == 0 && c >= K::kOBufs) {
           const int cp = c - K::kOBufs;
           mbar_wait(&bar_odrained[cp & 1], (cp >> 1) & 1);
         }
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 12] = clock64();
+        if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 12] = clock64();
         if (H16) mbar_wait(&bar_vfull[st], vph);
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 13] = clock64();
+        if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 13] = clock64();
         mbar_wait(&bar_kfull[b], kph);
         tc_after();
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 3] = clock64();
+        if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 3] = clock64();
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const uint32_t kb = tmem + K::tile_col(t);
         const uint64_t dv = umma_desc(base);
-        if (!(p.dbg & 2) && !H16) {
+        if (!(dbg & 2) && !H16) {
           static_assert(H16 || K::kLoOff == 64, "mma2_tile_tf32 assumes k_lo 64 columns after k_hi");
           mma2_tile_tf32(o, kb, dv, dv + box, id2, tc > 0 ? 1u : 0u);
-        } else if (!(p.dbg & 2)) {
+        } else if (!(dbg & 2)) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             if constexpr (H16) {
@@ -450,18 +467,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 5] = clock64();
-        if (t == 0 && p.ctatime && lane == 0) {
+        if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 5] = clock64();
+        if (t == 0 && ctatime && lane == 0) {
           long long gt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-          p.ctatime[blockIdx.x * 12 + 10] = gt;  // first MMA-2 issued
+          ctatime[blockIdx.x * 12 + 10] = gt;  // first MMA-2 issued
         }
         mma_commit(&bar_m2done[t & (kDoneRing - 1)]);
         if (tc == C - 1 || t == T - 1) mma_commit(&bar_ofull[c & 1]);
-        if (t == T - 1 && p.ctatime && lane == 0) {
+        if (t == T - 1 && ctatime && lane == 0) {
           long long gt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-          p.ctatime[blockIdx.x * 12 + 6] = gt;  // last MMA-2 issued
+          ctatime[blockIdx.x * 12 + 6] = gt;  // last MMA-2 issued
         }
         if (++st == NV) st = 0, vph ^= 1u;
         if (++b == NBUF) b = 0, kph ^= 1u;
@@ -481,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (valid) g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
     const float sf2 = p.hyp ? p.hyp[0] : p.sf2, ac = p.hyp ? p.hyp[1] : p.a;
     const float hdiag = p.hyp ? p.hyp[2] : p.diag;
-    const bool nomath = p.dbg & 1;
+    const bool nomath = dbg & 1;
     const int nch = (T + C - 1) / C;
     const bool diag = g >= p.j0 && g < p.j1;
     if (K::kATmem && w == 0 && T > 0) {
@@ -564,10 +581,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto finish = [&](int c) {
       mbar_wait(&bar_ofull[c & 1], (c >> 1) & 1);
       tc_after();
-      if (p.ctatime && threadIdx.x == 0) {
+      if (ctatime && threadIdx.x == 0) {
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.ctatime[blockIdx.x * 12 + 4] = gt;  // last ofull observed
+        ctatime[blockIdx.x * 12 + 4] = gt;  // last ofull observed
       }
       const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
       const bool fresh = c % FE == 0;
@@ -577,10 +594,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 0; k < kDrainK; ++k)
         if (cb + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + cb + 8 * k, o[k]);
       tmem_wait_ld();
-      if (p.ctatime && threadIdx.x == 0) {
+      if (ctatime && threadIdx.x == 0) {
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.ctatime[blockIdx.x * 12 + 7] = gt;  // last accumulator read
+        ctatime[blockIdx.x * 12 + 7] = gt;  // last accumulator read
       }
       // split partial as one TMA store of R (all 384 epilogue threads fold
       // their rows first; rows past m land in the padding rows of `part`)
@@ -608,10 +625,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             R[col * 128] = (H16 && tma_out) ? r * colsc(col) : r;
           }
         }
-      if (p.ctatime && threadIdx.x == 0) {
+      if (ctatime && threadIdx.x == 0) {
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.ctatime[blockIdx.x * 12 + 8] = gt;  // folded into R
+        ctatime[blockIdx.x * 12 + 8] = gt;  // folded into R
       }
       if (tma_out) {
         // 27 coalesced column stores per thread cost ~3 us per CTA, 4% of the
@@ -629,12 +646,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         return;
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
-      if (p.ctatime && threadIdx.x == 0) {
+      if (ctatime && threadIdx.x == 0) {
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.ctatime[blockIdx.x * 12 + 9] = gt;  // prefetch complete
+        ctatime[blockIdx.x * 12 + 9] = gt;  // prefetch complete
       }
-      const int cend = min(ce, p.dbg & 256 ? cb : p.s);  // dbg 256: no final stores (ablation)
+      const int cend = min(ce, dbg & 256 ? cb : p.s);  // dbg 256: no final stores (ablation)
       if (p.splits > 1) {
         float* part = p.part + static_cast<int64_t>(sp) * spad * p.m_pad + lr;
 #pragma unroll 1
@@ -682,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (single O: drained as soon as possible, MMA-2 waits for it)
     const int lag = K::kOBufs == 1 ? 0 : max(2, C / 2);
     int dc = 0;  // next chunk to drain
-    const bool turns = p.dbg & 512;
+    const bool turns = dbg & 512;
     uint32_t turn_ph = 0;
     for (int t = w; t < T; t += kEpiGroups) {
       while (dc < nch - 1 && t >= (dc + 1) * C + lag) drain(dc++);
@@ -694,9 +711,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < TJ);
       mbar_wait(&bar_m1done[gr & (kDoneRing - 1)], (gr >> 3) & 1);
       tc_after();
-      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 16 + 1] = clock64();
+      if (trace && blockIdx.x == 0 && q == 0 && lane == 0) trace[t * 16 + 1] = clock64();
       const int dgi = static_cast<int>(dg < 0 || dg >= TJ ? -1 : dg);
-      if (!(p.dbg & 16)) {
+      if (!(dbg & 16)) {
         if constexpr (H16) {
           // each 32-column half of S is read, converted and overwritten in
           // place by [k1 pairs (16 cols) | k2 pairs (16 cols)]; the second
@@ -719,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 32; ++i) wds[i] = r[i];
             } else if (diag_tile) {
               to_k_f16<false, true>(r, wds, dh);
-            } else if (p.dbg & 128) {
+            } else if (dbg & 128) {
               to_k_f16<true, false>(r, wds, dh);
             } else {
               to_k_f16<false, false>(r, wds, dh);
@@ -761,24 +778,511 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_kfull[b]);
-      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0) p.trace[t * 16 + 2] = clock64();
-      if (p.trace && blockIdx.x == 0 && lane == 0) p.trace[t * 16 + 8 + q] = clock64();
+      if (trace && blockIdx.x == 0 && q == 0 && lane == 0) trace[t * 16 + 2] = clock64();
+      if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 8 + q] = clock64();
     }
-    if (p.ctatime && threadIdx.x == 0) {
+    if (ctatime && threadIdx.x == 0) {
       long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      p.ctatime[blockIdx.x * 12 + 2] = gt;  // epilogue tile loop done (before the last drain)
+      ctatime[blockIdx.x * 12 + 2] = gt;  // epilogue tile loop done (before the last drain)
     }
     while (dc < nch - 1) drain(dc++);
     if (nch > 0) {
       finish(dc++);
-      if (p.ctatime && threadIdx.x == 0) {
+      if (ctatime && threadIdx.x == 0) {
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        p.ctatime[blockIdx.x * 12 + 5] = gt;  // final drain done
+        ctatime[blockIdx.x * 12 + 5] = gt;  // final drain done
       }
     }
   }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (ctatime && threadIdx.x == 0) {
+    uint32_t smid;
+    long long gt;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    ctatime[blockIdx.x * 12 + 0] = smid;
+    ctatime[blockIdx.x * 12 + 1] = gt0;
+    ctatime[blockIdx.x * 12 + 3] = gt;
+  }
+  if (warp == kWarpVProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ------------------------------------------------------------------ persistent fp16 engine
+// hv_f16p_kernel: the fp16x3 K.V pipeline of hv_tc_kernel<true> as ONE CTA per
+// SM that walks a contiguous range of work instead of a CTA per (row tile,
+// split).  The per-CTA fill (A_I load and copy, the first Gram and
+// conversion) and tail (last K.V, drain, fold, store) cost ~11 us per CTA at
+// config 1 against ~45 us of steady state, and 424 CTAs made 2.86 waves; here
+// the pipeline runs through item boundaries and the work is dealt evenly.
+//
+// Work: items i = sp * R + rt (split-major, as the grid order of
+// hv_tc_kernel: the CTAs running together share a J range that stays in L2),
+// item i owns the J tiles of split sp; the units (item, J tile) of all items,
+// concatenated in item order, are dealt to the G CTAs in contiguous ranges
+// [c U / G, (c + 1) U / G) (stream-K).  A CTA's range is a sequence of
+// pieces (a J-tile subrange of one item); each piece leaves its fp32 partial
+// in slot sp * kp + (c - the first CTA of the item), and tc_reduce_pieces sums
+// an item's pieces in CTA order: deterministic for a given launch shape.
+//
+// Item boundaries: the TMEM A_I of the next piece is copied by the epilogue
+// group that converts the current piece's last tile, right after that tile's
+// Gram completed (MMA-1 is done with the old A_I); MMA-1 resumes on the new
+// A_I while MMA-2 and the other groups work through the tiles in flight.  The
+// accumulator chunks alternate O0 / O1 across pieces, so MMA-2 does not wait
+// for a piece's final drain.
+__device__ __forceinline__ int split_begin(const TcArgs& p, int s) {
+  return p.num_jt * s / p.splits;  // 32-bit: num_jt * splits < 2^31 (host-checked)
+}
+// the CTA whose unit range holds unit x (ranges [c U / G, (c + 1) U / G))
+__device__ __forceinline__ int cta_of(const TcArgs& p, int64_t x) {
+  return static_cast<int>(((x + 1) * p.ctas - 1) / p.units);
+}
+// Walks this CTA's pieces.  The 64-bit divisions (a call on the GPU, whose
+// register save / restore spilled the epilogue) happen once, when the first
+// piece is located; later pieces start at item boundaries (slot k = 0).
+struct PieceWalk {
+  int64_t u, uend;
+  int sp, rt, a, b0, Ts, k0;
+  __device__ __forceinline__ explicit PieceWalk(const TcArgs& p) {
+    u = p.units * blockIdx.x / p.ctas;
+    uend = p.units * (blockIdx.x + 1) / p.ctas;
+    sp = 0;
+    while (sp + 1 < p.splits && static_cast<int64_t>(split_begin(p, sp + 1)) * p.row_tiles <= u) ++sp;
+    b0 = split_begin(p, sp);
+    Ts = split_begin(p, sp + 1) - b0;
+    const int64_t off = u - static_cast<int64_t>(b0) * p.row_tiles;
+    rt = Ts > 0 ? static_cast<int>(off / Ts) : 0;
+    a = static_cast<int>(off - static_cast<int64_t>(rt) * Ts);
+    const int64_t istart = static_cast<int64_t>(b0) * p.row_tiles + static_cast<int64_t>(rt) * Ts;
+    k0 = static_cast<int>(blockIdx.x) - (u < uend ? cta_of(p, istart) : static_cast<int>(blockIdx.x));
+  }
+  // next piece: row tile, first J tile, tile count, partial slot
+  __device__ __forceinline__ bool next(const TcArgs& p, int& rt_, int& jt0, int& T, int& slot) {
+    if (u >= uend) return false;
+    const int64_t left = uend - u;
+    T = Ts - a < left ? Ts - a : static_cast<int>(left);
+    rt_ = rt;
+    jt0 = b0 + a;
+    slot = sp * p.kp + k0;
+    k0 = 0;
+    u += T;
+    a += T;
+    if (a == Ts) {  // the next item: the next row tile, or the first of the next (non-empty) split
+      a = 0;
+      if (++rt == p.row_tiles) {
+        rt = 0;
+        do {
+          ++sp;
+          b0 = split_begin(p, sp);
+          Ts = split_begin(p, sp + 1) - b0;
+        } while (Ts == 0 && sp + 1 < p.splits);
+      }
+    }
+    return true;
+  }
+};
+
+// Pipeline of the persistent engine.  A unit is a 64-point J tile: one TMA
+// stage of B and of V, one N = 64 Gram group (12 kind::tf32 MMAs, MMA-1
+// warp), one conversion by one epilogue group, one K.V step (12 kind::f16
+// MMAs, MMA-2 warp); four units in flight in TMEM.  Two issuing warps, so
+// each one's barrier waits and commits (~100 clk apiece even when the phase
+// is complete: scripts/ubench/ubench_loop.cu) overlap the other's MMAs; one
+// warp issuing both streams left the tensor pipe idle during its
+// bookkeeping (0.195 vs 0.175 ms at config 1).
+struct F16P {
+  static constexpr int kUJ = 64;             // points per unit
+  static constexpr int kBufs = 4;            // TMEM S / K buffers of 64 columns
+  static constexpr uint32_t kOStride = 96, kAhi = 192, kAlo = 224, kGrp0 = 256;
+  static constexpr uint32_t kBStage = 2u * kUJ * 128u;  // B hi | lo (64 points x 32 fp32)
+  static __device__ __forceinline__ uint32_t buf_col(int g) {
+    return kGrp0 + 64u * static_cast<uint32_t>(g & (kBufs - 1));
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    hv_f16p_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
+                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
+                   const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
+                   const __grid_constant__ CUtensorMap mPart, const TcArgs p) {
+  using K = F16P;
+  constexpr int NBUF = K::kBufs;
+  constexpr int UJ = K::kUJ;
+  if (p.done && *p.done) return;
+  long long gt0 = 0;
+  if (p.ctatime && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+  // Instrumentation (builds with -DWGP_TC_ABLATE only: the stamps and
+  // ablation branches cost the latency-critical MMA warps ~5%):
+  // WGP_TC_TRACE per-unit clock64 stamps of CTA 0 (hv_tc_kernel's slots),
+  // WGP_TC_DEBUG ablation bits 2 / 4 / 8 / 16 / 32 as in hv_tc_kernel.
+#ifdef WGP_TC_ABLATE
+  const bool trc = p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0;
+  const int trmax = p.num_jt + 3;
+  const int dbg = p.dbg;
+#define WGP_TR(unit, slot_)                                                   \
+  do {                                                                        \
+    if (trc && (unit) < trmax) p.trace[(unit) * 16 + (slot_)] = clock64();     \
+  } while (0)
+#else
+  constexpr int dbg = 0;
+#define WGP_TR(unit, slot_) \
+  do {                      \
+  } while (0)
+#endif
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bar_bfull[kMaxStages], bar_vfull[kMaxStages], bar_m1done[kDoneRing],
+      bar_m2done[kDoneRing];
+  __shared__ __align__(8) uint64_t bar_a, bar_atm, bar_kfull[NBUF], bar_ofull[2], bar_odrained[2];
+  __shared__ uint32_t tmem_slot;
+  __shared__ float sColScale[kEpiWarps][8 * kDrainK];
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sAhi = smem;
+  uint8_t* sAlo = smem + 16384;
+  // R: [s_pad][128] fp32 running sum of the current piece (not aliased with A:
+  // the next piece's A_I lands while R is live)
+  float* sR = reinterpret_cast<float*>(smem + 32768);
+  uint8_t* sB = smem + p.a_region;
+  uint8_t* sV = sB + static_cast<size_t>(p.nb) * K::kBStage;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int C = p.chunk;  // units per accumulation chunk
+  const int NB = p.nb, NV = p.nv;
+  const int spad = p.s_pad;
+  const uint32_t vbox = static_cast<uint32_t>(spad) * 128u;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NB; ++i) mbar_init(&bar_bfull[i], 1);
+    for (int i = 0; i < NV; ++i) mbar_init(&bar_vfull[i], 1);
+    for (int i = 0; i < kDoneRing; ++i) {
+      mbar_init(&bar_m1done[i], 1);
+      mbar_init(&bar_m2done[i], 1);
+    }
+    mbar_init(&bar_a, 1);
+    mbar_init(&bar_atm, 4);
+    for (int i = 0; i < NBUF; ++i) mbar_init(&bar_kfull[i], 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_ofull[i], 1);
+      mbar_init(&bar_odrained[i], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kWarpVProd) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_slot;
+  int rt, ju0, U, slot;  // piece: row tile, first unit (global J unit), unit count, partial slot
+
+  if (warp == kWarpBProd) {
+    // ------------------------------------------------------------ TMA: A_I per piece, B ring (per unit)
+    PieceWalk pw(p);
+    int k = 0, gu = 0, st = 0;
+    while (pw.next(p, rt, ju0, U, slot)) {
+      if (k > 0) mbar_wait(&bar_atm, (k - 1) & 1);  // A of the previous piece is in TMEM: sA is free
+      mbar_expect_tx_warp(&bar_a, 2 * 16384);
+      tma_load_2d_warp(sAhi, &mAhi, &bar_a, 0, p.a_row0 + rt * kTI);
+      tma_load_2d_warp(sAlo, &mAlo, &bar_a, 0, p.a_row0 + rt * kTI);
+      for (int j = 0; j < U; ++j, ++gu, st = (st + 1 == NB) ? 0 : st + 1) {
+        if (gu >= NB) mbar_wait(&bar_m1done[(gu - NB) & (kDoneRing - 1)], ((gu - NB) >> 3) & 1);
+        uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
+        if (dbg & 32) {  // (ablation: no B loads)
+          mbar_arrive_warp(&bar_bfull[st]);
+          continue;
+        }
+        mbar_expect_tx_warp(&bar_bfull[st], K::kBStage);
+        const int pt = static_cast<int>(p.j0) + (ju0 + j) * UJ;
+        tma_load_2d_warp(base, &mBhi, &bar_bfull[st], 0, pt);
+        tma_load_2d_warp(base + K::kBStage / 2, &mBlo, &bar_bfull[st], 0, pt);
+      }
+      ++k;
+    }
+  } else if (warp == kWarpVProd) {
+    // ------------------------------------------------------------ TMA: V ring (per unit)
+    PieceWalk pw(p);
+    int gu = 0, st = 0;
+    while (pw.next(p, rt, ju0, U, slot)) {
+      for (int j = 0; j < U; ++j, ++gu, st = (st + 1 == NV) ? 0 : st + 1) {
+        if (gu >= NV) mbar_wait(&bar_m2done[(gu - NV) & (kDoneRing - 1)], ((gu - NV) >> 3) & 1);
+        uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
+        if (dbg & 8) {  // (ablation: no V loads)
+          mbar_arrive_warp(&bar_vfull[st]);
+          continue;
+        }
+        mbar_expect_tx_warp(&bar_vfull[st], p.vstage_bytes);
+        tma_load_2d_warp(base, &mVhi, &bar_vfull[st], (ju0 + j) * UJ, 0);
+        tma_load_2d_warp(base + vbox, &mVlo, &bar_vfull[st], (ju0 + j) * UJ, 0);
+      }
+    }
+  } else if (warp == kWarpM1) {
+    // ------------------------------------------------------------ MMA-1 (Gram, 3xTF32, A from TMEM), per unit
+    constexpr uint32_t id1 = idesc_tf32(kTI, UJ);
+    PieceWalk pw(p);
+    int k = 0, gu = 0, st = 0;
+    uint32_t bph = 0;
+    while (pw.next(p, rt, ju0, U, slot)) {
+      mbar_wait(&bar_atm, k & 1);  // this piece's A_I is in TMEM
+      for (int j = 0; j < U; ++j, ++gu) {
+        WGP_TR(gu, 6);
+        if (gu >= NBUF) {  // the buffer's previous unit has been multiplied
+          const int u = gu - NBUF;
+          mbar_wait(&bar_m2done[u & (kDoneRing - 1)], (u >> 3) & 1);
+        }
+        mbar_wait(&bar_bfull[st], bph);
+        tc_after();
+        WGP_TR(gu, 7);
+        uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
+        const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + K::kBStage / 2);
+        const uint32_t d = tmem + K::buf_col(gu);
+        if (dbg & 4) {  // (ablation: no Gram)
+        } else if (p.nk1) {
+          mma1_packed_tf32_ts(d, tmem + K::kAhi, dBhi, dBlo, id1, p.nk1);
+        } else {
+          mma1_group_tf32_ts(d, tmem + K::kAhi, tmem + K::kAlo, dBhi, dBlo, id1);
+        }
+        mma_commit(&bar_m1done[gu & (kDoneRing - 1)]);
+        WGP_TR(gu, 0);
+        if (++st == NB) st = 0, bph ^= 1u;
+      }
+      ++k;
+    }
+  } else if (warp == kWarpM2) {
+    // ------------------------------------------------------------ MMA-2 (K.V, fp16 x 3), per unit
+    const uint32_t id2 = idesc_f16(kTI, spad);
+    const uint64_t box = vbox >> 4;
+    PieceWalk pw(p);
+    int st = 0, cg = 0, gu = 0;
+    uint32_t vph = 0;
+    while (pw.next(p, rt, ju0, U, slot)) {
+      int tc = 0;
+      for (int j = 0; j < U; ++j, ++gu) {
+        const uint32_t o = tmem + static_cast<uint32_t>(cg & 1) * K::kOStride;
+        WGP_TR(gu, 4);
+        if (tc == 0 && cg >= 2) mbar_wait(&bar_odrained[cg & 1], ((cg - 2) >> 1) & 1);
+        WGP_TR(gu, 12);
+        mbar_wait(&bar_vfull[st], vph);
+        WGP_TR(gu, 13);
+        mbar_wait(&bar_kfull[gu & (NBUF - 1)], (gu / NBUF) & 1);
+        tc_after();
+        WGP_TR(gu, 3);
+        const uint64_t dv = umma_desc(sV + static_cast<size_t>(st) * p.vstage_bytes);
+        if (!(dbg & 2)) mma2_tile_f16(o, tmem + K::buf_col(gu), dv, dv + box, id2, tc > 0 ? 1u : 0u);
+        WGP_TR(gu, 5);
+        mma_commit(&bar_m2done[gu & (kDoneRing - 1)]);
+        if (tc == C - 1 || j == U - 1) {
+          mma_commit(&bar_ofull[cg & 1]);
+          ++cg;
+          tc = 0;
+        } else {
+          ++tc;
+        }
+        if (++st == NV) st = 0, vph ^= 1u;
+      }
+    }
+  } else if (warp < kEpiWarps) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3, w = warp >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+    const float sf2 = p.hyp ? p.hyp[0] : p.sf2;
+    const float osc = sf2 * (1.f / kKScale);
+    const int cpg = ((spad + kEpiGroups * 8 - 1) / (kEpiGroups * 8)) * 8;
+    const int cb = min(spad, w * cpg), ce = min(spad, (w + 1) * cpg);
+    const int FE = p.flush_every;
+    const int lag = max(2, C / 2);
+    float* Rr = sR + row;  // column c at Rr[c * 128]
+    for (int c = cb + lane; c < ce; c += 32)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&sColScale[warp][c - cb])),
+                   "l"(p.vscale + c)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    // A_I of piece k: swizzled TMA tile -> TMEM (this warp's 32 lanes)
+    auto copy_a = [&](int k) {
+      mbar_wait(&bar_a, k & 1);
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {  // hi, lo: one plane's 32 registers at a time
+        uint32_t a[32];
+        const uint8_t* rp = (h ? sAlo : sAhi) + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 v = *reinterpret_cast<const uint4*>(rp + (c ^ (row & 7)) * 16);
+          a[4 * c] = v.x, a[4 * c + 1] = v.y, a[4 * c + 2] = v.z, a[4 * c + 3] = v.w;
+        }
+        __syncwarp();
+        tmem_st32(tmem + lanes + (h ? K::kAlo : K::kAhi), a);
+      }
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_atm);
+    };
+    // chunk c (global: O buffer and barrier phases), lc its index in the piece;
+    // read in two passes of half the group's columns (register pressure)
+    constexpr int kH = (kDrainK + 1) / 2;
+    auto drain = [&](int c, int lc, bool valid, int slot_, int64_t lr) {
+      mbar_wait(&bar_ofull[c & 1], (c >> 1) & 1);
+      tc_after();
+      const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
+      const bool fresh = lc % FE == 0, flush = (lc + 1) % FE == 0;
+      double* F = p.flush + static_cast<int64_t>(slot_) * spad * p.m_pad + lr;
+#pragma unroll 1
+      for (int hp = 0; hp < 2; ++hp) {
+        uint32_t o[kH][8];
+        const int c0 = cb + 8 * kH * hp;
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kH; ++k)
+          if (c0 + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + c0 + 8 * k, o[k]);
+        tmem_wait_ld();
+        if (hp == 1) {
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_odrained[c & 1]);
+        }
+#pragma unroll
+        for (int k = 0; k < kH; ++k) {
+          if (c0 + 8 * k >= ce) break;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int col = c0 + 8 * k + i;
+            const float r = (fresh ? 0.f : Rr[col * 128]) + __uint_as_float(o[k][i]);
+            if (!flush) {
+              Rr[col * 128] = r;
+            } else if (valid && col < p.s) {
+              double* f = F + static_cast<int64_t>(col) * p.m_pad;
+              *f = (lc + 1 == FE ? 0.0 : *f) + static_cast<double>(r);
+            }
+          }
+        }
+      }
+    };
+    // the piece's last chunk: its partial (scaled to H.V units) into the slot
+    auto finish = [&](int c, int lc, bool valid, int rt_, int slot_, int64_t lr) {
+      double* F = p.flush + static_cast<int64_t>(slot_) * spad * p.m_pad + lr;
+      mbar_wait(&bar_ofull[c & 1], (c >> 1) & 1);
+      tc_after();
+      const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
+      const bool fresh = lc % FE == 0;
+      const bool tma_out = lc < FE;  // no fp64 flush in this piece: R + O is its whole sum
+      float* part = p.part + static_cast<int64_t>(slot_) * spad * p.m_pad + lr;
+#pragma unroll 1
+      for (int hp = 0; hp < 2; ++hp) {
+        uint32_t o[kH][8];
+        const int c0 = cb + 8 * kH * hp;
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kH; ++k)
+          if (c0 + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + c0 + 8 * k, o[k]);
+        tmem_wait_ld();
+        if (hp == 1) {
+          tc_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_odrained[c & 1]);
+        }
+#pragma unroll
+        for (int k = 0; k < kH; ++k)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int col = c0 + 8 * k + i;
+            if (col >= ce) continue;
+            const float r = (fresh ? 0.f : Rr[col * 128]) + __uint_as_float(o[k][i]);
+            const float sc = osc * sColScale[warp][col - cb];
+            if (tma_out) {
+              Rr[col * 128] = r * sc;
+            } else if (valid && col < p.s) {
+              const double f = __ldcg(F + static_cast<int64_t>(col) * p.m_pad);
+              part[static_cast<int64_t>(col) * p.m_pad] = static_cast<float>(f + static_cast<double>(r)) * sc;
+            }
+          }
+      }
+      if (tma_out) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (warp == 0 && lane == 0) {
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&mPart),
+                       "r"(rt_ * kTI), "r"(slot_ * spad), "r"(smem_u32(sR))
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // R is free again
+      }
+    };
+
+    PieceWalk pw(p);
+    bool have = pw.next(p, rt, ju0, U, slot);
+    if (have && w == 0) copy_a(0);
+    int k = 0, gb = 0, c0 = 0;  // piece ordinal, its first global unit, its first global chunk
+    while (have) {
+      const bool has_next = pw.u < pw.uend;
+      const int64_t lr = static_cast<int64_t>(rt) * kTI + row;
+      const bool valid = lr < p.m;
+      const int64_t g = valid ? (p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr) : -1;
+      const int nch = (U + C - 1) / C;
+      const int64_t pstart = p.j0 + static_cast<int64_t>(ju0) * UJ;  // the piece's first point
+      int dc = 0;
+      for (int gu = gb + ((w - gb % kEpiGroups) + kEpiGroups) % kEpiGroups; gu < gb + U; gu += kEpiGroups) {
+        const int t = gu - gb;
+        while (dc < nch - 1 && t >= (dc + 1) * C + lag) {
+          drain(c0 + dc, dc, valid, slot, lr);
+          ++dc;
+        }
+        const uint32_t bcol = K::buf_col(gu);
+        const int64_t dg = valid ? g - (pstart + static_cast<int64_t>(t) * UJ) : -1;
+        const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < UJ);
+        const int dgi = static_cast<int>(dg < 0 || dg >= UJ ? -1 : dg);
+        mbar_wait(&bar_m1done[gu & (kDoneRing - 1)], (gu >> 3) & 1);
+        tc_after();
+        if (q == 0) WGP_TR(gu, 1);
+        if (has_next && t == U - 1) copy_a(k + 1);  // this piece's Grams are all done
+        if (!(dbg & 16)) {  // (ablation: 16 no epilogue TMEM traffic)
+          // each 32-column half of S is read, converted and overwritten in
+          // place by [k1 pairs (16 cols) | k2 pairs (16 cols)]
+          uint32_t r[32], wds[32];
+          __syncwarp();
+          tmem_ld32(tmem + lanes + bcol, r);
+          tmem_wait_ld();
+#pragma unroll 1
+          for (int half = 0; half < 2; ++half) {
+            const int dh = dgi - 32 * half;
+            if (diag_tile)
+              to_k_f16<false, true>(r, wds, dh);
+            else
+              to_k_f16<false, false>(r, wds, dh);
+            __syncwarp();
+            if (half == 0) tmem_ld32(tmem + lanes + bcol + 32, r);
+            tmem_st32(tmem + lanes + bcol + 32 * half, wds);
+            if (half == 0) tmem_wait_ld();
+          }
+          tmem_wait_st();
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_kfull[gu & (NBUF - 1)]);
+        if (q == 0) WGP_TR(gu, 2);
+        WGP_TR(gu, 8 + q);
+      }
+      while (dc < nch - 1) {
+        drain(c0 + dc, dc, valid, slot, lr);
+        ++dc;
+      }
+      finish(c0 + dc, dc, valid, rt, slot, lr);
+      gb += U;
+      c0 += nch;
+      ++k;
+      have = pw.next(p, rt, ju0, U, slot);
+    }
+  }
+#undef WGP_TR
   tc_before();
   __syncthreads();
   tc_after();
@@ -792,6 +1296,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     p.ctatime[blockIdx.x * 12 + 3] = gt;
   }
   if (warp == kWarpVProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// Sum of an item's piece partials (fp64, CTA order) + the row epilogue of tc_reduce_kernel.
+__global__ void tc_reduce_pieces_kernel(const TcArgs p) {
+  if (p.done && *p.done) return;
+  const int64_t lr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (lr >= p.m) return;
+  const int rt = static_cast<int>(lr / kTI);
+  double acc = 0.0;
+  for (int sp = 0; sp < p.splits; ++sp) {
+    const int b0 = split_begin(p, sp), Ts = split_begin(p, sp + 1) - b0;
+    if (Ts <= 0) continue;
+    const int64_t istart = static_cast<int64_t>(b0) * p.row_tiles + static_cast<int64_t>(rt) * Ts;
+    const int n = cta_of(p, istart + Ts - 1) - cta_of(p, istart) + 1;
+    for (int k = 0; k < n; ++k)
+      acc += static_cast<double>(p.part[(static_cast<int64_t>(sp * p.kp + k) * p.s_pad + c) * p.m_pad + lr]);
+  }
+  float v = static_cast<float>(acc);
+  const int64_t g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
+  if (g >= p.j0 && g < p.j1) v = fmaf(p.hyp ? p.hyp[2] : p.diag, p.V[g + c * p.ldv], v);
+  float* dst = p.out + lr + c * p.ldo;
+  if (p.mode == kHvStore)
+    *dst = v;
+  else if (p.mode == kHvResidual)
+    *dst = p.B[g + c * p.ldb] - v;
+  else
+    *dst -= v;
 }
 
 // Sum of the split partials (in fp64, fixed order) + the kernel's row epilogue.
@@ -827,27 +1359,6 @@ __global__ void split_v_kernel(const float* V, int64_t ldv, int64_t j0, int64_t 
   lo[c * ldw + j] = v - vh;
 }
 
-// Column max |V[j0:j1, c]| as float bits (monotone for |v|) -> cmax[c]
-// (zeroed by the caller); NaN sorts above every finite value.
-__global__ void colmax_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, unsigned* cmax) {
-  const int c = blockIdx.y;
-  unsigned m = 0u;
-  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < nv;
-       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    m = max(m, __float_as_uint(V[j0 + j + c * ldv]) & 0x7FFFFFFFu);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ unsigned sm[32];
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    m = threadIdx.x < blockDim.x / 32 ? sm[threadIdx.x] : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0 && m) atomicMax(cmax + c, m);
-  }
-}
-
 // Power of two 2^e_c putting the column max into [2^14, 2^15): the fp16 planes
 // of the scaled column are then normal down to 2^-28 of its max (hi) and the
 // lo residual down to 2^-17 of it; below, their absolute error is < 2^-39 of
@@ -860,19 +1371,42 @@ __device__ __forceinline__ float col_scale(unsigned mbits) {
   return __int_as_float((127 + e) << 23);
 }
 
-// V[j0:j1, :s] -> fp16 planes v1 = f16(2^e_c v), v2 = f16(2^e_c v - v1) [s][ldw];
-// vscale[c] = 2^-e_c (exact: |e_c| <= 100).
-__global__ void split_v_f16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, const unsigned* cmax,
-                                   __half* v1, __half* v2, int64_t ldw, float* vscale) {
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int c = blockIdx.y;
-  const float sc = col_scale(cmax[c]);
-  if (j == 0) vscale[c] = 1.f / sc;
-  if (j >= nv) return;
-  const float v = V[j0 + j + c * ldv] * sc;
-  const __half h = __float2half_rn(v);
-  v1[c * ldw + j] = h;
-  v2[c * ldw + j] = __float2half_rn(v - __half2float(h));
+// V[j0:j1, :s] -> fp16 planes v1 = f16(2^e_c v), v2 = f16(2^e_c v - v1)
+// [s][ldw] and vscale[c] = 2^-e_c (exact: |e_c| <= 100).  One CTA per column:
+// the column's max |v| (block reduction, float bits are monotone in |v|,
+// NaN sorts above every finite value), then its planes -- one launch instead
+// of memset + column max + split (~12 us at config 1 under ncu).
+__global__ void __launch_bounds__(1024) split_v_f16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv,
+                                                           __half* v1, __half* v2, int64_t ldw, float* vscale) {
+  const int c = blockIdx.x;
+  const float* col = V + j0 + static_cast<int64_t>(c) * ldv;
+  unsigned m = 0u;
+  for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) m = max(m, __float_as_uint(col[j]) & 0x7FFFFFFFu);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ unsigned sm[32];
+  __shared__ float ssc;
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < blockDim.x / 32 ? sm[threadIdx.x] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) {
+      ssc = col_scale(m);
+      vscale[c] = 1.f / ssc;
+    }
+  }
+  __syncthreads();
+  const float sc = ssc;
+  __half* h1 = v1 + static_cast<int64_t>(c) * ldw;
+  __half* h2 = v2 + static_cast<int64_t>(c) * ldw;
+  for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) {
+    const float v = col[j] * sc;
+    const __half h = __float2half_rn(v);
+    h1[j] = h;
+    h2[j] = __float2half_rn(v - __half2float(h));
+  }
 }
 
 // Augmented operand rows from the prepared points (see TcOperands).
@@ -1097,228 +1631,17 @@ int tc_sm_count() { return sm_count(); }
 
 bool hv_tc_supported(int d, int s) { return d + 2 <= kKA && s >= 1 && s <= 128; }
 
-void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
-  if (hp.s > 96) {  // the V ring holds at most 96 columns: balanced column chunks
-    const int chunks = static_cast<int>(ceil_div(hp.s, 96));
-    for (int c = 0; c < chunks; ++c) {
-      const int c0 = hp.s * c / chunks, c1 = hp.s * (c + 1) / chunks;
-      HvParams q = hp;
-      q.s = c1 - c0;
-      q.V = hp.V + c0 * hp.ldv;
-      q.out = hp.out + c0 * hp.ldo;
-      if (hp.B) q.B = hp.B + c0 * hp.ldb;
-      q.vplanes = nullptr;
-      hv_tc(ops, q, st, bf16);
-    }
-    return;
-  }
-  if (!ops.ws) ops.ws = new TcWorkspaces();
-  Workspace& ws_v = ops.ws->v;
-  Workspace& ws_rows = ops.ws->rows;
-  Workspace& ws_part = ops.ws->part;
-  if (hp.m <= 0 || hp.j1 <= hp.j0) return;
-  const int s = hp.s;
-  const int spad = static_cast<int>(round_up(s, 16));
-  const int64_t nv = hp.j1 - hp.j0;
-  const int64_t ldw = round_up(nv, 8);
-  const int TJ = bf16 ? Cfg<true>::kTJ : Cfg<false>::kTJ;
-  // hi / lo planes of V[j0:j1]: tf32 (fp32 storage) or column-scaled fp16 (split_v_f16_kernel)
-  const size_t esz = bf16 ? 2 : 4;
-  // caller-maintained planes (16-byte aligned rows for TMA) or this launch's split
-  const bool pre = !bf16 && hp.vplanes && hp.j0 % 4 == 0 && hp.vplanes_ld % 4 == 0 && hp.vplanes_ld >= hp.j1;
-  // (the split workspace is sized even when unused: a later launch in a CUDA
-  // graph capture, e.g. CG's refresh H.V of X, must not allocate)
-  const size_t plane_bytes = round_up(esz * ldw * s * 2, 256);
-  char* wsv = static_cast<char*>(ws_v.ensure(plane_bytes + 8 * 128));
-  unsigned* cmax = reinterpret_cast<unsigned*>(wsv + plane_bytes);  // [128] (H16)
-  float* vscale = reinterpret_cast<float*>(cmax + 128);             // [128] (H16)
-  char* vhi = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0)) : wsv;
-  char* vlo = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0 + hp.vplanes_ld * s))
-                  : vhi + esz * ldw * s;
-  const int64_t ldp = pre ? hp.vplanes_ld : ldw;  // plane leading dimension
-  const dim3 vgrid(static_cast<unsigned>(ceil_div(nv, 256)), s);
-  if (pre) {
-  } else if (bf16) {
-    WGP_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned) * s, st));
-    const unsigned mb = static_cast<unsigned>(std::min<int64_t>(ceil_div(nv, 256 * 8), std::max(1, 2 * sm_count() / s)));
-    colmax_kernel<<<dim3(mb, s), 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, cmax);
-    WGP_LAUNCH_CHECK();
-    split_v_f16_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, cmax, reinterpret_cast<__half*>(vhi),
-                                              reinterpret_cast<__half*>(vlo), ldw, vscale);
-  }
-  else
-    split_v_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<float*>(vhi),
-                                          reinterpret_cast<float*>(vlo), ldw);
-  WGP_LAUNCH_CHECK();
-  // A rows: the operand planes directly (row range) or a gathered copy
-  const float* ahi = static_cast<const float*>(ops.a_hi);
-  const float* alo = static_cast<const float*>(ops.a_lo);
-  int64_t a_rows = ops.n_pad;
-  int a_row0 = static_cast<int>(hp.r0);
-  const int64_t m_pad = round_up(hp.m, 128);
-  if (hp.row_idx) {
-    float* g = static_cast<float*>(ws_rows.ensure(sizeof(float) * m_pad * kKA * 2));
-    gather_rows_kernel<<<static_cast<unsigned>(ceil_div(m_pad * kKA, 256)), 256, 0, st>>>(
-        ahi, alo, hp.row_idx, hp.m, g, g + m_pad * kKA, m_pad);
-    WGP_LAUNCH_CHECK();
-    ahi = g;
-    alo = g + m_pad * kKA;
-    a_rows = m_pad;
-    a_row0 = 0;
-  }
-  const CUtensorMap mAhi = make_map(ahi, kKA, a_rows, kKA * 4, kKA, kTI);
-  const CUtensorMap mAlo = make_map(alo, kKA, a_rows, kKA * 4, kKA, kTI);
-  const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, 64);  // MMA-1 N = 64 points
-  const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, 64);
-  // one TJ-point x s_pad box per plane (128-byte rows: 32 tf32 / 64 bf16 points)
-  const CUtensorMapDataType vt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  const CUtensorMap mVhi = make_map(vhi, nv, s, ldp * esz, TJ, spad, vt);
-  const CUtensorMap mVlo = make_map(vlo, nv, s, ldp * esz, TJ, spad, vt);
-
-  TcArgs a{};
-  a.m = hp.m;
-  a.a_row0 = a_row0;
-  a.j0 = hp.j0;
-  a.j1 = hp.j1;
-  a.num_jt = static_cast<int>(ceil_div(nv, TJ));
-  a.s = s;
-  a.s_pad = spad;
-  // Ring depths: V tiles are consumed by MMA-2 and must be prefetched far
-  // enough ahead to cover the L2->SMEM latency (measured: 3 stages starve
-  // MMA-2); the B ring only feeds MMA-1, which runs ahead anyway.
-  static const int env_nb = [] {
-    const char* e = getenv("WGP_TC_NB");
-    return e ? atoi(e) : 0;
-  }();
-  static const int env_nv = [] {
-    const char* e = getenv("WGP_TC_NV");
-    return e ? atoi(e) : 0;
-  }();
-  a.vstage_bytes = 2u * static_cast<uint32_t>(spad) * 128u;
-  // A_I (32 KB) + the running sum R (512 s_pad bytes; aliases A when A lives in TMEM)
-  const bool a_tmem = bf16 ? Cfg<true>::kATmem : Cfg<false>::kATmem;
-  a.a_region = a_tmem ? std::max(32768u, 512u * spad) : 32768u + 512u * spad;
-  const int bstage = 2 * 64 * 128;
-  a.nb = env_nb > 0 ? std::min(env_nb, kMaxStages) : 3;
-  a.nv = std::min<int>(kMaxStages, (kSmemLimit - static_cast<int>(a.a_region) - 512 * spad - 1024 - a.nb * bstage) /
-                                       static_cast<int>(a.vstage_bytes));
-  if (env_nv > 0) a.nv = std::min(a.nv, env_nv);
-  if (!bf16) a.nv = Cfg<false>::kTilesInFlight;  // V slots share the K slots' barriers
-  if (a.nv < 2 || a.nb < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
-  a.row_idx = hp.row_idx;
-  a.r0 = hp.r0;
-  a.V = hp.V;
-  a.ldv = hp.ldv;
-  a.out = hp.out;
-  a.ldo = hp.ldo;
-  a.B = hp.B;
-  a.ldb = hp.ldb;
-  a.mode = hp.mode;
-  a.sf2 = hp.sf2;
-  a.a = hp.a;
-  a.diag = hp.diag;
-  a.hyp = hp.hyp;
-  a.vscale = vscale;
-  a.m_pad = m_pad;
-  a.done = hp.done;
-  static const int dbg = [] {
-    const char* e = getenv("WGP_TC_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  a.dbg = dbg;
-  a.nk1 = ops.nk1;
-  static const bool tracing = getenv("WGP_TC_TRACE") != nullptr;
-  static Workspace ws_trace;
-  a.trace = nullptr;
-  if (tracing) {
-    a.trace = static_cast<long long*>(ws_trace.ensure(sizeof(long long) * 16 * (a.num_jt + 4)));
-    WGP_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(long long) * 16 * (a.num_jt + 4), st));
-  }
-  const int64_t row_tiles = ceil_div(hp.m, kTI);
-  const int64_t key_tiles = hp.split_rows > 0 ? ceil_div(hp.split_rows, kTI) : row_tiles;
-  // L2 rasterisation: every CTA streams the operand planes of its J range
-  // (B hi / lo + V hi / lo: 256 + 2 esz s_pad bytes per point).  With one
-  // split the concurrently running row tiles drift apart along J over the
-  // waves, and once the planes outgrow L2 they re-read them from HBM
-  // (config 3, n = 391k: 463 GB of DRAM reads per H.V at a 53% L2 hit rate,
-  // ncu).  Splits whose J range fits the budget, with the split-major grid,
-  // keep the range L2-resident across all row tiles; the fp32 partials are
-  // capped at WGP_TC_PART_GB (default 32 GB, keyed like the splits: a row
-  // shard allocates its share).
-  static const double l2_budget = [] {
-    const char* e = getenv("WGP_TC_L2MB");
-    return (e ? atof(e) : 48.0) * 1e6;
-  }();
-  int min_sp = 1;
-  if (l2_budget > 0) {
-    const double plane_bytes = static_cast<double>(nv) * (256.0 + 2.0 * static_cast<double>(esz) * spad);
-    min_sp = static_cast<int>(std::ceil(plane_bytes / l2_budget));
-    // the cap uses the split key's rows, so a row shard picks the full operator's splits
-    const double part_row = 4.0 * spad * static_cast<double>(key_tiles * kTI);
-    static const double part_cap = [] {
-      const char* e = getenv("WGP_TC_PART_GB");
-      return (e ? atof(e) : 32.0) * 1e9;
-    }();
-    min_sp = std::max(1, std::min({min_sp, static_cast<int>(part_cap / part_row), 64}));
-  }
-  a.splits = choose_splits(key_tiles, a.num_jt, sm_count(), min_sp);
-  static const int force_splits = [] {
-    const char* e = getenv("WGP_TC_SPLITS");
-    return e ? atoi(e) : 0;
-  }();
-  if (force_splits > 0) a.splits = std::min(force_splits, a.num_jt);
-  // fp32 accumulation chunk (tiles): bounds the accumulation error, see the kernel
-  static const int env_chunk = [] {
-    const char* e = getenv("WGP_TC_CHUNK");
-    return e ? atoi(e) : 0;
-  }();
-  a.chunk = env_chunk >= 4 ? env_chunk : 1024 / TJ;
-  static const int env_flush = [] {
-    const char* e = getenv("WGP_TC_FLUSH");
-    return e ? atoi(e) : 0;
-  }();
-  a.flush_every = env_flush >= 1 ? env_flush : 64;
-  const int max_tiles = static_cast<int>(ceil_div(a.num_jt, a.splits));
-  const bool flushes = max_tiles > a.flush_every * a.chunk;
-  const size_t part_bytes = a.splits > 1 ? sizeof(float) * a.splits * spad * m_pad : 0;
-  const size_t flush_bytes = flushes ? sizeof(double) * a.splits * spad * m_pad : 0;
-  char* pw = static_cast<char*>(ws_part.ensure(round_up(part_bytes, 256) + flush_bytes + 256));
-  a.part = reinterpret_cast<float*>(pw);
-  a.flush = reinterpret_cast<double*>(pw + round_up(part_bytes, 256));
-  // The split partial of a CTA, R = [s_pad][128] fp32 in shared memory, is one
-  // box of the partial buffer viewed as [splits * s_pad] columns x [m_pad] rows.
-  CUtensorMap mPart = mAhi;  // unused unless tma_part
-  a.tma_part = 0;
-  if (a.splits > 1) {
-    mPart = make_map(a.part, static_cast<uint64_t>(m_pad), static_cast<uint64_t>(a.splits) * spad, m_pad * 4, kTI,
-                     static_cast<uint32_t>(spad), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_NONE);
-    a.tma_part = 1;
-  }
-  const int smem = static_cast<int>(a.a_region) + 1024 + a.nb * bstage + a.nv * static_cast<int>(a.vstage_bytes) +
-                   512 * spad;  // + sVd
-  const unsigned grid = static_cast<unsigned>(row_tiles * a.splits);
-  static Workspace ws_cta;
-  a.ctatime = nullptr;
-  if (tracing) a.ctatime = static_cast<long long*>(ws_cta.ensure(sizeof(long long) * 12 * grid));
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  if (ops.profiling) {
-    WGP_CUDA(cudaEventCreate(&ev0));
-    WGP_CUDA(cudaEventCreate(&ev1));
-    WGP_CUDA(cudaEventRecord(ev0, st));
-  }
-  if (bf16)
-    launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st);
-  else
-    launch_tc<false>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st);
-  if (ops.profiling) {
-    WGP_CUDA(cudaEventRecord(ev1, st));
-    ops.events.emplace_back(ev0, ev1);
-  }
-  if (tracing) {
-    const int T0 = static_cast<int>(static_cast<int64_t>(a.num_jt) / a.splits);
+// WGP_TC_TRACE report: per-tile stamps of CTA 0 (T0 steady-state tiles) and per-CTA timers.
+void trace_report(const TcArgs& a, int T0, unsigned grid, cudaStream_t st) {
     std::vector<long long> h(16 * (a.num_jt + 4));
     WGP_CUDA(cudaMemcpyAsync(h.data(), a.trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
+    if (const char* dump = getenv("WGP_TC_TRACE_DUMP")) {  // raw stamps, 16 per tile, for offline analysis
+      if (FILE* f = fopen(dump, "wb")) {
+        fwrite(h.data(), sizeof(long long), h.size(), f);
+        fclose(f);
+      }
+    }
     // per tile: [0] MMA-1 committed, [1] epilogue woke (S ready), [2] epilogue
     // arrived kfull, [3] MMA-2 passed its waits, [4] MMA-2 loop top, [5] MMA-2
     // issued, [6] MMA-1 loop top, [7] MMA-1 passed its waits.  Means over the
@@ -1408,6 +1731,279 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
       fprintf(stderr, "[hv_tc trace] epilogue per lane quarter (SMSP): %.0f %.0f %.0f %.0f clk\n", v[10] / cnt,
               v[11] / cnt, v[12] / cnt, v[13] / cnt);
   }
+
+void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
+  if (hp.s > 96) {  // the V ring holds at most 96 columns: balanced column chunks
+    const int chunks = static_cast<int>(ceil_div(hp.s, 96));
+    for (int c = 0; c < chunks; ++c) {
+      const int c0 = hp.s * c / chunks, c1 = hp.s * (c + 1) / chunks;
+      HvParams q = hp;
+      q.s = c1 - c0;
+      q.V = hp.V + c0 * hp.ldv;
+      q.out = hp.out + c0 * hp.ldo;
+      if (hp.B) q.B = hp.B + c0 * hp.ldb;
+      q.vplanes = nullptr;
+      hv_tc(ops, q, st, bf16);
+    }
+    return;
+  }
+  if (!ops.ws) ops.ws = new TcWorkspaces();
+  Workspace& ws_v = ops.ws->v;
+  Workspace& ws_rows = ops.ws->rows;
+  Workspace& ws_part = ops.ws->part;
+  if (hp.m <= 0 || hp.j1 <= hp.j0) return;
+  const int s = hp.s;
+  const int spad = static_cast<int>(round_up(s, 16));
+  const int64_t nv = hp.j1 - hp.j0;
+  const int64_t ldw = round_up(nv, 8);
+  const int TJ = bf16 ? Cfg<true>::kTJ : Cfg<false>::kTJ;
+  // hi / lo planes of V[j0:j1]: tf32 (fp32 storage) or column-scaled fp16 (split_v_f16_kernel)
+  const size_t esz = bf16 ? 2 : 4;
+  // caller-maintained planes (16-byte aligned rows for TMA) or this launch's split
+  const bool pre = !bf16 && hp.vplanes && hp.j0 % 4 == 0 && hp.vplanes_ld % 4 == 0 && hp.vplanes_ld >= hp.j1;
+  // (the split workspace is sized even when unused: a later launch in a CUDA
+  // graph capture, e.g. CG's refresh H.V of X, must not allocate)
+  const size_t plane_bytes = round_up(esz * ldw * s * 2, 256);
+  char* wsv = static_cast<char*>(ws_v.ensure(plane_bytes + 8 * 128));
+  float* vscale = reinterpret_cast<float*>(wsv + plane_bytes);  // [128] 2^-e_c (H16)
+  char* vhi = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0)) : wsv;
+  char* vlo = pre ? reinterpret_cast<char*>(const_cast<float*>(hp.vplanes + hp.j0 + hp.vplanes_ld * s))
+                  : vhi + esz * ldw * s;
+  const int64_t ldp = pre ? hp.vplanes_ld : ldw;  // plane leading dimension
+  const dim3 vgrid(static_cast<unsigned>(ceil_div(nv, 256)), s);
+  if (pre) {
+  } else if (bf16) {
+    split_v_f16_kernel<<<s, 1024, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<__half*>(vhi),
+                                           reinterpret_cast<__half*>(vlo), ldw, vscale);
+  } else
+    split_v_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<float*>(vhi),
+                                          reinterpret_cast<float*>(vlo), ldw);
+  WGP_LAUNCH_CHECK();
+  // A rows: the operand planes directly (row range) or a gathered copy
+  const float* ahi = static_cast<const float*>(ops.a_hi);
+  const float* alo = static_cast<const float*>(ops.a_lo);
+  int64_t a_rows = ops.n_pad;
+  int a_row0 = static_cast<int>(hp.r0);
+  const int64_t m_pad = round_up(hp.m, 128);
+  if (hp.row_idx) {
+    float* g = static_cast<float*>(ws_rows.ensure(sizeof(float) * m_pad * kKA * 2));
+    gather_rows_kernel<<<static_cast<unsigned>(ceil_div(m_pad * kKA, 256)), 256, 0, st>>>(
+        ahi, alo, hp.row_idx, hp.m, g, g + m_pad * kKA, m_pad);
+    WGP_LAUNCH_CHECK();
+    ahi = g;
+    alo = g + m_pad * kKA;
+    a_rows = m_pad;
+    a_row0 = 0;
+  }
+  const CUtensorMap mAhi = make_map(ahi, kKA, a_rows, kKA * 4, kKA, kTI);
+  const CUtensorMap mAlo = make_map(alo, kKA, a_rows, kKA * 4, kKA, kTI);
+  const CUtensorMap mBhi = make_map(ops.b_hi, kKA, ops.n_pad, kKA * 4, kKA, 64);  // MMA-1 N = 64 points
+  const CUtensorMap mBlo = make_map(ops.b_lo, kKA, ops.n_pad, kKA * 4, kKA, 64);
+  // one TJ-point x s_pad box per plane (128-byte rows: 32 tf32 / 64 bf16 points)
+  const CUtensorMapDataType vt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUtensorMap mVhi = make_map(vhi, nv, s, ldp * esz, TJ, spad, vt);
+  const CUtensorMap mVlo = make_map(vlo, nv, s, ldp * esz, TJ, spad, vt);
+
+  TcArgs a{};
+  a.m = hp.m;
+  a.a_row0 = a_row0;
+  a.j0 = hp.j0;
+  a.j1 = hp.j1;
+  a.num_jt = static_cast<int>(ceil_div(nv, TJ));
+  a.s = s;
+  a.s_pad = spad;
+  // Ring depths: V tiles are consumed by MMA-2 and must be prefetched far
+  // enough ahead to cover the L2->SMEM latency (measured: 3 stages starve
+  // MMA-2); the B ring only feeds MMA-1, which runs ahead anyway.
+  static const int env_nb = [] {
+    const char* e = getenv("WGP_TC_NB");
+    return e ? atoi(e) : 0;
+  }();
+  static const int env_nv = [] {
+    const char* e = getenv("WGP_TC_NV");
+    return e ? atoi(e) : 0;
+  }();
+  a.vstage_bytes = 2u * static_cast<uint32_t>(spad) * 128u;
+  // A_I (32 KB) + the running sum R (512 s_pad bytes; aliases A when A lives in TMEM)
+  const bool a_tmem = bf16 ? Cfg<true>::kATmem : Cfg<false>::kATmem;
+  a.a_region = a_tmem ? std::max(32768u, 512u * spad) : 32768u + 512u * spad;
+  const int bstage = 2 * 64 * 128;
+  a.nb = env_nb > 0 ? std::min(env_nb, kMaxStages) : 3;
+  a.nv = std::min<int>(kMaxStages, (kSmemLimit - static_cast<int>(a.a_region) - 512 * spad - 1024 - a.nb * bstage) /
+                                       static_cast<int>(a.vstage_bytes));
+  if (env_nv > 0) a.nv = std::min(a.nv, env_nv);
+  if (!bf16) a.nv = Cfg<false>::kTilesInFlight;  // V slots share the K slots' barriers
+  if (a.nv < 2 || a.nb < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
+  a.row_idx = hp.row_idx;
+  a.r0 = hp.r0;
+  a.V = hp.V;
+  a.ldv = hp.ldv;
+  a.out = hp.out;
+  a.ldo = hp.ldo;
+  a.B = hp.B;
+  a.ldb = hp.ldb;
+  a.mode = hp.mode;
+  a.sf2 = hp.sf2;
+  a.a = hp.a;
+  a.diag = hp.diag;
+  a.hyp = hp.hyp;
+  a.vscale = vscale;
+  a.m_pad = m_pad;
+  a.done = hp.done;
+  static const int dbg = [] {
+    const char* e = getenv("WGP_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  a.dbg = dbg;
+  a.nk1 = ops.nk1;
+#ifdef WGP_TC_ABLATE
+  static const bool tracing = getenv("WGP_TC_TRACE") != nullptr;
+#else
+  static const bool tracing = [] {  // the stamps are compiled out of the default build
+    if (getenv("WGP_TC_TRACE")) fprintf(stderr, "[hv_tc] WGP_TC_TRACE needs a -DWGP_TC_ABLATE build\n");
+    return false;
+  }();
+#endif
+  static Workspace ws_trace;
+  a.trace = nullptr;
+  if (tracing) {
+    a.trace = static_cast<long long*>(ws_trace.ensure(sizeof(long long) * 16 * (a.num_jt + 4)));
+    WGP_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(long long) * 16 * (a.num_jt + 4), st));
+  }
+  const int64_t row_tiles = ceil_div(hp.m, kTI);
+  const int64_t key_tiles = hp.split_rows > 0 ? ceil_div(hp.split_rows, kTI) : row_tiles;
+  // L2 rasterisation: every CTA streams the operand planes of its J range
+  // (B hi / lo + V hi / lo: 256 + 2 esz s_pad bytes per point).  With one
+  // split the concurrently running row tiles drift apart along J over the
+  // waves, and once the planes outgrow L2 they re-read them from HBM
+  // (config 3, n = 391k: 463 GB of DRAM reads per H.V at a 53% L2 hit rate,
+  // ncu).  Splits whose J range fits the budget, with the split-major grid,
+  // keep the range L2-resident across all row tiles; the fp32 partials are
+  // capped at WGP_TC_PART_GB (default 32 GB, keyed like the splits: a row
+  // shard allocates its share).
+  static const double l2_budget = [] {
+    const char* e = getenv("WGP_TC_L2MB");
+    return (e ? atof(e) : 48.0) * 1e6;
+  }();
+  int min_sp = 1;
+  if (l2_budget > 0) {
+    const double plane_bytes = static_cast<double>(nv) * (256.0 + 2.0 * static_cast<double>(esz) * spad);
+    min_sp = static_cast<int>(std::ceil(plane_bytes / l2_budget));
+    // the cap uses the split key's rows, so a row shard picks the full operator's splits
+    const double part_row = 4.0 * spad * static_cast<double>(key_tiles * kTI);
+    static const double part_cap = [] {
+      const char* e = getenv("WGP_TC_PART_GB");
+      return (e ? atof(e) : 32.0) * 1e9;
+    }();
+    min_sp = std::max(1, std::min({min_sp, static_cast<int>(part_cap / part_row), 64}));
+  }
+  a.splits = choose_splits(key_tiles, a.num_jt, sm_count(), min_sp);
+  static const int force_splits = [] {
+    const char* e = getenv("WGP_TC_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  if (force_splits > 0) a.splits = std::min(force_splits, a.num_jt);
+  // fp32 accumulation chunk (tiles): bounds the accumulation error, see the kernel
+  static const int env_chunk = [] {
+    const char* e = getenv("WGP_TC_CHUNK");
+    return e ? atoi(e) : 0;
+  }();
+  a.chunk = env_chunk >= 4 ? env_chunk : 1024 / TJ;
+  static const int env_flush = [] {
+    const char* e = getenv("WGP_TC_FLUSH");
+    return e ? atoi(e) : 0;
+  }();
+  a.flush_every = env_flush >= 1 ? env_flush : 64;
+  // fp16 engine on the full operator (not a row shard: the stream-K pieces
+  // depend on the launch's row tiles): the persistent kernel
+  static const bool persist_env = [] {
+    const char* e = getenv("WGP_TC_PERSIST");
+    return e && atoi(e) != 0;  // opt-in: measured slower than the per-(row tile, split) grid once the
+                               // instrumentation was compiled out (config 1: 0.180 vs 0.169 ms)
+  }();
+  if (bf16 && persist_env && key_tiles == row_tiles) {
+    a.splits = std::max(1, std::min(min_sp, a.num_jt));  // L2 locality only; the balance is stream-K's
+    a.row_tiles = static_cast<int>(row_tiles);
+    a.units = row_tiles * a.num_jt;
+    a.ctas = static_cast<int>(std::min<int64_t>(sm_count(), a.units));
+    const int64_t per_cta = a.units / a.ctas;
+    const int64_t t_max = ceil_div(a.num_jt, a.splits);
+    a.kp = static_cast<int>(std::min<int64_t>(a.ctas, t_max / per_cta + 2));
+    const int64_t slots = static_cast<int64_t>(a.splits) * a.kp;
+    const size_t pbytes = sizeof(float) * slots * spad * m_pad;
+    const size_t fbytes = t_max > static_cast<int64_t>(a.flush_every) * a.chunk ? sizeof(double) * slots * spad * m_pad : 0;
+    char* pw = static_cast<char*>(ws_part.ensure(round_up(pbytes, 256) + fbytes + 256));
+    a.part = reinterpret_cast<float*>(pw);
+    a.flush = reinterpret_cast<double*>(pw + round_up(pbytes, 256));
+    a.tma_part = 1;
+    const CUtensorMap mPart = make_map(a.part, static_cast<uint64_t>(m_pad), static_cast<uint64_t>(slots) * spad,
+                                       m_pad * 4, kTI, static_cast<uint32_t>(spad), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                       CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.a_region = 32768u + 512u * spad;  // A_I | R (not aliased: the next piece's A lands while R is live)
+    a.nv = std::min<int>(kMaxStages, (kSmemLimit - static_cast<int>(a.a_region) - 1024 - a.nb * bstage) /
+                                         static_cast<int>(a.vstage_bytes));
+    if (env_nv > 0) a.nv = std::min(a.nv, env_nv);
+    if (a.nv < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
+    const int psmem = static_cast<int>(a.a_region) + 1024 + a.nb * bstage + a.nv * static_cast<int>(a.vstage_bytes);
+    static Workspace ws_pcta;
+    a.ctatime = tracing ? static_cast<long long*>(ws_pcta.ensure(sizeof(long long) * 12 * a.ctas)) : nullptr;
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+    if (ops.profiling) {
+      WGP_CUDA(cudaEventCreate(&pe0));
+      WGP_CUDA(cudaEventCreate(&pe1));
+      WGP_CUDA(cudaEventRecord(pe0, st));
+    }
+    WGP_SMEM_ATTR(hv_f16p_kernel, kSmemLimit);
+    hv_f16p_kernel<<<static_cast<unsigned>(a.ctas), kThreads, psmem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart,
+                                                                           a);
+    WGP_LAUNCH_CHECK();
+    if (ops.profiling) {
+      WGP_CUDA(cudaEventRecord(pe1, st));
+      ops.events.emplace_back(pe0, pe1);
+    }
+    tc_reduce_pieces_kernel<<<dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), 256, 0, st>>>(a);
+    WGP_LAUNCH_CHECK();
+    if (tracing) trace_report(a, static_cast<int>(std::min<int64_t>(a.units / a.ctas, a.num_jt + 3)),
+                              static_cast<unsigned>(a.ctas), st);
+    return;
+  }
+  const int max_tiles = static_cast<int>(ceil_div(a.num_jt, a.splits));
+  const bool flushes = max_tiles > a.flush_every * a.chunk;
+  const size_t part_bytes = a.splits > 1 ? sizeof(float) * a.splits * spad * m_pad : 0;
+  const size_t flush_bytes = flushes ? sizeof(double) * a.splits * spad * m_pad : 0;
+  char* pw = static_cast<char*>(ws_part.ensure(round_up(part_bytes, 256) + flush_bytes + 256));
+  a.part = reinterpret_cast<float*>(pw);
+  a.flush = reinterpret_cast<double*>(pw + round_up(part_bytes, 256));
+  // The split partial of a CTA, R = [s_pad][128] fp32 in shared memory, is one
+  // box of the partial buffer viewed as [splits * s_pad] columns x [m_pad] rows.
+  CUtensorMap mPart = mAhi;  // unused unless tma_part
+  a.tma_part = 0;
+  if (a.splits > 1) {
+    mPart = make_map(a.part, static_cast<uint64_t>(m_pad), static_cast<uint64_t>(a.splits) * spad, m_pad * 4, kTI,
+                     static_cast<uint32_t>(spad), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_NONE);
+    a.tma_part = 1;
+  }
+  const int smem = static_cast<int>(a.a_region) + 1024 + a.nb * bstage + a.nv * static_cast<int>(a.vstage_bytes) +
+                   512 * spad;  // + sVd
+  const unsigned grid = static_cast<unsigned>(row_tiles * a.splits);
+  static Workspace ws_cta;
+  a.ctatime = nullptr;
+  if (tracing) a.ctatime = static_cast<long long*>(ws_cta.ensure(sizeof(long long) * 12 * grid));
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (ops.profiling) {
+    WGP_CUDA(cudaEventCreate(&ev0));
+    WGP_CUDA(cudaEventCreate(&ev1));
+    WGP_CUDA(cudaEventRecord(ev0, st));
+  }
+  if (bf16)
+    launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st);
+  else
+    launch_tc<false>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st);
+  if (ops.profiling) {
+    WGP_CUDA(cudaEventRecord(ev1, st));
+    ops.events.emplace_back(ev0, ev1);
+  }
+  if (tracing) trace_report(a, static_cast<int>(static_cast<int64_t>(a.num_jt) / a.splits), grid, st);
   if (a.splits > 1) {
     tc_reduce_kernel<<<dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), 256, 0, st>>>(a);
     WGP_LAUNCH_CHECK();

@@ -383,6 +383,79 @@ __device__ __forceinline__ void mma2_tile_tf32(uint32_t o, uint32_t kcol, uint64
       "}\n"
       ::"r"(o), "r"(kcol), "l"(vh), "l"(vl), "r"(idesc), "r"(acc));
 }
+// The 12 MMAs of one fp16 MMA-2 tile (64 points, 4 K steps of 16 in fp16 x 3):
+// per 32-column half h of the tile's TMEM columns, k1 pairs in [32h, 32h+16)
+// and k2 pairs in [32h+16, 32h+32) (8 columns per K step); V hi / lo
+// descriptors advance 32 bytes per K step.  One asm block, one elect.
+__device__ __forceinline__ void mma2_tile_f16(uint32_t o, uint32_t kcol, uint64_t vh, uint64_t vl, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, p, t;\n"
+      " .reg .b32 a1, a2;\n"
+      " .reg .b64 yh, yl;\n"
+      " setp.ne.b32 p, %5, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 a1, %1, 0;\n"
+      " add.u32 a2, %1, 16;\n"
+      " add.s64 yh, %2, 0;\n"
+      " add.s64 yl, %3, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yh, %4, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], yh, %4, t;\n"
+      " add.u32 a1, %1, 8;\n"
+      " add.u32 a2, %1, 24;\n"
+      " add.s64 yh, %2, 2;\n"
+      " add.s64 yl, %3, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], yh, %4, t;\n"
+      " add.u32 a1, %1, 32;\n"
+      " add.u32 a2, %1, 48;\n"
+      " add.s64 yh, %2, 4;\n"
+      " add.s64 yl, %3, 4;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], yh, %4, t;\n"
+      " add.u32 a1, %1, 40;\n"
+      " add.u32 a2, %1, 56;\n"
+      " add.s64 yh, %2, 6;\n"
+      " add.s64 yl, %3, 6;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], yh, %4, t;\n"
+      "}\n"
+      ::"r"(o), "r"(kcol), "l"(vh), "l"(vl), "r"(idesc), "r"(acc));
+}
+// The 6 MMAs of one 32-point fp16 MMA-2 tile (2 K steps of 16): k1 pairs in
+// [kcol, kcol + 16), k2 pairs in [kcol + 16, kcol + 32); vh / vl already point
+// at the tile's 32 points of the 64-point V stage.
+__device__ __forceinline__ void mma2_tile32_f16(uint32_t o, uint32_t kcol, uint64_t vh, uint64_t vl, uint32_t idesc,
+                                                uint32_t acc) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, p, t;\n"
+      " .reg .b32 a1, a2;\n"
+      " .reg .b64 yh, yl;\n"
+      " setp.ne.b32 p, %5, 0;\n"
+      " setp.eq.b32 t, 0, 0;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " add.u32 a1, %1, 0;\n"
+      " add.u32 a2, %1, 16;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], %2, %4, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], %3, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], %2, %4, t;\n"
+      " add.u32 a1, %1, 8;\n"
+      " add.u32 a2, %1, 24;\n"
+      " add.s64 yh, %2, 2;\n"
+      " add.s64 yl, %3, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yh, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yl, %4, t;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], yh, %4, t;\n"
+      "}\n"
+      ::"r"(o), "r"(kcol), "l"(vh), "l"(vl), "r"(idesc), "r"(acc));
+}
 // TMA 2D load multicast to the CTAs of `mask` in the cluster: the box lands at
 // the same shared-memory offset in each and completes tx bytes on the
 // mbarrier at the same offset in each (one elected lane).
