@@ -144,11 +144,6 @@ struct TcArgs {
   long long* trace;  // WGP_TC_TRACE: per-tile clock64 stamps of CTA 0 ([T][16])
   long long* ctatime;  // WGP_TC_TRACE: per CTA {smid, globaltimer at start, after the tile loop, at exit}
   int nk1;  // packed Gram K steps (TcOperands::nk1), 0: 12 hi / lo MMAs
-  // persistent fp16 engine (hv_f16p_kernel): stream-K over (item, J tile) units
-  int row_tiles;   // R: row tiles of this launch
-  int64_t units;   // R * num_jt
-  int kp;          // partial slots per item (pieces an item can be cut into)
-  int ctas;        // G: CTAs of the persistent launch
   int dbg;  // ablation bits (WGP_TC_DEBUG): 1 no epilogue math, 2 no MMA-2, 4 no MMA-1, 8 no V loads,
             // 16 no epilogue TMEM traffic, 32 no B loads, 128 (H16) FMA-pipe ex2 for odd entries
 };
@@ -448,24 +443,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
         const uint32_t kb = tmem + K::tile_col(t);
         const uint64_t dv = umma_desc(base);
-        if (!(dbg & 2) && !H16) {
+        if (dbg & 2) {  // (ablation: no K.V)
+        } else if constexpr (H16) {
+          // per 32-point half h: k1 pairs in columns [32h, 32h+16), k2 in
+          // [32h+16, 32h+32); 12 MMAs from one asm block
+          mma2_tile_f16(o, kb, dv, dv + box, id2, tc > 0 ? 1u : 0u);
+        } else {
           static_assert(H16 || K::kLoOff == 64, "mma2_tile_tf32 assumes k_lo 64 columns after k_hi");
           mma2_tile_tf32(o, kb, dv, dv + box, id2, tc > 0 ? 1u : 0u);
-        } else if (!(dbg & 2)) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if constexpr (H16) {
-              // per 32-point half h: k1 in columns [32h, 32h+16), k2 in
-              // [32h+16, 32h+32); a 16-point K step is 8 columns
-              const uint32_t c1 = 32u * (k >> 1) + 8u * (k & 1);
-              mma3_ts_f16(o, kb + c1, kb + c1 + 16, dv + 2 * k, dv + box + 2 * k, id2,
-                           (tc > 0 || k > 0) ? 1u : 0u);
-            } else {
-              // k_hi in the tile's 32 columns, k_lo kLoOff further; an 8-point K step is 8 columns
-              mma3_ts(o, kb + 8 * k, kb + K::kLoOff + 8 * k, dv + 2 * k, dv + box + 2 * k, id2,
-                      (tc > 0 || k > 0) ? 1u : 0u);
-            }
-          }
         }
         if (trace && blockIdx.x == 0 && lane == 0) trace[t * 16 + 5] = clock64();
         if (t == 0 && ctatime && lane == 0) {
@@ -809,521 +794,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     ctatime[blockIdx.x * 12 + 3] = gt;
   }
   if (warp == kWarpVProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-// ------------------------------------------------------------------ persistent fp16 engine
-// hv_f16p_kernel: the fp16x3 K.V pipeline of hv_tc_kernel<true> as ONE CTA per
-// SM that walks a contiguous range of work instead of a CTA per (row tile,
-// split).  The per-CTA fill (A_I load and copy, the first Gram and
-// conversion) and tail (last K.V, drain, fold, store) cost ~11 us per CTA at
-// config 1 against ~45 us of steady state, and 424 CTAs made 2.86 waves; here
-// the pipeline runs through item boundaries and the work is dealt evenly.
-//
-// Work: items i = sp * R + rt (split-major, as the grid order of
-// hv_tc_kernel: the CTAs running together share a J range that stays in L2),
-// item i owns the J tiles of split sp; the units (item, J tile) of all items,
-// concatenated in item order, are dealt to the G CTAs in contiguous ranges
-// [c U / G, (c + 1) U / G) (stream-K).  A CTA's range is a sequence of
-// pieces (a J-tile subrange of one item); each piece leaves its fp32 partial
-// in slot sp * kp + (c - the first CTA of the item), and tc_reduce_pieces sums
-// an item's pieces in CTA order: deterministic for a given launch shape.
-//
-// Item boundaries: the TMEM A_I of the next piece is copied by the epilogue
-// group that converts the current piece's last tile, right after that tile's
-// Gram completed (MMA-1 is done with the old A_I); MMA-1 resumes on the new
-// A_I while MMA-2 and the other groups work through the tiles in flight.  The
-// accumulator chunks alternate O0 / O1 across pieces, so MMA-2 does not wait
-// for a piece's final drain.
-__device__ __forceinline__ int split_begin(const TcArgs& p, int s) {
-  return p.num_jt * s / p.splits;  // 32-bit: num_jt * splits < 2^31 (host-checked)
-}
-// the CTA whose unit range holds unit x (ranges [c U / G, (c + 1) U / G))
-__device__ __forceinline__ int cta_of(const TcArgs& p, int64_t x) {
-  return static_cast<int>(((x + 1) * p.ctas - 1) / p.units);
-}
-// Walks this CTA's pieces.  The 64-bit divisions (a call on the GPU, whose
-// register save / restore spilled the epilogue) happen once, when the first
-// piece is located; later pieces start at item boundaries (slot k = 0).
-struct PieceWalk {
-  int64_t u, uend;
-  int sp, rt, a, b0, Ts, k0;
-  __device__ __forceinline__ explicit PieceWalk(const TcArgs& p) {
-    u = p.units * blockIdx.x / p.ctas;
-    uend = p.units * (blockIdx.x + 1) / p.ctas;
-    sp = 0;
-    while (sp + 1 < p.splits && static_cast<int64_t>(split_begin(p, sp + 1)) * p.row_tiles <= u) ++sp;
-    b0 = split_begin(p, sp);
-    Ts = split_begin(p, sp + 1) - b0;
-    const int64_t off = u - static_cast<int64_t>(b0) * p.row_tiles;
-    rt = Ts > 0 ? static_cast<int>(off / Ts) : 0;
-    a = static_cast<int>(off - static_cast<int64_t>(rt) * Ts);
-    const int64_t istart = static_cast<int64_t>(b0) * p.row_tiles + static_cast<int64_t>(rt) * Ts;
-    k0 = static_cast<int>(blockIdx.x) - (u < uend ? cta_of(p, istart) : static_cast<int>(blockIdx.x));
-  }
-  // next piece: row tile, first J tile, tile count, partial slot
-  __device__ __forceinline__ bool next(const TcArgs& p, int& rt_, int& jt0, int& T, int& slot) {
-    if (u >= uend) return false;
-    const int64_t left = uend - u;
-    T = Ts - a < left ? Ts - a : static_cast<int>(left);
-    rt_ = rt;
-    jt0 = b0 + a;
-    slot = sp * p.kp + k0;
-    k0 = 0;
-    u += T;
-    a += T;
-    if (a == Ts) {  // the next item: the next row tile, or the first of the next (non-empty) split
-      a = 0;
-      if (++rt == p.row_tiles) {
-        rt = 0;
-        do {
-          ++sp;
-          b0 = split_begin(p, sp);
-          Ts = split_begin(p, sp + 1) - b0;
-        } while (Ts == 0 && sp + 1 < p.splits);
-      }
-    }
-    return true;
-  }
-};
-
-// Pipeline of the persistent engine.  A unit is a 64-point J tile: one TMA
-// stage of B and of V, one N = 64 Gram group (12 kind::tf32 MMAs, MMA-1
-// warp), one conversion by one epilogue group, one K.V step (12 kind::f16
-// MMAs, MMA-2 warp); four units in flight in TMEM.  Two issuing warps, so
-// each one's barrier waits and commits (~100 clk apiece even when the phase
-// is complete: scripts/ubench/ubench_loop.cu) overlap the other's MMAs; one
-// warp issuing both streams left the tensor pipe idle during its
-// bookkeeping (0.195 vs 0.175 ms at config 1).
-struct F16P {
-  static constexpr int kUJ = 64;             // points per unit
-  static constexpr int kBufs = 4;            // TMEM S / K buffers of 64 columns
-  static constexpr uint32_t kOStride = 96, kAhi = 192, kAlo = 224, kGrp0 = 256;
-  static constexpr uint32_t kBStage = 2u * kUJ * 128u;  // B hi | lo (64 points x 32 fp32)
-  static __device__ __forceinline__ uint32_t buf_col(int g) {
-    return kGrp0 + 64u * static_cast<uint32_t>(g & (kBufs - 1));
-  }
-};
-
-__global__ void __launch_bounds__(kThreads, 1)
-    hv_f16p_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
-                   const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
-                   const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
-                   const __grid_constant__ CUtensorMap mPart, const TcArgs p) {
-  using K = F16P;
-  constexpr int NBUF = K::kBufs;
-  constexpr int UJ = K::kUJ;
-  if (p.done && *p.done) return;
-  long long gt0 = 0;
-  if (p.ctatime && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
-  // Instrumentation (builds with -DWGP_TC_ABLATE only: the stamps and
-  // ablation branches cost the latency-critical MMA warps ~5%):
-  // WGP_TC_TRACE per-unit clock64 stamps of CTA 0 (hv_tc_kernel's slots),
-  // WGP_TC_DEBUG ablation bits 2 / 4 / 8 / 16 / 32 as in hv_tc_kernel.
-#ifdef WGP_TC_ABLATE
-  const bool trc = p.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0;
-  const int trmax = p.num_jt + 3;
-  const int dbg = p.dbg;
-#define WGP_TR(unit, slot_)                                                   \
-  do {                                                                        \
-    if (trc && (unit) < trmax) p.trace[(unit) * 16 + (slot_)] = clock64();     \
-  } while (0)
-#else
-  constexpr int dbg = 0;
-#define WGP_TR(unit, slot_) \
-  do {                      \
-  } while (0)
-#endif
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bar_bfull[kMaxStages], bar_vfull[kMaxStages], bar_m1done[kDoneRing],
-      bar_m2done[kDoneRing];
-  __shared__ __align__(8) uint64_t bar_a, bar_atm, bar_kfull[NBUF], bar_ofull[2], bar_odrained[2];
-  __shared__ uint32_t tmem_slot;
-  __shared__ float sColScale[kEpiWarps][8 * kDrainK];
-
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sAhi = smem;
-  uint8_t* sAlo = smem + 16384;
-  // R: [s_pad][128] fp32 running sum of the current piece (not aliased with A:
-  // the next piece's A_I lands while R is live)
-  float* sR = reinterpret_cast<float*>(smem + 32768);
-  uint8_t* sB = smem + p.a_region;
-  uint8_t* sV = sB + static_cast<size_t>(p.nb) * K::kBStage;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int C = p.chunk;  // units per accumulation chunk
-  const int NB = p.nb, NV = p.nv;
-  const int spad = p.s_pad;
-  const uint32_t vbox = static_cast<uint32_t>(spad) * 128u;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NB; ++i) mbar_init(&bar_bfull[i], 1);
-    for (int i = 0; i < NV; ++i) mbar_init(&bar_vfull[i], 1);
-    for (int i = 0; i < kDoneRing; ++i) {
-      mbar_init(&bar_m1done[i], 1);
-      mbar_init(&bar_m2done[i], 1);
-    }
-    mbar_init(&bar_a, 1);
-    mbar_init(&bar_atm, 4);
-    for (int i = 0; i < NBUF; ++i) mbar_init(&bar_kfull[i], 4);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_ofull[i], 1);
-      mbar_init(&bar_odrained[i], kEpiWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == kWarpVProd) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_before();
-  __syncthreads();
-  tc_after();
-  const uint32_t tmem = tmem_slot;
-  int rt, ju0, U, slot;  // piece: row tile, first unit (global J unit), unit count, partial slot
-
-  if (warp == kWarpBProd) {
-    // ------------------------------------------------------------ TMA: A_I per piece, B ring (per unit)
-    PieceWalk pw(p);
-    int k = 0, gu = 0, st = 0;
-    while (pw.next(p, rt, ju0, U, slot)) {
-      if (k > 0) mbar_wait(&bar_atm, (k - 1) & 1);  // A of the previous piece is in TMEM: sA is free
-      mbar_expect_tx_warp(&bar_a, 2 * 16384);
-      tma_load_2d_warp(sAhi, &mAhi, &bar_a, 0, p.a_row0 + rt * kTI);
-      tma_load_2d_warp(sAlo, &mAlo, &bar_a, 0, p.a_row0 + rt * kTI);
-      for (int j = 0; j < U; ++j, ++gu, st = (st + 1 == NB) ? 0 : st + 1) {
-        if (gu >= NB) mbar_wait(&bar_m1done[(gu - NB) & (kDoneRing - 1)], ((gu - NB) >> 3) & 1);
-        uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
-        if (dbg & 32) {  // (ablation: no B loads)
-          mbar_arrive_warp(&bar_bfull[st]);
-          continue;
-        }
-        mbar_expect_tx_warp(&bar_bfull[st], K::kBStage);
-        const int pt = static_cast<int>(p.j0) + (ju0 + j) * UJ;
-        tma_load_2d_warp(base, &mBhi, &bar_bfull[st], 0, pt);
-        tma_load_2d_warp(base + K::kBStage / 2, &mBlo, &bar_bfull[st], 0, pt);
-      }
-      ++k;
-    }
-  } else if (warp == kWarpVProd) {
-    // ------------------------------------------------------------ TMA: V ring (per unit)
-    PieceWalk pw(p);
-    int gu = 0, st = 0;
-    while (pw.next(p, rt, ju0, U, slot)) {
-      for (int j = 0; j < U; ++j, ++gu, st = (st + 1 == NV) ? 0 : st + 1) {
-        if (gu >= NV) mbar_wait(&bar_m2done[(gu - NV) & (kDoneRing - 1)], ((gu - NV) >> 3) & 1);
-        uint8_t* base = sV + static_cast<size_t>(st) * p.vstage_bytes;
-        if (dbg & 8) {  // (ablation: no V loads)
-          mbar_arrive_warp(&bar_vfull[st]);
-          continue;
-        }
-        mbar_expect_tx_warp(&bar_vfull[st], p.vstage_bytes);
-        tma_load_2d_warp(base, &mVhi, &bar_vfull[st], (ju0 + j) * UJ, 0);
-        tma_load_2d_warp(base + vbox, &mVlo, &bar_vfull[st], (ju0 + j) * UJ, 0);
-      }
-    }
-  } else if (warp == kWarpM1) {
-    // ------------------------------------------------------------ MMA-1 (Gram, 3xTF32, A from TMEM), per unit
-    constexpr uint32_t id1 = idesc_tf32(kTI, UJ);
-    PieceWalk pw(p);
-    int k = 0, gu = 0, st = 0;
-    uint32_t bph = 0;
-    while (pw.next(p, rt, ju0, U, slot)) {
-      mbar_wait(&bar_atm, k & 1);  // this piece's A_I is in TMEM
-      for (int j = 0; j < U; ++j, ++gu) {
-        WGP_TR(gu, 6);
-        if (gu >= NBUF) {  // the buffer's previous unit has been multiplied
-          const int u = gu - NBUF;
-          mbar_wait(&bar_m2done[u & (kDoneRing - 1)], (u >> 3) & 1);
-        }
-        mbar_wait(&bar_bfull[st], bph);
-        tc_after();
-        WGP_TR(gu, 7);
-        uint8_t* base = sB + static_cast<size_t>(st) * K::kBStage;
-        const uint64_t dBhi = umma_desc(base), dBlo = umma_desc(base + K::kBStage / 2);
-        const uint32_t d = tmem + K::buf_col(gu);
-        if (dbg & 4) {  // (ablation: no Gram)
-        } else if (p.nk1) {
-          mma1_packed_tf32_ts(d, tmem + K::kAhi, dBhi, dBlo, id1, p.nk1);
-        } else {
-          mma1_group_tf32_ts(d, tmem + K::kAhi, tmem + K::kAlo, dBhi, dBlo, id1);
-        }
-        mma_commit(&bar_m1done[gu & (kDoneRing - 1)]);
-        WGP_TR(gu, 0);
-        if (++st == NB) st = 0, bph ^= 1u;
-      }
-      ++k;
-    }
-  } else if (warp == kWarpM2) {
-    // ------------------------------------------------------------ MMA-2 (K.V, fp16 x 3), per unit
-    const uint32_t id2 = idesc_f16(kTI, spad);
-    const uint64_t box = vbox >> 4;
-    PieceWalk pw(p);
-    int st = 0, cg = 0, gu = 0;
-    uint32_t vph = 0;
-    while (pw.next(p, rt, ju0, U, slot)) {
-      int tc = 0;
-      for (int j = 0; j < U; ++j, ++gu) {
-        const uint32_t o = tmem + static_cast<uint32_t>(cg & 1) * K::kOStride;
-        WGP_TR(gu, 4);
-        if (tc == 0 && cg >= 2) mbar_wait(&bar_odrained[cg & 1], ((cg - 2) >> 1) & 1);
-        WGP_TR(gu, 12);
-        mbar_wait(&bar_vfull[st], vph);
-        WGP_TR(gu, 13);
-        mbar_wait(&bar_kfull[gu & (NBUF - 1)], (gu / NBUF) & 1);
-        tc_after();
-        WGP_TR(gu, 3);
-        const uint64_t dv = umma_desc(sV + static_cast<size_t>(st) * p.vstage_bytes);
-        if (!(dbg & 2)) mma2_tile_f16(o, tmem + K::buf_col(gu), dv, dv + box, id2, tc > 0 ? 1u : 0u);
-        WGP_TR(gu, 5);
-        mma_commit(&bar_m2done[gu & (kDoneRing - 1)]);
-        if (tc == C - 1 || j == U - 1) {
-          mma_commit(&bar_ofull[cg & 1]);
-          ++cg;
-          tc = 0;
-        } else {
-          ++tc;
-        }
-        if (++st == NV) st = 0, vph ^= 1u;
-      }
-    }
-  } else if (warp < kEpiWarps) {
-    // ------------------------------------------------------------ epilogue
-    const int q = warp & 3, w = warp >> 2;
-    const int row = q * 32 + lane;
-    const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
-    const float sf2 = p.hyp ? p.hyp[0] : p.sf2;
-    const float osc = sf2 * (1.f / kKScale);
-    const int cpg = ((spad + kEpiGroups * 8 - 1) / (kEpiGroups * 8)) * 8;
-    const int cb = min(spad, w * cpg), ce = min(spad, (w + 1) * cpg);
-    const int FE = p.flush_every;
-    const int lag = max(2, C / 2);
-    float* Rr = sR + row;  // column c at Rr[c * 128]
-    for (int c = cb + lane; c < ce; c += 32)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&sColScale[warp][c - cb])),
-                   "l"(p.vscale + c)
-                   : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
-    // A_I of piece k: swizzled TMA tile -> TMEM (this warp's 32 lanes)
-    auto copy_a = [&](int k) {
-      mbar_wait(&bar_a, k & 1);
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {  // hi, lo: one plane's 32 registers at a time
-        uint32_t a[32];
-        const uint8_t* rp = (h ? sAlo : sAhi) + (row >> 3) * 1024 + (row & 7) * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 v = *reinterpret_cast<const uint4*>(rp + (c ^ (row & 7)) * 16);
-          a[4 * c] = v.x, a[4 * c + 1] = v.y, a[4 * c + 2] = v.z, a[4 * c + 3] = v.w;
-        }
-        __syncwarp();
-        tmem_st32(tmem + lanes + (h ? K::kAlo : K::kAhi), a);
-      }
-      tmem_wait_st();
-      tc_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_atm);
-    };
-    // chunk c (global: O buffer and barrier phases), lc its index in the piece;
-    // read in two passes of half the group's columns (register pressure)
-    constexpr int kH = (kDrainK + 1) / 2;
-    auto drain = [&](int c, int lc, bool valid, int slot_, int64_t lr) {
-      mbar_wait(&bar_ofull[c & 1], (c >> 1) & 1);
-      tc_after();
-      const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
-      const bool fresh = lc % FE == 0, flush = (lc + 1) % FE == 0;
-      double* F = p.flush + static_cast<int64_t>(slot_) * spad * p.m_pad + lr;
-#pragma unroll 1
-      for (int hp = 0; hp < 2; ++hp) {
-        uint32_t o[kH][8];
-        const int c0 = cb + 8 * kH * hp;
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < kH; ++k)
-          if (c0 + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + c0 + 8 * k, o[k]);
-        tmem_wait_ld();
-        if (hp == 1) {
-          tc_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_odrained[c & 1]);
-        }
-#pragma unroll
-        for (int k = 0; k < kH; ++k) {
-          if (c0 + 8 * k >= ce) break;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int col = c0 + 8 * k + i;
-            const float r = (fresh ? 0.f : Rr[col * 128]) + __uint_as_float(o[k][i]);
-            if (!flush) {
-              Rr[col * 128] = r;
-            } else if (valid && col < p.s) {
-              double* f = F + static_cast<int64_t>(col) * p.m_pad;
-              *f = (lc + 1 == FE ? 0.0 : *f) + static_cast<double>(r);
-            }
-          }
-        }
-      }
-    };
-    // the piece's last chunk: its partial (scaled to H.V units) into the slot
-    auto finish = [&](int c, int lc, bool valid, int rt_, int slot_, int64_t lr) {
-      double* F = p.flush + static_cast<int64_t>(slot_) * spad * p.m_pad + lr;
-      mbar_wait(&bar_ofull[c & 1], (c >> 1) & 1);
-      tc_after();
-      const uint32_t ocol = static_cast<uint32_t>(c & 1) * K::kOStride;
-      const bool fresh = lc % FE == 0;
-      const bool tma_out = lc < FE;  // no fp64 flush in this piece: R + O is its whole sum
-      float* part = p.part + static_cast<int64_t>(slot_) * spad * p.m_pad + lr;
-#pragma unroll 1
-      for (int hp = 0; hp < 2; ++hp) {
-        uint32_t o[kH][8];
-        const int c0 = cb + 8 * kH * hp;
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < kH; ++k)
-          if (c0 + 8 * k < ce) tmem_ld8(tmem + lanes + ocol + c0 + 8 * k, o[k]);
-        tmem_wait_ld();
-        if (hp == 1) {
-          tc_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_odrained[c & 1]);
-        }
-#pragma unroll
-        for (int k = 0; k < kH; ++k)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int col = c0 + 8 * k + i;
-            if (col >= ce) continue;
-            const float r = (fresh ? 0.f : Rr[col * 128]) + __uint_as_float(o[k][i]);
-            const float sc = osc * sColScale[warp][col - cb];
-            if (tma_out) {
-              Rr[col * 128] = r * sc;
-            } else if (valid && col < p.s) {
-              const double f = __ldcg(F + static_cast<int64_t>(col) * p.m_pad);
-              part[static_cast<int64_t>(col) * p.m_pad] = static_cast<float>(f + static_cast<double>(r)) * sc;
-            }
-          }
-      }
-      if (tma_out) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-        if (warp == 0 && lane == 0) {
-          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&mPart),
-                       "r"(rt_ * kTI), "r"(slot_ * spad), "r"(smem_u32(sR))
-                       : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // R is free again
-      }
-    };
-
-    PieceWalk pw(p);
-    bool have = pw.next(p, rt, ju0, U, slot);
-    if (have && w == 0) copy_a(0);
-    int k = 0, gb = 0, c0 = 0;  // piece ordinal, its first global unit, its first global chunk
-    while (have) {
-      const bool has_next = pw.u < pw.uend;
-      const int64_t lr = static_cast<int64_t>(rt) * kTI + row;
-      const bool valid = lr < p.m;
-      const int64_t g = valid ? (p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr) : -1;
-      const int nch = (U + C - 1) / C;
-      const int64_t pstart = p.j0 + static_cast<int64_t>(ju0) * UJ;  // the piece's first point
-      int dc = 0;
-      for (int gu = gb + ((w - gb % kEpiGroups) + kEpiGroups) % kEpiGroups; gu < gb + U; gu += kEpiGroups) {
-        const int t = gu - gb;
-        while (dc < nch - 1 && t >= (dc + 1) * C + lag) {
-          drain(c0 + dc, dc, valid, slot, lr);
-          ++dc;
-        }
-        const uint32_t bcol = K::buf_col(gu);
-        const int64_t dg = valid ? g - (pstart + static_cast<int64_t>(t) * UJ) : -1;
-        const bool diag_tile = __any_sync(0xffffffffu, dg >= 0 && dg < UJ);
-        const int dgi = static_cast<int>(dg < 0 || dg >= UJ ? -1 : dg);
-        mbar_wait(&bar_m1done[gu & (kDoneRing - 1)], (gu >> 3) & 1);
-        tc_after();
-        if (q == 0) WGP_TR(gu, 1);
-        if (has_next && t == U - 1) copy_a(k + 1);  // this piece's Grams are all done
-        if (!(dbg & 16)) {  // (ablation: 16 no epilogue TMEM traffic)
-          // each 32-column half of S is read, converted and overwritten in
-          // place by [k1 pairs (16 cols) | k2 pairs (16 cols)]
-          uint32_t r[32], wds[32];
-          __syncwarp();
-          tmem_ld32(tmem + lanes + bcol, r);
-          tmem_wait_ld();
-#pragma unroll 1
-          for (int half = 0; half < 2; ++half) {
-            const int dh = dgi - 32 * half;
-            if (diag_tile)
-              to_k_f16<false, true>(r, wds, dh);
-            else
-              to_k_f16<false, false>(r, wds, dh);
-            __syncwarp();
-            if (half == 0) tmem_ld32(tmem + lanes + bcol + 32, r);
-            tmem_st32(tmem + lanes + bcol + 32 * half, wds);
-            if (half == 0) tmem_wait_ld();
-          }
-          tmem_wait_st();
-        }
-        tc_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_kfull[gu & (NBUF - 1)]);
-        if (q == 0) WGP_TR(gu, 2);
-        WGP_TR(gu, 8 + q);
-      }
-      while (dc < nch - 1) {
-        drain(c0 + dc, dc, valid, slot, lr);
-        ++dc;
-      }
-      finish(c0 + dc, dc, valid, rt, slot, lr);
-      gb += U;
-      c0 += nch;
-      ++k;
-      have = pw.next(p, rt, ju0, U, slot);
-    }
-  }
-#undef WGP_TR
-  tc_before();
-  __syncthreads();
-  tc_after();
-  if (p.ctatime && threadIdx.x == 0) {
-    uint32_t smid;
-    long long gt;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.ctatime[blockIdx.x * 12 + 0] = smid;
-    p.ctatime[blockIdx.x * 12 + 1] = gt0;
-    p.ctatime[blockIdx.x * 12 + 3] = gt;
-  }
-  if (warp == kWarpVProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-// Sum of an item's piece partials (fp64, CTA order) + the row epilogue of tc_reduce_kernel.
-__global__ void tc_reduce_pieces_kernel(const TcArgs p) {
-  if (p.done && *p.done) return;
-  const int64_t lr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int c = blockIdx.y;
-  if (lr >= p.m) return;
-  const int rt = static_cast<int>(lr / kTI);
-  double acc = 0.0;
-  for (int sp = 0; sp < p.splits; ++sp) {
-    const int b0 = split_begin(p, sp), Ts = split_begin(p, sp + 1) - b0;
-    if (Ts <= 0) continue;
-    const int64_t istart = static_cast<int64_t>(b0) * p.row_tiles + static_cast<int64_t>(rt) * Ts;
-    const int n = cta_of(p, istart + Ts - 1) - cta_of(p, istart) + 1;
-    for (int k = 0; k < n; ++k)
-      acc += static_cast<double>(p.part[(static_cast<int64_t>(sp * p.kp + k) * p.s_pad + c) * p.m_pad + lr]);
-  }
-  float v = static_cast<float>(acc);
-  const int64_t g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
-  if (g >= p.j0 && g < p.j1) v = fmaf(p.hyp ? p.hyp[2] : p.diag, p.V[g + c * p.ldv], v);
-  float* dst = p.out + lr + c * p.ldo;
-  if (p.mode == kHvStore)
-    *dst = v;
-  else if (p.mode == kHvResidual)
-    *dst = p.B[g + c * p.ldb] - v;
-  else
-    *dst -= v;
 }
 
 // Sum of the split partials (in fp64, fixed order) + the kernel's row epilogue.
@@ -1914,59 +1384,6 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
     return e ? atoi(e) : 0;
   }();
   a.flush_every = env_flush >= 1 ? env_flush : 64;
-  // fp16 engine on the full operator (not a row shard: the stream-K pieces
-  // depend on the launch's row tiles): the persistent kernel
-  static const bool persist_env = [] {
-    const char* e = getenv("WGP_TC_PERSIST");
-    return e && atoi(e) != 0;  // opt-in: measured slower than the per-(row tile, split) grid once the
-                               // instrumentation was compiled out (config 1: 0.180 vs 0.169 ms)
-  }();
-  if (bf16 && persist_env && key_tiles == row_tiles) {
-    a.splits = std::max(1, std::min(min_sp, a.num_jt));  // L2 locality only; the balance is stream-K's
-    a.row_tiles = static_cast<int>(row_tiles);
-    a.units = row_tiles * a.num_jt;
-    a.ctas = static_cast<int>(std::min<int64_t>(sm_count(), a.units));
-    const int64_t per_cta = a.units / a.ctas;
-    const int64_t t_max = ceil_div(a.num_jt, a.splits);
-    a.kp = static_cast<int>(std::min<int64_t>(a.ctas, t_max / per_cta + 2));
-    const int64_t slots = static_cast<int64_t>(a.splits) * a.kp;
-    const size_t pbytes = sizeof(float) * slots * spad * m_pad;
-    const size_t fbytes = t_max > static_cast<int64_t>(a.flush_every) * a.chunk ? sizeof(double) * slots * spad * m_pad : 0;
-    char* pw = static_cast<char*>(ws_part.ensure(round_up(pbytes, 256) + fbytes + 256));
-    a.part = reinterpret_cast<float*>(pw);
-    a.flush = reinterpret_cast<double*>(pw + round_up(pbytes, 256));
-    a.tma_part = 1;
-    const CUtensorMap mPart = make_map(a.part, static_cast<uint64_t>(m_pad), static_cast<uint64_t>(slots) * spad,
-                                       m_pad * 4, kTI, static_cast<uint32_t>(spad), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                       CU_TENSOR_MAP_SWIZZLE_NONE);
-    a.a_region = 32768u + 512u * spad;  // A_I | R (not aliased: the next piece's A lands while R is live)
-    a.nv = std::min<int>(kMaxStages, (kSmemLimit - static_cast<int>(a.a_region) - 1024 - a.nb * bstage) /
-                                         static_cast<int>(a.vstage_bytes));
-    if (env_nv > 0) a.nv = std::min(a.nv, env_nv);
-    if (a.nv < 2) throw DeviceError("hv_tc: right-hand side too wide for the V ring");
-    const int psmem = static_cast<int>(a.a_region) + 1024 + a.nb * bstage + a.nv * static_cast<int>(a.vstage_bytes);
-    static Workspace ws_pcta;
-    a.ctatime = tracing ? static_cast<long long*>(ws_pcta.ensure(sizeof(long long) * 12 * a.ctas)) : nullptr;
-    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
-    if (ops.profiling) {
-      WGP_CUDA(cudaEventCreate(&pe0));
-      WGP_CUDA(cudaEventCreate(&pe1));
-      WGP_CUDA(cudaEventRecord(pe0, st));
-    }
-    WGP_SMEM_ATTR(hv_f16p_kernel, kSmemLimit);
-    hv_f16p_kernel<<<static_cast<unsigned>(a.ctas), kThreads, psmem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart,
-                                                                           a);
-    WGP_LAUNCH_CHECK();
-    if (ops.profiling) {
-      WGP_CUDA(cudaEventRecord(pe1, st));
-      ops.events.emplace_back(pe0, pe1);
-    }
-    tc_reduce_pieces_kernel<<<dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), 256, 0, st>>>(a);
-    WGP_LAUNCH_CHECK();
-    if (tracing) trace_report(a, static_cast<int>(std::min<int64_t>(a.units / a.ctas, a.num_jt + 3)),
-                              static_cast<unsigned>(a.ctas), st);
-    return;
-  }
   const int max_tiles = static_cast<int>(ceil_div(a.num_jt, a.splits));
   const bool flushes = max_tiles > a.flush_every * a.chunk;
   const size_t part_bytes = a.splits > 1 ? sizeof(float) * a.splits * spad * m_pad : 0;

@@ -153,17 +153,6 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-// 16-bit x 3 MMA-2 (kind::f16, K = 16 per instruction): D (+)= k1 v1 + k1 v2 + k2 v1.
-__device__ __forceinline__ void mma3_ts_f16(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
-                                             uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p, t, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %6, 0;\n"
-      " setp.eq.u32 t, 0, 0;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, t;\n}\n" ::"r"(d),
-      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
-}
 // kind::f16 instruction descriptor: D f32, A/B fp16 (a/b format 0), both K-major.
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
   return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
@@ -422,34 +411,6 @@ __device__ __forceinline__ void mma2_tile_f16(uint32_t o, uint32_t kcol, uint64_
       " add.u32 a2, %1, 56;\n"
       " add.s64 yh, %2, 6;\n"
       " add.s64 yl, %3, 6;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yh, %4, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yl, %4, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], yh, %4, t;\n"
-      "}\n"
-      ::"r"(o), "r"(kcol), "l"(vh), "l"(vl), "r"(idesc), "r"(acc));
-}
-// The 6 MMAs of one 32-point fp16 MMA-2 tile (2 K steps of 16): k1 pairs in
-// [kcol, kcol + 16), k2 pairs in [kcol + 16, kcol + 32); vh / vl already point
-// at the tile's 32 points of the 64-point V stage.
-__device__ __forceinline__ void mma2_tile32_f16(uint32_t o, uint32_t kcol, uint64_t vh, uint64_t vl, uint32_t idesc,
-                                                uint32_t acc) {
-  asm volatile(
-      "{\n"
-      " .reg .pred e, p, t;\n"
-      " .reg .b32 a1, a2;\n"
-      " .reg .b64 yh, yl;\n"
-      " setp.ne.b32 p, %5, 0;\n"
-      " setp.eq.b32 t, 0, 0;\n"
-      " elect.sync _|e, 0xffffffff;\n"
-      " add.u32 a1, %1, 0;\n"
-      " add.u32 a2, %1, 16;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], %2, %4, p;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], %3, %4, t;\n"
-      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], %2, %4, t;\n"
-      " add.u32 a1, %1, 8;\n"
-      " add.u32 a2, %1, 24;\n"
-      " add.s64 yh, %2, 2;\n"
-      " add.s64 yl, %3, 2;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yh, %4, t;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], yl, %4, t;\n"
       " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], yh, %4, t;\n"
