@@ -28,8 +28,9 @@
 // epilogue folds into a shared-memory fp32 sum and an fp64 CTA sum (error
 // independent of n).  J tiles of a row tile may be split across CTAs (split
 // count keyed on the global n, partials summed in fixed order ->
-// deterministic and shard-invariant).  WGP_HV_TC_F16 selects the opt-in
-// bf16x3 K.V variant (kind::f16, 64-point tiles).
+// deterministic and shard-invariant).  WGP_HV_TC_F16 selects the fp16x3 K.V
+// engine (kind::f16, 64-point tiles, k1 v1 + k1 v2 + k2 v1 over V scaled per
+// column by a power of two; bench.py's headline engine).
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -157,11 +158,12 @@ struct TcArgs {
 //     tf32 MMA costs >= 35 clk whatever its size, so N = 32 ran at half the
 //     tensor rate, measured), the epilogue overwrites each S in place with
 //     k_hi and writes k_lo 64 columns further.
-//   H16 = true (WGP_HV_TC_F16): K.V in bf16x3 (k1 v1 + k1 v2 + k2 v1, ~2^-17
-//     per product: half the tensor work, too coarse for tight solver
-//     tolerances), 64-point J tiles.  TMEM: O0, O1, five 64-column groups
-//     from 192 of one tile each (S: 64 fp32 columns, overwritten by the packed
-//     k1 | k2 pairs); A_I stays in shared memory (SS MMA-1).
+//   H16 = true (WGP_HV_TC_F16): K.V in fp16x3 (k1 v1 + k1 v2 + k2 v1, 11 + 11
+//     significant bits per operand; k' = 2^14 k / sf^2 and V scaled per column
+//     by a power of two keep both halves normal -- to_k_f16, split_v_f16_kernel;
+//     half the tensor work of 3xTF32), 64-point J tiles.  TMEM (layout 2): O0,
+//     O1, A_I hi/lo, four 64-column groups from 256 of one tile each (S: 64
+//     fp32 columns, overwritten by the packed k1 | k2 pairs).
 // The Gram (MMA-1) is 3xTF32 in both, over 64 points per instruction.
 // tf32 TMEM layout (compile-time WGP_TC_LAYOUT): 0 = single O [0, 96), A_I in
 // shared memory, three groups from 96; 1 = O0 | O1 [0, 192), A_I in shared
@@ -802,9 +804,20 @@ __global__ void tc_reduce_kernel(const TcArgs p) {
   const int64_t lr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (lr >= p.m) return;
+  // the split partials' loads are issued together (a serial loop waited one
+  // L2 round trip per split); summed in split order as before
+  const float* src = p.part + static_cast<int64_t>(c) * p.m_pad + lr;
+  const int64_t sstride = static_cast<int64_t>(p.s_pad) * p.m_pad;
   double acc = 0.0;
-  for (int sp = 0; sp < p.splits; ++sp)
-    acc += static_cast<double>(p.part[(static_cast<int64_t>(sp) * p.s_pad + c) * p.m_pad + lr]);
+  int sp = 0;
+  for (; sp + 4 <= p.splits; sp += 4) {
+    float x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = __ldcg(src + (sp + i) * sstride);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc += static_cast<double>(x[i]);
+  }
+  for (; sp < p.splits; ++sp) acc += static_cast<double>(__ldcg(src + sp * sstride));
   float v = static_cast<float>(acc);
   const int64_t g = p.row_idx ? static_cast<int64_t>(p.row_idx[lr]) : p.r0 + lr;
   if (g >= p.j0 && g < p.j1) v = fmaf(p.hyp ? p.hyp[2] : p.diag, p.V[g + c * p.ldv], v);
@@ -842,44 +855,81 @@ __device__ __forceinline__ float col_scale(unsigned mbits) {
 }
 
 // V[j0:j1, :s] -> fp16 planes v1 = f16(2^e_c v), v2 = f16(2^e_c v - v1)
-// [s][ldw] and vscale[c] = 2^-e_c (exact: |e_c| <= 100).  One CTA per column:
-// the column's max |v| (block reduction, float bits are monotone in |v|,
-// NaN sorts above every finite value), then its planes -- one launch instead
-// of memset + column max + split (~12 us at config 1 under ncu).
-__global__ void __launch_bounds__(1024) split_v_f16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv,
-                                                           __half* v1, __half* v2, int64_t ldw, float* vscale) {
-  const int c = blockIdx.x;
+// [s][ldw] and vscale[c] = 2^-e_c (exact: |e_c| <= 100).  One cluster of
+// kSplitCl CTAs per column, each CTA a contiguous slice of its rows: the
+// slice's max |v| (float bits are monotone in |v|, NaN sorts above every
+// finite value), the column max over the cluster through distributed shared
+// memory, then the planes -- one launch; the slice stays in registers when
+// it fits (kSplitKeep values per thread), otherwise it is re-read.  (One CTA
+// per column walking the column serially: 8.8 us at config 1, ncu.)
+constexpr int kSplitCl = 8, kSplitThreads = 256, kSplitKeep = 8;
+__global__ void __cluster_dims__(kSplitCl, 1, 1) __launch_bounds__(kSplitThreads)
+    split_v_f16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, __half* v1, __half* v2, int64_t ldw,
+                       float* vscale) {
+  const int c = blockIdx.y;
+  const uint32_t rank = cluster_ctarank();
+  const int64_t b0 = nv * rank / kSplitCl, b1 = nv * (rank + 1) / kSplitCl;
   const float* col = V + j0 + static_cast<int64_t>(c) * ldv;
+  const bool keep = b1 - b0 <= static_cast<int64_t>(kSplitKeep) * kSplitThreads;
+  float x[kSplitKeep];
   unsigned m = 0u;
-  for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) m = max(m, __float_as_uint(col[j]) & 0x7FFFFFFFu);
+  if (keep) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ unsigned sm[32];
-  __shared__ float ssc;
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    m = threadIdx.x < blockDim.x / 32 ? sm[threadIdx.x] : 0u;
+    for (int i = 0; i < kSplitKeep; ++i) {
+      const int64_t j = b0 + threadIdx.x + static_cast<int64_t>(i) * kSplitThreads;
+      x[i] = j < b1 ? col[j] : 0.f;
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0) {
-      ssc = col_scale(m);
-      vscale[c] = 1.f / ssc;
+    for (int i = 0; i < kSplitKeep; ++i) m = max(m, __float_as_uint(x[i]) & 0x7FFFFFFFu);
+  } else {
+    for (int64_t j = b0 + threadIdx.x; j < b1; j += kSplitThreads * kSplitKeep) {
+#pragma unroll
+      for (int i = 0; i < kSplitKeep; ++i) {
+        const int64_t jj = j + static_cast<int64_t>(i) * kSplitThreads;
+        x[i] = jj < b1 ? col[jj] : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < kSplitKeep; ++i) m = max(m, __float_as_uint(x[i]) & 0x7FFFFFFFu);
     }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ unsigned sm[kSplitThreads / 32];
+  __shared__ unsigned scta;
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
   __syncthreads();
-  const float sc = ssc;
+  if (threadIdx.x == 0) {
+    unsigned t = 0u;
+#pragma unroll
+    for (int w = 0; w < kSplitThreads / 32; ++w) t = max(t, sm[w]);
+    scta = t;
+  }
+  cluster_sync_all();  // every CTA's slice max is visible to the cluster
+  unsigned mc = 0u;
+#pragma unroll
+  for (int r = 0; r < kSplitCl; ++r) mc = max(mc, ld_shared_cluster_u32(&scta, static_cast<uint32_t>(r)));
+  const float sc = col_scale(mc);
+  if (rank == 0 && threadIdx.x == 0) vscale[c] = 1.f / sc;
   __half* h1 = v1 + static_cast<int64_t>(c) * ldw;
   __half* h2 = v2 + static_cast<int64_t>(c) * ldw;
-  for (int64_t j = threadIdx.x; j < nv; j += blockDim.x) {
-    const float v = col[j] * sc;
+  auto put = [&](int64_t j, float xv) {
+    const float v = xv * sc;
     const __half h = __float2half_rn(v);
     h1[j] = h;
     h2[j] = __float2half_rn(v - __half2float(h));
+  };
+  if (keep) {
+#pragma unroll
+    for (int i = 0; i < kSplitKeep; ++i) {
+      const int64_t j = b0 + threadIdx.x + static_cast<int64_t>(i) * kSplitThreads;
+      if (j < b1) put(j, x[i]);
+    }
+  } else {
+    for (int64_t j = b0 + threadIdx.x; j < b1; j += kSplitThreads) put(j, col[j]);
   }
+  cluster_sync_all();  // no CTA leaves while a peer may still read its scta
 }
 
-// Augmented operand rows from the prepared points (see TcOperands).
 __global__ void build_ops_kernel(const float* xs, int64_t n, int64_t n_pad, int dp, int d, bool packed, float* ahi,
                                  float* alo, float* bhi, float* blo) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1243,8 +1293,9 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   const dim3 vgrid(static_cast<unsigned>(ceil_div(nv, 256)), s);
   if (pre) {
   } else if (bf16) {
-    split_v_f16_kernel<<<s, 1024, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<__half*>(vhi),
-                                           reinterpret_cast<__half*>(vlo), ldw, vscale);
+    split_v_f16_kernel<<<dim3(kSplitCl, s), kSplitThreads, 0, st>>>(hp.V, hp.ldv, hp.j0, nv,
+                                                                     reinterpret_cast<__half*>(vhi),
+                                                                     reinterpret_cast<__half*>(vlo), ldw, vscale);
   } else
     split_v_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<float*>(vhi),
                                           reinterpret_cast<float*>(vlo), ldw);

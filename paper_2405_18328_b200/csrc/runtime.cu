@@ -1999,7 +1999,7 @@ extern "C" {
 const char* wgp_last_error(void) { return wgp::g_last_error.c_str(); }
 
 const char* wgp_version(void) {
-  return "warmgp_b200 0.2 (sm_100a; tcgen05 H.V: 3xTF32 Gram + bf16x3 K.V, fp64 chunk sums; SIMT fp32/fp64 kernel)";
+  return "warmgp_b200 0.2 (sm_100a; tcgen05 H.V: 3xTF32 Gram + 3xTF32 or fp16x3 K.V, fp64 chunk sums; fp64 DMMA CG operator; SIMT fp32/fp64 kernel)";
 }
 
 uint64_t wgp_launch_count(void) { return wgp::launch_counter().load(); }

@@ -6,6 +6,6 @@ export PYTHONPATH=.
 reps=$1; shift
 for r in $(seq $reps); do
   for lib in "$@"; do
-    WGP_LIBRARY=$PWD/ab/$lib timeout 60 python scripts/time_hv.py tc 13500 26 65 30 2>&1 | tail -1 | sed "s/^/[$lib] /"
+    WGP_LIBRARY=$PWD/ab/$lib timeout 60 python scripts/time_hv.py ${HV_IMPL:-tc_f16} 13500 26 65 30 2>&1 | tail -1 | sed "s/^/[$lib] /"
   done
 done | sort
