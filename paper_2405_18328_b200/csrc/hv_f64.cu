@@ -295,7 +295,7 @@ size_t hv64_workspace_bytes(int64_t n, int64_t m, int s) {
   return sizeof(double) * static_cast<size_t>(hv64_splits(n)) * s * round_up(m, TM);
 }
 
-void hv64(const Hv64Params& p, cudaStream_t st) {
+static void hv64_launch(const Hv64Params& p, cudaStream_t st, bool reduce, int* splits_out, int64_t* m_pad_out) {
   if (p.s <= 0 || p.m <= 0) return;
   if (p.s > 8 * kMaxNF) {  // column chunks of <= 80 (accumulator registers)
     for (int c0 = 0; c0 < p.s; c0 += 8 * kMaxNF) {
@@ -304,7 +304,7 @@ void hv64(const Hv64Params& p, cudaStream_t st) {
       q.V = p.V + c0 * p.ldv;
       q.out = p.out + c0 * p.ldo;
       if (p.B) q.B = p.B + c0 * p.ldb;
-      hv64(q, st);
+      hv64_launch(q, st, true, nullptr, nullptr);
     }
     return;
   }
@@ -324,8 +324,19 @@ void hv64(const Hv64Params& p, cudaStream_t st) {
     case 9: launch<9>(p, m_pad, splits, st); break;
     default: launch<10>(p, m_pad, splits, st); break;
   }
+  if (splits_out) *splits_out = splits;
+  if (m_pad_out) *m_pad_out = m_pad;
+  if (!reduce) return;
   hv64_reduce_kernel<<<dim3(static_cast<unsigned>(ceil_div(p.m, 256)), p.s), 256, 0, st>>>(p, m_pad, splits);
   WGP_LAUNCH_CHECK();
+}
+
+void hv64(const Hv64Params& p, cudaStream_t st) { hv64_launch(p, st, true, nullptr, nullptr); }
+
+bool hv64_partials(const Hv64Params& p, cudaStream_t st, int* splits, int64_t* m_pad) {
+  if (p.s <= 0 || p.m <= 0 || p.s > 8 * kMaxNF) return false;
+  hv64_launch(p, st, false, splits, m_pad);
+  return true;
 }
 
 }  // namespace wgp

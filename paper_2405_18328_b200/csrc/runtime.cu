@@ -741,6 +741,27 @@ struct Ctx {
 
   // fp64 CG operator: out = H V (store) or B - H V (residual) for output rows
   // [rr0, rr0 + m), fp64 V (all n rows) / out / B (hv_f64.cu).
+  Hv64Params hv64_params(const double* V, int64_t ldv, int s, double* out, int64_t ldo, int mode, const double* B,
+                         int64_t ldb, int64_t rr0, int64_t m, const int* done) {
+    Hv64Params q{};
+    q.xs = xs.as<float>();
+    q.n = n;
+    q.dp = dp;
+    q.d = d;
+    q.r0 = rr0;
+    q.m = m;
+    q.V = V;
+    q.ldv = ldv;
+    q.s = s;
+    q.out = out;
+    q.ldo = ldo;
+    q.B = B;
+    q.ldb = ldb;
+    q.mode = mode;
+    q.hyp = dhyp.as<float>();
+    q.done = done;
+    return q;
+  }
   void hv64_rows(const double* V, int64_t ldv, int s, double* out, int64_t ldo, int mode, const double* B,
                  int64_t ldb, int64_t rr0, int64_t m, const int* done) {
     Hv64Params q{};
@@ -829,6 +850,21 @@ struct Ctx {
     bool use_fused = !no_fused;
     auto iteration = [&](bool refresh) {
       if (sh) gather_rows(Pp, s);
+      // fp64, unsharded: hv64's split reduction runs inside cg_fused (HvFold)
+      static const bool no_fold = getenv("WGP_CG_NO_FOLD") != nullptr;
+      if (f64 && !refresh && !sh && use_fused && !no_fold) {
+        HvFold fold;
+        Hv64Params q = hv64_params(reinterpret_cast<const double*>(Pp), ld, s, reinterpret_cast<double*>(HPp), ld,
+                                   kHv64Store, nullptr, ld, 0, n, done);
+        hv64_ws.ensure(hv64_workspace_bytes(n, n, s));
+        q.part = hv64_ws.as<double>();
+        if (hv64_partials(q, st, &fold.splits, &fold.m_pad)) {
+          fold.part = q.part;
+          fold.hyp = q.hyp;
+          if (cg_fused(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, st, PPp, fold)) return;
+          use_fused = false;  // (the partials are re-formed below)
+        }
+      }
       cg_hv(Pp, s, HPp, kHvStore, nullptr, done, PPp);
       if (!refresh && !sh && use_fused) {  // alpha + update + direction in one cooperative kernel
         if (cg_fused(Xo, R, Pp, HPp, ld, n, s, cs, pt, c, st, PPp)) return;

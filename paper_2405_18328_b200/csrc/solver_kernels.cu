@@ -372,9 +372,48 @@ __device__ void store_partials(Red& red, int s, double* part) {
   }
 }
 
+// hv64's split reduction for this CTA's rows and column group (fp64 CG,
+// HvFold): HP = the fp64 split partials summed in split order + diag P,
+// bitwise hv64_reduce_kernel; every split's loads are issued together.
 template <class T>
-__global__ void cg_fused_kernel(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs,
-                                double* part, SolveCtrl* ctrl, float* pp) {
+__device__ __forceinline__ void fold_hv(T* HP, const T* P, int64_t ld, int s, int64_t rb, int64_t re,
+                                        const HvFold& fold) {
+  const double diag = static_cast<double>(fold.hyp[2]);
+  const int64_t ks = static_cast<int64_t>(s) * fold.m_pad;
+  for (int c0 = 4 * static_cast<int>(blockIdx.y); c0 < s; c0 += 4 * static_cast<int>(gridDim.y)) {
+    const int nu = s - c0 < 4 ? s - c0 : 4;
+    for (int64_t i = rb + threadIdx.x; i < re; i += NT) {
+      const double* src = fold.part + static_cast<int64_t>(c0) * fold.m_pad + i;
+      double h[4] = {0.0, 0.0, 0.0, 0.0};
+      int k = 0;
+      for (; k + 4 <= fold.splits; k += 4) {
+        double x[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[q][u] = u < nu ? __ldcg(src + (k + q) * ks + u * fold.m_pad) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) h[u] += x[q][u];
+      }
+      for (; k < fold.splits; ++k)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < nu) h[u] += __ldcg(src + k * ks + u * fold.m_pad);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < nu) {
+          const int64_t e = i + static_cast<int64_t>(c0 + u) * ld;
+          HP[e] = static_cast<T>(fma(diag, static_cast<double>(P[e]), h[u]));
+        }
+    }
+  }
+}
+
+template <class T>
+__global__ void cg_fused_kernel(T* X, T* R, T* P, T* HP, int64_t ld, int64_t n, int s, ColState cs,
+                                double* part, SolveCtrl* ctrl, float* pp, HvFold fold) {
   if (ctrl->done) return;  // read once by every CTA; CTA 0 updates the control state last
   __shared__ Red red;
   __shared__ int sconv[SMAX], snew[SMAX];
@@ -386,6 +425,8 @@ __global__ void cg_fused_kernel(T* X, T* R, T* P, const T* HP, int64_t ld, int64
     srs[c] = cs.rs[c];
   }
   if (threadIdx.x == 0) sfail = 0;
+  // (each thread's HP elements are the ones it reads below: no barrier needed)
+  if (fold.part) fold_hv(HP, P, ld, s, rb, re, fold);
   __syncthreads();
   // alpha_c = rs_c / (p_c . Hp_c)  (cg_alpha)
   cols4(s, rb, re, ld, red, [&](int c, int64_t e) {
@@ -888,8 +929,8 @@ void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
 }
 
 template <class T>
-bool cg_fused(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs, double* part,
-              SolveCtrl* ctrl, cudaStream_t st, float* pp) {
+bool cg_fused(T* X, T* R, T* P, T* HP, int64_t ld, int64_t n, int s, ColState cs, double* part,
+              SolveCtrl* ctrl, cudaStream_t st, float* pp, HvFold fold) {
   check_s(s);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = coop_grid(n, s);
@@ -901,7 +942,7 @@ bool cg_fused(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColSt
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, cg_fused_kernel<T>, X, R, P, HP, ld, n, s, cs, part, ctrl, pp);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, cg_fused_kernel<T>, X, R, P, HP, ld, n, s, cs, part, ctrl, pp, fold);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -925,8 +966,8 @@ bool cg_fused(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColSt
                                    cudaStream_t);                                                            \
   template void cg_direction<T>(T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,         \
                                 cudaStream_t, float*);                                                       \
-  template bool cg_fused<T>(T*, T*, T*, const T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,      \
-                            cudaStream_t, float*);
+  template bool cg_fused<T>(T*, T*, T*, T*, int64_t, int64_t, int, ColState, double*, SolveCtrl*,            \
+                            cudaStream_t, float*, HvFold);
 WGP_CG_INSTANTIATE(float)
 WGP_CG_INSTANTIATE(double)
 #undef WGP_CG_INSTANTIATE

@@ -110,9 +110,19 @@ void cg_direction(T* P, const T* R, int64_t ld, int64_t n, int s, ColState cs,
 // partials in the same fixed order, so results are bitwise those of the
 // three kernels.  Unsharded solves only.  Returns false (nothing launched)
 // when the cooperative launch is unavailable; the caller then runs the three.
+// fp64 H.V split partials for cg_fused to sum first (hv64_reduce_kernel's
+// sum: part[(k s + c) m_pad + r] over k < splits, in order, + hyp[2] P, for
+// the CTA's own rows and columns: one launch fewer per iteration);
+// part == nullptr: HP is already formed.
+struct HvFold {
+  const double* part = nullptr;
+  int splits = 0;
+  int64_t m_pad = 0;
+  const float* hyp = nullptr;
+};
 template <class T>
-bool cg_fused(T* X, T* R, T* P, const T* HP, int64_t ld, int64_t n, int s, ColState cs, double* part,
-              SolveCtrl* ctrl, cudaStream_t st, float* pp = nullptr);
+bool cg_fused(T* X, T* R, T* P, T* HP, int64_t ld, int64_t n, int s, ColState cs, double* part,
+              SolveCtrl* ctrl, cudaStream_t st, float* pp, HvFold fold = HvFold());
 // B = A (fp32 -> fp64) / B = A rounded to fp32, n x s column blocks.
 void widen(const float* A, int64_t lda, double* B, int64_t ldb, int64_t n, int s, cudaStream_t st);
 // out = A - B (n x s column blocks, leading dimension ld; float or double).

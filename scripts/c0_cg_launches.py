@@ -9,7 +9,7 @@ import paper_2405_18328_b200 as wg  # noqa: E402
 from paper_2405_18328_b200 import datasets  # noqa: E402
 
 p = datasets.config0()
-ctx = wg.Context(0)
+ctx = wg.Context(0, hv_impl=os.environ.get("HV_IMPL", "tc"))
 ctx.set_data(p.X)
 ctx.set_hyper([1.0] * 8 + [1.0, 0.5])
 rhs = np.random.default_rng(0).standard_normal((p.X.shape[0], 17)).astype(np.float32)

@@ -26,7 +26,7 @@ def timed(ctx, fn, reps=3):
 
 
 p = datasets.config0()
-ctx = wg.Context(0)
+ctx = wg.Context(0, hv_impl=os.environ.get("HV_IMPL", "tc"))
 ctx.set_data(p.X)
 ctx.set_hyper([2.6] * 8 + [1.14, 0.1])  # config 0's late hyperparameters (ill-conditioned)
 rhs = np.random.default_rng(0).standard_normal((p.X.shape[0], 17)).astype(np.float32)

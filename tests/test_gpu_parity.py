@@ -655,6 +655,31 @@ def test_ap_epoch_graph_matches_eager_subprocess():
     assert np.array_equal(outs[0], outs[1])
 
 
+def test_cg_iteration_paths_bitwise_subprocess():
+    """The implementations of a CG iteration's vector work give bitwise the
+    same solutions and iteration counts (fp64 and fp32 CG): the cooperative
+    kernel with hv64's split reduction folded in (the fp64 default), the
+    cooperative kernel after a separate reduction (WGP_CG_NO_FOLD=1) and the
+    three separate kernels (WGP_CG_NO_FUSED=1)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    outs = []
+    for extra in ({}, {"WGP_CG_NO_FOLD": "1"}, {"WGP_CG_NO_FUSED": "1"}):
+        path = os.path.join(root, "gpurun_out", "_cgp_%d.npy" % len(outs))
+        env = {k: v for k, v in os.environ.items() if k not in ("WGP_CG_NO_FOLD", "WGP_CG_NO_FUSED")}
+        env.update(PYTHONPATH=root, **extra)
+        r = subprocess.run([sys.executable, os.path.join(root, "scripts", "cg_path_check.py"), path], env=env,
+                           cwd=root, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, (extra, r.stderr[-2000:])
+        outs.append(np.load(path))
+        os.remove(path)
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])
+
+
 def test_cg_unreachable_tolerance_stays_bounded(ctx):
     """fp32 CG (cg_precision f32): a tolerance below the fp32 attainable accuracy never converges: every
     column stalls, is restored to its best iterate (exact residual at a
