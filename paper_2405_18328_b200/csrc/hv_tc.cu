@@ -24,7 +24,9 @@
 // (double-buffered chunk drains), A_I hi/lo, and two 128-column groups each
 // holding S(t) | S(t+1) and then, in place, their K planes -- 4 tiles in
 // flight, so MMA-1 runs ahead of MMA-2 and one tile's epilogue hides behind
-// the MMAs of the next.  MMA-2 accumulates in fp32 chunks of 32 tiles that the
+// the MMAs of the next (the fp16 engine: four epilogue warpgroups, 640
+// threads, A_I in shared memory and five 64-point tiles in flight).  MMA-2
+// accumulates in fp32 chunks of 32 tiles that the
 // epilogue folds into a shared-memory fp32 sum and an fp64 CTA sum (error
 // independent of n).  J tiles of a row tile may be split across CTAs (split
 // count keyed on the global n, partials summed in fixed order ->
@@ -53,9 +55,20 @@ constexpr int kKA = 32;    // augmented Gram dimension (d + 2 <= 32)
 #ifndef WGP_TC_EPI
 #define WGP_TC_EPI 3
 #endif
-constexpr int kEpiGroups = WGP_TC_EPI;          // epilogue warpgroups
-constexpr int kThreads = 128 * kEpiGroups + 128;  // + 4 control warps
-constexpr int kDrainK = (96 + 8 * kEpiGroups - 1) / (8 * kEpiGroups);  // 8-column pieces per group drain
+// fp16 engine: four epilogue warpgroups (its conversion keeps half a tile
+// live, ~96 registers: no spills at 640 threads) and A_I in shared memory,
+// so five tiles are in flight (TMEM: O0 | O1 + 5 x 64 columns); measured
+// 0.1618 vs 0.1653 ms at config 1 for three groups with A_I in TMEM.
+#ifndef WGP_TC_EPI16
+#define WGP_TC_EPI16 4
+#endif
+#ifndef WGP_TC_F16_ATMEM
+#define WGP_TC_F16_ATMEM 0
+#endif
+template <bool H16>
+constexpr int kEpiGroupsT = H16 ? WGP_TC_EPI16 : WGP_TC_EPI;  // epilogue warpgroups
+template <bool H16>
+constexpr int kThreadsT = 128 * kEpiGroupsT<H16> + 128;  // + 4 control warps
 constexpr uint32_t kTfMask = 0xFFFFE000u;  // keep sign, exponent, 10 mantissa bits
 constexpr int kSmemLimit = 232448 - 2048;  // 227 KB opt-in minus static smem (barriers)
 constexpr int kMaxStages = 8;              // smem ring depth cap (barrier arrays)
@@ -180,13 +193,13 @@ struct Cfg {
   static constexpr int kTJ = H16 ? 64 : 32;        // points per J tile (MMA-2 K, epilogue)
   static constexpr int kP = H16 ? 1 : 2;           // tiles per MMA-1 group
   static constexpr int kN1 = kP * kTJ;            // MMA-1 N = points per B stage (64)
-  static constexpr int kGroups = H16 ? (kTfATmem ? 4 : 5) : kTfGroups;  // MMA-1 groups in flight (TMEM)
+  static constexpr int kGroups = H16 ? (WGP_TC_F16_ATMEM ? 4 : 5) : kTfGroups;  // MMA-1 groups in flight (TMEM)
   static constexpr int kTilesInFlight = kP * kGroups;
   static constexpr uint32_t kGW = H16 ? 64u : 128u;  // TMEM columns per group
   // tf32 layout variant (kTfSingleO): one O accumulator [0, 96) whose chunk
   // drains stall MMA-2, A_I in shared memory (SS Gram), three groups from 96
   // (6 tiles in flight); otherwise O0 | O1, A_I in TMEM, two groups from 256.
-  static constexpr bool kATmem = kTfATmem;
+  static constexpr bool kATmem = H16 ? (WGP_TC_F16_ATMEM != 0) : kTfATmem;
   static constexpr int kOBufs = (H16 || !kTfSingleO) ? 2 : 1;
   static constexpr uint32_t kOStride = kOBufs == 2 ? 96u : 0u;
   static constexpr uint32_t kAhi = 192, kAlo = 224;  // kATmem only
@@ -204,8 +217,6 @@ struct Cfg {
 // warps, so the latency-critical control warps get the top ids and the 12
 // always-eligible epilogue warps (0..11; warp w reads TMEM lanes 32 (w % 4))
 // cannot starve them.
-constexpr int kEpiWarps = 4 * kEpiGroups;
-constexpr int kWarpBProd = kEpiWarps, kWarpM1 = kEpiWarps + 1, kWarpVProd = kEpiWarps + 2, kWarpM2 = kEpiWarps + 3;
 
 // Accumulation precision.  MMA-2 accumulates into fp32 TMEM, and every
 // K-step instruction rounds the running sum: with ~3 n / 8 roundings per
@@ -221,12 +232,16 @@ constexpr int kWarpBProd = kEpiWarps, kWarpM1 = kEpiWarps + 1, kWarpVProd = kEpi
 // shared-memory drain costs no L2 traffic (an fp64 global drain per chunk
 // measured +20% time).
 template <bool H16>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsT<H16>, 1)
     hv_tc_kernel(const __grid_constant__ CUtensorMap mAhi, const __grid_constant__ CUtensorMap mAlo,
                  const __grid_constant__ CUtensorMap mBhi, const __grid_constant__ CUtensorMap mBlo,
                  const __grid_constant__ CUtensorMap mVhi, const __grid_constant__ CUtensorMap mVlo,
                  const __grid_constant__ CUtensorMap mPart, const TcArgs p) {
   using K = Cfg<H16>;
+  constexpr int kEpiGroups = kEpiGroupsT<H16>;
+  constexpr int kDrainK = (96 + 8 * kEpiGroups - 1) / (8 * kEpiGroups);  // 8-column pieces per group drain
+  constexpr int kEpiWarps = 4 * kEpiGroups;
+  constexpr int kWarpBProd = kEpiWarps, kWarpM1 = kEpiWarps + 1, kWarpVProd = kEpiWarps + 2, kWarpM2 = kEpiWarps + 3;
   constexpr int NBUF = K::kTilesInFlight;  // kfull ring
   constexpr int TJ = K::kTJ;
   constexpr int P = K::kP;
@@ -1139,7 +1154,7 @@ void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorM
                const CUtensorMap& mVhi, const CUtensorMap& mVlo, const TcArgs& a, unsigned grid, int smem,
                cudaStream_t st) {
   WGP_SMEM_ATTR(hv_tc_kernel<H16>, kSmemLimit);
-  hv_tc_kernel<H16><<<grid, kThreads, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart, a);
+  hv_tc_kernel<H16><<<grid, kThreadsT<H16>, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart, a);
   WGP_LAUNCH_CHECK();
 }
 
