@@ -7,7 +7,7 @@ import paper_2405_18328_b200 as wg  # noqa: E402
 from paper_2405_18328_b200 import datasets  # noqa: E402
 
 p = datasets.config3()
-ctx = wg.Context(0)
+ctx = wg.Context(0, hv_impl=os.environ.get("HV_IMPL", "tc"))
 ctx.set_data(p.X)
 cfg = wg.TrainConfig(steps=1, learning_rate=0.1, num_probes=64, mode="warm", seed=0, transform="log",
                      estimator="pathwise", rff_features=1000, init_noise=0.5, init_constrained=1.0,
