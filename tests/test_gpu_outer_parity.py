@@ -37,18 +37,26 @@ def ctx():
     c.close()
 
 
-@pytest.mark.parametrize("name", CASES)
-def test_outer_loop_matches_oracle(ctx, name):
+# AP and SGD (and the gradient) also on the fp16x3 K.V engine bench.py times them with
+ENGINE_CASES = [(name, "tc") for name in CASES] + [(name, "tc_f16") for name in ("c2_sgd", "c2_ap", "c3_ap_n20000")]
+
+
+@pytest.mark.parametrize("name,engine", ENGINE_CASES)
+def test_outer_loop_matches_oracle(ctx, name, engine):
     g = load(name)
     case = g["config"]
     gen = datasets.CONFIGS[case["config"]]
     p = gen(n=case["n"]) if "n" in case else gen()
+    ctx.set_hv_impl(engine)
     ctx.set_data(p.X)
     cfg = wg.TrainConfig(steps=case["steps"], learning_rate=0.1, num_probes=64, mode="warm", seed=0,
                          transform="log", estimator="pathwise", rff_features=case.get("rff_features", 1000),
                          init_noise=0.5,
                          init_constrained=1.0, warm_start_distance=True, solver=wg.SolverConfig(**case["solver"]))
-    tr = ctx.train(p.y, cfg)
+    try:
+        tr = ctx.train(p.y, cfg)
+    finally:
+        ctx.set_hv_impl("tc")
     theta = np.array([r.constrained_params for r in tr.steps])
     ref = np.array(g["constrained_params"])
     assert np.max(np.abs(theta - ref) / np.abs(ref)) <= 1e-3

@@ -192,11 +192,15 @@ def kernel_problem(n, d, s, seed, sigma=0.5):
     return X, ls, 1.1, sigma, rhs
 
 
-@pytest.mark.parametrize("kind,extra,prec", [("cg", {}, "f64"), ("cg", {}, "f32"), ("ap", dict(block_size=200), "f64"),
-                                             ("sgd", dict(minibatch_size=200, learning_rate=3.0,
-                                                          momentum=0.9), "f64")])
-def test_solvers_match_oracle(ctx, kind, extra, prec):
+SOLVER_CASES = [("cg", {}, "f64"), ("cg", {}, "f32"), ("ap", dict(block_size=200), "f64"),
+                ("sgd", dict(minibatch_size=200, learning_rate=3.0, momentum=0.9), "f64")]
+
+
+@pytest.mark.parametrize("engine", ["tc", "tc_f16"])
+@pytest.mark.parametrize("kind,extra,prec", SOLVER_CASES)
+def test_solvers_match_oracle(ctx, kind, extra, prec, engine):
     X, ls, sf, sig, rhs = kernel_problem(1000, 8, 5, seed=11)
+    ctx.set_hv_impl(engine)
     ctx.set_data(X)
     ctx.set_hyper([*ls, sf, sig])
     ctx.set_cg_precision(prec)
@@ -205,6 +209,7 @@ def test_solvers_match_oracle(ctx, kind, extra, prec):
         g = ctx.solve(rhs, wg.SolverConfig(**cfg))
     finally:
         ctx.set_cg_precision("f64")
+        ctx.set_hv_impl("tc")
     o = orc.solve(rhs, orc.SolverConfig(**cfg), X=X, ls=ls, sf=sf, sigma=sig)
     assert g.all_converged() and o.all_converged()
     ref_it = o.iterations_used
