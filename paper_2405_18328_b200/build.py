@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libwarmgp_b200.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["hv_simt.cu", "hv_tc.cu", "hv_f64.cu", "grad_rff.cu", "grad_tc.cu", "solver_kernels.cu", "exact.cu", "predict.cu", "runtime.cu"]
+SOURCES = ["hv_simt.cu", "hv_tc.cu", "hv_f64.cu", "hv_i8.cu", "grad_rff.cu", "grad_tc.cu", "solver_kernels.cu", "exact.cu", "predict.cu", "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -25,6 +25,8 @@
 // summed in split order by hv64_reduce (deterministic, no atomics).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "hv_f64.cuh"
@@ -291,8 +293,20 @@ int hv64_splits(int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(smax, wave / rt)));
 }
 
+// The operator engine: the exact integer-slice product on the int8 tensor
+// core (hv_i8.cu) where it applies, else the DMMA kernel below;
+// WGP_HV64_ENGINE=dmma keeps the DMMA kernel (A/B).
+static bool use_i8(int d, int s) {
+  static const bool dmma = [] {
+    const char* e = getenv("WGP_HV64_ENGINE");
+    return e && std::string(e) == "dmma";
+  }();
+  return !dmma && hv_i8_supported(d, s);
+}
+
 size_t hv64_workspace_bytes(int64_t n, int64_t m, int s) {
-  return sizeof(double) * static_cast<size_t>(hv64_splits(n)) * s * round_up(m, TM);
+  return std::max(sizeof(double) * static_cast<size_t>(hv64_splits(n)) * s * round_up(m, TM),
+                  hv_i8_workspace_bytes(n, m, std::min(s, 8 * kMaxNF)));
 }
 
 static void hv64_launch(const Hv64Params& p, cudaStream_t st, bool reduce, int* splits_out, int64_t* m_pad_out) {
@@ -308,10 +322,20 @@ static void hv64_launch(const Hv64Params& p, cudaStream_t st, bool reduce, int* 
     }
     return;
   }
+  int splits = 0;
+  int64_t m_pad = 0;
+  if (use_i8(p.d, p.s) && hv_i8_partials(p, st, &splits, &m_pad)) {
+    if (splits_out) *splits_out = splits;
+    if (m_pad_out) *m_pad_out = m_pad;
+    if (!reduce) return;
+    hv64_reduce_kernel<<<dim3(static_cast<unsigned>(ceil_div(p.m, 256)), p.s), 256, 0, st>>>(p, m_pad, splits);
+    WGP_LAUNCH_CHECK();
+    return;
+  }
   if ((p.ldv & 1) || (reinterpret_cast<uintptr_t>(p.V) & 15) || (p.dp & 3))
     throw std::invalid_argument("hv64: V needs an even leading dimension and 16-byte alignment");
-  const int splits = hv64_splits(p.n);
-  const int64_t m_pad = round_up(p.m, TM);
+  splits = hv64_splits(p.n);
+  m_pad = round_up(p.m, TM);
   switch ((p.s + 7) / 8) {
     case 1: launch<1>(p, m_pad, splits, st); break;
     case 2: launch<2>(p, m_pad, splits, st); break;

@@ -30,6 +30,11 @@ struct Hv64Params {
 int hv64_splits(int64_t n);
 size_t hv64_workspace_bytes(int64_t n, int64_t m, int s);  // per launch of <= 80 columns
 void hv64(const Hv64Params& p, cudaStream_t st);
+// Exact integer-slice engine (hv_i8.cu): d <= 16, s <= 80; writes the fp64
+// split partials into p.part (hv_i8_workspace_bytes: partials + V byte images).
+bool hv_i8_supported(int d, int s);
+size_t hv_i8_workspace_bytes(int64_t n, int64_t m, int s);
+bool hv_i8_partials(const Hv64Params& p, cudaStream_t st, int* splits, int64_t* m_pad);
 // The kernel only (s <= 80 columns): p.part holds the fp64 split partials
 // part[(k s + c) m_pad + r], k < *splits, for the caller to sum in split
 // order (cg_fused_cl); false (nothing launched) for wider V.

@@ -1,0 +1,482 @@
+// hv_i8.cu — the fp64 CG operator as an exact integer-slice product on the
+// 5th-generation tensor core (tcgen05.mma kind::i8, int32 accumulation).
+//
+// What it computes: the same fixed symmetric linear map as hv_f64.cu's DMMA
+// engine, H V with entries k_ij from direct coordinate differences (bitwise
+// symmetric) -- but K.V is done exactly in integers instead of in fp64:
+//   * entries: k_ij in fp32 bit for bit as the DMMA engine forms them, as the
+//     39-bit integer K_ij = rint(k_ij 2^eK) (sf^2 2^eK in [2^38, 2^39)): k_ij
+//     itself for k_ij >= sf^2 2^-15, within 2^-39 sf^2 below -- the same
+//     FIXED symmetric operator up to those tiny entries (fixed
+//     symmetric perturbations cost CG nothing; noise that is not a fixed
+//     linear map does), split into four unsigned bytes K = sum_i K_i 256^i;
+//   * V: each column scaled by a power of two 2^e_c so its max |v| lands in
+//     [2^53, 2^54), rounded to an integer (2^-53 of the column max) and split
+//     into seven balanced signed bytes V = sum_j V_j 256^j;
+//   * K.V = sum_ij 256^(i+j) K_i V_j: every byte product is exact and every
+//     int32 accumulation is exact (drained to fp64 every 128 tiles, before it
+//     could overflow).  Classes i + j = 5..10 are kept (20 byte pairs); the
+//     dropped classes 0..4 weigh < 2^-44 of the result.  So the product is
+//     linear in V to ~1e-12 and deterministic.
+// The 20 pairs x 2 K steps are 40 kind::i8 MMAs (M = 128, N = s padded to 16,
+// K = 32) per 64-point tile into six int32 accumulators in TMEM (6 x N <= 480
+// columns); the int8 tensor rate (~4.5 POPS) makes that ~6x cheaper than the
+// fp64 tensor core's 37 TF/s for the same product.
+//
+// Warp roles (320 threads): warps 0..7 evaluate the entries (warp w: rows
+// 32 (w % 4) .. +31 = its TMEM lane quarter, points 32 (w / 4) .. +31 of each
+// tile) and write K's bytes into the 128-byte-swizzled K-major A operand in
+// shared memory, and drain the accumulators into the fp64 split partials;
+// warp 8 streams the per-tile V byte images (pre-swizzled by i8_vimg_kernel)
+// and the points' coordinates with 1-D bulk copies; warp 9 issues the MMAs.
+// Output: fp64 split partials in hv64's layout (hv64_reduce_kernel / the
+// CG fold add the diagonal and sum the splits in order).
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "hv_f64.cuh"
+#include "tc_ptx.cuh"
+
+namespace wgp {
+namespace {
+
+constexpr int TI = 128;          // output rows per CTA (MMA M, TMEM lanes)
+constexpr int TJ = 64;           // points per tile (two K steps of 32 bytes)
+constexpr int kNCls = 6;         // accumulator classes i + j = 5 .. 10
+constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (4 x 64 x 255 x 128))
+constexpr int kMaxD = 16;        // coordinates kept in registers
+constexpr int NBK = 2, NV = 3;   // K buffers, V / coordinate stages
+constexpr int kEpiWarps = 8, kWarpProd = 8, kWarpMma = 9, kThreads = 320;
+constexpr int kNKB = 5;                            // K bytes (39-bit K)
+constexpr uint32_t kKBuf = 3u * TI * 128u;  // K planes [K0 | K1], [K2 | K3], [K4 | -]: 48 KB
+
+__host__ __device__ inline uint32_t vstage_bytes(int spad) { return 3u * static_cast<uint32_t>(spad) * 128u; }
+
+struct I8Args {
+  const float* xs;     // [n_pad][dp] prepared points
+  const float* xtile;  // [num_jt][D][64] the tiles' points, negated, coordinate-major
+  int dp, d;
+  int64_t n, r0, m;  // contracted points, first output row (global), rows
+  int num_jt, splits, s, spad;
+  const uint8_t* vimg;   // [num_jt][3][spad][128] swizzled V byte images
+  const double* vscale;  // [s] 2^-e_c
+  const float* hyp;      // device [sf2, a, diag]
+  double* part;          // [splits][s][m_pad] fp64 partials
+  int64_t m_pad;
+  const int* done;
+};
+
+// 36 MMAs of one tile: pairs (i, j), i + j >= 4, K byte i (plane i / 2, half
+// i % 2) times V byte j (plane (j - 1) / 2, half (j - 1) % 2) into class
+// i + j - 4; two K steps (+32 bytes) each.  a0 / a1: K plane descriptors, b0..b2:
+// V plane descriptors, d: TMEM base, cs: class stride (columns), acc: 0 for the
+// first tile of a chunk (each class's first MMA overwrites).
+__device__ __forceinline__ void mma_tile_i8(uint32_t d, uint64_t a0, uint64_t a1, uint64_t a2, uint64_t b0,
+                                            uint64_t b1, uint64_t b2, uint32_t cs, uint32_t idesc, uint32_t acc) {
+  const uint64_t A[3] = {a0, a1, a2}, B[3] = {b0, b1, b2};
+  bool first[kNCls] = {true, true, true, true, true, true};
+#pragma unroll
+  for (int i = 0; i < kNKB; ++i)
+#pragma unroll
+    for (int j = 1; j < 7; ++j) {
+      if (i + j < 5) continue;
+      const int c = i + j - 5;
+      const uint64_t a = A[i / 2] + static_cast<uint64_t>(4 * (i % 2));
+      const uint64_t b = B[(j - 1) / 2] + static_cast<uint64_t>(4 * ((j - 1) % 2));
+      const uint32_t dc = d + cs * static_cast<uint32_t>(c);
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint32_t en = (first[c] && ks == 0) ? acc : 1u;
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+            " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dc),
+            "l"(a + 2 * ks), "l"(b + 2 * ks), "r"(idesc), "r"(en));
+      }
+      first[c] = false;
+    }
+}
+
+__device__ __forceinline__ void commit_one(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
+  if (p.done && *p.done) return;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t vsb = vstage_bytes(p.spad);
+  uint8_t* sK = smem;                                  // NBK x 32 KB
+  uint8_t* sV = sK + NBK * kKBuf;                      // NV x vsb (multiples of 1024)
+  float* sX = reinterpret_cast<float*>(sV + NV * vsb); // NV x [D][TJ] negated coordinates
+  __shared__ __align__(8) uint64_t bar_vfull[NV], bar_kfull[NBK], bar_mdone[8], bar_ofull, bar_odrained;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row_tiles = static_cast<int>(gridDim.x) / p.splits;
+  const int rt = blockIdx.x % row_tiles, sp = blockIdx.x / row_tiles;  // split-major (L2)
+  const int jt0 = static_cast<int>(static_cast<int64_t>(p.num_jt) * sp / p.splits);
+  const int T = static_cast<int>(static_cast<int64_t>(p.num_jt) * (sp + 1) / p.splits) - jt0;
+  constexpr uint32_t xbytes = static_cast<uint32_t>(TJ * D * 4);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NV; ++i) mbar_init(&bar_vfull[i], 1);
+    for (int i = 0; i < NBK; ++i) mbar_init(&bar_kfull[i], kEpiWarps);
+    for (int i = 0; i < 8; ++i) mbar_init(&bar_mdone[i], 1);
+    mbar_init(&bar_ofull, 1);
+    mbar_init(&bar_odrained, kEpiWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kWarpProd) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == kWarpProd) {
+    // -------------------------------------------------------------- producer
+    for (int t = 0; t < T; ++t) {
+      const int st = t % NV;
+      if (t >= NV) mbar_wait(&bar_mdone[(t - NV) & 7], ((t - NV) >> 3) & 1);
+      mbar_expect_tx_warp(&bar_vfull[st], vsb + xbytes);
+      const int64_t jt = jt0 + t;
+      bulk_load_warp(sV + st * vsb, p.vimg + jt * vsb, vsb, &bar_vfull[st]);
+      bulk_load_warp(sX + st * TJ * D, p.xtile + jt * TJ * D, xbytes, &bar_vfull[st]);
+    }
+  } else if (warp == kWarpMma) {
+    // -------------------------------------------------------------- MMA issuer
+    const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | (static_cast<uint32_t>(p.spad >> 3) << 17) |
+                           (static_cast<uint32_t>(TI >> 4) << 24);  // D s32, A u8, B s8, K-major
+    int nd = 0;  // drains completed (chunks)
+    for (int t = 0; t < T; ++t) {
+      const int b = t % NBK, st = t % NV;
+      if (t > 0 && t % kChunk == 0) {  // the accumulators were drained
+        mbar_wait(&bar_odrained, nd & 1);
+        ++nd;
+      }
+      mbar_wait(&bar_kfull[b], (t / NBK) & 1);
+      mbar_wait(&bar_vfull[st], (t / NV) & 1);
+      tc_after();
+      const uint8_t* kb = sK + b * kKBuf;
+      const uint8_t* vb = sV + st * vsb;
+      const uint32_t pv = static_cast<uint32_t>(p.spad) * 128u;
+      // lane 0 issues the tile's MMAs and the commits that track them
+      if (lane == 0) {
+        mma_tile_i8(tmem, umma_desc(kb), umma_desc(kb + TI * 128), umma_desc(kb + 2 * TI * 128), umma_desc(vb),
+                    umma_desc(vb + pv),
+                    umma_desc(vb + 2 * pv), static_cast<uint32_t>(p.spad), idesc, t % kChunk != 0 ? 1u : 0u);
+        commit_one(&bar_mdone[t & 7]);
+        if ((t + 1) % kChunk == 0 || t == T - 1) commit_one(&bar_ofull);
+      }
+      __syncwarp();
+    }
+  } else {
+    // -------------------------------------------------------------- entries + drains
+    const int q = warp & 3, h = warp >> 2;
+    const int r = 32 * q + lane;  // row in the tile = TMEM lane
+    const int64_t lr = static_cast<int64_t>(rt) * TI + r;
+    const int64_t g = p.r0 + lr;  // global row (n_pad rows of xs exist)
+    // (x_ik, x_ik) pairs: x_i - x_j for two points per FADD2 against the
+    // tile's negated coordinates; (x_i - x_j)^2 = (x_j - x_i)^2 exactly and
+    // the sum runs k = 0..D-1 for both orders, so K is bitwise symmetric
+    float2 xi2[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const float v = p.xs[g * p.dp + k];
+      xi2[k] = make_float2(v, v);
+    }
+    const uint32_t lanes = static_cast<uint32_t>(32 * q) << 16;
+    // k_ij = (sf^2 + a u) 2^-u in fp32 exactly as the DMMA engine forms it,
+    // then scaled by 2^eK (exact), sf^2 2^eK in [2^30, 2^31): K_ij is k_ij
+    // itself for k_ij >= sf^2 2^-7 and within 2^-31 sf^2 below
+    const float hsf2 = p.hyp[0], ha = p.hyp[1];
+    const int eK = 38 - (static_cast<int>((__float_as_uint(hsf2) >> 23) & 255u) - 127);
+    const float kscale = __int_as_float((127 + eK) << 23);
+    const double oscale = ldexp(1.0, -eK);
+    int nd = 0;
+    for (int t = 0; t < T; ++t) {
+      const int b = t % NBK, st = t % NV;
+      mbar_wait(&bar_vfull[st], (t / NV) & 1);
+      if (t >= NBK) mbar_wait(&bar_mdone[(t - NBK) & 7], ((t - NBK) >> 3) & 1);  // K buffer b is free
+      const float* xt = sX + st * TJ * D + 32 * h;  // [k][64] negated, this warp's 32 points
+      const int64_t pbase = static_cast<int64_t>(jt0 + t) * TJ + 32 * h;  // this warp's first point
+      // warp-uniform: do any of the warp's entries need zeroing?
+      const bool edge = pbase + 32 > p.n || __any_sync(0xffffffffu, g >= pbase && g < pbase + 32);
+      uint32_t w[kNKB][8];  // digit i: 32 bytes = 8 words (points 4 c .. 4 c + 3)
+#pragma unroll
+      for (int grp = 0; grp < 4; ++grp) {  // 8 points at a time, packed in pairs
+        float2 r2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const float4 a = *reinterpret_cast<const float4*>(xt + k * TJ + 8 * grp);
+          const float4 c = *reinterpret_cast<const float4*>(xt + k * TJ + 8 * grp + 4);
+          const float2 d0 = __fadd2_rn(xi2[k], make_float2(a.x, a.y));
+          const float2 d1 = __fadd2_rn(xi2[k], make_float2(a.z, a.w));
+          const float2 d2 = __fadd2_rn(xi2[k], make_float2(c.x, c.y));
+          const float2 d3 = __fadd2_rn(xi2[k], make_float2(c.z, c.w));
+          r2[0] = __ffma2_rn(d0, d0, r2[0]);
+          r2[1] = __ffma2_rn(d1, d1, r2[1]);
+          r2[2] = __ffma2_rn(d2, d2, r2[2]);
+          r2[3] = __ffma2_rn(d3, d3, r2[3]);
+        }
+        uint32_t K[8], KH[8];  // low 32 bits, bits 32..38
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float rr = (e & 1) ? r2[e >> 1].y : r2[e >> 1].x;
+          const float u = sqrt_approx(rr);
+          const float kp = matern_from_u(u, hsf2, ha) * kscale;
+          unsigned long long kv;
+          asm("cvt.rni.sat.u64.f32 %0, %1;" : "=l"(kv) : "f"(kp));
+          K[e] = static_cast<uint32_t>(kv);
+          KH[e] = static_cast<uint32_t>(kv >> 32);
+        }
+        if (edge) {  // the diagonal (H_ii V_i is added exactly in the reduction) and points >= n
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int64_t gj = pbase + 8 * grp + e;
+            if (gj >= p.n || gj == g) K[e] = KH[e] = 0u;
+          }
+        }
+        // 4 x 4 byte transposes: w[i][.] holds byte i of 4 consecutive points
+#pragma unroll
+        for (int hq = 0; hq < 2; ++hq) {
+          const uint32_t t0 = __byte_perm(K[4 * hq], K[4 * hq + 1], 0x5140);
+          const uint32_t t1 = __byte_perm(K[4 * hq], K[4 * hq + 1], 0x7362);
+          const uint32_t t2 = __byte_perm(K[4 * hq + 2], K[4 * hq + 3], 0x5140);
+          const uint32_t t3 = __byte_perm(K[4 * hq + 2], K[4 * hq + 3], 0x7362);
+          w[0][2 * grp + hq] = __byte_perm(t0, t2, 0x5410);
+          w[1][2 * grp + hq] = __byte_perm(t0, t2, 0x7632);
+          w[2][2 * grp + hq] = __byte_perm(t1, t3, 0x5410);
+          w[3][2 * grp + hq] = __byte_perm(t1, t3, 0x7632);
+          w[4][2 * grp + hq] = __byte_perm(__byte_perm(KH[4 * hq], KH[4 * hq + 1], 0x0040),
+                                           __byte_perm(KH[4 * hq + 2], KH[4 * hq + 3], 0x0040), 0x5410);
+        }
+      }
+      // K bytes -> the A operand: plane i / 2, byte (i % 2) 64 + 32 h + point,
+      // 16-byte chunk c at (c ^ (r % 8)) in the row (128-byte swizzle)
+      uint8_t* kb = sK + b * kKBuf + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+      for (int i = 0; i < kNKB; ++i)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = 4 * (i % 2) + 2 * h + u;
+          uint4 v = make_uint4(w[i][4 * u], w[i][4 * u + 1], w[i][4 * u + 2], w[i][4 * u + 3]);
+          *reinterpret_cast<uint4*>(kb + (i / 2) * (TI * 128) + ((c ^ (r & 7)) << 4)) = v;
+        }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_kfull[b]);
+      if ((t + 1) % kChunk == 0 || t == T - 1) {
+        // drain: class sums -> fp64, this warp's half of the columns
+        mbar_wait(&bar_ofull, nd & 1);
+        tc_after();
+        const int half = p.spad / 2;
+#pragma unroll 1
+        for (int c0 = h * half; c0 < (h + 1) * half; c0 += 8) {
+          uint32_t cv[kNCls][8];
+#pragma unroll
+          for (int c = 0; c < kNCls; ++c) tmem_ld8(tmem + lanes + static_cast<uint32_t>(c * p.spad + c0), cv[c]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int col = c0 + e;
+            double v = 0.0;
+#pragma unroll
+            for (int c = kNCls - 1; c >= 0; --c)  // high classes first, fixed order
+              v += ldexp(static_cast<double>(static_cast<int>(cv[c][e])), 8 * (c + 5));
+            if (col < p.s && lr < p.m) {
+              double* dst = p.part + (static_cast<int64_t>(sp) * p.s + col) * p.m_pad + lr;
+              const double val = v * p.vscale[col] * oscale;
+              *dst = nd == 0 ? val : *dst + val;
+            }
+          }
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_odrained);
+        ++nd;
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == kWarpProd) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// Per column: max |v| (fp64 bits are monotone in |v|) -> colbits[c].
+__global__ void i8_colmax_kernel(const double* V, int64_t ldv, int64_t n, unsigned long long* colbits) {
+  const int c = blockIdx.y;
+  unsigned long long m = 0ull;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = max(m, static_cast<unsigned long long>(__double_as_longlong(V[j + c * ldv])) & 0x7FFFFFFFFFFFFFFFull);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(colbits + c, m);
+}
+
+// Column exponent: max |v| 2^e in [2^53, 2^54) (e = 0 for a zero or
+// non-finite column: its digits are then 0 / garbage-free, see below).
+__device__ __forceinline__ int col_exp(unsigned long long mbits) {
+  const double m = __longlong_as_double(static_cast<long long>(mbits));
+  if (!(m > 0.0) || !isfinite(m)) return 0;
+  int E;
+  frexp(m, &E);  // m = f 2^E, f in [0.5, 1)
+  return max(-1000, min(1000, 54 - E));
+}
+
+// V -> per-tile byte images [num_jt][3][spad][128], each 3 x spad rows of
+// 128 bytes = [byte 2q + 1 | byte 2q + 2] of 64 points, 16-byte chunks at
+// (chunk ^ (row % 8)) (the UMMA 128-byte swizzle, K-major B operand), plus
+// vscale[c] = 2^-e_c.  One thread per 16-byte chunk.
+__global__ void i8_vimg_kernel(const double* V, int64_t ldv, int64_t n, int s, int spad, int num_jt,
+                               const unsigned long long* colbits, uint8_t* img, double* vscale) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t per_tile = 3LL * spad * 8;
+  if (idx >= per_tile * num_jt) return;
+  const int64_t t = idx / per_tile;
+  const int rem = static_cast<int>(idx - t * per_tile);
+  const int plane = rem / (spad * 8), row = (rem / 8) % spad, chunk = rem % 8;
+  const int c = row;
+  const int digit = 2 * plane + 1 + (chunk >= 4 ? 1 : 0);
+  const int p0 = 16 * (chunk & 3);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  if (c < s) {
+    const int e = col_exp(colbits[c]);
+    const double sc = ldexp(1.0, e);
+    if (t == 0 && plane == 0 && chunk == 0) vscale[c] = ldexp(1.0, -e);
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+      const int64_t j = t * TJ + p0 + k;
+      int dv = 0;
+      if (j < n) {
+        const double x = V[j + c * ldv] * sc;
+        long long vi = isfinite(x) ? __double2ll_rn(x) : 0ll;
+#pragma unroll 1
+        for (int q = 0; q <= digit; ++q) {  // balanced base-256 digits, least significant first
+          const int dq = static_cast<int>(static_cast<signed char>(vi & 0xFF));
+          vi = (vi - dq) >> 8;
+          dv = dq;
+        }
+      }
+      w[k / 4] |= (static_cast<uint32_t>(dv) & 0xFFu) << (8 * (k % 4));
+    }
+  }
+  uint8_t* dst = img + t * (3LL * spad * 128) + static_cast<int64_t>(plane) * spad * 128 + (row >> 3) * 1024 +
+                 (row & 7) * 128 + ((chunk ^ (row & 7)) << 4);
+  *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// xtile[t][k][p] = -xs[64 t + p][k] (points past n_pad read as zero rows of
+// xs' padding; the entries of points >= n are zeroed in the kernel anyway).
+__global__ void i8_xtile_kernel(const float* xs, int dp, int d, int64_t n_pad, int num_jt, float* xtile) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(num_jt) * d * TJ) return;
+  const int64_t t = idx / (d * TJ);
+  const int k = static_cast<int>((idx / TJ) % d), pt = static_cast<int>(idx % TJ);
+  const int64_t j = t * TJ + pt;
+  xtile[idx] = j < n_pad ? -xs[j * dp + k] : 0.f;
+}
+
+int i8_splits(int64_t n) {
+  // keyed on the global n (row shards reproduce the full operator's rows):
+  // whole waves of 148 CTAs, >= 4 tiles per split
+  const int64_t rt = ceil_div(n, TI), nt = ceil_div(n, TJ);
+  const int64_t wave = 148;
+  const int64_t smax = std::max<int64_t>(1, nt / 4);
+  for (int64_t s = 1; s <= smax; ++s) {
+    const int64_t ctas = rt * s;
+    if (ctas < wave) continue;
+    const double waves = static_cast<double>(ctas) / wave;
+    if (waves / std::ceil(waves) >= 0.85) return static_cast<int>(s);
+  }
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(smax, wave / rt)));
+}
+
+}  // namespace
+
+bool hv_i8_supported(int d, int s) { return d >= 1 && d <= kMaxD && s >= 1 && s <= 80; }
+
+size_t hv_i8_workspace_bytes(int64_t n, int64_t m, int s) {
+  const int spad = static_cast<int>(round_up(s, 16));
+  const size_t part = sizeof(double) * static_cast<size_t>(i8_splits(n)) * s * round_up(m, TI);
+  const size_t img = static_cast<size_t>(ceil_div(n, TJ)) * vstage_bytes(spad);
+  const size_t xt = sizeof(float) * static_cast<size_t>(ceil_div(n, TJ)) * kMaxD * TJ;
+  return round_up(part, 1024) + round_up(img, 1024) + 2 * 8 * 128 + round_up(xt, 1024);
+}
+
+bool hv_i8_partials(const Hv64Params& hp, cudaStream_t st, int* splits_out, int64_t* m_pad_out) {
+  if (!hv_i8_supported(hp.d, hp.s) || hp.m <= 0) return false;
+  const int s = hp.s, spad = static_cast<int>(round_up(s, 16));
+  const int num_jt = static_cast<int>(ceil_div(hp.n, TJ));
+  const int splits = i8_splits(hp.n);
+  const int64_t m_pad = round_up(hp.m, TI);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(hp.part);
+  const size_t part_b = round_up(sizeof(double) * static_cast<size_t>(splits) * s * m_pad, 1024);
+  uint8_t* img = ws + part_b;
+  const size_t img_b = round_up(static_cast<size_t>(num_jt) * vstage_bytes(spad), 1024);
+  auto* colbits = reinterpret_cast<unsigned long long*>(img + img_b);
+  double* vscale = reinterpret_cast<double*>(colbits + 128);
+  float* xtile = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(colbits) + 2 * 8 * 128);
+  {
+    const int64_t nx = static_cast<int64_t>(num_jt) * hp.d * TJ;
+    i8_xtile_kernel<<<static_cast<unsigned>(ceil_div(nx, 256)), 256, 0, st>>>(hp.xs, hp.dp, hp.d,
+                                                                             round_up(hp.n, 128), num_jt, xtile);
+    WGP_LAUNCH_CHECK();
+  }
+  WGP_CUDA(cudaMemsetAsync(colbits, 0, sizeof(unsigned long long) * 128, st));
+  i8_colmax_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(64, ceil_div(hp.n, 256))), s), 256, 0, st>>>(
+      hp.V, hp.ldv, hp.n, colbits);
+  WGP_LAUNCH_CHECK();
+  const int64_t chunks = 3LL * spad * 8 * num_jt;
+  i8_vimg_kernel<<<static_cast<unsigned>(ceil_div(chunks, 256)), 256, 0, st>>>(hp.V, hp.ldv, hp.n, s, spad, num_jt,
+                                                                             colbits, img, vscale);
+  WGP_LAUNCH_CHECK();
+  I8Args a{};
+  a.xs = hp.xs;
+  a.xtile = xtile;
+  a.dp = hp.dp;
+  a.d = hp.d;
+  a.n = hp.n;
+  a.r0 = hp.r0;
+  a.m = hp.m;
+  a.num_jt = num_jt;
+  a.splits = splits;
+  a.s = s;
+  a.spad = spad;
+  a.vimg = img;
+  a.vscale = vscale;
+  a.hyp = hp.hyp;
+  a.part = hp.part;
+  a.m_pad = m_pad;
+  a.done = hp.done;
+  const int smem = 1024 + NBK * static_cast<int>(kKBuf) + NV * static_cast<int>(vstage_bytes(spad)) +
+                   NV * TJ * hp.d * 4;
+  const unsigned grid = static_cast<unsigned>(ceil_div(hp.m, TI) * splits);
+  switch (hp.d) {
+#define WGP_I8_CASE(D)                                            \
+  case D:                                                         \
+    WGP_SMEM_ATTR(hv_i8_kernel<D>, 200 * 1024);                   \
+    hv_i8_kernel<D><<<grid, kThreads, smem, st>>>(a);             \
+    break;
+    WGP_I8_CASE(1) WGP_I8_CASE(2) WGP_I8_CASE(3) WGP_I8_CASE(4) WGP_I8_CASE(5) WGP_I8_CASE(6) WGP_I8_CASE(7)
+    WGP_I8_CASE(8) WGP_I8_CASE(9) WGP_I8_CASE(10) WGP_I8_CASE(11) WGP_I8_CASE(12) WGP_I8_CASE(13)
+    WGP_I8_CASE(14) WGP_I8_CASE(15) WGP_I8_CASE(16)
+#undef WGP_I8_CASE
+    default:
+      return false;
+  }
+  WGP_LAUNCH_CHECK();
+  if (splits_out) *splits_out = splits;
+  if (m_pad_out) *m_pad_out = m_pad;
+  return true;
+}
+
+}  // namespace wgp
