@@ -33,6 +33,7 @@
 // CG fold add the diagonal and sum the splits in order).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "hv_f64.cuh"
@@ -46,12 +47,30 @@ constexpr int TJ = 64;           // points per tile (two K steps of 32 bytes)
 constexpr int kNCls = 6;         // accumulator classes i + j = 5 .. 10
 constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (4 x 64 x 255 x 128))
 constexpr int kMaxD = 16;        // coordinates kept in registers
-constexpr int NBK = 2, NV = 3;   // K buffers, V / coordinate stages
-constexpr int kEpiWarps = 8, kWarpProd = 8, kWarpMma = 9, kThreads = 320;
+#ifndef WGP_I8_NBK
+#define WGP_I8_NBK 2
+#endif
+constexpr int NBK = WGP_I8_NBK, NV = 3;   // K buffers, V / coordinate stages
+#ifndef WGP_I8_EPI
+#define WGP_I8_EPI 16  // 16: 2.91 vs 3.16 ms per config-2 CG iteration with 8 (interleaved A/B)
+#endif
+constexpr int kEpiWarps = WGP_I8_EPI;                 // entry warps: 4 lane quarters x kEpiWarps / 4 point slices
+constexpr int kWarpProd = kEpiWarps, kWarpMma = kEpiWarps + 1, kThreads = 32 * (kEpiWarps + 2);
+constexpr int kPW = 4 * TJ / kEpiWarps;               // points per entry warp per tile (32 or 16)
+static_assert(kPW % 16 == 0, "16-byte K chunks per warp");
 constexpr int kNKB = 5;                            // K bytes (39-bit K)
-constexpr uint32_t kKBuf = 3u * TI * 128u;  // K planes [K0 | K1], [K2 | K3], [K4 | -]: 48 KB
+constexpr uint32_t kKBlk = TI * 64u;           // one K byte: 128 rows x 64 points, 64-byte swizzle
+constexpr uint32_t kKBuf = kNKB * kKBlk;       // 40 KB
 
-__host__ __device__ inline uint32_t vstage_bytes(int spad) { return 3u * static_cast<uint32_t>(spad) * 128u; }
+// V stage: bytes j = 1..6, each spad rows (columns of V) x 64 points, 64-byte
+// swizzle, stacked so that consecutive bytes form one B operand of N = L spad
+__host__ __device__ inline uint32_t vstage_bytes(int spad) { return 6u * static_cast<uint32_t>(spad) * 64u; }
+// UMMA shared-memory descriptor, K-major, 64-byte swizzle (8-row atoms of 512 bytes)
+__device__ __forceinline__ uint64_t umma_desc_sw64(const void* p) {
+  const uint32_t a = smem_u32(p);
+  return static_cast<uint64_t>((a >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(4) << 61);
+}
 
 struct I8Args {
   const float* xs;     // [n_pad][dp] prepared points
@@ -67,34 +86,37 @@ struct I8Args {
   const int* done;
 };
 
-// 36 MMAs of one tile: pairs (i, j), i + j >= 4, K byte i (plane i / 2, half
-// i % 2) times V byte j (plane (j - 1) / 2, half (j - 1) % 2) into class
-// i + j - 4; two K steps (+32 bytes) each.  a0 / a1: K plane descriptors, b0..b2:
-// V plane descriptors, d: TMEM base, cs: class stride (columns), acc: 0 for the
-// first tile of a chunk (each class's first MMA overwrites).
-__device__ __forceinline__ void mma_tile_i8(uint32_t d, uint64_t a0, uint64_t a1, uint64_t a2, uint64_t b0,
-                                            uint64_t b1, uint64_t b2, uint32_t cs, uint32_t idesc, uint32_t acc) {
-  const uint64_t A[3] = {a0, a1, a2}, B[3] = {b0, b1, b2};
-  bool first[kNCls] = {true, true, true, true, true, true};
+// One tile's MMAs: for K byte i its partner V bytes j = max(1, 5 - i) .. 6
+// are consecutive row blocks of the V stage and their classes i + j - 5
+// consecutive accumulators, so one instruction covers up to three of them
+// (N = 3 spad <= 240): 8 groups x 2 K steps = 16 MMAs per tile (20 byte
+// pairs; the A tile is read once per group instead of once per pair -- the
+// shared-memory reads of the operands bound the SS MMAs).  ka / vb: shared
+// addresses of K byte 0 and V byte 1.  The accumulators are zeroed by the
+// entry warps at the start and after every drain, so every MMA accumulates.
+__device__ __forceinline__ void mma_tile_i8(uint32_t d, const uint8_t* ka, const uint8_t* vb, int spad,
+                                            uint32_t idesc_base) {
 #pragma unroll
-  for (int i = 0; i < kNKB; ++i)
+  for (int i = 0; i < kNKB; ++i) {
+    const int j0 = 5 - i > 1 ? 5 - i : 1;
 #pragma unroll
-    for (int j = 1; j < 7; ++j) {
-      if (i + j < 5) continue;
-      const int c = i + j - 5;
-      const uint64_t a = A[i / 2] + static_cast<uint64_t>(4 * (i % 2));
-      const uint64_t b = B[(j - 1) / 2] + static_cast<uint64_t>(4 * ((j - 1) % 2));
-      const uint32_t dc = d + cs * static_cast<uint32_t>(c);
+    for (int jg = j0; jg <= 6; jg += 3) {
+      const int L = 6 - jg + 1 < 3 ? 6 - jg + 1 : 3;  // bytes in this group
+      const uint64_t a = umma_desc_sw64(ka + i * kKBlk);
+      const uint64_t b = umma_desc_sw64(vb + (jg - 1) * spad * 64);
+      const uint32_t dc = d + static_cast<uint32_t>(spad * (i + jg - 5));
+      const uint32_t idesc = idesc_base | (static_cast<uint32_t>((L * spad) >> 3) << 17);
 #pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const uint32_t en = (first[c] && ks == 0) ? acc : 1u;
-        asm volatile(
-            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-            " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dc),
-            "l"(a + 2 * ks), "l"(b + 2 * ks), "r"(idesc), "r"(en));
-      }
-      first[c] = false;
+      for (int ks = 0; ks < 2; ++ks)
+        asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;" ::"r"(dc), "l"(a + 2 * ks),
+                     "l"(b + 2 * ks), "r"(idesc));
     }
+  }
+}
+
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr), "r"(0)
+               : "memory");
 }
 
 __device__ __forceinline__ void commit_one(uint64_t* bar) {
@@ -150,26 +172,23 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
     }
   } else if (warp == kWarpMma) {
     // -------------------------------------------------------------- MMA issuer
-    const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | (static_cast<uint32_t>(p.spad >> 3) << 17) |
-                           (static_cast<uint32_t>(TI >> 4) << 24);  // D s32, A u8, B s8, K-major
-    int nd = 0;  // drains completed (chunks)
+    const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) |
+                           (static_cast<uint32_t>(TI >> 4) << 24);  // D s32, A u8, B s8, K-major (+ N per group)
+    int nz = 0;  // accumulator zeroings (the start, then after every drain)
     for (int t = 0; t < T; ++t) {
       const int b = t % NBK, st = t % NV;
-      if (t > 0 && t % kChunk == 0) {  // the accumulators were drained
-        mbar_wait(&bar_odrained, nd & 1);
-        ++nd;
+      if (t % kChunk == 0) {  // the accumulators are zero
+        mbar_wait(&bar_odrained, nz & 1);
+        ++nz;
       }
       mbar_wait(&bar_kfull[b], (t / NBK) & 1);
       mbar_wait(&bar_vfull[st], (t / NV) & 1);
       tc_after();
       const uint8_t* kb = sK + b * kKBuf;
       const uint8_t* vb = sV + st * vsb;
-      const uint32_t pv = static_cast<uint32_t>(p.spad) * 128u;
       // lane 0 issues the tile's MMAs and the commits that track them
       if (lane == 0) {
-        mma_tile_i8(tmem, umma_desc(kb), umma_desc(kb + TI * 128), umma_desc(kb + 2 * TI * 128), umma_desc(vb),
-                    umma_desc(vb + pv),
-                    umma_desc(vb + 2 * pv), static_cast<uint32_t>(p.spad), idesc, t % kChunk != 0 ? 1u : 0u);
+        mma_tile_i8(tmem, kb, vb, p.spad, idesc);
         commit_one(&bar_mdone[t & 7]);
         if ((t + 1) % kChunk == 0 || t == T - 1) commit_one(&bar_ofull);
       }
@@ -197,25 +216,43 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
     const float hsf2 = p.hyp[0], ha = p.hyp[1];
     const int eK = 38 - (static_cast<int>((__float_as_uint(hsf2) >> 23) & 255u) - 127);
     const float kscale = __int_as_float((127 + eK) << 23);
+    // (sf^2 + a u) 2^-u 2^eK = (sf^2 2^eK + a 2^eK u) 2^-u bit for bit: power-of-two scaling is exact
+    const float hsS = hsf2 * kscale, haS = ha * kscale;
     const double oscale = ldexp(1.0, -eK);
+    // zero this warp's accumulator pieces before the first MMA
+    if (T > 0) {
+#pragma unroll 1
+      for (int c0 = 8 * h; c0 < p.spad; c0 += 8 * (kEpiWarps / 4))
+#pragma unroll
+        for (int c = 0; c < kNCls; ++c) tmem_zero8(tmem + lanes + static_cast<uint32_t>(c * p.spad + c0));
+      tmem_wait_st();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_odrained);
+    }
     int nd = 0;
     for (int t = 0; t < T; ++t) {
       const int b = t % NBK, st = t % NV;
       mbar_wait(&bar_vfull[st], (t / NV) & 1);
       if (t >= NBK) mbar_wait(&bar_mdone[(t - NBK) & 7], ((t - NBK) >> 3) & 1);  // K buffer b is free
-      const float* xt = sX + st * TJ * D + 32 * h;  // [k][64] negated, this warp's 32 points
-      const int64_t pbase = static_cast<int64_t>(jt0 + t) * TJ + 32 * h;  // this warp's first point
+      const uint32_t xt_s = smem_u32(sX + st * TJ * D + kPW * h);  // [k][64] negated, this warp's points
+      const int64_t pbase = static_cast<int64_t>(jt0 + t) * TJ + kPW * h;  // this warp's first point
       // warp-uniform: do any of the warp's entries need zeroing?
-      const bool edge = pbase + 32 > p.n || __any_sync(0xffffffffu, g >= pbase && g < pbase + 32);
-      uint32_t w[kNKB][8];  // digit i: 32 bytes = 8 words (points 4 c .. 4 c + 3)
+      const bool edge = pbase + kPW > p.n || __any_sync(0xffffffffu, g >= pbase && g < pbase + kPW);
+      uint32_t w[kNKB][kPW / 4];  // digit i: kPW bytes (points 4 c .. 4 c + 3 in word c)
 #pragma unroll
-      for (int grp = 0; grp < 4; ++grp) {  // 8 points at a time, packed in pairs
+      for (int grp = 0; grp < kPW / 8; ++grp) {  // 8 points at a time, packed in pairs
         float2 r2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                         make_float2(0.f, 0.f)};
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-          const float4 a = *reinterpret_cast<const float4*>(xt + k * TJ + 8 * grp);
-          const float4 c = *reinterpret_cast<const float4*>(xt + k * TJ + 8 * grp + 4);
+          // explicit shared-space loads (a generic load through the cast
+          // pointer waits on the long scoreboard)
+          float4 a, c;
+          const uint32_t ad = xt_s + static_cast<uint32_t>((k * TJ + 8 * grp) * 4);
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(ad));
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w)
+                       : "r"(ad + 16));
           const float2 d0 = __fadd2_rn(xi2[k], make_float2(a.x, a.y));
           const float2 d1 = __fadd2_rn(xi2[k], make_float2(a.z, a.w));
           const float2 d2 = __fadd2_rn(xi2[k], make_float2(c.x, c.y));
@@ -230,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
         for (int e = 0; e < 8; ++e) {
           const float rr = (e & 1) ? r2[e >> 1].y : r2[e >> 1].x;
           const float u = sqrt_approx(rr);
-          const float kp = matern_from_u(u, hsf2, ha) * kscale;
+          const float kp = matern_from_u(u, hsS, haS);
           unsigned long long kv;
           asm("cvt.rni.sat.u64.f32 %0, %1;" : "=l"(kv) : "f"(kp));
           K[e] = static_cast<uint32_t>(kv);
@@ -258,31 +295,34 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
                                            __byte_perm(KH[4 * hq + 2], KH[4 * hq + 3], 0x0040), 0x5410);
         }
       }
-      // K bytes -> the A operand: plane i / 2, byte (i % 2) 64 + 32 h + point,
-      // 16-byte chunk c at (c ^ (r % 8)) in the row (128-byte swizzle)
-      uint8_t* kb = sK + b * kKBuf + (r >> 3) * 1024 + (r & 7) * 128;
+      // K bytes -> the A operand: byte i's block, row r, 16-byte chunk c (of 4
+      // per 64-point row) at (c ^ ((r % 8) / 2)) (64-byte swizzle)
+      uint8_t* kb = sK + b * kKBuf + (r >> 3) * 512 + (r & 7) * 64;
 #pragma unroll
       for (int i = 0; i < kNKB; ++i)
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int c = 4 * (i % 2) + 2 * h + u;
+        for (int u = 0; u < kPW / 16; ++u) {
+          const int c = (kPW / 16) * h + u;
           uint4 v = make_uint4(w[i][4 * u], w[i][4 * u + 1], w[i][4 * u + 2], w[i][4 * u + 3]);
-          *reinterpret_cast<uint4*>(kb + (i / 2) * (TI * 128) + ((c ^ (r & 7)) << 4)) = v;
+          *reinterpret_cast<uint4*>(kb + i * kKBlk + ((c ^ ((r & 7) >> 1)) << 4)) = v;
         }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_kfull[b]);
       if ((t + 1) % kChunk == 0 || t == T - 1) {
-        // drain: class sums -> fp64, this warp's half of the columns
+        // drain: class sums -> fp64, this warp's share of the columns
         mbar_wait(&bar_ofull, nd & 1);
         tc_after();
-        const int half = p.spad / 2;
+        // 8-column pieces dealt round-robin to the warps sharing the lane quarter
 #pragma unroll 1
-        for (int c0 = h * half; c0 < (h + 1) * half; c0 += 8) {
+        for (int c0 = 8 * h; c0 < p.spad; c0 += 8 * (kEpiWarps / 4)) {
           uint32_t cv[kNCls][8];
 #pragma unroll
           for (int c = 0; c < kNCls; ++c) tmem_ld8(tmem + lanes + static_cast<uint32_t>(c * p.spad + c0), cv[c]);
           tmem_wait_ld();
+          if (t + 1 < T)  // the next chunk accumulates from zero
+#pragma unroll
+            for (int c = 0; c < kNCls; ++c) tmem_zero8(tmem + lanes + static_cast<uint32_t>(c * p.spad + c0));
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int col = c0 + e;
@@ -297,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
             }
           }
         }
+        tmem_wait_st();
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar_odrained);
@@ -332,26 +373,26 @@ __device__ __forceinline__ int col_exp(unsigned long long mbits) {
   return max(-1000, min(1000, 54 - E));
 }
 
-// V -> per-tile byte images [num_jt][3][spad][128], each 3 x spad rows of
-// 128 bytes = [byte 2q + 1 | byte 2q + 2] of 64 points, 16-byte chunks at
-// (chunk ^ (row % 8)) (the UMMA 128-byte swizzle, K-major B operand), plus
-// vscale[c] = 2^-e_c.  One thread per 16-byte chunk.
+// V -> per-tile byte images [num_jt][6][spad][64]: byte j = 1..6 of the
+// balanced base-256 digits of V 2^e_c, row = column of V, 64 points, 16-byte
+// chunks at (chunk ^ ((row % 8) / 2)) (the UMMA 64-byte swizzle, K-major B
+// operand), plus vscale[c] = 2^-e_c.  One thread per 16-byte chunk.
 __global__ void i8_vimg_kernel(const double* V, int64_t ldv, int64_t n, int s, int spad, int num_jt,
                                const unsigned long long* colbits, uint8_t* img, double* vscale) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t per_tile = 3LL * spad * 8;
+  const int64_t per_tile = 6LL * spad * 4;
   if (idx >= per_tile * num_jt) return;
   const int64_t t = idx / per_tile;
   const int rem = static_cast<int>(idx - t * per_tile);
-  const int plane = rem / (spad * 8), row = (rem / 8) % spad, chunk = rem % 8;
+  const int blk = rem / (spad * 4), row = (rem / 4) % spad, chunk = rem % 4;
   const int c = row;
-  const int digit = 2 * plane + 1 + (chunk >= 4 ? 1 : 0);
-  const int p0 = 16 * (chunk & 3);
+  const int digit = blk + 1;
+  const int p0 = 16 * chunk;
   uint32_t w[4] = {0u, 0u, 0u, 0u};
   if (c < s) {
     const int e = col_exp(colbits[c]);
     const double sc = ldexp(1.0, e);
-    if (t == 0 && plane == 0 && chunk == 0) vscale[c] = ldexp(1.0, -e);
+    if (t == 0 && blk == 0 && chunk == 0) vscale[c] = ldexp(1.0, -e);
 #pragma unroll 4
     for (int k = 0; k < 16; ++k) {
       const int64_t j = t * TJ + p0 + k;
@@ -369,8 +410,8 @@ __global__ void i8_vimg_kernel(const double* V, int64_t ldv, int64_t n, int s, i
       w[k / 4] |= (static_cast<uint32_t>(dv) & 0xFFu) << (8 * (k % 4));
     }
   }
-  uint8_t* dst = img + t * (3LL * spad * 128) + static_cast<int64_t>(plane) * spad * 128 + (row >> 3) * 1024 +
-                 (row & 7) * 128 + ((chunk ^ (row & 7)) << 4);
+  uint8_t* dst = img + t * (6LL * spad * 64) + static_cast<int64_t>(blk) * spad * 64 + (row >> 3) * 512 +
+                 (row & 7) * 64 + ((chunk ^ ((row & 7) >> 1)) << 4);
   *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
@@ -388,14 +429,23 @@ __global__ void i8_xtile_kernel(const float* xs, int dp, int d, int64_t n_pad, i
 int i8_splits(int64_t n) {
   // keyed on the global n (row shards reproduce the full operator's rows):
   // whole waves of 148 CTAs, >= 4 tiles per split
+  static const int force = [] {
+    const char* e = getenv("WGP_I8_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  static const double fill = [] {
+    const char* e = getenv("WGP_I8_FILL");
+    return e ? atof(e) : 0.95;  // config 2: 4 splits (8.7 waves), 2.75 vs 2.96 ms per CG iteration with 2
+  }();
   const int64_t rt = ceil_div(n, TI), nt = ceil_div(n, TJ);
+  if (force > 0) return static_cast<int>(std::min<int64_t>(force, nt));
   const int64_t wave = 148;
   const int64_t smax = std::max<int64_t>(1, nt / 4);
   for (int64_t s = 1; s <= smax; ++s) {
     const int64_t ctas = rt * s;
     if (ctas < wave) continue;
     const double waves = static_cast<double>(ctas) / wave;
-    if (waves / std::ceil(waves) >= 0.85) return static_cast<int>(s);
+    if (waves / std::ceil(waves) >= fill) return static_cast<int>(s);
   }
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(smax, wave / rt)));
 }
@@ -435,7 +485,7 @@ bool hv_i8_partials(const Hv64Params& hp, cudaStream_t st, int* splits_out, int6
   i8_colmax_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(64, ceil_div(hp.n, 256))), s), 256, 0, st>>>(
       hp.V, hp.ldv, hp.n, colbits);
   WGP_LAUNCH_CHECK();
-  const int64_t chunks = 3LL * spad * 8 * num_jt;
+  const int64_t chunks = 6LL * spad * 4 * num_jt;
   i8_vimg_kernel<<<static_cast<unsigned>(ceil_div(chunks, 256)), 256, 0, st>>>(hp.V, hp.ldv, hp.n, s, spad, num_jt,
                                                                              colbits, img, vscale);
   WGP_LAUNCH_CHECK();
@@ -463,7 +513,7 @@ bool hv_i8_partials(const Hv64Params& hp, cudaStream_t st, int* splits_out, int6
   switch (hp.d) {
 #define WGP_I8_CASE(D)                                            \
   case D:                                                         \
-    WGP_SMEM_ATTR(hv_i8_kernel<D>, 200 * 1024);                   \
+    WGP_SMEM_ATTR(hv_i8_kernel<D>, 225 * 1024);                   \
     hv_i8_kernel<D><<<grid, kThreads, smem, st>>>(a);             \
     break;
     WGP_I8_CASE(1) WGP_I8_CASE(2) WGP_I8_CASE(3) WGP_I8_CASE(4) WGP_I8_CASE(5) WGP_I8_CASE(6) WGP_I8_CASE(7)

@@ -1,0 +1,5 @@
+export PYTHONPATH=.
+for r in 1 2; do for l in lib_nbk2 lib_nbk3; do
+  echo "$l $(WGP_LIBRARY=$PWD/ab/$l.so timeout 300 python scripts/time_cg64_c2.py | tr '\n' ' ')"
+done; done
+timeout 300 python scripts/diag_i8.py gpurun_out/i8.npz 2>&1 | tail -3
