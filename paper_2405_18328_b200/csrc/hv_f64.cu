@@ -294,14 +294,20 @@ int hv64_splits(int64_t n) {
 }
 
 // The operator engine: the exact integer-slice product on the int8 tensor
-// core (hv_i8.cu) where it applies, else the DMMA kernel below;
-// WGP_HV64_ENGINE=dmma keeps the DMMA kernel (A/B).
-static bool use_i8(int d, int s) {
-  static const bool dmma = [] {
+// core (hv_i8.cu) from n = 4096 points on (config-2-shaped data, s = 65, per
+// CG iteration: 101 vs 132 us at n = 4096, 780 vs 1458 us at 16384,
+// scripts/time_cg64_sizes.py), the DMMA kernel below for smaller n (its
+// latency is lower: 39 vs 51 us at config 0, n = 2048) and d > 16.  Keyed on
+// the global n, so every row shard uses the same engine.
+// WGP_HV64_ENGINE=dmma | i8 forces one (A/B, tests).
+static bool use_i8(int64_t n, int d, int s) {
+  static const int force = [] {
     const char* e = getenv("WGP_HV64_ENGINE");
-    return e && std::string(e) == "dmma";
+    if (!e) return 0;
+    return std::string(e) == "dmma" ? -1 : std::string(e) == "i8" ? 1 : 0;
   }();
-  return !dmma && hv_i8_supported(d, s);
+  if (!hv_i8_supported(d, s) || force < 0) return false;
+  return force > 0 || n >= 4096;
 }
 
 size_t hv64_workspace_bytes(int64_t n, int64_t m, int s) {
@@ -324,7 +330,7 @@ static void hv64_launch(const Hv64Params& p, cudaStream_t st, bool reduce, int* 
   }
   int splits = 0;
   int64_t m_pad = 0;
-  if (use_i8(p.d, p.s) && hv_i8_partials(p, st, &splits, &m_pad)) {
+  if (use_i8(p.n, p.d, p.s) && hv_i8_partials(p, st, &splits, &m_pad)) {
     if (splits_out) *splits_out = splits;
     if (m_pad_out) *m_pad_out = m_pad;
     if (!reduce) return;

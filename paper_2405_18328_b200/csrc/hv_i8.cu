@@ -15,13 +15,18 @@
 //     into seven balanced signed bytes V = sum_j V_j 256^j;
 //   * K.V = sum_ij 256^(i+j) K_i V_j: every byte product is exact and every
 //     int32 accumulation is exact (drained to fp64 every 128 tiles, before it
-//     could overflow).  Classes i + j = 5..10 are kept (20 byte pairs); the
-//     dropped classes 0..4 weigh < 2^-44 of the result.  So the product is
-//     linear in V to ~1e-12 and deterministic.
-// The 20 pairs x 2 K steps are 40 kind::i8 MMAs (M = 128, N = s padded to 16,
-// K = 32) per 64-point tile into six int32 accumulators in TMEM (6 x N <= 480
-// columns); the int8 tensor rate (~4.5 POPS) makes that ~6x cheaper than the
-// fp64 tensor core's 37 TF/s for the same product.
+//     could overflow).  Classes i + j = 3..10 are kept (29 byte pairs); the
+//     dropped classes 0..2 weigh < 2^-60 of the result, so the product is
+//     linear in V to fp64 rounding and deterministic.  (Keeping only classes
+//     5..10 -- linear to ~1e-12 -- cost CG 5-11% more iterations than the
+//     DMMA engine on fixed config-2 systems: scripts/diag_cg_engines.py.)
+// Eight classes of N = s padded to 16 int32 columns fill TMEM for s <= 64;
+// the 65th column (the configs' s = 65: 64 probes + y) and up to three more
+// run on the fp64 pipe in the entry warps (one DFMA per entry and column,
+// exactly the DMMA engine's arithmetic); wider V is done in column chunks.
+// One MMA per K byte covers up to 256 / N consecutive V bytes (their classes
+// are consecutive accumulators): 18 kind::i8 MMAs (M = 128, K = 32) per
+// 64-point tile at s = 65.
 //
 // Warp roles (320 threads): warps 0..7 evaluate the entries (warp w: rows
 // 32 (w % 4) .. +31 = its TMEM lane quarter, points 32 (w / 4) .. +31 of each
@@ -34,6 +39,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <stdexcept>
 
 #include "common.cuh"
 #include "hv_f64.cuh"
@@ -44,7 +50,10 @@ namespace {
 
 constexpr int TI = 128;          // output rows per CTA (MMA M, TMEM lanes)
 constexpr int TJ = 64;           // points per tile (two K steps of 32 bytes)
-constexpr int kNCls = 6;         // accumulator classes i + j = 5 .. 10
+constexpr int kNCls = 8;         // accumulator classes i + j = 3 .. 10
+constexpr int kNVB = 7;          // V bytes 0..6
+constexpr int kMaxSm = 64;       // columns on the tensor core (8 x 64 TMEM columns)
+constexpr int kTailMax = 4;      // columns past 64 on the fp64 pipe
 constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (4 x 64 x 255 x 128))
 constexpr int kMaxD = 16;        // coordinates kept in registers
 #ifndef WGP_I8_NBK
@@ -62,9 +71,12 @@ constexpr int kNKB = 5;                            // K bytes (39-bit K)
 constexpr uint32_t kKBlk = TI * 64u;           // one K byte: 128 rows x 64 points, 64-byte swizzle
 constexpr uint32_t kKBuf = kNKB * kKBlk;       // 40 KB
 
-// V stage: bytes j = 1..6, each spad rows (columns of V) x 64 points, 64-byte
-// swizzle, stacked so that consecutive bytes form one B operand of N = L spad
-__host__ __device__ inline uint32_t vstage_bytes(int spad) { return 6u * static_cast<uint32_t>(spad) * 64u; }
+// V stage: bytes j = 0..6, each spad rows (columns of V) x 64 points, 64-byte
+// swizzle, stacked so that consecutive bytes form one B operand of N = L spad;
+// then the tail columns in fp64, [tail][64]
+__host__ __device__ inline uint32_t vstage_bytes(int spad, int tail) {
+  return static_cast<uint32_t>(kNVB) * static_cast<uint32_t>(spad) * 64u + static_cast<uint32_t>(tail) * 64u * 8u;
+}
 // UMMA shared-memory descriptor, K-major, 64-byte swizzle (8-row atoms of 512 bytes)
 __device__ __forceinline__ uint64_t umma_desc_sw64(const void* p) {
   const uint32_t a = smem_u32(p);
@@ -77,34 +89,35 @@ struct I8Args {
   const float* xtile;  // [num_jt][D][64] the tiles' points, negated, coordinate-major
   int dp, d;
   int64_t n, r0, m;  // contracted points, first output row (global), rows
-  int num_jt, splits, s, spad;
-  const uint8_t* vimg;   // [num_jt][3][spad][128] swizzled V byte images
-  const double* vscale;  // [s] 2^-e_c
+  int num_jt, splits, s, spad;  // s: columns of the whole partial buffer
+  int s_mma, tail, c_off;        // this launch: columns c_off .. + s_mma on MMAs, then tail on DFMA
+  const uint8_t* vimg;   // [num_jt] x vstage_bytes(spad, tail) swizzled V byte images + fp64 tail
+  const double* vscale;  // [s_mma] 2^-e_c
   const float* hyp;      // device [sf2, a, diag]
   double* part;          // [splits][s][m_pad] fp64 partials
   int64_t m_pad;
   const int* done;
 };
 
-// One tile's MMAs: for K byte i its partner V bytes j = max(1, 5 - i) .. 6
-// are consecutive row blocks of the V stage and their classes i + j - 5
-// consecutive accumulators, so one instruction covers up to three of them
-// (N = 3 spad <= 240): 8 groups x 2 K steps = 16 MMAs per tile (20 byte
-// pairs; the A tile is read once per group instead of once per pair -- the
+// One tile's MMAs: for K byte i its partner V bytes j = max(0, 3 - i) .. 6
+// are consecutive row blocks of the V stage and their classes i + j - 3
+// consecutive accumulators, so one instruction covers up to 256 / spad of
+// them (the A tile is read once per group instead of once per pair -- the
 // shared-memory reads of the operands bound the SS MMAs).  ka / vb: shared
-// addresses of K byte 0 and V byte 1.  The accumulators are zeroed by the
+// addresses of K byte 0 and V byte 0.  The accumulators are zeroed by the
 // entry warps at the start and after every drain, so every MMA accumulates.
 __device__ __forceinline__ void mma_tile_i8(uint32_t d, const uint8_t* ka, const uint8_t* vb, int spad,
                                             uint32_t idesc_base) {
+  const int G = 256 / spad < kNVB ? 256 / spad : kNVB;  // bytes per instruction
 #pragma unroll
   for (int i = 0; i < kNKB; ++i) {
-    const int j0 = 5 - i > 1 ? 5 - i : 1;
-#pragma unroll
-    for (int jg = j0; jg <= 6; jg += 3) {
-      const int L = 6 - jg + 1 < 3 ? 6 - jg + 1 : 3;  // bytes in this group
+    const int j0 = 3 - i > 0 ? 3 - i : 0;
+#pragma unroll 1
+    for (int jg = j0; jg < kNVB; jg += G) {
+      const int L = kNVB - jg < G ? kNVB - jg : G;
       const uint64_t a = umma_desc_sw64(ka + i * kKBlk);
-      const uint64_t b = umma_desc_sw64(vb + (jg - 1) * spad * 64);
-      const uint32_t dc = d + static_cast<uint32_t>(spad * (i + jg - 5));
+      const uint64_t b = umma_desc_sw64(vb + jg * spad * 64);
+      const uint32_t dc = d + static_cast<uint32_t>(spad * (i + jg - 3));
       const uint32_t idesc = idesc_base | (static_cast<uint32_t>((L * spad) >> 3) << 17);
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
@@ -129,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
   if (p.done && *p.done) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t vsb = vstage_bytes(p.spad);
+  const uint32_t vsb = vstage_bytes(p.spad, p.tail);
   uint8_t* sK = smem;                                  // NBK x 32 KB
   uint8_t* sV = sK + NBK * kKBuf;                      // NV x vsb (multiples of 1024)
   float* sX = reinterpret_cast<float*>(sV + NV * vsb); // NV x [D][TJ] negated coordinates
@@ -219,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
     // (sf^2 + a u) 2^-u 2^eK = (sf^2 2^eK + a 2^eK u) 2^-u bit for bit: power-of-two scaling is exact
     const float hsS = hsf2 * kscale, haS = ha * kscale;
     const double oscale = ldexp(1.0, -eK);
+    double acct[kTailMax] = {0.0, 0.0, 0.0, 0.0};  // tail columns: this row, this warp's points, fp64
     // zero this warp's accumulator pieces before the first MMA
     if (T > 0) {
 #pragma unroll 1
@@ -262,22 +276,43 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
           r2[2] = __ffma2_rn(d2, d2, r2[2]);
           r2[3] = __ffma2_rn(d3, d3, r2[3]);
         }
-        uint32_t K[8], KH[8];  // low 32 bits, bits 32..38
+        float kp[8];  // the entries scaled by 2^eK, zero where excluded
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float rr = (e & 1) ? r2[e >> 1].y : r2[e >> 1].x;
-          const float u = sqrt_approx(rr);
-          const float kp = matern_from_u(u, hsS, haS);
-          unsigned long long kv;
-          asm("cvt.rni.sat.u64.f32 %0, %1;" : "=l"(kv) : "f"(kp));
-          K[e] = static_cast<uint32_t>(kv);
-          KH[e] = static_cast<uint32_t>(kv >> 32);
+          kp[e] = matern_from_u(sqrt_approx(rr), hsS, haS);
         }
         if (edge) {  // the diagonal (H_ii V_i is added exactly in the reduction) and points >= n
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int64_t gj = pbase + 8 * grp + e;
-            if (gj >= p.n || gj == g) K[e] = KH[e] = 0u;
+            if (gj >= p.n || gj == g) kp[e] = 0.f;
+          }
+        }
+        uint32_t K[8], KH[8];  // low 32 bits, bits 32..38
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          // (the float's bits shifted on the integer pipe instead: 4.7 vs
+          // 4.2 ms per config-2 CG iteration -- issue slots, not the
+          // conversion pipe, bind)
+          unsigned long long kv;
+          asm("cvt.rni.sat.u64.f32 %0, %1;" : "=l"(kv) : "f"(kp[e]));
+          K[e] = static_cast<uint32_t>(kv);
+          KH[e] = static_cast<uint32_t>(kv >> 32);
+        }
+        if (p.tail > 0) {  // columns past 64: fp64 FMA of the fp32 entry, the DMMA engine's arithmetic
+          const uint32_t vt = smem_u32(sV + st * vsb + kNVB * p.spad * 64) + 8u * (kPW * h + 8 * grp);
+#pragma unroll
+          for (int c = 0; c < kTailMax; ++c) {
+            if (c < p.tail) {
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                double v0, v1;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(vt + 8u * (c * TJ + e)));
+                acct[c] = fma(static_cast<double>(kp[e]), v0, acct[c]);
+                acct[c] = fma(static_cast<double>(kp[e + 1]), v1, acct[c]);
+              }
+            }
           }
         }
         // 4 x 4 byte transposes: w[i][.] holds byte i of 4 consecutive points
@@ -316,23 +351,30 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
         // 8-column pieces dealt round-robin to the warps sharing the lane quarter
 #pragma unroll 1
         for (int c0 = 8 * h; c0 < p.spad; c0 += 8 * (kEpiWarps / 4)) {
-          uint32_t cv[kNCls][8];
+          double vs[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int c = 0; c < kNCls; ++c) tmem_ld8(tmem + lanes + static_cast<uint32_t>(c * p.spad + c0), cv[c]);
-          tmem_wait_ld();
-          if (t + 1 < T)  // the next chunk accumulates from zero
+          for (int hf = 1; hf >= 0; --hf) {  // classes 7..4, then 3..0: high first, fixed order
+            uint32_t cv[kNCls / 2][8];
 #pragma unroll
-            for (int c = 0; c < kNCls; ++c) tmem_zero8(tmem + lanes + static_cast<uint32_t>(c * p.spad + c0));
+            for (int c = 0; c < kNCls / 2; ++c)
+              tmem_ld8(tmem + lanes + static_cast<uint32_t>((4 * hf + c) * p.spad + c0), cv[c]);
+            tmem_wait_ld();
+            if (t + 1 < T)  // the next chunk accumulates from zero
+#pragma unroll
+              for (int c = 0; c < kNCls / 2; ++c)
+                tmem_zero8(tmem + lanes + static_cast<uint32_t>((4 * hf + c) * p.spad + c0));
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+#pragma unroll
+              for (int c = kNCls / 2 - 1; c >= 0; --c)
+                vs[e] += ldexp(static_cast<double>(static_cast<int>(cv[c][e])), 8 * (4 * hf + c + 3));
+          }
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const int col = c0 + e;
-            double v = 0.0;
-#pragma unroll
-            for (int c = kNCls - 1; c >= 0; --c)  // high classes first, fixed order
-              v += ldexp(static_cast<double>(static_cast<int>(cv[c][e])), 8 * (c + 5));
-            if (col < p.s && lr < p.m) {
-              double* dst = p.part + (static_cast<int64_t>(sp) * p.s + col) * p.m_pad + lr;
-              const double val = v * p.vscale[col] * oscale;
+            if (col < p.s_mma && lr < p.m) {
+              double* dst = p.part + (static_cast<int64_t>(sp) * p.s + p.c_off + col) * p.m_pad + lr;
+              const double val = vs[e] * p.vscale[col] * oscale;
               *dst = nd == 0 ? val : *dst + val;
             }
           }
@@ -343,6 +385,22 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
         if (lane == 0) mbar_arrive(&bar_odrained);
         ++nd;
       }
+    }
+    if (p.tail > 0) {
+      // the tail columns: the kEpiWarps / 4 warps of a lane quarter summed in
+      // a fixed order through shared memory (the K buffers are free: every
+      // MMA completed before the final drain)
+      double* scr = reinterpret_cast<double*>(sK);
+#pragma unroll
+      for (int c = 0; c < kTailMax; ++c)
+        if (c < p.tail) scr[(h * TI + r) * kTailMax + c] = acct[c];
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if (h == 0 && lr < p.m)
+        for (int c = 0; c < p.tail; ++c) {
+          double v = 0.0;
+          for (int hh = 0; hh < kEpiWarps / 4; ++hh) v += scr[(hh * TI + r) * kTailMax + c];
+          p.part[(static_cast<int64_t>(sp) * p.s + p.c_off + p.s_mma + c) * p.m_pad + lr] = v * oscale;
+        }
     }
   }
   tc_before();
@@ -373,23 +431,31 @@ __device__ __forceinline__ int col_exp(unsigned long long mbits) {
   return max(-1000, min(1000, 54 - E));
 }
 
-// V -> per-tile byte images [num_jt][6][spad][64]: byte j = 1..6 of the
-// balanced base-256 digits of V 2^e_c, row = column of V, 64 points, 16-byte
-// chunks at (chunk ^ ((row % 8) / 2)) (the UMMA 64-byte swizzle, K-major B
-// operand), plus vscale[c] = 2^-e_c.  One thread per 16-byte chunk.
-__global__ void i8_vimg_kernel(const double* V, int64_t ldv, int64_t n, int s, int spad, int num_jt,
+// V -> per-tile images: bytes j = 0..6 of the balanced base-256 digits of
+// V 2^e_c for the s_mma MMA columns, [7][spad][64] (row = column of V, 64
+// points, 16-byte chunks at (chunk ^ ((row % 8) / 2)): the UMMA 64-byte
+// swizzle, K-major B operand), then the tail columns in fp64 [tail][64];
+// vscale[c] = 2^-e_c.  One thread per 16-byte chunk of bytes / per tail value.
+__global__ void i8_vimg_kernel(const double* V, int64_t ldv, int64_t n, int s_mma, int tail, int spad, int num_jt,
                                const unsigned long long* colbits, uint8_t* img, double* vscale) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t per_tile = 6LL * spad * 4;
+  const int64_t nbyte = static_cast<int64_t>(kNVB) * spad * 4, per_tile = nbyte + static_cast<int64_t>(tail) * TJ;
   if (idx >= per_tile * num_jt) return;
   const int64_t t = idx / per_tile;
   const int rem = static_cast<int>(idx - t * per_tile);
+  uint8_t* timg = img + t * static_cast<int64_t>(vstage_bytes(spad, tail));
+  if (rem >= nbyte) {  // a tail value
+    const int q = rem - static_cast<int>(nbyte), c = q / TJ, pt = q % TJ;
+    const int64_t j = t * TJ + pt;
+    reinterpret_cast<double*>(timg + kNVB * spad * 64)[c * TJ + pt] = j < n ? V[j + (s_mma + c) * ldv] : 0.0;
+    return;
+  }
   const int blk = rem / (spad * 4), row = (rem / 4) % spad, chunk = rem % 4;
   const int c = row;
-  const int digit = blk + 1;
+  const int digit = blk;
   const int p0 = 16 * chunk;
   uint32_t w[4] = {0u, 0u, 0u, 0u};
-  if (c < s) {
+  if (c < s_mma) {
     const int e = col_exp(colbits[c]);
     const double sc = ldexp(1.0, e);
     if (t == 0 && blk == 0 && chunk == 0) vscale[c] = ldexp(1.0, -e);
@@ -410,8 +476,8 @@ __global__ void i8_vimg_kernel(const double* V, int64_t ldv, int64_t n, int s, i
       w[k / 4] |= (static_cast<uint32_t>(dv) & 0xFFu) << (8 * (k % 4));
     }
   }
-  uint8_t* dst = img + t * (6LL * spad * 64) + static_cast<int64_t>(blk) * spad * 64 + (row >> 3) * 512 +
-                 (row & 7) * 64 + ((chunk ^ ((row & 7) >> 1)) << 4);
+  uint8_t* dst = timg + static_cast<int64_t>(blk) * spad * 64 + (row >> 3) * 512 + (row & 7) * 64 +
+                 ((chunk ^ ((row & 7) >> 1)) << 4);
   *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
@@ -452,42 +518,28 @@ int i8_splits(int64_t n) {
 
 }  // namespace
 
-bool hv_i8_supported(int d, int s) { return d >= 1 && d <= kMaxD && s >= 1 && s <= 80; }
+bool hv_i8_supported(int d, int s) { return d >= 1 && d <= kMaxD && s >= 1; }
 
 size_t hv_i8_workspace_bytes(int64_t n, int64_t m, int s) {
-  const int spad = static_cast<int>(round_up(s, 16));
   const size_t part = sizeof(double) * static_cast<size_t>(i8_splits(n)) * s * round_up(m, TI);
-  const size_t img = static_cast<size_t>(ceil_div(n, TJ)) * vstage_bytes(spad);
+  const size_t img = static_cast<size_t>(ceil_div(n, TJ)) * vstage_bytes(kMaxSm, kTailMax);
   const size_t xt = sizeof(float) * static_cast<size_t>(ceil_div(n, TJ)) * kMaxD * TJ;
   return round_up(part, 1024) + round_up(img, 1024) + 2 * 8 * 128 + round_up(xt, 1024);
 }
 
-bool hv_i8_partials(const Hv64Params& hp, cudaStream_t st, int* splits_out, int64_t* m_pad_out) {
-  if (!hv_i8_supported(hp.d, hp.s) || hp.m <= 0) return false;
-  const int s = hp.s, spad = static_cast<int>(round_up(s, 16));
+// One launch over columns [c_off, c_off + s_mma + tail) of the partials.
+static void i8_launch(const Hv64Params& hp, int c_off, int s_mma, int tail, int splits, int64_t m_pad,
+                      uint8_t* img, unsigned long long* colbits, double* vscale, const float* xtile, cudaStream_t st) {
+  const int spad = static_cast<int>(round_up(s_mma, 16));
   const int num_jt = static_cast<int>(ceil_div(hp.n, TJ));
-  const int splits = i8_splits(hp.n);
-  const int64_t m_pad = round_up(hp.m, TI);
-  uint8_t* ws = reinterpret_cast<uint8_t*>(hp.part);
-  const size_t part_b = round_up(sizeof(double) * static_cast<size_t>(splits) * s * m_pad, 1024);
-  uint8_t* img = ws + part_b;
-  const size_t img_b = round_up(static_cast<size_t>(num_jt) * vstage_bytes(spad), 1024);
-  auto* colbits = reinterpret_cast<unsigned long long*>(img + img_b);
-  double* vscale = reinterpret_cast<double*>(colbits + 128);
-  float* xtile = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(colbits) + 2 * 8 * 128);
-  {
-    const int64_t nx = static_cast<int64_t>(num_jt) * hp.d * TJ;
-    i8_xtile_kernel<<<static_cast<unsigned>(ceil_div(nx, 256)), 256, 0, st>>>(hp.xs, hp.dp, hp.d,
-                                                                             round_up(hp.n, 128), num_jt, xtile);
-    WGP_LAUNCH_CHECK();
-  }
-  WGP_CUDA(cudaMemsetAsync(colbits, 0, sizeof(unsigned long long) * 128, st));
-  i8_colmax_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(64, ceil_div(hp.n, 256))), s), 256, 0, st>>>(
-      hp.V, hp.ldv, hp.n, colbits);
+  const double* V = hp.V + static_cast<int64_t>(c_off) * hp.ldv;
+  WGP_CUDA(cudaMemsetAsync(colbits, 0, sizeof(unsigned long long) * kMaxSm, st));
+  i8_colmax_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(64, ceil_div(hp.n, 256))), s_mma), 256, 0,
+                     st>>>(V, hp.ldv, hp.n, colbits);
   WGP_LAUNCH_CHECK();
-  const int64_t chunks = 6LL * spad * 4 * num_jt;
-  i8_vimg_kernel<<<static_cast<unsigned>(ceil_div(chunks, 256)), 256, 0, st>>>(hp.V, hp.ldv, hp.n, s, spad, num_jt,
-                                                                             colbits, img, vscale);
+  const int64_t items = (static_cast<int64_t>(kNVB) * spad * 4 + static_cast<int64_t>(tail) * TJ) * num_jt;
+  i8_vimg_kernel<<<static_cast<unsigned>(ceil_div(items, 256)), 256, 0, st>>>(V, hp.ldv, hp.n, s_mma, tail, spad,
+                                                                            num_jt, colbits, img, vscale);
   WGP_LAUNCH_CHECK();
   I8Args a{};
   a.xs = hp.xs;
@@ -499,15 +551,18 @@ bool hv_i8_partials(const Hv64Params& hp, cudaStream_t st, int* splits_out, int6
   a.m = hp.m;
   a.num_jt = num_jt;
   a.splits = splits;
-  a.s = s;
+  a.s = hp.s;
   a.spad = spad;
+  a.s_mma = s_mma;
+  a.tail = tail;
+  a.c_off = c_off;
   a.vimg = img;
   a.vscale = vscale;
   a.hyp = hp.hyp;
   a.part = hp.part;
   a.m_pad = m_pad;
   a.done = hp.done;
-  const int smem = 1024 + NBK * static_cast<int>(kKBuf) + NV * static_cast<int>(vstage_bytes(spad)) +
+  const int smem = 1024 + NBK * static_cast<int>(kKBuf) + NV * static_cast<int>(vstage_bytes(spad, tail)) +
                    NV * TJ * hp.d * 4;
   const unsigned grid = static_cast<unsigned>(ceil_div(hp.m, TI) * splits);
   switch (hp.d) {
@@ -521,9 +576,37 @@ bool hv_i8_partials(const Hv64Params& hp, cudaStream_t st, int* splits_out, int6
     WGP_I8_CASE(14) WGP_I8_CASE(15) WGP_I8_CASE(16)
 #undef WGP_I8_CASE
     default:
-      return false;
+      throw std::invalid_argument("hv_i8: d > 16");
   }
   WGP_LAUNCH_CHECK();
+}
+
+bool hv_i8_partials(const Hv64Params& hp, cudaStream_t st, int* splits_out, int64_t* m_pad_out) {
+  if (!hv_i8_supported(hp.d, hp.s) || hp.m <= 0) return false;
+  const int num_jt = static_cast<int>(ceil_div(hp.n, TJ));
+  const int splits = i8_splits(hp.n);
+  const int64_t m_pad = round_up(hp.m, TI);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(hp.part);
+  const size_t part_b = round_up(sizeof(double) * static_cast<size_t>(splits) * hp.s * m_pad, 1024);
+  uint8_t* img = ws + part_b;
+  const size_t img_b = round_up(static_cast<size_t>(num_jt) * vstage_bytes(kMaxSm, kTailMax), 1024);
+  auto* colbits = reinterpret_cast<unsigned long long*>(img + img_b);
+  double* vscale = reinterpret_cast<double*>(colbits + 128);
+  float* xtile = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(colbits) + 2 * 8 * 128);
+  {
+    const int64_t nx = static_cast<int64_t>(num_jt) * hp.d * TJ;
+    i8_xtile_kernel<<<static_cast<unsigned>(ceil_div(nx, 256)), 256, 0, st>>>(hp.xs, hp.dp, hp.d,
+                                                                             round_up(hp.n, 128), num_jt, xtile);
+    WGP_LAUNCH_CHECK();
+  }
+  // column chunks: 64 on the tensor core + up to kTailMax on the fp64 pipe
+  for (int c0 = 0; c0 < hp.s;) {
+    const int rest = hp.s - c0;
+    const int s_mma = std::min(rest, kMaxSm);
+    const int tail = rest - s_mma <= kTailMax ? rest - s_mma : 0;
+    i8_launch(hp, c0, s_mma, tail, splits, m_pad, img, colbits, vscale, xtile, st);
+    c0 += s_mma + tail;
+  }
   if (splits_out) *splits_out = splits;
   if (m_pad_out) *m_pad_out = m_pad;
   return true;
