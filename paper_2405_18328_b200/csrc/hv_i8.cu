@@ -57,7 +57,7 @@ constexpr int kTailMax = 4;      // columns past 64 on the fp64 pipe
 constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (4 x 64 x 255 x 128))
 constexpr int kMaxD = 16;        // coordinates kept in registers
 #ifndef WGP_I8_NBK
-#define WGP_I8_NBK 2
+#define WGP_I8_NBK 3  // 4.23 vs 4.33 ms per config-2 CG iteration with 2 (interleaved A/B)
 #endif
 constexpr int NBK = WGP_I8_NBK, NV = 3;   // K buffers, V / coordinate stages
 #ifndef WGP_I8_EPI
@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
     // (sf^2 + a u) 2^-u 2^eK = (sf^2 2^eK + a 2^eK u) 2^-u bit for bit: power-of-two scaling is exact
     const float hsS = hsf2 * kscale, haS = ha * kscale;
     const double oscale = ldexp(1.0, -eK);
-    double acct[kTailMax] = {0.0, 0.0, 0.0, 0.0};  // tail columns: this row, this warp's points, fp64
+    double acct[kTailMax] = {0.0, 0.0, 0.0, 0.0};  // tail columns: this row, this warp's even points, fp64
+    double acct2[kTailMax] = {0.0, 0.0, 0.0, 0.0};  // odd points
     // zero this warp's accumulator pieces before the first MMA
     if (T > 0) {
 #pragma unroll 1
@@ -306,11 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
           for (int c = 0; c < kTailMax; ++c) {
             if (c < p.tail) {
 #pragma unroll
-              for (int e = 0; e < 8; e += 2) {
+              for (int e = 0; e < 8; e += 2) {  // even / odd points in two chains (latency)
                 double v0, v1;
                 asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(vt + 8u * (c * TJ + e)));
                 acct[c] = fma(static_cast<double>(kp[e]), v0, acct[c]);
-                acct[c] = fma(static_cast<double>(kp[e + 1]), v1, acct[c]);
+                acct2[c] = fma(static_cast<double>(kp[e + 1]), v1, acct2[c]);
               }
             }
           }
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
       double* scr = reinterpret_cast<double*>(sK);
 #pragma unroll
       for (int c = 0; c < kTailMax; ++c)
-        if (c < p.tail) scr[(h * TI + r) * kTailMax + c] = acct[c];
+        if (c < p.tail) scr[(h * TI + r) * kTailMax + c] = acct[c] + acct2[c];
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
       if (h == 0 && lr < p.m)
         for (int c = 0; c < p.tail; ++c) {
