@@ -53,7 +53,7 @@ constexpr int TJ = 64;           // points per tile (two K steps of 32 bytes)
 constexpr int kNCls = 8;         // accumulator classes i + j = 3 .. 10
 constexpr int kNVB = 7;          // V bytes 0..6
 constexpr int kMaxSm = 64;       // columns on the tensor core (8 x 64 TMEM columns)
-constexpr int kTailMax = 4;      // columns past 64 on the fp64 pipe
+constexpr int kTailMax = 1;      // column 64 on the fp64 pipe (4 columns: register spills in the entry loop)
 constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (4 x 64 x 255 x 128))
 constexpr int kMaxD = 16;        // coordinates kept in registers
 #ifndef WGP_I8_NBK
@@ -74,8 +74,9 @@ constexpr uint32_t kKBuf = kNKB * kKBlk;       // 40 KB
 // V stage: bytes j = 0..6, each spad rows (columns of V) x 64 points, 64-byte
 // swizzle, stacked so that consecutive bytes form one B operand of N = L spad;
 // then the tail columns in fp64, [tail][64]
-__host__ __device__ inline uint32_t vstage_bytes(int spad, int tail) {
-  return static_cast<uint32_t>(kNVB) * static_cast<uint32_t>(spad) * 64u + static_cast<uint32_t>(tail) * 64u * 8u;
+__host__ __device__ inline uint32_t vstage_bytes(int spad, int tail) {  // (1024-aligned stages)
+  return (static_cast<uint32_t>(kNVB) * static_cast<uint32_t>(spad) * 64u + static_cast<uint32_t>(tail) * 64u * 8u +
+          1023u) & ~1023u;
 }
 // UMMA shared-memory descriptor, K-major, 64-byte swizzle (8-row atoms of 512 bytes)
 __device__ __forceinline__ uint64_t umma_desc_sw64(const void* p) {
@@ -125,6 +126,22 @@ __device__ __forceinline__ void mma_tile_i8(uint32_t d, const uint8_t* ka, const
                      "l"(b + 2 * ks), "r"(idesc));
     }
   }
+}
+
+#ifndef WGP_I8_F2D_ALU
+#define WGP_I8_F2D_ALU 0
+#endif
+// fp32 -> fp64 of an entry for the tail columns: F2F, or (WGP_I8_F2D_ALU) the
+// bits re-biased on the integer pipe (exact for normal numbers; subnormals,
+// entries under 2^-126 in units of sf^2 2^-eK, as 0)
+__device__ __forceinline__ double f2d(float x) {
+#if WGP_I8_F2D_ALU
+  const uint32_t b = __float_as_uint(x);
+  const bool nz = b >= 0x00800000u;
+  return __hiloint2double(static_cast<int>(nz ? (b >> 3) + (896u << 20) : 0u), static_cast<int>(nz ? (b << 29) : 0u));
+#else
+  return static_cast<double>(x);
+#endif
 }
 
 __device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
@@ -232,8 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
     // (sf^2 + a u) 2^-u 2^eK = (sf^2 2^eK + a 2^eK u) 2^-u bit for bit: power-of-two scaling is exact
     const float hsS = hsf2 * kscale, haS = ha * kscale;
     const double oscale = ldexp(1.0, -eK);
-    double acct[kTailMax] = {0.0, 0.0, 0.0, 0.0};  // tail columns: this row, this warp's even points, fp64
-    double acct2[kTailMax] = {0.0, 0.0, 0.0, 0.0};  // odd points
+    double acct[4] = {0.0, 0.0, 0.0, 0.0};  // column 64: this row, this warp's points (point mod 4), fp64
     // zero this warp's accumulator pieces before the first MMA
     if (T > 0) {
 #pragma unroll 1
@@ -301,19 +317,14 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
           K[e] = static_cast<uint32_t>(kv);
           KH[e] = static_cast<uint32_t>(kv >> 32);
         }
-        if (p.tail > 0) {  // columns past 64: fp64 FMA of the fp32 entry, the DMMA engine's arithmetic
+        if (p.tail > 0) {  // column 64: fp64 FMA of the fp32 entry (the DMMA engine's arithmetic), four chains
           const uint32_t vt = smem_u32(sV + st * vsb + kNVB * p.spad * 64) + 8u * (kPW * h + 8 * grp);
 #pragma unroll
-          for (int c = 0; c < kTailMax; ++c) {
-            if (c < p.tail) {
-#pragma unroll
-              for (int e = 0; e < 8; e += 2) {  // even / odd points in two chains (latency)
-                double v0, v1;
-                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(vt + 8u * (c * TJ + e)));
-                acct[c] = fma(static_cast<double>(kp[e]), v0, acct[c]);
-                acct2[c] = fma(static_cast<double>(kp[e + 1]), v1, acct2[c]);
-              }
-            }
+          for (int e = 0; e < 8; e += 2) {
+            double v0, v1;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(vt + 8u * e));
+            acct[e & 3] = fma(f2d(kp[e]), v0, acct[e & 3]);
+            acct[(e + 1) & 3] = fma(f2d(kp[e + 1]), v1, acct[(e + 1) & 3]);
           }
         }
         // 4 x 4 byte transposes: w[i][.] holds byte i of 4 consecutive points
@@ -388,20 +399,17 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
       }
     }
     if (p.tail > 0) {
-      // the tail columns: the kEpiWarps / 4 warps of a lane quarter summed in
+      // column 64: the kEpiWarps / 4 warps of a lane quarter summed in
       // a fixed order through shared memory (the K buffers are free: every
       // MMA completed before the final drain)
       double* scr = reinterpret_cast<double*>(sK);
-#pragma unroll
-      for (int c = 0; c < kTailMax; ++c)
-        if (c < p.tail) scr[(h * TI + r) * kTailMax + c] = acct[c] + acct2[c];
+      scr[h * TI + r] = (acct[0] + acct[1]) + (acct[2] + acct[3]);
       asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      if (h == 0 && lr < p.m)
-        for (int c = 0; c < p.tail; ++c) {
-          double v = 0.0;
-          for (int hh = 0; hh < kEpiWarps / 4; ++hh) v += scr[(hh * TI + r) * kTailMax + c];
-          p.part[(static_cast<int64_t>(sp) * p.s + p.c_off + p.s_mma + c) * p.m_pad + lr] = v * oscale;
-        }
+      if (h == 0 && lr < p.m) {
+        double v = 0.0;
+        for (int hh = 0; hh < kEpiWarps / 4; ++hh) v += scr[hh * TI + r];
+        p.part[(static_cast<int64_t>(sp) * p.s + p.c_off + p.s_mma) * p.m_pad + lr] = v * oscale;
+      }
     }
   }
   tc_before();
