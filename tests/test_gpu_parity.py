@@ -268,6 +268,33 @@ def test_hv_f64_symmetric_linear_and_shard_invariant(ctx):
     assert np.array_equal(part, ha[128:384])
 
 
+def test_hv_f64_i8_engine_rows_and_linearity(ctx):
+    """At n >= 4096 the fp64 operator runs on the int8-slice engine (hv_i8):
+    row shards reproduce the full operator's rows bitwise (splits keyed on the
+    global n), it is linear to fp64 rounding, bitwise reproducible, and matches
+    the fp64 oracle on row samples (the fp32 entries: ~1e-7); s = 65 exercises
+    the fp64 tail column, s = 130 the column chunks."""
+    rng = np.random.default_rng(21)
+    n, d = 4500, 9
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    ls = rng.uniform(0.7, 1.4, d)
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, 1.1, 0.2])
+    for s in (65, 130):
+        a, b = rng.standard_normal((n, s)), rng.standard_normal((n, s))
+        ha, hb, hab = ctx.hv_f64(a), ctx.hv_f64(b), ctx.hv_f64(a + b)
+        assert np.abs(hab - ha - hb).max() <= 1e-13 * np.abs(hab).max()
+        assert np.array_equal(ha, ctx.hv_f64(a))
+        ref = orc.hv_rows(X, ls, 1.1, 0.2, a, 0, 300)
+        assert rel(ha[:300], ref) <= 1e-6
+        ctx.set_rows(1024, 3072)
+        try:
+            part = ctx.hv_f64(a, rows=2048)
+        finally:
+            ctx.set_rows(0, n)
+        assert np.array_equal(part, ha[1024:3072])
+
+
 def test_hv_f64_engines_agree_subprocess():
     """The fp64 CG operator's two engines -- the exact int8-slice product on
     tcgen05 (hv_i8.cu, WGP_HV64_ENGINE=i8; the default for n >= 4096, d <= 16) and the DMMA kernel
