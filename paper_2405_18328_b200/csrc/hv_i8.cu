@@ -56,6 +56,9 @@ constexpr int kMaxSm = 64;       // columns on the tensor core (8 x 64 TMEM colu
 constexpr int kTailMax = 1;      // column 64 on the fp64 pipe (4 columns: register spills in the entry loop)
 constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (4 x 64 x 255 x 128))
 constexpr int kMaxD = 16;        // coordinates kept in registers
+#ifndef WGP_I8_ABLATE
+#define WGP_I8_ABLATE 0
+#endif
 #ifndef WGP_I8_NBK
 #define WGP_I8_NBK 3  // 4.23 vs 4.33 ms per config-2 CG iteration with 2 (interleaved A/B)
 #endif
@@ -218,7 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
       const uint8_t* vb = sV + st * vsb;
       // lane 0 issues the tile's MMAs and the commits that track them
       if (lane == 0) {
+#if !(WGP_I8_ABLATE & 1)  // (ablation build: no MMAs)
         mma_tile_i8(tmem, kb, vb, p.spad, idesc);
+#endif
         commit_one(&bar_mdone[t & 7]);
         if ((t + 1) % kChunk == 0 || t == T - 1) commit_one(&bar_ofull);
       }
@@ -271,6 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
       // warp-uniform: do any of the warp's entries need zeroing?
       const bool edge = pbase + kPW > p.n || __any_sync(0xffffffffu, g >= pbase && g < pbase + kPW);
       uint32_t w[kNKB][kPW / 4];  // digit i: kPW bytes (points 4 c .. 4 c + 3 in word c)
+#if WGP_I8_ABLATE & 2  // (ablation build: no entry math)
+#pragma unroll
+      for (int i = 0; i < kNKB; ++i)
+#pragma unroll
+        for (int c = 0; c < kPW / 4; ++c) w[i][c] = 0u;
+#else
 #pragma unroll
       for (int grp = 0; grp < kPW / 8; ++grp) {  // 8 points at a time, packed in pairs
         float2 r2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
@@ -342,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
                                            __byte_perm(KH[4 * hq + 2], KH[4 * hq + 3], 0x0040), 0x5410);
         }
       }
+#endif
       // K bytes -> the A operand: byte i's block, row r, 16-byte chunk c (of 4
       // per 64-point row) at (c ^ ((r % 8) / 2)) (64-byte swizzle)
       uint8_t* kb = sK + b * kKBuf + (r >> 3) * 512 + (r & 7) * 64;
