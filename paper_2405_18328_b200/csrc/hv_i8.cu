@@ -479,7 +479,10 @@ __global__ void i8_vimg_kernel(const double* V, int64_t ldv, int64_t n, int s_mm
   if (c < s_mma) {
     const int e = col_exp(colbits[c]);
     const double sc = ldexp(1.0, e);
-    if (t == 0 && blk == 0 && chunk == 0) vscale[c] = ldexp(1.0, -e);
+    if (t == 0 && blk == 0 && chunk == 0) {  // a non-finite column propagates NaN like the fp64 product
+      const double m = __longlong_as_double(static_cast<long long>(colbits[c]));
+      vscale[c] = isfinite(m) ? ldexp(1.0, -e) : __longlong_as_double(0x7FF8000000000000LL);
+    }
 #pragma unroll 4
     for (int k = 0; k < 16; ++k) {
       const int64_t j = t * TJ + p0 + k;

@@ -295,6 +295,22 @@ def test_hv_f64_i8_engine_rows_and_linearity(ctx):
         assert np.array_equal(part, ha[1024:3072])
 
 
+def test_hv_f64_i8_engine_nonfinite_column(ctx):
+    """A NaN in V makes its whole output column NaN on the int8-slice engine
+    as on the fp64 product (CG's NaN detection relies on it); the other columns
+    are unaffected."""
+    rng = np.random.default_rng(22)
+    n, d = 4200, 5
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    ctx.set_data(X)
+    ctx.set_hyper([*rng.uniform(0.7, 1.4, d), 1.0, 0.3])
+    V = rng.standard_normal((n, 3))
+    V[17, 1] = np.nan
+    out = ctx.hv_f64(V)
+    assert np.all(np.isnan(out[:, 1]))
+    assert np.all(np.isfinite(out[:, [0, 2]]))
+
+
 def test_hv_f64_engines_agree_subprocess():
     """The fp64 CG operator's two engines -- the exact int8-slice product on
     tcgen05 (hv_i8.cu, WGP_HV64_ENGINE=i8; the default for n >= 4096, d <= 16) and the DMMA kernel
