@@ -4,8 +4,10 @@ entries/s; ms per marginal-likelihood step).
 
 A step is one fused H.V over BASELINE config 1 (n=13,500, d=26, s=65,
 Matern-3/2 ARD, fp32): ``value`` is whole-job entries/s (n^2 per H.V) with
-inputs resident in HBM, timed per launch with CUDA events on the launching
-stream; ``e2e`` is the same H.V through the C-ABI host-pointer entry point
+inputs resident in HBM, timed per step (V split + H.V kernel + split
+reduction) with CUDA events on the launching stream, and the dominant
+kernel's own time (the roofline) from a second pass with events around each
+H.V launch; ``e2e`` is the same H.V through the C-ABI host-pointer entry point
 (``wgp_hv``: pinned host V in, host H.V out, copies inside the timed region).
 Between timed iterations L2 is flushed (a 512 MiB write; the inputs, 3.5 MB,
 would otherwise stay L2-resident).  With --gpus N under torchrun every rank's
@@ -544,8 +546,6 @@ def main():
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         launches0 = wg.launch_count()
-        if args.hv_impl != "simt":
-            ctx.profile(True)
         clk.phase("hv")
         for a, b in evs:
             flush.zero_()
@@ -553,10 +553,21 @@ def main():
             one_step()
             b.record(stream)
         stream.synchronize()
+        launches = wg.launch_count() - launches0
+        # the dominant kernel's own time (roofline): the same steps again with
+        # CUDA events around each hv_tc launch -- a separate pass, because an
+        # event between the V split and the H.V kernel breaks their
+        # programmatic dependent launch (the split overlaps the kernel's fill)
+        kernel_ms, kernel_launches = 0.0, 0
+        if args.hv_impl != "simt":
+            ctx.profile(True)
+            for _ in range(args.steps):
+                flush.zero_()
+                one_step()
+            stream.synchronize()
+            kernel_ms, kernel_launches = ctx.profile_read()
+            ctx.profile(False)
         clk.phase("e2e")
-    launches = wg.launch_count() - launches0
-    kernel_ms, kernel_launches = ctx.profile_read() if args.hv_impl != "simt" else (0.0, 0)
-    ctx.profile(False)
     times = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.mean(times))
     # dominant kernel's mean launch duration (events on the context stream);

@@ -41,6 +41,8 @@
 #include <algorithm>
 #include <mutex>
 #include <vector>
+#include <utility>
+#include <cstdlib>
 #include <cstdio>
 
 #include "common.cuh"
@@ -358,6 +360,7 @@ __global__ void __launch_bounds__(kThreadsT<H16>, 1)
     // (separate warp so the two rings never block each other); one box of
     // 128-byte rows (32 tf32 / 64 bf16 points) per plane and tile
     if (T > 0) {
+      if constexpr (H16) asm volatile("griddepcontrol.wait;" ::: "memory");  // V planes from the split kernel
       // ring slots and phases advance incrementally: runtime divisions by
       // NV / NB / C cost tens of clk each in these single-warp loops
       int st = 0;
@@ -689,6 +692,9 @@ __global__ void __launch_bounds__(kThreadsT<H16>, 1)
                      : "memory");
     }
     if constexpr (H16) {
+      // (programmatic dependent launch: the column scales come from the split
+      // kernel still running when this grid starts)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int c = cb + lane; c < ce; c += 32)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&sColScale[warp][c - cb])),
                      "l"(p.vscale + c)
@@ -815,6 +821,7 @@ __global__ void __launch_bounds__(kThreadsT<H16>, 1)
 
 // Sum of the split partials (in fp64, fixed order) + the kernel's row epilogue.
 __global__ void tc_reduce_kernel(const TcArgs p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // (launched programmatically after the H.V grid)
   if (p.done && *p.done) return;
   const int64_t lr = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
@@ -881,6 +888,9 @@ constexpr int kSplitCl = 8, kSplitThreads = 256, kSplitKeep = 8;
 __global__ void __cluster_dims__(kSplitCl, 1, 1) __launch_bounds__(kSplitThreads)
     split_v_f16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, __half* v1, __half* v2, int64_t ldw,
                        float* vscale) {
+  // the H.V grid may start its fill (A / B loads, Gram, K conversion) now;
+  // it waits for this grid before touching V's planes and scales
+  asm volatile("griddepcontrol.launch_dependents;");
   const int c = blockIdx.y;
   const uint32_t rank = cluster_ctarank();
   const int64_t b0 = nv * rank / kSplitCl, b1 = nv * (rank + 1) / kSplitCl;
@@ -1159,13 +1169,36 @@ void TcOperands::build(const float* xs, int64_t n_, int dp, int d_, cudaStream_t
   valid = true;
 }
 
+// Programmatic dependent launch (the fp16 engine): the H.V grid starts while
+// split_v_f16 runs (its fill overlaps the split), the reduction as soon as the
+// H.V grid ends.  WGP_TC_NO_PDL=1: ordinary stream order (A/B).
+bool tc_pdl() {
+  static const bool off = getenv("WGP_TC_NO_PDL") != nullptr;
+  return !off;
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, int smem, cudaStream_t st, bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  WGP_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 template <bool H16>
 void launch_tc(const CUtensorMap& mAhi, const CUtensorMap& mAlo, const CUtensorMap& mBhi, const CUtensorMap& mBlo,
                const CUtensorMap& mPart,
                const CUtensorMap& mVhi, const CUtensorMap& mVlo, const TcArgs& a, unsigned grid, int smem,
-               cudaStream_t st) {
+               cudaStream_t st, bool pdl) {
   WGP_SMEM_ATTR(hv_tc_kernel<H16>, kSmemLimit);
-  hv_tc_kernel<H16><<<grid, kThreadsT<H16>, smem, st>>>(mAhi, mAlo, mBhi, mBlo, mVhi, mVlo, mPart, a);
+  launch_pdl(hv_tc_kernel<H16>, dim3(grid), dim3(kThreadsT<H16>), smem, st, pdl, mAhi, mAlo, mBhi, mBlo, mVhi, mVlo,
+             mPart, a);
   WGP_LAUNCH_CHECK();
 }
 
@@ -1489,17 +1522,21 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
     WGP_CUDA(cudaEventCreate(&ev1));
     WGP_CUDA(cudaEventRecord(ev0, st));
   }
+  // PDL after the fp16 split only (the tf32 engine's planes may come from the
+  // caller's kernels, which do not trigger)
+  const bool pdl = bf16 && !pre && tc_pdl() && !ops.profiling && !tracing;
   if (bf16)
-    launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st);
+    launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st, pdl);
   else
-    launch_tc<false>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st);
+    launch_tc<false>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st, false);
   if (ops.profiling) {
     WGP_CUDA(cudaEventRecord(ev1, st));
     ops.events.emplace_back(ev0, ev1);
   }
   if (tracing) trace_report(a, static_cast<int>(static_cast<int64_t>(a.num_jt) / a.splits), grid, st);
   if (a.splits > 1) {
-    tc_reduce_kernel<<<dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), 256, 0, st>>>(a);
+    launch_pdl(tc_reduce_kernel, dim3(static_cast<unsigned>(ceil_div(hp.m, 256)), s), dim3(256), 0, st,
+               bf16 && tc_pdl() && !ops.profiling, a);
     WGP_LAUNCH_CHECK();
   }
 }

@@ -26,7 +26,8 @@ with torch.cuda.stream(st):
     for _ in range(3):
         ctx.hv_device(Vt.data_ptr(), n, s, out.data_ptr(), n)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if impl in ("tc", "tc_f16"):
+    prof = impl in ("tc", "tc_f16") and not os.environ.get("TIME_HV_NOPROF")
+    if prof:
         ctx.profile(True)
     a.record(st)
     for _ in range(reps):
@@ -34,7 +35,7 @@ with torch.cuda.stream(st):
     b.record(st)
     b.synchronize()
 ms = a.elapsed_time(b) / reps
-kms, kl = ctx.profile_read() if impl in ("tc", "tc_f16") else (ms * reps, reps)
+kms, kl = ctx.profile_read() if prof else (ms * reps, reps)
 env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("WGP_TC"))
 print(f"impl={impl} n={n} d={d} s={s} [{env}] ms={ms:.4f} kernel_ms={kms / max(kl, 1):.4f} "
       f"entries/s={n * n / ms * 1e3:.3e}")
