@@ -855,11 +855,10 @@ inline dim3 cgrid(int64_t n, int s) {
   const int y = std::max(1, std::min(groups, (592 + rb - 1) / rb));
   return dim3(static_cast<unsigned>(rb), static_cast<unsigned>(y));
 }
-// the cooperative cg_fused kernel: every CTA resident (<= 2 per SM at 256 threads)
-inline dim3 coop_grid(int64_t n, int s) {
-  const int rb = reduce_blocks(n);
-  return dim3(static_cast<unsigned>(rb), rb < 148 ? static_cast<unsigned>((s + 3) / 4) : 1u);
-}
+// the cooperative cg_fused kernel: every CTA resident; column groups as in
+// cgrid (~4 CTAs per SM): one column group per CTA left config 2's fused fp64
+// iteration latency-bound (161 CTAs walking 17 groups of 4 columns: 226 us)
+inline dim3 coop_grid(int64_t n, int s) { return cgrid(n, s); }
 
 void check_s(int s) {
   if (s < 1 || s >= SMAX) throw std::invalid_argument("solver kernels support 1 <= s < 256 columns");
