@@ -459,50 +459,51 @@ __device__ __forceinline__ int col_exp(unsigned long long mbits) {
 // vscale[c] = 2^-e_c.  One thread per 16-byte chunk of bytes / per tail value.
 __global__ void i8_vimg_kernel(const double* V, int64_t ldv, int64_t n, int s_mma, int tail, int spad, int num_jt,
                                const unsigned long long* colbits, uint8_t* img, double* vscale) {
+  // one thread per (tile, column, 16-point chunk): all seven digits of its 16
+  // values (each value converted once), then the tail values
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t nbyte = static_cast<int64_t>(kNVB) * spad * 4, per_tile = nbyte + static_cast<int64_t>(tail) * TJ;
+  const int64_t nchunk = static_cast<int64_t>(spad) * 4, per_tile = nchunk + static_cast<int64_t>(tail) * TJ;
   if (idx >= per_tile * num_jt) return;
   const int64_t t = idx / per_tile;
   const int rem = static_cast<int>(idx - t * per_tile);
   uint8_t* timg = img + t * static_cast<int64_t>(vstage_bytes(spad, tail));
-  if (rem >= nbyte) {  // a tail value
-    const int q = rem - static_cast<int>(nbyte), c = q / TJ, pt = q % TJ;
+  if (rem >= nchunk) {  // a tail value
+    const int q = rem - static_cast<int>(nchunk), c = q / TJ, pt = q % TJ;
     const int64_t j = t * TJ + pt;
     reinterpret_cast<double*>(timg + kNVB * spad * 64)[c * TJ + pt] = j < n ? V[j + (s_mma + c) * ldv] : 0.0;
     return;
   }
-  const int blk = rem / (spad * 4), row = (rem / 4) % spad, chunk = rem % 4;
+  const int row = rem / 4, chunk = rem % 4;
   const int c = row;
-  const int digit = blk;
   const int p0 = 16 * chunk;
-  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  uint32_t w[kNVB][4] = {};
   if (c < s_mma) {
     const int e = col_exp(colbits[c]);
     const double sc = ldexp(1.0, e);
-    if (t == 0 && blk == 0 && chunk == 0) {  // a non-finite column propagates NaN like the fp64 product
+    if (t == 0 && chunk == 0) {  // a non-finite column propagates NaN like the fp64 product
       const double m = __longlong_as_double(static_cast<long long>(colbits[c]));
       vscale[c] = isfinite(m) ? ldexp(1.0, -e) : __longlong_as_double(0x7FF8000000000000LL);
     }
 #pragma unroll 4
     for (int k = 0; k < 16; ++k) {
       const int64_t j = t * TJ + p0 + k;
-      int dv = 0;
+      long long vi = 0;
       if (j < n) {
         const double x = V[j + c * ldv] * sc;
-        long long vi = isfinite(x) ? __double2ll_rn(x) : 0ll;
-#pragma unroll 1
-        for (int q = 0; q <= digit; ++q) {  // balanced base-256 digits, least significant first
-          const int dq = static_cast<int>(static_cast<signed char>(vi & 0xFF));
-          vi = (vi - dq) >> 8;
-          dv = dq;
-        }
+        vi = isfinite(x) ? __double2ll_rn(x) : 0ll;
       }
-      w[k / 4] |= (static_cast<uint32_t>(dv) & 0xFFu) << (8 * (k % 4));
+#pragma unroll
+      for (int q = 0; q < kNVB; ++q) {  // balanced base-256 digits, least significant first
+        const int dq = static_cast<int>(static_cast<signed char>(vi & 0xFF));
+        vi = (vi - dq) >> 8;
+        w[q][k / 4] |= (static_cast<uint32_t>(dq) & 0xFFu) << (8 * (k % 4));
+      }
     }
   }
-  uint8_t* dst = timg + static_cast<int64_t>(blk) * spad * 64 + (row >> 3) * 512 + (row & 7) * 64 +
-                 ((chunk ^ ((row & 7) >> 1)) << 4);
-  *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+  uint8_t* dst = timg + (row >> 3) * 512 + (row & 7) * 64 + ((chunk ^ ((row & 7) >> 1)) << 4);
+#pragma unroll
+  for (int q = 0; q < kNVB; ++q)
+    *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(q) * spad * 64) = make_uint4(w[q][0], w[q][1], w[q][2], w[q][3]);
 }
 
 // xtile[t][k][p] = -xs[64 t + p][k] (points past n_pad read as zero rows of
@@ -561,7 +562,7 @@ static void i8_launch(const Hv64Params& hp, int c_off, int s_mma, int tail, int 
   i8_colmax_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(64, ceil_div(hp.n, 256))), s_mma), 256, 0,
                      st>>>(V, hp.ldv, hp.n, colbits);
   WGP_LAUNCH_CHECK();
-  const int64_t items = (static_cast<int64_t>(kNVB) * spad * 4 + static_cast<int64_t>(tail) * TJ) * num_jt;
+  const int64_t items = (static_cast<int64_t>(spad) * 4 + static_cast<int64_t>(tail) * TJ) * num_jt;
   i8_vimg_kernel<<<static_cast<unsigned>(ceil_div(items, 256)), 256, 0, st>>>(V, hp.ldv, hp.n, s_mma, tail, spad,
                                                                             num_jt, colbits, img, vscale);
   WGP_LAUNCH_CHECK();
