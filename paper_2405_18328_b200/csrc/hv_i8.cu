@@ -9,7 +9,7 @@
 //     itself for k_ij >= sf^2 2^-15, within 2^-39 sf^2 below -- the same
 //     FIXED symmetric operator up to those tiny entries (fixed
 //     symmetric perturbations cost CG nothing; noise that is not a fixed
-//     linear map does), split into four unsigned bytes K = sum_i K_i 256^i;
+//     linear map does), split into five unsigned bytes K = sum_i K_i 256^i;
 //   * V: each column scaled by a power of two 2^e_c so its max |v| lands in
 //     [2^53, 2^54), rounded to an integer (2^-53 of the column max) and split
 //     into seven balanced signed bytes V = sum_j V_j 256^j;
@@ -21,19 +21,20 @@
 //     5..10 -- linear to ~1e-12 -- cost CG 5-11% more iterations than the
 //     DMMA engine on fixed config-2 systems: scripts/diag_cg_engines.py.)
 // Eight classes of N = s padded to 16 int32 columns fill TMEM for s <= 64;
-// the 65th column (the configs' s = 65: 64 probes + y) and up to three more
-// run on the fp64 pipe in the entry warps (one DFMA per entry and column,
-// exactly the DMMA engine's arithmetic); wider V is done in column chunks.
+// the 65th column (the configs' s = 65: 64 probes + y) runs on the fp64 pipe
+// in the entry warps (one DFMA per entry, exactly the DMMA engine's
+// arithmetic); wider V is done in column chunks (each re-evaluates K).
 // One MMA per K byte covers up to 256 / N consecutive V bytes (their classes
 // are consecutive accumulators): 18 kind::i8 MMAs (M = 128, K = 32) per
 // 64-point tile at s = 65.
 //
-// Warp roles (320 threads): warps 0..7 evaluate the entries (warp w: rows
-// 32 (w % 4) .. +31 = its TMEM lane quarter, points 32 (w / 4) .. +31 of each
-// tile) and write K's bytes into the 128-byte-swizzled K-major A operand in
-// shared memory, and drain the accumulators into the fp64 split partials;
-// warp 8 streams the per-tile V byte images (pre-swizzled by i8_vimg_kernel)
-// and the points' coordinates with 1-D bulk copies; warp 9 issues the MMAs.
+// Warp roles (576 threads): warps 0..15 evaluate the entries (warp w: rows
+// 32 (w % 4) .. +31 = its TMEM lane quarter, points 16 (w / 4) .. +15 of each
+// tile) and write K's bytes into the 64-byte-swizzled K-major A operand in
+// shared memory (one 8 KB block per byte), accumulate the 65th column, and
+// drain / re-zero the accumulators into the fp64 split partials; warp 16
+// streams the per-tile V byte images (pre-swizzled by i8_vimg_kernel) and the
+// tile's negated coordinates with 1-D bulk copies; warp 17 issues the MMAs.
 // Output: fp64 split partials in hv64's layout (hv64_reduce_kernel / the
 // CG fold add the diagonal and sum the splits in order).
 #include <algorithm>
@@ -54,17 +55,17 @@ constexpr int kNCls = 8;         // accumulator classes i + j = 3 .. 10
 constexpr int kNVB = 7;          // V bytes 0..6
 constexpr int kMaxSm = 64;       // columns on the tensor core (8 x 64 TMEM columns)
 constexpr int kTailMax = 1;      // column 64 on the fp64 pipe (4 columns: register spills in the entry loop)
-constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (4 x 64 x 255 x 128))
+constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (5 x 64 x 255 x 128) = 205)
 constexpr int kMaxD = 16;        // coordinates kept in registers
 #ifndef WGP_I8_ABLATE
 #define WGP_I8_ABLATE 0
 #endif
 #ifndef WGP_I8_NBK
-#define WGP_I8_NBK 3  // 4.23 vs 4.33 ms per config-2 CG iteration with 2 (interleaved A/B)
+#define WGP_I8_NBK 3  // 4.23 vs 4.33 ms per config-2 CG iteration with 2 (interleaved A/B, before the tail fixes)
 #endif
 constexpr int NBK = WGP_I8_NBK, NV = 3;   // K buffers, V / coordinate stages
 #ifndef WGP_I8_EPI
-#define WGP_I8_EPI 16  // 16: 2.91 vs 3.16 ms per config-2 CG iteration with 8 (interleaved A/B)
+#define WGP_I8_EPI 16  // 16: 2.91 vs 3.16 ms per config-2 CG iteration with 8 (interleaved A/B, 6-class version)
 #endif
 constexpr int kEpiWarps = WGP_I8_EPI;                 // entry warps: 4 lane quarters x kEpiWarps / 4 point slices
 constexpr int kWarpProd = kEpiWarps, kWarpMma = kEpiWarps + 1, kThreads = 32 * (kEpiWarps + 2);
