@@ -111,19 +111,22 @@ struct I8Args {
 // shared-memory reads of the operands bound the SS MMAs).  ka / vb: shared
 // addresses of K byte 0 and V byte 0.  The accumulators are zeroed by the
 // entry warps at the start and after every drain, so every MMA accumulates.
-__device__ __forceinline__ void mma_tile_i8(uint32_t d, const uint8_t* ka, const uint8_t* vb, int spad,
-                                            uint32_t idesc_base) {
-  const int G = 256 / spad < kNVB ? 256 / spad : kNVB;  // bytes per instruction
+// (SPAD known at compile time: every descriptor is the tile's two base
+// descriptors plus a constant, ~3 instructions per MMA for the issuing
+// thread instead of ~25 with runtime group bounds and descriptor builds)
+template <int SPAD>
+__device__ __forceinline__ void mma_tile_i8_t(uint32_t d, uint64_t ka, uint64_t vb, uint32_t idesc_base) {
+  constexpr int G = 256 / SPAD < kNVB ? 256 / SPAD : kNVB;  // bytes per instruction
 #pragma unroll
   for (int i = 0; i < kNKB; ++i) {
     const int j0 = 3 - i > 0 ? 3 - i : 0;
-#pragma unroll 1
+#pragma unroll
     for (int jg = j0; jg < kNVB; jg += G) {
       const int L = kNVB - jg < G ? kNVB - jg : G;
-      const uint64_t a = umma_desc_sw64(ka + i * kKBlk);
-      const uint64_t b = umma_desc_sw64(vb + jg * spad * 64);
-      const uint32_t dc = d + static_cast<uint32_t>(spad * (i + jg - 3));
-      const uint32_t idesc = idesc_base | (static_cast<uint32_t>((L * spad) >> 3) << 17);
+      const uint64_t a = ka + static_cast<uint64_t>(i * (kKBlk >> 4));
+      const uint64_t b = vb + static_cast<uint64_t>(jg * (SPAD * 64 >> 4));
+      const uint32_t dc = d + static_cast<uint32_t>(SPAD * (i + jg - 3));
+      const uint32_t idesc = idesc_base | (static_cast<uint32_t>((L * SPAD) >> 3) << 17);
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
         asm volatile("tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, 1;" ::"r"(dc), "l"(a + 2 * ks),
@@ -131,22 +134,18 @@ __device__ __forceinline__ void mma_tile_i8(uint32_t d, const uint8_t* ka, const
     }
   }
 }
-
-#ifndef WGP_I8_F2D_ALU
-#define WGP_I8_F2D_ALU 0
-#endif
-// fp32 -> fp64 of an entry for the tail columns: F2F, or (WGP_I8_F2D_ALU) the
-// bits re-biased on the integer pipe (exact for normal numbers; subnormals,
-// entries under 2^-126 in units of sf^2 2^-eK, as 0)
-__device__ __forceinline__ double f2d(float x) {
-#if WGP_I8_F2D_ALU
-  const uint32_t b = __float_as_uint(x);
-  const bool nz = b >= 0x00800000u;
-  return __hiloint2double(static_cast<int>(nz ? (b >> 3) + (896u << 20) : 0u), static_cast<int>(nz ? (b << 29) : 0u));
-#else
-  return static_cast<double>(x);
-#endif
+__device__ __forceinline__ void mma_tile_i8(uint32_t d, uint64_t ka, uint64_t vb, int spad, uint32_t idesc_base) {
+  switch (spad) {
+    case 16: mma_tile_i8_t<16>(d, ka, vb, idesc_base); break;
+    case 32: mma_tile_i8_t<32>(d, ka, vb, idesc_base); break;
+    case 48: mma_tile_i8_t<48>(d, ka, vb, idesc_base); break;
+    default: mma_tile_i8_t<64>(d, ka, vb, idesc_base); break;
+  }
 }
+
+// fp32 -> fp64 of an entry for the 65th column (F2F; the bits re-biased on
+// the integer pipe instead measured the same)
+__device__ __forceinline__ double f2d(float x) { return static_cast<double>(x); }
 
 __device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr), "r"(0)
@@ -206,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
     }
   } else if (warp == kWarpMma) {
     // -------------------------------------------------------------- MMA issuer
+    const uint64_t dK0 = umma_desc_sw64(sK), dV0 = umma_desc_sw64(sV);  // + (byte offset >> 4) per buffer / stage
     const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) |
                            (static_cast<uint32_t>(TI >> 4) << 24);  // D s32, A u8, B s8, K-major (+ N per group)
     int nz = 0;  // accumulator zeroings (the start, then after every drain)
@@ -218,12 +218,11 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
       mbar_wait(&bar_kfull[b], (t / NBK) & 1);
       mbar_wait(&bar_vfull[st], (t / NV) & 1);
       tc_after();
-      const uint8_t* kb = sK + b * kKBuf;
-      const uint8_t* vb = sV + st * vsb;
       // lane 0 issues the tile's MMAs and the commits that track them
       if (lane == 0) {
 #if !(WGP_I8_ABLATE & 1)  // (ablation build: no MMAs)
-        mma_tile_i8(tmem, kb, vb, p.spad, idesc);
+        mma_tile_i8(tmem, dK0 + static_cast<uint64_t>((b * kKBuf) >> 4), dV0 + static_cast<uint64_t>((st * vsb) >> 4),
+                    p.spad, idesc);
 #endif
         commit_one(&bar_mdone[t & 7]);
         if ((t + 1) % kChunk == 0 || t == T - 1) commit_one(&bar_ofull);
