@@ -1522,9 +1522,10 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
     WGP_CUDA(cudaEventCreate(&ev1));
     WGP_CUDA(cudaEventRecord(ev0, st));
   }
-  // PDL after the fp16 split only (the tf32 engine's planes may come from the
-  // caller's kernels, which do not trigger)
-  const bool pdl = bf16 && !pre && tc_pdl() && !ops.profiling && !tracing;
+  // PDL after the fp16 split only: the tf32 engine's planes may come from the
+  // caller's kernels, and with gathered rows the kernel right before this one
+  // writes A (the A / B producer does not wait)
+  const bool pdl = bf16 && !pre && !hp.row_idx && tc_pdl() && !ops.profiling && !tracing;
   if (bf16)
     launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st, pdl);
   else
