@@ -28,13 +28,14 @@
 // are consecutive accumulators): 18 kind::i8 MMAs (M = 128, K = 32) per
 // 64-point tile at s = 65.
 //
-// Warp roles (576 threads): warps 0..15 evaluate the entries (warp w: rows
-// 32 (w % 4) .. +31 = its TMEM lane quarter, points 16 (w / 4) .. +15 of each
-// tile) and write K's bytes into the 64-byte-swizzled K-major A operand in
-// shared memory (one 8 KB block per byte), accumulate the 65th column, and
-// drain / re-zero the accumulators into the fp64 split partials; warp 16
-// streams the per-tile V byte images (pre-swizzled by i8_vimg_kernel) and the
-// tile's negated coordinates with 1-D bulk copies; warp 17 issues the MMAs.
+// Warp roles (320 threads): warps 0..7 evaluate the entries (warp w: rows
+// 32 (w % 4) .. +31 = its TMEM lane quarter, points 32 (w / 4) .. +31 of each
+// tile, all 32 at once for independent dependency chains) and write K's bytes
+// into the 64-byte-swizzled K-major A operand in shared memory (one 8 KB block
+// per byte), accumulate the 65th column, and drain / re-zero the accumulators
+// into the fp64 split partials; warp 8 streams the per-tile V byte images
+// (pre-swizzled by i8_vimg_kernel) and the tile's negated coordinates with 1-D
+// bulk copies; warp 9 issues the MMAs.
 // Output: fp64 split partials in hv64's layout (hv64_reduce_kernel / the
 // CG fold add the diagonal and sum the splits in order).
 #include <algorithm>
@@ -65,11 +66,16 @@ constexpr int kMaxD = 16;        // coordinates kept in registers
 #endif
 constexpr int NBK = WGP_I8_NBK, NV = 3;   // K buffers, V / coordinate stages
 #ifndef WGP_I8_EPI
-#define WGP_I8_EPI 16  // 16: 2.91 vs 3.16 ms per config-2 CG iteration with 8 (interleaved A/B, 6-class version)
+#define WGP_I8_EPI 8  // with 32-point groups: 3.31 ms per config-2 CG iteration vs 3.47 for 16 warps x 16-point groups (interleaved A/B)
 #endif
 constexpr int kEpiWarps = WGP_I8_EPI;                 // entry warps: 4 lane quarters x kEpiWarps / 4 point slices
 constexpr int kWarpProd = kEpiWarps, kWarpMma = kEpiWarps + 1, kThreads = 32 * (kEpiWarps + 2);
 constexpr int kPW = 4 * TJ / kEpiWarps;               // points per entry warp per tile (32 or 16)
+#ifndef WGP_I8_G
+#define WGP_I8_G 32  // one group per warp-tile: 16-point groups 3.43 vs 8-point 3.87 ms (16 warps), 32 with 8 warps 3.31 ms -- independent chains
+#endif
+constexpr int kG = WGP_I8_G;                          // points per entry group (8 or 16)
+static_assert(kPW % kG == 0 && kG % 4 == 0, "entry groups of whole quads");
 static_assert(kPW % 16 == 0, "16-byte K chunks per warp");
 constexpr int kNKB = 5;                            // K bytes (39-bit K)
 constexpr uint32_t kKBlk = TI * 64u;           // one K byte: 128 rows x 64 points, 64-byte swizzle
@@ -283,43 +289,42 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
         for (int c = 0; c < kPW / 4; ++c) w[i][c] = 0u;
 #else
 #pragma unroll
-      for (int grp = 0; grp < kPW / 8; ++grp) {  // 8 points at a time, packed in pairs
-        float2 r2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                        make_float2(0.f, 0.f)};
+      for (int grp = 0; grp < kPW / kG; ++grp) {  // kG points at a time, packed in pairs
+        float2 r2[kG / 2];
+#pragma unroll
+        for (int e = 0; e < kG / 2; ++e) r2[e] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < D; ++k) {
           // explicit shared-space loads (a generic load through the cast
           // pointer waits on the long scoreboard)
-          float4 a, c;
-          const uint32_t ad = xt_s + static_cast<uint32_t>((k * TJ + 8 * grp) * 4);
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(ad));
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w)
-                       : "r"(ad + 16));
-          const float2 d0 = __fadd2_rn(xi2[k], make_float2(a.x, a.y));
-          const float2 d1 = __fadd2_rn(xi2[k], make_float2(a.z, a.w));
-          const float2 d2 = __fadd2_rn(xi2[k], make_float2(c.x, c.y));
-          const float2 d3 = __fadd2_rn(xi2[k], make_float2(c.z, c.w));
-          r2[0] = __ffma2_rn(d0, d0, r2[0]);
-          r2[1] = __ffma2_rn(d1, d1, r2[1]);
-          r2[2] = __ffma2_rn(d2, d2, r2[2]);
-          r2[3] = __ffma2_rn(d3, d3, r2[3]);
-        }
-        float kp[8];  // the entries scaled by 2^eK, zero where excluded
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+          for (int qd = 0; qd < kG / 4; ++qd) {
+            float4 a;
+            const uint32_t ad = xt_s + static_cast<uint32_t>((k * TJ + kG * grp + 4 * qd) * 4);
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
+                         : "r"(ad));
+            const float2 d0 = __fadd2_rn(xi2[k], make_float2(a.x, a.y));
+            const float2 d1 = __fadd2_rn(xi2[k], make_float2(a.z, a.w));
+            r2[2 * qd] = __ffma2_rn(d0, d0, r2[2 * qd]);
+            r2[2 * qd + 1] = __ffma2_rn(d1, d1, r2[2 * qd + 1]);
+          }
+        }
+        float kp[kG];  // the entries scaled by 2^eK, zero where excluded
+#pragma unroll
+        for (int e = 0; e < kG; ++e) {
           const float rr = (e & 1) ? r2[e >> 1].y : r2[e >> 1].x;
           kp[e] = matern_from_u(sqrt_approx(rr), hsS, haS);
         }
         if (edge) {  // the diagonal (H_ii V_i is added exactly in the reduction) and points >= n
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int64_t gj = pbase + 8 * grp + e;
+          for (int e = 0; e < kG; ++e) {
+            const int64_t gj = pbase + kG * grp + e;
             if (gj >= p.n || gj == g) kp[e] = 0.f;
           }
         }
-        uint32_t K[8], KH[8];  // low 32 bits, bits 32..38
+        uint32_t K[kG], KH[kG];  // low 32 bits, bits 32..38
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int e = 0; e < kG; ++e) {
           // (the float's bits shifted on the integer pipe instead: 4.7 vs
           // 4.2 ms per config-2 CG iteration -- issue slots, not the
           // conversion pipe, bind)
@@ -329,9 +334,9 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
           KH[e] = static_cast<uint32_t>(kv >> 32);
         }
         if (p.tail > 0) {  // column 64: fp64 FMA of the fp32 entry (the DMMA engine's arithmetic), four chains
-          const uint32_t vt = smem_u32(sV + st * vsb + kNVB * p.spad * 64) + 8u * (kPW * h + 8 * grp);
+          const uint32_t vt = smem_u32(sV + st * vsb + kNVB * p.spad * 64) + 8u * (kPW * h + kG * grp);
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
+          for (int e = 0; e < kG; e += 2) {
             double v0, v1;
             asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(vt + 8u * e));
             acct[e & 3] = fma(f2d(kp[e]), v0, acct[e & 3]);
@@ -340,17 +345,18 @@ __global__ void __launch_bounds__(kThreads, 1) hv_i8_kernel(const I8Args p) {
         }
         // 4 x 4 byte transposes: w[i][.] holds byte i of 4 consecutive points
 #pragma unroll
-        for (int hq = 0; hq < 2; ++hq) {
+        for (int hq = 0; hq < kG / 4; ++hq) {
           const uint32_t t0 = __byte_perm(K[4 * hq], K[4 * hq + 1], 0x5140);
           const uint32_t t1 = __byte_perm(K[4 * hq], K[4 * hq + 1], 0x7362);
           const uint32_t t2 = __byte_perm(K[4 * hq + 2], K[4 * hq + 3], 0x5140);
           const uint32_t t3 = __byte_perm(K[4 * hq + 2], K[4 * hq + 3], 0x7362);
-          w[0][2 * grp + hq] = __byte_perm(t0, t2, 0x5410);
-          w[1][2 * grp + hq] = __byte_perm(t0, t2, 0x7632);
-          w[2][2 * grp + hq] = __byte_perm(t1, t3, 0x5410);
-          w[3][2 * grp + hq] = __byte_perm(t1, t3, 0x7632);
-          w[4][2 * grp + hq] = __byte_perm(__byte_perm(KH[4 * hq], KH[4 * hq + 1], 0x0040),
-                                           __byte_perm(KH[4 * hq + 2], KH[4 * hq + 3], 0x0040), 0x5410);
+          const int wi = (kG / 4) * grp + hq;
+          w[0][wi] = __byte_perm(t0, t2, 0x5410);
+          w[1][wi] = __byte_perm(t0, t2, 0x7632);
+          w[2][wi] = __byte_perm(t1, t3, 0x5410);
+          w[3][wi] = __byte_perm(t1, t3, 0x7632);
+          w[4][wi] = __byte_perm(__byte_perm(KH[4 * hq], KH[4 * hq + 1], 0x0040),
+                                 __byte_perm(KH[4 * hq + 2], KH[4 * hq + 3], 0x0040), 0x5410);
         }
       }
 #endif
