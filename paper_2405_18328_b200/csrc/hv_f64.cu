@@ -295,9 +295,9 @@ int hv64_splits(int64_t n) {
 
 // The operator engine: the exact integer-slice product on the int8 tensor
 // core (hv_i8.cu) from n = 4096 points on (config-2-shaped data, s = 65, per
-// CG iteration: 101 vs 132 us at n = 4096, 780 vs 1458 us at 16384,
+// CG iteration: 92 vs 128 us at n = 4096, 625 vs 1456 us at 16384,
 // scripts/time_cg64_sizes.py), the DMMA kernel below for smaller n (its
-// latency is lower: 39 vs 51 us at config 0, n = 2048) and d > 16.  Keyed on
+// latency is lower: 39.5 vs 49.3 us at config 0, n = 2048) and d > 16.  Keyed on
 // the global n, so every row shard uses the same engine.
 // WGP_HV64_ENGINE=dmma | i8 forces one (A/B, tests).
 static bool use_i8(int64_t n, int d, int s) {
