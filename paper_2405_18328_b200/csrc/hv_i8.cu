@@ -14,7 +14,7 @@
 //     [2^53, 2^54), rounded to an integer (2^-53 of the column max) and split
 //     into seven balanced signed bytes V = sum_j V_j 256^j;
 //   * K.V = sum_ij 256^(i+j) K_i V_j: every byte product is exact and every
-//     int32 accumulation is exact (drained to fp64 every 128 tiles, before it
+//     int32 accumulation is exact (drained to fp64 every 192 tiles, before it
 //     could overflow).  Classes i + j = 3..10 are kept (29 byte pairs); the
 //     dropped classes 0..2 weigh < 2^-60 of the result, so the product is
 //     linear in V to fp64 rounding and deterministic.  (Keeping only classes
@@ -56,7 +56,7 @@ constexpr int kNCls = 8;         // accumulator classes i + j = 3 .. 10
 constexpr int kNVB = 7;          // V bytes 0..6
 constexpr int kMaxSm = 64;       // columns on the tensor core (8 x 64 TMEM columns)
 constexpr int kTailMax = 1;      // column 64 on the fp64 pipe (4 columns: register spills in the entry loop)
-constexpr int kChunk = 128;      // tiles between drains (int32 headroom: < 2^31 / (5 x 64 x 255 x 128) = 205)
+constexpr int kChunk = 192;      // tiles between drains (int32 headroom: < 2^31 / (5 x 64 x 255 x 128) = 205)
 constexpr int kMaxD = 16;        // coordinates kept in registers
 #ifndef WGP_I8_ABLATE
 #define WGP_I8_ABLATE 0

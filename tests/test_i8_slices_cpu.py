@@ -63,7 +63,7 @@ def test_class_sums_reproduce_the_product(seed):
     """sum over kept byte classes w = i + j >= 3 of 256^w sum_{i+j=w} K_i V_j, each
     class an exact integer sum (the int32 accumulators), equals the exact
     integer product up to the dropped classes, which stay below 2^-60 of the
-    column's bound |K|max |V|max n; the int32 headroom covers 128 tiles of 64
+    column's bound |K|max |V|max n; the int32 headroom covers 192 tiles of 64
     points between drains (hv_i8.cu kChunk)."""
     rng = np.random.default_rng(seed)
     n = 300
@@ -85,5 +85,5 @@ def test_class_sums_reproduce_the_product(seed):
     kept = sum(c * 256 ** w for w, c in classes.items() if w >= KEEP)
     bound = 2 ** 39 * 2 ** 54 * n
     assert abs(kept - exact) <= 2.0 ** -60 * bound
-    # one class over 128 tiles of 64 points: <= 5 pairs x 255 x 128 per point
-    assert 5 * 255 * 128 * 64 * 128 < 2 ** 31
+    # one class over 192 tiles of 64 points: <= 5 pairs x 255 x 128 per point
+    assert 5 * 255 * 128 * 64 * 192 < 2 ** 31
