@@ -601,6 +601,8 @@ def main():
         if i >= args.warmup:
             e2e_times.append(a.elapsed_time(b))
     e2e_ms = float(np.mean(e2e_times))
+    e2e_med = float(np.median(e2e_times))
+    print("e2e times (ms):", " ".join(f"{t:.3f}" for t in e2e_times), file=sys.stderr)
     if ws > 1:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -680,7 +682,7 @@ def main():
                    "parallelism": f"rows{ws}" if ws > 1 else "single"},
         "e2e": {"value": n * n / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(n * s * 4), "d2h_bytes_per_step": int(m_out * s * 4),
-                "ms_per_step": e2e_ms},
+                "ms_per_step": e2e_ms, "ms_median": e2e_med},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_profile": traffic_profile,
                      "peak_basis": f"{pk['src']} peaks: F_hv={f_entry} flop/entry; " + basis,

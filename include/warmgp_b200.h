@@ -99,7 +99,11 @@ int wgp_set_rows(wgp_ctx* ctx, int64_t r0, int64_t r1);
 
 /** out = H V = (K + sigma^2 I) V, V/out n x s (host).  Replaces the dense
  *  products H * P / H * X at proj/src/solvers.cpp:71,92,110,120,169,188,211
- *  and proj/src/estimator.cpp:90. */
+ *  and proj/src/estimator.cpp:90.  On the tcgen05 engines from
+ *  8192 rows the result's download overlaps the launches (row chunks, each
+ *  chunk's copy under the next chunk; WGP_HV_PIPE=1 turns it off): rows then
+ *  equal wgp_hv_device's one-launch product to fp32 rounding, not bitwise.
+ *  Page-locked host buffers make the copies asynchronous. */
 int wgp_hv(wgp_ctx* ctx, const float* V_host, int s, float* out_host);
 /** fp64 H V on host fp64 V / out (n x s; rows of wgp_set_rows): the operator
  *  of the fp64 CG path -- entries evaluated in fp32 (bitwise symmetric),

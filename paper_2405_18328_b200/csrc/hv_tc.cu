@@ -1210,6 +1210,21 @@ int tc_sm_count() { return sm_count(); }
 
 bool hv_tc_supported(int d, int s) { return d + 2 <= kKA && s >= 1 && s <= 128; }
 
+// choose_splits' cost model of one launch over m rows and nv points, in
+// J-tile units of one CTA (wgp_hv picks its row chunks with it; the L2 split
+// floor as in hv_tc, partial cap left out)
+double hv_tc_model_cost(int64_t m, int64_t nv, int s, bool f16) {
+  const int TJ = f16 ? Cfg<true>::kTJ : Cfg<false>::kTJ;
+  const int jt = static_cast<int>(ceil_div(nv, TJ));
+  const int64_t rt = ceil_div(m, kTI);
+  const double spad = static_cast<double>(round_up(s, 16));
+  const int min_sp = std::max(1, std::min(64, static_cast<int>(std::ceil(static_cast<double>(nv) *
+                                                                        (256.0 + 2.0 * (f16 ? 2 : 4) * spad) / 48e6))));
+  const int sp = choose_splits(rt, jt, sm_count(), min_sp);
+  return std::ceil(static_cast<double>(rt * sp) / sm_count()) * (std::ceil(static_cast<double>(jt) / sp) + 16.0) +
+         (sp > 1 ? 4.0 + 0.5 * sp : 0.0);
+}
+
 // WGP_TC_TRACE report: per-tile stamps of CTA 0 (T0 steady-state tiles) and per-CTA timers.
 void trace_report(const TcArgs& a, int T0, unsigned grid, cudaStream_t st) {
     std::vector<long long> h(16 * (a.num_jt + 4));
@@ -1322,6 +1337,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
       q.out = hp.out + c0 * hp.ldo;
       if (hp.B) q.B = hp.B + c0 * hp.ldb;
       q.vplanes = nullptr;
+      q.reuse_vsplit = false;
       hv_tc(ops, q, st, bf16);
     }
     return;
@@ -1350,7 +1366,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
                   : vhi + esz * ldw * s;
   const int64_t ldp = pre ? hp.vplanes_ld : ldw;  // plane leading dimension
   const dim3 vgrid(static_cast<unsigned>(ceil_div(nv, 256)), s);
-  if (pre) {
+  if (pre || hp.reuse_vsplit) {
   } else if (bf16) {
     split_v_f16_kernel<<<dim3(kSplitCl, s), kSplitThreads, 0, st>>>(hp.V, hp.ldv, hp.j0, nv,
                                                                      reinterpret_cast<__half*>(vhi),
@@ -1525,7 +1541,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   // PDL after the fp16 split only: the tf32 engine's planes may come from the
   // caller's kernels, and with gathered rows the kernel right before this one
   // writes A (the A / B producer does not wait)
-  const bool pdl = bf16 && !pre && !hp.row_idx && tc_pdl() && !ops.profiling && !tracing;
+  const bool pdl = bf16 && !pre && !hp.reuse_vsplit && !hp.row_idx && tc_pdl() && !ops.profiling && !tracing;
   if (bf16)
     launch_tc<true>(mAhi, mAlo, mBhi, mBlo, mPart, mVhi, mVlo, a, grid, smem, st, pdl);
   else

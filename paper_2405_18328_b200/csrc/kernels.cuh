@@ -50,6 +50,8 @@ struct HvParams {
   const float* vplanes;  // optional caller-maintained tf32 planes of V (hv_tc, s <= 96):
   int64_t vplanes_ld;    // hi[j + c ld], lo[j + (s + c) ld] for global j, bitwise
                          // split_v's; the launch then skips its own split of V
+  bool reuse_vsplit;     // hv_tc: the previous launch split this same V[j0:j1, :s] (row
+                         // chunks of one product, wgp_hv): skip the split, reuse its planes
 };
 
 // SIMT fp32 fused H.V (direct differences; any d, s <= 128).
@@ -59,6 +61,7 @@ void hv_simt(const HvParams& p, cudaStream_t st);
 // if the shape is unsupported (caller falls back to the SIMT CUDA kernel).
 struct TcPoints;  // prepared operand set, see hv_tc.cu
 bool hv_tc_supported(int d, int s);
+double hv_tc_model_cost(int64_t m, int64_t nv, int s, bool f16);
 
 // Gradient contractions.  W_ij = 1/2 vy_i vy_j (A) and
 // coef_b sum_c L_ic R_jc (B).  Writes per-block fp64 partials

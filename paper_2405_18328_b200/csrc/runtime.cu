@@ -309,9 +309,16 @@ struct Ctx {
   Buf cublas_ws;  // explicit cuBLAS workspace: no allocation inside a captured AP epoch
   PinnedCtrl hctrl;
   PinnedBuf sgd_hidx;  // SGD minibatch indices, two rounds (double buffer)
+  // wgp_hv's row-chunk pipeline: the result's device->host copy of one chunk
+  // runs on its own stream under the next chunk's H.V
+  cudaStream_t cst = nullptr;
+  cudaEvent_t ev_chunk = nullptr, ev_copied = nullptr;
 
   ~Ctx() {
     drop_cg_graphs();
+    if (ev_chunk) cudaEventDestroy(ev_chunk);
+    if (ev_copied) cudaEventDestroy(ev_copied);
+    if (cst) cudaStreamDestroy(cst);
     if (cublas) cublasDestroy(cublas);
     if (cusolver) cusolverDnDestroy(cusolver);
     if (st) cudaStreamDestroy(st);
@@ -394,8 +401,9 @@ struct Ctx {
   void hv(const float* V, int64_t ldv, int s, float* out, int64_t ldo, int mode, const float* B,
           int64_t ldb, int64_t j0, int64_t j1, const int* row_idx, int64_t rr0, int64_t m,
           const int* done = nullptr, bool shard_invariant = true, const float* vplanes = nullptr,
-          int64_t vplanes_ld = 0) {
+          int64_t vplanes_ld = 0, bool reuse_vsplit = false) {
     HvParams p{};
+    p.reuse_vsplit = reuse_vsplit;
     p.vplanes = vplanes;
     p.vplanes_ld = vplanes_ld;
     p.xs = xs.as<float>();
@@ -2214,6 +2222,78 @@ int wgp_set_rows(wgp_ctx* ctx, int64_t r0, int64_t r1) {
   });
 }
 
+// wgp_hv's copy / compute pipeline on the tcgen05 engines: the product in
+// row chunks, each chunk's result copy running under the next chunk's launch
+// (the short last chunk's copy is the exposed one).  Each launch keys its J
+// splits on its own rows, so the result equals the one-launch product to fp32
+// rounding.  The cut comes from hv_tc's launch cost model (choose_splits) and
+// a PCIe model (D2H 40 GB/s + 10 us): chunks sized to whole waves can even beat the
+// one launch's wave tail (config 1: 0.30 vs 0.33 ms end to end, one launch
+// 0.178 ms on the device).  Cutting the contracted points instead, so that a
+// first J range's launch hides the rest of V's upload, was measured slower
+// (0.315 ms at the best cut, 0.62 ms combined with the row chunks).
+// WGP_HV_PIPE (read per call): "1" one launch, or comma-separated row fractions.
+struct HvPlan {
+  std::vector<int64_t> cuts{0};  // row offsets of the launches, then m
+};
+
+static HvPlan hv_plan(const wgp::Ctx& c, int64_t m, int s) {
+  const char* env = getenv("WGP_HV_PIPE");  // read per call (A/B within one process)
+  const std::string spec(env ? env : "");
+  HvPlan pl;
+  const bool tc = (c.hv_impl == WGP_HV_TC || c.hv_impl == WGP_HV_TC_F16) && wgp::hv_tc_supported(c.d, s);
+  if (!tc || s > 96 || m < 8192 || spec == "1") {
+    pl.cuts.push_back(m);
+    return pl;
+  }
+  if (!spec.empty()) {  // row fractions
+    std::vector<double> fr;
+    size_t pos = 0;
+    while (pos <= spec.size()) {
+      const size_t q = spec.find(',', pos);
+      const std::string t = spec.substr(pos, q == std::string::npos ? std::string::npos : q - pos);
+      if (!t.empty()) fr.push_back(std::max(0.0, atof(t.c_str())));
+      if (q == std::string::npos) break;
+      pos = q + 1;
+    }
+    double tot = 0, acc = 0;
+    for (double f : fr) tot += f;
+    for (size_t k = 0; k + 1 < fr.size() && tot > 0; ++k) {
+      acc += fr[k] / tot;
+      const int64_t r = wgp::round_up(static_cast<int64_t>(acc * static_cast<double>(m)), 128);
+      if (r > pl.cuts.back() && r < m) pl.cuts.push_back(r);
+    }
+    pl.cuts.push_back(m);
+    return pl;
+  }
+  const bool f16 = c.hv_impl == WGP_HV_TC_F16;
+  // seconds per cost unit (config-1 calibration: 0.166 ms / 213 units fp16,
+  // 0.207 ms / 431 units tf32) plus launch overhead
+  const double t_unit = f16 ? 0.78e-6 : 0.48e-6, t_launch = 4e-6;
+  // D2H 40 GB/s + 10 us per copy: conservative, so the first chunk's copy
+  // stays hidden under the second launch (measured: cuts where the model's
+  // 50 GB/s said "just hidden" ran ~0.01 ms slower)
+  auto d2h = [&](int64_t rows) { return static_cast<double>(rows) * 4.0 * s / 40e9 + 10e-6; };
+  auto T = [&](int64_t rows) { return wgp::hv_tc_model_cost(rows, c.n, s, f16) * t_unit + t_launch; };
+  double best = T(m) + d2h(m);
+  int64_t cut = 0;
+  const int64_t step = std::max<int64_t>(128, wgp::round_up(m / 64, 128));
+  for (int64_t r = 1024; r <= m - 1024; r += step) {
+    const double e1 = T(r);
+    const double e = std::max(e1 + T(m - r), e1 + d2h(r)) + d2h(m - r);
+    if (e < best - 1e-12) {
+      best = e;
+      cut = r;
+    }
+  }
+  if (cut > 0) pl.cuts.push_back(cut);
+  pl.cuts.push_back(m);
+  if (getenv("WGP_HV_PLAN_DEBUG"))
+    fprintf(stderr, "[wgp_hv plan] m=%lld n=%lld s=%d cut=%lld model %.1f us\n", (long long)m, (long long)c.n, s,
+            (long long)cut, best * 1e6);
+  return pl;
+}
+
 int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
   return guarded([&] {
     wgp::Ctx& c = ctx->c;
@@ -2225,9 +2305,9 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
     // V uploaded as one contiguous copy (leading dimension n: the H.V kernels
     // take any ldv), faster than a pitched copy into the padded layout
     dv.ensure(sizeof(float) * c.ld * s);
-    WGP_CUDA(cudaMemcpyAsync(dv.p, V, sizeof(float) * c.n * s, cudaMemcpyHostToDevice, c.st));
     const int64_t ldv = c.n;
     if (c.sharded()) {  // the rank's rows, then the all-gather of the n x s result
+      WGP_CUDA(cudaMemcpyAsync(dv.p, V, sizeof(float) * c.n * s, cudaMemcpyHostToDevice, c.st));
       dout.ensure(sizeof(float) * c.ld * s);
       float* o = dout.as<float>();
       c.hv(dv.as<float>(), ldv, s, o + c.own0, c.ld, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.own0,
@@ -2238,8 +2318,32 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
     } else {
       const int64_t m = c.r1 - c.r0;
       dout.ensure(sizeof(float) * m * s);
-      c.hv(dv.as<float>(), ldv, s, dout.as<float>(), m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, m);
-      WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(float) * m * s, cudaMemcpyDeviceToHost, c.st));
+      const HvPlan pl = hv_plan(c, m, s);
+      if (!c.cst) {
+        WGP_CUDA(cudaStreamCreateWithFlags(&c.cst, cudaStreamNonBlocking));
+        WGP_CUDA(cudaEventCreateWithFlags(&c.ev_chunk, cudaEventDisableTiming));
+        WGP_CUDA(cudaEventCreateWithFlags(&c.ev_copied, cudaEventDisableTiming));
+      }
+      WGP_CUDA(cudaMemcpyAsync(dv.p, V, sizeof(float) * c.n * s, cudaMemcpyHostToDevice, c.st));
+      if (pl.cuts.size() <= 2) {
+        c.hv(dv.as<float>(), ldv, s, dout.as<float>(), m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, m);
+        WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(float) * m * s, cudaMemcpyDeviceToHost, c.st));
+      } else {
+        float* o = dout.as<float>();
+        // chunk 0 splits V, the others reuse its planes; chunk k's result copy
+        // overlaps chunk k + 1's launch
+        for (size_t k = 0; k + 1 < pl.cuts.size(); ++k) {
+          const int64_t a = pl.cuts[k], len = pl.cuts[k + 1] - pl.cuts[k];
+          c.hv(dv.as<float>(), ldv, s, o + a, m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0 + a, len, nullptr,
+               false, nullptr, 0, k > 0);
+          WGP_CUDA(cudaEventRecord(c.ev_chunk, c.st));
+          WGP_CUDA(cudaStreamWaitEvent(c.cst, c.ev_chunk, 0));
+          WGP_CUDA(cudaMemcpy2DAsync(out + a, sizeof(float) * m, o + a, sizeof(float) * m, sizeof(float) * len, s,
+                                     cudaMemcpyDeviceToHost, c.cst));
+        }
+        WGP_CUDA(cudaEventRecord(c.ev_copied, c.cst));
+        WGP_CUDA(cudaStreamWaitEvent(c.st, c.ev_copied, 0));
+      }
     }
     WGP_CUDA(cudaStreamSynchronize(c.st));
   });

@@ -581,7 +581,15 @@ def test_row_shards_reassemble_bitwise(ctx):
     X, V, ls = make(5000, 9, 65, seed=31)
     ctx.set_data(X)
     ctx.set_hyper([*ls, 1.0, 0.3])
-    full = ctx.hv(V)
+    # the single-GPU result: one launch over all rows (the host entry point
+    # pipelines chunks, equal to fp32 rounding only)
+    Vt = torch.from_numpy(np.ascontiguousarray(V.T)).cuda()
+    O = torch.empty_like(Vt)
+    torch.cuda.synchronize()
+    ctx.hv_device(Vt.data_ptr(), 5000, 65, O.data_ptr(), 5000)
+    torch.cuda.synchronize()
+    full = O.cpu().numpy().T
+    assert rel(ctx.hv(V), full.astype(np.float64)) <= 1e-6
     Vd = torch.from_numpy(V).cuda()
     for world in (2, 3, 8):
         parts = []
@@ -926,3 +934,30 @@ def test_ap_incremental_residual_and_wsd_from_residuals_subprocess():
     assert np.linalg.norm(fast["x"] - ref["x"]) <= 1e-4 * np.linalg.norm(ref["x"])
     assert np.allclose(fast["rel"], ref["rel"], rtol=1e-2)
     assert np.allclose(fast["wsd"], ref["wsd"], rtol=1e-4, atol=1e-9)
+
+
+def test_hv_host_row_chunks_match_one_launch(ctx):
+    """wgp_hv with host buffers runs row chunks whose result copies overlap
+    the next chunk's launch (runtime.cu hv_plan); each launch keys its J splits
+    on its own rows, so rows equal the one-launch product to fp32 rounding, and
+    the call is deterministic."""
+    import torch
+
+    n, d, s = 13500, 26, 65
+    X, V, ls = make(n, d, s, seed=11)
+    ctx.set_data(X)
+    ctx.set_hyper([*ls, 1.3, 0.4])
+    Vt = torch.from_numpy(np.ascontiguousarray(V.T)).cuda()
+    for impl in ("tc_f16", "tc"):
+        ctx.set_hv_impl(impl)
+        a = ctx.hv(V)
+        assert np.array_equal(a, ctx.hv(V))
+        O = torch.empty_like(Vt)
+        torch.cuda.synchronize()
+        ctx.hv_device(Vt.data_ptr(), n, s, O.data_ptr(), n)
+        torch.cuda.synchronize()
+        b = O.cpu().numpy().T
+        assert rel(a, b.astype(np.float64)) <= 1e-6
+        # the last chunk's rows (the diagonal term at global row indices)
+        assert rel(a[-500:], b[-500:].astype(np.float64)) <= 1e-6
+    ctx.set_hv_impl("tc")
