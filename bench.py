@@ -603,6 +603,26 @@ def main():
     e2e_ms = float(np.mean(e2e_times))
     e2e_med = float(np.median(e2e_times))
     print("e2e times (ms):", " ".join(f"{t:.3f}" for t in e2e_times), file=sys.stderr)
+    # the box's PCIe rates for the same buffers (plain pinned copies on the context
+    # stream, after the timed calls): e2e ~ H2D + step + exposed D2H, and the host
+    # link differs a lot between boxes (H2D 14-50 GB/s seen)
+    pcie = {}
+    dprobe = torch.empty_like(Vh, device=dev)
+    with torch.cuda.stream(stream):
+        for name, fn in (("h2d", lambda: dprobe.copy_(Vh, non_blocking=True)),
+                         ("d2h", lambda: Vh.copy_(dprobe, non_blocking=True))):
+            fn()
+            stream.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(10):
+                fn()
+            b.record(stream)
+            b.synchronize()
+            pcie[name + "_ms"] = a.elapsed_time(b) / 10
+            pcie[name + "_GBps"] = Vh.numel() * 4 / (pcie[name + "_ms"] * 1e-3) / 1e9
+    del dprobe
     if ws > 1:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -682,7 +702,8 @@ def main():
                    "parallelism": f"rows{ws}" if ws > 1 else "single"},
         "e2e": {"value": n * n / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(n * s * 4), "d2h_bytes_per_step": int(m_out * s * 4),
-                "ms_per_step": e2e_ms, "ms_median": e2e_med},
+                "ms_per_step": e2e_ms, "ms_median": e2e_med, "ms_min": float(np.min(e2e_times)),
+                "pcie_probe": pcie},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_profile": traffic_profile,
                      "peak_basis": f"{pk['src']} peaks: F_hv={f_entry} flop/entry; " + basis,
