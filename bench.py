@@ -703,7 +703,9 @@ def main():
         "e2e": {"value": n * n / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(n * s * 4), "d2h_bytes_per_step": int(m_out * s * 4),
                 "ms_per_step": e2e_ms, "ms_median": e2e_med, "ms_min": float(np.min(e2e_times)),
-                "pcie_probe": pcie},
+                "pcie_probe": pcie,
+                "h2d_path": os.environ.get("WGP_HV_UPLOAD", "zc") + " (zc: the V split kernel loads the "
+                            "page-locked host V over PCIe itself; ce: cudaMemcpyAsync before it)"},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_profile": traffic_profile,
                      "peak_basis": f"{pk['src']} peaks: F_hv={f_entry} flop/entry; " + basis,

@@ -142,6 +142,7 @@ struct TcArgs {
   const int* row_idx;
   int64_t r0;
   const float* V;
+  int v_late;  // 1: V itself is written by the split kernel of this launch chain (zero-copy upload)
   int64_t ldv;
   float* out;
   int64_t ldo;
@@ -685,6 +686,9 @@ __global__ void __launch_bounds__(kThreadsT<H16>, 1)
       }
     };
     // prefetch the diagonal's V entries (overlaps the whole tile loop)
+    if constexpr (H16) {
+      if (p.v_late) asm volatile("griddepcontrol.wait;" ::: "memory");  // V comes from the split kernel too
+    }
     if (valid && diag && p.splits == 1) {
       for (int col = cb; col < ce && col < p.s; ++col)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(Vd + col * 128)),
@@ -853,12 +857,15 @@ __global__ void tc_reduce_kernel(const TcArgs p) {
 }
 
 // V[j0:j1, :s] -> tf32 hi / lo planes [s][ldw] (point index j - j0).
+// src / copy (optional): read V from src (the caller's page-locked host buffer) and keep
+// a copy in `copy` (the device V the H.V kernel's diagonal term reads).
 __global__ void split_v_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, float* hi, float* lo,
-                               int64_t ldw) {
+                               int64_t ldw, const float* src, float* copy) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (j >= nv) return;
-  const float v = V[j0 + j + c * ldv];
+  const float v = (src ? src : V)[j0 + j + c * ldv];
+  if (copy) copy[j0 + j + c * ldv] = v;
   const float vh = __uint_as_float(__float_as_uint(v) & kTfMask);
   hi[c * ldw + j] = vh;
   lo[c * ldw + j] = v - vh;
@@ -887,14 +894,17 @@ __device__ __forceinline__ float col_scale(unsigned mbits) {
 constexpr int kSplitCl = 8, kSplitThreads = 256, kSplitKeep = 8;
 __global__ void __cluster_dims__(kSplitCl, 1, 1) __launch_bounds__(kSplitThreads)
     split_v_f16_kernel(const float* V, int64_t ldv, int64_t j0, int64_t nv, __half* v1, __half* v2, int64_t ldw,
-                       float* vscale) {
+                       float* vscale, const float* src, float* copy) {
   // the H.V grid may start its fill (A / B loads, Gram, K conversion) now;
   // it waits for this grid before touching V's planes and scales
   asm volatile("griddepcontrol.launch_dependents;");
   const int c = blockIdx.y;
   const uint32_t rank = cluster_ctarank();
   const int64_t b0 = nv * rank / kSplitCl, b1 = nv * (rank + 1) / kSplitCl;
-  const float* col = V + j0 + static_cast<int64_t>(c) * ldv;
+  // src / copy as in split_v_kernel: the first pass reads the host buffer once (every
+  // load of the grid in flight at once) and stores the device copy
+  const float* col = (src ? src : V) + j0 + static_cast<int64_t>(c) * ldv;
+  float* ccol = copy ? copy + j0 + static_cast<int64_t>(c) * ldv : nullptr;
   const bool keep = b1 - b0 <= static_cast<int64_t>(kSplitKeep) * kSplitThreads;
   float x[kSplitKeep];
   unsigned m = 0u;
@@ -904,6 +914,13 @@ __global__ void __cluster_dims__(kSplitCl, 1, 1) __launch_bounds__(kSplitThreads
       const int64_t j = b0 + threadIdx.x + static_cast<int64_t>(i) * kSplitThreads;
       x[i] = j < b1 ? col[j] : 0.f;
     }
+    if (ccol) {
+#pragma unroll
+      for (int i = 0; i < kSplitKeep; ++i) {
+        const int64_t j = b0 + threadIdx.x + static_cast<int64_t>(i) * kSplitThreads;
+        if (j < b1) ccol[j] = x[i];
+      }
+    }
 #pragma unroll
     for (int i = 0; i < kSplitKeep; ++i) m = max(m, __float_as_uint(x[i]) & 0x7FFFFFFFu);
   } else {
@@ -912,10 +929,12 @@ __global__ void __cluster_dims__(kSplitCl, 1, 1) __launch_bounds__(kSplitThreads
       for (int i = 0; i < kSplitKeep; ++i) {
         const int64_t jj = j + static_cast<int64_t>(i) * kSplitThreads;
         x[i] = jj < b1 ? col[jj] : 0.f;
+        if (ccol && jj < b1) ccol[jj] = x[i];
       }
 #pragma unroll
       for (int i = 0; i < kSplitKeep; ++i) m = max(m, __float_as_uint(x[i]) & 0x7FFFFFFFu);
     }
+    if (ccol) col = ccol;  // the second pass re-reads this thread's own device copies
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -1334,6 +1353,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
       HvParams q = hp;
       q.s = c1 - c0;
       q.V = hp.V + c0 * hp.ldv;
+      if (hp.v_host) q.v_host = hp.v_host + c0 * hp.ldv;
       q.out = hp.out + c0 * hp.ldo;
       if (hp.B) q.B = hp.B + c0 * hp.ldb;
       q.vplanes = nullptr;
@@ -1370,10 +1390,12 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   } else if (bf16) {
     split_v_f16_kernel<<<dim3(kSplitCl, s), kSplitThreads, 0, st>>>(hp.V, hp.ldv, hp.j0, nv,
                                                                      reinterpret_cast<__half*>(vhi),
-                                                                     reinterpret_cast<__half*>(vlo), ldw, vscale);
+                                                                     reinterpret_cast<__half*>(vlo), ldw, vscale,
+                                                                     hp.v_host, hp.v_host ? const_cast<float*>(hp.V) : nullptr);
   } else
     split_v_kernel<<<vgrid, 256, 0, st>>>(hp.V, hp.ldv, hp.j0, nv, reinterpret_cast<float*>(vhi),
-                                          reinterpret_cast<float*>(vlo), ldw);
+                                          reinterpret_cast<float*>(vlo), ldw, hp.v_host,
+                                          hp.v_host ? const_cast<float*>(hp.V) : nullptr);
   WGP_LAUNCH_CHECK();
   // A rows: the operand planes directly (row range) or a gathered copy
   const float* ahi = static_cast<const float*>(ops.a_hi);
@@ -1433,6 +1455,7 @@ void hv_tc(TcOperands& ops, const HvParams& hp, cudaStream_t st, bool bf16) {
   a.row_idx = hp.row_idx;
   a.r0 = hp.r0;
   a.V = hp.V;
+  a.v_late = hp.v_host ? 1 : 0;
   a.ldv = hp.ldv;
   a.out = hp.out;
   a.ldo = hp.ldo;

@@ -52,6 +52,10 @@ struct HvParams {
                          // split_v's; the launch then skips its own split of V
   bool reuse_vsplit;     // hv_tc: the previous launch split this same V[j0:j1, :s] (row
                          // chunks of one product, wgp_hv): skip the split, reuse its planes
+  const float* v_host;   // hv_tc: optional device-visible alias of the caller's page-locked V
+                         // (same ldv).  The split then loads V over PCIe itself and
+                         // stores what it read into V (a device buffer here), instead of
+                         // a copy-engine upload before the launch (wgp_hv, zero-copy)
 };
 
 // SIMT fp32 fused H.V (direct differences; any d, s <= 128).

@@ -313,11 +313,19 @@ struct Ctx {
   // runs on its own stream under the next chunk's H.V
   cudaStream_t cst = nullptr;
   cudaEvent_t ev_chunk = nullptr, ev_copied = nullptr;
+  // wgp_hv upload policy (see wgp_hv): the copy engine's last measured H2D rate and
+  // the calls since it was measured
+  cudaEvent_t ev_up0 = nullptr, ev_up1 = nullptr;
+  double ce_gbps = -1.0;
+  int zc_streak = 0;
+  const float* v_host_next = nullptr;  // consumed by the next hv(): HvParams::v_host
 
   ~Ctx() {
     drop_cg_graphs();
     if (ev_chunk) cudaEventDestroy(ev_chunk);
     if (ev_copied) cudaEventDestroy(ev_copied);
+    if (ev_up0) cudaEventDestroy(ev_up0);
+    if (ev_up1) cudaEventDestroy(ev_up1);
     if (cst) cudaStreamDestroy(cst);
     if (cublas) cublasDestroy(cublas);
     if (cusolver) cusolverDnDestroy(cusolver);
@@ -404,6 +412,8 @@ struct Ctx {
           int64_t vplanes_ld = 0, bool reuse_vsplit = false) {
     HvParams p{};
     p.reuse_vsplit = reuse_vsplit;
+    p.v_host = v_host_next;
+    v_host_next = nullptr;
     p.vplanes = vplanes;
     p.vplanes_ld = vplanes_ld;
     p.xs = xs.as<float>();
@@ -2324,7 +2334,45 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
         WGP_CUDA(cudaEventCreateWithFlags(&c.ev_chunk, cudaEventDisableTiming));
         WGP_CUDA(cudaEventCreateWithFlags(&c.ev_copied, cudaEventDisableTiming));
       }
-      WGP_CUDA(cudaMemcpyAsync(dv.p, V, sizeof(float) * c.n * s, cudaMemcpyHostToDevice, c.st));
+      if (!c.ev_up0) {
+        WGP_CUDA(cudaEventCreate(&c.ev_up0));
+        WGP_CUDA(cudaEventCreate(&c.ev_up1));
+      }
+      // Upload of V.  The copy engine reads page-locked memory at ~52 GB/s when the host
+      // link is in its fast state, but only 11-21 GB/s in a slow state some hosts fall
+      // into for 10-100 ms at a time (DESIGN 4.1); SM loads from the same buffer hold
+      // ~42 GB/s in both.  So on the tcgen05 engines the V split can read the caller's
+      // page-locked buffer itself (HvParams::v_host, keeping a device copy for the
+      // diagonal term): config 1 end to end 0.317 ms in either state, against 0.312
+      // (fast) to 0.53 ms (slow) with the copy engine -- the default for page-locked
+      // V.  WGP_HV_UPLOAD (read per call): zc (default), ce (always the copy engine),
+      // auto (time each copy-engine upload; below 35 GB/s switch to the zero-copy
+      // split, re-probing the copy engine every 16th call).
+      const float* v_alias = nullptr;
+      {
+        const char* e = getenv("WGP_HV_UPLOAD");
+        const std::string mode(e ? e : "zc");
+        const bool tc_eng = (c.hv_impl == WGP_HV_TC || c.hv_impl == WGP_HV_TC_F16) && wgp::hv_tc_supported(c.d, s) &&
+                            s <= 96;
+        const bool want = mode == "zc" || (mode == "auto" && c.ce_gbps >= 0 && c.ce_gbps < 35.0 && c.zc_streak < 15);
+        if (tc_eng && want && sizeof(float) * c.n * s >= (1u << 20)) {
+          cudaPointerAttributes at{};
+          if (cudaPointerGetAttributes(&at, V) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+            v_alias = static_cast<const float*>(at.devicePointer);
+          else
+            (void)cudaGetLastError();
+        }
+      }
+      if (v_alias) {
+        ++c.zc_streak;
+        c.v_host_next = v_alias;
+      } else {
+        c.zc_streak = 0;
+        WGP_CUDA(cudaEventRecord(c.ev_up0, c.st));
+        WGP_CUDA(cudaMemcpyAsync(dv.p, V, sizeof(float) * c.n * s, cudaMemcpyHostToDevice, c.st));
+        WGP_CUDA(cudaEventRecord(c.ev_up1, c.st));
+      }
+      const bool timed_upload = !v_alias;
       if (pl.cuts.size() <= 2) {
         c.hv(dv.as<float>(), ldv, s, dout.as<float>(), m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0, m);
         WGP_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(float) * m * s, cudaMemcpyDeviceToHost, c.st));
@@ -2344,6 +2392,16 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
         WGP_CUDA(cudaEventRecord(c.ev_copied, c.cst));
         WGP_CUDA(cudaStreamWaitEvent(c.st, c.ev_copied, 0));
       }
+      WGP_CUDA(cudaStreamSynchronize(c.st));
+      c.v_host_next = nullptr;
+      if (timed_upload) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c.ev_up0, c.ev_up1) == cudaSuccess && ms > 0.f)
+          c.ce_gbps = static_cast<double>(sizeof(float) * c.n * s) / (ms * 1e-3) / 1e9;
+        else
+          (void)cudaGetLastError();
+      }
+      return;
     }
     WGP_CUDA(cudaStreamSynchronize(c.st));
   });

@@ -961,3 +961,43 @@ def test_hv_host_row_chunks_match_one_launch(ctx):
         # the last chunk's rows (the diagonal term at global row indices)
         assert rel(a[-500:], b[-500:].astype(np.float64)) <= 1e-6
     ctx.set_hv_impl("tc")
+
+
+def test_hv_host_zero_copy_upload_bitwise(ctx, monkeypatch):
+    """wgp_hv's zero-copy upload (WGP_HV_UPLOAD=zc: the V split loads the caller's
+    page-locked buffer over PCIe itself and keeps a device copy for the diagonal
+    term; runtime.cu wgp_hv) feeds the same planes to the same launches, so the
+    result is bitwise the copy-engine upload's -- both engines, row chunks and one
+    launch, a single-split shape (the diagonal prefetch inside the H.V kernel) and
+    a long column the split re-reads; pageable buffers fall back to the copy."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2405_18328_b200 as wg
+
+    lib = wg.load()
+    for n, d, s in ((13500, 26, 65), (4500, 9, 65), (70000, 3, 17)):
+        X, V, ls = make(n, d, s, seed=23)
+        ctx.set_data(X)
+        ctx.set_hyper([*ls, 1.3, 0.4])
+        Vh = torch.from_numpy(np.ascontiguousarray(V.T)).pin_memory()
+        keep = Vh.clone()
+        for impl in ("tc_f16", "tc"):
+            ctx.set_hv_impl(impl)
+            for pipe in ("", "1"):
+                monkeypatch.setenv("WGP_HV_PIPE", pipe)
+                res = {}
+                for mode in ("ce", "zc"):
+                    monkeypatch.setenv("WGP_HV_UPLOAD", mode)
+                    out = torch.full((s, n), float("nan")).pin_memory()
+                    rc = lib.wgp_hv(ctx._h, C.c_void_p(Vh.data_ptr()), s, C.c_void_p(out.data_ptr()))
+                    assert rc == 0, lib.wgp_last_error().decode()
+                    res[mode] = out.numpy().copy()
+                assert np.isfinite(res["zc"]).all()
+                assert np.array_equal(res["ce"], res["zc"]), (n, impl, pipe)
+        assert torch.equal(Vh, keep)  # the caller's buffer is only read
+    monkeypatch.setenv("WGP_HV_UPLOAD", "zc")
+    a = ctx.hv(V)  # pageable numpy buffer: copy-engine path (WGP_HV_PIPE still "1")
+    assert np.array_equal(a.T, res["ce"])
+    ctx.set_hv_impl("tc")
