@@ -107,8 +107,9 @@ int wgp_set_rows(wgp_ctx* ctx, int64_t r0, int64_t r1);
  *  asynchronous, and on the tcgen05 engines (s <= 96, V of 1 MB or more) a
  *  page-locked V is not copied at all: the V split kernel loads it over PCIe
  *  itself (bitwise the same result; steadier than the copy engine on hosts
- *  whose DMA read rate dips; WGP_HV_UPLOAD=ce|zc|auto).  The
- *  buffer is only read. */
+ *  whose DMA read rate dips; WGP_HV_UPLOAD=ce|zc|auto), and the
+ *  last row chunk is stored straight into a page-locked out_host
+ *  (WGP_HV_DOWNLOAD=ce: copied).  V_host is only read. */
 int wgp_hv(wgp_ctx* ctx, const float* V_host, int s, float* out_host);
 /** fp64 H V on host fp64 V / out (n x s; rows of wgp_set_rows): the operator
  *  of the fp64 CG path -- entries evaluated in fp32 (bitwise symmetric),

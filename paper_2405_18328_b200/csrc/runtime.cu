@@ -2380,8 +2380,29 @@ int wgp_hv(wgp_ctx* ctx, const float* V, int s, float* out) {
         float* o = dout.as<float>();
         // chunk 0 splits V, the others reuse its planes; chunk k's result copy
         // overlaps chunk k + 1's launch
+        // The last chunk's copy is the exposed one: with a page-locked result buffer
+        // its launch can store straight into the caller's memory instead (plain
+        // coalesced stores in store mode, no read of the destination; same values).
+        // Config 1: 0.316 vs 0.321 ms per call.  WGP_HV_DOWNLOAD=ce turns it off (read
+        // per call).
+        float* out_alias = nullptr;
+        {
+          const char* e = getenv("WGP_HV_DOWNLOAD");
+          if (!e || std::string(e) != "ce") {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, out) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+              out_alias = static_cast<float*>(at.devicePointer);
+            else
+              (void)cudaGetLastError();
+          }
+        }
         for (size_t k = 0; k + 1 < pl.cuts.size(); ++k) {
           const int64_t a = pl.cuts[k], len = pl.cuts[k + 1] - pl.cuts[k];
+          if (out_alias && k + 2 == pl.cuts.size()) {
+            c.hv(dv.as<float>(), ldv, s, out_alias + a, m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0 + a, len,
+                 nullptr, false, nullptr, 0, k > 0);
+            break;
+          }
           c.hv(dv.as<float>(), ldv, s, o + a, m, wgp::kHvStore, nullptr, 0, 0, c.n, nullptr, c.r0 + a, len, nullptr,
                false, nullptr, 0, k > 0);
           WGP_CUDA(cudaEventRecord(c.ev_chunk, c.st));

@@ -23,14 +23,16 @@ ctx.set_hv_impl(impl)
 st = torch.cuda.ExternalStream(ctx.stream)
 Vh = torch.from_numpy(np.asfortranarray(p.V).T.copy()).pin_memory()
 outh = torch.empty((s, n), pin_memory=True)
+outs = {}
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 lib = wg.load()
-modes = ["ce", "zc", "auto"]
+var = sys.argv[3] if len(sys.argv) > 3 else "WGP_HV_UPLOAD"  # or WGP_HV_DOWNLOAD (modes ce, zc)
+modes = ["ce", "zc", "auto"] if var == "WGP_HV_UPLOAD" else ["ce", "zc"]
 ts = {m: [] for m in modes}
 for rnd in range(rounds):
     line = []
     for mode in modes:
-        os.environ["WGP_HV_UPLOAD"] = mode
+        os.environ[var] = mode
         t = []
         for i in range(22):
             flush.zero_()
@@ -44,10 +46,12 @@ for rnd in range(rounds):
             if i >= 2:
                 t.append(a.elapsed_time(b))
         ts[mode] += t
+        outs[mode] = outh.numpy().copy()
         line.append(f"{mode} {np.median(t):.3f}")
     print(f"round {rnd}: " + "  ".join(line) + " ms")
+print("results bitwise equal across modes:", all(np.array_equal(outs[modes[0]], outs[m]) for m in modes))
 for mode in modes:
     t = np.array(ts[mode])
-    print(f"impl={impl} upload={mode:5s} e2e median {np.median(t):.4f} mean {t.mean():.4f} p10 {np.percentile(t, 10):.4f} "
+    print(f"impl={impl} {var}={mode:5s} e2e median {np.median(t):.4f} mean {t.mean():.4f} p10 {np.percentile(t, 10):.4f} "
           f"p90 {np.percentile(t, 90):.4f} ms  entries/s (mean) {n * n / (t.mean() / 1e3):.3e}")
 os._exit(0)

@@ -964,7 +964,7 @@ def test_hv_host_row_chunks_match_one_launch(ctx):
 
 
 def test_hv_host_zero_copy_upload_bitwise(ctx, monkeypatch):
-    """wgp_hv's zero-copy upload (WGP_HV_UPLOAD=zc: the V split loads the caller's
+    """wgp_hv's zero-copy transfers (WGP_HV_UPLOAD=zc: the V split loads the caller's
     page-locked buffer over PCIe itself and keeps a device copy for the diagonal
     term; runtime.cu wgp_hv) feeds the same planes to the same launches, so the
     result is bitwise the copy-engine upload's -- both engines, row chunks and one
@@ -988,14 +988,18 @@ def test_hv_host_zero_copy_upload_bitwise(ctx, monkeypatch):
             for pipe in ("", "1"):
                 monkeypatch.setenv("WGP_HV_PIPE", pipe)
                 res = {}
-                for mode in ("ce", "zc"):
+                # upload mode, and the last row chunk stored straight into the caller's
+                # page-locked result (WGP_HV_DOWNLOAD, the default) or copied out
+                for mode, down in (("ce", "ce"), ("zc", "ce"), ("zc", "zc"), ("ce", "zc")):
                     monkeypatch.setenv("WGP_HV_UPLOAD", mode)
+                    monkeypatch.setenv("WGP_HV_DOWNLOAD", down)
                     out = torch.full((s, n), float("nan")).pin_memory()
                     rc = lib.wgp_hv(ctx._h, C.c_void_p(Vh.data_ptr()), s, C.c_void_p(out.data_ptr()))
                     assert rc == 0, lib.wgp_last_error().decode()
-                    res[mode] = out.numpy().copy()
-                assert np.isfinite(res["zc"]).all()
-                assert np.array_equal(res["ce"], res["zc"]), (n, impl, pipe)
+                    res[mode, down] = out.numpy().copy()
+                    assert np.isfinite(res[mode, down]).all()
+                    assert np.array_equal(res["ce", "ce"], res[mode, down]), (n, impl, pipe, mode, down)
+                res["ce"] = res["ce", "ce"]
         assert torch.equal(Vh, keep)  # the caller's buffer is only read
     monkeypatch.setenv("WGP_HV_UPLOAD", "zc")
     a = ctx.hv(V)  # pageable numpy buffer: copy-engine path (WGP_HV_PIPE still "1")
